@@ -1,0 +1,200 @@
+/*
+ * mhdg.h -- C ABI of the B200 (sm_100a) macro-element HDG hot path.
+ *
+ * Plain pointers and sizes only (no torch types).  Every pointer inside the
+ * structs and every array argument is a DEVICE pointer (FP64 unless noted,
+ * int32 for index tables); `stream` is a cudaStream_t passed as void*.
+ * All calls are stream-ordered and asynchronous unless documented otherwise.
+ *
+ * Each entry point replaces one reference operation (paths relative to
+ * /root/reference/pkg/src/macrohdg/):
+ *
+ *   mhdg_assemble           assembly.py:339-618  assemble_system
+ *                           (residual(): assembly.py:621, jacobian(): :626)
+ *   mhdg_condense           condense.py:62-70 + 130-158
+ *                           CondensedSchur.build (_schur_correction + inv;
+ *                           here: Schur GEMM + batched LU, partial pivoting)
+ *   mhdg_apply_trace        condense.py:91-103  CondensedSchur.apply_trace
+ *   mhdg_condensed_rhs      condense.py:105-110 CondensedSchur.rhs
+ *   mhdg_recover            condense.py:112-127 CondensedSchur.recover
+ *   mhdg_gradient_refresh   assembly.py:247-252 Discretization.gradient_refresh
+ *   mhdg_precond_build      krylov.py:194-232   block_precond_build
+ *   mhdg_precond_apply      krylov.py:234-236   (closure returned by it)
+ *   mhdg_face_reduce        condense.py:48-51   _scatter_add (deterministic)
+ *
+ * Layouts are the reference's (assembly.py:6-8): volume dof node*ns+s,
+ * gradient dof (l*L+node)*ns+s, trace dof (f*Lf+g)*ns+s, local trace
+ * (mac, lf, g, s).  Blocks use the LocalBlocks shapes of assembly.py:293-312.
+ *
+ * Errors: the return value is MHDG_OK or MHDG_ERR_CUDA (launch failure).
+ * Data-dependent failures are reported through the device status word
+ * `status` (mhdg_status, int32[4]): code, macro/face index, component, and
+ * the value bits are written by the first failing thread; the host reads it
+ * after the call and maps it to the reference exception classes
+ * (AdmissibilityError physics.py:23, FactorizationError condense.py:40,
+ * PreconditionerError krylov.py:47).
+ */
+#ifndef MHDG_H
+#define MHDG_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MHDG_OK 0
+#define MHDG_ERR_ADMISSIBILITY 1
+#define MHDG_ERR_FACTORIZATION 2
+#define MHDG_ERR_PRECONDITIONER 3
+#define MHDG_ERR_CONFIG 4
+#define MHDG_ERR_CUDA 5
+
+/* discretization: reference tables, geometry, layouts (device pointers) */
+typedef struct {
+  int dim, ns, nf;            /* d, d+2, d+1 */
+  int n_mac, n_faces, n_trace;
+  int L, Lf;                  /* volume / face lattice sizes */
+  int n_sub, nloc, nq;        /* sub-elements, nodes per sub, volume qp per sub */
+  int n_tri, nlocf, nqf;      /* face sub-elements, nodes per face sub, qp per face sub */
+  double face_fac;            /* (d-1)!: face weight = w_face_ref * face_fac * area */
+  /* reference tables */
+  const double *mass;         /* L*L */
+  const double *mass_inv;     /* L*L */
+  const double *minv_d;       /* d*L*L   M^-1 D[r] */
+  const double *weak_deriv;   /* d*L*L   D[r][i][j] = int phi_j d_r phi_i (basis.py:412-424) */
+  const double *gf;           /* nf*L*Lf  M^-1[:, fvn[f]] face_mass */
+  const double *face_mass;    /* Lf*Lf */
+  const int *face_vol_nodes;  /* nf*Lf */
+  const int *sub_conn;        /* n_sub*nloc */
+  const double *phi_vol;      /* nq*nloc */
+  const double *grad_ref;     /* n_sub*nq*nloc*d */
+  const double *w_ref;        /* n_sub*nq */
+  const int *tri_conn;        /* n_tri*nlocf */
+  const double *phi_face;     /* nqf*nlocf */
+  const double *w_face_ref;   /* n_tri*nqf */
+  const double *pm_vol;       /* n_sub*nq*d*L : sum_b phi[q,b] minv_d[r][conn[K,b], :] */
+  const double *pm_face;      /* nf*n_tri*nqf*d*L */
+  /* inverse incidence (CSR) for deterministic gathers */
+  const int *vn_ptr, *vn_sub;  /* L+1 ; entries K*nloc+a with sub_conn[K,a] = node */
+  const int *vf_ptr, *vf_ent;  /* L+1 ; entries f*Lf+g with face_vol_nodes[f,g] = node */
+  const int *fn_ptr, *fn_ent;  /* Lf+1 ; entries T*nlocf+a with tri_conn[T,a] = g */
+  /* geometry per macro */
+  const double *det;          /* n_mac */
+  const double *inv_jac;      /* n_mac*d*d */
+  const double *normals;      /* n_mac*nf*d */
+  const double *areas;        /* n_mac*nf */
+  const double *h_sub;        /* n_mac*n_sub */
+  const int *gather;          /* n_mac*nf*Lf*ns  global trace dof of each local dof */
+  const int *scatter_src;     /* n_trace*2  local flat indices summed per dof, -1 = none */
+  /* boundary data */
+  const int *bc_kind;         /* n_mac*nf  0 interior, 1 Dirichlet, 2 wall */
+  const double *wall_e;       /* n_mac*nf */
+  const double *wall_u;       /* n_mac*nf*d */
+  const double *u_dir;        /* n_mac*nf*n_tri*nqf*ns */
+  const double *source;       /* n_mac*n_sub*nq*ns or NULL */
+  /* face skeleton for the block preconditioner */
+  const int *face_macros;     /* n_faces*2 (-1 = none) */
+  const int *face_locals;     /* n_faces*2 */
+} mhdg_disc;
+
+typedef struct {
+  double gamma, prandtl, re_acoustic, mach_ref, mu, re_flow;
+} mhdg_flow;
+
+typedef struct {
+  double dt_coeff;      /* d_ii/dt, 0 when steady */
+  const double *hist;   /* n_mac*L*ns or NULL */
+  double pseudo_dt;     /* +inf: none */
+  double supg_dt;       /* +inf: none */
+} mhdg_stage;
+
+typedef struct {
+  double *state_state;       /* n_mac*(L ns)^2 */
+  double *face_state_trace;  /* n_mac*nf*(Lf ns)^2 */
+  double *face_trace_state;
+  double *face_trace_trace;
+  double *wdgdq_vol;         /* n_mac*n_sub*nq*d*d*ns*ns */
+  double *wdgdq_face;        /* n_mac*nf*(n_tri nqf)*d*ns*ns */
+  double *trace_face_scale;  /* n_mac*nf */
+} mhdg_blocks;
+
+typedef struct {
+  double *supg_tau;          /* n_mac*n_sub*nq */
+  double *supg_jac;          /* n_mac*n_sub*nq*d*ns*ns */
+  double *face_stab;         /* n_mac*nf*(n_tri nqf)*ns*ns */
+  double *face_visc_state;   /* n_mac*nf*(n_tri nqf)*ns */
+} mhdg_frozen;
+
+/* condensed operator: S = P^T L U per macro, row-major n x n, n = L*ns;
+   L unit lower (strictly below the diagonal), U on and above it; perm[i] is
+   the original row of factor row i. */
+typedef struct {
+  double *lu;                /* n_mac*n*n */
+  int *perm;                 /* n_mac*n */
+} mhdg_factors;
+
+/* Residuals (and, with want_jac, blocks + frozen coefficients).
+   frozen_in != NULL evaluates the residual with frozen coefficients (the
+   finite-difference oracle mode of assembly.py:84-96).
+   R_trace_loc: n_mac*nf*Lf*ns scratch; R_trace = its deterministic face sum. */
+int mhdg_assemble(const mhdg_disc *disc, const mhdg_flow *flow, const mhdg_stage *stage,
+                  const double *u, const double *q, const double *uhat,
+                  double *R_grad, double *R_state, double *R_trace_loc, double *R_trace,
+                  int want_jac, const mhdg_blocks *blocks, const mhdg_frozen *frozen_out,
+                  const mhdg_frozen *frozen_in, int *status, void *stream);
+
+/* S = state_state - A_uq A_qq^-1 A_qu, then in-place batched LU with partial pivoting. */
+int mhdg_condense(const mhdg_disc *disc, const mhdg_blocks *blocks, const mhdg_factors *fac,
+                  int *status, void *stream);
+
+/* Schur complement only (no factorization), into fac->lu; for parity tests. */
+int mhdg_schur_matrix(const mhdg_disc *disc, const mhdg_blocks *blocks, const mhdg_factors *fac,
+                      void *stream);
+
+/* LU-factor n_mac dense n x n matrices in place (fac->lu) with partial pivoting. */
+int mhdg_lu_factor(const mhdg_disc *disc, const mhdg_factors *fac, int *status, void *stream);
+
+/* y_mac = S^-1 b_mac for all macros (b, y: n_mac*n; may alias). */
+int mhdg_lu_solve(const mhdg_disc *disc, const mhdg_factors *fac, const double *b, double *y,
+                  void *stream);
+
+/* y = A_hat x (global trace vectors, n_trace).  y_loc: n_mac*nf*Lf*ns scratch. */
+int mhdg_apply_trace(const mhdg_disc *disc, const mhdg_blocks *blocks, const mhdg_factors *fac,
+                     const double *x, double *y, double *y_loc, void *stream);
+
+/* Local (unscattered) part of the apply, y_loc only. */
+int mhdg_apply_trace_local(const mhdg_disc *disc, const mhdg_blocks *blocks,
+                           const mhdg_factors *fac, const double *x, double *y_loc, void *stream);
+
+/* y[dof] = sum of the (one or two) local contributions, in flat-index order. */
+int mhdg_face_reduce(const mhdg_disc *disc, const double *y_loc, double *y, void *stream);
+
+/* b = -R_trace + scatter(A_hu S^-1 (R_U - A_uq A_qq^-1 R_Q) ... ) (condense.py:105-110). */
+int mhdg_condensed_rhs(const mhdg_disc *disc, const mhdg_blocks *blocks, const mhdg_factors *fac,
+                       const double *R_grad, const double *R_state, const double *R_trace,
+                       double *b, double *b_loc, void *stream);
+
+/* (du, dq) from the trace update (condense.py:112-127). */
+int mhdg_recover(const mhdg_disc *disc, const mhdg_blocks *blocks, const mhdg_factors *fac,
+                 const double *R_grad, const double *R_state, const double *dtrace,
+                 double *du, double *dq, void *stream);
+
+/* q = A_qq^-1 (-A_qu u - A_qh uhat) (assembly.py:247-252). */
+int mhdg_gradient_refresh(const mhdg_disc *disc, const double *u, const double *uhat, double *q,
+                          void *stream);
+
+/* Per-face B_f = sym(sum_sides P^T face_trace_trace P), Cholesky, explicit
+   inverse (krylov.py:194-232).  inv: n_faces*bs*bs, bs = Lf*ns. */
+int mhdg_precond_build(const mhdg_disc *disc, const mhdg_blocks *blocks, double *inv, int *status,
+                       void *stream);
+
+/* y = blockdiag(inv) v (krylov.py:234-236). */
+int mhdg_precond_apply(const mhdg_disc *disc, const double *inv, const double *v, double *y,
+                       void *stream);
+
+/* number of kernel launches issued by this library since load (diagnostics) */
+long long mhdg_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MHDG_H */

@@ -471,14 +471,20 @@ def schur_matrix(blocks):
 
 
 class CondensedSchur:
-    def __init__(self, blocks, schur_inv):
+    """mode "inv": explicit inverse as the reference (condense.py:67);
+    mode "lu": LAPACK LU solves, the same algebra the device path uses."""
+
+    def __init__(self, blocks, schur_inv, lu=None):
         self.blocks = blocks
         self.schur_inv = schur_inv
+        self.lu = lu
 
     @classmethod
-    def build(cls, blocks):
+    def build(cls, blocks, mode="inv"):
         S = schur_matrix(blocks)
         try:
+            if mode == "lu":
+                return cls(blocks, None, [scipy.linalg.lu_factor(s) for s in S])
             inv = np.linalg.inv(S)
         except np.linalg.LinAlgError as exc:
             raise FactorizationError(f"singular interior Schur complement: {exc}")
@@ -490,6 +496,9 @@ class CondensedSchur:
 
     def schur_solve(self, y):
         M = self.disc.n_mac
+        if self.lu is not None:
+            yy = y.reshape(M, -1)
+            return np.stack([scipy.linalg.lu_solve(self.lu[m], yy[m]) for m in range(M)]).reshape(y.shape)
         return np.matmul(self.schur_inv, y.reshape(M, -1, 1)).reshape(y.shape)
 
     def interior_elim(self, y):
@@ -533,10 +542,10 @@ class CondensedSchur:
         return du, dq
 
 
-def condense(blocks, path="schur"):
+def condense(blocks, path="schur", mode="inv"):
     if path != "schur":
         raise ValueError(f"unknown condensation path {path!r}")
-    return CondensedSchur.build(blocks)
+    return CondensedSchur.build(blocks, mode)
 
 
 # ---------------------------------------------------------------------------

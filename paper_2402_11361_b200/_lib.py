@@ -1,0 +1,118 @@
+"""ctypes binding of libmhdg.so (the C ABI declared in include/mhdg.h).
+
+The shared library is built in-tree (``python -c "import __graft_entry__ as g;
+g.build()"`` or ``make -C paper_2402_11361_b200/csrc``).  There is no fallback:
+if the library or a CUDA device is missing, every device operation raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libmhdg.so")
+
+MHDG_OK = 0
+MHDG_ERR_ADMISSIBILITY = 1
+MHDG_ERR_FACTORIZATION = 2
+MHDG_ERR_PRECONDITIONER = 3
+MHDG_ERR_CONFIG = 4
+MHDG_ERR_CUDA = 5
+
+_dp = C.c_void_p  # device pointer
+
+
+class Disc(C.Structure):
+    _fields_ = [
+        ("dim", C.c_int), ("ns", C.c_int), ("nf", C.c_int),
+        ("n_mac", C.c_int), ("n_faces", C.c_int), ("n_trace", C.c_int),
+        ("L", C.c_int), ("Lf", C.c_int),
+        ("n_sub", C.c_int), ("nloc", C.c_int), ("nq", C.c_int),
+        ("n_tri", C.c_int), ("nlocf", C.c_int), ("nqf", C.c_int),
+        ("face_fac", C.c_double),
+        ("mass", _dp), ("mass_inv", _dp), ("minv_d", _dp), ("weak_deriv", _dp), ("gf", _dp), ("face_mass", _dp),
+        ("face_vol_nodes", _dp), ("sub_conn", _dp), ("phi_vol", _dp), ("grad_ref", _dp), ("w_ref", _dp),
+        ("tri_conn", _dp), ("phi_face", _dp), ("w_face_ref", _dp), ("pm_vol", _dp), ("pm_face", _dp),
+        ("vn_ptr", _dp), ("vn_sub", _dp), ("vf_ptr", _dp), ("vf_ent", _dp), ("fn_ptr", _dp), ("fn_ent", _dp),
+        ("det", _dp), ("inv_jac", _dp), ("normals", _dp), ("areas", _dp), ("h_sub", _dp),
+        ("gather", _dp), ("scatter_src", _dp),
+        ("bc_kind", _dp), ("wall_e", _dp), ("wall_u", _dp), ("u_dir", _dp), ("source", _dp),
+        ("face_macros", _dp), ("face_locals", _dp),
+    ]
+
+
+class Flow(C.Structure):
+    _fields_ = [("gamma", C.c_double), ("prandtl", C.c_double), ("re_acoustic", C.c_double),
+                ("mach_ref", C.c_double), ("mu", C.c_double), ("re_flow", C.c_double)]
+
+
+class Stage(C.Structure):
+    _fields_ = [("dt_coeff", C.c_double), ("hist", _dp), ("pseudo_dt", C.c_double), ("supg_dt", C.c_double)]
+
+
+class Blocks(C.Structure):
+    _fields_ = [("state_state", _dp), ("face_state_trace", _dp), ("face_trace_state", _dp),
+                ("face_trace_trace", _dp), ("wdgdq_vol", _dp), ("wdgdq_face", _dp), ("trace_face_scale", _dp)]
+
+
+class Frozen(C.Structure):
+    _fields_ = [("supg_tau", _dp), ("supg_jac", _dp), ("face_stab", _dp), ("face_visc_state", _dp)]
+
+
+class Factors(C.Structure):
+    _fields_ = [("lu", _dp), ("perm", _dp)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libmhdg.so once; raise if it is not built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is not built; run __graft_entry__.build() (no CPU fallback exists)")
+        L = C.CDLL(LIB_PATH)
+        P = C.POINTER
+        sigs = {
+            "mhdg_assemble": [P(Disc), P(Flow), P(Stage), _dp, _dp, _dp, _dp, _dp, _dp, _dp, C.c_int, P(Blocks),
+                              P(Frozen), P(Frozen), _dp, _dp],
+            "mhdg_condense": [P(Disc), P(Blocks), P(Factors), _dp, _dp],
+            "mhdg_schur_matrix": [P(Disc), P(Blocks), P(Factors), _dp],
+            "mhdg_lu_factor": [P(Disc), P(Factors), _dp, _dp],
+            "mhdg_lu_solve": [P(Disc), P(Factors), _dp, _dp, _dp],
+            "mhdg_apply_trace": [P(Disc), P(Blocks), P(Factors), _dp, _dp, _dp, _dp],
+            "mhdg_apply_trace_local": [P(Disc), P(Blocks), P(Factors), _dp, _dp, _dp],
+            "mhdg_face_reduce": [P(Disc), _dp, _dp, _dp],
+            "mhdg_condensed_rhs": [P(Disc), P(Blocks), P(Factors), _dp, _dp, _dp, _dp, _dp, _dp],
+            "mhdg_recover": [P(Disc), P(Blocks), P(Factors), _dp, _dp, _dp, _dp, _dp, _dp],
+            "mhdg_gradient_refresh": [P(Disc), _dp, _dp, _dp, _dp],
+            "mhdg_precond_build": [P(Disc), P(Blocks), _dp, _dp, _dp],
+            "mhdg_precond_apply": [P(Disc), _dp, _dp, _dp, _dp],
+        }
+        for name, args in sigs.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = C.c_int
+        L.mhdg_launch_count.argtypes = []
+        L.mhdg_launch_count.restype = C.c_longlong
+        _lib = L
+    return _lib
+
+
+EXPORTED = (
+    "mhdg_assemble", "mhdg_condense", "mhdg_schur_matrix", "mhdg_lu_factor", "mhdg_lu_solve",
+    "mhdg_apply_trace", "mhdg_apply_trace_local", "mhdg_face_reduce", "mhdg_condensed_rhs", "mhdg_recover",
+    "mhdg_gradient_refresh", "mhdg_precond_build", "mhdg_precond_apply", "mhdg_launch_count",
+)
+
+
+def check(rc: int, what: str) -> None:
+    if rc != MHDG_OK:
+        raise RuntimeError(f"{what} failed with status {rc}")
+
+
+def ptr(t) -> int | None:
+    """Device pointer of a torch tensor (None -> NULL)."""
+    return None if t is None else t.data_ptr()

@@ -1,0 +1,129 @@
+"""Second-layer static condensation on the device (the reference's condense API).
+
+CondensedSchur mirrors condense.py:54-127 of the reference: build() forms
+S = A_uu - A_uq A_qq^-1 A_qu and factorizes it (batched LU with partial
+pivoting instead of the reference's explicit np.linalg.inv, condense.py:67),
+apply_trace() is the matrix-free reduced trace operator (condense.py:91-103),
+rhs() and recover() the condensed right-hand side and local back-solve
+(condense.py:105-127).  Vectors are torch CUDA float64 tensors in the
+reference's global trace layout.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+from .assembly import LocalBlocks, raise_status
+from .device import current_stream
+
+
+class FactorizationError(RuntimeError):
+    """Local factorization failed (condense.py:40-41)."""
+
+
+class CondensedSchur:
+    def __init__(self, blocks: LocalBlocks, lu: torch.Tensor, perm: torch.Tensor):
+        self.blocks = blocks
+        self.lu = lu
+        self.perm = perm
+        fac = _lib.Factors()
+        fac.lu, fac.perm = _lib.ptr(lu), _lib.ptr(perm)
+        self._fac = fac
+        dd = blocks.disc.device
+        self._y_loc = torch.empty(dd.n_local_trace, dtype=torch.float64, device=dd.device)
+
+    @classmethod
+    def allocate(cls, blocks: LocalBlocks) -> "CondensedSchur":
+        disc = blocks.disc
+        n = disc.L * disc.ns
+        dev = disc.device.device
+        lu = torch.empty((disc.n_mac, n, n), dtype=torch.float64, device=dev)
+        perm = torch.empty((disc.n_mac, n), dtype=torch.int32, device=dev)
+        return cls(blocks, lu, perm)
+
+    @classmethod
+    def build(cls, blocks: LocalBlocks) -> "CondensedSchur":
+        self = cls.allocate(blocks)
+        self.refactor()
+        return self
+
+    def refactor(self) -> None:
+        """Schur complement + batched LU (mhdg_condense); raises FactorizationError."""
+        dd = self.disc.device
+        status = dd.status_buffer()
+        rc = _lib.lib().mhdg_condense(dd.c, self.blocks.c, self._fac, _lib.ptr(status), current_stream())
+        _lib.check(rc, "mhdg_condense")
+        raise_status(status, "condense")
+
+    def refactor_async(self, status: torch.Tensor) -> None:
+        """Same as refactor() without the host synchronisation (benchmarks)."""
+        dd = self.disc.device
+        rc = _lib.lib().mhdg_condense(dd.c, self.blocks.c, self._fac, _lib.ptr(status), current_stream())
+        _lib.check(rc, "mhdg_condense")
+
+    @property
+    def disc(self):
+        return self.blocks.disc
+
+    @property
+    def factor_entries(self) -> int:
+        return self.lu.numel()
+
+    # ------------------------------------------------------------------
+    def schur_matrix_into_factors(self) -> None:
+        """Write S (unfactorized) into self.lu; for parity tests."""
+        dd = self.disc.device
+        rc = _lib.lib().mhdg_schur_matrix(dd.c, self.blocks.c, self._fac, current_stream())
+        _lib.check(rc, "mhdg_schur_matrix")
+
+    def schur_solve(self, y: torch.Tensor) -> torch.Tensor:
+        dd = self.disc.device
+        out = torch.empty_like(y)
+        rc = _lib.lib().mhdg_lu_solve(dd.c, self._fac, _lib.ptr(y.contiguous()), _lib.ptr(out), current_stream())
+        _lib.check(rc, "mhdg_lu_solve")
+        return out
+
+    def apply_trace(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        """Matrix-free action of the reduced trace operator (condense.py:91-103)."""
+        dd = self.disc.device
+        y = torch.empty_like(x) if out is None else out
+        rc = _lib.lib().mhdg_apply_trace(dd.c, self.blocks.c, self._fac, _lib.ptr(x), _lib.ptr(y),
+                                         _lib.ptr(self._y_loc), current_stream())
+        _lib.check(rc, "mhdg_apply_trace")
+        return y
+
+    def apply_trace_local(self, x: torch.Tensor) -> torch.Tensor:
+        dd = self.disc.device
+        rc = _lib.lib().mhdg_apply_trace_local(dd.c, self.blocks.c, self._fac, _lib.ptr(x),
+                                               _lib.ptr(self._y_loc), current_stream())
+        _lib.check(rc, "mhdg_apply_trace_local")
+        return self._y_loc.view(self.disc.n_mac, self.disc.nf, self.disc.Lf, self.disc.ns).clone()
+
+    def rhs(self, res_grad, res_state, res_trace) -> torch.Tensor:
+        dd = self.disc.device
+        b = torch.empty(self.disc.n_trace, dtype=torch.float64, device=dd.device)
+        rc = _lib.lib().mhdg_condensed_rhs(dd.c, self.blocks.c, self._fac, _lib.ptr(res_grad.contiguous()),
+                                           _lib.ptr(res_state.contiguous()), _lib.ptr(res_trace.contiguous()),
+                                           _lib.ptr(b), _lib.ptr(self._y_loc), current_stream())
+        _lib.check(rc, "mhdg_condensed_rhs")
+        return b
+
+    def recover(self, res_grad, res_state, dtrace):
+        disc = self.disc
+        dev = disc.device.device
+        du = torch.empty((disc.n_mac, disc.L, disc.ns), dtype=torch.float64, device=dev)
+        dq = torch.empty((disc.n_mac, disc.dim, disc.L, disc.ns), dtype=torch.float64, device=dev)
+        rc = _lib.lib().mhdg_recover(disc.device.c, self.blocks.c, self._fac, _lib.ptr(res_grad.contiguous()),
+                                     _lib.ptr(res_state.contiguous()), _lib.ptr(dtrace.contiguous()),
+                                     _lib.ptr(du), _lib.ptr(dq), current_stream())
+        _lib.check(rc, "mhdg_recover")
+        return du, dq
+
+
+def condense(blocks: LocalBlocks, path: str = "schur") -> CondensedSchur:
+    """condense.py:261-266; only the second-layer path runs on the device (the
+    one-shot 'standard' path is a CPU oracle in the reference)."""
+    if path != "schur":
+        raise ValueError(f"unknown condensation path {path!r} (the device path is 'schur')")
+    return CondensedSchur.build(blocks)

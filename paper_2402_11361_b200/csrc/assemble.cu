@@ -1,0 +1,532 @@
+// Residual and Jacobian assembly, one CTA per macro-element.
+//
+// Restates assemble_system (assembly.py:339-618) of the reference:
+//   R_Q   = J M Q + weak-derivative(U) - face term(Uhat)      (assembly.py:360-365)
+//   R_U   = temporal mass + volume flux/source/SUPG terms      (assembly.py:367-457)
+//           + face numerical fluxes                           (assembly.py:477-533)
+//   R_hat = interior: -int phi [(F+G)(uhat).n + S(u-uhat)]; boundary: the
+//           boundary-operator rows (Dirichlet / isothermal wall, optionally
+//           moving)                                           (assembly.py:533-554)
+//   Jacobian: state_state (flux, SUPG W1^T tau W1, SUPG temporal, mass/PTC,
+//   face S), face_state_trace / face_trace_state / face_trace_trace with the
+//   boundary rows, the w*dG/dq stashes and the frozen coefficients
+//   (assembly.py:397-405, 459-475, 556-612).
+// Per-point Jacobian arrays are generated one entry per thread
+// (pointwise.cuh), so the stash stores are coalesced.  Every accumulation runs
+// in a fixed order (sub-element loop, inverse-incidence gathers): results are
+// bitwise reproducible run to run.
+#include "local_ops.cuh"
+#include "pointwise.cuh"
+
+namespace mhdg {
+
+constexpr int ASM_THREADS = 256;
+
+template <int D>
+struct AsmSmem {
+  int us, qs, uh, td, tf, gph, upt, qpt, wq, tq, prv, As, Adu, FG, Pp, sw, W1, cvol;
+  int fuh, fu, fq, fuv, fw, fpr, fpv, fS, fK1, ffn, fbh, cf, ctr, total;
+};
+
+template <int D>
+__host__ __device__ inline AsmSmem<D> asm_smem(const Sz& s) {
+  constexpr int NS = D + 2, NF = D + 1;
+  constexpr int PRIM = (int)((sizeof(Prim<D>) + 7) / 8);
+  AsmSmem<D> m;
+  int o = 0;
+#define TAKE(field, cnt) \
+  m.field = o;           \
+  o += (cnt);
+  TAKE(us, s.n)
+  TAKE(qs, D * s.n)
+  TAKE(uh, s.ltr)
+  TAKE(td, s.n)
+  TAKE(tf, s.ltr)
+  TAKE(gph, s.nq * s.nloc * D)
+  TAKE(upt, s.nq * NS)
+  TAKE(qpt, s.nq * D * NS)
+  TAKE(wq, s.nq)
+  TAKE(tq, s.nq)
+  TAKE(prv, s.nq * PRIM)
+  TAKE(As, s.nq * D * NS * NS)
+  TAKE(Adu, s.nq * D * NS * NS)
+  TAKE(FG, s.nq * NS * D)
+  TAKE(Pp, s.nq * D * NS)
+  TAKE(sw, s.nq * NS)
+  TAKE(W1, s.nq * s.nloc * NS * NS)
+  TAKE(cvol, s.n_sub * s.nloc * NS)
+  TAKE(fuh, s.nqf * NS)
+  TAKE(fu, s.nqf * NS)
+  TAKE(fq, s.nqf * D * NS)
+  TAKE(fuv, s.nqf * NS)
+  TAKE(fw, s.nqf)
+  TAKE(fpr, s.nqf * PRIM)
+  TAKE(fpv, s.nqf * PRIM)
+  TAKE(fS, s.nqf * NS * NS)
+  TAKE(fK1, s.nqf * NS * NS)
+  TAKE(ffn, s.nqf * NS)
+  TAKE(fbh, s.nqf * NS)
+  TAKE(cf, NF * s.n_tri * s.nlocf * NS)
+  TAKE(ctr, NF * s.n_tri * s.nlocf * NS)
+#undef TAKE
+  m.total = o;
+  return m;
+}
+
+// Interpolate nodal state (and gradient) to one quadrature point.
+template <int D>
+__device__ __forceinline__ void interp_point(const double* ph, int nb, const int* nodes, const int* nmap,
+                                             const double* src, int src_stride_l, const double* qs, int L,
+                                             double* uu, double* qv) {
+  constexpr int NS = D + 2;
+#pragma unroll
+  for (int s = 0; s < NS; ++s) uu[s] = 0.0;
+  if (qv) {
+#pragma unroll
+    for (int s = 0; s < D * NS; ++s) qv[s] = 0.0;
+  }
+  for (int a = 0; a < nb; ++a) {
+    const int node = nmap ? nmap[nodes[a]] : nodes[a];
+    const double p = ph[a];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) uu[s] += p * src[node * NS + s];
+    if (qv) {
+#pragma unroll
+      for (int l = 0; l < D; ++l)
+#pragma unroll
+        for (int s = 0; s < NS; ++s) qv[l * NS + s] += p * qs[(l * L + node) * NS + s];
+    }
+  }
+  (void)src_stride_l;
+}
+
+template <int D>
+__global__ void __launch_bounds__(ASM_THREADS)
+    k_assemble(mhdg_disc g, mhdg_flow flow, mhdg_stage stage, const double* __restrict__ u,
+               const double* __restrict__ q, const double* __restrict__ uhat, double* __restrict__ R_grad,
+               double* __restrict__ R_state, double* __restrict__ R_tl, int want_jac, mhdg_blocks bk,
+               mhdg_frozen fo, mhdg_frozen fi, int use_frozen, int* status) {
+  extern __shared__ double sm[];
+  constexpr int NS = D + 2, NF = D + 1, E = D + 1;
+  const Sz sz = make_sz<D>(g);
+  const AsmSmem<D> o = asm_smem<D>(sz);
+  const FlowC fl = make_flow<D>(flow);
+  const int mac = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+  const int n = sz.n, L = sz.L, Lf = sz.Lf, nq = sz.nq, nloc = sz.nloc, nqf = sz.nqf, nlocf = sz.nlocf;
+  const double det = g.det[mac];
+  const double* ij = g.inv_jac + (size_t)mac * D * D;
+  const bool temporal = stage.dt_coeff != 0.0 || stage.hist != nullptr;
+  const double inv_sdt = isinf(stage.supg_dt) ? 0.0 : 1.0 / stage.supg_dt;
+
+  double *us = sm + o.us, *qs = sm + o.qs, *uh = sm + o.uh, *td = sm + o.td, *tf = sm + o.tf;
+  double *gph = sm + o.gph, *upt = sm + o.upt, *qpt = sm + o.qpt, *wq = sm + o.wq, *tq = sm + o.tq;
+  Prim<D>* prv = (Prim<D>*)(sm + o.prv);
+  double *As = sm + o.As, *Adu = sm + o.Adu, *FG = sm + o.FG, *Pp = sm + o.Pp, *sw = sm + o.sw;
+  double *W1 = sm + o.W1, *cvol = sm + o.cvol;
+
+  // ---- load state ---------------------------------------------------------
+  for (int i = tid; i < n; i += nt) us[i] = u[(size_t)mac * n + i];
+  for (int i = tid; i < D * n; i += nt) qs[i] = q[(size_t)mac * D * n + i];
+  for (int i = tid; i < sz.ltr; i += nt) uh[i] = uhat[g.gather[(size_t)mac * sz.ltr + i]];
+  __syncthreads();
+  if (temporal)
+    for (int i = tid; i < n; i += nt)
+      td[i] = stage.hist ? stage.dt_coeff * us[i] + stage.hist[(size_t)mac * n + i] : stage.dt_coeff * us[i];
+
+  // ---- gradient equation residual (linear, assembly.py:360-365) -----------
+  for (int idx = tid; idx < sz.ltr; idx += nt) {
+    const int s = idx % NS, gg = (idx / NS) % Lf, f = idx / sz.bs;
+    double a = 0.0;
+    for (int h = 0; h < Lf; ++h) a += g.face_mass[gg * Lf + h] * uh[(f * Lf + h) * NS + s];
+    tf[idx] = a * (g.face_fac * g.areas[mac * NF + f]);
+  }
+  __syncthreads();
+  for (int idx = tid; idx < D * n; idx += nt) {
+    const int s = idx % NS, I = (idx / NS) % L, l = idx / n;
+    double a = 0.0;
+    for (int J = 0; J < L; ++J) a += g.mass[I * L + J] * qs[(l * L + J) * NS + s];
+    double b = 0.0;
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+      const double* Dr = g.weak_deriv + ((size_t)r * L + I) * L;
+      double t = 0.0;
+      for (int J = 0; J < L; ++J) t += Dr[J] * us[J * NS + s];
+      b += ij[r * D + l] * t;
+    }
+    double c = 0.0;
+    for (int e = g.vf_ptr[I]; e < g.vf_ptr[I + 1]; ++e) {
+      const int ent = g.vf_ent[e], f = ent / Lf;
+      c -= g.normals[(mac * NF + f) * D + l] * tf[ent * NS + s];
+    }
+    R_grad[(size_t)mac * D * n + idx] = (det * a + det * b) + c;
+  }
+
+  // ---- Jacobian initialisation (mass / PTC term, assembly.py:397-405) -----
+  if (want_jac) {
+    const double coeff = stage.dt_coeff + (isinf(stage.pseudo_dt) ? 0.0 : 1.0 / stage.pseudo_dt);
+    double* SSm = bk.state_state + (size_t)mac * n * n;
+    for (size_t i = tid; i < (size_t)n * n; i += nt) {
+      const int r = (int)(i / n), c = (int)(i % n);
+      const int I = r / NS, s = r % NS, J = c / NS, t = c % NS;
+      SSm[i] = (s == t && coeff != 0.0) ? coeff * det * g.mass[I * L + J] : 0.0;
+    }
+    const size_t fb = (size_t)NF * sz.bs * sz.bs;
+    for (size_t i = tid; i < fb; i += nt) {
+      bk.face_state_trace[(size_t)mac * fb + i] = 0.0;
+      bk.face_trace_state[(size_t)mac * fb + i] = 0.0;
+      bk.face_trace_trace[(size_t)mac * fb + i] = 0.0;
+    }
+    if (tid < NF) bk.trace_face_scale[mac * NF + tid] = g.bc_kind[mac * NF + tid] > 0 ? 0.0 : 1.0;
+  }
+  __syncthreads();
+
+  // ---- volume terms, one sub-element at a time (assembly.py:409-475) ------
+  const int nA = D * NS * NS;
+  for (int K = 0; K < sz.n_sub; ++K) {
+    const int* conn = g.sub_conn + K * nloc;
+    for (int idx = tid; idx < nq * nloc * D; idx += nt) {
+      const int k = idx % D, a = (idx / D) % nloc, qq = idx / (D * nloc);
+      const double* gr = g.grad_ref + (((size_t)K * nq + qq) * nloc + a) * D;
+      double v = 0.0;
+#pragma unroll
+      for (int r = 0; r < D; ++r) v += gr[r] * ij[r * D + k];
+      gph[idx] = v;  // gphys[q][a][k]
+    }
+    for (int qq = tid; qq < nq; qq += nt) {
+      double uu[NS], qv[D * NS];
+      interp_point<D>(g.phi_vol + qq * nloc, nloc, conn, nullptr, us, 0, qs, L, uu, qv);
+#pragma unroll
+      for (int s = 0; s < NS; ++s) upt[qq * NS + s] = uu[s];
+#pragma unroll
+      for (int s = 0; s < D * NS; ++s) qpt[qq * D * NS + s] = qv[s];
+      const int bad = admissible_code<D>(uu, fl.gamma);
+      if (bad) set_status(status, MHDG_ERR_ADMISSIBILITY, mac, bad - 1, uu[0]);
+      const Prim<D> p = prim<D>(uu, fl);
+      prv[qq] = p;
+      wq[qq] = g.w_ref[K * nq + qq] * det;
+      const size_t fidx = ((size_t)mac * sz.n_sub + K) * nq + qq;
+      tq[qq] = use_frozen ? fi.supg_tau[fidx] : supg_tau<D>(p, fl, g.h_sub[mac * sz.n_sub + K], inv_sdt);
+      if (want_jac) fo.supg_tau[fidx] = tq[qq];
+    }
+    __syncthreads();
+    // pointwise Jacobians and fluxes, one entry per thread
+    for (int idx = tid; idx < nq * nA; idx += nt) {
+      const int qq = idx / nA, e = idx % nA, t = e % NS, s = (e / NS) % NS, k = e / (NS * NS);
+      const size_t fidx = (((size_t)mac * sz.n_sub + K) * nq + qq) * nA + e;
+      const double a = euler_jac<D>(prv[qq], fl, k, s, t);
+      As[idx] = use_frozen ? fi.supg_jac[fidx] : a;
+      if (want_jac) {
+        Adu[idx] = a + visc_dgdu<D>(prv[qq], fl, qpt + qq * D * NS, k, s, t);
+        fo.supg_jac[fidx] = a;
+      }
+    }
+    for (int idx = tid; idx < nq * NS * D; idx += nt) {
+      const int qq = idx / (NS * D), k = idx % D, s = (idx / D) % NS;
+      FG[idx] = euler_flux<D>(prv[qq], upt + qq * NS, s, k) + visc_flux<D>(prv[qq], fl, qpt + qq * D * NS, s, k);
+    }
+    if (want_jac) {
+      const int nW = D * D * NS * NS;
+      double* Wd = bk.wdgdq_vol + (((size_t)mac * sz.n_sub + K) * nq) * nW;
+      for (int idx = tid; idx < nq * nW; idx += nt) {
+        const int qq = idx / nW, e = idx % nW, t = e % NS, s = (e / NS) % NS, l = (e / (NS * NS)) % D,
+                  k = e / (D * NS * NS);
+        Wd[idx] = wq[qq] * visc_dgdq<D>(prv[qq], fl, k, l, s, t);
+      }
+    }
+    __syncthreads();
+    // strong SUPG residual and the per-point residual vector Pp[q][k][s]
+    for (int qq = tid; qq < nq; qq += nt) {
+      double gu[D][NS], tdp[NS];
+#pragma unroll
+      for (int t = 0; t < NS; ++t) {
+        tdp[t] = 0.0;
+#pragma unroll
+        for (int k = 0; k < D; ++k) gu[k][t] = 0.0;
+      }
+      for (int a = 0; a < nloc; ++a) {
+        const int node = conn[a];
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+          const double gp = gph[(qq * nloc + a) * D + k];
+#pragma unroll
+          for (int t = 0; t < NS; ++t) gu[k][t] += gp * us[node * NS + t];
+        }
+        if (temporal) {
+          const double ph = g.phi_vol[qq * nloc + a];
+#pragma unroll
+          for (int t = 0; t < NS; ++t) tdp[t] += ph * td[node * NS + t];
+        }
+      }
+      const double* A = As + qq * nA;
+      double r[NS];
+#pragma unroll
+      for (int uu = 0; uu < NS; ++uu) {
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < D; ++k)
+#pragma unroll
+          for (int t = 0; t < NS; ++t) acc += A[(k * NS + uu) * NS + t] * gu[k][t];
+        r[uu] = acc + tdp[uu];
+      }
+      const double w = wq[qq], wt = w * tq[qq];
+#pragma unroll
+      for (int k = 0; k < D; ++k)
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+          double acc = 0.0;
+#pragma unroll
+          for (int uu = 0; uu < NS; ++uu) acc += A[(k * NS + uu) * NS + s] * r[uu];
+          Pp[(qq * D + k) * NS + s] = -w * FG[(qq * NS + s) * D + k] + wt * acc;
+        }
+      if (g.source) {
+        const double* src = g.source + (((size_t)mac * sz.n_sub + K) * nq + qq) * NS;
+#pragma unroll
+        for (int s = 0; s < NS; ++s) sw[qq * NS + s] = -w * src[s];
+      }
+    }
+    __syncthreads();
+    for (int idx = tid; idx < nloc * NS; idx += nt) {
+      const int s = idx % NS, a = idx / NS;
+      double acc = 0.0;
+      for (int qq = 0; qq < nq; ++qq) {
+#pragma unroll
+        for (int k = 0; k < D; ++k) acc += gph[(qq * nloc + a) * D + k] * Pp[(qq * D + k) * NS + s];
+        if (g.source) acc += g.phi_vol[qq * nloc + a] * sw[qq * NS + s];
+      }
+      cvol[(K * nloc + a) * NS + s] = acc;
+    }
+    if (want_jac) {
+      const int nw = nloc * NS * NS;
+      for (int idx = tid; idx < nq * nw; idx += nt) {
+        const int qq = idx / nw, e = idx % nw, s = e % NS, uu = (e / NS) % NS, a = e / (NS * NS);
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < D; ++k) acc += As[((qq * D + k) * NS + uu) * NS + s] * gph[(qq * nloc + a) * D + k];
+        W1[idx] = acc;  // W1[q][a][u][s]
+      }
+      __syncthreads();
+      // contrib[a,s,b,t] = -sum w Adu[k,s,t] gphys[a,k] phi[b] + sum w tau W1[a,u,s] W1[b,u,t]
+      //                    + dt_coeff sum w tau W1[a,t,s] phi[b]          (assembly.py:465-470)
+      double* SSm = bk.state_state + (size_t)mac * n * n;
+      const int nr = nloc * NS;
+      for (int idx = tid; idx < nr * nr; idx += nt) {
+        const int t = idx % NS, b = (idx / NS) % nloc, s = (idx / nr) % NS, a = idx / (nr * NS);
+        double acc = 0.0;
+        for (int qq = 0; qq < nq; ++qq) {
+          const double w = wq[qq], wt = w * tq[qq];
+          double y = 0.0;
+#pragma unroll
+          for (int k = 0; k < D; ++k) y += Adu[((qq * D + k) * NS + s) * NS + t] * gph[(qq * nloc + a) * D + k];
+          y = -w * y;
+          if (stage.dt_coeff != 0.0) y += stage.dt_coeff * wt * W1[((qq * nloc + a) * NS + t) * NS + s];
+          double z = 0.0;
+#pragma unroll
+          for (int uu = 0; uu < NS; ++uu)
+            z += W1[((qq * nloc + a) * NS + uu) * NS + s] * W1[((qq * nloc + b) * NS + uu) * NS + t];
+          acc += y * g.phi_vol[qq * nloc + b] + wt * z;
+        }
+        SSm[(size_t)(conn[a] * NS + s) * n + conn[b] * NS + t] += acc;
+      }
+    }
+    __syncthreads();
+  }
+
+  // ---- face terms (assembly.py:477-612) -----------------------------------
+  double *fuh = sm + o.fuh, *fu = sm + o.fu, *fq = sm + o.fq, *fuv = sm + o.fuv, *fw = sm + o.fw;
+  Prim<D>* fpr = (Prim<D>*)(sm + o.fpr);
+  Prim<D>* fpv = (Prim<D>*)(sm + o.fpv);
+  double *fS = sm + o.fS, *fK1 = sm + o.fK1, *ffn = sm + o.ffn, *fbh = sm + o.fbh, *cf = sm + o.cf,
+         *ctr = sm + o.ctr;
+  const int nqt = sz.n_tri * nqf;
+  for (int f = 0; f < NF; ++f) {
+    const int kind = g.bc_kind[mac * NF + f];
+    const double* nv = g.normals + (mac * NF + f) * D;
+    const int* fvn = g.face_vol_nodes + f * Lf;
+    const double e_w = g.wall_e[mac * NF + f];
+    const double* u_w = g.wall_u + (mac * NF + f) * D;
+    double uw2 = 0.0;
+#pragma unroll
+    for (int i = 0; i < D; ++i) uw2 += u_w[i] * u_w[i];
+    const double e_tot = e_w + 0.5 * uw2;
+    for (int T = 0; T < sz.n_tri; ++T) {
+      const int* tc = g.tri_conn + T * nlocf;
+      const size_t pbase = ((size_t)mac * NF + f) * nqt + T * nqf;  // face point index (frozen / stash)
+      for (int qq = tid; qq < nqf; qq += nt) {
+        double a_uh[NS], a_u[NS], a_q[D * NS];
+        const double* ph = g.phi_face + qq * nlocf;
+        interp_point<D>(ph, nlocf, tc, nullptr, uh + f * Lf * NS, 0, qs, L, a_uh, nullptr);
+        interp_point<D>(ph, nlocf, tc, fvn, us, 0, qs, L, a_u, a_q);
+        const int bad = admissible_code<D>(a_uh, fl.gamma);
+        if (bad) set_status(status, MHDG_ERR_ADMISSIBILITY, mac, bad - 1, a_uh[0]);
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+          fuh[qq * NS + s] = a_uh[s];
+          fu[qq * NS + s] = a_u[s];
+          fuv[qq * NS + s] = use_frozen ? fi.face_visc_state[(pbase + qq) * NS + s] : a_uh[s];
+          if (want_jac) fo.face_visc_state[(pbase + qq) * NS + s] = a_uh[s];
+        }
+#pragma unroll
+        for (int s = 0; s < D * NS; ++s) fq[qq * D * NS + s] = a_q[s];
+        fpr[qq] = prim<D>(a_uh, fl);
+        fpv[qq] = prim<D>(fuv + qq * NS, fl);
+        fw[qq] = g.w_face_ref[T * nqf + qq] * (g.face_fac * g.areas[mac * NF + f]);
+      }
+      __syncthreads();
+      for (int idx = tid; idx < nqf * NS * NS; idx += nt) {
+        const int qq = idx / (NS * NS), s = (idx / NS) % NS, t = idx % NS;
+        const double S = use_frozen ? fi.face_stab[(pbase + qq) * NS * NS + s * NS + t]
+                                    : ((s == t) ? stab_diag<D>(fpr[qq], fl, nv, s) : 0.0);
+        fS[idx] = S;
+        if (want_jac) {
+          fo.face_stab[(pbase + qq) * NS * NS + s * NS + t] = S;
+          double an = 0.0;
+#pragma unroll
+          for (int k = 0; k < D; ++k) an += euler_jac<D>(fpr[qq], fl, k, s, t) * nv[k];
+          fK1[idx] = an - S;  // d(flux.n)/d uhat, viscous uhat-dependence dropped
+        }
+      }
+      if (want_jac) {
+        const int nW = D * NS * NS;
+        double* Wf = bk.wdgdq_face + pbase * nW;
+        for (int idx = tid; idx < nqf * nW; idx += nt) {
+          const int qq = idx / nW, e = idx % nW, t = e % NS, s = (e / NS) % NS, l = e / (NS * NS);
+          double acc = 0.0;
+#pragma unroll
+          for (int k = 0; k < D; ++k) acc += visc_dgdq<D>(fpv[qq], fl, k, l, s, t) * nv[k];
+          Wf[idx] = fw[qq] * acc;
+        }
+      }
+      __syncthreads();
+      for (int idx = tid; idx < nqf * NS; idx += nt) {
+        const int qq = idx / NS, s = idx % NS;
+        double fn = 0.0;
+#pragma unroll
+        for (int k = 0; k < D; ++k)
+          fn += (euler_flux<D>(fpr[qq], fuh + qq * NS, s, k) + visc_flux<D>(fpv[qq], fl, fq + qq * D * NS, s, k)) *
+                nv[k];
+        double sa = 0.0;
+#pragma unroll
+        for (int t = 0; t < NS; ++t) sa += fS[(qq * NS + s) * NS + t] * (fu[qq * NS + t] - fuh[qq * NS + t]);
+        ffn[idx] = fn + sa;
+        if (kind == 1) {  // Dirichlet: uhat - u_D
+          fbh[idx] = fuh[idx] - g.u_dir[(pbase + qq) * NS + s];
+        } else if (kind == 2) {  // isothermal wall (moving with u_w)
+          const double rh = fuh[qq * NS];
+          double v;
+          if (s == 0) v = rh - fu[qq * NS];
+          else if (s <= D) v = fuh[idx] - rh * u_w[s - 1];
+          else v = fuh[qq * NS + E] - rh * e_tot;
+          fbh[idx] = v;
+        }
+      }
+      __syncthreads();
+      // projections onto the face sub-element's nodes
+      for (int idx = tid; idx < nlocf * NS; idx += nt) {
+        const int s = idx % NS, a = idx / NS;
+        double acc = 0.0, accb = 0.0;
+        for (int qq = 0; qq < nqf; ++qq) {
+          const double wp = fw[qq] * g.phi_face[qq * nlocf + a];
+          acc += wp * ffn[qq * NS + s];
+          if (kind > 0) accb += wp * fbh[qq * NS + s];
+        }
+        const int slot = ((f * sz.n_tri + T) * nlocf + a) * NS + s;
+        cf[slot] = acc;
+        ctr[slot] = kind > 0 ? accb : -acc;
+      }
+      if (want_jac) {
+        const int nr = nlocf * NS;
+        double* SSm = bk.state_state + (size_t)mac * n * n;
+        const size_t fboff = ((size_t)mac * NF + f) * sz.bs * sz.bs;
+        for (int idx = tid; idx < nr * nr; idx += nt) {
+          const int t = idx % NS, b = (idx / NS) % nlocf, s = (idx / nr) % NS, a = idx / (nr * NS);
+          double ust = 0.0, uss = 0.0, pr = 0.0;
+          for (int qq = 0; qq < nqf; ++qq) {
+            const double p = fw[qq] * g.phi_face[qq * nlocf + a] * g.phi_face[qq * nlocf + b];
+            ust += p * fK1[(qq * NS + s) * NS + t];
+            uss += p * fS[(qq * NS + s) * NS + t];
+            pr += p;
+          }
+          const int rl = tc[a] * NS + s, cl = tc[b] * NS + t;
+          bk.face_state_trace[fboff + (size_t)rl * sz.bs + cl] += ust;
+          SSm[(size_t)(fvn[tc[a]] * NS + s) * n + fvn[tc[b]] * NS + t] += uss;
+          double tst, ttt;
+          if (kind == 0) {
+            tst = -uss;
+            ttt = -ust;
+          } else {
+            // boundary rows: Khh (identity; wall: [1+i,0] = -u_w, [E,0] = -(e_w+|u_w|^2/2)), Kuu
+            double khh = (s == t) ? 1.0 : 0.0, kuu = 0.0;
+            if (kind == 2) {
+              if (t == 0 && s >= 1 && s <= D) khh = -u_w[s - 1];
+              if (t == 0 && s == E) khh = -e_tot;
+              if (s == 0 && t == 0) kuu = -1.0;
+            }
+            tst = pr * kuu;
+            ttt = pr * khh;
+          }
+          bk.face_trace_state[fboff + (size_t)rl * sz.bs + cl] += tst;
+          bk.face_trace_trace[fboff + (size_t)rl * sz.bs + cl] += ttt;
+        }
+      }
+      __syncthreads();
+    }
+  }
+
+  // ---- R_U and the local trace residual ------------------------------------
+  for (int idx = tid; idx < n; idx += nt) {
+    const int I = idx / NS, s = idx % NS;
+    double acc = 0.0;
+    if (temporal) {
+      double t = 0.0;
+      for (int J = 0; J < L; ++J) t += g.mass[I * L + J] * td[J * NS + s];
+      acc = det * t;
+    }
+    for (int e = g.vn_ptr[I]; e < g.vn_ptr[I + 1]; ++e) acc += cvol[g.vn_sub[e] * NS + s];
+    for (int e = g.vf_ptr[I]; e < g.vf_ptr[I + 1]; ++e) {
+      const int ent = g.vf_ent[e], f = ent / Lf, gg = ent % Lf;
+      for (int e2 = g.fn_ptr[gg]; e2 < g.fn_ptr[gg + 1]; ++e2)
+        acc += cf[(f * sz.n_tri * nlocf + g.fn_ent[e2]) * NS + s];
+    }
+    R_state[(size_t)mac * n + idx] = acc;
+  }
+  for (int idx = tid; idx < sz.ltr; idx += nt) {
+    const int s = idx % NS, gg = (idx / NS) % Lf, f = idx / sz.bs;
+    double acc = 0.0;
+    for (int e2 = g.fn_ptr[gg]; e2 < g.fn_ptr[gg + 1]; ++e2) acc += ctr[(f * sz.n_tri * nlocf + g.fn_ent[e2]) * NS + s];
+    R_tl[(size_t)mac * sz.ltr + idx] = acc;
+  }
+}
+
+int face_reduce(const mhdg_disc&, const double*, const double*, double, double*, cudaStream_t);
+
+template <int D>
+int assemble(const mhdg_disc& g, const mhdg_flow& fl, const mhdg_stage& sg, const double* u, const double* q,
+             const double* uhat, double* Rg, double* Ru, double* Rtl, double* Rt, int want_jac, const mhdg_blocks* b,
+             const mhdg_frozen* fo, const mhdg_frozen* fi, int* status, cudaStream_t st) {
+  const Sz sz = make_sz<D>(g);
+  const size_t bytes = sizeof(double) * asm_smem<D>(sz).total;
+  if (bytes > 227 * 1024) return MHDG_ERR_CONFIG;
+  if (bytes > 48 * 1024) cudaFuncSetAttribute(k_assemble<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  mhdg_blocks bb{};
+  mhdg_frozen fzo{}, fzi{};
+  if (want_jac) {
+    if (!b || !fo) return MHDG_ERR_CONFIG;
+    bb = *b;
+    fzo = *fo;
+  }
+  if (fi) fzi = *fi;
+  k_assemble<D><<<g.n_mac, ASM_THREADS, bytes, st>>>(g, fl, sg, u, q, uhat, Rg, Ru, Rtl, want_jac, bb, fzo, fzi,
+                                                     fi ? 1 : 0, status);
+  int rc = launch_ok();
+  if (rc) return rc;
+  return face_reduce(g, Rtl, nullptr, 0.0, Rt, st);
+}
+
+template int assemble<2>(const mhdg_disc&, const mhdg_flow&, const mhdg_stage&, const double*, const double*,
+                         const double*, double*, double*, double*, double*, int, const mhdg_blocks*, const mhdg_frozen*,
+                         const mhdg_frozen*, int*, cudaStream_t);
+template int assemble<3>(const mhdg_disc&, const mhdg_flow&, const mhdg_stage&, const double*, const double*,
+                         const double*, double*, double*, double*, double*, int, const mhdg_blocks*, const mhdg_frozen*,
+                         const mhdg_frozen*, int*, cudaStream_t);
+
+}  // namespace mhdg

@@ -1,0 +1,102 @@
+// extern "C" boundary (include/mhdg.h): dispatch on the dimension and launch.
+#include "common.cuh"
+
+namespace mhdg {
+long long g_launches = 0;
+
+template <int D> int apply_local(const mhdg_disc&, const mhdg_blocks&, const mhdg_factors&, const double*, double*, cudaStream_t);
+template <int D> int rhs_local(const mhdg_disc&, const mhdg_blocks&, const mhdg_factors&, const double*, const double*, double*, cudaStream_t);
+template <int D> int recover(const mhdg_disc&, const mhdg_blocks&, const mhdg_factors&, const double*, const double*, const double*, double*, double*, cudaStream_t);
+template <int D> int grad_refresh(const mhdg_disc&, const double*, const double*, double*, cudaStream_t);
+template <int D> int schur_matrix(const mhdg_disc&, const mhdg_blocks&, double*, cudaStream_t);
+template <int D> int assemble(const mhdg_disc&, const mhdg_flow&, const mhdg_stage&, const double*, const double*,
+                              const double*, double*, double*, double*, double*, int, const mhdg_blocks*,
+                              const mhdg_frozen*, const mhdg_frozen*, int*, cudaStream_t);
+template <int D> int precond_build(const mhdg_disc&, const mhdg_blocks&, double*, int*, cudaStream_t);
+int precond_apply(const mhdg_disc&, const double*, const double*, double*, cudaStream_t);
+int face_reduce(const mhdg_disc&, const double*, const double*, double, double*, cudaStream_t);
+int lu_solve(const mhdg_disc&, const mhdg_factors&, const double*, double*, cudaStream_t);
+int lu_factor(int n, int n_mac, double* LU, int* perm, int* status, cudaStream_t st);
+size_t lu_smem_bytes(int n);
+}  // namespace mhdg
+
+using namespace mhdg;
+
+#define DISPATCH(g, call2, call3) \
+  ((g)->dim == 2 ? (call2) : (g)->dim == 3 ? (call3) : MHDG_ERR_CONFIG)
+
+static inline cudaStream_t S(void* s) { return (cudaStream_t)s; }
+
+extern "C" {
+
+long long mhdg_launch_count(void) { return g_launches; }
+
+int mhdg_apply_trace_local(const mhdg_disc* g, const mhdg_blocks* b, const mhdg_factors* f, const double* x,
+                           double* y_loc, void* st) {
+  return DISPATCH(g, apply_local<2>(*g, *b, *f, x, y_loc, S(st)), apply_local<3>(*g, *b, *f, x, y_loc, S(st)));
+}
+
+int mhdg_face_reduce(const mhdg_disc* g, const double* y_loc, double* y, void* st) {
+  return face_reduce(*g, y_loc, nullptr, 0.0, y, S(st));
+}
+
+int mhdg_apply_trace(const mhdg_disc* g, const mhdg_blocks* b, const mhdg_factors* f, const double* x, double* y,
+                     double* y_loc, void* st) {
+  int rc = mhdg_apply_trace_local(g, b, f, x, y_loc, st);
+  if (rc) return rc;
+  return face_reduce(*g, y_loc, nullptr, 0.0, y, S(st));
+}
+
+int mhdg_condensed_rhs(const mhdg_disc* g, const mhdg_blocks* b, const mhdg_factors* f, const double* Rg,
+                       const double* Ru, const double* Rt, double* bvec, double* b_loc, void* st) {
+  int rc = DISPATCH(g, rhs_local<2>(*g, *b, *f, Rg, Ru, b_loc, S(st)), rhs_local<3>(*g, *b, *f, Rg, Ru, b_loc, S(st)));
+  if (rc) return rc;
+  return face_reduce(*g, b_loc, Rt, -1.0, bvec, S(st));
+}
+
+int mhdg_recover(const mhdg_disc* g, const mhdg_blocks* b, const mhdg_factors* f, const double* Rg,
+                 const double* Ru, const double* dtr, double* du, double* dq, void* st) {
+  return DISPATCH(g, recover<2>(*g, *b, *f, Rg, Ru, dtr, du, dq, S(st)),
+                  recover<3>(*g, *b, *f, Rg, Ru, dtr, du, dq, S(st)));
+}
+
+int mhdg_gradient_refresh(const mhdg_disc* g, const double* u, const double* uhat, double* q, void* st) {
+  return DISPATCH(g, grad_refresh<2>(*g, u, uhat, q, S(st)), grad_refresh<3>(*g, u, uhat, q, S(st)));
+}
+
+int mhdg_schur_matrix(const mhdg_disc* g, const mhdg_blocks* b, const mhdg_factors* f, void* st) {
+  return DISPATCH(g, schur_matrix<2>(*g, *b, f->lu, S(st)), schur_matrix<3>(*g, *b, f->lu, S(st)));
+}
+
+int mhdg_lu_factor(const mhdg_disc* g, const mhdg_factors* f, int* status, void* st) {
+  const int n = g->L * g->ns;
+  if (lu_smem_bytes(n) > 227 * 1024) return MHDG_ERR_CONFIG;
+  return lu_factor(n, g->n_mac, f->lu, f->perm, status, S(st));
+}
+
+int mhdg_condense(const mhdg_disc* g, const mhdg_blocks* b, const mhdg_factors* f, int* status, void* st) {
+  int rc = mhdg_schur_matrix(g, b, f, st);
+  if (rc) return rc;
+  return mhdg_lu_factor(g, f, status, st);
+}
+
+int mhdg_lu_solve(const mhdg_disc* g, const mhdg_factors* f, const double* bvec, double* y, void* st) {
+  return lu_solve(*g, *f, bvec, y, S(st));
+}
+
+int mhdg_assemble(const mhdg_disc* g, const mhdg_flow* fl, const mhdg_stage* sg, const double* u, const double* q,
+                  const double* uhat, double* Rg, double* Ru, double* Rtl, double* Rt, int want_jac,
+                  const mhdg_blocks* b, const mhdg_frozen* fo, const mhdg_frozen* fi, int* status, void* st) {
+  return DISPATCH(g, assemble<2>(*g, *fl, *sg, u, q, uhat, Rg, Ru, Rtl, Rt, want_jac, b, fo, fi, status, S(st)),
+                  assemble<3>(*g, *fl, *sg, u, q, uhat, Rg, Ru, Rtl, Rt, want_jac, b, fo, fi, status, S(st)));
+}
+
+int mhdg_precond_build(const mhdg_disc* g, const mhdg_blocks* b, double* inv, int* status, void* st) {
+  return DISPATCH(g, precond_build<2>(*g, *b, inv, status, S(st)), precond_build<3>(*g, *b, inv, status, S(st)));
+}
+
+int mhdg_precond_apply(const mhdg_disc* g, const double* inv, const double* v, double* y, void* st) {
+  return precond_apply(*g, inv, v, y, S(st));
+}
+
+}  // extern "C"

@@ -1,0 +1,79 @@
+// Shared helpers for the sm_100a macro-element HDG kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/mhdg.h"
+
+#define MHDG_FULL 0xffffffffu
+
+namespace mhdg {
+
+extern long long g_launches;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(MHDG_FULL, v, o);
+  return v;
+}
+
+__device__ __forceinline__ double ldg(const double* p) { return __ldg(p); }
+__device__ __forceinline__ int ldg(const int* p) { return __ldg(p); }
+
+// First failing thread records (code, index, component, value) in status[4].
+__device__ __forceinline__ void set_status(int* status, int code, int index, int comp, double val) {
+  if (status == nullptr) return;
+  if (atomicCAS(status, 0, code) == 0) {
+    status[1] = index;
+    status[2] = comp;
+    status[3] = __float_as_int((float)val);
+    __threadfence();
+  }
+}
+
+inline int launch_ok() {
+  ++g_launches;
+  return cudaPeekAtLastError() == cudaSuccess ? MHDG_OK : MHDG_ERR_CUDA;
+}
+
+// Row-major (rows x cols) global matrix times a shared-memory vector:
+// out[r] (op)= sum_c A[r, c] * xs[c].  One warp per row, four rows in flight.
+template <bool ACCUM>
+__device__ __forceinline__ void warp_gemv(const double* __restrict__ A, int rows, int cols,
+                                          const double* xs, double* out, double sign) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int r = warp * 4;
+  for (; r + 3 < rows; r += nw * 4) {
+    const double* a0 = A + (size_t)r * cols;
+    double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+    for (int c = lane; c < cols; c += 32) {
+      double xc = xs[c];
+      s0 += __ldg(a0 + c) * xc;
+      s1 += __ldg(a0 + cols + c) * xc;
+      s2 += __ldg(a0 + 2 * cols + c) * xc;
+      s3 += __ldg(a0 + 3 * cols + c) * xc;
+    }
+    s0 = warp_sum(s0);
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    s3 = warp_sum(s3);
+    if (lane == 0) {
+      if (ACCUM) {
+        out[r] += sign * s0; out[r + 1] += sign * s1; out[r + 2] += sign * s2; out[r + 3] += sign * s3;
+      } else {
+        out[r] = sign * s0; out[r + 1] = sign * s1; out[r + 2] = sign * s2; out[r + 3] = sign * s3;
+      }
+    }
+  }
+  for (; r < rows; ++r) {  // tail rows (< 4), handled by the warp that reached them
+    const double* a0 = A + (size_t)r * cols;
+    double s0 = 0;
+    for (int c = lane; c < cols; c += 32) s0 += __ldg(a0 + c) * xs[c];
+    s0 = warp_sum(s0);
+    if (lane == 0) {
+      if (ACCUM) out[r] += sign * s0; else out[r] = sign * s0;
+    }
+  }
+}
+
+}  // namespace mhdg

@@ -1,0 +1,326 @@
+// Second-layer static condensation on the device.
+//
+// k_schur   S = state_state - A_uq A_qq^-1 A_qu   (_schur_correction,
+//           condense.py:130-158).  Per sub-element (and face sub-element) the
+//           correction is one GEMM  X[(a,s,r), j] = sum_{(q,l)} T1[(a,s,r),(q,l)] VW[(q,l), j]
+//           with T1 = sum_k gphys W (the dG/dq stash) and
+//           VW[q,l,j] = sum_r inv_jac[r,l] PM[q,r,j], PM = phi M^-1 D (a
+//           macro-independent table), scattered into the rows of the
+//           sub-element's nodes.
+// k_lu      in-place LU with partial pivoting of each macro's S (replaces the
+//           reference's np.linalg.inv, condense.py:66-69; FactorizationError on
+//           an exactly zero pivot).  Right-looking, 32-column panels in shared
+//           memory, 64x64 register-tiled trailing updates.
+#include "common.cuh"
+#include "local_ops.cuh"
+
+namespace mhdg {
+
+constexpr int SCHUR_THREADS = 256;
+constexpr int LU_THREADS = 256;
+constexpr int LU_NB = 32;
+
+// --------------------------------------------------------------------------
+// Schur complement
+// --------------------------------------------------------------------------
+
+template <int D>
+__global__ void __launch_bounds__(SCHUR_THREADS) k_schur(mhdg_disc g, mhdg_blocks b, double* __restrict__ S) {
+  extern __shared__ double sm[];
+  constexpr int NS = D + 2, NF = D + 1;
+  const Sz sz = make_sz<D>(g);
+  const int mac = blockIdx.x, n = sz.n, L = sz.L;
+  const double* ij = g.inv_jac + (size_t)mac * D * D;
+  double* Sm = S + (size_t)mac * n * n;
+  const double* SS = b.state_state + (size_t)mac * n * n;
+  for (size_t i = threadIdx.x; i < (size_t)n * n; i += blockDim.x) Sm[i] = SS[i];
+  __syncthreads();
+
+  // shared: T1 (rows nloc*NS, k = nq*D) for one r, VW (nq*D x L), ijs
+  const int kv = sz.nq * D, kf = sz.nqf * D;
+  const int kmax = kv > kf ? kv : kf;
+  const int rmax = sz.nloc * NS > sz.nlocf * NS ? sz.nloc * NS : sz.nlocf * NS;
+  double* T1 = sm;
+  double* VW = T1 + rmax * kmax;
+
+  // ---- volume sub-elements ----
+  for (int K = 0; K < sz.n_sub; ++K) {
+    // VW[(q,l), j] = sum_r inv_jac[r,l] PM[K,q,r,j]
+    for (int idx = threadIdx.x; idx < kv * L; idx += blockDim.x) {
+      const int j = idx % L, ql = idx / L, l = ql % D, q = ql / D;
+      const double* pm = g.pm_vol + (((size_t)K * sz.nq + q) * D) * L + j;
+      double a = 0.0;
+#pragma unroll
+      for (int r = 0; r < D; ++r) a += __ldg(ij + r * D + l) * __ldg(pm + r * L);
+      VW[idx] = a;
+    }
+    for (int rr = 0; rr < NS; ++rr) {
+      // T1[(a,s),(q,l)] = sum_k gphys[q,a,k] W[K,q,k,l,s,rr]
+      for (int idx = threadIdx.x; idx < sz.nloc * NS * kv; idx += blockDim.x) {
+        const int ql = idx % kv, as = idx / kv, s = as % NS, a = as / NS, l = ql % D, q = ql / D;
+        const double* gr = g.grad_ref + (((size_t)K * sz.nq + q) * sz.nloc + a) * D;
+        const double* W = b.wdgdq_vol + ((((size_t)mac * sz.n_sub + K) * sz.nq + q) * D * D) * NS * NS;
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+          double gp = 0.0;
+#pragma unroll
+          for (int r = 0; r < D; ++r) gp += __ldg(gr + r) * __ldg(ij + r * D + k);
+          acc += gp * __ldg(W + ((k * D + l) * NS + s) * NS + rr);
+        }
+        T1[idx] = acc;
+      }
+      __syncthreads();
+      // S[(conn[a],s), (j,rr)] += sum_{ql} T1[(a,s), ql] VW[ql, j]
+      for (int idx = threadIdx.x; idx < sz.nloc * NS * L; idx += blockDim.x) {
+        const int j = idx % L, as = idx / L, s = as % NS, a = as / NS;
+        const double* t = T1 + as * kv;
+        double acc = 0.0;
+        for (int k = 0; k < kv; ++k) acc += t[k] * VW[k * L + j];
+        const int row = __ldg(g.sub_conn + K * sz.nloc + a) * NS + s;
+        Sm[(size_t)row * n + j * NS + rr] += acc;
+      }
+      __syncthreads();
+    }
+  }
+  // ---- face sub-elements ----
+  for (int f = 0; f < NF; ++f) {
+    for (int T = 0; T < sz.n_tri; ++T) {
+      for (int idx = threadIdx.x; idx < kf * L; idx += blockDim.x) {
+        const int j = idx % L, ql = idx / L, l = ql % D, q = ql / D;
+        const double* pm = g.pm_face + ((((size_t)f * sz.n_tri + T) * sz.nqf + q) * D) * L + j;
+        double a = 0.0;
+#pragma unroll
+        for (int r = 0; r < D; ++r) a += __ldg(ij + r * D + l) * __ldg(pm + r * L);
+        VW[idx] = a;
+      }
+      for (int rr = 0; rr < NS; ++rr) {
+        for (int idx = threadIdx.x; idx < sz.nlocf * NS * kf; idx += blockDim.x) {
+          const int ql = idx % kf, as = idx / kf, s = as % NS, a = as / NS, l = ql % D, q = ql / D;
+          const double* W = b.wdgdq_face +
+                            ((((size_t)mac * NF + f) * sz.n_tri * sz.nqf + T * sz.nqf + q) * D + l) * NS * NS;
+          T1[idx] = __ldg(W + s * NS + rr) * __ldg(g.phi_face + q * sz.nlocf + a);
+        }
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < sz.nlocf * NS * L; idx += blockDim.x) {
+          const int j = idx % L, as = idx / L, s = as % NS, a = as / NS;
+          const double* t = T1 + as * kf;
+          double acc = 0.0;
+          for (int k = 0; k < kf; ++k) acc += t[k] * VW[k * L + j];
+          const int node = __ldg(g.face_vol_nodes + f * sz.Lf + __ldg(g.tri_conn + T * sz.nlocf + a));
+          Sm[(size_t)(node * NS + s) * n + j * NS + rr] -= acc;
+        }
+        __syncthreads();
+      }
+    }
+  }
+}
+
+// --------------------------------------------------------------------------
+// batched LU with partial pivoting
+// --------------------------------------------------------------------------
+
+__device__ __forceinline__ void block_argmax(double v, int i, double* rv, int* ri, double* outv, int* outi) {
+  // max |v|, ties -> smallest index (LAPACK idamax semantics)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    double v2 = __shfl_xor_sync(MHDG_FULL, v, o);
+    int i2 = __shfl_xor_sync(MHDG_FULL, i, o);
+    if (v2 > v || (v2 == v && i2 < i)) { v = v2; i = i2; }
+  }
+  if (lane == 0) { rv[warp] = v; ri[warp] = i; }
+  __syncthreads();
+  if (warp == 0) {
+    v = lane < nw ? rv[lane] : -1.0;
+    i = lane < nw ? ri[lane] : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      double v2 = __shfl_xor_sync(MHDG_FULL, v, o);
+      int i2 = __shfl_xor_sync(MHDG_FULL, i, o);
+      if (v2 > v || (v2 == v && i2 < i)) { v = v2; i = i2; }
+    }
+    if (lane == 0) { *outv = v; *outi = i; }
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(LU_THREADS) k_lu(int n, double* __restrict__ LU, int* __restrict__ perm,
+                                                   int* status) {
+  extern __shared__ double sm[];
+  constexpr int PW = LU_NB + 1;  // padded panel row
+  const int mac = blockIdx.x, tid = threadIdx.x;
+  double* A = LU + (size_t)mac * n * n;
+  int* pm = perm + (size_t)mac * n;
+  double* P = sm;                               // n x PW panel
+  double* Ut = P + (size_t)n * PW;              // LU_NB x 64 U12 tile
+  double* Ar = Ut + LU_NB * 64;                 // LU_NB x 64 staged A12 tile
+  double* Li = Ar + LU_NB * 64;                 // LU_NB x PW  L11^-1
+  double* red_v = Li + LU_NB * PW;              // 32
+  int* red_i = (int*)(red_v + 32);              // 32
+  int* piv = red_i + 32;                        // LU_NB
+  double* bcast = (double*)(piv + LU_NB + 2);   // 2 (aligned below)
+  int* bidx = (int*)(bcast + 2);
+  for (int i = tid; i < n; i += blockDim.x) pm[i] = i;
+  bool singular = false;
+
+  for (int k0 = 0; k0 < n; k0 += LU_NB) {
+    const int nb = min(LU_NB, n - k0), m = n - k0;
+    for (int idx = tid; idx < m * nb; idx += blockDim.x) {
+      const int i = idx / nb, c = idx - i * nb;
+      P[i * PW + c] = A[(size_t)(k0 + i) * n + k0 + c];
+    }
+    __syncthreads();
+    for (int j = 0; j < nb; ++j) {
+      // pivot search over panel rows j..m-1 of column j
+      double best = -1.0;
+      int bi = 0x7fffffff;
+      for (int i = j + tid; i < m; i += blockDim.x) {
+        const double v = fabs(P[i * PW + j]);
+        if (v > best || (v == best && i < bi)) { best = v; bi = i; }
+      }
+      block_argmax(best, bi, red_v, red_i, bcast, bidx);
+      const int p = *bidx;
+      if (tid == 0) piv[j] = p;
+      if (*bcast == 0.0) singular = true;
+      if (p != j) {
+        for (int c = tid; c < nb; c += blockDim.x) {
+          const double t = P[j * PW + c];
+          P[j * PW + c] = P[p * PW + c];
+          P[p * PW + c] = t;
+        }
+      }
+      __syncthreads();
+      const double dinv = singular ? 0.0 : 1.0 / P[j * PW + j];
+      for (int i = j + 1 + tid; i < m; i += blockDim.x) P[i * PW + j] *= dinv;
+      __syncthreads();
+      // rank-1 update of the remaining panel columns
+      const int w = nb - j - 1;
+      if (w > 0) {
+        for (int idx = tid; idx < (m - j - 1) * w; idx += blockDim.x) {
+          const int i = j + 1 + idx / w, c = j + 1 + idx % w;
+          P[i * PW + c] -= P[i * PW + j] * P[j * PW + c];
+        }
+      }
+      __syncthreads();
+    }
+    // write the panel back; apply the panel's interchanges to the other columns
+    for (int idx = tid; idx < m * nb; idx += blockDim.x) {
+      const int i = idx / nb, c = idx - i * nb;
+      A[(size_t)(k0 + i) * n + k0 + c] = P[i * PW + c];
+    }
+    for (int j = 0; j < nb; ++j) {
+      const int p = piv[j];
+      if (p == j) continue;
+      const size_t r1 = (size_t)(k0 + j) * n, r2 = (size_t)(k0 + p) * n;
+      for (int c = tid; c < n - nb; c += blockDim.x) {
+        const int cc = c < k0 ? c : c + nb;
+        const double t = A[r1 + cc];
+        A[r1 + cc] = A[r2 + cc];
+        A[r2 + cc] = t;
+      }
+      if (tid == 0) {
+        const int t = pm[k0 + j];
+        pm[k0 + j] = pm[k0 + p];
+        pm[k0 + p] = t;
+      }
+      __syncthreads();
+    }
+    __syncthreads();
+    const int c0 = k0 + nb;
+    if (c0 >= n) break;
+    // Li = L11^-1 (unit lower), one column per thread
+    for (int c = tid; c < LU_NB; c += blockDim.x) {
+      for (int i = 0; i < LU_NB; ++i) Li[i * PW + c] = (i == c) ? 1.0 : 0.0;
+      for (int i = c + 1; i < nb; ++i) {
+        double acc = 0.0;
+        for (int k = c; k < i; ++k) acc += P[i * PW + k] * Li[k * PW + c];
+        Li[i * PW + c] = -acc;
+      }
+    }
+    __syncthreads();
+    // per 64-column tile: U12 = Li A12 (staged in smem), then A22 -= L21 U12
+    const int rows = n - c0;
+    const int tx = tid & 15, ty = tid >> 4;
+    for (int tc = 0; tc < rows; tc += 64) {
+      const int wc = min(64, rows - tc);
+      for (int idx = tid; idx < LU_NB * 64; idx += blockDim.x) {
+        const int r = idx / 64, c = idx % 64;
+        Ar[r * 64 + c] = (c < wc && r < nb) ? A[(size_t)(k0 + r) * n + c0 + tc + c] : 0.0;
+      }
+      __syncthreads();
+      for (int idx = tid; idx < LU_NB * 64; idx += blockDim.x) {
+        const int r = idx / 64, c = idx % 64;
+        double acc = 0.0;
+        for (int k = 0; k <= r; ++k) acc += Li[r * PW + k] * Ar[k * 64 + c];
+        Ut[r * 64 + c] = acc;
+        if (c < wc && r < nb) A[(size_t)(k0 + r) * n + c0 + tc + c] = acc;
+      }
+      __syncthreads();
+      for (int tr = 0; tr < rows; tr += 64) {
+        double acc[4][4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int bq = 0; bq < 4; ++bq) acc[a][bq] = 0.0;
+        for (int k = 0; k < nb; ++k) {
+          double lv[4], uv[4];
+#pragma unroll
+          for (int a = 0; a < 4; ++a) {
+            const int i = tr + ty + 16 * a;
+            lv[a] = i < rows ? P[(nb + i) * PW + k] : 0.0;
+          }
+#pragma unroll
+          for (int bq = 0; bq < 4; ++bq) uv[bq] = Ut[k * 64 + tx + 16 * bq];
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int bq = 0; bq < 4; ++bq) acc[a][bq] += lv[a] * uv[bq];
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          const int i = tr + ty + 16 * a;
+          if (i >= rows) continue;
+#pragma unroll
+          for (int bq = 0; bq < 4; ++bq) {
+            const int c = tx + 16 * bq;
+            if (c < wc) A[(size_t)(c0 + i) * n + c0 + tc + c] -= acc[a][bq];
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (singular && tid == 0) set_status(status, MHDG_ERR_FACTORIZATION, mac, 0, 0.0);
+}
+
+// --------------------------------------------------------------------------
+// host launchers
+// --------------------------------------------------------------------------
+
+template <int D>
+int schur_matrix(const mhdg_disc& g, const mhdg_blocks& b, double* S, cudaStream_t st) {
+  constexpr int NS = D + 2;
+  const int kv = g.nq * D, kf = g.nqf * D, kmax = kv > kf ? kv : kf;
+  const int rmax = (g.nloc > g.nlocf ? g.nloc : g.nlocf) * NS;
+  const size_t bytes = sizeof(double) * ((size_t)rmax * kmax + (size_t)kmax * g.L);
+  if (bytes > 48 * 1024) cudaFuncSetAttribute(k_schur<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  k_schur<D><<<g.n_mac, SCHUR_THREADS, bytes, st>>>(g, b, S);
+  return launch_ok();
+}
+
+size_t lu_smem_bytes(int n) {
+  return sizeof(double) * ((size_t)n * (LU_NB + 1) + 2 * LU_NB * 64 + LU_NB * (LU_NB + 1) + 32 + 8) + sizeof(int) * (32 + LU_NB + 8) + 64;
+}
+
+int lu_factor(int n, int n_mac, double* LU, int* perm, int* status, cudaStream_t st) {
+  const size_t bytes = lu_smem_bytes(n);
+  if (bytes > 48 * 1024) cudaFuncSetAttribute(k_lu, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  k_lu<<<n_mac, LU_THREADS, bytes, st>>>(n, LU, perm, status);
+  return launch_ok();
+}
+
+template int schur_matrix<2>(const mhdg_disc&, const mhdg_blocks&, double*, cudaStream_t);
+template int schur_matrix<3>(const mhdg_disc&, const mhdg_blocks&, double*, cudaStream_t);
+
+}  // namespace mhdg

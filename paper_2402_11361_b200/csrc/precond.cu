@@ -1,0 +1,131 @@
+// Face-block preconditioner (krylov.py:194-238).
+//
+// k_precond_build: one CTA per skeleton face: B_f = sum over the face's sides
+// (flat (mac, lf) order, as np.add.at) of P^T face_trace_trace P, with P the
+// side's canonical node permutation (recovered from `gather`); symmetrise,
+// Cholesky (PreconditionerError naming the face if not positive definite),
+// explicit inverse via L^-T L^-1 as cho_solve(., I) does.
+// k_precond_apply: y_f = inv_f v_f, one CTA per face.
+#include "common.cuh"
+
+namespace mhdg {
+
+constexpr int PRE_THREADS = 256;
+
+template <int D>
+__global__ void __launch_bounds__(PRE_THREADS) k_precond_build(mhdg_disc g, mhdg_blocks b, double* __restrict__ inv,
+                                                               int* status) {
+  extern __shared__ double sm[];
+  constexpr int NS = D + 2, NF = D + 1;
+  const int f = blockIdx.x, bs = g.Lf * NS, tid = threadIdx.x;
+  double* B = sm;            // bs x bs
+  double* X = B + bs * bs;   // bs x bs
+  __shared__ int fail;
+  if (tid == 0) fail = 0;
+  for (int i = tid; i < bs * bs; i += blockDim.x) B[i] = 0.0;
+  __syncthreads();
+  // sides in flat (mac, lf) order
+  int m0 = g.face_macros[2 * f], m1 = g.face_macros[2 * f + 1];
+  int l0 = g.face_locals[2 * f], l1 = g.face_locals[2 * f + 1];
+  if (m1 >= 0 && (m1 * NF + l1) < (m0 * NF + l0)) {
+    int t = m0; m0 = m1; m1 = t;
+    t = l0; l0 = l1; l1 = t;
+  }
+  for (int side = 0; side < 2; ++side) {
+    const int mac = side ? m1 : m0, lf = side ? l1 : l0;
+    if (mac < 0) continue;
+    const int* gat = g.gather + ((size_t)mac * NF + lf) * bs;
+    const double* A = b.face_trace_trace + ((size_t)mac * NF + lf) * bs * bs;
+    for (int idx = tid; idx < bs * bs; idx += blockDim.x) {
+      const int r = idx / bs, c = idx - r * bs;
+      const int pr = gat[r] - f * bs, pc = gat[c] - f * bs;
+      B[pr * bs + pc] += A[idx];  // each (pr, pc) hit once per side: no race
+    }
+    __syncthreads();
+  }
+  for (int idx = tid; idx < bs * bs; idx += blockDim.x) {
+    const int r = idx / bs, c = idx - r * bs;
+    if (c <= r) {
+      const double v = 0.5 * (B[r * bs + c] + B[c * bs + r]);
+      X[r * bs + c] = v;  // symmetric part, lower triangle
+    }
+  }
+  __syncthreads();
+  // right-looking Cholesky in X (lower)
+  for (int j = 0; j < bs; ++j) {
+    const double d = X[j * bs + j];
+    if (!(d > 0.0)) {
+      if (tid == 0) fail = 1;
+      break;
+    }
+    const double ljj = sqrt(d);
+    __syncthreads();
+    for (int i = j + 1 + tid; i < bs; i += blockDim.x) X[i * bs + j] /= ljj;
+    if (tid == 0) X[j * bs + j] = ljj;
+    __syncthreads();
+    const int w = bs - j - 1;
+    for (int idx = tid; idx < w * w; idx += blockDim.x) {
+      const int i = j + 1 + idx / w, k = j + 1 + idx % w;
+      if (k <= i) X[i * bs + k] -= X[i * bs + j] * X[k * bs + j];
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  if (fail) {
+    if (tid == 0) set_status(status, MHDG_ERR_PRECONDITIONER, f, 0, 0.0);
+    return;
+  }
+  // B <- L^-1 (lower), one column per thread
+  for (int c = tid; c < bs; c += blockDim.x) {
+    for (int i = 0; i < c; ++i) B[i * bs + c] = 0.0;
+    B[c * bs + c] = 1.0 / X[c * bs + c];
+    for (int i = c + 1; i < bs; ++i) {
+      double acc = 0.0;
+      for (int k = c; k < i; ++k) acc += X[i * bs + k] * B[k * bs + c];
+      B[i * bs + c] = -acc / X[i * bs + i];
+    }
+  }
+  __syncthreads();
+  // inv = L^-T L^-1
+  double* out = inv + (size_t)f * bs * bs;
+  for (int idx = tid; idx < bs * bs; idx += blockDim.x) {
+    const int i = idx / bs, j = idx - i * bs;
+    const int k0 = i > j ? i : j;
+    double acc = 0.0;
+    for (int k = k0; k < bs; ++k) acc += B[k * bs + i] * B[k * bs + j];
+    out[idx] = acc;
+  }
+}
+
+__global__ void __launch_bounds__(PRE_THREADS) k_precond_apply(int bs, const double* __restrict__ inv,
+                                                               const double* __restrict__ v, double* __restrict__ y) {
+  extern __shared__ double sm[];
+  const int f = blockIdx.x;
+  for (int i = threadIdx.x; i < bs; i += blockDim.x) sm[i] = v[(size_t)f * bs + i];
+  __syncthreads();
+  warp_gemv<false>(inv + (size_t)f * bs * bs, bs, bs, sm, sm + bs, 1.0);
+  __syncthreads();
+  for (int i = threadIdx.x; i < bs; i += blockDim.x) y[(size_t)f * bs + i] = sm[bs + i];
+}
+
+template <int D>
+int precond_build(const mhdg_disc& g, const mhdg_blocks& b, double* inv, int* status, cudaStream_t st) {
+  const int bs = g.Lf * (D + 2);
+  const size_t bytes = sizeof(double) * 2 * bs * bs;
+  if (bytes > 227 * 1024) return MHDG_ERR_CONFIG;
+  if (bytes > 48 * 1024)
+    cudaFuncSetAttribute(k_precond_build<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  k_precond_build<D><<<g.n_faces, PRE_THREADS, bytes, st>>>(g, b, inv, status);
+  return launch_ok();
+}
+
+int precond_apply(const mhdg_disc& g, const double* inv, const double* v, double* y, cudaStream_t st) {
+  const int bs = g.Lf * g.ns;
+  k_precond_apply<<<g.n_faces, PRE_THREADS, sizeof(double) * 2 * bs, st>>>(bs, inv, v, y);
+  return launch_ok();
+}
+
+template int precond_build<2>(const mhdg_disc&, const mhdg_blocks&, double*, int*, cudaStream_t);
+template int precond_build<3>(const mhdg_disc&, const mhdg_blocks&, double*, int*, cudaStream_t);
+
+}  // namespace mhdg
