@@ -1,0 +1,414 @@
+"""Benchmark: BASELINE.json configs[1] (C2), the isolated 2D operator benchmark.
+
+Mesh 64x64 squares -> 8192 triangular macro-elements, m=4 (16 sub-triangles),
+p=3, FP64; uniform flow rho=1, v=(1,0.3), P=1/(1.4*0.2^2) plus seeded N(0,1e-2)
+noise on every nodal conserved value; one Jacobian assembly, second-layer
+condensation + batched LU of all macros, then trace-operator applies on seeded
+N(0,1) trace vectors (default_rng(1)).  A "step" is one matrix-free apply of
+the condensed trace operator over all 8192 macros.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+Prints one JSON line (rank 0).  value = trace-operator DOF-applies/s (whole
+job); the condensation metric (macro-elements condensed/s) and the assembly
+rate ride along in the same line.  --impl reference times the CPU restatement
+of the reference algorithm (oracle/, the reference is 3D-only and cannot run
+C2) on the host cores, on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_CELLS, M_SUB, P_DEG = 64, 4, 3
+SIGMA = 1e-2
+METRIC = "trace-operator DOF-applies/s"
+
+
+# ---------------------------------------------------------------------------
+# workload
+# ---------------------------------------------------------------------------
+
+
+def c2_discretization(n_cells=N_CELLS):
+    from paper_2402_11361_b200.cases import UniformFlow2D
+    from paper_2402_11361_b200.discretization import Discretization
+    from paper_2402_11361_b200.mesh import build_square_mesh
+
+    case = UniformFlow2D()
+    disc = Discretization(build_square_mesh(case.domain, n_cells, M_SUB, periodic=(True, True)), P_DEG, case.params)
+    return case, disc
+
+
+def c2_state(case, disc, seed=0):
+    """Nodal state + N(0, sigma) noise (seed 0); owner-side trace copy."""
+    X = disc.node_coords().reshape(-1, 2)
+    u = case.state(X).reshape(disc.n_mac, disc.L, disc.ns)
+    u = u + SIGMA * np.random.default_rng(seed).standard_normal(u.shape)
+    return u, disc.owner_trace_from_nodes(u)
+
+
+def algorithmic_bytes_per_macro(disc):
+    """B_ref: the reference's stored-operator bytes per
+    macro apply."""
+    d, ns, nf, L, Lf, m, p = disc.dim, disc.ns, disc.nf, disc.L, disc.Lf, disc.mesh.m, disc.p
+    nq = disc.rm.n_quad
+    nqf = disc.rm.n_quad_face
+    ltr = nf * Lf * ns
+    return 8 * ((L * ns) ** 2 + 3 * nf * (Lf * ns) ** 2 + m**d * nq * d * d * ns * ns
+                + nf * m ** (d - 1) * nqf * d * ns * ns + 2 * ltr + (1 + d * d + nf * d + 2 * nf)) + 4 * ltr
+
+
+def condense_flops_per_macro(disc):
+    """F_cond = 2 d L^3 ns^2 + (2/3) (L ns)^3."""
+    d, L, ns = disc.dim, disc.L, disc.ns
+    return 2 * d * L**3 * ns**2 + (2.0 / 3.0) * (L * ns) ** 3
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh)
+    except OSError:
+        return {}
+
+
+def committed_traffic():
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            return json.load(fh)
+    except OSError:
+        return {}
+
+
+# ---------------------------------------------------------------------------
+# clocks sampling (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+
+
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.5)  # let the sampler start before the timed region
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in getattr(self, "lines", []):
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
+        loaded = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": float(np.median(loaded)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (oracle restatement of the reference algorithm)
+# ---------------------------------------------------------------------------
+
+
+def cpu_apply_rate(n_cells, applies, threads):
+    """DOF-applies/s of the CPU restatement on an n_cells^2 periodic sample of
+    the C2 workload (same m, p, state distribution and context)."""
+    from threadpoolctl import threadpool_limits
+
+    import oracle.hdg_oracle as O
+
+    case, disc = c2_discretization(n_cells)
+    u, uhat = c2_state(case, disc)
+    with threadpool_limits(threads):
+        f = O.Fields(u, O.gradient_refresh(disc, u, uhat), uhat)
+        blocks, _ = O.jacobian(disc, f, O.Ctx.steady(1.0))
+        cond = O.condense(blocks)
+        xs = np.random.default_rng(1).standard_normal((applies, disc.n_trace))
+        cond.apply_trace(xs[0])
+        t0 = time.perf_counter()
+        for x in xs:
+            cond.apply_trace(x)
+        dt = time.perf_counter() - t0
+    return disc.n_trace * applies / dt, disc, dt
+
+
+def run_reference(args, rank):
+    """CPU restatement of the reference algorithm on the host cores: setup once
+    on a bounded C2 sample, each step one apply over the sample."""
+    if rank != 0:
+        return
+    from threadpoolctl import threadpool_limits
+
+    import oracle.hdg_oracle as O
+
+    threads = len(os.sched_getaffinity(0))
+    n_cells = 8
+    case, disc = c2_discretization(n_cells)
+    u, uhat = c2_state(case, disc)
+    with threadpool_limits(threads):
+        f = O.Fields(u, O.gradient_refresh(disc, u, uhat), uhat)
+        blocks, _ = O.jacobian(disc, f, O.Ctx.steady(1.0))
+        cond = O.condense(blocks)
+        xs = np.random.default_rng(1).standard_normal((args.warmup + args.steps, disc.n_trace))
+        for i in range(args.warmup):
+            cond.apply_trace(xs[i])
+        t0 = time.perf_counter()
+        for i in range(args.steps):
+            cond.apply_trace(xs[args.warmup + i])
+        dt = time.perf_counter() - t0
+    value = disc.n_trace * args.steps / dt
+    sample = (f"C2 restatement (oracle/) on a {n_cells}x{n_cells} periodic sample ({disc.n_mac} macros, m=4, "
+              f"p=3, {disc.n_trace} trace dofs), one apply per step; the per-DOF rate is intensive")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "DOF-applies/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "C2 2D operator benchmark (64x64x2 macros, m=4, p=3)", "global_batch": None,
+                   "seq_len": None, "parallelism": "cpu"},
+        "cpu_baseline": {"value": value, "unit": "DOF-applies/s", "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "DOF-applies/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU leg
+# ---------------------------------------------------------------------------
+
+
+def fp64_gemm_peak(torch, n=8192, reps=5):
+    a = torch.randn(n, n, dtype=torch.float64, device="cuda")
+    b = torch.randn(n, n, dtype=torch.float64, device="cuda")
+    torch.matmul(a, b)
+    torch.cuda.synchronize()
+    best = math.inf
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch.matmul(a, b)
+        e1.record()
+        e1.synchronize()
+        best = min(best, e0.elapsed_time(e1) / 1e3)
+    del a, b
+    torch.cuda.empty_cache()
+    return 2.0 * n**3 / best / 1e12
+
+
+def run_gpu(args, rank, world):
+    import torch
+
+    from paper_2402_11361_b200 import _lib
+    from paper_2402_11361_b200 import assembly as A
+    from paper_2402_11361_b200.condense import CondensedSchur
+    from paper_2402_11361_b200.device import current_stream
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist  # noqa: F811
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    L = _lib.lib()
+
+    case, disc = c2_discretization()
+    u, uhat = c2_state(case, disc)
+    dd = disc.device
+    fields = A.FieldState(torch.as_tensor(u, device="cuda"), None, torch.as_tensor(uhat, device="cuda"))
+    fields.q = A.gradient_refresh(disc, fields.u, fields.uhat)
+    ctx = A.StageContext.steady(1.0)
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+    # ---- assembly (one Jacobian assembly, timed) ----
+    torch.cuda.synchronize()
+    blocks, _ = A.jacobian(disc, fields, ctx)  # warm (also the real one)
+    a0, a1 = ev(), ev()
+    a0.record()
+    blocks, _ = A.jacobian(disc, fields, ctx)
+    a1.record()
+    a1.synchronize()
+    t_asm = a0.elapsed_time(a1) / 1e3
+
+    # ---- condensation: Schur correction + batched LU, timed ----
+    cond = CondensedSchur.allocate(blocks)
+    status = dd.status_buffer()
+    cond.refactor_async(status)
+    torch.cuda.synchronize()
+    c_times = []
+    for _ in range(3):
+        c0, c1 = ev(), ev()
+        c0.record()
+        cond.refactor_async(status)
+        c1.record()
+        c1.synchronize()
+        c_times.append(c0.elapsed_time(c1) / 1e3)
+    A.raise_status(status, "condense")
+    t_cond = float(np.median(c_times))
+
+    # ---- applies ----
+    K, W = args.steps, args.warmup
+    xs = torch.as_tensor(np.random.default_rng(1).standard_normal((K + W, disc.n_trace)), device="cuda")
+    y = torch.empty(disc.n_trace, dtype=torch.float64, device="cuda")
+    y_loc = torch.empty(dd.n_local_trace, dtype=torch.float64, device="cuda")
+    st = current_stream()
+
+    def apply_split(x, ev0, ev1):
+        ev0.record()
+        _lib.check(L.mhdg_apply_trace_local(dd.c, blocks.c, cond._fac, _lib.ptr(x), _lib.ptr(y_loc), st), "apply")
+        ev1.record()
+        _lib.check(L.mhdg_face_reduce(dd.c, _lib.ptr(y_loc), _lib.ptr(y), st), "reduce")
+
+    clk = Clocks(local).__enter__()
+    for i in range(W):
+        apply_split(xs[i], ev(), ev())
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    kev = [(ev(), ev()) for _ in range(K)]
+    launches0 = L.mhdg_launch_count()
+    t0, t1 = ev(), ev()
+    torch.cuda.synchronize()
+    t0.record()
+    for i in range(K):
+        apply_split(xs[W + i], *kev[i])
+    t1.record()
+    torch.cuda.synchronize()
+    launches = L.mhdg_launch_count() - launches0
+    clk.__exit__(None, None, None)
+    t_apply = t0.elapsed_time(t1) / 1e3
+    if dist:
+        tt = torch.tensor([t_apply], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_apply = float(tt)
+    k_apply = float(np.mean([a.elapsed_time(b) / 1e3 for a, b in kev]))
+
+    # ---- e2e through the public API with pinned host buffers ----
+    xh = torch.empty(disc.n_trace, dtype=torch.float64, pin_memory=True)
+    yh = torch.empty(disc.n_trace, dtype=torch.float64, pin_memory=True)
+    xh.copy_(xs[0].cpu())
+    xd = torch.empty_like(y)
+    for _ in range(2):
+        xd.copy_(xh, non_blocking=True)
+        yh.copy_(cond.apply_trace(xd, out=y), non_blocking=True)
+    torch.cuda.synchronize()
+    e0, e1 = ev(), ev()
+    ne = max(3, min(K, 20))
+    e0.record()
+    for _ in range(ne):
+        xd.copy_(xh, non_blocking=True)
+        yh.copy_(cond.apply_trace(xd, out=y), non_blocking=True)
+    e1.record()
+    e1.synchronize()
+    t_e2e = e0.elapsed_time(e1) / 1e3 / ne
+
+    peaks = measured_peaks()
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    fp64 = fp64_gemm_peak(torch) if rank == 0 else None
+    b_mac = algorithmic_bytes_per_macro(disc)
+    achieved = b_mac * disc.n_mac / k_apply / 1e9
+    traffic = committed_traffic().get("apply_local_dram_bytes_per_launch")
+    f_mac = condense_flops_per_macro(disc)
+    cond_tf = f_mac * disc.n_mac / t_cond / 1e12
+
+    value = world * disc.n_trace * K / t_apply
+    line = {
+        "metric": METRIC, "value": value, "unit": "DOF-applies/s", "n_gpus": world, "steps": K, "warmup": W,
+        "ms_per_step": 1e3 * t_apply / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "C2 2D operator benchmark: 64x64 squares -> 8192 triangular macros, m=4, p=3, "
+                               "periodic, uniform flow + N(0,1e-2), StageContext.steady(pseudo_dt=1)",
+                   "n_macros": disc.n_mac, "n_trace_dofs": disc.n_trace, "global_batch": None, "seq_len": None,
+                   "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "l2": "inputs larger than L2 (each apply streams ~%.1f GB of operator data)"
+                         % (b_mac * disc.n_mac / 1e9)},
+        "roofline": {"kernel": "k_apply_local", "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": achieved / hbm, "traffic": traffic,
+                     "algorithmic_bytes_per_launch": b_mac * disc.n_mac, "avg_launch_s": k_apply,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"},
+        "condense": {"metric": "macro-elements condensed/s", "value": disc.n_mac / t_cond, "unit": "macros/s",
+                     "seconds": t_cond, "flops_per_macro": f_mac,
+                     "roofline": {"bound": "fp64", "achieved": cond_tf, "peak": fp64, "unit": "TFLOP/s",
+                                  "frac": (cond_tf / fp64) if fp64 else None,
+                                  "peak_source": "cuBLAS DGEMM 8192^3 measured in this run"}},
+        "assembly": {"metric": "macro-elements assembled/s (Jacobian + residual)", "value": disc.n_mac / t_asm,
+                     "seconds": t_asm},
+        "e2e": {"value": world * disc.n_trace / t_e2e, "unit": "DOF-applies/s",
+                "h2d_bytes_per_step": 8 * disc.n_trace, "d2h_bytes_per_step": 8 * disc.n_trace},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        v, sdisc, dt = cpu_apply_rate(8, 10, 1)
+        line["cpu_baseline"] = {"value": v, "unit": "DOF-applies/s", "cores": 1, "kind": "port",
+                                "sample": f"oracle restatement, 8x8 periodic C2 sample ({sdisc.n_mac} macros, "
+                                          f"{sdisc.n_trace} dofs), 10 applies in {dt:.1f} s, 1 thread"}
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    run_gpu(args, rank, world)
+
+
+if __name__ == "__main__":
+    main()
