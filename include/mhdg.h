@@ -124,13 +124,19 @@ typedef struct {
   double *face_visc_state;   /* n_mac*nf*(n_tri nqf)*ns */
 } mhdg_frozen;
 
-/* condensed operator: S = P^T L U per macro, row-major n x n, n = L*ns;
-   L unit lower (strictly below the diagonal), U on and above it; perm[i] is
-   the original row of factor row i. */
+/* condensed operator S = A_uu - A_uq A_qq^-1 A_qu (n = L*ns), P S = L U with
+   partial pivoting.  `lu` holds each macro's factor in the packed solve order
+   of csrc/packed_lu.cuh (mhdg_packed_lu_size(n) doubles per macro: L/U panels
+   row-major, diagonal tiles inverted); perm[i] is the original row of factor
+   row i; `scratch` (n_mac*n*n) holds S / the in-place LU before packing. */
 typedef struct {
-  double *lu;                /* n_mac*n*n */
+  double *lu;                /* n_mac*mhdg_packed_lu_size(n) */
   int *perm;                 /* n_mac*n */
+  double *scratch;           /* n_mac*n*n */
 } mhdg_factors;
+
+/* doubles per macro of the packed LU factor */
+long long mhdg_packed_lu_size(int n);
 
 /* Residuals (and, with want_jac, blocks + frozen coefficients).
    frozen_in != NULL evaluates the residual with frozen coefficients (the
@@ -146,11 +152,11 @@ int mhdg_assemble(const mhdg_disc *disc, const mhdg_flow *flow, const mhdg_stage
 int mhdg_condense(const mhdg_disc *disc, const mhdg_blocks *blocks, const mhdg_factors *fac,
                   int *status, void *stream);
 
-/* Schur complement only (no factorization), into fac->lu; for parity tests. */
+/* Schur complement only (no factorization), into fac->scratch (n x n per macro). */
 int mhdg_schur_matrix(const mhdg_disc *disc, const mhdg_blocks *blocks, const mhdg_factors *fac,
                       void *stream);
 
-/* LU-factor n_mac dense n x n matrices in place (fac->lu) with partial pivoting. */
+/* LU-factor the n x n matrices in fac->scratch in place (partial pivoting) and pack into fac->lu. */
 int mhdg_lu_factor(const mhdg_disc *disc, const mhdg_factors *fac, int *status, void *stream);
 
 /* y_mac = S^-1 b_mac for all macros (b, y: n_mac*n; may alias). */
@@ -190,6 +196,10 @@ int mhdg_precond_build(const mhdg_disc *disc, const mhdg_blocks *blocks, double 
 /* y = blockdiag(inv) v (krylov.py:234-236). */
 int mhdg_precond_apply(const mhdg_disc *disc, const double *inv, const double *v, double *y,
                        void *stream);
+
+/* 1 (default): use the compile-time specialised TMA-streamed apply kernel when
+   one matches (dim, m, p); 0: always the generic kernel (cross-checks). */
+void mhdg_set_stream_enabled(int on);
 
 /* number of kernel launches issued by this library since load (diagnostics) */
 long long mhdg_launch_count(void);

@@ -61,7 +61,7 @@ class Frozen(C.Structure):
 
 
 class Factors(C.Structure):
-    _fields_ = [("lu", _dp), ("perm", _dp)]
+    _fields_ = [("lu", _dp), ("perm", _dp), ("scratch", _dp)]
 
 
 _lib = None
@@ -95,6 +95,10 @@ def lib():
             fn = getattr(L, name)
             fn.argtypes = args
             fn.restype = C.c_int
+        L.mhdg_set_stream_enabled.argtypes = [C.c_int]
+        L.mhdg_set_stream_enabled.restype = None
+        L.mhdg_packed_lu_size.argtypes = [C.c_int]
+        L.mhdg_packed_lu_size.restype = C.c_longlong
         L.mhdg_launch_count.argtypes = []
         L.mhdg_launch_count.restype = C.c_longlong
         _lib = L
@@ -105,6 +109,7 @@ EXPORTED = (
     "mhdg_assemble", "mhdg_condense", "mhdg_schur_matrix", "mhdg_lu_factor", "mhdg_lu_solve",
     "mhdg_apply_trace", "mhdg_apply_trace_local", "mhdg_face_reduce", "mhdg_condensed_rhs", "mhdg_recover",
     "mhdg_gradient_refresh", "mhdg_precond_build", "mhdg_precond_apply", "mhdg_launch_count",
+    "mhdg_packed_lu_size", "mhdg_set_stream_enabled",
 )
 
 

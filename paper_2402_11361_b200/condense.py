@@ -23,12 +23,13 @@ class FactorizationError(RuntimeError):
 
 
 class CondensedSchur:
-    def __init__(self, blocks: LocalBlocks, lu: torch.Tensor, perm: torch.Tensor):
+    def __init__(self, blocks: LocalBlocks, lu: torch.Tensor, perm: torch.Tensor, scratch: torch.Tensor):
         self.blocks = blocks
-        self.lu = lu
+        self.lu = lu  # packed factors (csrc/packed_lu.cuh)
         self.perm = perm
+        self.scratch = scratch  # S, then its in-place LU, before packing
         fac = _lib.Factors()
-        fac.lu, fac.perm = _lib.ptr(lu), _lib.ptr(perm)
+        fac.lu, fac.perm, fac.scratch = _lib.ptr(lu), _lib.ptr(perm), _lib.ptr(scratch)
         self._fac = fac
         dd = blocks.disc.device
         self._y_loc = torch.empty(dd.n_local_trace, dtype=torch.float64, device=dd.device)
@@ -38,9 +39,11 @@ class CondensedSchur:
         disc = blocks.disc
         n = disc.L * disc.ns
         dev = disc.device.device
-        lu = torch.empty((disc.n_mac, n, n), dtype=torch.float64, device=dev)
+        packed = int(_lib.lib().mhdg_packed_lu_size(n))
+        lu = torch.empty((disc.n_mac, packed), dtype=torch.float64, device=dev)
         perm = torch.empty((disc.n_mac, n), dtype=torch.int32, device=dev)
-        return cls(blocks, lu, perm)
+        scratch = torch.empty((disc.n_mac, n, n), dtype=torch.float64, device=dev)
+        return cls(blocks, lu, perm, scratch)
 
     @classmethod
     def build(cls, blocks: LocalBlocks) -> "CondensedSchur":
@@ -71,11 +74,12 @@ class CondensedSchur:
         return self.lu.numel()
 
     # ------------------------------------------------------------------
-    def schur_matrix_into_factors(self) -> None:
-        """Write S (unfactorized) into self.lu; for parity tests."""
+    def schur_matrix_into_factors(self) -> torch.Tensor:
+        """Write S (unfactorized) into self.scratch and return it; for parity tests."""
         dd = self.disc.device
         rc = _lib.lib().mhdg_schur_matrix(dd.c, self.blocks.c, self._fac, current_stream())
         _lib.check(rc, "mhdg_schur_matrix")
+        return self.scratch
 
     def schur_solve(self, y: torch.Tensor) -> torch.Tensor:
         dd = self.disc.device

@@ -1,5 +1,6 @@
 // extern "C" boundary (include/mhdg.h): dispatch on the dimension and launch.
 #include "common.cuh"
+#include "packed_lu.cuh"
 
 namespace mhdg {
 long long g_launches = 0;
@@ -16,7 +17,8 @@ template <int D> int precond_build(const mhdg_disc&, const mhdg_blocks&, double*
 int precond_apply(const mhdg_disc&, const double*, const double*, double*, cudaStream_t);
 int face_reduce(const mhdg_disc&, const double*, const double*, double, double*, cudaStream_t);
 int lu_solve(const mhdg_disc&, const mhdg_factors&, const double*, double*, cudaStream_t);
-int lu_factor(int n, int n_mac, double* LU, int* perm, int* status, cudaStream_t st);
+int lu_factor(int n, int n_mac, double* scratch, double* packed, int* perm, int* status, cudaStream_t st);
+int apply_stream(const mhdg_disc&, const mhdg_blocks&, const mhdg_factors&, const double*, double*, cudaStream_t);
 size_t lu_smem_bytes(int n);
 }  // namespace mhdg
 
@@ -31,8 +33,18 @@ extern "C" {
 
 long long mhdg_launch_count(void) { return g_launches; }
 
+long long mhdg_packed_lu_size(int n) { return plu_size(n); }
+
+static int g_stream_enabled = 1;
+void mhdg_set_stream_enabled(int on) { g_stream_enabled = on; }
+
 int mhdg_apply_trace_local(const mhdg_disc* g, const mhdg_blocks* b, const mhdg_factors* f, const double* x,
                            double* y_loc, void* st) {
+  // compile-time specialised, TMA-streamed kernel when one matches (dim, m, p)
+  if (g_stream_enabled) {
+    const int rc = apply_stream(*g, *b, *f, x, y_loc, S(st));
+    if (rc >= 0) return rc;
+  }
   return DISPATCH(g, apply_local<2>(*g, *b, *f, x, y_loc, S(st)), apply_local<3>(*g, *b, *f, x, y_loc, S(st)));
 }
 
@@ -65,13 +77,13 @@ int mhdg_gradient_refresh(const mhdg_disc* g, const double* u, const double* uha
 }
 
 int mhdg_schur_matrix(const mhdg_disc* g, const mhdg_blocks* b, const mhdg_factors* f, void* st) {
-  return DISPATCH(g, schur_matrix<2>(*g, *b, f->lu, S(st)), schur_matrix<3>(*g, *b, f->lu, S(st)));
+  return DISPATCH(g, schur_matrix<2>(*g, *b, f->scratch, S(st)), schur_matrix<3>(*g, *b, f->scratch, S(st)));
 }
 
 int mhdg_lu_factor(const mhdg_disc* g, const mhdg_factors* f, int* status, void* st) {
   const int n = g->L * g->ns;
   if (lu_smem_bytes(n) > 227 * 1024) return MHDG_ERR_CONFIG;
-  return lu_factor(n, g->n_mac, f->lu, f->perm, status, S(st));
+  return lu_factor(n, g->n_mac, f->scratch, f->lu, f->perm, status, S(st));
 }
 
 int mhdg_condense(const mhdg_disc* g, const mhdg_blocks* b, const mhdg_factors* f, int* status, void* st) {

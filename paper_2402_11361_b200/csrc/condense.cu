@@ -13,6 +13,7 @@
 //           memory, 64x64 register-tiled trailing updates.
 #include "common.cuh"
 #include "local_ops.cuh"
+#include "packed_lu.cuh"
 
 namespace mhdg {
 
@@ -295,6 +296,73 @@ __global__ void __launch_bounds__(LU_THREADS) k_lu(int n, double* __restrict__ L
 }
 
 // --------------------------------------------------------------------------
+// pack: factored n x n (scratch) -> packed solve layout with inverted diagonal
+// tiles (packed_lu.cuh)
+// --------------------------------------------------------------------------
+
+__global__ void __launch_bounds__(256) k_pack(int n, const double* __restrict__ F, double* __restrict__ out) {
+  __shared__ double T[PLU_NB][PLU_NB + 1], X[PLU_NB][PLU_NB + 1];
+  const int mac = blockIdx.x, tid = threadIdx.x;
+  const double* A = F + (size_t)mac * n * n;
+  double* O = out + (size_t)mac * plu_size(n);
+  const int nblk = plu_nblk(n);
+  for (int b = 0; b < nblk; ++b) {
+    const PluOffsets o = plu_offsets(n, b);
+    const int nb = o.nb, r0 = o.r0;
+    for (int idx = tid; idx < nb * o.ncol_fwd; idx += blockDim.x) {
+      const int r = idx / o.ncol_fwd, c = idx % o.ncol_fwd;
+      O[o.fwd_panel + plu_panel_idx(nb, o.ncol_fwd, r, c)] = A[(size_t)(r0 + r) * n + c];
+    }
+    for (int idx = tid; idx < nb * o.ncol_bwd; idx += blockDim.x) {
+      const int r = idx / o.ncol_bwd, c = idx % o.ncol_bwd;
+      O[o.bwd_panel + plu_panel_idx(nb, o.ncol_bwd, r, c)] = A[(size_t)(r0 + r) * n + r0 + nb + c];
+    }
+    for (int idx = tid; idx < nb * nb; idx += blockDim.x) {
+      const int r = idx / nb, c = idx % nb;
+      T[r][c] = A[(size_t)(r0 + r) * n + r0 + c];
+    }
+    __syncthreads();
+    if (tid < nb) {  // inverse of the unit lower tile, column tid
+      const int c = tid;
+      X[c][c] = 1.0;
+      for (int i = c + 1; i < nb; ++i) {
+        double acc = 0.0;
+        for (int k = c; k < i; ++k) acc += T[i][k] * X[k][c];
+        X[i][c] = -acc;
+      }
+    }
+    __syncthreads();
+    for (int idx = tid; idx < nb * nb; idx += blockDim.x) {
+      const int r = idx / nb, c = idx % nb;
+      if (c < r) O[o.fwd_diag + plu_lo(r, c)] = X[r][c];
+    }
+    __syncthreads();
+    if (tid < nb) {  // inverse of the upper tile, column tid
+      const int c = tid;
+      X[c][c] = 1.0 / T[c][c];
+      for (int i = c - 1; i >= 0; --i) {
+        double acc = 0.0;
+        for (int k = i + 1; k <= c; ++k) acc += T[i][k] * X[k][c];
+        X[i][c] = -acc / T[i][i];
+      }
+    }
+    __syncthreads();
+    for (int idx = tid; idx < nb * nb; idx += blockDim.x) {
+      const int r = idx / nb, c = idx % nb;
+      if (c >= r) O[o.bwd_diag + plu_up(nb, r, c)] = X[r][c];
+    }
+    if (tid == 0) {  // zero the even-size padding of the last (narrow) tiles and triangles
+      if ((nb * (nb - 1) / 2) & 1) O[o.fwd_diag + nb * (nb - 1) / 2] = 0.0;
+      if ((nb * (nb + 1) / 2) & 1) O[o.bwd_diag + nb * (nb + 1) / 2] = 0.0;
+      const int wf = o.ncol_fwd % PLU_TW, wb = o.ncol_bwd % PLU_TW;
+      if ((nb * wf) & 1) O[o.fwd_diag - 1] = 0.0;
+      if ((nb * wb) & 1) O[o.bwd_diag - 1] = 0.0;
+    }
+    __syncthreads();
+  }
+}
+
+// --------------------------------------------------------------------------
 // host launchers
 // --------------------------------------------------------------------------
 
@@ -313,10 +381,13 @@ size_t lu_smem_bytes(int n) {
   return sizeof(double) * ((size_t)n * (LU_NB + 1) + 2 * LU_NB * 64 + LU_NB * (LU_NB + 1) + 32 + 8) + sizeof(int) * (32 + LU_NB + 8) + 64;
 }
 
-int lu_factor(int n, int n_mac, double* LU, int* perm, int* status, cudaStream_t st) {
+int lu_factor(int n, int n_mac, double* scratch, double* packed, int* perm, int* status, cudaStream_t st) {
   const size_t bytes = lu_smem_bytes(n);
   if (bytes > 48 * 1024) cudaFuncSetAttribute(k_lu, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  k_lu<<<n_mac, LU_THREADS, bytes, st>>>(n, LU, perm, status);
+  k_lu<<<n_mac, LU_THREADS, bytes, st>>>(n, scratch, perm, status);
+  int rc = launch_ok();
+  if (rc) return rc;
+  k_pack<<<n_mac, 256, 0, st>>>(n, scratch, packed);
   return launch_ok();
 }
 

@@ -45,9 +45,12 @@ class DeviceDisc:
         fvn = rm.face_vol_nodes
         t["mass"] = f64(rm.mass)
         t["mass_inv"] = f64(rm.mass_inv)
-        t["minv_d"] = f64(rm.mass_inv_weak_deriv)
+        # tables streamed by bulk copies are padded so an even-rounded piece
+        # never reads past the allocation
+        pad2 = lambda a: np.concatenate([np.ascontiguousarray(a, dtype=np.float64).ravel(), np.zeros(2)])  # noqa: E731
+        t["minv_d"] = f64(pad2(rm.mass_inv_weak_deriv))
         t["weak_deriv"] = f64(rm.weak_deriv)
-        t["gf"] = f64(np.stack([rm.mass_inv[:, fvn[f]] @ rm.face_mass for f in range(disc.nf)]))
+        t["gf"] = f64(pad2(np.stack([rm.mass_inv[:, fvn[f]] @ rm.face_mass for f in range(disc.nf)])))
         t["face_mass"] = f64(rm.face_mass)
         t["face_vol_nodes"] = i32(fvn)
         t["sub_conn"] = i32(rm.sub_conn)
