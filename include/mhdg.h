@@ -94,6 +94,10 @@ typedef struct {
   /* face skeleton for the block preconditioner */
   const int *face_macros;     /* n_faces*2 (-1 = none) */
   const int *face_locals;     /* n_faces*2 */
+  /* volume nodes lying on the macro boundary (ascending) */
+  int n_face_nodes;
+  const int *node_to_face;    /* L: index into the face-node list, -1 for interior nodes */
+  const double *minv_d_face;  /* d*n_face_nodes*L: rows of M^-1 D_r at the face nodes */
 } mhdg_disc;
 
 typedef struct {

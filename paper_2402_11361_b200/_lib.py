@@ -39,6 +39,7 @@ class Disc(C.Structure):
         ("gather", _dp), ("scatter_src", _dp),
         ("bc_kind", _dp), ("wall_e", _dp), ("wall_u", _dp), ("u_dir", _dp), ("source", _dp),
         ("face_macros", _dp), ("face_locals", _dp),
+        ("n_face_nodes", C.c_int), ("node_to_face", _dp), ("minv_d_face", _dp),
     ]
 
 

@@ -15,6 +15,7 @@
 // Results match k_apply_local to rounding; all reductions are in a fixed order.
 #include "local_ops.cuh"
 #include "packed_lu.cuh"
+#include "tiled_inv.cuh"
 #include "tma.cuh"
 
 namespace mhdg {
@@ -31,7 +32,7 @@ __host__ __device__ constexpr int cpow(int b, int e) {
 }
 __host__ __device__ constexpr int ceven(int x) { return x + (x & 1); }
 
-constexpr int ST_DBL = 2048;  // doubles per ring stage (16 KB)
+constexpr int ST_DBL = 2112;  // doubles per ring stage (16.5 KB: one 64x32 LU tile or a 64-row inverted triangle)
 constexpr int NCONS = 256;    // consumer threads (8 warps)
 
 template <int D_, int M_, int P_>
@@ -48,10 +49,11 @@ struct Cfg {
   static constexpr int RPP = (BS & 1) ? ((ST_DBL / BS) & ~1) : ST_DBL / BS;
   static constexpr int PPV = (NW & 1) ? ((ST_DBL / NW) & ~1) : ST_DBL / NW;
   static constexpr int PPF = (NWF & 1) ? ((ST_DBL / NWF) & ~1) : ST_DBL / NWF;
-  static constexpr int NBLK = (n + PLU_NB - 1) / PLU_NB;
+  static constexpr int NBLK = (n + TI_RB - 1) / TI_RB;
+  static constexpr int NFN = L - (N - 1 >= D ? cbinom(N - 1, D) : 0);  // boundary lattice nodes
 };
 
-enum : int { K_FST = 0, K_FTT, K_WV, K_WFZ, K_LF, K_LFD, K_UB, K_UBD, K_WF2, K_FTS, K_GF, K_MD };
+enum : int { K_FST = 0, K_FTT, K_WV, K_WFZ, K_SI, K_LFD, K_UB, K_UBD, K_WF2, K_FTS, K_GF, K_MD };
 
 struct Piece {
   unsigned char kind, blk;
@@ -91,62 +93,31 @@ struct Sched {
         case 2: if (rows(p, K_FTT, C::NF * C::BS, C::BS)) return true; break;
         case 3: if (rows(p, K_WV, C::NPV, C::NW)) return true; break;
         case 4: if (rows(p, K_WFZ, C::NPF, C::NWF)) return true; break;
-        case 5:
+        case 5:  // S^-1: row blocks of TI_RB rows, each as TI_CW-column tiles
           if (b < C::NBLK) {
-            const PluOffsets o = plu_offsets(C::n, b);
-            if (r < o.ncol_fwd) {  // column tile [r, r + w) holding all nb rows
-              const int w = (o.ncol_fwd - r) < PLU_TW ? o.ncol_fwd - r : PLU_TW;
-              p.kind = K_LF;
-              p.u0 = (unsigned short)r;
-              p.nu = (unsigned short)w;
-              p.off = (unsigned)(o.fwd_panel + (long long)(r / PLU_TW) * o.nb * PLU_TW);
-              p.cnt = (unsigned short)even_ll((long long)o.nb * w);
-              p.blk = (unsigned char)b;
-              r += w;
-              return true;
-            }
-            p.kind = K_LFD;
-            p.u0 = 0;
-            p.nu = (unsigned short)o.nb;
-            p.off = (unsigned)o.fwd_diag;
-            p.cnt = (unsigned short)even_ll((long long)o.nb * (o.nb - 1) / 2);
-            p.blk = (unsigned char)(b++);
-            r = 0;
+            const int nb = ti_rows(C::n, b);
+            const int w = (C::n - r) < TI_CW ? C::n - r : TI_CW;
+            p.kind = K_SI;
+            p.u0 = (unsigned short)r;
+            p.nu = (unsigned short)w;
+            p.off = (unsigned)(ti_block_off(C::n, b) + (long long)(r / TI_CW) * nb * TI_CW);
+            p.cnt = (unsigned short)ti_even((long long)nb * w);
+            p.blk = (unsigned char)b;
+            r += w;
+            if (r >= C::n) { r = 0; ++b; }
             return true;
           }
           break;
         case 6:
-          if (b >= 0) {
-            const PluOffsets o = plu_offsets(C::n, b);
-            if (r < o.ncol_bwd) {
-              const int w = (o.ncol_bwd - r) < PLU_TW ? o.ncol_bwd - r : PLU_TW;
-              p.kind = K_UB;
-              p.u0 = (unsigned short)r;
-              p.nu = (unsigned short)w;
-              p.off = (unsigned)(o.bwd_panel + (long long)(r / PLU_TW) * o.nb * PLU_TW);
-              p.cnt = (unsigned short)even_ll((long long)o.nb * w);
-              p.blk = (unsigned char)b;
-              r += w;
-              return true;
-            }
-            p.kind = K_UBD;
-            p.u0 = 0;
-            p.nu = (unsigned short)o.nb;
-            p.off = (unsigned)o.bwd_diag;
-            p.cnt = (unsigned short)even_ll((long long)o.nb * (o.nb + 1) / 2);
-            p.blk = (unsigned char)(b--);
-            r = 0;
-            return true;
-          }
           break;
-        case 7: if (rows(p, K_MD, C::D * C::L, C::L)) return true; break;
+        case 7: if (rows(p, K_MD, C::D * C::NFN, C::L)) return true; break;
         case 8: if (rows(p, K_WF2, C::NPF, C::NWF)) return true; break;
         case 9: if (rows(p, K_FTS, C::NF * C::BS, C::BS)) return true; break;
       }
       ++seg;
       i = 0;
       r = 0;
-      b = (seg == 6) ? C::NBLK - 1 : 0;
+      b = 0;
     }
     return false;
   }
@@ -170,7 +141,7 @@ struct SSm {  // consumer work layout (doubles), after the ring
   static constexpr int vv = wf2 + C::NPF * C::NS;  // 8 warps x 32 doubles
   static constexpr int cv = vv + 8 * 32;
   static constexpr int tg = cv + C::NSUB * C::NLOC * C::NS;  // Gf x | W_vol results | M^-1 D y
-  static constexpr int TGN0 = (C::NF > C::D ? C::NF : C::D) * C::n;
+  static constexpr int TGN0 = C::NF * C::n;
   static constexpr int TGN = TGN0 > C::NPV * C::D * C::NS ? TGN0 : C::NPV * C::D * C::NS;
   static constexpr int tp = tg + TGN;
   static constexpr int total = tp + PLU_NB;
@@ -222,13 +193,12 @@ __global__ void __launch_bounds__(NCONS + 32) k_apply_stream(mhdg_disc g, mhdg_b
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES];
   __shared__ Piece pieces[MAXP];
-  __shared__ PluOffsets plu[C::NBLK];
   __shared__ int npieces;
   double* ring = smem;
   double* W = smem + STAGES * ST_DBL;
   using S = SSm<C>;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const long long PK = plu_size(n);
+  const long long PK = ti_size(n);
 
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -241,7 +211,6 @@ __global__ void __launch_bounds__(NCONS + 32) k_apply_stream(mhdg_disc g, mhdg_b
     int np = 0;
     while (np < MAXP && sc.next(pieces[np])) ++np;
     npieces = np;
-    for (int b = 0; b < C::NBLK; ++b) plu[b] = plu_offsets(n, b);
   }
   __syncthreads();
   const int np = npieces;
@@ -255,14 +224,14 @@ __global__ void __launch_bounds__(NCONS + 32) k_apply_stream(mhdg_disc g, mhdg_b
       auto src_of = [&](int mac, const Piece& p) -> const double* {
         switch (p.kind) {
           case K_GF: return g.gf + p.off;
-          case K_MD: return g.minv_d + p.off;
+          case K_MD: return g.minv_d_face + p.off;
           case K_FST: return bk.face_state_trace + (size_t)mac * NF * BS * BS + p.off;
           case K_FTT: return bk.face_trace_trace + (size_t)mac * NF * BS * BS + p.off;
           case K_FTS: return bk.face_trace_state + (size_t)mac * NF * BS * BS + p.off;
           case K_WV: return bk.wdgdq_vol + (size_t)mac * C::NPV * C::NW + p.off;
           case K_WFZ:
           case K_WF2: return bk.wdgdq_face + (size_t)mac * C::NPF * C::NWF + p.off;
-          default: return fac.lu + (size_t)mac * PK + p.off;
+          default: return fac.lu + (size_t)mac * PK + p.off;  // S^-1 tiles
         }
       };
       constexpr int PREF_AHEAD = 16;
@@ -304,7 +273,7 @@ __global__ void __launch_bounds__(NCONS + 32) k_apply_stream(mhdg_disc g, mhdg_b
     for (int a = 0; a < D; ++a)
 #pragma unroll
       for (int b = 0; b < D; ++b) ij[a][b] = __ldg(g.inv_jac + (size_t)mac * D * D + a * D + b);
-    const int* perm = fac.perm + (size_t)mac * n;
+    double siacc = 0.0;  // per-lane partial of S^-1 y1 for the rows this lane owns
     for (int i = tid; i < LTR; i += NCONS) xl[i] = __ldg(x + __ldg(g.gather + (size_t)mac * LTR + i));
     cbar();
 
@@ -337,8 +306,8 @@ __global__ void __launch_bounds__(NCONS + 32) k_apply_stream(mhdg_disc g, mhdg_b
             for (int l = 0; l < D; ++l) z[l * n + idx] = acc[l];
           }
           cbar();
-        } else if ((p.kind == K_LF || p.kind == K_LFD) && prev == K_WFZ) {
-          // y1 = -A_uh x + A_uq z ; y <- P y1
+        } else if (p.kind == K_SI) {
+          // y1 = -A_uh x + A_uq z
           // cv[K][a][s] = sum_q sum_k gphys[K,q,a,k] w[K,q][k][s]
           for (int idx = tid; idx < C::NSUB * NLOC * NS; idx += NCONS) {
             const int s = idx % NS, a = (idx / NS) % NLOC, K = idx / (NS * NLOC);
@@ -378,29 +347,30 @@ __global__ void __launch_bounds__(NCONS + 32) k_apply_stream(mhdg_disc g, mhdg_b
             for (int e = __ldg(g.vf_ptr + I); e < __ldg(g.vf_ptr + I + 1); ++e) st += rfst[__ldg(g.vf_ent + e) * NS + s];
             for (int e = __ldg(g.vn_ptr + I); e < __ldg(g.vn_ptr + I + 1); ++e) sg -= cv[__ldg(g.vn_sub + e) * NS + s];
             for (int e = __ldg(g.vf_ptr + I); e < __ldg(g.vf_ptr + I + 1); ++e) sg += cfgz[__ldg(g.vf_ent + e) * NS + s];
-            t[idx] = -st + sg;
+            y[idx] = -st + sg;
           }
           cbar();
-          for (int i = tid; i < n; i += NCONS) y[i] = t[__ldg(perm + i)];
-          cbar();
         } else if (p.kind == K_MD) {
-          // y2 restricted to the face nodes, for A_hu
+          // y <- y2 = S^-1 y1 (held in t); y2 restricted to the face nodes, for A_hu
+          for (int i = tid; i < n; i += NCONS) y[i] = t[i];
+          cbar();
           for (int idx = tid; idx < LTR; idx += NCONS) {
             const int s = idx % NS, h = (idx / NS) % LF, f = idx / BS;
             yf[idx] = y[__ldg(g.face_vol_nodes + f * LF + h) * NS + s];
           }
         } else if (p.kind == K_WF2) {
-          // z2 = A_qq^-1 A_qu y2 = sum_r inv_jac[r][l] (M^-1 D_r y2)
-          for (int idx = tid; idx < n; idx += NCONS) {
+          // z2 = A_qq^-1 A_qu y2 = sum_r inv_jac[r][l] (M^-1 D_r y2), at the face nodes only
+          constexpr int FNS = C::NFN * NS;
+          for (int idx = tid; idx < FNS; idx += NCONS) {
             double tr[D];
 #pragma unroll
-            for (int r = 0; r < D; ++r) tr[r] = tg[r * n + idx];
+            for (int r = 0; r < D; ++r) tr[r] = tg[r * FNS + idx];
 #pragma unroll
             for (int l = 0; l < D; ++l) {
               double v = 0.0;
 #pragma unroll
               for (int r = 0; r < D; ++r) v += ij[r][l] * tr[r];
-              z2[l * n + idx] = v;
+              z2[l * FNS + idx] = v;
             }
           }
           cbar();
@@ -430,7 +400,7 @@ __global__ void __launch_bounds__(NCONS + 32) k_apply_stream(mhdg_disc g, mhdg_b
           }
           break;
         }
-        case K_MD: {  // tg[r][I][s] = sum_J (M^-1 D_r)[I][J] y2[J][s]
+        case K_MD: {  // tg[r][i][s] = sum_J (M^-1 D_r)[fnode_i][J] y2[J][s], face nodes only
           constexpr int LPR = 8, RPW = 32 / LPR;
           const int sub = lane / LPR, l = lane % LPR;
           for (int r0 = warp * RPW; r0 < p.nu; r0 += NWARP_C * RPW) {
@@ -500,7 +470,9 @@ __global__ void __launch_bounds__(NCONS + 32) k_apply_stream(mhdg_disc g, mhdg_b
         case K_WFZ:
         case K_WF2: {  // warp-local, as K_WV
           constexpr int DN = D * NS, PPI = 32 / DN;
-          const double* zs = p.kind == K_WFZ ? z : z2;
+          const bool second = p.kind == K_WF2;
+          const double* zs = second ? z2 : z;
+          const int lstride = second ? C::NFN : L;
           double* wf = p.kind == K_WFZ ? wfz : wf2;
           const int per = (p.nu + NWARP_C - 1) / NWARP_C;
           const int pbeg = warp * per, pend = min(p.nu, pbeg + per);
@@ -514,8 +486,9 @@ __global__ void __launch_bounds__(NCONS + 32) k_apply_stream(mhdg_disc g, mhdg_b
               double a = 0.0;
 #pragma unroll
               for (int b = 0; b < NLOCF; ++b) {
-                const int node = __ldg(g.face_vol_nodes + f * LF + __ldg(g.tri_conn + T * NLOCF + b));
-                a += __ldg(g.phi_face + q * NLOCF + b) * zs[(l * L + node) * NS + tt];
+                int node = __ldg(g.face_vol_nodes + f * LF + __ldg(g.tri_conn + T * NLOCF + b));
+                if (second) node = __ldg(g.node_to_face + node);
+                a += __ldg(g.phi_face + q * NLOCF + b) * zs[(l * lstride + node) * NS + tt];
               }
               vw[pi * DN + j] = a;
             }
@@ -535,66 +508,27 @@ __global__ void __launch_bounds__(NCONS + 32) k_apply_stream(mhdg_disc g, mhdg_b
           }
           break;
         }
-        case K_LF:
-        case K_UB: {  // one column tile (all nb rows); warp w owns rows 4w..4w+3 in every tile
-          const PluOffsets& o = plu[p.blk];
-          const int w = p.nu, c0 = p.u0;
-          const double* yv = y + (p.kind == K_LF ? 0 : o.r0 + o.nb) + c0;
-          const int r = 4 * warp + (lane >> 3), l = lane & 7;
-          double acc = 0.0;
-          if (r < o.nb) {
+        case K_SI: {  // one column tile of a row block; warp w owns rows 8w..8w+7 of every block
+          const int nb = ti_rows(n, p.blk), w = p.nu, c0 = p.u0;
+          const int r = 8 * warp + (lane >> 2), l = lane & 3;
+          if (c0 == 0) siacc = 0.0;
+          if (r < nb) {
             const double* a = A + r * w;
+            const double* yv = y + c0;
+            double a0 = 0.0, a1 = 0.0;
 #pragma unroll
-            for (int k = 0; k < PLU_TW / 8; ++k) {
-              const int c = l + 8 * k;
-              if (c < w) acc += a[c] * yv[c];
+            for (int k = 0; k < TI_CW / 4; k += 2) {
+              const int c = l + 4 * k;
+              if (c < w) a0 += a[c] * yv[c];
+              if (c + 4 < w) a1 += a[c + 4] * yv[c + 4];
             }
+            siacc += a0 + a1;
           }
-          acc += __shfl_xor_sync(MHDG_FULL, acc, 4);
-          acc += __shfl_xor_sync(MHDG_FULL, acc, 2);
-          acc += __shfl_xor_sync(MHDG_FULL, acc, 1);
-          if (l == 0 && r < o.nb) tp[r] = (c0 == 0 ? y[o.r0 + r] : tp[r]) - acc;
-          break;
-        }
-        case K_LFD: {  // y_b = inv(L_bb) t, inv(L_bb) unit lower (packed strict lower)
-          const PluOffsets& o = plu[p.blk];
-          if (o.ncol_fwd == 0) {
-            if (tid < o.nb) tp[tid] = y[o.r0 + tid];
-            cbar();
-          }
-          {
-            const int r = 4 * warp + (lane >> 3), l = lane & 7;
-            double acc = 0.0;
-#pragma unroll
-            for (int k = 0; k < PLU_NB / 8; ++k) {
-              const int c = l + 8 * k;
-              if (c < r && r < o.nb) acc += A[plu_lo(r, c)] * tp[c];
-            }
-            acc += __shfl_xor_sync(MHDG_FULL, acc, 4);
+          if (c0 + w == n) {  // last tile of the block: reduce over the row's 4 lanes
+            double acc = siacc;
             acc += __shfl_xor_sync(MHDG_FULL, acc, 2);
             acc += __shfl_xor_sync(MHDG_FULL, acc, 1);
-            if (l == 0 && r < o.nb) y[o.r0 + r] = tp[r] + acc;
-          }
-          break;
-        }
-        case K_UBD: {  // y_b = inv(U_bb) t (packed upper incl. diagonal)
-          const PluOffsets& o = plu[p.blk];
-          if (o.ncol_bwd == 0) {
-            if (tid < o.nb) tp[tid] = y[o.r0 + tid];
-            cbar();
-          }
-          {
-            const int r = 4 * warp + (lane >> 3), l = lane & 7;
-            double acc = 0.0;
-#pragma unroll
-            for (int k = 0; k < PLU_NB / 8; ++k) {
-              const int c = l + 8 * k;
-              if (c >= r && c < o.nb && r < o.nb) acc += A[plu_up(o.nb, r, c)] * tp[c];
-            }
-            acc += __shfl_xor_sync(MHDG_FULL, acc, 4);
-            acc += __shfl_xor_sync(MHDG_FULL, acc, 2);
-            acc += __shfl_xor_sync(MHDG_FULL, acc, 1);
-            if (l == 0 && r < o.nb) y[o.r0 + r] = acc;
+            if (l == 0 && r < nb) t[p.blk * TI_RB + r] = acc;
           }
           break;
         }

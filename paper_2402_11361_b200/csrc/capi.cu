@@ -1,6 +1,6 @@
 // extern "C" boundary (include/mhdg.h): dispatch on the dimension and launch.
 #include "common.cuh"
-#include "packed_lu.cuh"
+#include "tiled_inv.cuh"
 
 namespace mhdg {
 long long g_launches = 0;
@@ -17,7 +17,8 @@ template <int D> int precond_build(const mhdg_disc&, const mhdg_blocks&, double*
 int precond_apply(const mhdg_disc&, const double*, const double*, double*, cudaStream_t);
 int face_reduce(const mhdg_disc&, const double*, const double*, double, double*, cudaStream_t);
 int lu_solve(const mhdg_disc&, const mhdg_factors&, const double*, double*, cudaStream_t);
-int lu_factor(int n, int n_mac, double* scratch, double* packed, int* perm, int* status, cudaStream_t st);
+int inv_factor(int n, int n_mac, double* scratch, double* tiled, int* status, cudaStream_t st);
+size_t gj_smem_bytes(int n);
 int apply_stream(const mhdg_disc&, const mhdg_blocks&, const mhdg_factors&, const double*, double*, cudaStream_t);
 size_t lu_smem_bytes(int n);
 }  // namespace mhdg
@@ -33,7 +34,7 @@ extern "C" {
 
 long long mhdg_launch_count(void) { return g_launches; }
 
-long long mhdg_packed_lu_size(int n) { return plu_size(n); }
+long long mhdg_packed_lu_size(int n) { return ti_size(n); }
 
 static int g_stream_enabled = 1;
 void mhdg_set_stream_enabled(int on) { g_stream_enabled = on; }
@@ -82,8 +83,8 @@ int mhdg_schur_matrix(const mhdg_disc* g, const mhdg_blocks* b, const mhdg_facto
 
 int mhdg_lu_factor(const mhdg_disc* g, const mhdg_factors* f, int* status, void* st) {
   const int n = g->L * g->ns;
-  if (lu_smem_bytes(n) > 227 * 1024) return MHDG_ERR_CONFIG;
-  return lu_factor(n, g->n_mac, f->scratch, f->lu, f->perm, status, S(st));
+  if (gj_smem_bytes(n) > 227 * 1024) return MHDG_ERR_CONFIG;
+  return inv_factor(n, g->n_mac, f->scratch, f->lu, status, S(st));
 }
 
 int mhdg_condense(const mhdg_disc* g, const mhdg_blocks* b, const mhdg_factors* f, int* status, void* st) {

@@ -14,6 +14,7 @@
 #include "common.cuh"
 #include "local_ops.cuh"
 #include "packed_lu.cuh"
+#include "tiled_inv.cuh"
 
 namespace mhdg {
 
@@ -301,7 +302,9 @@ __global__ void __launch_bounds__(LU_THREADS) k_lu(int n, double* __restrict__ L
 // --------------------------------------------------------------------------
 
 __global__ void __launch_bounds__(256) k_pack(int n, const double* __restrict__ F, double* __restrict__ out) {
-  __shared__ double T[PLU_NB][PLU_NB + 1], X[PLU_NB][PLU_NB + 1];
+  extern __shared__ double pk_sm[];
+  double(*T)[PLU_NB + 1] = reinterpret_cast<double(*)[PLU_NB + 1]>(pk_sm);
+  double(*X)[PLU_NB + 1] = reinterpret_cast<double(*)[PLU_NB + 1]>(pk_sm + PLU_NB * (PLU_NB + 1));
   const int mac = blockIdx.x, tid = threadIdx.x;
   const double* A = F + (size_t)mac * n * n;
   double* O = out + (size_t)mac * plu_size(n);
@@ -362,6 +365,203 @@ __global__ void __launch_bounds__(256) k_pack(int n, const double* __restrict__ 
   }
 }
 
+
+// --------------------------------------------------------------------------
+// batched in-place Gauss-Jordan inversion with partial pivoting
+// --------------------------------------------------------------------------
+// Replaces np.linalg.inv (LAPACK getrf + getri, condense.py:67) with the same
+// 2n^3-flop inverse computed panel by panel: a 32-column panel of all n rows
+// is reduced in shared memory (row pivoting, scaling, elimination of every
+// other row), which yields the panel's columns of the composite elementary
+// transform T; every other column is then updated as A[:, c] += (T - I)[:, panel]
+// A_old[panel rows, c] with 64x64 register-tiled rank-32 updates.  Column
+// interchanges are undone at the end.  An exactly zero pivot raises
+// FactorizationError (np.linalg.inv raises LinAlgError).
+
+constexpr int GJ_NB = 32;
+
+size_t gj_smem_bytes(int n) {
+  return sizeof(double) * ((size_t)n * (GJ_NB + 1) + GJ_NB * 64 + 32 + 8) + sizeof(int) * ((size_t)n + 32 + 8) + 64;
+}
+
+__global__ void __launch_bounds__(LU_THREADS) k_gj(int n, double* __restrict__ S, int* status) {
+  extern __shared__ double sm[];
+  constexpr int PW = GJ_NB + 1;
+  const int mac = blockIdx.x, tid = threadIdx.x;
+  double* A = S + (size_t)mac * n * n;
+  double* P = sm;                          // n x PW panel
+  double* Bt = P + (size_t)n * PW;         // GJ_NB x 64 tile of the old pivot rows
+  double* red_v = Bt + GJ_NB * 64;         // 32
+  int* red_i = (int*)(red_v + 32);         // 32
+  int* pivg = red_i + 32;                  // n (+ pad)
+  double* bcast = (double*)(pivg + n + (n & 1) + 2);
+  int* bidx = (int*)(bcast + 2);
+  bool singular = false;
+  const int tx = tid & 15, ty = tid >> 4;
+
+  for (int k0 = 0; k0 < n; k0 += GJ_NB) {
+    const int nb = min(GJ_NB, n - k0);
+    for (int idx = tid; idx < n * nb; idx += blockDim.x) {
+      const int i = idx / nb, c = idx - i * nb;
+      P[i * PW + c] = A[(size_t)i * n + k0 + c];
+    }
+    __syncthreads();
+    for (int j = 0; j < nb; ++j) {
+      const int k = k0 + j;
+      double best = -1.0;
+      int bi = 0x7fffffff;
+      for (int i = k + tid; i < n; i += blockDim.x) {
+        const double v = fabs(P[i * PW + j]);
+        if (v > best || (v == best && i < bi)) { best = v; bi = i; }
+      }
+      block_argmax(best, bi, red_v, red_i, bcast, bidx);
+      const int p = *bidx;
+      if (tid == 0) pivg[k] = p;
+      if (*bcast == 0.0) singular = true;
+      if (p != k) {
+        for (int c = tid; c < nb; c += blockDim.x) {
+          const double t = P[k * PW + c];
+          P[k * PW + c] = P[p * PW + c];
+          P[p * PW + c] = t;
+        }
+      }
+      __syncthreads();
+      const double d = singular ? 0.0 : 1.0 / P[k * PW + j];
+      // scale the pivot row (its column j becomes d)
+      for (int c = tid; c < nb; c += blockDim.x) P[k * PW + c] = (c == j) ? d : P[k * PW + c] * d;
+      __syncthreads();
+      // eliminate column j from every other row
+      for (int idx = tid; idx < n * nb; idx += blockDim.x) {
+        const int i = idx / nb, c = idx - i * nb;
+        if (i == k) continue;
+        const double f = P[i * PW + j];
+        if (c == j) continue;
+        P[i * PW + c] -= f * P[k * PW + c];
+      }
+      __syncthreads();
+      for (int i = tid; i < n; i += blockDim.x)
+        if (i != k) P[i * PW + j] = -P[i * PW + j] * d;
+      __syncthreads();
+    }
+    // interchange the pivot rows in the columns outside the panel
+    for (int j = 0; j < nb; ++j) {
+      const int k = k0 + j, p = pivg[k];
+      if (p != k) {
+        for (int c = tid; c < n - nb; c += blockDim.x) {
+          const int cc = c < k0 ? c : c + nb;
+          const double t = A[(size_t)k * n + cc];
+          A[(size_t)k * n + cc] = A[(size_t)p * n + cc];
+          A[(size_t)p * n + cc] = t;
+        }
+      }
+      __syncthreads();
+    }
+    // T - I on the panel
+    for (int j = tid; j < nb; j += blockDim.x) P[(k0 + j) * PW + j] -= 1.0;
+    __syncthreads();
+    // A[:, c] += (T - I)[:, panel] B[:, c] for every column c outside the panel
+    const int nrest = n - nb;
+    for (int tc = 0; tc < nrest; tc += 64) {
+      const int wc = min(64, nrest - tc);
+      for (int idx = tid; idx < GJ_NB * 64; idx += blockDim.x) {
+        const int r = idx / 64, c = idx % 64;
+        const int cc = tc + c < k0 ? tc + c : tc + c + nb;
+        Bt[idx] = (c < wc && r < nb) ? A[(size_t)(k0 + r) * n + cc] : 0.0;
+      }
+      __syncthreads();
+      for (int tr = 0; tr < n; tr += 64) {
+        double acc[4][4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int bq = 0; bq < 4; ++bq) acc[a][bq] = 0.0;
+        for (int kk = 0; kk < nb; ++kk) {
+          double lv[4], uv[4];
+#pragma unroll
+          for (int a = 0; a < 4; ++a) {
+            const int i = tr + ty + 16 * a;
+            lv[a] = i < n ? P[i * PW + kk] : 0.0;
+          }
+#pragma unroll
+          for (int bq = 0; bq < 4; ++bq) uv[bq] = Bt[kk * 64 + tx + 16 * bq];
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int bq = 0; bq < 4; ++bq) acc[a][bq] += lv[a] * uv[bq];
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          const int i = tr + ty + 16 * a;
+          if (i >= n) continue;
+#pragma unroll
+          for (int bq = 0; bq < 4; ++bq) {
+            const int c = tx + 16 * bq;
+            if (c < wc) {
+              const int cc = tc + c < k0 ? tc + c : tc + c + nb;
+              A[(size_t)i * n + cc] += acc[a][bq];
+            }
+          }
+        }
+      }
+      __syncthreads();
+    }
+    for (int j = tid; j < nb; j += blockDim.x) P[(k0 + j) * PW + j] += 1.0;
+    __syncthreads();
+    for (int idx = tid; idx < n * nb; idx += blockDim.x) {
+      const int i = idx / nb, c = idx - i * nb;
+      A[(size_t)i * n + k0 + c] = P[i * PW + c];
+    }
+    __syncthreads();
+  }
+  // undo the column interchanges, last pivot first
+  for (int k = n - 1; k >= 0; --k) {
+    const int p = pivg[k];
+    if (p != k) {
+      for (int i = tid; i < n; i += blockDim.x) {
+        const double t = A[(size_t)i * n + k];
+        A[(size_t)i * n + k] = A[(size_t)i * n + p];
+        A[(size_t)i * n + p] = t;
+      }
+    }
+    __syncthreads();
+  }
+  if (singular && tid == 0) set_status(status, MHDG_ERR_FACTORIZATION, mac, 0, 0.0);
+}
+
+// n x n inverse (scratch) -> tiled layout (tiled_inv.cuh)
+__global__ void __launch_bounds__(256) k_pack_inv(int n, const double* __restrict__ F, double* __restrict__ out) {
+  const int mac = blockIdx.x;
+  const double* A = F + (size_t)mac * n * n;
+  double* O = out + (size_t)mac * ti_size(n);
+  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
+    const int r = idx / n, c = idx % n;
+    O[ti_idx(n, r, c)] = A[idx];
+  }
+  // zero the even padding of odd-sized tiles
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < ti_nblk(n); ++b) {
+      const int nb = ti_rows(n, b);
+      long long o = ti_block_off(n, b);
+      for (int c = 0; c < n; c += TI_CW) {
+        const int w = (n - c) < TI_CW ? n - c : TI_CW;
+        if (((long long)nb * w) & 1) O[o + (long long)nb * w] = 0.0;
+        o += ti_even((long long)nb * w);
+      }
+    }
+  }
+}
+
+int inv_factor(int n, int n_mac, double* scratch, double* tiled, int* status, cudaStream_t st) {
+  const size_t bytes = gj_smem_bytes(n);
+  if (bytes > 227 * 1024) return MHDG_ERR_CONFIG;
+  if (bytes > 48 * 1024) cudaFuncSetAttribute(k_gj, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  k_gj<<<n_mac, LU_THREADS, bytes, st>>>(n, scratch, status);
+  int rc = launch_ok();
+  if (rc) return rc;
+  k_pack_inv<<<n_mac, 256, 0, st>>>(n, scratch, tiled);
+  return launch_ok();
+}
+
 // --------------------------------------------------------------------------
 // host launchers
 // --------------------------------------------------------------------------
@@ -387,7 +587,9 @@ int lu_factor(int n, int n_mac, double* scratch, double* packed, int* perm, int*
   k_lu<<<n_mac, LU_THREADS, bytes, st>>>(n, scratch, perm, status);
   int rc = launch_ok();
   if (rc) return rc;
-  k_pack<<<n_mac, 256, 0, st>>>(n, scratch, packed);
+  const size_t pbytes = sizeof(double) * 2 * PLU_NB * (PLU_NB + 1);
+  cudaFuncSetAttribute(k_pack, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pbytes);
+  k_pack<<<n_mac, 256, pbytes, st>>>(n, scratch, packed);
   return launch_ok();
 }
 

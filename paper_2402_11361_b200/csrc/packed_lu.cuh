@@ -2,11 +2,11 @@
 //
 // After LU with partial pivoting (P S = L U, L unit lower), each macro's
 // factor is re-laid out in the order the two triangular solves read it, in
-// 32-row blocks b = 0..nblk-1 (nb_b rows each):
+// 64-row blocks b = 0..nblk-1 (nb_b rows each):
 //   forward  section, b ascending : [ L[b, 0:32b] panel | inv(L_bb) strict lower, packed ]
 //   backward section, b descending: [ U[b, 32b+nb_b:n] panel | inv(U_bb) upper incl. diag, packed ]
 // A panel (nb_b rows x ncol) is stored as consecutive column tiles of
-// PLU_TW = 64 columns (the last one narrower), each tile row-major with its
+// PLU_TW = 32 columns (the last one narrower), each tile row-major with its
 // own width as row stride, so one tile is one contiguous bulk copy holding
 // every row of the block.  Every tile / triangle is padded to an even number
 // of doubles so each piece is a 16-byte aligned bulk copy.
@@ -17,8 +17,8 @@
 
 namespace mhdg {
 
-constexpr int PLU_NB = 32;
-constexpr int PLU_TW = 64;
+constexpr int PLU_NB = 64;
+constexpr int PLU_TW = 32;
 
 __host__ __device__ __forceinline__ long long even_ll(long long x) { return x + (x & 1); }
 

@@ -91,6 +91,12 @@ class DeviceDisc:
         t["source"] = f64(src) if src is not None else None
         t["face_macros"] = i32(disc.mesh.face_macros)
         t["face_locals"] = i32(disc.mesh.face_locals)
+        fnodes = np.unique(fvn)
+        n2f = np.full(L, -1, dtype=np.int64)
+        n2f[fnodes] = np.arange(len(fnodes))
+        t["node_to_face"] = i32(n2f)
+        t["minv_d_face"] = f64(pad2(rm.mass_inv_weak_deriv[:, fnodes, :]))
+        self.n_face_nodes = len(fnodes)
         self.t = t
 
         c = _lib.Disc()
@@ -100,6 +106,7 @@ class DeviceDisc:
         c.n_sub, c.nloc, c.nq = rm.n_sub, rm.n_loc, rm.n_quad
         c.n_tri, c.nlocf, c.nqf = rm.n_tri, rm.n_loc_face, rm.n_quad_face
         c.face_fac = disc.face_fac
+        c.n_face_nodes = self.n_face_nodes
         for name, tensor in t.items():
             setattr(c, name, _lib.ptr(tensor))
         self.c = c
