@@ -366,7 +366,7 @@ def run_gpu(args, rank, world):
                    "parallelism": f"replicas{world}" if world > 1 else "single",
                    "l2": "inputs larger than L2 (each apply streams ~%.1f GB of operator data)"
                          % (b_mac * disc.n_mac / 1e9)},
-        "roofline": {"kernel": "k_apply_local", "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+        "roofline": {"kernel": "k_apply_stream<2,4,3> (TMA-streamed apply, C2 specialisation)", "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": traffic,
                      "algorithmic_bytes_per_launch": b_mac * disc.n_mac, "avg_launch_s": k_apply,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"},

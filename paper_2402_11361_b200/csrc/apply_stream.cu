@@ -187,7 +187,7 @@ __device__ __forceinline__ void rows_dot(const double* A, int nu, int ncol, VecF
 template <class C, int STAGES>
 __global__ void __launch_bounds__(NCONS + 32) k_apply_stream(mhdg_disc g, mhdg_blocks bk, mhdg_factors fac,
                                                              const double* __restrict__ x,
-                                                             double* __restrict__ y_loc) {
+                                                             double* __restrict__ y_loc, int pref_ahead) {
   constexpr int D = C::D, NS = C::NS, NF = C::NF, L = C::L, LF = C::LF, BS = C::BS, LTR = C::LTR, n = C::n;
   constexpr int NLOC = C::NLOC, NQ = C::NQ, NLOCF = C::NLOCF, NQF = C::NQF, NTRI = C::NTRI;
   extern __shared__ __align__(128) double smem[];
@@ -234,7 +234,6 @@ __global__ void __launch_bounds__(NCONS + 32) k_apply_stream(mhdg_disc g, mhdg_b
           default: return fac.lu + (size_t)mac * PK + p.off;  // S^-1 tiles
         }
       };
-      constexpr int PREF_AHEAD = 16;
       int pm = blockIdx.x, pp = 0, pref = 0;  // prefetch cursor (macro, piece), pieces issued
       int it = 0;
       for (int mac = blockIdx.x; mac < g.n_mac; mac += gridDim.x) {
@@ -242,7 +241,7 @@ __global__ void __launch_bounds__(NCONS + 32) k_apply_stream(mhdg_disc g, mhdg_b
           const Piece& p = pieces[pi];
           const int s = it % STAGES;
           // keep the prefetch cursor PREF_AHEAD pieces ahead of the copy cursor
-          while (pref < it + PREF_AHEAD && pm < g.n_mac) {
+          while (pref < it + pref_ahead && pm < g.n_mac) {
             const Piece& q = pieces[pp];
             if (q.kind != K_GF && q.kind != K_MD && q.cnt) bulk_prefetch_l2(src_of(pm, q), (uint32_t)q.cnt * 8u);
             ++pref;
@@ -565,6 +564,8 @@ __global__ void __launch_bounds__(NCONS + 32) k_apply_stream(mhdg_disc g, mhdg_b
 // ---------------------------------------------------------------------------
 
 static int g_stream_grid = 0;
+static int g_pref_ahead = 0;  // L2 prefetch lookahead in pieces (0: ring only)
+extern "C" void mhdg_set_stream_prefetch(int pieces) { g_pref_ahead = pieces < 0 ? 0 : pieces; }
 extern "C" int mhdg_stream_grid(void) { return g_stream_grid; }
 
 template <class C>
@@ -607,7 +608,7 @@ static int launch_stream(const mhdg_disc& g, const mhdg_blocks& b, const mhdg_fa
   }
   const int grid = g.n_mac < ctas ? g.n_mac : ctas;
   g_stream_grid = grid;
-  kern<<<grid, NCONS + 32, bytes, st>>>(g, b, f, x, y_loc);
+  kern<<<grid, NCONS + 32, bytes, st>>>(g, b, f, x, y_loc, g_pref_ahead);
   return launch_ok();
 }
 
