@@ -205,6 +205,9 @@ int mhdg_precond_apply(const mhdg_disc *disc, const double *inv, const double *v
    one matches (dim, m, p); 0: always the generic kernel (cross-checks). */
 void mhdg_set_stream_enabled(int on);
 
+/* L2 prefetch lookahead (pieces) of the streamed apply; 0 (default) = shared-memory ring only. */
+void mhdg_set_stream_prefetch(int pieces);
+
 /* number of kernel launches issued by this library since load (diagnostics) */
 long long mhdg_launch_count(void);
 
