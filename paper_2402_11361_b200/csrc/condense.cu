@@ -26,6 +26,45 @@ constexpr int LU_NB = 32;
 // Schur complement
 // --------------------------------------------------------------------------
 
+
+// S rows of one (face) sub-element += sign * X, X[(a,s),(j,r)] = sum_k T1[r][(a,s)][k] VW[k][j].
+// Each thread owns one (a,s) row and 4 consecutive nodes j for all NS components r:
+// per k it loads 4 VW and NS T1 values for 4*NS FMAs; the NS*4 outputs are contiguous.
+template <int D>
+__device__ __forceinline__ void schur_tile_update(const double* T1, const double* VW, int nas, int kk, int L,
+                                                  double* Sm, int n, const int* loc, const int* fmap, double sign) {
+  constexpr int NS = D + 2;
+  const int nj = (L + 3) / 4;
+  for (int task = threadIdx.x; task < nas * nj; task += blockDim.x) {
+    const int as = task / nj, j0 = (task - as * nj) * 4;
+    double acc[4][NS];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int r = 0; r < NS; ++r) acc[u][r] = 0.0;
+    for (int k = 0; k < kk; ++k) {
+      double tv[NS], vw[4];
+#pragma unroll
+      for (int r = 0; r < NS; ++r) tv[r] = T1[(r * nas + as) * kk + k];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) vw[u] = (j0 + u < L) ? VW[k * L + j0 + u] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int r = 0; r < NS; ++r) acc[u][r] += tv[r] * vw[u];
+    }
+    int node = __ldg(loc + as / NS);
+    if (fmap) node = __ldg(fmap + node);
+    double* out = Sm + (size_t)(node * NS + as % NS) * n + j0 * NS;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (j0 + u < L) {
+#pragma unroll
+        for (int r = 0; r < NS; ++r) out[u * NS + r] += sign * acc[u][r];
+      }
+  }
+}
+
 template <int D>
 __global__ void __launch_bounds__(SCHUR_THREADS) k_schur(mhdg_disc g, mhdg_blocks b, double* __restrict__ S) {
   extern __shared__ double sm[];
@@ -38,16 +77,15 @@ __global__ void __launch_bounds__(SCHUR_THREADS) k_schur(mhdg_disc g, mhdg_block
   for (size_t i = threadIdx.x; i < (size_t)n * n; i += blockDim.x) Sm[i] = SS[i];
   __syncthreads();
 
-  // shared: T1 (rows nloc*NS, k = nq*D) for one r, VW (nq*D x L), ijs
+  // shared: T1[r][(a,s)][(q,l)] for all r, VW[(q,l)][j]
   const int kv = sz.nq * D, kf = sz.nqf * D;
   const int kmax = kv > kf ? kv : kf;
   const int rmax = sz.nloc * NS > sz.nlocf * NS ? sz.nloc * NS : sz.nlocf * NS;
   double* T1 = sm;
-  double* VW = T1 + rmax * kmax;
+  double* VW = T1 + NS * rmax * kmax;
 
-  // ---- volume sub-elements ----
+  // ---- volume sub-elements: X[(a,s),(j,r)] = sum_{(q,l)} T1[r][(a,s),(q,l)] VW[(q,l), j] ----
   for (int K = 0; K < sz.n_sub; ++K) {
-    // VW[(q,l), j] = sum_r inv_jac[r,l] PM[K,q,r,j]
     for (int idx = threadIdx.x; idx < kv * L; idx += blockDim.x) {
       const int j = idx % L, ql = idx / L, l = ql % D, q = ql / D;
       const double* pm = g.pm_vol + (((size_t)K * sz.nq + q) * D) * L + j;
@@ -56,34 +94,26 @@ __global__ void __launch_bounds__(SCHUR_THREADS) k_schur(mhdg_disc g, mhdg_block
       for (int r = 0; r < D; ++r) a += __ldg(ij + r * D + l) * __ldg(pm + r * L);
       VW[idx] = a;
     }
-    for (int rr = 0; rr < NS; ++rr) {
-      // T1[(a,s),(q,l)] = sum_k gphys[q,a,k] W[K,q,k,l,s,rr]
-      for (int idx = threadIdx.x; idx < sz.nloc * NS * kv; idx += blockDim.x) {
-        const int ql = idx % kv, as = idx / kv, s = as % NS, a = as / NS, l = ql % D, q = ql / D;
-        const double* gr = g.grad_ref + (((size_t)K * sz.nq + q) * sz.nloc + a) * D;
-        const double* W = b.wdgdq_vol + ((((size_t)mac * sz.n_sub + K) * sz.nq + q) * D * D) * NS * NS;
-        double acc = 0.0;
+    const int nas = sz.nloc * NS;
+    for (int idx = threadIdx.x; idx < NS * nas * kv; idx += blockDim.x) {
+      const int ql = idx % kv, rest = idx / kv, as = rest % nas, rr = rest / nas;
+      const int s = as % NS, a = as / NS, l = ql % D, q = ql / D;
+      const double* gr = g.grad_ref + (((size_t)K * sz.nq + q) * sz.nloc + a) * D;
+      const double* W = b.wdgdq_vol + ((((size_t)mac * sz.n_sub + K) * sz.nq + q) * D * D) * NS * NS;
+      double acc = 0.0;
 #pragma unroll
-        for (int k = 0; k < D; ++k) {
-          double gp = 0.0;
+      for (int k = 0; k < D; ++k) {
+        double gp = 0.0;
 #pragma unroll
-          for (int r = 0; r < D; ++r) gp += __ldg(gr + r) * __ldg(ij + r * D + k);
-          acc += gp * __ldg(W + ((k * D + l) * NS + s) * NS + rr);
-        }
-        T1[idx] = acc;
+        for (int r = 0; r < D; ++r) gp += __ldg(gr + r) * __ldg(ij + r * D + k);
+        acc += gp * __ldg(W + ((k * D + l) * NS + s) * NS + rr);
       }
-      __syncthreads();
-      // S[(conn[a],s), (j,rr)] += sum_{ql} T1[(a,s), ql] VW[ql, j]
-      for (int idx = threadIdx.x; idx < sz.nloc * NS * L; idx += blockDim.x) {
-        const int j = idx % L, as = idx / L, s = as % NS, a = as / NS;
-        const double* t = T1 + as * kv;
-        double acc = 0.0;
-        for (int k = 0; k < kv; ++k) acc += t[k] * VW[k * L + j];
-        const int row = __ldg(g.sub_conn + K * sz.nloc + a) * NS + s;
-        Sm[(size_t)row * n + j * NS + rr] += acc;
-      }
-      __syncthreads();
+      T1[idx] = acc;
     }
+    __syncthreads();
+    // S[(conn[a],s), (j,rr)] += X, register-tiled: 4 nodes j x NS components per thread
+    schur_tile_update<D>(T1, VW, nas, kv, L, Sm, n, g.sub_conn + K * sz.nloc, nullptr, 1.0);
+    __syncthreads();
   }
   // ---- face sub-elements ----
   for (int f = 0; f < NF; ++f) {
@@ -96,24 +126,17 @@ __global__ void __launch_bounds__(SCHUR_THREADS) k_schur(mhdg_disc g, mhdg_block
         for (int r = 0; r < D; ++r) a += __ldg(ij + r * D + l) * __ldg(pm + r * L);
         VW[idx] = a;
       }
-      for (int rr = 0; rr < NS; ++rr) {
-        for (int idx = threadIdx.x; idx < sz.nlocf * NS * kf; idx += blockDim.x) {
-          const int ql = idx % kf, as = idx / kf, s = as % NS, a = as / NS, l = ql % D, q = ql / D;
-          const double* W = b.wdgdq_face +
-                            ((((size_t)mac * NF + f) * sz.n_tri * sz.nqf + T * sz.nqf + q) * D + l) * NS * NS;
-          T1[idx] = __ldg(W + s * NS + rr) * __ldg(g.phi_face + q * sz.nlocf + a);
-        }
-        __syncthreads();
-        for (int idx = threadIdx.x; idx < sz.nlocf * NS * L; idx += blockDim.x) {
-          const int j = idx % L, as = idx / L, s = as % NS, a = as / NS;
-          const double* t = T1 + as * kf;
-          double acc = 0.0;
-          for (int k = 0; k < kf; ++k) acc += t[k] * VW[k * L + j];
-          const int node = __ldg(g.face_vol_nodes + f * sz.Lf + __ldg(g.tri_conn + T * sz.nlocf + a));
-          Sm[(size_t)(node * NS + s) * n + j * NS + rr] -= acc;
-        }
-        __syncthreads();
+      const int nas = sz.nlocf * NS;
+      for (int idx = threadIdx.x; idx < NS * nas * kf; idx += blockDim.x) {
+        const int ql = idx % kf, rest = idx / kf, as = rest % nas, rr = rest / nas;
+        const int s = as % NS, a = as / NS, l = ql % D, q = ql / D;
+        const double* W = b.wdgdq_face +
+                          ((((size_t)mac * NF + f) * sz.n_tri * sz.nqf + T * sz.nqf + q) * D + l) * NS * NS;
+        T1[idx] = __ldg(W + s * NS + rr) * __ldg(g.phi_face + q * sz.nlocf + a);
       }
+      __syncthreads();
+      schur_tile_update<D>(T1, VW, nas, kf, L, Sm, n, g.tri_conn + T * sz.nlocf, g.face_vol_nodes + f * sz.Lf, -1.0);
+      __syncthreads();
     }
   }
 }
@@ -551,6 +574,391 @@ __global__ void __launch_bounds__(256) k_pack_inv(int n, const double* __restric
   }
 }
 
+
+// --------------------------------------------------------------------------
+// k_gj2: Gauss-Jordan inverse with 64-column panels and DMMA updates
+// --------------------------------------------------------------------------
+// Same algorithm as k_gj; the rank-64 update of the columns outside the panel,
+// A[:, c] += (T - I)[:, panel] B[:, c], runs on the FP64 tensor cores
+// (mma.sync.m8n8k4.f64 -> DMMA) with A-fragments from the shared panel and
+// B-fragments from a staged 64x64 tile of the old pivot rows; C tiles are
+// read-modify-written from global memory (L2).  The column interchanges are
+// not undone here: the pivots go to `piv` and k_pack_inv applies the
+// composed column permutation while tiling.
+
+constexpr int GJ2_NB = 64, GJ2_PW = 68, GJ2_TC = 48, GJ2_BS = 52;  // strides chosen for conflict-free DMMA fragments
+
+#ifdef MHDG_STREAM_PROFILE
+__device__ unsigned long long g_gjprof[8];
+#define GJT(v) long long v = clock64()
+#define GJADD(k, v) if (threadIdx.x == 0) atomicAdd(&g_gjprof[k], (unsigned long long)(clock64() - (v)))
+extern "C" int mhdg_gj_profile(unsigned long long* out, int reset) {
+  if (out) cudaMemcpyFromSymbol(out, g_gjprof, sizeof(g_gjprof));
+  if (reset) {
+    unsigned long long z[8] = {};
+    cudaMemcpyToSymbol(g_gjprof, z, sizeof(z));
+  }
+  return 0;
+}
+#else
+#define GJT(v)
+#define GJADD(k, v)
+#endif
+
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+size_t gj2_smem_bytes(int n) {
+  return sizeof(double) * ((size_t)n * GJ2_PW + GJ2_NB * GJ2_BS + 32 + 8) + sizeof(int) * (32 + 8) + 64;
+}
+
+__global__ void __launch_bounds__(512, 1) k_gj2(int n, double* __restrict__ S, int* __restrict__ piv_out,
+                                                 int* status) {
+  extern __shared__ double sm[];
+  const int mac = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* A = S + (size_t)mac * n * n;
+  int* pivg = piv_out + (size_t)mac * n;
+  double* P = sm;                            // n x GJ2_PW panel
+  double* Bt = P + (size_t)n * GJ2_PW;       // GJ2_NB x GJ2_TC old pivot rows (row stride GJ2_BS)
+  double* red_v = Bt + GJ2_NB * GJ2_BS;      // 32
+  int* red_i = (int*)(red_v + 32);           // 32
+  double* bcast = (double*)(red_i + 32);     // 2
+  int* bidx = (int*)(bcast + 2);
+  bool singular = false;
+
+  for (int k0 = 0; k0 < n; k0 += GJ2_NB) {
+    const int nb = min(GJ2_NB, n - k0);
+    GJT(t0);
+    for (int idx = tid; idx < n * nb; idx += blockDim.x) {
+      const int i = idx / nb, c = idx - i * nb;
+      P[i * GJ2_PW + c] = A[(size_t)i * n + k0 + c];
+    }
+    __syncthreads();
+    GJADD(0, t0);
+    // ---- panel: sub-panels of 16 columns; GJ steps inside the sub-panel,
+    //      then the sub-panel's transform applied to the other panel columns
+    //      with DMMA (C in shared memory) ----
+    for (int js = 0; js < nb; js += 16) {
+      GJT(t1);
+      const int ns = min(16, nb - js);
+      const int cl = tid & 15, rg = tid >> 4;  // thread -> (sub-panel column, row group)
+      // partial pivot candidates for the next column, one per row group
+      __shared__ double cand_v[32];
+      __shared__ int cand_i[32];
+      constexpr int RPT = 12;  // rows per thread (n <= 32 * RPT = 384)
+      const int rbeg = rg * RPT;
+      for (int j = js; j < js + ns; ++j) {
+        const int k = k0 + j;
+        if (warp == 0) {
+          double best = -1.0;
+          int bi = 0x7fffffff;
+          if (j == js) {  // first column of the sub-panel: full scan
+            for (int i = k + lane; i < n; i += 32) {
+              const double v = fabs(P[i * GJ2_PW + j]);
+              if (v > best || (v == best && i < bi)) { best = v; bi = i; }
+            }
+          } else {  // fused candidates from the previous step's elimination
+            best = cand_v[lane];
+            bi = cand_i[lane];
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            const double v2 = __shfl_xor_sync(MHDG_FULL, best, o);
+            const int i2 = __shfl_xor_sync(MHDG_FULL, bi, o);
+            if (v2 > best || (v2 == best && i2 < bi)) { best = v2; bi = i2; }
+          }
+          if (lane == 0) {
+            *bidx = bi;
+            bcast[0] = best;
+            bcast[1] = best == 0.0 ? 0.0 : 1.0 / P[bi * GJ2_PW + j];  // one reciprocal per step
+            pivg[k] = bi;
+          }
+        }
+        __syncthreads();
+        const int p = *bidx;
+        if (bcast[0] == 0.0) singular = true;
+        const double d = singular ? 0.0 : bcast[1];
+        const int c = js + cl;
+        const bool inside = cl < ns;
+        const double rowp_c = inside ? P[p * GJ2_PW + c] : 0.0;
+        const double rowk_c = inside ? P[k * GJ2_PW + c] : 0.0;
+        const double rowk_j = P[k * GJ2_PW + j];
+        __syncthreads();  // everyone has read rows k and p before anyone writes
+        const bool next_col = (c == j + 1) && (j + 1 < js + ns);
+        double cb = -1.0;
+        int ci = 0x7fffffff;
+        if (inside) {
+          const double piv_c = (c == j) ? d : rowp_c * d;  // new row k
+#pragma unroll
+          for (int q = 0; q < RPT; ++q) {
+            const int i = rbeg + q;
+            if (i < n && i != k) {
+              const double old_i = (i == p) ? rowk_c : P[i * GJ2_PW + c];
+              const double old_ij = (i == p) ? rowk_j : P[i * GJ2_PW + j];
+              const double nvl = (c == j) ? -old_ij * d : old_i - old_ij * piv_c;
+              P[i * GJ2_PW + c] = nvl;
+              if (next_col && i > k) {
+                const double a = fabs(nvl);
+                if (a > cb || (a == cb && i < ci)) { cb = a; ci = i; }
+              }
+            }
+          }
+          if (rg == (k / RPT)) P[k * GJ2_PW + c] = piv_c;
+          if (next_col && k + 1 < n && rg == ((k + 1) / RPT) && false) {
+          }
+        }
+        if (next_col) {
+          cand_v[rg] = cb;
+          cand_i[rg] = ci;
+        }
+        // columns of the panel outside the sub-panel: plain row interchange
+        if (p != k)
+          for (int cc = tid; cc < GJ2_NB; cc += blockDim.x)
+            if (cc < js || cc >= js + ns) {
+              const double t = P[k * GJ2_PW + cc];
+              P[k * GJ2_PW + cc] = P[p * GJ2_PW + cc];
+              P[p * GJ2_PW + cc] = t;
+            }
+        __syncthreads();
+      }
+      GJADD(1, t1);
+      GJT(t2);
+      // other panel columns c (outside [js, js+ns)): P[:, c] += (Ts - I) Bs[:, c]
+      for (int idx = tid; idx < 16 * GJ2_NB; idx += blockDim.x) {
+        const int r = idx >> 6, c = idx & 63;
+        const bool other = (c < js || c >= js + ns) && c < nb && r < ns;
+        Bt[r * 68 + c] = other ? P[(k0 + js + r) * GJ2_PW + c] : 0.0;
+      }
+      __syncthreads();
+      for (int r = tid; r < ns; r += blockDim.x) P[(k0 + js + r) * GJ2_PW + js + r] -= 1.0;
+      __syncthreads();
+      {
+        const int g = lane >> 2, t4 = lane & 3;
+        // warp -> row band of 8 rows (step 8 * warps); all 8 column tiles of the panel
+        for (int r0 = warp * 8; r0 < n; r0 += 8 * (int)(blockDim.x >> 5)) {
+          double acc[8][2];
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) {
+            const int row = r0 + g, col = 8 * jj + 2 * t4;
+            const bool ok = row < n;
+            acc[jj][0] = ok ? P[row * GJ2_PW + col] : 0.0;
+            acc[jj][1] = ok ? P[row * GJ2_PW + col + 1] : 0.0;
+          }
+#pragma unroll
+          for (int kk = 0; kk < 16; kk += 4) {
+            const int row = r0 + g;
+            const double a = (row < n && kk + t4 < ns) ? P[row * GJ2_PW + js + kk + t4] : 0.0;
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) dmma_8x8x4(acc[jj][0], acc[jj][1], a, Bt[(kk + t4) * 68 + 8 * jj + g]);
+          }
+          __syncwarp();
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) {
+            const int row = r0 + g, col = 8 * jj + 2 * t4;
+            if (row < n) {
+              if (col < js || col >= js + ns) P[row * GJ2_PW + col] = acc[jj][0];
+              if (col + 1 < js || col + 1 >= js + ns) P[row * GJ2_PW + col + 1] = acc[jj][1];
+            }
+          }
+        }
+      }
+      __syncthreads();
+      for (int r = tid; r < ns; r += blockDim.x) P[(k0 + js + r) * GJ2_PW + js + r] += 1.0;
+      __syncthreads();
+      GJADD(2, t2);
+    }
+    GJT(t3);
+    // ---- row interchanges outside the panel: the panel's swaps composed into
+    //      one permutation (source map, O(n)), applied to the touched rows
+    //      through shared memory ----
+    {
+      int* srcmap = (int*)Bt;          // n
+      int* rows = srcmap + n + 1;      // touched rows (<= 2 GJ2_NB)
+      double* stage = (double*)(rows + 2 * GJ2_NB + 2 - ((n + 1) & 1));  // 8-byte aligned
+      __shared__ int nrows;
+      for (int r = tid; r < n; r += blockDim.x) srcmap[r] = r;
+      if (tid == 0) nrows = 0;
+      __syncthreads();
+      if (tid == 0)
+        for (int j = 0; j < nb; ++j) {
+          const int k = k0 + j, p = pivg[k];
+          const int t = srcmap[k];
+          srcmap[k] = srcmap[p];
+          srcmap[p] = t;
+        }
+      __syncthreads();
+      for (int r = tid; r < n; r += blockDim.x)
+        if (srcmap[r] != r) rows[atomicAdd(&nrows, 1)] = r;
+      __syncthreads();
+      const int m = nrows;
+      const int CW = 32;
+      for (int c0 = 0; c0 < n - nb && m > 0; c0 += CW) {
+        for (int idx = tid; idx < m * CW; idx += blockDim.x) {
+          const int q = idx / CW, c = c0 + idx % CW;
+          if (c < n - nb) {
+            const int cc = c < k0 ? c : c + nb;
+            stage[idx] = A[(size_t)srcmap[rows[q]] * n + cc];
+          }
+        }
+        __syncthreads();
+        for (int idx = tid; idx < m * CW; idx += blockDim.x) {
+          const int q = idx / CW, c = c0 + idx % CW;
+          if (c < n - nb) {
+            const int cc = c < k0 ? c : c + nb;
+            A[(size_t)rows[q] * n + cc] = stage[idx];
+          }
+        }
+        __syncthreads();
+      }
+    }
+    GJADD(3, t3);
+    GJT(t_up);
+    for (int j = tid; j < nb; j += blockDim.x) P[(k0 + j) * GJ2_PW + j] -= 1.0;  // T - I
+    // zero the panel's unused columns so the k-loop can run over a full GJ2_NB
+    for (int idx = tid; idx < n * (GJ2_NB - nb); idx += blockDim.x) {
+      const int i = idx / (GJ2_NB - nb), c = nb + idx % (GJ2_NB - nb);
+      P[i * GJ2_PW + c] = 0.0;
+    }
+    __syncthreads();
+    // ---- update: C += (T - I) B over 64x64 tiles; 16 warps, warp tile 16 x 16,
+    //      the next row tile's C prefetched into registers during the DMMAs ----
+    const int nrest = n - nb;
+    const int wr = (warp / 3) * 16, wc = (warp % 3) * 16;
+    const int g = lane >> 2, t4 = lane & 3;
+    for (int tc = 0; tc < nrest; tc += GJ2_TC) {
+      const int wct = min(GJ2_TC, nrest - tc);
+      for (int idx = tid; idx < GJ2_NB * GJ2_TC; idx += blockDim.x) {
+        const int r = idx / GJ2_TC, c = idx % GJ2_TC;
+        const int cc = tc + c < k0 ? tc + c : tc + c + nb;
+        Bt[r * GJ2_BS + c] = (c < wct && r < nb) ? A[(size_t)(k0 + r) * n + cc] : 0.0;
+      }
+      __syncthreads();
+      // 48-column tiles: warps 0..11 own 16x16 sub-tiles of each 64x48 C tile
+      if (warp < 12) {
+      // global column of this thread's two C columns per 8-wide tile
+      int gcol[2][2];
+      bool cok[2][2];
+#pragma unroll
+      for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int col = wc + 8 * jj + 2 * t4 + e;
+          cok[jj][e] = col < wct;
+          gcol[jj][e] = tc + col < k0 ? tc + col : tc + col + nb;
+        }
+      double nxt[2][2][2];
+      auto load_c = [&](int tr, double (&c)[2][2][2]) {
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int row = tr + wr + 8 * i + g;
+#pragma unroll
+          for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) c[i][jj][e] = (row < n && cok[jj][e]) ? A[(size_t)row * n + gcol[jj][e]] : 0.0;
+        }
+      };
+      load_c(0, nxt);
+      for (int tr = 0; tr < n; tr += 64) {
+        double acc[2][2][2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int jj = 0; jj < 2; ++jj) {
+            acc[i][jj][0] = nxt[i][jj][0];
+            acc[i][jj][1] = nxt[i][jj][1];
+          }
+        if (tr + 64 < n) load_c(tr + 64, nxt);
+#pragma unroll 8
+        for (int kk = 0; kk < GJ2_NB; kk += 4) {
+          double a[2], b[2];
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int row = tr + wr + 8 * i + g;
+            a[i] = row < n ? P[row * GJ2_PW + kk + t4] : 0.0;
+          }
+#pragma unroll
+          for (int jj = 0; jj < 2; ++jj) b[jj] = Bt[(kk + t4) * GJ2_BS + wc + 8 * jj + g];
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int jj = 0; jj < 2; ++jj) dmma_8x8x4(acc[i][jj][0], acc[i][jj][1], a[i], b[jj]);
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int row = tr + wr + 8 * i + g;
+#pragma unroll
+          for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+              if (row < n && cok[jj][e]) A[(size_t)row * n + gcol[jj][e]] = acc[i][jj][e];
+        }
+      }
+      }  // warp < 12
+      __syncthreads();
+    }
+    GJADD(4, t_up);
+    GJT(t5);
+    for (int j = tid; j < nb; j += blockDim.x) P[(k0 + j) * GJ2_PW + j] += 1.0;
+    __syncthreads();
+    for (int idx = tid; idx < n * nb; idx += blockDim.x) {
+      const int i = idx / nb, c = idx - i * nb;
+      A[(size_t)i * n + k0 + c] = P[i * GJ2_PW + c];
+    }
+    __syncthreads();
+    GJADD(5, t5);
+  }
+  if (singular && tid == 0) set_status(status, MHDG_ERR_FACTORIZATION, mac, 0, 0.0);
+}
+
+// n x n inverse with pending column interchanges -> tiled layout.  The swaps
+// (k <-> piv[k]) applied last-first compose into X[:, j] = A[:, idx[j]].
+__global__ void __launch_bounds__(256) k_pack_inv_perm(int n, const double* __restrict__ F, const int* __restrict__ piv,
+                                                       double* __restrict__ out) {
+  extern __shared__ int idxs[];
+  const int mac = blockIdx.x;
+  const double* A = F + (size_t)mac * n * n;
+  double* O = out + (size_t)mac * ti_size(n);
+  if (threadIdx.x == 0) {
+    for (int j = 0; j < n; ++j) idxs[j] = j;
+    for (int k = n - 1; k >= 0; --k) {
+      const int p = piv[(size_t)mac * n + k];
+      const int t = idxs[k];
+      idxs[k] = idxs[p];
+      idxs[p] = t;
+    }
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
+    const int r = idx / n, c = idx % n;
+    O[ti_idx(n, r, c)] = A[(size_t)r * n + idxs[c]];
+  }
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < ti_nblk(n); ++b) {
+      const int nb = ti_rows(n, b);
+      long long o = ti_block_off(n, b);
+      for (int c = 0; c < n; c += TI_CW) {
+        const int w = (n - c) < TI_CW ? n - c : TI_CW;
+        if (((long long)nb * w) & 1) O[o + (long long)nb * w] = 0.0;
+        o += ti_even((long long)nb * w);
+      }
+    }
+  }
+}
+
+int inv_factor2(int n, int n_mac, double* scratch, int* piv, double* tiled, int* status, cudaStream_t st) {
+  const size_t bytes = gj2_smem_bytes(n);
+  if (bytes > 227 * 1024 || n > 384) return -1;  // 12 rows per thread x 32 row groups
+  cudaFuncSetAttribute(k_gj2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  k_gj2<<<n_mac, 512, bytes, st>>>(n, scratch, piv, status);
+  int rc = launch_ok();
+  if (rc) return rc;
+  k_pack_inv_perm<<<n_mac, 256, sizeof(int) * n, st>>>(n, scratch, piv, tiled);
+  return launch_ok();
+}
+
 int inv_factor(int n, int n_mac, double* scratch, double* tiled, int* status, cudaStream_t st) {
   const size_t bytes = gj_smem_bytes(n);
   if (bytes > 227 * 1024) return MHDG_ERR_CONFIG;
@@ -571,7 +979,7 @@ int schur_matrix(const mhdg_disc& g, const mhdg_blocks& b, double* S, cudaStream
   constexpr int NS = D + 2;
   const int kv = g.nq * D, kf = g.nqf * D, kmax = kv > kf ? kv : kf;
   const int rmax = (g.nloc > g.nlocf ? g.nloc : g.nlocf) * NS;
-  const size_t bytes = sizeof(double) * ((size_t)rmax * kmax + (size_t)kmax * g.L);
+  const size_t bytes = sizeof(double) * ((size_t)NS * rmax * kmax + (size_t)kmax * g.L);
   if (bytes > 48 * 1024) cudaFuncSetAttribute(k_schur<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   k_schur<D><<<g.n_mac, SCHUR_THREADS, bytes, st>>>(g, b, S);
   return launch_ok();
