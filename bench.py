@@ -51,6 +51,20 @@ def c2_discretization(n_cells=N_CELLS):
     return case, disc
 
 
+def c2_slab_discretization(world, comm):
+    """Weak scaling: a (64 N) x 64 periodic strip of unit cells (same h as C2);
+    rank r owns the 64 x 64-cell slab r (8192 macros, exactly C2's per-GPU
+    work) and exchanges halos with its two neighbours."""
+    from paper_2402_11361_b200.cases import UniformFlow2D
+    from paper_2402_11361_b200.dist import DistDiscretization
+    from paper_2402_11361_b200.mesh import build_square_mesh
+
+    case = UniformFlow2D()
+    mesh = build_square_mesh(((0.0, 0.0), (float(world), 1.0)), (N_CELLS * world, N_CELLS), M_SUB,
+                             periodic=(True, True))
+    return case, DistDiscretization(mesh, P_DEG, case.params, comm=comm)
+
+
 def c2_state(case, disc, seed=0):
     """Nodal state + N(0, sigma) noise (seed 0); owner-side trace copy."""
     X = disc.node_coords().reshape(-1, 2)
@@ -239,43 +253,71 @@ def fp64_gemm_peak(torch, n=8192, reps=5):
     return 2.0 * n**3 / best / 1e12
 
 
+def _max_over_ranks(dist, t):
+    import torch
+
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    tt = torch.tensor([t], dtype=torch.float64, device=dev)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    return float(tt)
+
+
 def run_gpu(args, rank, world):
     import torch
 
     from paper_2402_11361_b200 import _lib
     from paper_2402_11361_b200 import assembly as A
     from paper_2402_11361_b200.condense import CondensedSchur
+    from paper_2402_11361_b200.dist import DistCondensed
     from paper_2402_11361_b200.device import current_stream
 
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    torch.cuda.set_device(local % torch.cuda.device_count())
     dist = None
     if world > 1:
         import torch.distributed as dist  # noqa: F811
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # MHDG_DIST_BACKEND=gloo: functional check of the slab path with several
+        # ranks on one GPU (host-staged halos; not a measurement)
+        backend = os.environ.get("MHDG_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     L = _lib.lib()
 
-    case, disc = c2_discretization()
-    u, uhat = c2_state(case, disc)
+    ddisc = None
+    if world > 1:
+        from paper_2402_11361_b200.dist import Comm
+
+        case, ddisc = c2_slab_discretization(world, Comm())
+        disc = ddisc.local
+        u, uhat_local = c2_state(case, disc, seed=rank)
+        uhat = uhat_local[: ddisc.n_trace]  # owned faces (side 0 is local on every owned face)
+    else:
+        case, disc = c2_discretization()
+        u, uhat = c2_state(case, disc)
     dd = disc.device
+    top = ddisc if ddisc is not None else disc  # the discretization the public API is called with
     fields = A.FieldState(torch.as_tensor(u, device="cuda"), None, torch.as_tensor(uhat, device="cuda"))
-    fields.q = A.gradient_refresh(disc, fields.u, fields.uhat)
+    uh_local = ddisc.forward(fields.uhat) if ddisc is not None else fields.uhat
+    fields.q = A.gradient_refresh(disc, fields.u, uh_local)
     ctx = A.StageContext.steady(1.0)
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
     # ---- assembly (one Jacobian assembly, timed) ----
     torch.cuda.synchronize()
-    blocks, _ = A.jacobian(disc, fields, ctx)  # warm (also the real one)
+    blocks, _ = A.jacobian(top, fields, ctx)  # warm (also the real one)
     a0, a1 = ev(), ev()
     a0.record()
-    blocks, _ = A.jacobian(disc, fields, ctx)
+    blocks, _ = A.jacobian(top, fields, ctx)
     a1.record()
     a1.synchronize()
     t_asm = a0.elapsed_time(a1) / 1e3
 
     # ---- condensation: Schur correction + batched LU, timed ----
-    cond = CondensedSchur.allocate(blocks)
+    cond = CondensedSchur.allocate(blocks)  # this rank's macros (the slab when N > 1)
+    api = DistCondensed(ddisc, cond) if ddisc is not None else cond
     status = dd.status_buffer()
     cond.refactor_async(status)
     torch.cuda.synchronize()
@@ -292,16 +334,24 @@ def run_gpu(args, rank, world):
 
     # ---- applies ----
     K, W = args.steps, args.warmup
-    xs = torch.as_tensor(np.random.default_rng(1).standard_normal((K + W, disc.n_trace)), device="cuda")
-    y = torch.empty(disc.n_trace, dtype=torch.float64, device="cuda")
+    n_own = top.n_trace
+    xs = torch.as_tensor(np.random.default_rng(1 + rank).standard_normal((K + W, n_own)), device="cuda")
+    y = torch.empty(n_own, dtype=torch.float64, device="cuda")
+    y_face = torch.empty(disc.n_trace, dtype=torch.float64, device="cuda")
     y_loc = torch.empty(dd.n_local_trace, dtype=torch.float64, device="cuda")
     st = current_stream()
 
     def apply_split(x, ev0, ev1):
+        """One trace-operator apply; with slabs: forward halo, local apply,
+        face reduce, reverse halo (DistCondensed.apply_trace, split so the
+        streamed kernel is timed on its own)."""
+        xl = ddisc.forward(x) if ddisc is not None else x
         ev0.record()
-        _lib.check(L.mhdg_apply_trace_local(dd.c, blocks.c, cond._fac, _lib.ptr(x), _lib.ptr(y_loc), st), "apply")
+        _lib.check(L.mhdg_apply_trace_local(dd.c, blocks.c, cond._fac, _lib.ptr(xl), _lib.ptr(y_loc), st), "apply")
         ev1.record()
-        _lib.check(L.mhdg_face_reduce(dd.c, _lib.ptr(y_loc), _lib.ptr(y), st), "reduce")
+        _lib.check(L.mhdg_face_reduce(dd.c, _lib.ptr(y_loc), _lib.ptr(y_face), st), "reduce")
+        if ddisc is not None:
+            y.copy_(ddisc.reverse(y_face))
 
     clk = Clocks(local).__enter__()
     for i in range(W):
@@ -322,29 +372,31 @@ def run_gpu(args, rank, world):
     clk.__exit__(None, None, None)
     t_apply = t0.elapsed_time(t1) / 1e3
     if dist:
-        tt = torch.tensor([t_apply], device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_apply = float(tt)
+        t_apply = _max_over_ranks(dist, t_apply)
     k_apply = float(np.mean([a.elapsed_time(b) / 1e3 for a, b in kev]))
 
     # ---- e2e through the public API with pinned host buffers ----
-    xh = torch.empty(disc.n_trace, dtype=torch.float64, pin_memory=True)
-    yh = torch.empty(disc.n_trace, dtype=torch.float64, pin_memory=True)
+    xh = torch.empty(n_own, dtype=torch.float64, pin_memory=True)
+    yh = torch.empty(n_own, dtype=torch.float64, pin_memory=True)
     xh.copy_(xs[0].cpu())
     xd = torch.empty_like(y)
     for _ in range(2):
         xd.copy_(xh, non_blocking=True)
-        yh.copy_(cond.apply_trace(xd, out=y), non_blocking=True)
+        yh.copy_(api.apply_trace(xd, out=y), non_blocking=True)
     torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
     e0, e1 = ev(), ev()
     ne = max(3, min(K, 20))
     e0.record()
     for _ in range(ne):
         xd.copy_(xh, non_blocking=True)
-        yh.copy_(cond.apply_trace(xd, out=y), non_blocking=True)
+        yh.copy_(api.apply_trace(xd, out=y), non_blocking=True)
     e1.record()
     e1.synchronize()
     t_e2e = e0.elapsed_time(e1) / 1e3 / ne
+    if dist:
+        t_e2e = _max_over_ranks(dist, t_e2e)
 
     peaks = measured_peaks()
     hbm = float(peaks.get("hbm_gbs", 6650.0))
@@ -355,15 +407,18 @@ def run_gpu(args, rank, world):
     f_mac = condense_flops_per_macro(disc)
     cond_tf = f_mac * disc.n_mac / t_cond / 1e12
 
-    value = world * disc.n_trace * K / t_apply
+    n_dofs_job = world * n_own if ddisc is None else ddisc.global_mesh.n_faces * disc.Lf * disc.ns
+    value = n_dofs_job * K / t_apply
     line = {
         "metric": METRIC, "value": value, "unit": "DOF-applies/s", "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": 1e3 * t_apply / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
         "config": {"workload": "C2 2D operator benchmark: 64x64 squares -> 8192 triangular macros, m=4, p=3, "
                                "periodic, uniform flow + N(0,1e-2), StageContext.steady(pseudo_dt=1)",
-                   "n_macros": disc.n_mac, "n_trace_dofs": disc.n_trace, "global_batch": None, "seq_len": None,
-                   "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "n_macros": disc.n_mac * world, "n_trace_dofs": n_dofs_job, "macros_per_gpu": disc.n_mac,
+                   "global_batch": None, "seq_len": None,
+                   "parallelism": (f"slab{world} (({N_CELLS}*{world})x{N_CELLS} periodic strip, forward/reverse "
+                                   "face halos over NCCL P2P)") if world > 1 else "single",
                    "l2": "inputs larger than L2 (each apply streams ~%.1f GB of operator data)"
                          % (b_mac * disc.n_mac / 1e9)},
         "roofline": {"kernel": "k_apply_stream<2,4,3> (TMA-streamed apply, C2 specialisation)", "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
@@ -377,8 +432,8 @@ def run_gpu(args, rank, world):
                                   "peak_source": "cuBLAS DGEMM 8192^3 measured in this run"}},
         "assembly": {"metric": "macro-elements assembled/s (Jacobian + residual)", "value": disc.n_mac / t_asm,
                      "seconds": t_asm},
-        "e2e": {"value": world * disc.n_trace / t_e2e, "unit": "DOF-applies/s",
-                "h2d_bytes_per_step": 8 * disc.n_trace, "d2h_bytes_per_step": 8 * disc.n_trace},
+        "e2e": {"value": n_dofs_job / t_e2e, "unit": "DOF-applies/s",
+                "h2d_bytes_per_step": 8 * n_dofs_job, "d2h_bytes_per_step": 8 * n_dofs_job},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }

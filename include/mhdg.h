@@ -197,6 +197,20 @@ int mhdg_gradient_refresh(const mhdg_disc *disc, const double *u, const double *
 int mhdg_precond_build(const mhdg_disc *disc, const mhdg_blocks *blocks, double *inv, int *status,
                        void *stream);
 
+/* As mhdg_precond_build, adding extra[f] (n_faces*bs*bs, canonical face order, or
+   NULL) to each face block before symmetrising: the contribution of a face side
+   that lives on another rank (multi-GPU slabs).  Build and apply cover faces
+   [0, disc->n_faces) only, so a slab passes a copy of its disc with n_faces set
+   to its owned-face count (owned faces come first; ghost faces carry one side
+   and are never factorised). */
+int mhdg_precond_build_ext(const mhdg_disc *disc, const mhdg_blocks *blocks, const double *extra, double *inv,
+                           int *status, void *stream);
+
+/* out[i] = P^T face_trace_trace[macs[i], lfs[i]] P (bs x bs, the face's canonical
+   node order): one side's share of the block preconditioner, for export. */
+int mhdg_side_blocks(const mhdg_disc *disc, const mhdg_blocks *blocks, const int *macs, const int *lfs, int count,
+                     double *out, void *stream);
+
 /* y = blockdiag(inv) v (krylov.py:234-236). */
 int mhdg_precond_apply(const mhdg_disc *disc, const double *inv, const double *v, double *y,
                        void *stream);

@@ -91,6 +91,8 @@ def lib():
             "mhdg_gradient_refresh": [P(Disc), _dp, _dp, _dp, _dp],
             "mhdg_precond_build": [P(Disc), P(Blocks), _dp, _dp, _dp],
             "mhdg_precond_apply": [P(Disc), _dp, _dp, _dp, _dp],
+            "mhdg_precond_build_ext": [P(Disc), P(Blocks), _dp, _dp, _dp, _dp],
+            "mhdg_side_blocks": [P(Disc), P(Blocks), _dp, _dp, C.c_int, _dp, _dp],
         }
         for name, args in sigs.items():
             fn = getattr(L, name)
@@ -110,7 +112,7 @@ EXPORTED = (
     "mhdg_assemble", "mhdg_condense", "mhdg_schur_matrix", "mhdg_lu_factor", "mhdg_lu_solve",
     "mhdg_apply_trace", "mhdg_apply_trace_local", "mhdg_face_reduce", "mhdg_condensed_rhs", "mhdg_recover",
     "mhdg_gradient_refresh", "mhdg_precond_build", "mhdg_precond_apply", "mhdg_launch_count",
-    "mhdg_packed_lu_size", "mhdg_set_stream_enabled",
+    "mhdg_packed_lu_size", "mhdg_set_stream_enabled", "mhdg_precond_build_ext", "mhdg_side_blocks",
 )
 
 

@@ -206,10 +206,14 @@ def assemble_system(disc, fields: FieldState, ctx: StageContext, want_jac: bool 
 
 
 def residual(disc, fields, ctx, frozen: FrozenCoeffs | None = None):
+    if getattr(disc, "is_distributed", False):
+        return disc.residual(fields, ctx, frozen)
     return assemble_system(disc, fields, ctx, want_jac=False, frozen=frozen)
 
 
 def jacobian(disc, fields, ctx):
+    if getattr(disc, "is_distributed", False):
+        return disc.jacobian(fields, ctx)
     _, blocks, frozen = assemble_system(disc, fields, ctx, want_jac=True)
     return blocks, frozen
 
@@ -233,6 +237,12 @@ def to_device_fields(disc, u, q, uhat) -> FieldState:
 def interpolate(disc, state_fn) -> FieldState:
     """Nodal + owner-side trace interpolation, gradient refreshed on the device
     (Discretization.interpolate, assembly.py:228-245)."""
+    if getattr(disc, "is_distributed", False):
+        u, uhat = disc.local.nodal_interpolant(state_fn)
+        dev = disc.device.device
+        ut = torch.as_tensor(u, dtype=torch.float64, device=dev)
+        uh = torch.as_tensor(uhat[: disc.n_trace], dtype=torch.float64, device=dev)
+        return FieldState(ut, gradient_refresh(disc.local, ut, disc.forward(uh)), uh)
     u, uhat = disc.nodal_interpolant(state_fn)
     dev = disc.device.device
     ut = torch.as_tensor(u, dtype=torch.float64, device=dev)

@@ -130,4 +130,8 @@ def condense(blocks: LocalBlocks, path: str = "schur") -> CondensedSchur:
     one-shot 'standard' path is a CPU oracle in the reference)."""
     if path != "schur":
         raise ValueError(f"unknown condensation path {path!r} (the device path is 'schur')")
+    if getattr(blocks, "dist", None) is not None:
+        from .dist import condense_distributed
+
+        return condense_distributed(blocks, path)
     return CondensedSchur.build(blocks)

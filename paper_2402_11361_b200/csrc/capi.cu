@@ -13,7 +13,8 @@ template <int D> int schur_matrix(const mhdg_disc&, const mhdg_blocks&, double*,
 template <int D> int assemble(const mhdg_disc&, const mhdg_flow&, const mhdg_stage&, const double*, const double*,
                               const double*, double*, double*, double*, double*, int, const mhdg_blocks*,
                               const mhdg_frozen*, const mhdg_frozen*, int*, cudaStream_t);
-template <int D> int precond_build(const mhdg_disc&, const mhdg_blocks&, double*, int*, cudaStream_t);
+template <int D> int precond_build(const mhdg_disc&, const mhdg_blocks&, const double*, double*, int*, cudaStream_t);
+template <int D> int side_blocks(const mhdg_disc&, const mhdg_blocks&, const int*, const int*, int, double*, cudaStream_t);
 int precond_apply(const mhdg_disc&, const double*, const double*, double*, cudaStream_t);
 int face_reduce(const mhdg_disc&, const double*, const double*, double, double*, cudaStream_t);
 int lu_solve(const mhdg_disc&, const mhdg_factors&, const double*, double*, cudaStream_t);
@@ -109,7 +110,20 @@ int mhdg_assemble(const mhdg_disc* g, const mhdg_flow* fl, const mhdg_stage* sg,
 }
 
 int mhdg_precond_build(const mhdg_disc* g, const mhdg_blocks* b, double* inv, int* status, void* st) {
-  return DISPATCH(g, precond_build<2>(*g, *b, inv, status, S(st)), precond_build<3>(*g, *b, inv, status, S(st)));
+  return DISPATCH(g, precond_build<2>(*g, *b, nullptr, inv, status, S(st)),
+                  precond_build<3>(*g, *b, nullptr, inv, status, S(st)));
+}
+
+int mhdg_precond_build_ext(const mhdg_disc* g, const mhdg_blocks* b, const double* extra, double* inv, int* status,
+                           void* st) {
+  return DISPATCH(g, precond_build<2>(*g, *b, extra, inv, status, S(st)),
+                  precond_build<3>(*g, *b, extra, inv, status, S(st)));
+}
+
+int mhdg_side_blocks(const mhdg_disc* g, const mhdg_blocks* b, const int* macs, const int* lfs, int count, double* out,
+                     void* st) {
+  return DISPATCH(g, side_blocks<2>(*g, *b, macs, lfs, count, out, S(st)),
+                  side_blocks<3>(*g, *b, macs, lfs, count, out, S(st)));
 }
 
 int mhdg_precond_apply(const mhdg_disc* g, const double* inv, const double* v, double* y, void* st) {

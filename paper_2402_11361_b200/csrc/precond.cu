@@ -13,8 +13,8 @@ namespace mhdg {
 constexpr int PRE_THREADS = 256;
 
 template <int D>
-__global__ void __launch_bounds__(PRE_THREADS) k_precond_build(mhdg_disc g, mhdg_blocks b, double* __restrict__ inv,
-                                                               int* status) {
+__global__ void __launch_bounds__(PRE_THREADS) k_precond_build(mhdg_disc g, mhdg_blocks b, const double* __restrict__ extra,
+                                                               double* __restrict__ inv, int* status) {
   extern __shared__ double sm[];
   constexpr int NS = D + 2, NF = D + 1;
   const int f = blockIdx.x, bs = g.Lf * NS, tid = threadIdx.x;
@@ -41,6 +41,10 @@ __global__ void __launch_bounds__(PRE_THREADS) k_precond_build(mhdg_disc g, mhdg
       const int pr = gat[r] - f * bs, pc = gat[c] - f * bs;
       B[pr * bs + pc] += A[idx];  // each (pr, pc) hit once per side: no race
     }
+    __syncthreads();
+  }
+  if (extra) {  // the face's other side, held by another rank, already in canonical order
+    for (int idx = tid; idx < bs * bs; idx += blockDim.x) B[idx] += extra[(size_t)f * bs * bs + idx];
     __syncthreads();
   }
   for (int idx = tid; idx < bs * bs; idx += blockDim.x) {
@@ -108,14 +112,42 @@ __global__ void __launch_bounds__(PRE_THREADS) k_precond_apply(int bs, const dou
   for (int i = threadIdx.x; i < bs; i += blockDim.x) y[(size_t)f * bs + i] = sm[bs + i];
 }
 
+// out[i] = P^T face_trace_trace[macs[i], lfs[i]] P in the face's canonical order
 template <int D>
-int precond_build(const mhdg_disc& g, const mhdg_blocks& b, double* inv, int* status, cudaStream_t st) {
+__global__ void k_side_blocks(mhdg_disc g, mhdg_blocks b, const int* __restrict__ macs, const int* __restrict__ lfs,
+                              int count, double* __restrict__ out) {
+  constexpr int NS = D + 2, NF = D + 1;
+  const int i = blockIdx.x, bs = g.Lf * NS;
+  if (i >= count) return;
+  const int mac = macs[i], lf = lfs[i];
+  const int* gat = g.gather + ((size_t)mac * NF + lf) * bs;
+  const double* A = b.face_trace_trace + ((size_t)mac * NF + lf) * bs * bs;
+  const int base = (gat[0] / bs) * bs;  // face id * bs
+  for (int idx = threadIdx.x; idx < bs * bs; idx += blockDim.x) {
+    const int r = idx / bs, c = idx - r * bs;
+    out[(size_t)i * bs * bs + (gat[r] - base) * bs + (gat[c] - base)] = A[idx];
+  }
+}
+
+template <int D>
+int side_blocks(const mhdg_disc& g, const mhdg_blocks& b, const int* macs, const int* lfs, int count, double* out,
+                cudaStream_t st) {
+  if (count <= 0) return MHDG_OK;
+  k_side_blocks<D><<<count, PRE_THREADS, 0, st>>>(g, b, macs, lfs, count, out);
+  return launch_ok();
+}
+template int side_blocks<2>(const mhdg_disc&, const mhdg_blocks&, const int*, const int*, int, double*, cudaStream_t);
+template int side_blocks<3>(const mhdg_disc&, const mhdg_blocks&, const int*, const int*, int, double*, cudaStream_t);
+
+template <int D>
+int precond_build(const mhdg_disc& g, const mhdg_blocks& b, const double* extra, double* inv, int* status,
+                  cudaStream_t st) {
   const int bs = g.Lf * (D + 2);
   const size_t bytes = sizeof(double) * 2 * bs * bs;
   if (bytes > 227 * 1024) return MHDG_ERR_CONFIG;
   if (bytes > 48 * 1024)
     cudaFuncSetAttribute(k_precond_build<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  k_precond_build<D><<<g.n_faces, PRE_THREADS, bytes, st>>>(g, b, inv, status);
+  k_precond_build<D><<<g.n_faces, PRE_THREADS, bytes, st>>>(g, b, extra, inv, status);
   return launch_ok();
 }
 
@@ -125,7 +157,7 @@ int precond_apply(const mhdg_disc& g, const double* inv, const double* v, double
   return launch_ok();
 }
 
-template int precond_build<2>(const mhdg_disc&, const mhdg_blocks&, double*, int*, cudaStream_t);
-template int precond_build<3>(const mhdg_disc&, const mhdg_blocks&, double*, int*, cudaStream_t);
+template int precond_build<2>(const mhdg_disc&, const mhdg_blocks&, const double*, double*, int*, cudaStream_t);
+template int precond_build<3>(const mhdg_disc&, const mhdg_blocks&, const double*, double*, int*, cudaStream_t);
 
 }  // namespace mhdg
