@@ -98,6 +98,11 @@ typedef struct {
   int n_face_nodes;
   const int *node_to_face;    /* L: index into the face-node list, -1 for interior nodes */
   const double *minv_d_face;  /* d*n_face_nodes*L: rows of M^-1 D_r at the face nodes */
+  /* distinct grad_ref[K] tables (sub-elements of one orientation class share
+     them: 2 classes in 2D, <= 6 in 3D) */
+  int n_grad_cls;
+  const double *grad_cls;     /* n_grad_cls*nq*nloc*d */
+  const int *grad_cls_of;     /* n_sub: class of each sub-element */
 } mhdg_disc;
 
 typedef struct {
@@ -128,16 +133,27 @@ typedef struct {
   double *face_visc_state;   /* n_mac*nf*(n_tri nqf)*ns */
 } mhdg_frozen;
 
-/* condensed operator S = A_uu - A_uq A_qq^-1 A_qu (n = L*ns), P S = L U with
-   partial pivoting.  `lu` holds each macro's factor in the packed solve order
-   of csrc/packed_lu.cuh (mhdg_packed_lu_size(n) doubles per macro: L/U panels
-   row-major, diagonal tiles inverted); perm[i] is the original row of factor
-   row i; `scratch` (n_mac*n*n) holds S / the in-place LU before packing. */
+/* condensed operator S = A_uu - A_uq A_qq^-1 A_qu (n = L*ns).  `lu` holds
+   each macro's explicit inverse S^-1 in the tiled order of
+   csrc/tiled_inv.cuh (mhdg_packed_lu_size(n) doubles per macro: 64-row
+   blocks of 32-column tiles), computed by Gauss-Jordan with partial
+   pivoting; perm is the pivot workspace; `scratch` (n_mac*n*n) holds S before
+   inversion.  `work` (mhdg_apply_work_size doubles, or NULL) holds the
+   per-macro hand-off vectors of the split apply (pre -> S^-1 stream -> post);
+   with NULL the fused single-kernel apply runs. */
 typedef struct {
   double *lu;                /* n_mac*mhdg_packed_lu_size(n) */
   int *perm;                 /* n_mac*n */
   double *scratch;           /* n_mac*n*n */
+  double *work;              /* mhdg_apply_work_size(disc) or NULL */
 } mhdg_factors;
+
+/* doubles of mhdg_factors.work for this discretization */
+long long mhdg_apply_work_size(const mhdg_disc *disc);
+
+/* 1 (default): split apply (pre / S^-1 stream / post kernels) when `work` is
+   set; 0: fused single-kernel apply.  For A/B measurements. */
+void mhdg_set_apply_split(int on);
 
 /* doubles per macro of the packed LU factor */
 long long mhdg_packed_lu_size(int n);

@@ -40,6 +40,7 @@ class Disc(C.Structure):
         ("bc_kind", _dp), ("wall_e", _dp), ("wall_u", _dp), ("u_dir", _dp), ("source", _dp),
         ("face_macros", _dp), ("face_locals", _dp),
         ("n_face_nodes", C.c_int), ("node_to_face", _dp), ("minv_d_face", _dp),
+        ("n_grad_cls", C.c_int), ("grad_cls", _dp), ("grad_cls_of", _dp),
     ]
 
 
@@ -62,7 +63,7 @@ class Frozen(C.Structure):
 
 
 class Factors(C.Structure):
-    _fields_ = [("lu", _dp), ("perm", _dp), ("scratch", _dp)]
+    _fields_ = [("lu", _dp), ("perm", _dp), ("scratch", _dp), ("work", _dp)]
 
 
 _lib = None
@@ -104,6 +105,10 @@ def lib():
         L.mhdg_packed_lu_size.restype = C.c_longlong
         L.mhdg_launch_count.argtypes = []
         L.mhdg_launch_count.restype = C.c_longlong
+        L.mhdg_apply_work_size.argtypes = [P(Disc)]
+        L.mhdg_apply_work_size.restype = C.c_longlong
+        L.mhdg_set_apply_split.argtypes = [C.c_int]
+        L.mhdg_set_apply_split.restype = None
         _lib = L
     return _lib
 
@@ -113,6 +118,7 @@ EXPORTED = (
     "mhdg_apply_trace", "mhdg_apply_trace_local", "mhdg_face_reduce", "mhdg_condensed_rhs", "mhdg_recover",
     "mhdg_gradient_refresh", "mhdg_precond_build", "mhdg_precond_apply", "mhdg_launch_count",
     "mhdg_packed_lu_size", "mhdg_set_stream_enabled", "mhdg_precond_build_ext", "mhdg_side_blocks",
+    "mhdg_apply_work_size", "mhdg_set_apply_split",
 )
 
 

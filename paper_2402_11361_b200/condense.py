@@ -23,13 +23,16 @@ class FactorizationError(RuntimeError):
 
 
 class CondensedSchur:
-    def __init__(self, blocks: LocalBlocks, lu: torch.Tensor, perm: torch.Tensor, scratch: torch.Tensor):
+    def __init__(self, blocks: LocalBlocks, lu: torch.Tensor, perm: torch.Tensor, scratch: torch.Tensor,
+                 work: torch.Tensor | None = None):
         self.blocks = blocks
-        self.lu = lu  # packed factors (csrc/packed_lu.cuh)
+        self.lu = lu  # S^-1 per macro, tiled (csrc/tiled_inv.cuh)
         self.perm = perm
-        self.scratch = scratch  # S, then its in-place LU, before packing
+        self.scratch = scratch  # S before inversion
+        self.work = work  # hand-off vectors of the split apply (pre -> S^-1 stream -> post)
         fac = _lib.Factors()
         fac.lu, fac.perm, fac.scratch = _lib.ptr(lu), _lib.ptr(perm), _lib.ptr(scratch)
+        fac.work = _lib.ptr(work) if work is not None else None
         self._fac = fac
         dd = blocks.disc.device
         self._y_loc = torch.empty(dd.n_local_trace, dtype=torch.float64, device=dd.device)
@@ -43,7 +46,8 @@ class CondensedSchur:
         lu = torch.empty((disc.n_mac, packed), dtype=torch.float64, device=dev)
         perm = torch.empty((disc.n_mac, n), dtype=torch.int32, device=dev)
         scratch = torch.empty((disc.n_mac, n, n), dtype=torch.float64, device=dev)
-        return cls(blocks, lu, perm, scratch)
+        work = torch.empty(int(_lib.lib().mhdg_apply_work_size(disc.device.c)), dtype=torch.float64, device=dev)
+        return cls(blocks, lu, perm, scratch, work)
 
     @classmethod
     def build(cls, blocks: LocalBlocks) -> "CondensedSchur":

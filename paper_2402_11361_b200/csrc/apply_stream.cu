@@ -33,7 +33,13 @@ __host__ __device__ constexpr int cpow(int b, int e) {
 __host__ __device__ constexpr int ceven(int x) { return x + (x & 1); }
 
 constexpr int ST_DBL = 2112;  // doubles per ring stage (16.5 KB: one 64x32 LU tile or a 64-row inverted triangle)
-constexpr int NCONS = 256;    // consumer threads (8 warps)
+#ifndef MHDG_NCONS
+#define MHDG_NCONS 512
+#endif
+#ifndef MHDG_STAGES
+#define MHDG_STAGES 3
+#endif
+constexpr int NCONS = MHDG_NCONS;  // consumer threads of the pre / post / fused kernels (16 warps)
 
 template <int D_, int M_, int P_>
 struct Cfg {
@@ -53,7 +59,7 @@ struct Cfg {
   static constexpr int NFN = L - (N - 1 >= D ? cbinom(N - 1, D) : 0);  // boundary lattice nodes
 };
 
-enum : int { K_FST = 0, K_FTT, K_WV, K_WFZ, K_SI, K_LFD, K_UB, K_UBD, K_WF2, K_FTS, K_GF, K_MD };
+enum : int { K_FST = 0, K_FTT, K_WV, K_WFZ, K_SI, K_Y2, K_FC, K_UNUSED, K_WF2, K_FTS, K_GF, K_MD };
 
 struct Piece {
   unsigned char kind, blk;
@@ -69,12 +75,18 @@ __host__ __device__ __forceinline__ int units_per_piece(int unit) {
 
 // Walks one macro's pieces in consumption order; the producer and the
 // consumers run identical copies.  Segment order:
-//   Gf table | FST | FTT | W_vol | W_face(z) | LU fwd | LU bwd | M^-1 D table | W_face(z2) | FTS
-template <class C>
+//   Gf table | FST | FTT | W_vol | W_face(z) | S^-1 tiles | y2, face terms | M^-1 D table | W_face(z2) | FTS
+// PART 0 walks the fused apply (all but the hand-off pieces), PART 1 the
+// segments before S^-1 (pre kernel), PART 2 the hand-off pieces and the
+// segments after S^-1 (post kernel).
+template <class C, int PART = 0>
 struct Sched {
   int seg = 0, i = 0, b = 0, r = 0;
-  __host__ __device__ bool rows(Piece& p, int kind, int nrows, int unit) {
-    const int per = units_per_piece(unit);
+  // W_vol pieces hold whole sub-elements when they fit (one warp pass per point group)
+  static constexpr bool WV_ALIGN = C::NQ * C::NW <= ST_DBL && ((C::NQ * C::NW) % 2 == 0);
+  static constexpr int WV_PER = WV_ALIGN ? (ST_DBL / (C::NQ * C::NW)) * C::NQ : 0;
+  __host__ __device__ bool rows(Piece& p, int kind, int nrows, int unit, int per = 0) {
+    if (per <= 0) per = units_per_piece(unit);
     if (i * per >= nrows) return false;
     p.kind = (unsigned char)kind;
     p.u0 = (unsigned short)(i * per);
@@ -87,14 +99,19 @@ struct Sched {
   }
   __host__ __device__ bool next(Piece& p) {
     while (seg < 10) {
+      if (PART == 1 && seg > 4) return false;  // pre part: up to the W_face(z) stash
+      if (PART == 2 && seg < 6) {               // post part: from the hand-off pieces on
+        seg = 6;
+        i = r = b = 0;
+      }
       switch (seg) {
         case 0: if (rows(p, K_GF, C::NF * C::L, C::LF)) return true; break;
         case 1: if (rows(p, K_FST, C::NF * C::BS, C::BS)) return true; break;
         case 2: if (rows(p, K_FTT, C::NF * C::BS, C::BS)) return true; break;
-        case 3: if (rows(p, K_WV, C::NPV, C::NW)) return true; break;
+        case 3: if (rows(p, K_WV, C::NPV, C::NW, WV_PER)) return true; break;
         case 4: if (rows(p, K_WFZ, C::NPF, C::NWF)) return true; break;
         case 5:  // S^-1: row blocks of TI_RB rows, each as TI_CW-column tiles
-          if (b < C::NBLK) {
+          if (PART == 0 && b < C::NBLK) {
             const int nb = ti_rows(C::n, b);
             const int w = (C::n - r) < TI_CW ? C::n - r : TI_CW;
             p.kind = K_SI;
@@ -108,7 +125,17 @@ struct Sched {
             return true;
           }
           break;
-        case 6:
+        case 6:  // post part: y2 = S^-1 y1 and the pre part's face terms, from the work buffers
+          if (PART == 2 && i < 2) {
+            p.kind = (unsigned char)(i == 0 ? K_Y2 : K_FC);
+            p.u0 = 0;
+            p.nu = (unsigned short)(i == 0 ? C::n : C::LTR);
+            p.off = 0;
+            p.cnt = (unsigned short)(i == 0 ? ceven(C::n) : 2 * C::LTR);
+            p.blk = 0;
+            ++i;
+            return true;
+          }
           break;
         case 7: if (rows(p, K_MD, C::D * C::NFN, C::L)) return true; break;
         case 8: if (rows(p, K_WF2, C::NPF, C::NWF)) return true; break;
@@ -125,8 +152,6 @@ struct Sched {
 
 template <class C>
 struct SSm {  // consumer work layout (doubles), after the ring
-  static constexpr int PPV = ST_DBL / C::NW > 0 ? ((C::NW & 1) ? ((ST_DBL / C::NW) & ~1) : ST_DBL / C::NW) : 1;
-  static constexpr int PPF = (C::NWF & 1) ? ((ST_DBL / C::NWF) & ~1) : ST_DBL / C::NWF;
   static constexpr int xl = 0;
   static constexpr int z = xl + C::LTR;  // z, later z2
   static constexpr int y = z + C::D * C::n;
@@ -138,13 +163,36 @@ struct SSm {  // consumer work layout (doubles), after the ring
   static constexpr int yf = cfgz + C::LTR;
   static constexpr int wfz = yf + C::LTR;
   static constexpr int wf2 = wfz + C::NPF * C::NS;
-  static constexpr int vv = wf2 + C::NPF * C::NS;  // 8 warps x 32 doubles
-  static constexpr int cv = vv + 8 * 32;
+  static constexpr int vv = wf2 + C::NPF * C::NS;  // one 32-double scratch per consumer warp
+  static constexpr int cv = vv + (NCONS / 32) * 32;
   static constexpr int tg = cv + C::NSUB * C::NLOC * C::NS;  // Gf x | W_vol results | M^-1 D y
   static constexpr int TGN0 = C::NF * C::n;
   static constexpr int TGN = TGN0 > C::NPV * C::D * C::NS ? TGN0 : C::NPV * C::D * C::NS;
-  static constexpr int tp = tg + TGN;
-  static constexpr int total = tp + PLU_NB;
+  static constexpr int total = ceven(tg + TGN);
+};
+
+// Reference tables the consumers read, copied to shared memory once per CTA
+// (after the work area): doubles first, then ints; the gradient classes
+// (runtime count) go last.
+template <class C>
+struct TSm {
+  static constexpr int phi_vol = 0;                             // NQ*NLOC
+  static constexpr int phi_face = phi_vol + C::NQ * C::NLOC;    // NQF*NLOCF
+  static constexpr int ndbl = ceven(phi_face + C::NQF * C::NLOCF);
+  static constexpr int sub_conn = 0;                            // ints from here: NSUB*NLOC
+  static constexpr int tri_conn = sub_conn + C::NSUB * C::NLOC;  // NTRI*NLOCF
+  static constexpr int fvn = tri_conn + C::NTRI * C::NLOCF;      // NF*LF
+  static constexpr int n2f = fvn + C::NF * C::LF;                // L
+  static constexpr int fn_ptr = n2f + C::L;                      // LF+1
+  static constexpr int fn_ent = fn_ptr + C::LF + 1;              // NTRI*NLOCF
+  static constexpr int vf_ptr = fn_ent + C::NTRI * C::NLOCF;     // L+1
+  static constexpr int vf_ent = vf_ptr + C::L + 1;               // NF*LF
+  static constexpr int vn_ptr = vf_ent + C::NF * C::LF;          // L+1
+  static constexpr int vn_sub = vn_ptr + C::L + 1;               // NSUB*NLOC
+  static constexpr int gcls_of = vn_sub + C::NSUB * C::NLOC;     // NSUB
+  static constexpr int nint = gcls_of + C::NSUB;
+  static constexpr int total = ndbl + ceven((nint + 1) / 2);     // doubles
+  static constexpr int CLS = C::NQ * C::NLOC * C::D;            // doubles per gradient class
 };
 
 __device__ __forceinline__ void cbar() { named_bar(1, NCONS); }
@@ -163,40 +211,72 @@ __device__ unsigned long long g_prof[16][3];
 #endif
 constexpr int MAXP = 256;  // pieces per macro (checked on the host)
 
-// acc_r = sum_c A[r][c] vec_r[c] for the nu rows of a staged piece, LPR lanes
-// per row; out(r, acc) on one lane per row.  Warps take rows independently.
+// First group >= g0 that warp `warp` owns when groups are dealt round-robin
+// by global index: consecutive pieces of one kind keep all warps busy.
+__device__ __forceinline__ int first_group(int g0, int warp) {
+  return g0 + ((warp - g0 % NWARP_C) % NWARP_C + NWARP_C) % NWARP_C;
+}
+
+// acc_r = sum_c A[r][c] vec_r[c] for rows u0 .. u0+nu-1 of a staged piece, LPR
+// lanes per row, RPW = 32/LPR rows per warp group, groups dealt to warps by
+// global row index; out(r, acc) on one lane per row (r local to the piece).
 template <int LPR, class VecF, class OutF>
-__device__ __forceinline__ void rows_dot(const double* A, int nu, int ncol, VecF vec, OutF out) {
+__device__ __forceinline__ void rows_dot(const double* A, int u0, int nu, int ncol, VecF vec, OutF out) {
   constexpr int RPW = 32 / LPR;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int sub = lane / LPR, l = lane % LPR;
-  for (int r0 = warp * RPW; r0 < nu; r0 += NWARP_C * RPW) {
-    const int rl = r0 + sub;
-    double acc = 0.0;
-    if (rl < nu) {
+  const int g1 = (u0 + nu - 1) / RPW;
+  for (int gg = first_group(u0 / RPW, warp); gg <= g1; gg += NWARP_C) {
+    const int rl = gg * RPW + sub - u0;
+    const bool on = rl >= 0 && rl < nu;
+    double a0 = 0.0, a1 = 0.0;
+    if (on) {
       const double* a = A + rl * ncol;
       const double* v = vec(rl);
-      for (int c = l; c < ncol; c += LPR) acc += a[c] * v[c];
+      int c = l;
+      for (; c + LPR < ncol; c += 2 * LPR) {
+        a0 += a[c] * v[c];
+        a1 += a[c + LPR] * v[c + LPR];
+      }
+      if (c < ncol) a0 += a[c] * v[c];
     }
+    double acc = a0 + a1;
 #pragma unroll
     for (int o = LPR / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(MHDG_FULL, acc, o);
-    if (l == 0 && rl < nu) out(rl, acc);
+    if (l == 0 && on) out(rl, acc);
   }
 }
 
-template <class C, int STAGES>
-__global__ void __launch_bounds__(NCONS + 32) k_apply_stream(mhdg_disc g, mhdg_blocks bk, mhdg_factors fac,
+// Work buffers of the split apply (mhdg_factors.work), per macro:
+//   y1 [M][NP] | y2 [M][NP] | face terms [M][A_hh x (LTR) | g (LTR)]   (NP = n rounded up to even)
+template <class C>
+struct Work {
+  static constexpr int NP = ceven(C::n);
+  static __host__ __device__ __forceinline__ double* y1(double* w, int m) { return w + (size_t)m * NP; }
+  static __host__ __device__ __forceinline__ double* y2(double* w, int M, int m) { return w + ((size_t)M + m) * NP; }
+  static __host__ __device__ __forceinline__ double* fc(double* w, int M, int m) {
+    return w + (size_t)2 * M * NP + (size_t)m * 2 * C::LTR;
+  }
+};
+
+template <class C, int STAGES, int PART>
+__global__ void __launch_bounds__(NCONS + 32, 2) k_apply_stream(mhdg_disc g, mhdg_blocks bk, mhdg_factors fac,
                                                              const double* __restrict__ x,
                                                              double* __restrict__ y_loc, int pref_ahead) {
   constexpr int D = C::D, NS = C::NS, NF = C::NF, L = C::L, LF = C::LF, BS = C::BS, LTR = C::LTR, n = C::n;
-  constexpr int NLOC = C::NLOC, NQ = C::NQ, NLOCF = C::NLOCF, NQF = C::NQF, NTRI = C::NTRI;
+  constexpr int NLOC = C::NLOC, NQ = C::NQ, NLOCF = C::NLOCF, NQF = C::NQF, NTRI = C::NTRI, NSUB = C::NSUB;
+  static_assert(LTR <= NCONS, "one local trace entry per consumer thread");
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES];
   __shared__ Piece pieces[MAXP];
   __shared__ int npieces;
+  using S = SSm<C>;
+  using TS = TSm<C>;
   double* ring = smem;
   double* W = smem + STAGES * ST_DBL;
-  using S = SSm<C>;
+  double* Td = W + S::total;
+  int* Ti = reinterpret_cast<int*>(Td + TS::ndbl);
+  double* Gc = Td + TS::total;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const long long PK = ti_size(n);
 
@@ -207,18 +287,44 @@ __global__ void __launch_bounds__(NCONS + 32) k_apply_stream(mhdg_disc g, mhdg_b
     }
     fence_mbar_init();
     // the piece schedule is identical for every macro: build it once
-    Sched<C> sc;
+    Sched<C, PART> sc;
     int np = 0;
     while (np < MAXP && sc.next(pieces[np])) ++np;
     npieces = np;
+  }
+  {  // reference tables -> shared memory
+    const int nt = blockDim.x;
+    for (int i = tid; i < NQ * NLOC; i += nt) Td[TS::phi_vol + i] = g.phi_vol[i];
+    for (int i = tid; i < NQF * NLOCF; i += nt) Td[TS::phi_face + i] = g.phi_face[i];
+    for (int i = tid; i < NSUB * NLOC; i += nt) {
+      Ti[TS::sub_conn + i] = g.sub_conn[i];
+      Ti[TS::vn_sub + i] = g.vn_sub[i];
+    }
+    for (int i = tid; i < NTRI * NLOCF; i += nt) {
+      Ti[TS::tri_conn + i] = g.tri_conn[i];
+      Ti[TS::fn_ent + i] = g.fn_ent[i];
+    }
+    for (int i = tid; i < NF * LF; i += nt) {
+      Ti[TS::fvn + i] = g.face_vol_nodes[i];
+      Ti[TS::vf_ent + i] = g.vf_ent[i];
+    }
+    for (int i = tid; i < L; i += nt) Ti[TS::n2f + i] = g.node_to_face[i];
+    for (int i = tid; i <= L; i += nt) {
+      Ti[TS::vf_ptr + i] = g.vf_ptr[i];
+      Ti[TS::vn_ptr + i] = g.vn_ptr[i];
+    }
+    for (int i = tid; i <= LF; i += nt) Ti[TS::fn_ptr + i] = g.fn_ptr[i];
+    for (int i = tid; i < NSUB; i += nt) Ti[TS::gcls_of + i] = g.grad_cls_of[i];
+    if (PART != 2)
+      for (int i = tid; i < g.n_grad_cls * TS::CLS; i += nt) Gc[i] = g.grad_cls[i];
   }
   __syncthreads();
   const int np = npieces;
 
   // ----------------------------- producer ---------------------------------
-  // One thread walks the (macro, piece) sequence twice: a prefetch cursor
-  // pulls pieces from HBM into L2 up to PREF_AHEAD pieces ahead, and the copy
-  // cursor moves them L2 -> shared ring stage once the consumers free it.
+  // One thread walks the (macro, piece) sequence: an optional prefetch cursor
+  // pulls pieces from HBM into L2 pref_ahead pieces ahead, and the copy
+  // cursor moves them into the shared ring once the consumers free a stage.
   if (warp == NWARP_C) {
     if (lane == 0) {
       auto src_of = [&](int mac, const Piece& p) -> const double* {
@@ -231,6 +337,8 @@ __global__ void __launch_bounds__(NCONS + 32) k_apply_stream(mhdg_disc g, mhdg_b
           case K_WV: return bk.wdgdq_vol + (size_t)mac * C::NPV * C::NW + p.off;
           case K_WFZ:
           case K_WF2: return bk.wdgdq_face + (size_t)mac * C::NPF * C::NWF + p.off;
+          case K_Y2: return Work<C>::y2(fac.work, g.n_mac, mac);
+          case K_FC: return Work<C>::fc(fac.work, g.n_mac, mac);
           default: return fac.lu + (size_t)mac * PK + p.off;  // S^-1 tiles
         }
       };
@@ -240,7 +348,6 @@ __global__ void __launch_bounds__(NCONS + 32) k_apply_stream(mhdg_disc g, mhdg_b
         for (int pi = 0; pi < np; ++pi) {
           const Piece& p = pieces[pi];
           const int s = it % STAGES;
-          // keep the prefetch cursor PREF_AHEAD pieces ahead of the copy cursor
           while (pref < it + pref_ahead && pm < g.n_mac) {
             const Piece& q = pieces[pp];
             if (q.kind != K_GF && q.kind != K_MD && q.cnt) bulk_prefetch_l2(src_of(pm, q), (uint32_t)q.cnt * 8u);
@@ -261,10 +368,18 @@ __global__ void __launch_bounds__(NCONS + 32) k_apply_stream(mhdg_disc g, mhdg_b
   // ----------------------------- consumers --------------------------------
   double *xl = W + S::xl, *z = W + S::z, *y = W + S::y, *t = W + S::t, *rfst = W + S::rfst, *ftt = W + S::ftt,
          *fts = W + S::fts, *cfgz = W + S::cfgz, *yf = W + S::yf, *wfz = W + S::wfz, *wf2 = W + S::wf2,
-         *vv = W + S::vv, *cv = W + S::cv, *tg = W + S::tg, *tp = W + S::tp;
-  double* wv = tg;   // W_vol contraction results, lifetime: W_vol pieces .. LU start
+         *vv = W + S::vv, *cv = W + S::cv, *tg = W + S::tg;
+  const double *phs = Td + TS::phi_vol, *pfs = Td + TS::phi_face;
+  const int *conn = Ti + TS::sub_conn, *tconn = Ti + TS::tri_conn, *fvn = Ti + TS::fvn, *n2f = Ti + TS::n2f,
+            *fnp = Ti + TS::fn_ptr, *fne = Ti + TS::fn_ent, *vfp = Ti + TS::vf_ptr, *vfe = Ti + TS::vf_ent,
+            *vnp = Ti + TS::vn_ptr, *vns = Ti + TS::vn_sub, *gco = Ti + TS::gcls_of;
+  double* wv = tg;   // W_vol contraction results, lifetime: W_vol pieces .. y1
   double* z2 = z;    // z is dead once the W_face(z) pieces are consumed
   double* vw = vv + warp * 32;  // warp-private scratch
+  // this thread's trace entry of the next macro, gathered one macro ahead
+  double x_next = 0.0;
+  if (PART != 2 && tid < LTR && blockIdx.x < g.n_mac)
+    x_next = __ldg(x + __ldg(g.gather + (size_t)blockIdx.x * LTR + tid));
   int it = 0;
   for (int mac = blockIdx.x; mac < g.n_mac; mac += gridDim.x) {
     double ij[D][D];
@@ -272,9 +387,65 @@ __global__ void __launch_bounds__(NCONS + 32) k_apply_stream(mhdg_disc g, mhdg_b
     for (int a = 0; a < D; ++a)
 #pragma unroll
       for (int b = 0; b < D; ++b) ij[a][b] = __ldg(g.inv_jac + (size_t)mac * D * D + a * D + b);
-    double siacc = 0.0;  // per-lane partial of S^-1 y1 for the rows this lane owns
-    for (int i = tid; i < LTR; i += NCONS) xl[i] = __ldg(x + __ldg(g.gather + (size_t)mac * LTR + i));
+    double sc_mine = 0.0;  // trace_face_scale of this thread's face in the final sum
+    if (PART != 1 && tid < LTR) sc_mine = __ldg(bk.trace_face_scale + mac * NF + tid / BS);
+    double siacc = 0.0;  // per-lane partial of S^-1 y1 for the rows this lane owns (fused apply)
+    PROF_T(t_start);
+    if (PART != 2 && tid < LTR) {
+      xl[tid] = x_next;
+      const int nm = mac + gridDim.x;
+      if (nm < g.n_mac) x_next = __ldg(x + __ldg(g.gather + (size_t)nm * LTR + tid));
+    }
     cbar();
+    if (tid == 0) { PROF_ADD(13, 2, t_start); }
+
+    // y1 = -A_uh x + A_uq z (needs rfst, the W_vol results, the W_face(z) stash);
+    // leaves y1 in y and the face term g = A_hq z / scale in cfgz
+    auto make_y1 = [&]() {
+      // cv[K][a][s] = sum_q sum_k gphys[K,q,a,k] w[K,q][k][s], gphys = grad_ref[K] inv_jac
+      for (int idx = tid; idx < NSUB * NLOC * NS; idx += NCONS) {
+        const int s = idx % NS, a = (idx / NS) % NLOC, K = idx / (NS * NLOC);
+        const double* G = Gc + gco[K] * TS::CLS;
+        double acc = 0.0;
+#pragma unroll 4
+        for (int q = 0; q < NQ; ++q) {
+          const double* gr = G + (q * NLOC + a) * D;
+          const double* w = wv + (K * NQ + q) * D * NS + s;
+          double grv[D];
+#pragma unroll
+          for (int r2 = 0; r2 < D; ++r2) grv[r2] = gr[r2];
+#pragma unroll
+          for (int k = 0; k < D; ++k) {
+            double gp = 0.0;
+#pragma unroll
+            for (int r2 = 0; r2 < D; ++r2) gp += grv[r2] * ij[r2][k];
+            acc += gp * w[k * NS];
+          }
+        }
+        cv[idx] = acc;
+      }
+      for (int idx = tid; idx < LTR; idx += NCONS) {
+        const int s = idx % NS, gg = (idx / NS) % LF, f = idx / BS;
+        double acc = 0.0;
+        for (int e = fnp[gg]; e < fnp[gg + 1]; ++e) {
+          const int ent = fne[e], T = ent / NLOCF, a = ent % NLOCF;
+          const double* w = wfz + ((f * NTRI + T) * NQF) * NS + s;
+#pragma unroll
+          for (int q = 0; q < NQF; ++q) acc += pfs[q * NLOCF + a] * w[q * NS];
+        }
+        cfgz[idx] = acc;
+      }
+      cbar();
+      for (int idx = tid; idx < n; idx += NCONS) {
+        const int I = idx / NS, s = idx % NS;
+        double st = 0.0, sg = 0.0;
+        for (int e = vfp[I]; e < vfp[I + 1]; ++e) st += rfst[vfe[e] * NS + s];
+        for (int e = vnp[I]; e < vnp[I + 1]; ++e) sg -= cv[vns[e] * NS + s];
+        for (int e = vfp[I]; e < vfp[I + 1]; ++e) sg += cfgz[vfe[e] * NS + s];
+        y[idx] = -st + sg;
+      }
+      cbar();
+    };
 
     int prev = -1;
     for (int pi = 0; pi < np; ++pi) {
@@ -284,7 +455,7 @@ __global__ void __launch_bounds__(NCONS + 32) k_apply_stream(mhdg_disc g, mhdg_b
       if (p.kind != prev) {
         cbar();  // every warp has finished the previous kind
         if (p.kind == K_FST) {
-          // z = A_qq^-1 A_qh x = -(fac/det) sum_f area_f n_f (Gf x_f); then cv <- 0 (aliases tg)
+          // z = A_qq^-1 A_qh x = -(fac/det) sum_f area_f n_f (Gf x_f)
           const double idet = 1.0 / __ldg(g.det + mac);
           double cfl[NF][D];
 #pragma unroll
@@ -306,56 +477,16 @@ __global__ void __launch_bounds__(NCONS + 32) k_apply_stream(mhdg_disc g, mhdg_b
           }
           cbar();
         } else if (p.kind == K_SI) {
-          // y1 = -A_uh x + A_uq z
-          // cv[K][a][s] = sum_q sum_k gphys[K,q,a,k] w[K,q][k][s]
-          for (int idx = tid; idx < C::NSUB * NLOC * NS; idx += NCONS) {
-            const int s = idx % NS, a = (idx / NS) % NLOC, K = idx / (NS * NLOC);
-            double acc = 0.0;
-#pragma unroll 4
-            for (int q = 0; q < NQ; ++q) {
-              const double* gr = g.grad_ref + ((K * NQ + q) * NLOC + a) * D;
-              const double* w = wv + (K * NQ + q) * D * NS + s;
-              double grv[D];
-#pragma unroll
-              for (int r2 = 0; r2 < D; ++r2) grv[r2] = __ldg(gr + r2);
-#pragma unroll
-              for (int k = 0; k < D; ++k) {
-                double gp = 0.0;
-#pragma unroll
-                for (int r2 = 0; r2 < D; ++r2) gp += grv[r2] * ij[r2][k];
-                acc += gp * w[k * NS];
-              }
-            }
-            cv[idx] = acc;
-          }
-          for (int idx = tid; idx < LTR; idx += NCONS) {
-            const int s = idx % NS, gg = (idx / NS) % LF, f = idx / BS;
-            double acc = 0.0;
-            for (int e = __ldg(g.fn_ptr + gg); e < __ldg(g.fn_ptr + gg + 1); ++e) {
-              const int ent = __ldg(g.fn_ent + e), T = ent / NLOCF, a = ent % NLOCF;
-              const double* w = wfz + ((f * NTRI + T) * NQF) * NS + s;
-#pragma unroll
-              for (int q = 0; q < NQF; ++q) acc += __ldg(g.phi_face + q * NLOCF + a) * w[q * NS];
-            }
-            cfgz[idx] = acc;
-          }
-          cbar();
-          for (int idx = tid; idx < n; idx += NCONS) {
-            const int I = idx / NS, s = idx % NS;
-            double st = 0.0, sg = 0.0;
-            for (int e = __ldg(g.vf_ptr + I); e < __ldg(g.vf_ptr + I + 1); ++e) st += rfst[__ldg(g.vf_ent + e) * NS + s];
-            for (int e = __ldg(g.vn_ptr + I); e < __ldg(g.vn_ptr + I + 1); ++e) sg -= cv[__ldg(g.vn_sub + e) * NS + s];
-            for (int e = __ldg(g.vf_ptr + I); e < __ldg(g.vf_ptr + I + 1); ++e) sg += cfgz[__ldg(g.vf_ent + e) * NS + s];
-            y[idx] = -st + sg;
-          }
-          cbar();
+          make_y1();
         } else if (p.kind == K_MD) {
-          // y <- y2 = S^-1 y1 (held in t); y2 restricted to the face nodes, for A_hu
-          for (int i = tid; i < n; i += NCONS) y[i] = t[i];
-          cbar();
+          if (PART == 0) {  // y <- y2 = S^-1 y1 (held in t); the post kernel gets y2 as a piece
+            for (int i = tid; i < n; i += NCONS) y[i] = t[i];
+            cbar();
+          }
+          // y2 restricted to the face nodes, for A_hu
           for (int idx = tid; idx < LTR; idx += NCONS) {
             const int s = idx % NS, h = (idx / NS) % LF, f = idx / BS;
-            yf[idx] = y[__ldg(g.face_vol_nodes + f * LF + h) * NS + s];
+            yf[idx] = y[fvn[f * LF + h] * NS + s];
           }
         } else if (p.kind == K_WF2) {
           // z2 = A_qq^-1 A_qu y2 = sum_r inv_jac[r][l] (M^-1 D_r y2), at the face nodes only
@@ -387,6 +518,17 @@ __global__ void __launch_bounds__(NCONS + 32) k_apply_stream(mhdg_disc g, mhdg_b
 
       // ---------------- consume ----------------
       switch (p.kind) {
+        case K_Y2: {
+          for (int i = tid; i < n; i += NCONS) y[i] = A[i];
+          break;
+        }
+        case K_FC: {
+          for (int i = tid; i < LTR; i += NCONS) {
+            ftt[i] = A[i];
+            cfgz[i] = A[LTR + i];
+          }
+          break;
+        }
         case K_GF: {  // tg[f][I][s] = sum_h Gf[f][I][h] x[f][h][s]
           for (int idx = tid; idx < p.nu * NS; idx += NCONS) {
             const int s = idx % NS, rl = idx / NS, row = p.u0 + rl, f = row / L;
@@ -399,27 +541,22 @@ __global__ void __launch_bounds__(NCONS + 32) k_apply_stream(mhdg_disc g, mhdg_b
           }
           break;
         }
-        case K_MD: {  // tg[r][i][s] = sum_J (M^-1 D_r)[fnode_i][J] y2[J][s], face nodes only
-          constexpr int LPR = 8, RPW = 32 / LPR;
-          const int sub = lane / LPR, l = lane % LPR;
-          for (int r0 = warp * RPW; r0 < p.nu; r0 += NWARP_C * RPW) {
-            const int rl = r0 + sub;
-            double acc[NS] = {};
-            if (rl < p.nu) {
-              const double* a = A + rl * L;
-              for (int J = l; J < L; J += LPR) {
-                const double m = a[J];
-#pragma unroll
-                for (int s = 0; s < NS; ++s) acc[s] += m * y[J * NS + s];
+        case K_MD: {  // tg[r][i][s] = sum_J (M^-1 D_r)[fnode_i][J] y2[J][s]: lane = (row, s)
+          constexpr int RPW = 32 / NS;
+          const int rr = lane / NS, s = lane % NS;
+          const int g1 = (p.u0 + p.nu - 1) / RPW;
+          for (int gg = first_group(p.u0 / RPW, warp); gg <= g1; gg += NWARP_C) {
+            const int row = gg * RPW + rr;
+            if (rr < RPW && row >= p.u0 && row < p.u0 + p.nu) {
+              const double* a = A + (row - p.u0) * L;
+              double a0 = 0.0, a1 = 0.0;
+#pragma unroll 4
+              for (int J = 0; J + 1 < L; J += 2) {
+                a0 += a[J] * y[J * NS + s];
+                a1 += a[J + 1] * y[(J + 1) * NS + s];
               }
-            }
-#pragma unroll
-            for (int s = 0; s < NS; ++s)
-#pragma unroll
-              for (int o = LPR / 2; o > 0; o >>= 1) acc[s] += __shfl_xor_sync(MHDG_FULL, acc[s], o);
-            if (l == 0 && rl < p.nu) {
-#pragma unroll
-              for (int s = 0; s < NS; ++s) tg[(p.u0 + rl) * NS + s] = acc[s];
+              if (L & 1) a0 += a[L - 1] * y[(L - 1) * NS + s];
+              tg[row * NS + s] = a0 + a1;
             }
           }
           break;
@@ -430,36 +567,38 @@ __global__ void __launch_bounds__(NCONS + 32) k_apply_stream(mhdg_disc g, mhdg_b
           const double* vec = p.kind == K_FTS ? yf : xl;
           double* out = p.kind == K_FST ? rfst : p.kind == K_FTT ? ftt : fts;
           const int u0 = p.u0;
-          rows_dot<4>(A, p.nu, BS, [&](int rl) { return vec + ((u0 + rl) / BS) * BS; },
+          rows_dot<4>(A, u0, p.nu, BS, [&](int rl) { return vec + ((u0 + rl) / BS) * BS; },
                       [&](int rl, double acc) { out[u0 + rl] = acc; });
           break;
         }
-        case K_WV: {  // warp-local: each warp its own points, PPI points per pass
+        case K_WV: {  // point groups of PPI points per warp pass, dealt to warps by global index
           constexpr int DN = D * NS, PPI = 32 / DN;
-          const int per = (p.nu + NWARP_C - 1) / NWARP_C;
-          const int pbeg = warp * per, pend = min(p.nu, pbeg + per);
           const int pi = lane / DN, j = lane % DN;
-          for (int pl0 = pbeg; pl0 < pend; pl0 += PPI) {
-            const int pl = pl0 + pi;
-            const bool on = pi < PPI && pl < pend;
-            if (on) {
+          const int ngrp = (p.nu + PPI - 1) / PPI;
+          for (int grp = first_group(p.u0 / PPI, warp) - p.u0 / PPI; grp < ngrp; grp += NWARP_C) {
+            const int pl = grp * PPI + pi;
+            const bool on = pi < PPI && pl < p.nu;
+            if (on) {  // v[l][tt] = sum_b phi[q][b] z[l][conn[K][b]][tt]
               const int tt = j % NS, l = j / NS, pt = p.u0 + pl, K = pt / NQ, q = pt % NQ;
               double a = 0.0;
 #pragma unroll
-              for (int b = 0; b < NLOC; ++b)
-                a += __ldg(g.phi_vol + q * NLOC + b) * z[(l * L + __ldg(g.sub_conn + K * NLOC + b)) * NS + tt];
+              for (int b = 0; b < NLOC; ++b) a += phs[q * NLOC + b] * z[(l * L + conn[K * NLOC + b]) * NS + tt];
               vw[pi * DN + j] = a;
             }
             __syncwarp();
-            if (on) {
+            if (on) {  // out[k][s] = sum_{l,tt} W[k][l][s][tt] v[l][tt], (l, tt) order rotated per lane
               const int s = j % NS, k = j / NS;
               const double* w = A + pl * C::NW + k * D * NS * NS + s * NS;
               const double* v = vw + pi * DN;
+              const int rot = (pi * D + k) % DN;
               double a = 0.0;
 #pragma unroll
-              for (int l = 0; l < D; ++l)
-#pragma unroll
-                for (int tt = 0; tt < NS; ++tt) a += w[l * NS * NS + tt] * v[l * NS + tt];
+              for (int i = 0; i < DN; ++i) {
+                int ii = i + rot;
+                if (ii >= DN) ii -= DN;
+                const int l = ii / NS, tt = ii - l * NS;
+                a += w[l * NS * NS + tt] * v[ii];
+              }
               wv[(p.u0 + pl) * DN + j] = a;
             }
             __syncwarp();
@@ -467,27 +606,26 @@ __global__ void __launch_bounds__(NCONS + 32) k_apply_stream(mhdg_disc g, mhdg_b
           break;
         }
         case K_WFZ:
-        case K_WF2: {  // warp-local, as K_WV
+        case K_WF2: {  // as K_WV, on the face stash
           constexpr int DN = D * NS, PPI = 32 / DN;
           const bool second = p.kind == K_WF2;
           const double* zs = second ? z2 : z;
           const int lstride = second ? C::NFN : L;
-          double* wf = p.kind == K_WFZ ? wfz : wf2;
-          const int per = (p.nu + NWARP_C - 1) / NWARP_C;
-          const int pbeg = warp * per, pend = min(p.nu, pbeg + per);
+          double* wf = second ? wf2 : wfz;
           const int pi = lane / DN, j = lane % DN;
-          for (int pl0 = pbeg; pl0 < pend; pl0 += PPI) {
-            const int pl = pl0 + pi;
-            const bool on = pi < PPI && pl < pend;
+          const int ngrp = (p.nu + PPI - 1) / PPI;
+          for (int grp = first_group(p.u0 / PPI, warp) - p.u0 / PPI; grp < ngrp; grp += NWARP_C) {
+            const int pl = grp * PPI + pi;
+            const bool on = pi < PPI && pl < p.nu;
             if (on) {
               const int tt = j % NS, l = j / NS;
               const int pf = p.u0 + pl, q = pf % NQF, T = (pf / NQF) % NTRI, f = pf / (NQF * NTRI);
               double a = 0.0;
 #pragma unroll
               for (int b = 0; b < NLOCF; ++b) {
-                int node = __ldg(g.face_vol_nodes + f * LF + __ldg(g.tri_conn + T * NLOCF + b));
-                if (second) node = __ldg(g.node_to_face + node);
-                a += __ldg(g.phi_face + q * NLOCF + b) * zs[(l * lstride + node) * NS + tt];
+                int node = fvn[f * LF + tconn[T * NLOCF + b]];
+                if (second) node = n2f[node];
+                a += pfs[q * NLOCF + b] * zs[(l * lstride + node) * NS + tt];
               }
               vw[pi * DN + j] = a;
             }
@@ -507,26 +645,28 @@ __global__ void __launch_bounds__(NCONS + 32) k_apply_stream(mhdg_disc g, mhdg_b
           }
           break;
         }
-        case K_SI: {  // one column tile of a row block; warp w owns rows 8w..8w+7 of every block
+        case K_SI: {  // one column tile of a row block; warp w owns rows SRW*w .. SRW*w+SRW-1 of every block
+          constexpr int SRW = TI_RB / NWARP_C, SLR = 32 / SRW;  // rows per warp, lanes per row
+          static_assert(SRW * NWARP_C == TI_RB && SRW * SLR == 32, "S^-1 tile mapping");
           const int nb = ti_rows(n, p.blk), w = p.nu, c0 = p.u0;
-          const int r = 8 * warp + (lane >> 2), l = lane & 3;
+          const int r = SRW * warp + lane / SLR, l = lane % SLR;
           if (c0 == 0) siacc = 0.0;
           if (r < nb) {
             const double* a = A + r * w;
             const double* yv = y + c0;
             double a0 = 0.0, a1 = 0.0;
 #pragma unroll
-            for (int k = 0; k < TI_CW / 4; k += 2) {
-              const int c = l + 4 * k;
+            for (int k = 0; k < TI_CW / SLR; k += 2) {
+              const int c = l + SLR * k;
               if (c < w) a0 += a[c] * yv[c];
-              if (c + 4 < w) a1 += a[c + 4] * yv[c + 4];
+              if (c + SLR < w) a1 += a[c + SLR] * yv[c + SLR];
             }
             siacc += a0 + a1;
           }
-          if (c0 + w == n) {  // last tile of the block: reduce over the row's 4 lanes
+          if (c0 + w == n) {  // last tile of the block: reduce over the row's SLR lanes
             double acc = siacc;
-            acc += __shfl_xor_sync(MHDG_FULL, acc, 2);
-            acc += __shfl_xor_sync(MHDG_FULL, acc, 1);
+#pragma unroll
+            for (int o = SLR / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(MHDG_FULL, acc, o);
             if (l == 0 && r < nb) t[p.blk * TI_RB + r] = acc;
           }
           break;
@@ -540,22 +680,148 @@ __global__ void __launch_bounds__(NCONS + 32) k_apply_stream(mhdg_disc g, mhdg_b
     }
     PROF_T(t_end);
     cbar();
+    if (PART == 1) {  // pre part: hand y1 and the face terms to the S^-1 stream / post kernels
+      PROF_T(t_y1);
+      make_y1();
+      if (tid == 0) { PROF_ADD(14, 1, t_y1); }
+      PROF_T(t_wb);
+      double* y1g = Work<C>::y1(fac.work, mac);
+      for (int i = tid; i < n; i += NCONS) y1g[i] = y[i];
+      double* fc = Work<C>::fc(fac.work, g.n_mac, mac);
+      if (tid < LTR) {
+        fc[tid] = ftt[tid];
+        fc[LTR + tid] = cfgz[tid];
+      }
+      cbar();
+      if (tid == 0) { PROF_ADD(15, 2, t_wb); }
+      continue;
+    }
 
     // y4 = ((A_hu y2 - A_hq z2) + A_hh x) - A_hq z, with -A_hq z = scale * cfg
-    for (int idx = tid; idx < LTR; idx += NCONS) {
-      const int s = idx % NS, gg = (idx / NS) % LF, f = idx / BS;
+    if (tid < LTR) {
+      const int idx = tid, s = idx % NS, gg = (idx / NS) % LF, f = idx / BS;
       double acc = 0.0;
-      for (int e = __ldg(g.fn_ptr + gg); e < __ldg(g.fn_ptr + gg + 1); ++e) {
-        const int ent = __ldg(g.fn_ent + e), T = ent / NLOCF, a = ent % NLOCF;
+      for (int e = fnp[gg]; e < fnp[gg + 1]; ++e) {
+        const int ent = fne[e], T = ent / NLOCF, a = ent % NLOCF;
         const double* w = wf2 + ((f * NTRI + T) * NQF) * NS + s;
 #pragma unroll
-        for (int q = 0; q < NQF; ++q) acc += __ldg(g.phi_face + q * NLOCF + a) * w[q * NS];
+        for (int q = 0; q < NQF; ++q) acc += pfs[q * NLOCF + a] * w[q * NS];
       }
-      const double sc = __ldg(bk.trace_face_scale + mac * NF + f);
-      y_loc[(size_t)mac * LTR + idx] = ((fts[idx] + sc * acc) + ftt[idx]) + sc * cfgz[idx];
+      y_loc[(size_t)mac * LTR + idx] = ((fts[idx] + sc_mine * acc) + ftt[idx]) + sc_mine * cfgz[idx];
     }
     cbar();
     if (tid == 0) { PROF_ADD(12, 2, t_end); }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// S^-1 stream (split apply, middle kernel): y2 = S^-1 y1 for every macro.
+//
+// Pure streaming batched GEMV over the tiled inverse (tiled_inv.cuh): 76% of
+// the apply's bytes at C2 and no other work, so it runs with several CTAs per
+// SM and a TMA ring each.  Work units are (macro, 64-row block) pairs, split
+// contiguously across CTAs so consecutive units share the macro and y1 is
+// fetched once per macro (as the first ring piece).  Consumer mapping: warp w
+// owns rows SRW*w .. SRW*w+SRW-1 of the block, lane l column c0+l of every
+// tile: the lanes of one row read 32 consecutive doubles (conflict-free) and
+// each lane reads y once per tile; partial sums stay in registers across the
+// block's tiles and are reduced across lanes once per unit.
+// ---------------------------------------------------------------------------
+template <class C, int STAGES, int NCT>
+__global__ void __launch_bounds__(NCT + 32) k_si_stream(int n_mac, const double* __restrict__ inv,
+                                                       double* __restrict__ work) {
+  constexpr int n = C::n, NP = ceven(n), NBLK = C::NBLK, NT = (n + TI_CW - 1) / TI_CW;
+  constexpr int NW = NCT / 32, SRW = TI_RB / NW;
+  static_assert(SRW * NW == TI_RB && TI_CW == 32, "S^-1 stream mapping");
+  static_assert(NP <= ST_DBL, "y1 must fit one ring stage");
+  extern __shared__ __align__(128) double smem[];
+  __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES];
+  double* ring = smem;
+  double* ybuf = smem + STAGES * ST_DBL;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const long long PK = ti_size(n);
+  const long long U = (long long)n_mac * NBLK;
+  const long long u0 = U * blockIdx.x / gridDim.x, u1 = U * (blockIdx.x + 1) / gridDim.x;
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], NW);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == NW) {  // producer: y1 of each new macro, then the block's column tiles
+    if (lane == 0) {
+      int it = 0, cur = -1;
+      for (long long u = u0; u < u1; ++u) {
+        const int mac = (int)(u / NBLK), b = (int)(u % NBLK), nb = ti_rows(n, b);
+        const bool fresh = mac != cur;
+        for (int k = fresh ? -1 : 0; k < NT; ++k) {
+          const int s = it % STAGES;
+          if (it >= STAGES) mbar_wait(&empty_bar[s], ((it / STAGES) + 1) & 1);
+          const double* src;
+          uint32_t bytes;
+          if (k < 0) {
+            src = Work<C>::y1(work, mac);
+            bytes = NP * 8u;
+          } else {
+            const int w = (n - k * TI_CW) < TI_CW ? n - k * TI_CW : TI_CW;
+            src = inv + (size_t)mac * PK + ti_block_off(n, b) + (long long)k * nb * TI_CW;
+            bytes = (uint32_t)ti_even((long long)nb * w) * 8u;
+          }
+          mbar_arrive_expect_tx(&full_bar[s], bytes);
+          bulk_g2s(ring + s * ST_DBL, src, bytes, &full_bar[s]);
+          ++it;
+        }
+        cur = mac;
+      }
+    }
+    return;
+  }
+
+  int it = 0, cur = -1;
+  for (long long u = u0; u < u1; ++u) {
+    const int mac = (int)(u / NBLK), b = (int)(u % NBLK), nb = ti_rows(n, b);
+    if (mac != cur) {
+      named_bar(1, NCT);  // every warp is done with the previous macro's y1
+      const int s = it % STAGES;
+      mbar_wait(&full_bar[s], (it / STAGES) & 1);
+      for (int i = tid; i < NP; i += NCT) ybuf[i] = ring[s * ST_DBL + i];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar[s]);
+      ++it;
+      named_bar(1, NCT);
+      cur = mac;
+    }
+    double acc[SRW];
+#pragma unroll
+    for (int j = 0; j < SRW; ++j) acc[j] = 0.0;
+    const int r0 = SRW * warp;
+#pragma unroll 1
+    for (int k = 0; k < NT; ++k) {
+      const int s = it % STAGES;
+      const int c0 = k * TI_CW, w = (n - c0) < TI_CW ? n - c0 : TI_CW;
+      mbar_wait(&full_bar[s], (it / STAGES) & 1);
+      const double* A = ring + s * ST_DBL;
+      if (lane < w) {
+        const double yv = ybuf[c0 + lane];
+#pragma unroll
+        for (int j = 0; j < SRW; ++j)
+          if (r0 + j < nb) acc[j] += A[(r0 + j) * w + lane] * yv;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar[s]);
+      ++it;
+    }
+    double* y2 = Work<C>::y2(work, n_mac, mac) + b * TI_RB;
+#pragma unroll
+    for (int j = 0; j < SRW; ++j) {
+      double v = acc[j];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(MHDG_FULL, v, o);
+      if (lane == j && r0 + j < nb) y2[r0 + j] = v;
+    }
   }
 }
 
@@ -570,7 +836,7 @@ extern "C" int mhdg_stream_grid(void) { return g_stream_grid; }
 
 template <class C>
 static int count_pieces() {
-  Sched<C> sc;
+  Sched<C, 0> sc;
   Piece p;
   int k = 0;
   while (sc.next(p)) ++k;
@@ -588,15 +854,26 @@ static bool stream_ok(const mhdg_disc& g, const mhdg_blocks& b, const mhdg_facto
   auto al = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
   const bool sizes = ((C::NF * C::BS * C::BS) % 2 == 0) && ((C::NPV * C::NW) % 2 == 0) &&
                      ((C::NPF * C::NWF) % 2 == 0);
-  return sizes && al(b.face_state_trace) && al(b.face_trace_trace) && al(b.face_trace_state) && al(b.wdgdq_vol) &&
-         al(b.wdgdq_face) && al(f.lu);
+  const bool tables = g.n_grad_cls >= 1 && g.grad_cls && g.grad_cls_of && g.node_to_face && g.minv_d_face &&
+                      g.n_face_nodes == C::NFN;
+  const size_t smem = sizeof(double) * ((size_t)MHDG_STAGES * ST_DBL + SSm<C>::total + TSm<C>::total +
+                                        (size_t)g.n_grad_cls * TSm<C>::CLS);
+  return sizes && tables && smem <= 227 * 1024 && al(b.face_state_trace) && al(b.face_trace_trace) &&
+         al(b.face_trace_state) && al(b.wdgdq_vol) && al(b.wdgdq_face) && al(f.lu) && al(f.work);
 }
 
-template <class C, int STAGES>
+template <class C, int STAGES, int PART>
+static size_t stream_smem(const mhdg_disc& g) {
+  return sizeof(double) * ((size_t)STAGES * ST_DBL + SSm<C>::total + TSm<C>::total +
+                           (PART != 2 ? (size_t)g.n_grad_cls * TSm<C>::CLS : 0));
+}
+
+template <class C, int STAGES, int PART>
 static int launch_stream(const mhdg_disc& g, const mhdg_blocks& b, const mhdg_factors& f, const double* x,
                          double* y_loc, cudaStream_t st) {
-  const size_t bytes = sizeof(double) * ((size_t)STAGES * ST_DBL + SSm<C>::total);
-  auto kern = k_apply_stream<C, STAGES>;
+  const size_t bytes = stream_smem<C, STAGES, PART>(g);
+  if (bytes > 227 * 1024) return MHDG_ERR_CONFIG;
+  auto kern = k_apply_stream<C, STAGES, PART>;
   static int ctas = 0;
   if (!ctas) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
@@ -610,6 +887,48 @@ static int launch_stream(const mhdg_disc& g, const mhdg_blocks& b, const mhdg_fa
   g_stream_grid = grid;
   kern<<<grid, NCONS + 32, bytes, st>>>(g, b, f, x, y_loc, g_pref_ahead);
   return launch_ok();
+}
+
+#ifndef MHDG_SI_STAGES
+#define MHDG_SI_STAGES 3
+#endif
+#ifndef MHDG_SI_NCT
+#define MHDG_SI_NCT 256
+#endif
+
+template <class C>
+static int launch_si(const mhdg_disc& g, const mhdg_factors& f, cudaStream_t st) {
+  constexpr int STG = MHDG_SI_STAGES, NCT = MHDG_SI_NCT;
+  const size_t bytes = sizeof(double) * ((size_t)STG * ST_DBL + ceven(C::n));
+  auto kern = k_si_stream<C, STG, NCT>;
+  static int ctas = 0;
+  if (!ctas) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, NCT + 32, bytes);
+    ctas = sms * (per > 0 ? per : 1);
+  }
+  const long long units = (long long)g.n_mac * C::NBLK;
+  const int grid = units < ctas ? (int)units : ctas;
+  kern<<<grid, NCT + 32, bytes, st>>>(g.n_mac, f.lu, f.work);
+  return launch_ok();
+}
+
+static int g_split = 1;
+extern "C" void mhdg_set_apply_split(int on) { g_split = on; }
+
+// split apply: pre (y1, face terms) -> S^-1 stream (y2) -> post (y_loc)
+template <class C>
+static int launch_apply(const mhdg_disc& g, const mhdg_blocks& b, const mhdg_factors& f, const double* x,
+                        double* y_loc, cudaStream_t st) {
+  if (!f.work || !g_split) return launch_stream<C, MHDG_STAGES, 0>(g, b, f, x, y_loc, st);
+  int rc = launch_stream<C, MHDG_STAGES, 1>(g, b, f, x, y_loc, st);
+  if (rc) return rc;
+  rc = launch_si<C>(g, f, st);
+  if (rc) return rc;
+  return launch_stream<C, MHDG_STAGES, 2>(g, b, f, x, y_loc, st);
 }
 
 #ifdef MHDG_STREAM_PROFILE
@@ -626,11 +945,11 @@ extern "C" int mhdg_stream_profile(unsigned long long* out, int reset) {
 // returns -1 when no streamed instantiation matches (caller uses k_apply_local)
 int apply_stream(const mhdg_disc& g, const mhdg_blocks& b, const mhdg_factors& f, const double* x, double* y_loc,
                  cudaStream_t st) {
-  if (stream_ok<Cfg<2, 4, 3>>(g, b, f)) return launch_stream<Cfg<2, 4, 3>, 3>(g, b, f, x, y_loc, st);
-  if (stream_ok<Cfg<2, 2, 2>>(g, b, f)) return launch_stream<Cfg<2, 2, 2>, 3>(g, b, f, x, y_loc, st);
-  if (stream_ok<Cfg<3, 2, 2>>(g, b, f)) return launch_stream<Cfg<3, 2, 2>, 3>(g, b, f, x, y_loc, st);
-  if (stream_ok<Cfg<3, 1, 2>>(g, b, f)) return launch_stream<Cfg<3, 1, 2>, 3>(g, b, f, x, y_loc, st);
-  if (stream_ok<Cfg<3, 2, 1>>(g, b, f)) return launch_stream<Cfg<3, 2, 1>, 3>(g, b, f, x, y_loc, st);
+  if (stream_ok<Cfg<2, 4, 3>>(g, b, f)) return launch_apply<Cfg<2, 4, 3>>(g, b, f, x, y_loc, st);
+  if (stream_ok<Cfg<2, 2, 2>>(g, b, f)) return launch_apply<Cfg<2, 2, 2>>(g, b, f, x, y_loc, st);
+  if (stream_ok<Cfg<3, 2, 2>>(g, b, f)) return launch_apply<Cfg<3, 2, 2>>(g, b, f, x, y_loc, st);
+  if (stream_ok<Cfg<3, 1, 2>>(g, b, f)) return launch_apply<Cfg<3, 1, 2>>(g, b, f, x, y_loc, st);
+  if (stream_ok<Cfg<3, 2, 1>>(g, b, f)) return launch_apply<Cfg<3, 2, 1>>(g, b, f, x, y_loc, st);
   return -1;
 }
 

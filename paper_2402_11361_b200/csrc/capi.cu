@@ -38,6 +38,11 @@ long long mhdg_launch_count(void) { return g_launches; }
 
 long long mhdg_packed_lu_size(int n) { return ti_size(n); }
 
+long long mhdg_apply_work_size(const mhdg_disc* g) {
+  const long long n = (long long)g->L * g->ns, np = n + (n & 1), ltr = (long long)g->nf * g->Lf * g->ns;
+  return (long long)g->n_mac * (2 * np + 2 * ltr);
+}
+
 static int g_stream_enabled = 1;
 void mhdg_set_stream_enabled(int on) { g_stream_enabled = on; }
 

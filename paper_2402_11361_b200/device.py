@@ -97,6 +97,12 @@ class DeviceDisc:
         t["node_to_face"] = i32(n2f)
         t["minv_d_face"] = f64(pad2(rm.mass_inv_weak_deriv[:, fnodes, :]))
         self.n_face_nodes = len(fnodes)
+        # distinct per-sub-element gradient tables (exact comparison)
+        G = np.ascontiguousarray(rm.grad_ref).reshape(rm.n_sub, -1)
+        cls, cls_of = np.unique(G, axis=0, return_inverse=True)
+        t["grad_cls"] = f64(cls)
+        t["grad_cls_of"] = i32(cls_of.ravel())
+        self.n_grad_cls = len(cls)
         self.t = t
 
         c = _lib.Disc()
@@ -107,6 +113,7 @@ class DeviceDisc:
         c.n_tri, c.nlocf, c.nqf = rm.n_tri, rm.n_loc_face, rm.n_quad_face
         c.face_fac = disc.face_fac
         c.n_face_nodes = self.n_face_nodes
+        c.n_grad_cls = self.n_grad_cls
         for name, tensor in t.items():
             setattr(c, name, _lib.ptr(tensor))
         self.c = c

@@ -112,21 +112,28 @@ def test_apply_is_deterministic_and_linear():
     assert rel_err(host(y12), host(2.0 * y1 - 3.0 * cond.apply_trace(x2))) < 1e-13
 
 
+@pytest.mark.parametrize("split", [1, 0])
 @pytest.mark.parametrize("name", ["uniform_m2p2", "uniform_m4p3", "couette_m2p2"])
-def test_streamed_apply_matches_generic(name):
-    """The TMA-streamed specialised kernel and the generic kernel agree."""
+def test_streamed_apply_matches_generic(name, split):
+    """The TMA-streamed specialised kernels -- split (pre / S^-1 stream / post)
+    and fused -- agree with the generic kernel."""
     need_gpu()
     from paper_2402_11361_b200 import _lib
 
+    L = _lib.lib()
     d, fn, ctx = _cases_2d()[name]
     of = perturbed_fields(d, fn, 13)
     ob, _ = O.jacobian(d, of, ctx)
     cond = CondensedSchur.build(upload_blocks(d, ob))
     x = dev(np.random.default_rng(8).standard_normal(d.n_trace))
     try:
-        _lib.lib().mhdg_set_stream_enabled(0)
+        L.mhdg_set_stream_enabled(0)
         y_gen = host(cond.apply_trace(x))
+        L.mhdg_set_stream_enabled(1)
+        L.mhdg_set_apply_split(split)
+        y_str = host(cond.apply_trace(x))
+        assert torch.equal(cond.apply_trace(x), cond.apply_trace(x))
     finally:
-        _lib.lib().mhdg_set_stream_enabled(1)
-    y_str = host(cond.apply_trace(x))
+        L.mhdg_set_stream_enabled(1)
+        L.mhdg_set_apply_split(1)
     assert rel_err(y_str, y_gen) < 1e-10  # summation order differs; cond(S) ~ 1e6 at m=4, p=3

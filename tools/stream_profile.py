@@ -39,7 +39,7 @@ torch.cuda.synchronize()
 buf = (C.c_ulonglong * 48)()
 L.mhdg_stream_profile(buf, 0)
 a = np.array(buf, dtype=np.float64).reshape(16, 3)
-names = ["FST", "FTT", "WV", "WFZ", "SI", "-", "-", "-", "WF2", "FTS", "GF", "MD", "END"]
+names = ["FST", "FTT", "WV", "WFZ", "SI", "Y2", "FC", "-", "WF2", "FTS", "GF", "MD", "END", "MSTART", "Y1", "WB"]
 ms = e0.elapsed_time(e1) / reps
 L.mhdg_stream_grid.restype = C.c_int
 ncta = L.mhdg_stream_grid()
