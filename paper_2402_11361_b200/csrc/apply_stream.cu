@@ -67,10 +67,41 @@ struct Piece {
   unsigned off;                // doubles from the segment's per-macro (or table) base
 };
 
-__host__ __device__ __forceinline__ int units_per_piece(int unit) {
-  int r = ST_DBL / unit;
-  if (unit & 1) r &= ~1;
-  return r < 1 ? 1 : r;
+__host__ __device__ constexpr int units_per_piece(int unit) {
+  return (unit & 1) ? ((ST_DBL / unit) & ~1) < 1 ? 1 : ((ST_DBL / unit) & ~1) : (ST_DBL / unit) < 1 ? 1 : ST_DBL / unit;
+}
+
+// consumer-side ring cursor: stage index and phase in registers, barrier
+// addresses precomputed
+template <int STAGES>
+struct ConsRing {
+  uint32_t full0, empty0;
+  const double* base;
+  int stg = 0;
+  uint32_t ph = 0;
+  __device__ __forceinline__ const double* wait() {
+    mbar_wait_a(full0 + 8u * stg, ph);
+    return base + stg * ST_DBL;
+  }
+  __device__ __forceinline__ void release(int lane) {
+    __syncwarp();
+    if (lane == 0) mbar_arrive_a(empty0 + 8u * stg);
+    if (++stg == STAGES) {
+      stg = 0;
+      ph ^= 1u;
+    }
+  }
+};
+
+// consume the pieces of one segment: rows [u0, u0 + nu) of NROWS, PER per piece
+template <int NROWS, int PER, class R, class Body>
+__device__ __forceinline__ void seg_loop(R& rg, int lane, Body&& body) {
+#pragma unroll 1
+  for (int u0 = 0; u0 < NROWS; u0 += PER) {
+    const double* A = rg.wait();
+    body(A, u0, (NROWS - u0) < PER ? NROWS - u0 : PER);
+    rg.release(lane);
+  }
 }
 
 // Walks one macro's pieces in consumption order; the producer and the
@@ -220,8 +251,8 @@ __device__ __forceinline__ int first_group(int g0, int warp) {
 // acc_r = sum_c A[r][c] vec_r[c] for rows u0 .. u0+nu-1 of a staged piece, LPR
 // lanes per row, RPW = 32/LPR rows per warp group, groups dealt to warps by
 // global row index; out(r, acc) on one lane per row (r local to the piece).
-template <int LPR, class VecF, class OutF>
-__device__ __forceinline__ void rows_dot(const double* A, int u0, int nu, int ncol, VecF vec, OutF out) {
+template <int LPR, int NCOL, class VecF, class OutF>
+__device__ __forceinline__ void rows_dot(const double* A, int u0, int nu, VecF vec, OutF out) {
   constexpr int RPW = 32 / LPR;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int sub = lane / LPR, l = lane % LPR;
@@ -231,14 +262,14 @@ __device__ __forceinline__ void rows_dot(const double* A, int u0, int nu, int nc
     const bool on = rl >= 0 && rl < nu;
     double a0 = 0.0, a1 = 0.0;
     if (on) {
-      const double* a = A + rl * ncol;
-      const double* v = vec(rl);
-      int c = l;
-      for (; c + LPR < ncol; c += 2 * LPR) {
-        a0 += a[c] * v[c];
-        a1 += a[c + LPR] * v[c + LPR];
+      const double* a = A + rl * NCOL + l;
+      const double* v = vec(rl) + l;
+      constexpr int NK = (NCOL + LPR - 1) / LPR;  // columns l, l+LPR, ... (fixed trip count)
+#pragma unroll
+      for (int k = 0; k < NK; k += 2) {
+        if (k * LPR + l < NCOL) a0 += a[k * LPR] * v[k * LPR];
+        if (k + 1 < NK && (k + 1) * LPR + l < NCOL) a1 += a[(k + 1) * LPR] * v[(k + 1) * LPR];
       }
-      if (c < ncol) a0 += a[c] * v[c];
     }
     double acc = a0 + a1;
 #pragma unroll
@@ -366,6 +397,10 @@ __global__ void __launch_bounds__(NCONS + 32, 2) k_apply_stream(mhdg_disc g, mhd
   }
 
   // ----------------------------- consumers --------------------------------
+  // The piece sequence is compile-time: each segment is a loop over its
+  // pieces (ConsRing carries stage and phase), consumed in the order the
+  // producer issues them (Sched).  Barriers only where data flows between
+  // warps.
   double *xl = W + S::xl, *z = W + S::z, *y = W + S::y, *t = W + S::t, *rfst = W + S::rfst, *ftt = W + S::ftt,
          *fts = W + S::fts, *cfgz = W + S::cfgz, *yf = W + S::yf, *wfz = W + S::wfz, *wf2 = W + S::wf2,
          *vv = W + S::vv, *cv = W + S::cv, *tg = W + S::tg;
@@ -376,11 +411,14 @@ __global__ void __launch_bounds__(NCONS + 32, 2) k_apply_stream(mhdg_disc g, mhd
   double* wv = tg;   // W_vol contraction results, lifetime: W_vol pieces .. y1
   double* z2 = z;    // z is dead once the W_face(z) pieces are consumed
   double* vw = vv + warp * 32;  // warp-private scratch
+  using SC = Sched<C, PART>;
+  ConsRing<STAGES> rg{smem_u32(full_bar), smem_u32(empty_bar), ring};
+
   // this thread's trace entry of the next macro, gathered one macro ahead
   double x_next = 0.0;
   if (PART != 2 && tid < LTR && blockIdx.x < g.n_mac)
     x_next = __ldg(x + __ldg(g.gather + (size_t)blockIdx.x * LTR + tid));
-  int it = 0;
+
   for (int mac = blockIdx.x; mac < g.n_mac; mac += gridDim.x) {
     double ij[D][D];
 #pragma unroll
@@ -389,15 +427,75 @@ __global__ void __launch_bounds__(NCONS + 32, 2) k_apply_stream(mhdg_disc g, mhd
       for (int b = 0; b < D; ++b) ij[a][b] = __ldg(g.inv_jac + (size_t)mac * D * D + a * D + b);
     double sc_mine = 0.0;  // trace_face_scale of this thread's face in the final sum
     if (PART != 1 && tid < LTR) sc_mine = __ldg(bk.trace_face_scale + mac * NF + tid / BS);
-    double siacc = 0.0;  // per-lane partial of S^-1 y1 for the rows this lane owns (fused apply)
     PROF_T(t_start);
     if (PART != 2 && tid < LTR) {
       xl[tid] = x_next;
       const int nm = mac + gridDim.x;
       if (nm < g.n_mac) x_next = __ldg(x + __ldg(g.gather + (size_t)nm * LTR + tid));
     }
-    cbar();
+    cbar();  // xl complete; the previous macro's readers of every work array are done
     if (tid == 0) { PROF_ADD(13, 2, t_start); }
+
+    // W_vol / W_face contraction of one piece: v = phi z (gathered), out = W v.
+    // Point groups of PPI points per warp pass, dealt to warps by global index.
+    auto wcontract = [&](const double* A, int u0, int nu, bool face, bool second) {
+      constexpr int DN = D * NS, PPI = 32 / DN;
+      const int pi = lane / DN, j = lane % DN;
+      const int ngrp = (nu + PPI - 1) / PPI;
+      for (int grp = first_group(u0 / PPI, warp) - u0 / PPI; grp < ngrp; grp += NWARP_C) {
+        const int pl = grp * PPI + pi;
+        const bool on = pi < PPI && pl < nu;
+        if (on) {
+          const int tt = j % NS, l = j / NS;
+          double a = 0.0;
+          if (!face) {  // v[l][tt] = sum_b phi[q][b] z[l][conn[K][b]][tt]
+            const int pt = u0 + pl, K = pt / NQ, q = pt % NQ;
+#pragma unroll
+            for (int b = 0; b < NLOC; ++b) a += phs[q * NLOC + b] * z[(l * L + conn[K * NLOC + b]) * NS + tt];
+          } else {
+            const double* zs = second ? z2 : z;
+            const int lstride = second ? C::NFN : L;
+            const int pf = u0 + pl, q = pf % NQF, T = (pf / NQF) % NTRI, f = pf / (NQF * NTRI);
+#pragma unroll
+            for (int b = 0; b < NLOCF; ++b) {
+              int node = fvn[f * LF + tconn[T * NLOCF + b]];
+              if (second) node = n2f[node];
+              a += pfs[q * NLOCF + b] * zs[(l * lstride + node) * NS + tt];
+            }
+          }
+          vw[pi * DN + j] = a;
+        }
+        __syncwarp();
+        if (!face) {
+          if (on) {  // out[k][s] = sum_{l,tt} W[k][l][s][tt] v[l][tt], (l, tt) order rotated per lane
+            const int s = j % NS, k = j / NS;
+            const double* w = A + pl * C::NW + k * D * NS * NS + s * NS;
+            const double* v = vw + pi * DN;
+            const int rot = (pi * D + k) % DN;
+            double a = 0.0;
+#pragma unroll
+            for (int i = 0; i < DN; ++i) {
+              int ii = i + rot;
+              if (ii >= DN) ii -= DN;
+              const int l = ii / NS, tt = ii - l * NS;
+              a += w[l * NS * NS + tt] * v[ii];
+            }
+            wv[(u0 + pl) * DN + j] = a;
+          }
+        } else if (on && j < NS) {
+          const int s = j;
+          const double* w = A + pl * C::NWF + s * NS;
+          const double* v = vw + pi * DN;
+          double a = 0.0;
+#pragma unroll
+          for (int l = 0; l < D; ++l)
+#pragma unroll
+            for (int tt = 0; tt < NS; ++tt) a += w[l * NS * NS + tt] * v[l * NS + tt];
+          (second ? wf2 : wfz)[(u0 + pl) * NS + s] = a;
+        }
+        __syncwarp();
+      }
+    };
 
     // y1 = -A_uh x + A_uq z (needs rfst, the W_vol results, the W_face(z) stash);
     // leaves y1 in y and the face term g = A_hq z / scale in cfgz
@@ -424,8 +522,8 @@ __global__ void __launch_bounds__(NCONS + 32, 2) k_apply_stream(mhdg_disc g, mhd
         }
         cv[idx] = acc;
       }
-      for (int idx = tid; idx < LTR; idx += NCONS) {
-        const int s = idx % NS, gg = (idx / NS) % LF, f = idx / BS;
+      if (tid < LTR) {
+        const int idx = tid, s = idx % NS, gg = (idx / NS) % LF, f = idx / BS;
         double acc = 0.0;
         for (int e = fnp[gg]; e < fnp[gg + 1]; ++e) {
           const int ent = fne[e], T = ent / NLOCF, a = ent % NLOCF;
@@ -447,210 +545,93 @@ __global__ void __launch_bounds__(NCONS + 32, 2) k_apply_stream(mhdg_disc g, mhd
       cbar();
     };
 
-    int prev = -1;
-    for (int pi = 0; pi < np; ++pi) {
-      const Piece p = pieces[pi];
-      // ---------------- phase transitions (no stage held) ----------------
-      PROF_T(t_tr);
-      if (p.kind != prev) {
-        cbar();  // every warp has finished the previous kind
-        if (p.kind == K_FST) {
-          // z = A_qq^-1 A_qh x = -(fac/det) sum_f area_f n_f (Gf x_f)
-          const double idet = 1.0 / __ldg(g.det + mac);
-          double cfl[NF][D];
+    if (PART != 2) {
+      PROF_T(t0);
+      // tg[f][I][s] = sum_h Gf[f][I][h] x[f][h][s]
+      seg_loop<NF * L, units_per_piece(LF)>(rg, lane, [&](const double* A, int u0, int nu) {
+        for (int idx = tid; idx < nu * NS; idx += NCONS) {
+          const int s = idx % NS, rl = idx / NS, row = u0 + rl, f = row / L;
+          const double* a = A + rl * LF;
+          const double* xf = xl + f * BS + s;
+          double acc = 0.0;
 #pragma unroll
-          for (int f = 0; f < NF; ++f)
+          for (int h = 0; h < LF; ++h) acc += a[h] * xf[h * NS];
+          tg[row * NS + s] = acc;
+        }
+      });
+      if (tid == 0) { PROF_ADD(K_GF, 1, t0); }
+      PROF_T(t1);
+      cbar();
+      {  // z = A_qq^-1 A_qh x = -(fac/det) sum_f area_f n_f (Gf x_f)
+        const double idet = 1.0 / __ldg(g.det + mac);
+        double cfl[NF][D];
 #pragma unroll
-            for (int l = 0; l < D; ++l)
-              cfl[f][l] =
-                  -g.face_fac * __ldg(g.areas + mac * NF + f) * idet * __ldg(g.normals + (mac * NF + f) * D + l);
-          for (int idx = tid; idx < n; idx += NCONS) {
-            double acc[D] = {};
+        for (int f = 0; f < NF; ++f)
 #pragma unroll
-            for (int f = 0; f < NF; ++f) {
-              const double tv = tg[f * n + idx];
+          for (int l = 0; l < D; ++l)
+            cfl[f][l] = -g.face_fac * __ldg(g.areas + mac * NF + f) * idet * __ldg(g.normals + (mac * NF + f) * D + l);
+        for (int idx = tid; idx < n; idx += NCONS) {
+          double acc[D] = {};
 #pragma unroll
-              for (int l = 0; l < D; ++l) acc[l] += cfl[f][l] * tv;
-            }
+          for (int f = 0; f < NF; ++f) {
+            const double tv = tg[f * n + idx];
 #pragma unroll
-            for (int l = 0; l < D; ++l) z[l * n + idx] = acc[l];
+            for (int l = 0; l < D; ++l) acc[l] += cfl[f][l] * tv;
           }
-          cbar();
-        } else if (p.kind == K_SI) {
-          make_y1();
-        } else if (p.kind == K_MD) {
-          if (PART == 0) {  // y <- y2 = S^-1 y1 (held in t); the post kernel gets y2 as a piece
-            for (int i = tid; i < n; i += NCONS) y[i] = t[i];
-            cbar();
-          }
-          // y2 restricted to the face nodes, for A_hu
-          for (int idx = tid; idx < LTR; idx += NCONS) {
-            const int s = idx % NS, h = (idx / NS) % LF, f = idx / BS;
-            yf[idx] = y[fvn[f * LF + h] * NS + s];
-          }
-        } else if (p.kind == K_WF2) {
-          // z2 = A_qq^-1 A_qu y2 = sum_r inv_jac[r][l] (M^-1 D_r y2), at the face nodes only
-          constexpr int FNS = C::NFN * NS;
-          for (int idx = tid; idx < FNS; idx += NCONS) {
-            double tr[D];
 #pragma unroll
-            for (int r = 0; r < D; ++r) tr[r] = tg[r * FNS + idx];
-#pragma unroll
-            for (int l = 0; l < D; ++l) {
-              double v = 0.0;
-#pragma unroll
-              for (int r = 0; r < D; ++r) v += ij[r][l] * tr[r];
-              z2[l * FNS + idx] = v;
-            }
-          }
-          cbar();
+          for (int l = 0; l < D; ++l) z[l * n + idx] = acc[l];
         }
       }
-
-      if (tid == 0) { PROF_ADD(p.kind, 2, t_tr); }
-      // ---------------- wait for the stage ----------------
-      const int stg = it % STAGES;
-      PROF_T(t_w);
-      mbar_wait(&full_bar[stg], (it / STAGES) & 1);
-      if (tid == 0) { PROF_ADD(p.kind, 0, t_w); }
-      PROF_T(t_c);
-      const double* A = ring + stg * ST_DBL;
-
-      // ---------------- consume ----------------
-      switch (p.kind) {
-        case K_Y2: {
-          for (int i = tid; i < n; i += NCONS) y[i] = A[i];
-          break;
-        }
-        case K_FC: {
-          for (int i = tid; i < LTR; i += NCONS) {
-            ftt[i] = A[i];
-            cfgz[i] = A[LTR + i];
-          }
-          break;
-        }
-        case K_GF: {  // tg[f][I][s] = sum_h Gf[f][I][h] x[f][h][s]
-          for (int idx = tid; idx < p.nu * NS; idx += NCONS) {
-            const int s = idx % NS, rl = idx / NS, row = p.u0 + rl, f = row / L;
-            const double* a = A + rl * LF;
-            const double* xf = xl + f * BS + s;
-            double acc = 0.0;
-#pragma unroll
-            for (int h = 0; h < LF; ++h) acc += a[h] * xf[h * NS];
-            tg[row * NS + s] = acc;
-          }
-          break;
-        }
-        case K_MD: {  // tg[r][i][s] = sum_J (M^-1 D_r)[fnode_i][J] y2[J][s]: lane = (row, s)
-          constexpr int RPW = 32 / NS;
-          const int rr = lane / NS, s = lane % NS;
-          const int g1 = (p.u0 + p.nu - 1) / RPW;
-          for (int gg = first_group(p.u0 / RPW, warp); gg <= g1; gg += NWARP_C) {
-            const int row = gg * RPW + rr;
-            if (rr < RPW && row >= p.u0 && row < p.u0 + p.nu) {
-              const double* a = A + (row - p.u0) * L;
-              double a0 = 0.0, a1 = 0.0;
-#pragma unroll 4
-              for (int J = 0; J + 1 < L; J += 2) {
-                a0 += a[J] * y[J * NS + s];
-                a1 += a[J + 1] * y[(J + 1) * NS + s];
-              }
-              if (L & 1) a0 += a[L - 1] * y[(L - 1) * NS + s];
-              tg[row * NS + s] = a0 + a1;
-            }
-          }
-          break;
-        }
-        case K_FST:
-        case K_FTT:
-        case K_FTS: {
-          const double* vec = p.kind == K_FTS ? yf : xl;
-          double* out = p.kind == K_FST ? rfst : p.kind == K_FTT ? ftt : fts;
-          const int u0 = p.u0;
-          rows_dot<4>(A, u0, p.nu, BS, [&](int rl) { return vec + ((u0 + rl) / BS) * BS; },
-                      [&](int rl, double acc) { out[u0 + rl] = acc; });
-          break;
-        }
-        case K_WV: {  // point groups of PPI points per warp pass, dealt to warps by global index
-          constexpr int DN = D * NS, PPI = 32 / DN;
-          const int pi = lane / DN, j = lane % DN;
-          const int ngrp = (p.nu + PPI - 1) / PPI;
-          for (int grp = first_group(p.u0 / PPI, warp) - p.u0 / PPI; grp < ngrp; grp += NWARP_C) {
-            const int pl = grp * PPI + pi;
-            const bool on = pi < PPI && pl < p.nu;
-            if (on) {  // v[l][tt] = sum_b phi[q][b] z[l][conn[K][b]][tt]
-              const int tt = j % NS, l = j / NS, pt = p.u0 + pl, K = pt / NQ, q = pt % NQ;
-              double a = 0.0;
-#pragma unroll
-              for (int b = 0; b < NLOC; ++b) a += phs[q * NLOC + b] * z[(l * L + conn[K * NLOC + b]) * NS + tt];
-              vw[pi * DN + j] = a;
-            }
-            __syncwarp();
-            if (on) {  // out[k][s] = sum_{l,tt} W[k][l][s][tt] v[l][tt], (l, tt) order rotated per lane
-              const int s = j % NS, k = j / NS;
-              const double* w = A + pl * C::NW + k * D * NS * NS + s * NS;
-              const double* v = vw + pi * DN;
-              const int rot = (pi * D + k) % DN;
-              double a = 0.0;
-#pragma unroll
-              for (int i = 0; i < DN; ++i) {
-                int ii = i + rot;
-                if (ii >= DN) ii -= DN;
-                const int l = ii / NS, tt = ii - l * NS;
-                a += w[l * NS * NS + tt] * v[ii];
-              }
-              wv[(p.u0 + pl) * DN + j] = a;
-            }
-            __syncwarp();
-          }
-          break;
-        }
-        case K_WFZ:
-        case K_WF2: {  // as K_WV, on the face stash
-          constexpr int DN = D * NS, PPI = 32 / DN;
-          const bool second = p.kind == K_WF2;
-          const double* zs = second ? z2 : z;
-          const int lstride = second ? C::NFN : L;
-          double* wf = second ? wf2 : wfz;
-          const int pi = lane / DN, j = lane % DN;
-          const int ngrp = (p.nu + PPI - 1) / PPI;
-          for (int grp = first_group(p.u0 / PPI, warp) - p.u0 / PPI; grp < ngrp; grp += NWARP_C) {
-            const int pl = grp * PPI + pi;
-            const bool on = pi < PPI && pl < p.nu;
-            if (on) {
-              const int tt = j % NS, l = j / NS;
-              const int pf = p.u0 + pl, q = pf % NQF, T = (pf / NQF) % NTRI, f = pf / (NQF * NTRI);
-              double a = 0.0;
-#pragma unroll
-              for (int b = 0; b < NLOCF; ++b) {
-                int node = fvn[f * LF + tconn[T * NLOCF + b]];
-                if (second) node = n2f[node];
-                a += pfs[q * NLOCF + b] * zs[(l * lstride + node) * NS + tt];
-              }
-              vw[pi * DN + j] = a;
-            }
-            __syncwarp();
-            if (on && j < NS) {
-              const int s = j;
-              const double* w = A + pl * C::NWF + s * NS;
-              const double* v = vw + pi * DN;
-              double a = 0.0;
-#pragma unroll
-              for (int l = 0; l < D; ++l)
-#pragma unroll
-                for (int tt = 0; tt < NS; ++tt) a += w[l * NS * NS + tt] * v[l * NS + tt];
-              wf[(p.u0 + pl) * NS + s] = a;
-            }
-            __syncwarp();
-          }
-          break;
-        }
-        case K_SI: {  // one column tile of a row block; warp w owns rows SRW*w .. SRW*w+SRW-1 of every block
-          constexpr int SRW = TI_RB / NWARP_C, SLR = 32 / SRW;  // rows per warp, lanes per row
-          static_assert(SRW * NWARP_C == TI_RB && SRW * SLR == 32, "S^-1 tile mapping");
-          const int nb = ti_rows(n, p.blk), w = p.nu, c0 = p.u0;
-          const int r = SRW * warp + lane / SLR, l = lane % SLR;
-          if (c0 == 0) siacc = 0.0;
+      cbar();  // z complete; tg free for the W_vol results
+      if (tid == 0) { PROF_ADD(K_FST, 2, t1); }
+      PROF_T(t2);
+      seg_loop<NF * BS, units_per_piece(BS)>(rg, lane, [&](const double* A, int u0, int nu) {
+        rows_dot<4, BS>(A, u0, nu, [&](int rl) { return xl + ((u0 + rl) / BS) * BS; },
+                        [&](int rl, double acc) { rfst[u0 + rl] = acc; });
+      });
+      if (tid == 0) { PROF_ADD(K_FST, 1, t2); }
+      PROF_T(t3);
+      seg_loop<NF * BS, units_per_piece(BS)>(rg, lane, [&](const double* A, int u0, int nu) {
+        rows_dot<4, BS>(A, u0, nu, [&](int rl) { return xl + ((u0 + rl) / BS) * BS; },
+                        [&](int rl, double acc) { ftt[u0 + rl] = acc; });
+      });
+      if (tid == 0) { PROF_ADD(K_FTT, 1, t3); }
+      PROF_T(t4);
+      seg_loop<C::NPV, SC::WV_ALIGN ? SC::WV_PER : units_per_piece(C::NW)>(
+          rg, lane, [&](const double* A, int u0, int nu) { wcontract(A, u0, nu, false, false); });
+      if (tid == 0) { PROF_ADD(K_WV, 1, t4); }
+      PROF_T(t5);
+      seg_loop<C::NPF, units_per_piece(C::NWF)>(
+          rg, lane, [&](const double* A, int u0, int nu) { wcontract(A, u0, nu, true, false); });
+      if (tid == 0) { PROF_ADD(K_WFZ, 1, t5); }
+      PROF_T(t6);
+      cbar();  // rfst, W_vol results, W_face(z) stash complete
+      make_y1();
+      if (tid == 0) { PROF_ADD(14, 1, t6); }
+    }
+    if (PART == 1) {  // hand y1 and the face terms to the S^-1 stream / post kernels
+      PROF_T(t_wb);
+      double* y1g = Work<C>::y1(fac.work, mac);
+      for (int i = tid; i < n; i += NCONS) y1g[i] = y[i];
+      double* fc = Work<C>::fc(fac.work, g.n_mac, mac);
+      if (tid < LTR) {
+        fc[tid] = ftt[tid];
+        fc[LTR + tid] = cfgz[tid];
+      }
+      if (tid == 0) { PROF_ADD(15, 2, t_wb); }
+      continue;  // the next macro's first barrier orders these reads before any overwrite
+    }
+    if (PART == 0) {  // y2 = S^-1 y1: row blocks of column tiles; warp w owns rows SRW*w.. of every block
+      constexpr int SRW = TI_RB / NWARP_C, SLR = 32 / SRW;
+      static_assert(SRW * NWARP_C == TI_RB && SRW * SLR == 32, "S^-1 tile mapping");
+      PROF_T(t7);
+      for (int b = 0; b < C::NBLK; ++b) {
+        const int nb = ti_rows(n, b);
+        const int r = SRW * warp + lane / SLR, l = lane % SLR;
+        double acc = 0.0;
+        for (int c0 = 0; c0 < n; c0 += TI_CW) {
+          const int w = (n - c0) < TI_CW ? n - c0 : TI_CW;
+          const double* A = rg.wait();
           if (r < nb) {
             const double* a = A + r * w;
             const double* yv = y + c0;
@@ -661,41 +642,86 @@ __global__ void __launch_bounds__(NCONS + 32, 2) k_apply_stream(mhdg_disc g, mhd
               if (c < w) a0 += a[c] * yv[c];
               if (c + SLR < w) a1 += a[c + SLR] * yv[c + SLR];
             }
-            siacc += a0 + a1;
+            acc += a0 + a1;
           }
-          if (c0 + w == n) {  // last tile of the block: reduce over the row's SLR lanes
-            double acc = siacc;
-#pragma unroll
-            for (int o = SLR / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(MHDG_FULL, acc, o);
-            if (l == 0 && r < nb) t[p.blk * TI_RB + r] = acc;
-          }
-          break;
+          rg.release(lane);
         }
-      }
-      __syncwarp();
-      if (tid == 0) { PROF_ADD(p.kind, 1, t_c); }
-      if (lane == 0) mbar_arrive(&empty_bar[stg]);
-      ++it;
-      prev = p.kind;
-    }
-    PROF_T(t_end);
-    cbar();
-    if (PART == 1) {  // pre part: hand y1 and the face terms to the S^-1 stream / post kernels
-      PROF_T(t_y1);
-      make_y1();
-      if (tid == 0) { PROF_ADD(14, 1, t_y1); }
-      PROF_T(t_wb);
-      double* y1g = Work<C>::y1(fac.work, mac);
-      for (int i = tid; i < n; i += NCONS) y1g[i] = y[i];
-      double* fc = Work<C>::fc(fac.work, g.n_mac, mac);
-      if (tid < LTR) {
-        fc[tid] = ftt[tid];
-        fc[LTR + tid] = cfgz[tid];
+#pragma unroll
+        for (int o = SLR / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(MHDG_FULL, acc, o);
+        if (l == 0 && r < nb) t[b * TI_RB + r] = acc;
       }
       cbar();
-      if (tid == 0) { PROF_ADD(15, 2, t_wb); }
-      continue;
+      for (int i = tid; i < n; i += NCONS) y[i] = t[i];
+      if (tid == 0) { PROF_ADD(K_SI, 1, t7); }
+    } else {  // post part: y2 and the pre part's face terms arrive as the first two pieces
+      PROF_T(t8);
+      seg_loop<1, 1>(rg, lane, [&](const double* A, int, int) {
+        for (int i = tid; i < n; i += NCONS) y[i] = A[i];
+      });
+      seg_loop<1, 1>(rg, lane, [&](const double* A, int, int) {
+        if (tid < LTR) {
+          ftt[tid] = A[tid];
+          cfgz[tid] = A[LTR + tid];
+        }
+      });
+      if (tid == 0) { PROF_ADD(K_Y2, 1, t8); }
     }
+    PROF_T(t9);
+    cbar();  // y = y2 complete
+    if (tid < LTR) {  // y2 restricted to the face nodes, for A_hu
+      const int idx = tid, s = idx % NS, h = (idx / NS) % LF, f = idx / BS;
+      yf[idx] = y[fvn[f * LF + h] * NS + s];
+    }
+    // tg[r][i][s] = sum_J (M^-1 D_r)[fnode_i][J] y2[J][s]: lane = (row, s), row groups dealt to warps
+    seg_loop<D * C::NFN, units_per_piece(L)>(rg, lane, [&](const double* A, int u0, int nu) {
+      constexpr int RPW = 32 / NS;
+      const int rr = lane / NS, s = lane % NS;
+      const int g1 = (u0 + nu - 1) / RPW;
+      for (int gg = first_group(u0 / RPW, warp); gg <= g1; gg += NWARP_C) {
+        const int row = gg * RPW + rr;
+        if (rr < RPW && row >= u0 && row < u0 + nu) {
+          const double* a = A + (row - u0) * L;
+          double a0 = 0.0, a1 = 0.0;
+#pragma unroll 4
+          for (int J = 0; J + 1 < L; J += 2) {
+            a0 += a[J] * y[J * NS + s];
+            a1 += a[J + 1] * y[(J + 1) * NS + s];
+          }
+          if (L & 1) a0 += a[L - 1] * y[(L - 1) * NS + s];
+          tg[row * NS + s] = a0 + a1;
+        }
+      }
+    });
+    if (tid == 0) { PROF_ADD(K_MD, 1, t9); }
+    PROF_T(t10);
+    cbar();
+    {  // z2 = A_qq^-1 A_qu y2 = sum_r inv_jac[r][l] (M^-1 D_r y2), at the face nodes only
+      constexpr int FNS = C::NFN * NS;
+      for (int idx = tid; idx < FNS; idx += NCONS) {
+        double tr[D];
+#pragma unroll
+        for (int r = 0; r < D; ++r) tr[r] = tg[r * FNS + idx];
+#pragma unroll
+        for (int l = 0; l < D; ++l) {
+          double v = 0.0;
+#pragma unroll
+          for (int r = 0; r < D; ++r) v += ij[r][l] * tr[r];
+          z2[l * FNS + idx] = v;
+        }
+      }
+    }
+    cbar();  // z2 and yf complete
+    if (tid == 0) { PROF_ADD(K_WF2, 2, t10); }
+    PROF_T(t11);
+    seg_loop<C::NPF, units_per_piece(C::NWF)>(
+        rg, lane, [&](const double* A, int u0, int nu) { wcontract(A, u0, nu, true, true); });
+    seg_loop<NF * BS, units_per_piece(BS)>(rg, lane, [&](const double* A, int u0, int nu) {
+      rows_dot<4, BS>(A, u0, nu, [&](int rl) { return yf + ((u0 + rl) / BS) * BS; },
+                      [&](int rl, double acc) { fts[u0 + rl] = acc; });
+    });
+    if (tid == 0) { PROF_ADD(K_FTS, 1, t11); }
+    PROF_T(t_end);
+    cbar();  // wf2, fts complete
 
     // y4 = ((A_hu y2 - A_hq z2) + A_hh x) - A_hq z, with -A_hq z = scale * cfg
     if (tid < LTR) {
@@ -709,7 +735,6 @@ __global__ void __launch_bounds__(NCONS + 32, 2) k_apply_stream(mhdg_disc g, mhd
       }
       y_loc[(size_t)mac * LTR + idx] = ((fts[idx] + sc_mine * acc) + ftt[idx]) + sc_mine * cfgz[idx];
     }
-    cbar();
     if (tid == 0) { PROF_ADD(12, 2, t_end); }
   }
 }
