@@ -291,7 +291,7 @@ struct Work {
 };
 
 template <class C, int STAGES, int PART>
-__global__ void __launch_bounds__(NCONS + 32, 2) k_apply_stream(mhdg_disc g, mhdg_blocks bk, mhdg_factors fac,
+__global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 ? 1 : 2)) k_apply_stream(mhdg_disc g, mhdg_blocks bk, mhdg_factors fac,
                                                              const double* __restrict__ x,
                                                              double* __restrict__ y_loc, int pref_ahead) {
   constexpr int D = C::D, NS = C::NS, NF = C::NF, L = C::L, LF = C::LF, BS = C::BS, LTR = C::LTR, n = C::n;
@@ -500,27 +500,29 @@ __global__ void __launch_bounds__(NCONS + 32, 2) k_apply_stream(mhdg_disc g, mhd
     // y1 = -A_uh x + A_uq z (needs rfst, the W_vol results, the W_face(z) stash);
     // leaves y1 in y and the face term g = A_hq z / scale in cfgz
     auto make_y1 = [&]() {
-      // cv[K][a][s] = sum_q sum_k gphys[K,q,a,k] w[K,q][k][s], gphys = grad_ref[K] inv_jac
+      // cv[K][a][s] = sum_q sum_k gphys[K,q,a,k] w[K,q][k][s], gphys = grad_ref[K] inv_jac:
+      // gphys per gradient class once per macro (in z, dead by now, when it fits; else after the
+      // classes), then one dot per output
+      double* Gp = g.n_grad_cls * TS::CLS <= D * n ? z : Gc + g.n_grad_cls * TS::CLS;
+      for (int idx = tid; idx < g.n_grad_cls * TS::CLS; idx += NCONS) {
+        const int k = idx % D, base = idx - k;
+        double gp = 0.0;
+#pragma unroll
+        for (int r2 = 0; r2 < D; ++r2) gp += Gc[base + r2] * ij[r2][k];
+        Gp[idx] = gp;
+      }
+      cbar();
       for (int idx = tid; idx < NSUB * NLOC * NS; idx += NCONS) {
         const int s = idx % NS, a = (idx / NS) % NLOC, K = idx / (NS * NLOC);
-        const double* G = Gc + gco[K] * TS::CLS;
-        double acc = 0.0;
-#pragma unroll 4
+        const double* G = Gp + gco[K] * TS::CLS + a * D;
+        const double* w = wv + K * NQ * D * NS + s;
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll
         for (int q = 0; q < NQ; ++q) {
-          const double* gr = G + (q * NLOC + a) * D;
-          const double* w = wv + (K * NQ + q) * D * NS + s;
-          double grv[D];
 #pragma unroll
-          for (int r2 = 0; r2 < D; ++r2) grv[r2] = gr[r2];
-#pragma unroll
-          for (int k = 0; k < D; ++k) {
-            double gp = 0.0;
-#pragma unroll
-            for (int r2 = 0; r2 < D; ++r2) gp += grv[r2] * ij[r2][k];
-            acc += gp * w[k * NS];
-          }
+          for (int k = 0; k < D; ++k) ((q & 1) ? a1 : a0) += G[q * NLOC * D + k] * w[(q * D + k) * NS];
         }
-        cv[idx] = acc;
+        cv[idx] = a0 + a1;
       }
       if (tid < LTR) {
         const int idx = tid, s = idx % NS, gg = (idx / NS) % LF, f = idx / BS;
@@ -672,24 +674,30 @@ __global__ void __launch_bounds__(NCONS + 32, 2) k_apply_stream(mhdg_disc g, mhd
       const int idx = tid, s = idx % NS, h = (idx / NS) % LF, f = idx / BS;
       yf[idx] = y[fvn[f * LF + h] * NS + s];
     }
-    // tg[r][i][s] = sum_J (M^-1 D_r)[fnode_i][J] y2[J][s]: lane = (row, s), row groups dealt to warps
+    // tg[r][i][s] = sum_J (M^-1 D_r)[fnode_i][J] y2[J][s]: lane = (J half, row, s) for groups
+    // of MDR rows dealt to warps by global index; the two halves meet in one shuffle
     seg_loop<D * C::NFN, units_per_piece(L)>(rg, lane, [&](const double* A, int u0, int nu) {
-      constexpr int RPW = 32 / NS;
-      const int rr = lane / NS, s = lane % NS;
-      const int g1 = (u0 + nu - 1) / RPW;
-      for (int gg = first_group(u0 / RPW, warp); gg <= g1; gg += NWARP_C) {
-        const int row = gg * RPW + rr;
-        if (rr < RPW && row >= u0 && row < u0 + nu) {
+      constexpr int MDR = 16 / NS, JH = (L + 1) / 2;
+      const int h = lane >> 4, rr = (lane & 15) / NS, s = (lane & 15) % NS;
+      const int g1 = (u0 + nu - 1) / MDR;
+      for (int gg = first_group(u0 / MDR, warp); gg <= g1; gg += NWARP_C) {
+        const int row = gg * MDR + rr;
+        const bool on = rr < MDR && row >= u0 && row < u0 + nu;
+        double a0 = 0.0, a1 = 0.0;
+        if (on) {
+          const int j0 = h * JH, j1 = h ? L : JH;
           const double* a = A + (row - u0) * L;
-          double a0 = 0.0, a1 = 0.0;
+          int J = j0;
 #pragma unroll 4
-          for (int J = 0; J + 1 < L; J += 2) {
+          for (; J + 1 < j1; J += 2) {
             a0 += a[J] * y[J * NS + s];
             a1 += a[J + 1] * y[(J + 1) * NS + s];
           }
-          if (L & 1) a0 += a[L - 1] * y[(L - 1) * NS + s];
-          tg[row * NS + s] = a0 + a1;
+          if (J < j1) a0 += a[J] * y[J * NS + s];
         }
+        double acc = a0 + a1;
+        acc += __shfl_xor_sync(MHDG_FULL, acc, 16);
+        if (on && h == 0) tg[row * NS + s] = acc;
       }
     });
     if (tid == 0) { PROF_ADD(K_MD, 1, t9); }
@@ -881,16 +889,18 @@ static bool stream_ok(const mhdg_disc& g, const mhdg_blocks& b, const mhdg_facto
                      ((C::NPF * C::NWF) % 2 == 0);
   const bool tables = g.n_grad_cls >= 1 && g.grad_cls && g.grad_cls_of && g.node_to_face && g.minv_d_face &&
                       g.n_face_nodes == C::NFN;
+  const size_t cls = (size_t)g.n_grad_cls * TSm<C>::CLS;
   const size_t smem = sizeof(double) * ((size_t)MHDG_STAGES * ST_DBL + SSm<C>::total + TSm<C>::total +
-                                        (size_t)g.n_grad_cls * TSm<C>::CLS);
+                                        (cls <= (size_t)C::D * C::n ? cls : 2 * cls));
   return sizes && tables && smem <= 227 * 1024 && al(b.face_state_trace) && al(b.face_trace_trace) &&
          al(b.face_trace_state) && al(b.wdgdq_vol) && al(b.wdgdq_face) && al(f.lu) && al(f.work);
 }
 
 template <class C, int STAGES, int PART>
 static size_t stream_smem(const mhdg_disc& g) {
+  const size_t cls = (size_t)g.n_grad_cls * TSm<C>::CLS;  // classes (+ per-macro gphys unless it fits in z)
   return sizeof(double) * ((size_t)STAGES * ST_DBL + SSm<C>::total + TSm<C>::total +
-                           (PART != 2 ? (size_t)g.n_grad_cls * TSm<C>::CLS : 0));
+                           (PART != 2 ? (cls <= (size_t)C::D * C::n ? cls : 2 * cls) : 0));
 }
 
 template <class C, int STAGES, int PART>
