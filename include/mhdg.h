@@ -151,6 +151,14 @@ typedef struct {
 /* doubles of mhdg_factors.work for this discretization */
 long long mhdg_apply_work_size(const mhdg_disc *disc);
 
+/* Gauss-Jordan variant of mhdg_lu_factor: 3 (default) keeps pivot rows in
+   place, 2 interchanges rows (the earlier kernel).  For A/B measurements. */
+void mhdg_set_factor_variant(int v);
+
+/* Schur-complement kernel: 0 (default) FP64 tensor cores (DMMA), 1 shared-memory
+   row blocks, 2 per-macro FFMA.  For A/B measurements. */
+void mhdg_set_schur_variant(int v);
+
 /* 1 (default): split apply (pre / S^-1 stream / post kernels) when `work` is
    set; 0: fused single-kernel apply.  For A/B measurements. */
 void mhdg_set_apply_split(int on);

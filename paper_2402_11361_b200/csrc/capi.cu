@@ -20,6 +20,8 @@ int face_reduce(const mhdg_disc&, const double*, const double*, double, double*,
 int lu_solve(const mhdg_disc&, const mhdg_factors&, const double*, double*, cudaStream_t);
 int inv_factor(int n, int n_mac, double* scratch, double* tiled, int* status, cudaStream_t st);
 int inv_factor2(int n, int n_mac, double* scratch, int* piv, double* tiled, int* status, cudaStream_t st);
+int inv_factor3(int n, int n_mac, double* scratch, int* piv, double* tiled, int* status, cudaStream_t st);
+extern int g_schur_variant;
 size_t gj_smem_bytes(int n);
 int apply_stream(const mhdg_disc&, const mhdg_blocks&, const mhdg_factors&, const double*, double*, cudaStream_t);
 size_t lu_smem_bytes(int n);
@@ -88,10 +90,16 @@ int mhdg_schur_matrix(const mhdg_disc* g, const mhdg_blocks* b, const mhdg_facto
   return DISPATCH(g, schur_matrix<2>(*g, *b, f->scratch, S(st)), schur_matrix<3>(*g, *b, f->scratch, S(st)));
 }
 
+static int g_factor_variant = 3;
+void mhdg_set_factor_variant(int v) { g_factor_variant = v; }
+void mhdg_set_schur_variant(int v) { mhdg::g_schur_variant = v; }
+
 int mhdg_lu_factor(const mhdg_disc* g, const mhdg_factors* f, int* status, void* st) {
   const int n = g->L * g->ns;
-  // DMMA panel-64 Gauss-Jordan when its panel fits shared memory, else the 32-column FFMA one
-  const int rc = inv_factor2(n, g->n_mac, f->scratch, f->perm, f->lu, status, S(st));
+  // DMMA panel-64 Gauss-Jordan when its panel fits shared memory (without row interchanges
+  // by default), else the 32-column FFMA one
+  const int rc = g_factor_variant == 2 ? inv_factor2(n, g->n_mac, f->scratch, f->perm, f->lu, status, S(st))
+                                       : inv_factor3(n, g->n_mac, f->scratch, f->perm, f->lu, status, S(st));
   if (rc >= 0) return rc;
   if (gj_smem_bytes(n) > 227 * 1024) return MHDG_ERR_CONFIG;
   return inv_factor(n, g->n_mac, f->scratch, f->lu, status, S(st));

@@ -142,6 +142,165 @@ __global__ void __launch_bounds__(SCHUR_THREADS) k_schur(mhdg_disc g, mhdg_block
 }
 
 // --------------------------------------------------------------------------
+// k_schur_rb: the same correction, one CTA per (macro, block of SRB_NODES
+// lattice nodes).  The block's rows of S start from state_state in shared
+// memory, every (face) sub-element touching the block adds its rows there in
+// the order k_schur uses (so S is bitwise identical), and the rows are
+// written once: S costs one read of state_state and one write instead of a
+// read-modify-write of the touched rows per sub-element.
+// --------------------------------------------------------------------------
+constexpr int SRB_NODES = 4;
+
+// Cb rows of local nodes `ia` (lr[i] = local element node index, tr[i] = block row node)
+template <int D>
+__device__ __forceinline__ void schur_tile_rb(const double* T1, const double* VW, int m, int kk, int L, double* Cb,
+                                              int n, const int* tr, double sign) {
+  constexpr int NS = D + 2;
+  const int nas = m * NS, nj = (L + 3) / 4;
+  for (int task = threadIdx.x; task < nas * nj; task += blockDim.x) {
+    const int as = task / nj, j0 = (task - as * nj) * 4;
+    double acc[4][NS];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int r = 0; r < NS; ++r) acc[u][r] = 0.0;
+    for (int k = 0; k < kk; ++k) {
+      double tv[NS], vw[4];
+#pragma unroll
+      for (int r = 0; r < NS; ++r) tv[r] = T1[(r * nas + as) * kk + k];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) vw[u] = (j0 + u < L) ? VW[k * L + j0 + u] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int r = 0; r < NS; ++r) acc[u][r] += tv[r] * vw[u];
+    }
+    double* out = Cb + (size_t)(tr[as / NS] * NS + as % NS) * n + j0 * NS;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (j0 + u < L) {
+#pragma unroll
+        for (int r = 0; r < NS; ++r) out[u * NS + r] += sign * acc[u][r];
+      }
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(SCHUR_THREADS, 2) k_schur_rb(mhdg_disc g, mhdg_blocks b, double* __restrict__ S) {
+  extern __shared__ double sm[];
+  constexpr int NS = D + 2, NF = D + 1;
+  const Sz sz = make_sz<D>(g);
+  const int nrb = (sz.L + SRB_NODES - 1) / SRB_NODES;
+  const int mac = blockIdx.x / nrb, rb = blockIdx.x - mac * nrb;
+  const int I0 = rb * SRB_NODES, nI = min(SRB_NODES, sz.L - I0);
+  const int n = sz.n, L = sz.L, tid = threadIdx.x;
+  const double* ij = g.inv_jac + (size_t)mac * D * D;
+  const int kv = sz.nq * D, kf = sz.nqf * D, kmax = kv > kf ? kv : kf;
+  double* Cb = sm;                              // SRB_NODES*NS rows x n
+  double* VW = Cb + (size_t)SRB_NODES * NS * n;  // kmax x L
+  double* T1 = VW + (size_t)kmax * L;           // NS x (SRB_NODES*NS) x kmax
+  __shared__ int la[SRB_NODES], tr[SRB_NODES], cnt;
+
+  {  // the block's rows of state_state (contiguous, 16-byte vectors)
+    const double2* src = reinterpret_cast<const double2*>(b.state_state + ((size_t)mac * n + (size_t)I0 * NS) * n);
+    double2* dst = reinterpret_cast<double2*>(Cb);
+    const int nv = nI * NS * n / 2;
+    for (int i = tid; i < nv; i += blockDim.x) dst[i] = src[i];
+  }
+
+  // ---- volume sub-elements ----
+  for (int K = 0; K < sz.n_sub; ++K) {
+    if (tid == 0) {
+      int c = 0;
+      for (int a = 0; a < sz.nloc; ++a) {
+        const int I = __ldg(g.sub_conn + K * sz.nloc + a) - I0;
+        if (I >= 0 && I < nI) {
+          la[c] = a;
+          tr[c] = I;
+          ++c;
+        }
+      }
+      cnt = c;
+    }
+    __syncthreads();
+    const int m = cnt;
+    if (m == 0) continue;
+    for (int idx = tid; idx < kv * L; idx += blockDim.x) {
+      const int j = idx % L, ql = idx / L, l = ql % D, q = ql / D;
+      const double* pm = g.pm_vol + (((size_t)K * sz.nq + q) * D) * L + j;
+      double a = 0.0;
+#pragma unroll
+      for (int r = 0; r < D; ++r) a += __ldg(ij + r * D + l) * __ldg(pm + r * L);
+      VW[idx] = a;
+    }
+    const int nas = m * NS;
+    for (int idx = tid; idx < NS * nas * kv; idx += blockDim.x) {
+      const int ql = idx % kv, rest = idx / kv, as = rest % nas, rr = rest / nas;
+      const int s = as % NS, a = la[as / NS], l = ql % D, q = ql / D;
+      const double* gr = g.grad_ref + (((size_t)K * sz.nq + q) * sz.nloc + a) * D;
+      const double* W = b.wdgdq_vol + ((((size_t)mac * sz.n_sub + K) * sz.nq + q) * D * D) * NS * NS;
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        double gp = 0.0;
+#pragma unroll
+        for (int r = 0; r < D; ++r) gp += __ldg(gr + r) * __ldg(ij + r * D + k);
+        acc += gp * __ldg(W + ((k * D + l) * NS + s) * NS + rr);
+      }
+      T1[idx] = acc;
+    }
+    __syncthreads();
+    schur_tile_rb<D>(T1, VW, m, kv, L, Cb, n, tr, 1.0);
+    __syncthreads();
+  }
+  // ---- face sub-elements ----
+  for (int f = 0; f < NF; ++f) {
+    for (int T = 0; T < sz.n_tri; ++T) {
+      if (tid == 0) {
+        int c = 0;
+        for (int a = 0; a < sz.nlocf; ++a) {
+          const int I = __ldg(g.face_vol_nodes + f * sz.Lf + __ldg(g.tri_conn + T * sz.nlocf + a)) - I0;
+          if (I >= 0 && I < nI) {
+            la[c] = a;
+            tr[c] = I;
+            ++c;
+          }
+        }
+        cnt = c;
+      }
+      __syncthreads();
+      const int m = cnt;
+      if (m == 0) continue;
+      for (int idx = tid; idx < kf * L; idx += blockDim.x) {
+        const int j = idx % L, ql = idx / L, l = ql % D, q = ql / D;
+        const double* pm = g.pm_face + ((((size_t)f * sz.n_tri + T) * sz.nqf + q) * D) * L + j;
+        double a = 0.0;
+#pragma unroll
+        for (int r = 0; r < D; ++r) a += __ldg(ij + r * D + l) * __ldg(pm + r * L);
+        VW[idx] = a;
+      }
+      const int nas = m * NS;
+      for (int idx = tid; idx < NS * nas * kf; idx += blockDim.x) {
+        const int ql = idx % kf, rest = idx / kf, as = rest % nas, rr = rest / nas;
+        const int s = as % NS, a = la[as / NS], l = ql % D, q = ql / D;
+        const double* W = b.wdgdq_face +
+                          ((((size_t)mac * NF + f) * sz.n_tri * sz.nqf + T * sz.nqf + q) * D + l) * NS * NS;
+        T1[idx] = __ldg(W + s * NS + rr) * __ldg(g.phi_face + q * sz.nlocf + a);
+      }
+      __syncthreads();
+      schur_tile_rb<D>(T1, VW, m, kf, L, Cb, n, tr, -1.0);
+      __syncthreads();
+    }
+  }
+  {
+    double2* dst = reinterpret_cast<double2*>(S + ((size_t)mac * n + (size_t)I0 * NS) * n);
+    const double2* src = reinterpret_cast<const double2*>(Cb);
+    const int nv = nI * NS * n / 2;
+    for (int i = tid; i < nv; i += blockDim.x) dst[i] = src[i];
+  }
+}
+
+// --------------------------------------------------------------------------
 // batched LU with partial pivoting
 // --------------------------------------------------------------------------
 
@@ -959,6 +1118,479 @@ int inv_factor2(int n, int n_mac, double* scratch, int* piv, double* tiled, int*
   return launch_ok();
 }
 
+// --------------------------------------------------------------------------
+// k_gj3: Gauss-Jordan inverse without physical row interchanges
+// --------------------------------------------------------------------------
+// As k_gj2 (64-column panels in shared memory, 16-column sub-panels, DMMA
+// rank-16 / rank-64 updates), but the pivot of logical column k stays in its
+// physical row p_k: partial pivoting picks the largest |entry| among the rows
+// not yet used as pivots, the rows are never moved, and the identity part of
+// the composite transform sits at (p_k, k).  The in-place result M then holds
+// (P A)^-1 with row k stored in row p_k, so A^-1[i][j] = M[p_i][pi^-1(j)]
+// (k_pack_inv_gather).  This removes the row-interchange passes over the
+// matrix; each pivot step is two CTA barriers (every warp reduces the 32
+// pivot candidates itself, every thread forms the reciprocal itself).
+// --------------------------------------------------------------------------
+__global__ void __launch_bounds__(512, 1) k_gj3(int n, double* __restrict__ S, int* __restrict__ piv_out,
+                                                 int* status) {
+  extern __shared__ double sm[];
+  const int mac = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* A = S + (size_t)mac * n * n;
+  int* pivg = piv_out + (size_t)mac * n;
+  double* P = sm;                       // n x GJ2_PW panel
+  double* Bt = P + (size_t)n * GJ2_PW;  // old pivot rows (row stride GJ2_BS / 68)
+  __shared__ double cand_v[32];
+  __shared__ int cand_i[32];
+  __shared__ int pv[GJ2_NB];            // physical pivot rows of the current panel
+  constexpr int RPT = 12;               // rows per thread (n <= 32 * RPT = 384)
+  const int cl = tid & 15, rg = tid >> 4, rbeg = rg * RPT;
+  unsigned used = 0;                    // bit q: row rbeg + q is a pivot row already
+  bool singular = false;
+
+  // candidates for column `col` of P over this thread's unused rows (threads with cl == 0)
+  auto scan = [&](int col) {
+    if (cl == 0) {
+      double cb = -1.0;
+      int ci = 0x7fffffff;
+#pragma unroll
+      for (int q = 0; q < RPT; ++q) {
+        const int i = rbeg + q;
+        if (i < n && !((used >> q) & 1u)) {
+          const double a = fabs(P[i * GJ2_PW + col]);
+          if (a > cb) { cb = a; ci = i; }
+        }
+      }
+      cand_v[rg] = cb;
+      cand_i[rg] = ci;
+    }
+  };
+
+  for (int k0 = 0; k0 < n; k0 += GJ2_NB) {
+    const int nb = min(GJ2_NB, n - k0);
+    GJT(t0);
+    for (int idx = tid; idx < n * nb; idx += blockDim.x) {
+      const int i = idx / nb, c = idx - i * nb;
+      P[i * GJ2_PW + c] = A[(size_t)i * n + k0 + c];
+    }
+    __syncthreads();
+    scan(0);
+    __syncthreads();
+    GJADD(0, t0);
+    for (int js = 0; js < nb; js += 16) {
+      GJT(t1);
+      const int ns = min(16, nb - js);
+      const int c = js + cl;
+      const bool inside = cl < ns;
+      for (int j = js; j < js + ns; ++j) {
+        // pivot: every warp reduces the 32 candidates (lowest row wins ties)
+        double best = cand_v[lane];
+        int p = cand_i[lane];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double v2 = __shfl_xor_sync(MHDG_FULL, best, o);
+          const int i2 = __shfl_xor_sync(MHDG_FULL, p, o);
+          if (v2 > best || (v2 == best && i2 < p)) { best = v2; p = i2; }
+        }
+        if (!(best > 0.0)) singular = true;
+        if (singular) p = 0;
+        const double piv = P[p * GJ2_PW + j];
+        const double d = singular ? 0.0 : 1.0 / piv;
+        const double rowp_c = inside ? P[p * GJ2_PW + c] : 0.0;
+        double colj[RPT];
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) colj[q] = (rbeg + q < n) ? P[(rbeg + q) * GJ2_PW + j] : 0.0;
+        __syncthreads();  // row p and column j read by everyone before anyone writes
+        if (tid == 0) {
+          pv[j] = p;
+          pivg[k0 + j] = p;
+        }
+        if (p >= rbeg && p < rbeg + RPT) used |= 1u << (p - rbeg);
+        const bool next_col = (c == j + 1) && (j + 1 < js + ns);
+        double cb = -1.0;
+        int ci = 0x7fffffff;
+        if (inside) {
+          const double piv_c = (c == j) ? d : rowp_c * d;  // new pivot row
+#pragma unroll
+          for (int q = 0; q < RPT; ++q) {
+            const int i = rbeg + q;
+            if (i < n && i != p) {
+              const double nvl = (c == j) ? -colj[q] * d : P[i * GJ2_PW + c] - colj[q] * piv_c;
+              P[i * GJ2_PW + c] = nvl;
+              if (next_col && !((used >> q) & 1u)) {
+                const double a = fabs(nvl);
+                if (a > cb) { cb = a; ci = i; }
+              }
+            }
+          }
+          if (p >= rbeg && p < rbeg + RPT) P[p * GJ2_PW + c] = piv_c;
+        }
+        if (next_col) {
+          cand_v[rg] = cb;
+          cand_i[rg] = ci;
+        }
+        __syncthreads();
+      }
+      GJADD(1, t1);
+      GJT(t2);
+      // other panel columns c (outside [js, js+ns)): P[:, c] += (Ts - Es) Bs[:, c], Bs = old pivot rows
+      for (int idx = tid; idx < 16 * GJ2_NB; idx += blockDim.x) {
+        const int r = idx >> 6, cc = idx & 63;
+        const bool other = (cc < js || cc >= js + ns) && cc < nb && r < ns;
+        Bt[r * 68 + cc] = other ? P[pv[js + r] * GJ2_PW + cc] : 0.0;
+      }
+      __syncthreads();
+      for (int r = tid; r < ns; r += blockDim.x) P[pv[js + r] * GJ2_PW + js + r] -= 1.0;
+      __syncthreads();
+      {
+        const int g = lane >> 2, t4 = lane & 3;
+        for (int r0 = warp * 8; r0 < n; r0 += 8 * (int)(blockDim.x >> 5)) {
+          double acc[8][2];
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) {
+            const int row = r0 + g, col = 8 * jj + 2 * t4;
+            const bool ok = row < n;
+            acc[jj][0] = ok ? P[row * GJ2_PW + col] : 0.0;
+            acc[jj][1] = ok ? P[row * GJ2_PW + col + 1] : 0.0;
+          }
+#pragma unroll
+          for (int kk = 0; kk < 16; kk += 4) {
+            const int row = r0 + g;
+            const double a = (row < n && kk + t4 < ns) ? P[row * GJ2_PW + js + kk + t4] : 0.0;
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) dmma_8x8x4(acc[jj][0], acc[jj][1], a, Bt[(kk + t4) * 68 + 8 * jj + g]);
+          }
+          __syncwarp();
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) {
+            const int row = r0 + g, col = 8 * jj + 2 * t4;
+            if (row < n) {
+              if (col < js || col >= js + ns) P[row * GJ2_PW + col] = acc[jj][0];
+              if (col + 1 < js || col + 1 >= js + ns) P[row * GJ2_PW + col + 1] = acc[jj][1];
+            }
+          }
+        }
+      }
+      __syncthreads();
+      for (int r = tid; r < ns; r += blockDim.x) P[pv[js + r] * GJ2_PW + js + r] += 1.0;
+      __syncthreads();
+      if (js + 16 < nb) {
+        scan(js + 16);
+        __syncthreads();
+      }
+      GJADD(2, t2);
+    }
+    GJT(t_up);
+    for (int j = tid; j < nb; j += blockDim.x) P[pv[j] * GJ2_PW + j] -= 1.0;  // T - E
+    for (int idx = tid; idx < n * (GJ2_NB - nb); idx += blockDim.x) {
+      const int i = idx / (GJ2_NB - nb), cc = nb + idx % (GJ2_NB - nb);
+      P[i * GJ2_PW + cc] = 0.0;
+    }
+    __syncthreads();
+    // ---- update of the columns outside the panel: C += (T - E) B, B = old pivot rows ----
+    const int nrest = n - nb;
+    const int wr = (warp / 3) * 16, wc = (warp % 3) * 16;
+    const int g = lane >> 2, t4 = lane & 3;
+    for (int tc = 0; tc < nrest; tc += GJ2_TC) {
+      const int wct = min(GJ2_TC, nrest - tc);
+      for (int idx = tid; idx < GJ2_NB * GJ2_TC; idx += blockDim.x) {
+        const int r = idx / GJ2_TC, cc0 = idx % GJ2_TC;
+        const int cc = tc + cc0 < k0 ? tc + cc0 : tc + cc0 + nb;
+        Bt[r * GJ2_BS + cc0] = (cc0 < wct && r < nb) ? A[(size_t)pv[r] * n + cc] : 0.0;
+      }
+      __syncthreads();
+      if (warp < 12) {
+        int gcol[2][2];
+        bool cok[2][2];
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int col = wc + 8 * jj + 2 * t4 + e;
+            cok[jj][e] = col < wct;
+            gcol[jj][e] = tc + col < k0 ? tc + col : tc + col + nb;
+          }
+        double nxt[2][2][2];
+        auto load_c = [&](int tr, double (&cc)[2][2][2]) {
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int row = tr + wr + 8 * i + g;
+#pragma unroll
+            for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+              for (int e = 0; e < 2; ++e)
+                cc[i][jj][e] = (row < n && cok[jj][e]) ? A[(size_t)row * n + gcol[jj][e]] : 0.0;
+          }
+        };
+        load_c(0, nxt);
+        for (int tr = 0; tr < n; tr += 64) {
+          double acc[2][2][2];
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int jj = 0; jj < 2; ++jj) {
+              acc[i][jj][0] = nxt[i][jj][0];
+              acc[i][jj][1] = nxt[i][jj][1];
+            }
+          if (tr + 64 < n) load_c(tr + 64, nxt);
+#pragma unroll 8
+          for (int kk = 0; kk < GJ2_NB; kk += 4) {
+            double a[2], b[2];
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              const int row = tr + wr + 8 * i + g;
+              a[i] = row < n ? P[row * GJ2_PW + kk + t4] : 0.0;
+            }
+#pragma unroll
+            for (int jj = 0; jj < 2; ++jj) b[jj] = Bt[(kk + t4) * GJ2_BS + wc + 8 * jj + g];
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+              for (int jj = 0; jj < 2; ++jj) dmma_8x8x4(acc[i][jj][0], acc[i][jj][1], a[i], b[jj]);
+          }
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int row = tr + wr + 8 * i + g;
+#pragma unroll
+            for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+              for (int e = 0; e < 2; ++e)
+                if (row < n && cok[jj][e]) A[(size_t)row * n + gcol[jj][e]] = acc[i][jj][e];
+          }
+        }
+      }
+      __syncthreads();
+    }
+    GJADD(4, t_up);
+    GJT(t5);
+    for (int j = tid; j < nb; j += blockDim.x) P[pv[j] * GJ2_PW + j] += 1.0;
+    __syncthreads();
+    for (int idx = tid; idx < n * nb; idx += blockDim.x) {
+      const int i = idx / nb, cc = idx - i * nb;
+      A[(size_t)i * n + k0 + cc] = P[i * GJ2_PW + cc];
+    }
+    __syncthreads();
+    GJADD(5, t5);
+  }
+  if (singular && tid == 0) set_status(status, MHDG_ERR_FACTORIZATION, mac, 0, 0.0);
+}
+
+// (P A)^-1 stored with row k in physical row piv[k] -> A^-1 in the tiled layout:
+// A^-1[i][j] = M[piv[i]][inv[j]], inv = piv^-1.
+__global__ void __launch_bounds__(256) k_pack_inv_gather(int n, const double* __restrict__ F,
+                                                         const int* __restrict__ piv, double* __restrict__ out) {
+  extern __shared__ int pp[];  // piv | inv
+  int* inv = pp + n;
+  const int mac = blockIdx.x;
+  const double* A = F + (size_t)mac * n * n;
+  double* O = out + (size_t)mac * ti_size(n);
+  for (int k = threadIdx.x; k < n; k += blockDim.x) {
+    const int p = piv[(size_t)mac * n + k];
+    pp[k] = p;
+    inv[p] = k;
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
+    const int r = idx / n, c = idx % n;
+    O[ti_idx(n, r, c)] = A[(size_t)pp[r] * n + inv[c]];
+  }
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < ti_nblk(n); ++b) {
+      const int nb = ti_rows(n, b);
+      long long o = ti_block_off(n, b);
+      for (int c = 0; c < n; c += TI_CW) {
+        const int w = (n - c) < TI_CW ? n - c : TI_CW;
+        if (((long long)nb * w) & 1) O[o + (long long)nb * w] = 0.0;
+        o += ti_even((long long)nb * w);
+      }
+    }
+  }
+}
+
+int inv_factor3(int n, int n_mac, double* scratch, int* piv, double* tiled, int* status, cudaStream_t st) {
+  const size_t bytes = gj2_smem_bytes(n);
+  if (bytes > 227 * 1024 || n > 384) return -1;
+  cudaFuncSetAttribute(k_gj3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  k_gj3<<<n_mac, 512, bytes, st>>>(n, scratch, piv, status);
+  int rc = launch_ok();
+  if (rc) return rc;
+  k_pack_inv_gather<<<n_mac, 256, sizeof(int) * 2 * n, st>>>(n, scratch, piv, tiled);
+  return launch_ok();
+}
+
+// --------------------------------------------------------------------------
+// k_schur_mma: the Schur correction on the FP64 tensor cores.
+//
+// With the geometry folded into the left factor, each (face) sub-element's
+// correction is one GEMM against a macro-independent table:
+//   X[(a,s,r), j] = sum_{(q,r')} T1'[(a,s,r),(q,r')] PM[(q,r'), j],
+//   T1'[(a,s,r),(q,r')] = sum_l inv_jac[r',l] sum_k gphys[q,a,k] W[q][(k,l)][s][r],
+//   S[(conn[a], s), (j, r)] += X   (faces: -=, folded into T1').
+// One CTA per macro: W and PM staged in shared memory, T1' built there,
+// DMMA m8n8k4 tiles whose accumulators start from the S entries they update
+// (the read-modify-write of S is the MMA accumulate), sub-elements in the
+// reference order so S is deterministic.  Strides make the A (= 4 mod 16) and
+// B (= 8 mod 16) fragment loads conflict-free.
+// --------------------------------------------------------------------------
+constexpr int SCH_NT = 12, SCH_KS = 8;  // register tiles: L <= 96, (q, r') <= 32
+
+template <int D>
+struct SchurMmaDims {
+  int kv, kf, sA, MV, MF, MVp, LP, nks_v, nks_f;
+  __host__ __device__ SchurMmaDims(const mhdg_disc& g) {
+    constexpr int NS = D + 2;
+    kv = g.nq * D;
+    kf = g.nqf * D;
+    const int kmax = kv > kf ? kv : kf;
+    sA = (kmax + 3) / 4 * 4;
+    while (sA % 16 != 4) sA += 4;
+    MV = g.nloc * NS * NS;
+    MF = g.nlocf * NS * NS;
+    MVp = ((MV > MF ? MV : MF) + 7) / 8 * 8;
+    LP = (g.L + 7) / 8 * 8;
+    if (LP % 16 == 0) LP += 8;
+    nks_v = (kv + 3) / 4;
+    nks_f = (kf + 3) / 4;
+  }
+  __host__ __device__ size_t smem_doubles(const mhdg_disc& g) const {
+    constexpr int NS = D + 2;
+    const int kmax = kv > kf ? kv : kf;
+    const int nw = g.nq * D * D * NS * NS;
+    return (size_t)MVp * sA + (size_t)(kmax + 3) / 4 * 4 * LP + nw + (size_t)g.n_grad_cls * g.nq * g.nloc * D;
+  }
+};
+
+template <int D>
+__global__ void __launch_bounds__(256, 2) k_schur_mma(mhdg_disc g, mhdg_blocks b, double* __restrict__ S) {
+  extern __shared__ double sm[];
+  constexpr int NS = D + 2, NF = D + 1, NW = D * D * NS * NS;
+  const SchurMmaDims<D> dm(g);
+  const int mac = blockIdx.x, n = g.L * NS, L = g.L, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nq = g.nq, nloc = g.nloc, nqf = g.nqf, nlocf = g.nlocf;
+  const int kmaxp = ((dm.kv > dm.kf ? dm.kv : dm.kf) + 3) / 4 * 4;
+  double* Tp = sm;                                // MVp x sA   (rows (a,s,r), cols (q,r'))
+  double* PM = Tp + (size_t)dm.MVp * dm.sA;        // kmaxp x LP (rows (q,r'), cols j)
+  double* Wst = PM + (size_t)kmaxp * dm.LP;        // nq x NW (volume) / face stash
+  double* gph = Wst + (size_t)nq * NW;             // n_grad_cls x nq x nloc x D
+  double* Sm = S + (size_t)mac * n * n;
+  double ij[D][D];
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int c = 0; c < D; ++c) ij[a][c] = __ldg(g.inv_jac + (size_t)mac * D * D + a * D + c);
+
+  {  // S <- state_state
+    const double2* src = reinterpret_cast<const double2*>(b.state_state + (size_t)mac * n * n);
+    double2* dst = reinterpret_cast<double2*>(Sm);
+    for (int i = tid; i < n * n / 2; i += blockDim.x) dst[i] = src[i];
+  }
+  // physical gradients per class, zero padding of the GEMM operands
+  for (int idx = tid; idx < g.n_grad_cls * nq * nloc * D; idx += blockDim.x) {
+    const int k = idx % D, base = idx - k;
+    double v = 0.0;
+#pragma unroll
+    for (int r = 0; r < D; ++r) v += __ldg(g.grad_cls + base + r) * ij[r][k];
+    gph[idx] = v;
+  }
+  for (int idx = tid; idx < dm.MVp * dm.sA; idx += blockDim.x) Tp[idx] = 0.0;
+  for (int idx = tid; idx < kmaxp * dm.LP; idx += blockDim.x) PM[idx] = 0.0;
+  __syncthreads();  // S rows visible to every warp before the first accumulate
+
+  const int gq = lane >> 2, t4 = lane & 3;
+  // C[M x LP] = Tp[M x 4 nks] PM[4 nks x LP], accumulated into S rows; rows m -> (node, s, r).
+  // Per M tile all SCH_NT column tiles of C are loaded from S first (one memory latency per
+  // M tile), accumulated by DMMA and stored.
+  auto gemm_into_s = [&](int M, int nks, auto&& row_node) {
+    const int mtiles = (M + 7) / 8, ntiles = (L + 7) / 8;
+    for (int mt = warp; mt < mtiles; mt += 8) {
+      const int m = mt * 8 + gq;
+      const bool mok = m < M;
+      const int a = m / (NS * NS), s = (m / NS) % NS, r = m % NS;
+      double* srow = Sm + (size_t)((mok ? row_node(a) : 0) * NS + s) * n + r;
+      double af[SCH_KS];
+#pragma unroll
+      for (int ks = 0; ks < SCH_KS; ++ks) af[ks] = ks < nks ? Tp[m * dm.sA + 4 * ks + t4] : 0.0;
+      double c[SCH_NT][2];
+#pragma unroll
+      for (int nt = 0; nt < SCH_NT; ++nt) {
+        const int j0 = nt * 8 + 2 * t4;
+        c[nt][0] = (mok && nt < ntiles && j0 < L) ? srow[j0 * NS] : 0.0;
+        c[nt][1] = (mok && nt < ntiles && j0 + 1 < L) ? srow[(j0 + 1) * NS] : 0.0;
+      }
+#pragma unroll
+      for (int nt = 0; nt < SCH_NT; ++nt)
+        if (nt < ntiles) {
+#pragma unroll
+          for (int ks = 0; ks < SCH_KS; ++ks)
+            if (ks < nks) dmma_8x8x4(c[nt][0], c[nt][1], af[ks], PM[(4 * ks + t4) * dm.LP + nt * 8 + gq]);
+        }
+#pragma unroll
+      for (int nt = 0; nt < SCH_NT; ++nt) {
+        const int j0 = nt * 8 + 2 * t4;
+        if (mok && nt < ntiles && j0 < L) srow[j0 * NS] = c[nt][0];
+        if (mok && nt < ntiles && j0 + 1 < L) srow[(j0 + 1) * NS] = c[nt][1];
+      }
+    }
+  };
+
+  // ---- volume sub-elements ----
+  for (int K = 0; K < g.n_sub; ++K) {
+    const double* W = b.wdgdq_vol + ((size_t)mac * g.n_sub + K) * nq * NW;
+    for (int i = tid; i < nq * NW; i += blockDim.x) Wst[i] = W[i];
+    for (int idx = tid; idx < dm.kv * L; idx += blockDim.x) {
+      const int j = idx % L, qr = idx / L;
+      PM[qr * dm.LP + j] = __ldg(g.pm_vol + ((size_t)K * dm.kv + qr) * L + j);
+    }
+    __syncthreads();
+    const int cls = __ldg(g.grad_cls_of + K);
+    for (int idx = tid; idx < dm.MV * dm.kv; idx += blockDim.x) {
+      const int qr = idx % dm.kv, m = idx / dm.kv;
+      const int q = qr / D, rp = qr % D, a = m / (NS * NS), s = (m / NS) % NS, r = m % NS;
+      const double* gp = gph + ((cls * nq + q) * nloc + a) * D;
+      const double* w = Wst + q * NW + s * NS + r;
+      double v = 0.0;
+#pragma unroll
+      for (int l = 0; l < D; ++l) {
+        double t = 0.0;
+#pragma unroll
+        for (int k = 0; k < D; ++k) t += gp[k] * w[(k * D + l) * NS * NS];
+        v += ij[rp][l] * t;
+      }
+      Tp[m * dm.sA + qr] = v;
+    }
+    __syncthreads();
+    gemm_into_s(dm.MV, dm.nks_v, [&](int a) { return __ldg(g.sub_conn + K * nloc + a); });
+    __syncthreads();
+  }
+  // ---- face sub-elements (sign folded into T1') ----
+  for (int idx = tid; idx < dm.MVp * dm.sA; idx += blockDim.x) Tp[idx] = 0.0;
+  for (int idx = tid; idx < kmaxp * dm.LP; idx += blockDim.x) PM[idx] = 0.0;
+  __syncthreads();
+  for (int f = 0; f < NF; ++f) {
+    for (int T = 0; T < g.n_tri; ++T) {
+      const double* W = b.wdgdq_face + (((size_t)mac * NF + f) * g.n_tri + T) * nqf * D * NS * NS;
+      for (int i = tid; i < nqf * D * NS * NS; i += blockDim.x) Wst[i] = W[i];
+      for (int idx = tid; idx < dm.kf * L; idx += blockDim.x) {
+        const int j = idx % L, qr = idx / L;
+        PM[qr * dm.LP + j] = __ldg(g.pm_face + (((size_t)f * g.n_tri + T) * dm.kf + qr) * L + j);
+      }
+      __syncthreads();
+      for (int idx = tid; idx < dm.MF * dm.kf; idx += blockDim.x) {
+        const int qr = idx % dm.kf, m = idx / dm.kf;
+        const int q = qr / D, rp = qr % D, a = m / (NS * NS), s = (m / NS) % NS, r = m % NS;
+        double v = 0.0;
+#pragma unroll
+        for (int l = 0; l < D; ++l) v += ij[rp][l] * Wst[((q * D + l) * NS + s) * NS + r];
+        Tp[m * dm.sA + qr] = -v * __ldg(g.phi_face + q * nlocf + a);
+      }
+      __syncthreads();
+      gemm_into_s(dm.MF, dm.nks_f, [&](int a) {
+        return __ldg(g.face_vol_nodes + f * g.Lf + __ldg(g.tri_conn + T * nlocf + a));
+      });
+      __syncthreads();
+    }
+  }
+}
+
 int inv_factor(int n, int n_mac, double* scratch, double* tiled, int* status, cudaStream_t st) {
   const size_t bytes = gj_smem_bytes(n);
   if (bytes > 227 * 1024) return MHDG_ERR_CONFIG;
@@ -974,11 +1606,33 @@ int inv_factor(int n, int n_mac, double* scratch, double* tiled, int* status, cu
 // host launchers
 // --------------------------------------------------------------------------
 
+int g_schur_variant = 0;  // 0: tensor cores, 1: row blocks, 2: per-macro FFMA (A/B knob)
+
 template <int D>
 int schur_matrix(const mhdg_disc& g, const mhdg_blocks& b, double* S, cudaStream_t st) {
   constexpr int NS = D + 2;
   const int kv = g.nq * D, kf = g.nqf * D, kmax = kv > kf ? kv : kf;
   const int rmax = (g.nloc > g.nlocf ? g.nloc : g.nlocf) * NS;
+  const int n = g.L * NS;
+  {  // tensor-core kernel when its operands fit (k-steps <= 16)
+    const SchurMmaDims<D> dm(g);
+    const size_t mb = sizeof(double) * dm.smem_doubles(g);
+    if (g_schur_variant == 0 && n % 2 == 0 && dm.nks_v <= SCH_KS && dm.nks_f <= SCH_KS && g.L <= 8 * SCH_NT &&
+        mb <= 227 * 1024 && g.grad_cls) {
+      if (mb > 48 * 1024) cudaFuncSetAttribute(k_schur_mma<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mb);
+      k_schur_mma<D><<<g.n_mac, 256, mb, st>>>(g, b, S);
+      return launch_ok();
+    }
+  }
+  if (g_schur_variant <= 1 && (n * SRB_NODES * NS) % 2 == 0 && n % 2 == 0) {  // row-block kernel
+    const size_t rb = sizeof(double) * ((size_t)SRB_NODES * NS * n + (size_t)kmax * g.L + (size_t)NS * SRB_NODES * NS * kmax);
+    if (rb <= 227 * 1024) {
+      if (rb > 48 * 1024) cudaFuncSetAttribute(k_schur_rb<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rb);
+      const int nrb = (g.L + SRB_NODES - 1) / SRB_NODES;
+      k_schur_rb<D><<<g.n_mac * nrb, SCHUR_THREADS, rb, st>>>(g, b, S);
+      return launch_ok();
+    }
+  }
   const size_t bytes = sizeof(double) * ((size_t)NS * rmax * kmax + (size_t)kmax * g.L);
   if (bytes > 48 * 1024) cudaFuncSetAttribute(k_schur<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   k_schur<D><<<g.n_mac, SCHUR_THREADS, bytes, st>>>(g, b, S);
