@@ -1286,72 +1286,86 @@ __global__ void __launch_bounds__(512, 1) k_gj3(int n, double* __restrict__ S, i
       P[i * GJ2_PW + cc] = 0.0;
     }
     __syncthreads();
-    // ---- update of the columns outside the panel: C += (T - E) B, B = old pivot rows ----
+    // ---- update of the columns outside the panel: C += (T - E) B, B = old pivot rows.
+    //      128 x 48 C passes: warp (wm, wn) owns rows 16 wm.. (two 8-row tiles) of the
+    //      3 column tiles 24 wn.. -- 6 independent DMMA accumulators; C of the next
+    //      pass and the next chunk's pivot rows are prefetched into registers ----
     const int nrest = n - nb;
-    const int wr = (warp / 3) * 16, wc = (warp % 3) * 16;
+    const int wm = warp >> 1, wn = warp & 1;
     const int g = lane >> 2, t4 = lane & 3;
+    constexpr int BPT = GJ2_NB * GJ2_TC / 512;  // pivot-row tile entries per thread
+    double bnext[BPT];
+    auto load_b = [&](int tc) {
+      const int wct = min(GJ2_TC, nrest - tc);
+#pragma unroll
+      for (int u = 0; u < BPT; ++u) {
+        const int idx = tid + 512 * u, r = idx / GJ2_TC, cc0 = idx % GJ2_TC;
+        const int cc = tc + cc0 < k0 ? tc + cc0 : tc + cc0 + nb;
+        bnext[u] = (cc0 < wct && r < nb) ? A[(size_t)pv[r] * n + cc] : 0.0;
+      }
+    };
+    if (nrest > 0) load_b(0);
     for (int tc = 0; tc < nrest; tc += GJ2_TC) {
       const int wct = min(GJ2_TC, nrest - tc);
-      for (int idx = tid; idx < GJ2_NB * GJ2_TC; idx += blockDim.x) {
-        const int r = idx / GJ2_TC, cc0 = idx % GJ2_TC;
-        const int cc = tc + cc0 < k0 ? tc + cc0 : tc + cc0 + nb;
-        Bt[r * GJ2_BS + cc0] = (cc0 < wct && r < nb) ? A[(size_t)pv[r] * n + cc] : 0.0;
+#pragma unroll
+      for (int u = 0; u < BPT; ++u) {
+        const int idx = tid + 512 * u;
+        Bt[(idx / GJ2_TC) * GJ2_BS + idx % GJ2_TC] = bnext[u];
       }
       __syncthreads();
-      if (warp < 12) {
-        int gcol[2][2];
-        bool cok[2][2];
+      int gcol[3][2];
+      bool cok[3][2];
 #pragma unroll
-        for (int jj = 0; jj < 2; ++jj)
+      for (int jj = 0; jj < 3; ++jj)
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int col = wc + 8 * jj + 2 * t4 + e;
-            cok[jj][e] = col < wct;
-            gcol[jj][e] = tc + col < k0 ? tc + col : tc + col + nb;
+        for (int e = 0; e < 2; ++e) {
+          const int col = wn * 24 + 8 * jj + 2 * t4 + e;
+          cok[jj][e] = col < wct;
+          gcol[jj][e] = tc + col < k0 ? tc + col : tc + col + nb;
+        }
+      auto load_c = [&](int tr, double (&cc)[2][3][2]) {
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int row = tr + wm * 16 + 8 * i + g;
+#pragma unroll
+          for (int jj = 0; jj < 3; ++jj)
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+              cc[i][jj][e] = (row < n && cok[jj][e]) ? A[(size_t)row * n + gcol[jj][e]] : 0.0;
+        }
+      };
+      double nx[2][3][2];
+      load_c(0, nx);
+      if (tc + GJ2_TC < nrest) load_b(tc + GJ2_TC);
+      for (int tr = 0; tr < n; tr += 128) {
+        double acc[2][3][2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int jj = 0; jj < 3; ++jj) {
+            acc[i][jj][0] = nx[i][jj][0];
+            acc[i][jj][1] = nx[i][jj][1];
           }
-        double nxt[2][2][2];
-        auto load_c = [&](int tr, double (&cc)[2][2][2]) {
-#pragma unroll
-          for (int i = 0; i < 2; ++i) {
-            const int row = tr + wr + 8 * i + g;
-#pragma unroll
-            for (int jj = 0; jj < 2; ++jj)
-#pragma unroll
-              for (int e = 0; e < 2; ++e)
-                cc[i][jj][e] = (row < n && cok[jj][e]) ? A[(size_t)row * n + gcol[jj][e]] : 0.0;
-          }
-        };
-        load_c(0, nxt);
-        for (int tr = 0; tr < n; tr += 64) {
-          double acc[2][2][2];
-#pragma unroll
-          for (int i = 0; i < 2; ++i)
-#pragma unroll
-            for (int jj = 0; jj < 2; ++jj) {
-              acc[i][jj][0] = nxt[i][jj][0];
-              acc[i][jj][1] = nxt[i][jj][1];
-            }
-          if (tr + 64 < n) load_c(tr + 64, nxt);
-#pragma unroll 8
+        if (tr + 128 < n) load_c(tr + 128, nx);
+        const int row0 = tr + wm * 16 + g;
+        if (tr + wm * 16 < n) {
+#pragma unroll 4
           for (int kk = 0; kk < GJ2_NB; kk += 4) {
-            double a[2], b[2];
+            double a[2], bb[3];
 #pragma unroll
-            for (int i = 0; i < 2; ++i) {
-              const int row = tr + wr + 8 * i + g;
-              a[i] = row < n ? P[row * GJ2_PW + kk + t4] : 0.0;
-            }
+            for (int i = 0; i < 2; ++i) a[i] = row0 + 8 * i < n ? P[(row0 + 8 * i) * GJ2_PW + kk + t4] : 0.0;
 #pragma unroll
-            for (int jj = 0; jj < 2; ++jj) b[jj] = Bt[(kk + t4) * GJ2_BS + wc + 8 * jj + g];
+            for (int jj = 0; jj < 3; ++jj) bb[jj] = Bt[(kk + t4) * GJ2_BS + wn * 24 + 8 * jj + g];
 #pragma unroll
             for (int i = 0; i < 2; ++i)
 #pragma unroll
-              for (int jj = 0; jj < 2; ++jj) dmma_8x8x4(acc[i][jj][0], acc[i][jj][1], a[i], b[jj]);
+              for (int jj = 0; jj < 3; ++jj) dmma_8x8x4(acc[i][jj][0], acc[i][jj][1], a[i], bb[jj]);
           }
 #pragma unroll
           for (int i = 0; i < 2; ++i) {
-            const int row = tr + wr + 8 * i + g;
+            const int row = row0 + 8 * i;
 #pragma unroll
-            for (int jj = 0; jj < 2; ++jj)
+            for (int jj = 0; jj < 3; ++jj)
 #pragma unroll
               for (int e = 0; e < 2; ++e)
                 if (row < n && cok[jj][e]) A[(size_t)row * n + gcol[jj][e]] = acc[i][jj][e];
