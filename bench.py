@@ -84,6 +84,37 @@ def algorithmic_bytes_per_macro(disc):
                 + nf * m ** (d - 1) * nqf * d * ns * ns + 2 * ltr + (1 + d * d + nf * d + 2 * nf)) + 4 * ltr
 
 
+def apply_kernel_bytes(disc):
+    """Algorithmic HBM bytes per launch of each apply kernel (split apply): the
+    B_ref terms each kernel streams plus the hand-off vectors between them."""
+    d, ns, nf, L, Lf, m = disc.dim, disc.ns, disc.nf, disc.L, disc.Lf, disc.mesh.m
+    nq, nqf = disc.rm.n_quad, disc.rm.n_quad_face
+    n, bs, ltr = L * ns, Lf * ns, nf * Lf * ns
+    npad = n + (n & 1)
+    from paper_2402_11361_b200 import _lib
+
+    si_factor = int(_lib.lib().mhdg_packed_lu_size(n))
+    wv, wf = m**d * nq * d * d * ns * ns, nf * m ** (d - 1) * nqf * d * ns * ns
+    geom = 1 + d * d + nf * d + nf
+    M = disc.n_mac
+    return {
+        "apply_pre": M * (8 * (2 * nf * bs * bs + wv + wf + ltr + npad + 2 * ltr + geom) + 4 * ltr),
+        "apply_si": M * 8 * (si_factor + 2 * npad),
+        "apply_post": M * 8 * (nf * bs * bs + wf + npad + 2 * ltr + ltr + nf),
+        "face_reduce": disc.n_trace * (3 * 8 + 2 * 4),
+    }
+
+
+def condense_executed_flops_per_macro(disc):
+    """Flops the condensation kernels execute per macro: the Schur GEMMs on the
+    tensor cores (k_schur_mma) and the explicit Gauss-Jordan inverse (2 n^3)."""
+    d, ns, nf, L = disc.dim, disc.ns, disc.nf, disc.L
+    rm = disc.rm
+    schur = 2 * (rm.n_loc * ns * ns) * (rm.n_quad * d) * L * rm.n_sub
+    schur += 2 * (rm.n_loc_face * ns * ns) * (rm.n_quad_face * d) * L * nf * rm.n_tri
+    return {"schur": schur, "factor": 2 * (L * ns) ** 3}
+
+
 def condense_flops_per_macro(disc):
     """F_cond = 2 d L^3 ns^2 + (2/3) (L ns)^3."""
     d, L, ns = disc.dim, disc.L, disc.ns
@@ -99,6 +130,8 @@ def measured_peaks():
 
 
 def committed_traffic():
+    """ncu dram__bytes_read.sum + dram__bytes_write.sum per launch, from the
+    committed profiles (profiles/traffic.json)."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
             return json.load(fh)
@@ -307,13 +340,17 @@ def run_gpu(args, rank, world):
 
     # ---- assembly (one Jacobian assembly, timed) ----
     torch.cuda.synchronize()
-    blocks, _ = A.jacobian(top, fields, ctx)  # warm (also the real one)
+    blocks, _ = A.jacobian(top, fields, ctx)  # warm
+    del blocks  # the timed call reuses the cached block storage instead of allocating 11.5 GB
+    torch.cuda.synchronize()
     a0, a1 = ev(), ev()
-    a0.record()
-    blocks, _ = A.jacobian(top, fields, ctx)
-    a1.record()
-    a1.synchronize()
+    with _lib.Timeline(16) as tl_asm:
+        a0.record()
+        blocks, _ = A.jacobian(top, fields, ctx)
+        a1.record()
+        a1.synchronize()
     t_asm = a0.elapsed_time(a1) / 1e3
+    t_asm_k = tl_asm.ms.get("assemble", 0.0) / 1e3
 
     # ---- condensation: Schur correction + batched LU, timed ----
     cond = CondensedSchur.allocate(blocks)  # this rank's macros (the slab when N > 1)
@@ -322,15 +359,17 @@ def run_gpu(args, rank, world):
     cond.refactor_async(status)
     torch.cuda.synchronize()
     c_times = []
-    for _ in range(3):
-        c0, c1 = ev(), ev()
-        c0.record()
-        cond.refactor_async(status)
-        c1.record()
-        c1.synchronize()
-        c_times.append(c0.elapsed_time(c1) / 1e3)
+    with _lib.Timeline(64) as tl_cond:
+        for _ in range(3):
+            c0, c1 = ev(), ev()
+            c0.record()
+            cond.refactor_async(status)
+            c1.record()
+            c1.synchronize()
+            c_times.append(c0.elapsed_time(c1) / 1e3)
     A.raise_status(status, "condense")
     t_cond = float(np.median(c_times))
+    cond_k = {k: tl_cond.ms[k] / tl_cond.counts[k] / 1e3 for k in ("schur", "factor", "pack") if k in tl_cond.ms}
 
     # ---- applies ----
     K, W = args.steps, args.warmup
@@ -341,39 +380,40 @@ def run_gpu(args, rank, world):
     y_loc = torch.empty(dd.n_local_trace, dtype=torch.float64, device="cuda")
     st = current_stream()
 
-    def apply_split(x, ev0, ev1):
+    def apply_split(x):
         """One trace-operator apply; with slabs: forward halo, local apply,
-        face reduce, reverse halo (DistCondensed.apply_trace, split so the
-        streamed kernel is timed on its own)."""
+        face reduce, reverse halo (DistCondensed.apply_trace)."""
         xl = ddisc.forward(x) if ddisc is not None else x
-        ev0.record()
         _lib.check(L.mhdg_apply_trace_local(dd.c, blocks.c, cond._fac, _lib.ptr(xl), _lib.ptr(y_loc), st), "apply")
-        ev1.record()
         _lib.check(L.mhdg_face_reduce(dd.c, _lib.ptr(y_loc), _lib.ptr(y_face), st), "reduce")
         if ddisc is not None:
             y.copy_(ddisc.reverse(y_face))
 
     clk = Clocks(local).__enter__()
     for i in range(W):
-        apply_split(xs[i], ev(), ev())
+        apply_split(xs[i])
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
-    kev = [(ev(), ev()) for _ in range(K)]
     launches0 = L.mhdg_launch_count()
     t0, t1 = ev(), ev()
     torch.cuda.synchronize()
-    t0.record()
-    for i in range(K):
-        apply_split(xs[W + i], *kev[i])
-    t1.record()
-    torch.cuda.synchronize()
+    # every library kernel in the timed region is bracketed by CUDA events on its
+    # own (this) stream: per-kernel averages for the roofline
+    with _lib.Timeline(8 * K + 64) as tl_apply:
+        t0.record()
+        for i in range(K):
+            apply_split(xs[W + i])
+        t1.record()
+        torch.cuda.synchronize()
     launches = L.mhdg_launch_count() - launches0
     clk.__exit__(None, None, None)
     t_apply = t0.elapsed_time(t1) / 1e3
     if dist:
         t_apply = _max_over_ranks(dist, t_apply)
-    k_apply = float(np.mean([a.elapsed_time(b) / 1e3 for a, b in kev]))
+    kern_s = {k: tl_apply.ms[k] / tl_apply.counts[k] / 1e3 for k in tl_apply.ms}
+    local_kernels = [k for k in ("apply_pre", "apply_si", "apply_post", "apply_fused", "apply_generic") if k in kern_s]
+    k_apply = sum(kern_s[k] for k in local_kernels)
 
     # ---- e2e through the public API with pinned host buffers ----
     xh = torch.empty(n_own, dtype=torch.float64, pin_memory=True)
@@ -402,10 +442,26 @@ def run_gpu(args, rank, world):
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     fp64 = fp64_gemm_peak(torch) if rank == 0 else None
     b_mac = algorithmic_bytes_per_macro(disc)
-    achieved = b_mac * disc.n_mac / k_apply / 1e9
-    traffic = committed_traffic().get("apply_local_dram_bytes_per_launch")
+    achieved_local = b_mac * disc.n_mac / k_apply / 1e9
+    traffic = committed_traffic()
+    kbytes = apply_kernel_bytes(disc)
+    kernels = {}
+    for k, sec in kern_s.items():
+        entry = {"avg_launch_s": sec, "launches_per_step": tl_apply.counts[k] / K}
+        if k in kbytes:
+            gbs = kbytes[k] / sec / 1e9
+            entry.update({"algorithmic_bytes_per_launch": kbytes[k], "achieved_gbs": gbs, "frac": gbs / hbm})
+        kernels[k] = entry
+    dom = max(kern_s, key=kern_s.get)  # dominant kernel by time
+    dom_name = {"apply_si": "k_si_stream<2,4,3> (TMA-streamed S^-1 apply)",
+                "apply_pre": "k_apply_stream<2,4,3,pre>", "apply_post": "k_apply_stream<2,4,3,post>",
+                "apply_fused": "k_apply_stream<2,4,3,fused>", "apply_generic": "k_apply_local<2>"}.get(dom, dom)
+    dom_bytes = kbytes.get(dom, b_mac * disc.n_mac)
+    achieved = dom_bytes / kern_s[dom] / 1e9
     f_mac = condense_flops_per_macro(disc)
     cond_tf = f_mac * disc.n_mac / t_cond / 1e12
+    fx = condense_executed_flops_per_macro(disc)
+    exec_tf = (fx["schur"] + fx["factor"]) * disc.n_mac / t_cond / 1e12
 
     n_dofs_job = world * n_own if ddisc is None else ddisc.global_mesh.n_faces * disc.Lf * disc.ns
     value = n_dofs_job * K / t_apply
@@ -421,17 +477,29 @@ def run_gpu(args, rank, world):
                                    "face halos over NCCL P2P)") if world > 1 else "single",
                    "l2": "inputs larger than L2 (each apply streams ~%.1f GB of operator data)"
                          % (b_mac * disc.n_mac / 1e9)},
-        "roofline": {"kernel": "k_apply_stream<2,4,3> (TMA-streamed apply, C2 specialisation)", "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                     "frac": achieved / hbm, "traffic": traffic,
-                     "algorithmic_bytes_per_launch": b_mac * disc.n_mac, "avg_launch_s": k_apply,
+        "roofline": {"kernel": dom_name, "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": achieved / hbm, "traffic": traffic.get(dom + "_dram_bytes_per_launch"),
+                     "algorithmic_bytes_per_launch": dom_bytes, "avg_launch_s": kern_s[dom],
+                     "share_of_step": kern_s[dom] / (t_apply / K),
+                     "timing": "CUDA events around every library kernel on its stream (mhdg_timeline)",
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"},
+        "apply_local": {"what": "pre + S^-1 stream + post kernels against B_ref (SURVEY 8d)",
+                        "achieved": achieved_local, "unit": "GB/s", "frac": achieved_local / hbm,
+                        "algorithmic_bytes_per_launch": b_mac * disc.n_mac, "seconds": k_apply,
+                        "traffic": traffic.get("apply_local_dram_bytes_per_launch")},
+        "apply_kernels": kernels,
         "condense": {"metric": "macro-elements condensed/s", "value": disc.n_mac / t_cond, "unit": "macros/s",
-                     "seconds": t_cond, "flops_per_macro": f_mac,
+                     "seconds": t_cond, "kernels_s": cond_k, "flops_per_macro": f_mac,
                      "roofline": {"bound": "fp64", "achieved": cond_tf, "peak": fp64, "unit": "TFLOP/s",
                                   "frac": (cond_tf / fp64) if fp64 else None,
-                                  "peak_source": "cuBLAS DGEMM 8192^3 measured in this run"}},
+                                  "flops": "canonical F_cond = 2dL^3ns^2 + (2/3)(L ns)^3 (SURVEY 8d)",
+                                  "peak_source": "cuBLAS DGEMM 8192^3 measured in this run"},
+                     "executed": {"flops_per_macro": fx, "achieved_tflops": exec_tf,
+                                  "frac": (exec_tf / fp64) if fp64 else None,
+                                  "note": "S^-1 is formed explicitly (the reference's np.linalg.inv): 2 n^3, "
+                                          "3x the LU term of F_cond"}},
         "assembly": {"metric": "macro-elements assembled/s (Jacobian + residual)", "value": disc.n_mac / t_asm,
-                     "seconds": t_asm},
+                     "seconds": t_asm, "kernel_seconds": t_asm_k},
         "e2e": {"value": n_dofs_job / t_e2e, "unit": "DOF-applies/s",
                 "h2d_bytes_per_step": 8 * n_dofs_job, "d2h_bytes_per_step": 8 * n_dofs_job},
         "gpu_launches": int(launches),

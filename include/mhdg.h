@@ -151,6 +151,15 @@ typedef struct {
 /* doubles of mhdg_factors.work for this discretization */
 long long mhdg_apply_work_size(const mhdg_disc *disc);
 
+/* Per-kernel timeline: while enabled, the library records a CUDA event pair
+   around each of its kernels on the caller's stream (capacity = max records).
+   mhdg_timeline_end synchronises, disables recording and returns, per slot,
+   the summed milliseconds and the record counts (16 slots: 0 apply pre,
+   1 apply S^-1 stream, 2 apply post, 3 fused apply, 4 generic apply, 5 face
+   reduce, 6 Schur complement, 7 inverse factor, 8 factor tiling, 9 assembly). */
+int mhdg_timeline_begin(int capacity);
+int mhdg_timeline_end(double *ms, int *counts);
+
 /* Gauss-Jordan variant of mhdg_lu_factor: 3 (default) keeps pivot rows in
    place, 2 interchanges rows (the earlier kernel).  For A/B measurements. */
 void mhdg_set_factor_variant(int v);

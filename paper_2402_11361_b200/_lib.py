@@ -113,6 +113,10 @@ def lib():
         L.mhdg_set_factor_variant.restype = None
         L.mhdg_set_schur_variant.argtypes = [C.c_int]
         L.mhdg_set_schur_variant.restype = None
+        L.mhdg_timeline_begin.argtypes = [C.c_int]
+        L.mhdg_timeline_begin.restype = C.c_int
+        L.mhdg_timeline_end.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_int)]
+        L.mhdg_timeline_end.restype = C.c_int
         _lib = L
     return _lib
 
@@ -123,8 +127,31 @@ EXPORTED = (
     "mhdg_gradient_refresh", "mhdg_precond_build", "mhdg_precond_apply", "mhdg_launch_count",
     "mhdg_packed_lu_size", "mhdg_set_stream_enabled", "mhdg_precond_build_ext", "mhdg_side_blocks",
     "mhdg_apply_work_size", "mhdg_set_apply_split", "mhdg_set_factor_variant",
-    "mhdg_set_schur_variant",
+    "mhdg_set_schur_variant", "mhdg_timeline_begin", "mhdg_timeline_end",
 )
+
+
+TIMELINE_SLOTS = ("apply_pre", "apply_si", "apply_post", "apply_fused", "apply_generic", "face_reduce",
+                  "schur", "factor", "pack", "assemble")
+
+
+class Timeline:
+    """Per-kernel CUDA-event timeline of the library's launches (mhdg_timeline_*)."""
+
+    def __init__(self, capacity: int = 4096):
+        self.capacity = capacity
+        self.ms, self.counts = {}, {}
+
+    def __enter__(self):
+        check(lib().mhdg_timeline_begin(self.capacity), "mhdg_timeline_begin")
+        return self
+
+    def __exit__(self, *exc):
+        ms, cnt = (C.c_double * 16)(), (C.c_int * 16)()
+        check(lib().mhdg_timeline_end(ms, cnt), "mhdg_timeline_end")
+        for i, name in enumerate(TIMELINE_SLOTS):
+            if cnt[i]:
+                self.ms[name], self.counts[name] = ms[i], cnt[i]
 
 
 def check(rc: int, what: str) -> None:

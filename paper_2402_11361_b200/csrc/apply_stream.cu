@@ -958,12 +958,24 @@ extern "C" void mhdg_set_apply_split(int on) { g_split = on; }
 template <class C>
 static int launch_apply(const mhdg_disc& g, const mhdg_blocks& b, const mhdg_factors& f, const double* x,
                         double* y_loc, cudaStream_t st) {
-  if (!f.work || !g_split) return launch_stream<C, MHDG_STAGES, 0>(g, b, f, x, y_loc, st);
+  if (!f.work || !g_split) {
+    tl_begin(TL_APPLY_FUSED, st);
+    const int rc0 = launch_stream<C, MHDG_STAGES, 0>(g, b, f, x, y_loc, st);
+    tl_end(TL_APPLY_FUSED, st);
+    return rc0;
+  }
+  tl_begin(TL_APPLY_PRE, st);
   int rc = launch_stream<C, MHDG_STAGES, 1>(g, b, f, x, y_loc, st);
+  tl_end(TL_APPLY_PRE, st);
   if (rc) return rc;
+  tl_begin(TL_APPLY_SI, st);
   rc = launch_si<C>(g, f, st);
+  tl_end(TL_APPLY_SI, st);
   if (rc) return rc;
-  return launch_stream<C, MHDG_STAGES, 2>(g, b, f, x, y_loc, st);
+  tl_begin(TL_APPLY_POST, st);
+  rc = launch_stream<C, MHDG_STAGES, 2>(g, b, f, x, y_loc, st);
+  tl_end(TL_APPLY_POST, st);
+  return rc;
 }
 
 #ifdef MHDG_STREAM_PROFILE

@@ -34,7 +34,64 @@ using namespace mhdg;
 
 static inline cudaStream_t S(void* s) { return (cudaStream_t)s; }
 
+// ---- per-kernel timeline ----
+namespace mhdg {
+static bool g_tl_on = false;
+static int g_tl_cap = 0, g_tl_used = 0;
+static cudaEvent_t* g_tl_ev = nullptr;  // 2 per record
+static int* g_tl_slot = nullptr;
+static int g_tl_open[TL_NSLOTS];
+
+void tl_begin(int slot, cudaStream_t st) {
+  if (!g_tl_on || g_tl_used >= g_tl_cap) return;
+  g_tl_open[slot] = g_tl_used;
+  g_tl_slot[g_tl_used] = slot;
+  cudaEventRecord(g_tl_ev[2 * g_tl_used], st);
+  ++g_tl_used;
+}
+
+void tl_end(int slot, cudaStream_t st) {
+  if (!g_tl_on || g_tl_open[slot] < 0) return;
+  cudaEventRecord(g_tl_ev[2 * g_tl_open[slot] + 1], st);
+  g_tl_open[slot] = -1;
+}
+}  // namespace mhdg
+
 extern "C" {
+
+int mhdg_timeline_begin(int capacity) {
+  if (capacity > g_tl_cap) {
+    for (int i = 0; i < 2 * g_tl_cap; ++i) cudaEventDestroy(g_tl_ev[i]);
+    delete[] g_tl_ev;
+    delete[] g_tl_slot;
+    g_tl_ev = new cudaEvent_t[2 * capacity];
+    g_tl_slot = new int[capacity];
+    for (int i = 0; i < 2 * capacity; ++i)
+      if (cudaEventCreate(&g_tl_ev[i]) != cudaSuccess) return MHDG_ERR_CUDA;
+    g_tl_cap = capacity;
+  }
+  g_tl_used = 0;
+  for (int i = 0; i < TL_NSLOTS; ++i) g_tl_open[i] = -1;
+  g_tl_on = true;
+  return MHDG_OK;
+}
+
+int mhdg_timeline_end(double* ms, int* counts) {
+  g_tl_on = false;
+  for (int i = 0; i < TL_NSLOTS; ++i) {
+    ms[i] = 0.0;
+    counts[i] = 0;
+  }
+  if (g_tl_used && cudaEventSynchronize(g_tl_ev[2 * g_tl_used - 1]) != cudaSuccess) return MHDG_ERR_CUDA;
+  for (int r = 0; r < g_tl_used; ++r) {
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, g_tl_ev[2 * r], g_tl_ev[2 * r + 1]) != cudaSuccess) return MHDG_ERR_CUDA;
+    ms[g_tl_slot[r]] += t;
+    counts[g_tl_slot[r]] += 1;
+  }
+  return MHDG_OK;
+}
+
 
 long long mhdg_launch_count(void) { return g_launches; }
 
@@ -55,18 +112,25 @@ int mhdg_apply_trace_local(const mhdg_disc* g, const mhdg_blocks* b, const mhdg_
     const int rc = apply_stream(*g, *b, *f, x, y_loc, S(st));
     if (rc >= 0) return rc;
   }
-  return DISPATCH(g, apply_local<2>(*g, *b, *f, x, y_loc, S(st)), apply_local<3>(*g, *b, *f, x, y_loc, S(st)));
+  tl_begin(TL_APPLY_GENERIC, S(st));
+  const int rc2 =
+      DISPATCH(g, apply_local<2>(*g, *b, *f, x, y_loc, S(st)), apply_local<3>(*g, *b, *f, x, y_loc, S(st)));
+  tl_end(TL_APPLY_GENERIC, S(st));
+  return rc2;
 }
 
 int mhdg_face_reduce(const mhdg_disc* g, const double* y_loc, double* y, void* st) {
-  return face_reduce(*g, y_loc, nullptr, 0.0, y, S(st));
+  tl_begin(TL_FACE_REDUCE, S(st));
+  const int rc = face_reduce(*g, y_loc, nullptr, 0.0, y, S(st));
+  tl_end(TL_FACE_REDUCE, S(st));
+  return rc;
 }
 
 int mhdg_apply_trace(const mhdg_disc* g, const mhdg_blocks* b, const mhdg_factors* f, const double* x, double* y,
                      double* y_loc, void* st) {
   int rc = mhdg_apply_trace_local(g, b, f, x, y_loc, st);
   if (rc) return rc;
-  return face_reduce(*g, y_loc, nullptr, 0.0, y, S(st));
+  return mhdg_face_reduce(g, y_loc, y, st);
 }
 
 int mhdg_condensed_rhs(const mhdg_disc* g, const mhdg_blocks* b, const mhdg_factors* f, const double* Rg,
@@ -87,7 +151,11 @@ int mhdg_gradient_refresh(const mhdg_disc* g, const double* u, const double* uha
 }
 
 int mhdg_schur_matrix(const mhdg_disc* g, const mhdg_blocks* b, const mhdg_factors* f, void* st) {
-  return DISPATCH(g, schur_matrix<2>(*g, *b, f->scratch, S(st)), schur_matrix<3>(*g, *b, f->scratch, S(st)));
+  tl_begin(TL_SCHUR, S(st));
+  const int rc =
+      DISPATCH(g, schur_matrix<2>(*g, *b, f->scratch, S(st)), schur_matrix<3>(*g, *b, f->scratch, S(st)));
+  tl_end(TL_SCHUR, S(st));
+  return rc;
 }
 
 static int g_factor_variant = 3;
@@ -118,8 +186,11 @@ int mhdg_lu_solve(const mhdg_disc* g, const mhdg_factors* f, const double* bvec,
 int mhdg_assemble(const mhdg_disc* g, const mhdg_flow* fl, const mhdg_stage* sg, const double* u, const double* q,
                   const double* uhat, double* Rg, double* Ru, double* Rtl, double* Rt, int want_jac,
                   const mhdg_blocks* b, const mhdg_frozen* fo, const mhdg_frozen* fi, int* status, void* st) {
-  return DISPATCH(g, assemble<2>(*g, *fl, *sg, u, q, uhat, Rg, Ru, Rtl, Rt, want_jac, b, fo, fi, status, S(st)),
-                  assemble<3>(*g, *fl, *sg, u, q, uhat, Rg, Ru, Rtl, Rt, want_jac, b, fo, fi, status, S(st)));
+  tl_begin(TL_ASSEMBLE, S(st));
+  const int rc = DISPATCH(g, assemble<2>(*g, *fl, *sg, u, q, uhat, Rg, Ru, Rtl, Rt, want_jac, b, fo, fi, status, S(st)),
+                          assemble<3>(*g, *fl, *sg, u, q, uhat, Rg, Ru, Rtl, Rt, want_jac, b, fo, fi, status, S(st)));
+  tl_end(TL_ASSEMBLE, S(st));
+  return rc;
 }
 
 int mhdg_precond_build(const mhdg_disc* g, const mhdg_blocks* b, double* inv, int* status, void* st) {

@@ -11,6 +11,15 @@ namespace mhdg {
 
 extern long long g_launches;
 
+// Optional per-kernel timeline (mhdg_timeline_begin/end): instrumented launches
+// record a CUDA event pair on their own stream while it is enabled.
+enum TlSlot {
+  TL_APPLY_PRE = 0, TL_APPLY_SI, TL_APPLY_POST, TL_APPLY_FUSED, TL_APPLY_GENERIC, TL_FACE_REDUCE,
+  TL_SCHUR, TL_FACTOR, TL_PACK, TL_ASSEMBLE, TL_NSLOTS = 16
+};
+void tl_begin(int slot, cudaStream_t st);
+void tl_end(int slot, cudaStream_t st);
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(MHDG_FULL, v, o);

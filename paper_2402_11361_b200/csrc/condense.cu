@@ -1424,10 +1424,14 @@ int inv_factor3(int n, int n_mac, double* scratch, int* piv, double* tiled, int*
   const size_t bytes = gj2_smem_bytes(n);
   if (bytes > 227 * 1024 || n > 384) return -1;
   cudaFuncSetAttribute(k_gj3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  tl_begin(TL_FACTOR, st);
   k_gj3<<<n_mac, 512, bytes, st>>>(n, scratch, piv, status);
+  tl_end(TL_FACTOR, st);
   int rc = launch_ok();
   if (rc) return rc;
+  tl_begin(TL_PACK, st);
   k_pack_inv_gather<<<n_mac, 256, sizeof(int) * 2 * n, st>>>(n, scratch, piv, tiled);
+  tl_end(TL_PACK, st);
   return launch_ok();
 }
 
