@@ -151,6 +151,15 @@ typedef struct {
 /* doubles of mhdg_factors.work for this discretization */
 long long mhdg_apply_work_size(const mhdg_disc *disc);
 
+/* One ICGS Arnoldi orthogonalisation (krylov.py:51-58): with V_j = rows 0..j of
+   V (row stride ldv), h = V_j w; w -= V_j^T h; h2 = V_j w; w -= V_j^T h2;
+   out[0..j] = h + h2, out[j+1] = ||w|| (w updated in place).  Three fused
+   passes over V_j, deterministic reductions; j <= 62.  scratch:
+   mhdg_icgs_scratch_size(n) doubles. */
+int mhdg_icgs(int n, int j, const double *V, long long ldv, double *w, double *out, double *scratch,
+              void *stream);
+long long mhdg_icgs_scratch_size(int n);
+
 /* Per-kernel timeline: while enabled, the library records a CUDA event pair
    around each of its kernels on the caller's stream (capacity = max records).
    mhdg_timeline_end synchronises, disables recording and returns, per slot,

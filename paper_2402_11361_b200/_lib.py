@@ -113,6 +113,10 @@ def lib():
         L.mhdg_set_factor_variant.restype = None
         L.mhdg_set_schur_variant.argtypes = [C.c_int]
         L.mhdg_set_schur_variant.restype = None
+        L.mhdg_icgs.argtypes = [C.c_int, C.c_int, _dp, C.c_longlong, _dp, _dp, _dp, _dp]
+        L.mhdg_icgs.restype = C.c_int
+        L.mhdg_icgs_scratch_size.argtypes = [C.c_int]
+        L.mhdg_icgs_scratch_size.restype = C.c_longlong
         L.mhdg_timeline_begin.argtypes = [C.c_int]
         L.mhdg_timeline_begin.restype = C.c_int
         L.mhdg_timeline_end.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_int)]
@@ -127,7 +131,7 @@ EXPORTED = (
     "mhdg_gradient_refresh", "mhdg_precond_build", "mhdg_precond_apply", "mhdg_launch_count",
     "mhdg_packed_lu_size", "mhdg_set_stream_enabled", "mhdg_precond_build_ext", "mhdg_side_blocks",
     "mhdg_apply_work_size", "mhdg_set_apply_split", "mhdg_set_factor_variant",
-    "mhdg_set_schur_variant", "mhdg_timeline_begin", "mhdg_timeline_end",
+    "mhdg_set_schur_variant", "mhdg_timeline_begin", "mhdg_timeline_end", "mhdg_icgs", "mhdg_icgs_scratch_size",
 )
 
 

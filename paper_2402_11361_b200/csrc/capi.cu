@@ -22,6 +22,8 @@ int inv_factor(int n, int n_mac, double* scratch, double* tiled, int* status, cu
 int inv_factor2(int n, int n_mac, double* scratch, int* piv, double* tiled, int* status, cudaStream_t st);
 int inv_factor3(int n, int n_mac, double* scratch, int* piv, double* tiled, int* status, cudaStream_t st);
 extern int g_schur_variant;
+int icgs(int n, int j, const double* V, long long ldv, double* w, double* out, double* scratch, cudaStream_t st);
+long long icgs_scratch_size(int n);
 size_t gj_smem_bytes(int n);
 int apply_stream(const mhdg_disc&, const mhdg_blocks&, const mhdg_factors&, const double*, double*, cudaStream_t);
 size_t lu_smem_bytes(int n);
@@ -58,6 +60,12 @@ void tl_end(int slot, cudaStream_t st) {
 }  // namespace mhdg
 
 extern "C" {
+
+int mhdg_icgs(int n, int j, const double* V, long long ldv, double* w, double* out, double* scratch, void* st) {
+  return icgs(n, j, V, ldv, w, out, scratch, S(st));
+}
+
+long long mhdg_icgs_scratch_size(int n) { return icgs_scratch_size(n); }
 
 int mhdg_timeline_begin(int capacity) {
   if (capacity > g_tl_cap) {

@@ -6,7 +6,7 @@ cd "$(dirname "$0")/../paper_2402_11361_b200/csrc"
 OUT=../../tools/prof
 mkdir -p $OUT/vbuild
 F="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr"
-for s in capi apply condense precond assemble; do
+for s in capi apply condense precond assemble krylov; do
   nvcc $F -c $s.cu -o $OUT/vbuild/$s.o &
 done
 wait
@@ -17,5 +17,5 @@ done
 wait
 for v in "$@"; do
   nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $OUT/var_$v.so $OUT/vbuild/capi.o $OUT/vbuild/apply.o \
-    $OUT/vbuild/condense.o $OUT/vbuild/precond.o $OUT/vbuild/assemble.o $OUT/vbuild/as_$v.o -lcudart
+    $OUT/vbuild/condense.o $OUT/vbuild/precond.o $OUT/vbuild/assemble.o $OUT/vbuild/krylov.o $OUT/vbuild/as_$v.o -lcudart
 done
