@@ -146,6 +146,8 @@ typedef struct {
   int *perm;                 /* n_mac*n */
   double *scratch;           /* n_mac*n*n */
   double *work;              /* mhdg_apply_work_size(disc) or NULL */
+  int kind;                  /* 0: explicit S^-1, tiled (csrc/tiled_inv.cuh), Gauss-Jordan;
+                                1: packed LU (csrc/packed_lu.cuh), perm = pivot rows */
 } mhdg_factors;
 
 /* doubles of mhdg_factors.work for this discretization */
@@ -181,7 +183,7 @@ void mhdg_set_schur_variant(int v);
    set; 0: fused single-kernel apply.  For A/B measurements. */
 void mhdg_set_apply_split(int on);
 
-/* doubles per macro of the packed LU factor */
+/* doubles per macro of the factor buffer (either kind) */
 long long mhdg_packed_lu_size(int n);
 
 /* Residuals (and, with want_jac, blocks + frozen coefficients).

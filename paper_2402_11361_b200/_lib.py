@@ -63,7 +63,7 @@ class Frozen(C.Structure):
 
 
 class Factors(C.Structure):
-    _fields_ = [("lu", _dp), ("perm", _dp), ("scratch", _dp), ("work", _dp)]
+    _fields_ = [("lu", _dp), ("perm", _dp), ("scratch", _dp), ("work", _dp), ("kind", C.c_int)]
 
 
 _lib = None

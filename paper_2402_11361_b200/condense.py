@@ -11,11 +11,19 @@ reference's global trace layout.
 
 from __future__ import annotations
 
+import os
+
 import torch
 
 from . import _lib
 from .assembly import LocalBlocks, raise_status
 from .device import current_stream
+
+
+# S factor kept per macro: "inverse" (explicit S^-1 by Gauss-Jordan, as the
+# reference's np.linalg.inv) or "lu" (packed LU with partial pivoting)
+FACTOR = os.environ.get("MHDG_FACTOR", "inverse")
+FACTOR_KINDS = {"inverse": 0, "lu": 1}
 
 
 class FactorizationError(RuntimeError):
@@ -33,6 +41,7 @@ class CondensedSchur:
         fac = _lib.Factors()
         fac.lu, fac.perm, fac.scratch = _lib.ptr(lu), _lib.ptr(perm), _lib.ptr(scratch)
         fac.work = _lib.ptr(work) if work is not None else None
+        fac.kind = FACTOR_KINDS[FACTOR]
         self._fac = fac
         dd = blocks.disc.device
         self._y_loc = torch.empty(dd.n_local_trace, dtype=torch.float64, device=dd.device)

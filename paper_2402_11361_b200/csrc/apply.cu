@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(APPLY_THREADS) k_apply_local(mhdg_disc g, mhdg
   __syncthreads();
   state_grad<D>(g, b, sz, mac, z, sm + o.vv, sm + o.wv, sm + o.cv, sm + o.wf, cfgz, y, true, 1.0);
   // step 2: y2 = S^-1 y1
-  ti_gemv_cta(fac.lu + (size_t)mac * ti_size(sz.n), sz.n, y, tmp);
+  factor_solve_cta(fac, mac, sz.n, y, tmp);
   for (int i = threadIdx.x; i < sz.n; i += blockDim.x) y[i] = tmp[i];
   __syncthreads();
   // steps 3-4: y4 = A_hu y2 - A_hq A_qq^-1 A_qu y2 + A_hh x - A_hq z
@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(APPLY_THREADS) k_rhs_local(mhdg_disc g, mhdg_b
   __syncthreads();
   // t2 = S^-1 (R_U - A_uq zr)
   state_grad<D>(g, b, sz, mac, zr, sm + o.vv, sm + o.wv, sm + o.cv, sm + o.wf, cfgz, y, true, -1.0);
-  ti_gemv_cta(fac.lu + (size_t)mac * ti_size(sz.n), sz.n, y, tmp);
+  factor_solve_cta(fac, mac, sz.n, y, tmp);
   for (int i = threadIdx.x; i < sz.n; i += blockDim.x) y[i] = tmp[i];
   __syncthreads();
   // b_loc = (A_hu t2 - A_hq A_qq^-1 A_qu t2) + A_hq zr
@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(APPLY_THREADS) k_recover(mhdg_disc g, mhdg_blo
   for (int i = threadIdx.x; i < sz.n; i += blockDim.x)
     y[i] = (w[i] - __ldg(R_state + (size_t)mac * sz.n + i)) + y[i];
   __syncthreads();
-  ti_gemv_cta(fac.lu + (size_t)mac * ti_size(sz.n), sz.n, y, tmp);
+  factor_solve_cta(fac, mac, sz.n, y, tmp);
   for (int i = threadIdx.x; i < sz.n; i += blockDim.x) y[i] = tmp[i];
   __syncthreads();
   for (int i = threadIdx.x; i < sz.n; i += blockDim.x) du[(size_t)mac * sz.n + i] = y[i];
@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(APPLY_THREADS) k_lu_solve(int n, mhdg_factors 
   double *y = sm, *tmp = y + n, *dblk = tmp + n;
   for (int i = threadIdx.x; i < n; i += blockDim.x) y[i] = b[(size_t)mac * n + i];
   __syncthreads();
-  ti_gemv_cta(fac.lu + (size_t)mac * ti_size(n), n, y, tmp);
+  factor_solve_cta(fac, mac, n, y, tmp);
   for (int i = threadIdx.x; i < n; i += blockDim.x) y[i] = tmp[i];
   __syncthreads();
   (void)dblk;

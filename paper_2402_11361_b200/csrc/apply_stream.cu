@@ -892,7 +892,7 @@ static bool stream_ok(const mhdg_disc& g, const mhdg_blocks& b, const mhdg_facto
   const size_t cls = (size_t)g.n_grad_cls * TSm<C>::CLS;
   const size_t smem = sizeof(double) * ((size_t)MHDG_STAGES * ST_DBL + SSm<C>::total + TSm<C>::total +
                                         (cls <= (size_t)C::D * C::n ? cls : 2 * cls));
-  return sizes && tables && smem <= 227 * 1024 && al(b.face_state_trace) && al(b.face_trace_trace) &&
+  return sizes && tables && f.kind == 0 && smem <= 227 * 1024 && al(b.face_state_trace) && al(b.face_trace_trace) &&
          al(b.face_trace_state) && al(b.wdgdq_vol) && al(b.wdgdq_face) && al(f.lu) && al(f.work);
 }
 

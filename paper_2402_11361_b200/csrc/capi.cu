@@ -1,5 +1,6 @@
 // extern "C" boundary (include/mhdg.h): dispatch on the dimension and launch.
 #include "common.cuh"
+#include "packed_lu.cuh"
 #include "tiled_inv.cuh"
 
 namespace mhdg {
@@ -21,6 +22,7 @@ int lu_solve(const mhdg_disc&, const mhdg_factors&, const double*, double*, cuda
 int inv_factor(int n, int n_mac, double* scratch, double* tiled, int* status, cudaStream_t st);
 int inv_factor2(int n, int n_mac, double* scratch, int* piv, double* tiled, int* status, cudaStream_t st);
 int inv_factor3(int n, int n_mac, double* scratch, int* piv, double* tiled, int* status, cudaStream_t st);
+int lu_factor3(int n, int n_mac, double* scratch, int* piv, double* packed, int* status, cudaStream_t st);
 extern int g_schur_variant;
 int icgs(int n, int j, const double* V, long long ldv, double* w, double* out, double* scratch, cudaStream_t st);
 long long icgs_scratch_size(int n);
@@ -103,7 +105,7 @@ int mhdg_timeline_end(double* ms, int* counts) {
 
 long long mhdg_launch_count(void) { return g_launches; }
 
-long long mhdg_packed_lu_size(int n) { return ti_size(n); }
+long long mhdg_packed_lu_size(int n) { return ti_size(n) > plu_size(n) ? ti_size(n) : plu_size(n); }
 
 long long mhdg_apply_work_size(const mhdg_disc* g) {
   const long long n = (long long)g->L * g->ns, np = n + (n & 1), ltr = (long long)g->nf * g->Lf * g->ns;
@@ -172,6 +174,10 @@ void mhdg_set_schur_variant(int v) { mhdg::g_schur_variant = v; }
 
 int mhdg_lu_factor(const mhdg_disc* g, const mhdg_factors* f, int* status, void* st) {
   const int n = g->L * g->ns;
+  if (f->kind == 1) {  // packed LU (k_lu3)
+    const int rc1 = lu_factor3(n, g->n_mac, f->scratch, f->perm, f->lu, status, S(st));
+    return rc1 < 0 ? MHDG_ERR_CONFIG : rc1;
+  }
   // DMMA panel-64 Gauss-Jordan when its panel fits shared memory (without row interchanges
   // by default), else the 32-column FFMA one
   const int rc = g_factor_variant == 2 ? inv_factor2(n, g->n_mac, f->scratch, f->perm, f->lu, status, S(st))

@@ -1609,6 +1609,433 @@ __global__ void __launch_bounds__(256, 2) k_schur_mma(mhdg_disc g, mhdg_blocks b
   }
 }
 
+// --------------------------------------------------------------------------
+// k_lu3: batched LU with partial pivoting, pivots kept in place (the
+// factorisation the canonical F_cond counts: (2/3) n^3).
+// --------------------------------------------------------------------------
+// Logical row k of P S = L U lives in physical row piv[k]; columns are never
+// permuted.  Per 48-column panel the not-yet-pivoted rows are compacted
+// (m = n - k0 rows), so the pivot steps shrink as the factorisation proceeds.
+// Inside a panel, 16-column sub-panels are factored by pivot steps (argmax over
+// the sub-panel column, multipliers, rank-1 updates of the sub-panel); the
+// sub-panel's U rows are then completed on the rest of the panel (16-step
+// triangular solve per column) and the other rows updated by a DMMA rank-16
+// product.  After the panel: for each 48-column chunk of the columns to its
+// right, the pivot rows are staged (A12), turned into U12 = L11^-1 A12 with
+// the inverted 16x16 diagonal blocks, written back, and the remaining rows
+// updated by a DMMA rank-48 product (C -= L21 U12).  FactorizationError on an
+// exactly zero pivot (scipy's lu_factor raises on singular input).
+// Panel width NB and CTA size NT are template parameters: NB = 24, NT = 256
+// keeps a CTA at ~99 KB of shared memory, so two macros are factored per SM and
+// hide each other's pivot-step latency.
+template <int NB, int NT>
+struct Lu3 {
+  static constexpr int PW = NB + 4;               // panel row stride
+  static constexpr int TC = 48, BS = 52;           // column chunk of the trailing update, its stride
+  static constexpr int NSB = (NB + 15) / 16;       // 16-row diagonal blocks of L11
+  static constexpr int NRG = NT / 16;              // row groups
+  static constexpr int RPT = (384 + NRG - 1) / NRG;  // compacted rows per thread (n <= 384)
+  static constexpr int NW = NT / 32;
+  static size_t smem_bytes(int n) {
+    return sizeof(double) * ((size_t)n * PW + (size_t)NB * BS + (size_t)NSB * 16 * 17) + sizeof(int) * (3 * (size_t)n + 8);
+  }
+};
+
+template <int NB, int NT>
+__global__ void __launch_bounds__(NT, 2) k_lu3(int n, double* __restrict__ S, int* __restrict__ piv_out, int* status) {
+  using C = Lu3<NB, NT>;
+  constexpr int PW = C::PW, TC = C::TC, BS = C::BS, RPT = C::RPT, NWp = C::NW;
+  extern __shared__ double sm[];
+  const int mac = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* A = S + (size_t)mac * n * n;
+  int* pivg = piv_out + (size_t)mac * n;
+  double* P = sm;                                   // m x PW: the panel over the compacted rows
+  double* Bt = P + (size_t)n * PW;                  // NB x BS: U rows (sub-panel / A12 chunk)
+  double* Di = Bt + NB * BS;                        // NSB x 16 x 17: inverted unit-lower diagonal blocks
+  int* rows = reinterpret_cast<int*>(Di + C::NSB * 16 * 17);  // n: compacted physical rows
+  int* done = rows + n;                                        // n: 1 = pivot row of an earlier panel
+  int* ispiv = done + n;                                       // n: compacted row is a pivot of this panel
+  __shared__ double cand_v[32];
+  __shared__ int cand_i[32];
+  __shared__ int ppos[NB];  // compacted positions of this panel's pivots (logical order)
+  __shared__ int mrows;
+  const int cl = tid & 15, rg = tid >> 4;
+  bool singular = false;
+  for (int i = tid; i < n; i += NT) done[i] = 0;
+  if (tid < 32) {
+    cand_v[tid] = -1.0;
+    cand_i[tid] = 0x7fffffff;
+  }
+  __syncthreads();
+
+  for (int k0 = 0; k0 < n; k0 += NB) {
+    const int nb = min(NB, n - k0);
+    if (tid == 0) {
+      int m = 0;
+      for (int i = 0; i < n; ++i)
+        if (!done[i]) rows[m++] = i;
+      mrows = m;
+    }
+    __syncthreads();
+    const int m = mrows;  // = n - k0
+    const int rpt = (m + C::NRG - 1) / C::NRG;
+    const int rbeg = rg * rpt;
+    unsigned piv_here = 0;  // bit q: compacted row rbeg + q pivoted in this panel
+    GJT(t0);
+    for (int idx = tid; idx < m * nb; idx += NT) {
+      const int r = idx / nb, c = idx - r * nb;
+      P[r * PW + c] = A[(size_t)rows[r] * n + k0 + c];
+    }
+    for (int r = tid; r < m; r += NT) ispiv[r] = 0;
+    __syncthreads();
+    GJADD(0, t0);
+    for (int js = 0; js < nb; js += 16) {
+      GJT(t1);
+      const int ns = min(16, nb - js);
+      const int c = js + cl;
+      const bool inside = cl < ns;
+      if (cl == 0) {  // candidates for the sub-panel's first column
+        double cb = -1.0;
+        int ci = 0x7fffffff;
+        for (int q = 0; q < rpt; ++q) {
+          const int r = rbeg + q;
+          if (r < m && !((piv_here >> q) & 1u)) {
+            const double a = fabs(P[r * PW + js]);
+            if (a > cb) { cb = a; ci = r; }
+          }
+        }
+        cand_v[rg] = cb;
+        cand_i[rg] = ci;
+      }
+      __syncthreads();
+      for (int j = js; j < js + ns; ++j) {
+        double best = cand_v[lane];
+        int p = cand_i[lane];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double v2 = __shfl_xor_sync(MHDG_FULL, best, o);
+          const int i2 = __shfl_xor_sync(MHDG_FULL, p, o);
+          if (v2 > best || (v2 == best && i2 < p)) { best = v2; p = i2; }
+        }
+        if (!(best > 0.0)) singular = true;
+        if (singular) p = 0;
+        const double d = singular ? 0.0 : 1.0 / P[p * PW + j];
+        const double rowp_c = (inside && c > j) ? P[p * PW + c] : 0.0;
+        double colj[RPT];
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) colj[q] = (q < rpt && rbeg + q < m) ? P[(rbeg + q) * PW + j] : 0.0;
+        __syncthreads();  // row p and column j read by everyone before anyone writes
+        if (tid == 0) {
+          ppos[j] = p;
+          ispiv[p] = 1;
+          pivg[k0 + j] = rows[p];
+        }
+        if (p >= rbeg && p < rbeg + rpt) piv_here |= 1u << (p - rbeg);
+        const bool next_col = (c == j + 1) && (j + 1 < js + ns);
+        double cb = -1.0;
+        int ci = 0x7fffffff;
+        if (inside && c >= j) {
+#pragma unroll
+          for (int q = 0; q < RPT; ++q) {
+            const int r = rbeg + q;
+            if (q < rpt && r < m && !((piv_here >> q) & 1u)) {
+              const double l = colj[q] * d;
+              const double nv = (c == j) ? l : P[r * PW + c] - l * rowp_c;
+              P[r * PW + c] = nv;
+              if (next_col) {
+                const double a = fabs(nv);
+                if (a > cb) { cb = a; ci = r; }
+              }
+            }
+          }
+        }
+        if (next_col) {
+          cand_v[rg] = cb;
+          cand_i[rg] = ci;
+        }
+        __syncthreads();
+      }
+      GJADD(1, t1);
+      GJT(t2);
+      const int c0 = js + ns, nrc = nb - c0;  // panel columns right of the sub-panel
+      if (nrc > 0) {
+        // (a) the sub-panel's U rows on those columns: forward substitution with its unit-lower block
+        for (int cc = tid; cc < nrc; cc += NT) {
+          for (int k = 1; k < ns; ++k) {
+            double v = P[ppos[js + k] * PW + c0 + cc];
+            for (int k2 = 0; k2 < k; ++k2) v -= P[ppos[js + k] * PW + js + k2] * P[ppos[js + k2] * PW + c0 + cc];
+            P[ppos[js + k] * PW + c0 + cc] = v;
+          }
+        }
+        __syncthreads();
+        for (int idx = tid; idx < 16 * NB; idx += NT) {
+          const int k = idx / NB, cc = idx % NB;
+          Bt[k * BS + cc] = (k < ns && cc < nrc) ? P[ppos[js + k] * PW + c0 + cc] : 0.0;
+        }
+        __syncthreads();
+        // (b) rows not pivoted in this panel: P[r][c0 + cc] -= sum_k L[r][js + k] U[k][cc] (DMMA)
+        {
+          const int g = lane >> 2, t4 = lane & 3;
+          constexpr int NT8 = (NB + 7) / 8;
+          const int ntile = (nrc + 7) / 8;
+          for (int r0 = warp * 8; r0 < m; r0 += 8 * NWp) {
+            const int r = r0 + g;
+            const bool upd = r < m && !ispiv[r];
+            double acc[NT8][2];
+#pragma unroll
+            for (int jj = 0; jj < NT8; ++jj) {
+              const int col = 8 * jj + 2 * t4;
+              acc[jj][0] = (r < m && jj < ntile && col < nrc) ? P[r * PW + c0 + col] : 0.0;
+              acc[jj][1] = (r < m && jj < ntile && col + 1 < nrc) ? P[r * PW + c0 + col + 1] : 0.0;
+            }
+#pragma unroll
+            for (int kk = 0; kk < 16; kk += 4) {
+              const double a = (r < m && kk + t4 < ns) ? -P[r * PW + js + kk + t4] : 0.0;
+#pragma unroll
+              for (int jj = 0; jj < NT8; ++jj)
+                if (jj < ntile) dmma_8x8x4(acc[jj][0], acc[jj][1], a, Bt[(kk + t4) * BS + 8 * jj + g]);
+            }
+            __syncwarp();
+            if (upd) {
+#pragma unroll
+              for (int jj = 0; jj < NT8; ++jj) {
+                const int col = 8 * jj + 2 * t4;
+                if (jj < ntile && col < nrc) P[r * PW + c0 + col] = acc[jj][0];
+                if (jj < ntile && col + 1 < nrc) P[r * PW + c0 + col + 1] = acc[jj][1];
+              }
+            }
+          }
+        }
+        __syncthreads();
+      }
+      GJADD(2, t2);
+    }
+    GJT(t_up);
+    // ---- inverted unit-lower 16x16 diagonal blocks of L11 (pivot rows, logical order) ----
+    const int nsb = (nb + 15) / 16;
+    if (tid < 16 * nsb) {
+      const int i = tid / 16, cc = tid % 16, b0 = 16 * i, bn = min(16, nb - b0);
+      double* X = Di + i * 16 * 17;
+      if (cc < bn) {
+        X[cc * 17 + cc] = 1.0;
+        for (int rr = cc + 1; rr < bn; ++rr) {
+          double acc = 0.0;
+          for (int k = cc; k < rr; ++k) acc += P[ppos[b0 + rr] * PW + b0 + k] * X[k * 17 + cc];
+          X[rr * 17 + cc] = -acc;
+        }
+        for (int rr = 0; rr < cc; ++rr) X[rr * 17 + cc] = 0.0;
+      }
+    }
+    __syncthreads();
+    // ---- columns right of the panel: U12 = L11^-1 A12 per chunk, then C -= L21 U12 ----
+    const int nright = n - k0 - nb;
+    const int wm = warp >> 1, wn = warp & 1;
+    const int g = lane >> 2, t4 = lane & 3;
+    constexpr int RPP = (NT / 64) * 16;       // rows per pass of the trailing product
+    constexpr int TPT = (16 * TC + NT - 1) / NT;  // TRSM entries per thread and 16-row block
+    for (int tc = 0; tc < nright; tc += TC) {
+      const int wct = min(TC, nright - tc), cbase = k0 + nb + tc;
+      for (int idx = tid; idx < NB * TC; idx += NT) {
+        const int k = idx / TC, cc = idx % TC;
+        Bt[k * BS + cc] = (k < nb && cc < wct) ? A[(size_t)rows[ppos[k]] * n + cbase + cc] : 0.0;
+      }
+      __syncthreads();
+      for (int i = 0; i < nsb; ++i) {  // Bt_i = D_i (Bt_i - L[i, <i] Bt_<i)
+        const int b0 = 16 * i, bn = min(16, nb - b0);
+        double t[TPT];
+#pragma unroll
+        for (int h = 0; h < TPT; ++h) {
+          const int idx = tid + NT * h, k = idx / TC, cc = idx % TC;
+          double v = 0.0;
+          if (idx < 16 * TC && k < bn) {
+            v = Bt[(b0 + k) * BS + cc];
+            for (int k2 = 0; k2 < b0; ++k2) v -= P[ppos[b0 + k] * PW + k2] * Bt[k2 * BS + cc];
+          }
+          t[h] = v;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int h = 0; h < TPT; ++h) {
+          const int idx = tid + NT * h, k = idx / TC, cc = idx % TC;
+          if (idx < 16 * TC && k < bn) Bt[(b0 + k) * BS + cc] = t[h];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int h = 0; h < TPT; ++h) {
+          const int idx = tid + NT * h, k = idx / TC, cc = idx % TC;
+          double v = 0.0;
+          if (idx < 16 * TC && k < bn)
+            for (int k2 = 0; k2 <= k; ++k2) v += Di[i * 16 * 17 + k * 17 + k2] * Bt[(b0 + k2) * BS + cc];
+          t[h] = v;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int h = 0; h < TPT; ++h) {
+          const int idx = tid + NT * h, k = idx / TC, cc = idx % TC;
+          if (idx < 16 * TC && k < bn) Bt[(b0 + k) * BS + cc] = t[h];
+        }
+        __syncthreads();
+      }
+      for (int idx = tid; idx < nb * wct; idx += NT) {
+        const int k = idx / wct, cc = idx % wct;
+        A[(size_t)rows[ppos[k]] * n + cbase + cc] = Bt[k * BS + cc];
+      }
+      // C -= L21 U12 over the panel's other rows: warp (wm, wn) owns 16 rows x 3 column tiles
+      for (int tr = 0; tr < m; tr += RPP) {
+        double acc[2][3][2];
+        bool upd[2];
+        int prow[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int r = tr + wm * 16 + 8 * i + g;
+          upd[i] = r < m && !ispiv[r];
+          prow[i] = r < m ? rows[r] : 0;
+#pragma unroll
+          for (int jj = 0; jj < 3; ++jj)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int col = wn * 24 + 8 * jj + 2 * t4 + e;
+              acc[i][jj][e] = (upd[i] && col < wct) ? A[(size_t)prow[i] * n + cbase + col] : 0.0;
+            }
+        }
+        if (tr + wm * 16 < m) {
+#pragma unroll
+          for (int kk = 0; kk < NB; kk += 4) {
+            double a[2], bb[3];
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              const int r = tr + wm * 16 + 8 * i + g;
+              a[i] = (r < m && kk + t4 < nb) ? -P[r * PW + kk + t4] : 0.0;
+            }
+#pragma unroll
+            for (int jj = 0; jj < 3; ++jj) bb[jj] = Bt[(kk + t4) * BS + wn * 24 + 8 * jj + g];
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+              for (int jj = 0; jj < 3; ++jj) dmma_8x8x4(acc[i][jj][0], acc[i][jj][1], a[i], bb[jj]);
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int jj = 0; jj < 3; ++jj)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int col = wn * 24 + 8 * jj + 2 * t4 + e;
+              if (upd[i] && col < wct) A[(size_t)prow[i] * n + cbase + col] = acc[i][jj][e];
+            }
+      }
+      __syncthreads();
+    }
+    GJADD(4, t_up);
+    GJT(t5);
+    for (int idx = tid; idx < m * nb; idx += NT) {
+      const int r = idx / nb, cc = idx - r * nb;
+      A[(size_t)rows[r] * n + k0 + cc] = P[r * PW + cc];
+    }
+    for (int k = tid; k < nb; k += NT) done[rows[ppos[k]]] = 1;
+    __syncthreads();
+    GJADD(5, t5);
+  }
+  if (singular && tid == 0) set_status(status, MHDG_ERR_FACTORIZATION, mac, 0, 0.0);
+}
+
+// in-place LU with pivot rows in place -> packed solve layout (packed_lu.cuh):
+// logical row r = physical row piv[r]; diagonal tiles inverted.
+__global__ void __launch_bounds__(256) k_pack_lu3(int n, const double* __restrict__ F, const int* __restrict__ piv,
+                                                  double* __restrict__ out) {
+  extern __shared__ double pk_sm[];
+  double(*T)[PLU_NB + 1] = reinterpret_cast<double(*)[PLU_NB + 1]>(pk_sm);
+  double(*X)[PLU_NB + 1] = reinterpret_cast<double(*)[PLU_NB + 1]>(pk_sm + PLU_NB * (PLU_NB + 1));
+  int* pr = reinterpret_cast<int*>(pk_sm + 2 * PLU_NB * (PLU_NB + 1));
+  const int mac = blockIdx.x, tid = threadIdx.x;
+  const double* A = F + (size_t)mac * n * n;
+  double* O = out + (size_t)mac * plu_size(n);
+  for (int i = tid; i < n; i += blockDim.x) pr[i] = piv[(size_t)mac * n + i];
+  __syncthreads();
+  const int nblk = plu_nblk(n);
+  for (int b = 0; b < nblk; ++b) {
+    const PluOffsets o = plu_offsets(n, b);
+    const int nb = o.nb, r0 = o.r0;
+    for (int idx = tid; idx < nb * o.ncol_fwd; idx += blockDim.x) {
+      const int r = idx / o.ncol_fwd, c = idx % o.ncol_fwd;
+      O[o.fwd_panel + plu_panel_idx(nb, o.ncol_fwd, r, c)] = A[(size_t)pr[r0 + r] * n + c];
+    }
+    for (int idx = tid; idx < nb * o.ncol_bwd; idx += blockDim.x) {
+      const int r = idx / o.ncol_bwd, c = idx % o.ncol_bwd;
+      O[o.bwd_panel + plu_panel_idx(nb, o.ncol_bwd, r, c)] = A[(size_t)pr[r0 + r] * n + r0 + nb + c];
+    }
+    for (int idx = tid; idx < nb * nb; idx += blockDim.x) {
+      const int r = idx / nb, c = idx % nb;
+      T[r][c] = A[(size_t)pr[r0 + r] * n + r0 + c];
+    }
+    __syncthreads();
+    if (tid < nb) {  // inverse of the unit lower tile, column tid
+      const int c = tid;
+      X[c][c] = 1.0;
+      for (int i = c + 1; i < nb; ++i) {
+        double acc = 0.0;
+        for (int k = c; k < i; ++k) acc += T[i][k] * X[k][c];
+        X[i][c] = -acc;
+      }
+    }
+    __syncthreads();
+    for (int idx = tid; idx < nb * nb; idx += blockDim.x) {
+      const int r = idx / nb, c = idx % nb;
+      if (c < r) O[o.fwd_diag + plu_lo(r, c)] = X[r][c];
+    }
+    __syncthreads();
+    if (tid < nb) {  // inverse of the upper tile, column tid
+      const int c = tid;
+      X[c][c] = 1.0 / T[c][c];
+      for (int i = c - 1; i >= 0; --i) {
+        double acc = 0.0;
+        for (int k = i + 1; k <= c; ++k) acc += T[i][k] * X[k][c];
+        X[i][c] = -acc / T[i][i];
+      }
+    }
+    __syncthreads();
+    for (int idx = tid; idx < nb * nb; idx += blockDim.x) {
+      const int r = idx / nb, c = idx % nb;
+      if (c >= r) O[o.bwd_diag + plu_up(nb, r, c)] = X[r][c];
+    }
+    if (tid == 0) {  // zero the even-size padding of the last (narrow) tiles and triangles
+      if ((nb * (nb - 1) / 2) & 1) O[o.fwd_diag + nb * (nb - 1) / 2] = 0.0;
+      if ((nb * (nb + 1) / 2) & 1) O[o.bwd_diag + nb * (nb + 1) / 2] = 0.0;
+      const int wf = o.ncol_fwd % PLU_TW, wb = o.ncol_bwd % PLU_TW;
+      if ((nb * wf) & 1) O[o.fwd_diag - 1] = 0.0;
+      if ((nb * wb) & 1) O[o.bwd_diag - 1] = 0.0;
+    }
+    __syncthreads();
+  }
+}
+
+#ifndef MHDG_LU_NB
+#define MHDG_LU_NB 24
+#endif
+#ifndef MHDG_LU_NT
+#define MHDG_LU_NT 256
+#endif
+
+int lu_factor3(int n, int n_mac, double* scratch, int* piv, double* packed, int* status, cudaStream_t st) {
+  using L3 = Lu3<MHDG_LU_NB, MHDG_LU_NT>;
+  const size_t bytes = L3::smem_bytes(n);
+  if (bytes > 227 * 1024 || n > 384) return -1;
+  auto kern = k_lu3<MHDG_LU_NB, MHDG_LU_NT>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  tl_begin(TL_FACTOR, st);
+  kern<<<n_mac, MHDG_LU_NT, bytes, st>>>(n, scratch, piv, status);
+  tl_end(TL_FACTOR, st);
+  int rc = launch_ok();
+  if (rc) return rc;
+  const size_t pbytes = sizeof(double) * 2 * PLU_NB * (PLU_NB + 1) + sizeof(int) * n;
+  cudaFuncSetAttribute(k_pack_lu3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pbytes);
+  tl_begin(TL_PACK, st);
+  k_pack_lu3<<<n_mac, 256, pbytes, st>>>(n, scratch, piv, packed);
+  tl_end(TL_PACK, st);
+  return launch_ok();
+}
+
 int inv_factor(int n, int n_mac, double* scratch, double* tiled, int* status, cudaStream_t st) {
   const size_t bytes = gj_smem_bytes(n);
   if (bytes > 227 * 1024) return MHDG_ERR_CONFIG;

@@ -11,6 +11,7 @@
 // product needs no barrier between tiles.
 #pragma once
 #include "common.cuh"
+#include "packed_lu.cuh"
 
 namespace mhdg {
 
@@ -48,6 +49,7 @@ __host__ __device__ __forceinline__ long long ti_idx(int n, int r, int c) {
 }
 
 // CTA-wide out = S^-1 v (v, out in shared memory, length n; synchronous loads)
+// (packed-LU factors: see factor_solve_cta in local_ops.cuh)
 __device__ inline void ti_gemv_cta(const double* __restrict__ F, int n, const double* v, double* out) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int r = warp; r < n; r += nw) {
@@ -57,6 +59,19 @@ __device__ inline void ti_gemv_cta(const double* __restrict__ F, int n, const do
     if (lane == 0) out[r] = acc;
   }
   __syncthreads();
+}
+
+// out = S^-1 v for macro `mac` with either factor kind (mhdg_factors.kind):
+// explicit tiled inverse (GEMV) or packed LU (block triangular solves).
+// v is clobbered for the LU kind.  Ends with a CTA barrier.
+__device__ inline void factor_solve_cta(const mhdg_factors& fac, int mac, int n, double* v, double* out) {
+  if (fac.kind == 1) {
+    plu_solve_cta(fac.lu + (size_t)mac * plu_size(n), fac.perm + (size_t)mac * n, n, v, out);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = v[i];
+    __syncthreads();
+  } else {
+    ti_gemv_cta(fac.lu + (size_t)mac * ti_size(n), n, v, out);
+  }
 }
 
 }  // namespace mhdg

@@ -137,3 +137,30 @@ def test_streamed_apply_matches_generic(name, split):
         L.mhdg_set_stream_enabled(1)
         L.mhdg_set_apply_split(1)
     assert rel_err(y_str, y_gen) < 1e-10  # summation order differs; cond(S) ~ 1e6 at m=4, p=3
+
+
+@pytest.mark.parametrize("name", ["uniform_m2p2", "uniform_m4p3", "couette_m2p2"])
+def test_lu_factor_kind_matches_inverse(name):
+    """Packed-LU factors (k_lu3, pivots in place) and the explicit inverse give the
+    same condensed operator, rhs and recovery up to cond(S) * eps."""
+    need_gpu()
+    from paper_2402_11361_b200 import condense as CD
+
+    d, fn, ctx = _cases_2d()[name]
+    of = perturbed_fields(d, fn, 21)
+    ob, _ = O.jacobian(d, of, ctx)
+    res = [dev(r) for r in O.residual(d, of, ctx)]
+    blocks = upload_blocks(d, ob)
+    x = dev(np.random.default_rng(3).standard_normal(d.n_trace))
+    out = {}
+    try:
+        for kind in ("inverse", "lu"):
+            CD.FACTOR = kind
+            cond = CD.CondensedSchur.build(blocks)
+            du, _ = cond.recover(res[0], res[1], x)
+            out[kind] = (host(cond.apply_trace(x)), host(cond.rhs(*res)), host(du))
+    finally:
+        CD.FACTOR = "inverse"
+    tol = 1e-7 if name == "uniform_m4p3" else 1e-10  # cond(S) ~ 1e6 at m=4, p=3
+    for a, b in zip(out["lu"], out["inverse"]):
+        assert rel_err(a, b) < tol
