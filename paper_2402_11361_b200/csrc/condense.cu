@@ -1420,6 +1420,50 @@ __global__ void __launch_bounds__(256) k_pack_inv_gather(int n, const double* __
   }
 }
 
+// Same output as k_pack_inv_gather, row by row: each warp stages source row p_i
+// in shared memory with coalesced loads and writes the permuted row into its
+// 64-row block, one contiguous 32-column tile row per lane group.
+__global__ void __launch_bounds__(256) k_pack_inv_rows(int n, const double* __restrict__ F,
+                                                       const int* __restrict__ piv, double* __restrict__ out) {
+  extern __shared__ double rsm[];
+  const int NP = (n + 1) & ~1;
+  double* rowbuf = rsm + (threadIdx.x >> 5) * NP;
+  int* pp = reinterpret_cast<int*>(rsm + 8 * NP);
+  int* inv = pp + n;
+  const int mac = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double* A = F + (size_t)mac * n * n;
+  double* O = out + (size_t)mac * ti_size(n);
+  for (int k = threadIdx.x; k < n; k += blockDim.x) {
+    const int p = piv[(size_t)mac * n + k];
+    pp[k] = p;
+    inv[p] = k;
+  }
+  __syncthreads();
+  for (int r = warp; r < n; r += 8) {
+    const double* src = A + (size_t)pp[r] * n;
+    for (int c = lane; c < n; c += 32) rowbuf[c] = src[c];
+    __syncwarp();
+    const int b = r / TI_RB, rl = r - b * TI_RB, nb = ti_rows(n, b);
+    const long long base = ti_block_off(n, b);
+    for (int c = lane; c < n; c += 32) {
+      const int j = c / TI_CW, c0 = j * TI_CW, w = (n - c0) < TI_CW ? n - c0 : TI_CW;
+      O[base + (long long)j * nb * TI_CW + (long long)rl * w + (c - c0)] = rowbuf[inv[c]];
+    }
+    __syncwarp();
+  }
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < ti_nblk(n); ++b) {
+      const int nb = ti_rows(n, b);
+      long long o = ti_block_off(n, b);
+      for (int c = 0; c < n; c += TI_CW) {
+        const int w = (n - c) < TI_CW ? n - c : TI_CW;
+        if (((long long)nb * w) & 1) O[o + (long long)nb * w] = 0.0;
+        o += ti_even((long long)nb * w);
+      }
+    }
+  }
+}
+
 int inv_factor3(int n, int n_mac, double* scratch, int* piv, double* tiled, int* status, cudaStream_t st) {
   const size_t bytes = gj2_smem_bytes(n);
   if (bytes > 227 * 1024 || n > 384) return -1;
@@ -1430,7 +1474,9 @@ int inv_factor3(int n, int n_mac, double* scratch, int* piv, double* tiled, int*
   int rc = launch_ok();
   if (rc) return rc;
   tl_begin(TL_PACK, st);
-  k_pack_inv_gather<<<n_mac, 256, sizeof(int) * 2 * n, st>>>(n, scratch, piv, tiled);
+  const size_t pb = sizeof(double) * 8 * ((n + 1) & ~1) + sizeof(int) * 2 * n;
+  if (pb > 48 * 1024) cudaFuncSetAttribute(k_pack_inv_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pb);
+  k_pack_inv_rows<<<n_mac, 256, pb, st>>>(n, scratch, piv, tiled);
   tl_end(TL_PACK, st);
   return launch_ok();
 }
@@ -1496,11 +1542,10 @@ __global__ void __launch_bounds__(256, 2) k_schur_mma(mhdg_disc g, mhdg_blocks b
 #pragma unroll
     for (int c = 0; c < D; ++c) ij[a][c] = __ldg(g.inv_jac + (size_t)mac * D * D + a * D + c);
 
-  {  // S <- state_state
-    const double2* src = reinterpret_cast<const double2*>(b.state_state + (size_t)mac * n * n);
-    double2* dst = reinterpret_cast<double2*>(Sm);
-    for (int i = tid; i < n * n / 2; i += blockDim.x) dst[i] = src[i];
-  }
+  // S = state_state + corrections without a copy pass: the first volume sub-element
+  // touching a node row (smallest K in the node's sorted incidence list) seeds its MMA
+  // accumulators from state_state; later touches accumulate onto S.
+  const double* SSm = b.state_state + (size_t)mac * n * n;
   // physical gradients per class, zero padding of the GEMM operands
   for (int idx = tid; idx < g.n_grad_cls * nq * nloc * D; idx += blockDim.x) {
     const int k = idx % D, base = idx - k;
@@ -1517,13 +1562,16 @@ __global__ void __launch_bounds__(256, 2) k_schur_mma(mhdg_disc g, mhdg_blocks b
   // C[M x LP] = Tp[M x 4 nks] PM[4 nks x LP], accumulated into S rows; rows m -> (node, s, r).
   // Per M tile all SCH_NT column tiles of C are loaded from S first (one memory latency per
   // M tile), accumulated by DMMA and stored.
-  auto gemm_into_s = [&](int M, int nks, auto&& row_node) {
+  auto gemm_into_s = [&](int M, int nks, auto&& row_node, int Kfirst) {
     const int mtiles = (M + 7) / 8, ntiles = (L + 7) / 8;
     for (int mt = warp; mt < mtiles; mt += 8) {
       const int m = mt * 8 + gq;
       const bool mok = m < M;
       const int a = m / (NS * NS), s = (m / NS) % NS, r = m % NS;
-      double* srow = Sm + (size_t)((mok ? row_node(a) : 0) * NS + s) * n + r;
+      const int node = mok ? row_node(a) : 0;
+      const bool first = Kfirst >= 0 && __ldg(g.vn_sub + __ldg(g.vn_ptr + node)) / nloc == Kfirst;
+      double* srow = Sm + (size_t)(node * NS + s) * n + r;
+      const double* crow = first ? SSm + (size_t)(node * NS + s) * n + r : srow;
       double af[SCH_KS];
 #pragma unroll
       for (int ks = 0; ks < SCH_KS; ++ks) af[ks] = ks < nks ? Tp[m * dm.sA + 4 * ks + t4] : 0.0;
@@ -1531,8 +1579,8 @@ __global__ void __launch_bounds__(256, 2) k_schur_mma(mhdg_disc g, mhdg_blocks b
 #pragma unroll
       for (int nt = 0; nt < SCH_NT; ++nt) {
         const int j0 = nt * 8 + 2 * t4;
-        c[nt][0] = (mok && nt < ntiles && j0 < L) ? srow[j0 * NS] : 0.0;
-        c[nt][1] = (mok && nt < ntiles && j0 + 1 < L) ? srow[(j0 + 1) * NS] : 0.0;
+        c[nt][0] = (mok && nt < ntiles && j0 < L) ? crow[j0 * NS] : 0.0;
+        c[nt][1] = (mok && nt < ntiles && j0 + 1 < L) ? crow[(j0 + 1) * NS] : 0.0;
       }
 #pragma unroll
       for (int nt = 0; nt < SCH_NT; ++nt)
@@ -1576,7 +1624,7 @@ __global__ void __launch_bounds__(256, 2) k_schur_mma(mhdg_disc g, mhdg_blocks b
       Tp[m * dm.sA + qr] = v;
     }
     __syncthreads();
-    gemm_into_s(dm.MV, dm.nks_v, [&](int a) { return __ldg(g.sub_conn + K * nloc + a); });
+    gemm_into_s(dm.MV, dm.nks_v, [&](int a) { return __ldg(g.sub_conn + K * nloc + a); }, K);
     __syncthreads();
   }
   // ---- face sub-elements (sign folded into T1') ----
@@ -1603,7 +1651,7 @@ __global__ void __launch_bounds__(256, 2) k_schur_mma(mhdg_disc g, mhdg_blocks b
       __syncthreads();
       gemm_into_s(dm.MF, dm.nks_f, [&](int a) {
         return __ldg(g.face_vol_nodes + f * g.Lf + __ldg(g.tri_conn + T * nlocf + a));
-      });
+      }, -1);
       __syncthreads();
     }
   }
