@@ -22,6 +22,11 @@ namespace mhdg {
 
 constexpr int ASM_THREADS = 256;
 
+// W1[q][a] blocks (NS x NS) are stored with stride NS*NS + 4 (2D: 20 doubles): the
+// SUPG product reads W1[q][b][u][t] across (b, t) lanes without bank conflicts
+template <int D>
+__host__ __device__ constexpr int W1S() { return (D + 2) * (D + 2) + 4; }
+
 template <int D>
 struct AsmSmem {
   int us, qs, uh, td, tf, gph, upt, qpt, wq, tq, prv, As, Adu, FG, Pp, sw, W1, cvol;
@@ -53,7 +58,7 @@ __host__ __device__ inline AsmSmem<D> asm_smem(const Sz& s) {
   TAKE(FG, s.nq * NS * D)
   TAKE(Pp, s.nq * D * NS)
   TAKE(sw, s.nq * NS)
-  TAKE(W1, s.nq * s.nloc * NS * NS)
+  TAKE(W1, s.nq * s.nloc * W1S<D>())
   TAKE(cvol, s.n_sub * s.nloc * NS)
   TAKE(fuh, s.nqf * NS)
   TAKE(fu, s.nqf * NS)
@@ -165,10 +170,14 @@ __global__ void __launch_bounds__(ASM_THREADS)
   if (want_jac) {
     const double coeff = stage.dt_coeff + (isinf(stage.pseudo_dt) ? 0.0 : 1.0 / stage.pseudo_dt);
     double* SSm = bk.state_state + (size_t)mac * n * n;
-    for (size_t i = tid; i < (size_t)n * n; i += nt) {
-      const int r = (int)(i / n), c = (int)(i % n);
-      const int I = r / NS, s = r % NS, J = c / NS, t = c % NS;
-      SSm[i] = (s == t && coeff != 0.0) ? coeff * det * g.mass[I * L + J] : 0.0;
+    const int lane = tid & 31, nwarp = nt >> 5;
+    for (int r = tid >> 5; r < n; r += nwarp) {  // a warp per row: no runtime divisions per entry
+      const int I = r / NS, s = r % NS;
+      double* row = SSm + (size_t)r * n;
+      for (int c = lane; c < n; c += 32) {
+        const int J = c / NS, t = c - J * NS;
+        row[c] = (s == t && coeff != 0.0) ? coeff * det * g.mass[I * L + J] : 0.0;
+      }
     }
     const size_t fb = (size_t)NF * sz.bs * sz.bs;
     for (size_t i = tid; i < fb; i += nt) {
@@ -302,7 +311,7 @@ __global__ void __launch_bounds__(ASM_THREADS)
         double acc = 0.0;
 #pragma unroll
         for (int k = 0; k < D; ++k) acc += As[((qq * D + k) * NS + uu) * NS + s] * gph[(qq * nloc + a) * D + k];
-        W1[idx] = acc;  // W1[q][a][u][s]
+        W1[(qq * nloc + a) * W1S<D>() + uu * NS + s] = acc;  // W1[q][a][u][s]
       }
       __syncthreads();
       // contrib[a,s,b,t] = -sum w Adu[k,s,t] gphys[a,k] phi[b] + sum w tau W1[a,u,s] W1[b,u,t]
@@ -318,11 +327,11 @@ __global__ void __launch_bounds__(ASM_THREADS)
 #pragma unroll
           for (int k = 0; k < D; ++k) y += Adu[((qq * D + k) * NS + s) * NS + t] * gph[(qq * nloc + a) * D + k];
           y = -w * y;
-          if (stage.dt_coeff != 0.0) y += stage.dt_coeff * wt * W1[((qq * nloc + a) * NS + t) * NS + s];
+          if (stage.dt_coeff != 0.0) y += stage.dt_coeff * wt * W1[(qq * nloc + a) * W1S<D>() + t * NS + s];
           double z = 0.0;
 #pragma unroll
           for (int uu = 0; uu < NS; ++uu)
-            z += W1[((qq * nloc + a) * NS + uu) * NS + s] * W1[((qq * nloc + b) * NS + uu) * NS + t];
+            z += W1[(qq * nloc + a) * W1S<D>() + uu * NS + s] * W1[(qq * nloc + b) * W1S<D>() + uu * NS + t];
           acc += y * g.phi_vol[qq * nloc + b] + wt * z;
         }
         SSm[(size_t)(conn[a] * NS + s) * n + conn[b] * NS + t] += acc;

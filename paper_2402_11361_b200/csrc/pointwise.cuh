@@ -33,13 +33,14 @@ __host__ __device__ inline FlowC make_flow(const mhdg_flow& f) {
 
 template <int D>
 struct Prim {
-  double rho, v[D], kin, P, H, c, et;
+  double rho, irho, v[D], kin, P, H, c, et;  // irho = 1/rho: the Jacobian entries multiply by it
 };
 
 template <int D>
 __device__ __forceinline__ Prim<D> prim(const double* u, const FlowC& f) {
   Prim<D> p;
   p.rho = u[0];
+  p.irho = 1.0 / p.rho;
   p.kin = 0.0;
 #pragma unroll
   for (int i = 0; i < D; ++i) {
@@ -102,7 +103,7 @@ __device__ __forceinline__ double euler_jac(const Prim<D>& p, const FlowC& f, in
 template <int D>
 __device__ __forceinline__ double gvel(const Prim<D>& p, const double* q, int a, int b) {
   constexpr int NS = D + 2;
-  return (q[a * NS + 1 + b] - p.v[b] * q[a * NS]) / p.rho;
+  return (q[a * NS + 1 + b] - p.v[b] * q[a * NS]) * p.irho;
 }
 
 template <int D>
@@ -124,7 +125,8 @@ __device__ __forceinline__ double egrad(const Prim<D>& p, const double* q, int k
     vq += p.v[j] * qk[1 + j];
     v2 += p.v[j] * p.v[j];
   }
-  return qk[D + 1] / p.rho - p.et * qk[0] / (p.rho * p.rho) - vq / p.rho + v2 * qk[0] / p.rho;
+  const double ir = p.irho;
+  return qk[D + 1] * ir - p.et * qk[0] * (ir * ir) - vq * ir + v2 * qk[0] * ir;
 }
 
 // G[s][k]
@@ -141,8 +143,8 @@ __device__ __forceinline__ double visc_flux(const Prim<D>& p, const FlowC& f, co
 // g(b, t) = d gvel[a][b] / d q[a][t]
 template <int D>
 __device__ __forceinline__ double gq(const Prim<D>& p, int b, int t) {
-  if (t == 1 + b) return 1.0 / p.rho;
-  if (t == 0) return -p.v[b] / p.rho;
+  if (t == 1 + b) return p.irho;
+  if (t == 0) return -p.v[b] * p.irho;
   return 0.0;
 }
 
@@ -169,11 +171,11 @@ __device__ __forceinline__ double visc_dgdq(const Prim<D>& p, const FlowC& f, in
       double v2 = 0.0;
 #pragma unroll
       for (int j = 0; j < D; ++j) v2 += p.v[j] * p.v[j];
-      h = -p.et / (p.rho * p.rho) + v2 / p.rho;
+      h = -p.et * (p.irho * p.irho) + v2 * p.irho;
     } else if (t <= D) {
-      h = -p.v[t - 1] / p.rho;
+      h = -p.v[t - 1] * p.irho;
     } else {
-      h = 1.0 / p.rho;
+      h = p.irho;
     }
     out -= f.kg * h;
   }
@@ -186,8 +188,8 @@ template <int D>
 __device__ __forceinline__ double dgv_du(const Prim<D>& p, const double* q, int a, int b, int t) {
   constexpr int NS = D + 2;
   const double q0 = q[a * NS];
-  if (t == 0) return (p.v[b] / p.rho * q0 - gvel<D>(p, q, a, b)) / p.rho;
-  if (t == 1 + b) return -q0 / (p.rho * p.rho);
+  if (t == 0) return (p.v[b] * p.irho * q0 - gvel<D>(p, q, a, b)) * p.irho;
+  if (t == 1 + b) return -q0 * (p.irho * p.irho);
   return 0.0;
 }
 
@@ -212,12 +214,12 @@ __device__ __forceinline__ double visc_dgdu(const Prim<D>& p, const FlowC& f, co
   for (int j = 0; j < D; ++j) {
     acc += dtau_du<D>(p, f, q, k, j, t) * p.v[j];
     double dv = 0.0;
-    if (t == 0) dv = -p.v[j] / p.rho;
-    else if (t == 1 + j) dv = 1.0 / p.rho;
+    if (t == 0) dv = -p.v[j] * p.irho;
+    else if (t == 1 + j) dv = p.irho;
     if (dv != 0.0) acc += tau_entry<D>(p, f, q, k, j) * dv;
   }
   const double* qk = q + k * NS;
-  const double r2 = p.rho * p.rho;
+  const double ir2 = p.irho * p.irho;
   double dge;
   if (t == 0) {
     double vq = 0.0, v2 = 0.0;
@@ -226,11 +228,11 @@ __device__ __forceinline__ double visc_dgdu(const Prim<D>& p, const FlowC& f, co
       vq += p.v[j] * qk[1 + j];
       v2 += p.v[j] * p.v[j];
     }
-    dge = -qk[E] / r2 + 2.0 * p.et * qk[0] / (r2 * p.rho) + 2.0 * vq / r2 - 3.0 * v2 * qk[0] / r2;
+    dge = -qk[E] * ir2 + 2.0 * p.et * qk[0] * (ir2 * p.irho) + 2.0 * vq * ir2 - 3.0 * v2 * qk[0] * ir2;
   } else if (t <= D) {
-    dge = -qk[t] / r2 + 2.0 * p.v[t - 1] * qk[0] / r2;
+    dge = -qk[t] * ir2 + 2.0 * p.v[t - 1] * qk[0] * ir2;
   } else {
-    dge = -qk[0] / r2;
+    dge = -qk[0] * ir2;
   }
   return -acc - f.kg * dge;
 }
