@@ -174,9 +174,21 @@ __global__ void __launch_bounds__(ASM_THREADS)
     for (int r = tid >> 5; r < n; r += nwarp) {  // a warp per row: no runtime divisions per entry
       const int I = r / NS, s = r % NS;
       double* row = SSm + (size_t)r * n;
-      for (int c = lane; c < n; c += 32) {
-        const int J = c / NS, t = c - J * NS;
-        row[c] = (s == t && coeff != 0.0) ? coeff * det * g.mass[I * L + J] : 0.0;
+      if ((n & 1) == 0) {  // 16-byte stores
+        for (int c = 2 * lane; c < n; c += 64) {
+          double v[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int J = (c + e) / NS, t = c + e - J * NS;
+            v[e] = (s == t && coeff != 0.0) ? coeff * det * g.mass[I * L + J] : 0.0;
+          }
+          *reinterpret_cast<double2*>(row + c) = make_double2(v[0], v[1]);
+        }
+      } else {
+        for (int c = lane; c < n; c += 32) {
+          const int J = c / NS, t = c - J * NS;
+          row[c] = (s == t && coeff != 0.0) ? coeff * det * g.mass[I * L + J] : 0.0;
+        }
       }
     }
     const size_t fb = (size_t)NF * sz.bs * sz.bs;
