@@ -1495,7 +1495,12 @@ int inv_factor3(int n, int n_mac, double* scratch, int* piv, double* tiled, int*
 // reference order so S is deterministic.  Strides make the A (= 4 mod 16) and
 // B (= 8 mod 16) fragment loads conflict-free.
 // --------------------------------------------------------------------------
-constexpr int SCH_NT = 12, SCH_KS = 8;  // register tiles: L <= 96, (q, r') <= 32
+// register tiles per dimension: NT column tiles (L <= 8 NT), KS k-steps ((q, r') <= 4 KS);
+// the left factor is built for MC rows (a, s, r) at a time
+template <int D>
+struct SchT {
+  static constexpr int NT = D == 2 ? 12 : 5, KS = D == 2 ? 8 : 21, MC = D == 2 ? 160 : 64;
+};
 
 template <int D>
 struct SchurMmaDims {
@@ -1509,7 +1514,8 @@ struct SchurMmaDims {
     while (sA % 16 != 4) sA += 4;
     MV = g.nloc * NS * NS;
     MF = g.nlocf * NS * NS;
-    MVp = ((MV > MF ? MV : MF) + 7) / 8 * 8;
+    const int mmax = MV > MF ? MV : MF;
+    MVp = ((mmax < SchT<D>::MC ? mmax : SchT<D>::MC) + 7) / 8 * 8;  // rows of the left-factor buffer
     LP = (g.L + 7) / 8 * 8;
     if (LP % 16 == 0) LP += 8;
     nks_v = (kv + 3) / 4;
@@ -1562,35 +1568,37 @@ __global__ void __launch_bounds__(256, 2) k_schur_mma(mhdg_disc g, mhdg_blocks b
   // C[M x LP] = Tp[M x 4 nks] PM[4 nks x LP], accumulated into S rows; rows m -> (node, s, r).
   // Per M tile all SCH_NT column tiles of C are loaded from S first (one memory latency per
   // M tile), accumulated by DMMA and stored.
-  auto gemm_into_s = [&](int M, int nks, auto&& row_node, int Kfirst) {
+  constexpr int SNT = SchT<D>::NT, SKS = SchT<D>::KS;
+  // rows m0 .. m0 + M - 1 of the left factor, held in Tp rows 0 .. M - 1
+  auto gemm_into_s = [&](int M, int m0, int nks, auto&& row_node, int Kfirst) {
     const int mtiles = (M + 7) / 8, ntiles = (L + 7) / 8;
     for (int mt = warp; mt < mtiles; mt += 8) {
-      const int m = mt * 8 + gq;
-      const bool mok = m < M;
+      const int ml = mt * 8 + gq, m = m0 + ml;
+      const bool mok = ml < M;
       const int a = m / (NS * NS), s = (m / NS) % NS, r = m % NS;
       const int node = mok ? row_node(a) : 0;
       const bool first = Kfirst >= 0 && __ldg(g.vn_sub + __ldg(g.vn_ptr + node)) / nloc == Kfirst;
       double* srow = Sm + (size_t)(node * NS + s) * n + r;
       const double* crow = first ? SSm + (size_t)(node * NS + s) * n + r : srow;
-      double af[SCH_KS];
+      double af[SKS];
 #pragma unroll
-      for (int ks = 0; ks < SCH_KS; ++ks) af[ks] = ks < nks ? Tp[m * dm.sA + 4 * ks + t4] : 0.0;
-      double c[SCH_NT][2];
+      for (int ks = 0; ks < SKS; ++ks) af[ks] = ks < nks ? Tp[ml * dm.sA + 4 * ks + t4] : 0.0;
+      double c[SNT][2];
 #pragma unroll
-      for (int nt = 0; nt < SCH_NT; ++nt) {
+      for (int nt = 0; nt < SNT; ++nt) {
         const int j0 = nt * 8 + 2 * t4;
         c[nt][0] = (mok && nt < ntiles && j0 < L) ? crow[j0 * NS] : 0.0;
         c[nt][1] = (mok && nt < ntiles && j0 + 1 < L) ? crow[(j0 + 1) * NS] : 0.0;
       }
 #pragma unroll
-      for (int nt = 0; nt < SCH_NT; ++nt)
+      for (int nt = 0; nt < SNT; ++nt)
         if (nt < ntiles) {
 #pragma unroll
-          for (int ks = 0; ks < SCH_KS; ++ks)
+          for (int ks = 0; ks < SKS; ++ks)
             if (ks < nks) dmma_8x8x4(c[nt][0], c[nt][1], af[ks], PM[(4 * ks + t4) * dm.LP + nt * 8 + gq]);
         }
 #pragma unroll
-      for (int nt = 0; nt < SCH_NT; ++nt) {
+      for (int nt = 0; nt < SNT; ++nt) {
         const int j0 = nt * 8 + 2 * t4;
         if (mok && nt < ntiles && j0 < L) srow[j0 * NS] = c[nt][0];
         if (mok && nt < ntiles && j0 + 1 < L) srow[(j0 + 1) * NS] = c[nt][1];
@@ -1608,24 +1616,27 @@ __global__ void __launch_bounds__(256, 2) k_schur_mma(mhdg_disc g, mhdg_blocks b
     }
     __syncthreads();
     const int cls = __ldg(g.grad_cls_of + K);
-    for (int idx = tid; idx < dm.MV * dm.kv; idx += blockDim.x) {
-      const int qr = idx % dm.kv, m = idx / dm.kv;
-      const int q = qr / D, rp = qr % D, a = m / (NS * NS), s = (m / NS) % NS, r = m % NS;
-      const double* gp = gph + ((cls * nq + q) * nloc + a) * D;
-      const double* w = Wst + q * NW + s * NS + r;
-      double v = 0.0;
+    for (int m0 = 0; m0 < dm.MV; m0 += dm.MVp) {
+      const int mc = min(dm.MVp, dm.MV - m0);
+      for (int idx = tid; idx < mc * dm.kv; idx += blockDim.x) {
+        const int qr = idx % dm.kv, ml = idx / dm.kv, m = m0 + ml;
+        const int q = qr / D, rp = qr % D, a = m / (NS * NS), s = (m / NS) % NS, r = m % NS;
+        const double* gp = gph + ((cls * nq + q) * nloc + a) * D;
+        const double* w = Wst + q * NW + s * NS + r;
+        double v = 0.0;
 #pragma unroll
-      for (int l = 0; l < D; ++l) {
-        double t = 0.0;
+        for (int l = 0; l < D; ++l) {
+          double t = 0.0;
 #pragma unroll
-        for (int k = 0; k < D; ++k) t += gp[k] * w[(k * D + l) * NS * NS];
-        v += ij[rp][l] * t;
+          for (int k = 0; k < D; ++k) t += gp[k] * w[(k * D + l) * NS * NS];
+          v += ij[rp][l] * t;
+        }
+        Tp[ml * dm.sA + qr] = v;
       }
-      Tp[m * dm.sA + qr] = v;
+      __syncthreads();
+      gemm_into_s(mc, m0, dm.nks_v, [&](int a) { return __ldg(g.sub_conn + K * nloc + a); }, K);
+      __syncthreads();
     }
-    __syncthreads();
-    gemm_into_s(dm.MV, dm.nks_v, [&](int a) { return __ldg(g.sub_conn + K * nloc + a); }, K);
-    __syncthreads();
   }
   // ---- face sub-elements (sign folded into T1') ----
   for (int idx = tid; idx < dm.MVp * dm.sA; idx += blockDim.x) Tp[idx] = 0.0;
@@ -1640,18 +1651,22 @@ __global__ void __launch_bounds__(256, 2) k_schur_mma(mhdg_disc g, mhdg_blocks b
         PM[qr * dm.LP + j] = __ldg(g.pm_face + (((size_t)f * g.n_tri + T) * dm.kf + qr) * L + j);
       }
       __syncthreads();
-      for (int idx = tid; idx < dm.MF * dm.kf; idx += blockDim.x) {
-        const int qr = idx % dm.kf, m = idx / dm.kf;
-        const int q = qr / D, rp = qr % D, a = m / (NS * NS), s = (m / NS) % NS, r = m % NS;
-        double v = 0.0;
+      for (int m0 = 0; m0 < dm.MF; m0 += dm.MVp) {
+        const int mc = min(dm.MVp, dm.MF - m0);
+        for (int idx = tid; idx < mc * dm.kf; idx += blockDim.x) {
+          const int qr = idx % dm.kf, ml = idx / dm.kf, m = m0 + ml;
+          const int q = qr / D, rp = qr % D, a = m / (NS * NS), s = (m / NS) % NS, r = m % NS;
+          double v = 0.0;
 #pragma unroll
-        for (int l = 0; l < D; ++l) v += ij[rp][l] * Wst[((q * D + l) * NS + s) * NS + r];
-        Tp[m * dm.sA + qr] = -v * __ldg(g.phi_face + q * nlocf + a);
+          for (int l = 0; l < D; ++l) v += ij[rp][l] * Wst[((q * D + l) * NS + s) * NS + r];
+          Tp[ml * dm.sA + qr] = -v * __ldg(g.phi_face + q * nlocf + a);
+        }
+        __syncthreads();
+        gemm_into_s(mc, m0, dm.nks_f, [&](int a) {
+          return __ldg(g.face_vol_nodes + f * g.Lf + __ldg(g.tri_conn + T * nlocf + a));
+        }, -1);
+        __syncthreads();
       }
-      __syncthreads();
-      gemm_into_s(dm.MF, dm.nks_f, [&](int a) {
-        return __ldg(g.face_vol_nodes + f * g.Lf + __ldg(g.tri_conn + T * nlocf + a));
-      }, -1);
       __syncthreads();
     }
   }
@@ -2110,7 +2125,8 @@ int schur_matrix(const mhdg_disc& g, const mhdg_blocks& b, double* S, cudaStream
   {  // tensor-core kernel when its operands fit (k-steps <= 16)
     const SchurMmaDims<D> dm(g);
     const size_t mb = sizeof(double) * dm.smem_doubles(g);
-    if (g_schur_variant == 0 && n % 2 == 0 && dm.nks_v <= SCH_KS && dm.nks_f <= SCH_KS && g.L <= 8 * SCH_NT &&
+    if (g_schur_variant == 0 && dm.nks_v <= SchT<D>::KS && dm.nks_f <= SchT<D>::KS &&
+        g.L <= 8 * SchT<D>::NT &&
         mb <= 227 * 1024 && g.grad_cls) {
       if (mb > 48 * 1024) cudaFuncSetAttribute(k_schur_mma<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mb);
       k_schur_mma<D><<<g.n_mac, 256, mb, st>>>(g, b, S);

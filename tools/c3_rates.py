@@ -1,0 +1,64 @@
+"""C3 (3D TGV, 16^3 x 6 macros, m=2, p=2) rates: apply (split / fused / generic),
+condensation, assembly -- for DESIGN's table (not a bench line)."""
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import bench  # noqa: E402
+from paper_2402_11361_b200 import _lib  # noqa: E402
+from paper_2402_11361_b200 import assembly as A  # noqa: E402
+from paper_2402_11361_b200.cases import TgvCase  # noqa: E402
+from paper_2402_11361_b200.condense import CondensedSchur  # noqa: E402
+from paper_2402_11361_b200.discretization import Discretization  # noqa: E402
+from paper_2402_11361_b200.mesh import build_cube_mesh  # noqa: E402
+
+n1d = int(sys.argv[1]) if len(sys.argv) > 1 else 16
+case = TgvCase(reynolds=1600.0, mach=0.1)
+disc = Discretization(build_cube_mesh(case.domain, n1d, 2, periodic=(True, True, True)), 2, case.params)
+u, uhat = disc.nodal_interpolant(case.initial_state)
+f = A.FieldState(torch.as_tensor(u, device="cuda"), None, torch.as_tensor(uhat, device="cuda"))
+f.q = A.gradient_refresh(disc, f.u, f.uhat)
+ctx = A.StageContext(50.0, torch.zeros_like(f.u), np.inf, 0.02)
+L = _lib.lib()
+blocks, _ = A.jacobian(disc, f, ctx)
+del blocks
+torch.cuda.synchronize()
+with _lib.Timeline(16) as ta:
+    blocks, _ = A.jacobian(disc, f, ctx)
+    torch.cuda.synchronize()
+cond = CondensedSchur.allocate(blocks)
+st = disc.device.status_buffer()
+cond.refactor_async(st)
+torch.cuda.synchronize()
+with _lib.Timeline(16) as tc:
+    cond.refactor_async(st)
+    torch.cuda.synchronize()
+A.raise_status(st, "condense")
+x = torch.randn(disc.n_trace, dtype=torch.float64, device="cuda")
+b_mac = bench.algorithmic_bytes_per_macro(disc)
+print(f"C3: {disc.n_mac} macros, n_trace {disc.n_trace}, B_ref {b_mac / 1e3:.1f} KB/macro, "
+      f"{b_mac * disc.n_mac / 1e9:.2f} GB/apply")
+print(f"assembly kernel {ta.ms.get('assemble', 0):.2f} ms = {disc.n_mac / ta.ms.get('assemble', 1) * 1e3:.3g} macros/s")
+tot = sum(tc.ms.values())
+print(f"condense {tot:.2f} ms = {disc.n_mac / tot * 1e3:.3g} macros/s  " + ", ".join(f"{k} {v:.2f}" for k, v in tc.ms.items()))
+for name, split, stream in (("split", 1, 1), ("fused", 0, 1), ("generic", 1, 0)):
+    L.mhdg_set_apply_split(split)
+    L.mhdg_set_stream_enabled(stream)
+    for _ in range(2):
+        cond.apply_trace(x)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(10):
+        cond.apply_trace(x)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 10
+    print(f"apply {name:8s} {ms:.3f} ms = {disc.n_trace / ms * 1e3:.3g} DOF-applies/s, "
+          f"{b_mac * disc.n_mac / ms / 1e6:.0f} GB/s (B_ref) = {b_mac * disc.n_mac / ms / 1e6 / 6533.2:.3f}")
+L.mhdg_set_apply_split(1)
+L.mhdg_set_stream_enabled(1)
