@@ -291,7 +291,7 @@ struct Work {
 };
 
 template <class C, int STAGES, int PART>
-__global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 ? 1 : 2)) k_apply_stream(mhdg_disc g, mhdg_blocks bk, mhdg_factors fac,
+__global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 || C::D == 3 ? 1 : 2)) k_apply_stream(mhdg_disc g, mhdg_blocks bk, mhdg_factors fac,
                                                              const double* __restrict__ x,
                                                              double* __restrict__ y_loc, int pref_ahead) {
   constexpr int D = C::D, NS = C::NS, NF = C::NF, L = C::L, LF = C::LF, BS = C::BS, LTR = C::LTR, n = C::n;
@@ -876,6 +876,19 @@ static int count_pieces() {
   return k;
 }
 
+// ring stages per kernel: 2D runs two CTAs per SM with MHDG_STAGES each; the 3D
+// work area allows one CTA per SM only, which then gets a deeper ring
+#ifndef MHDG_STAGES_3D_PRE
+#define MHDG_STAGES_3D_PRE 5
+#endif
+#ifndef MHDG_STAGES_3D_POST
+#define MHDG_STAGES_3D_POST 7
+#endif
+template <class C>
+__host__ __device__ constexpr int stages_of(int part) {
+  return C::D == 2 ? MHDG_STAGES : (part == 2 ? MHDG_STAGES_3D_POST : (part == 1 ? MHDG_STAGES_3D_PRE : MHDG_STAGES));
+}
+
 template <class C>
 static bool stream_ok(const mhdg_disc& g, const mhdg_blocks& b, const mhdg_factors& f) {
   static const int npieces = count_pieces<C>();
@@ -890,7 +903,7 @@ static bool stream_ok(const mhdg_disc& g, const mhdg_blocks& b, const mhdg_facto
   const bool tables = g.n_grad_cls >= 1 && g.grad_cls && g.grad_cls_of && g.node_to_face && g.minv_d_face &&
                       g.n_face_nodes == C::NFN;
   const size_t cls = (size_t)g.n_grad_cls * TSm<C>::CLS;
-  const size_t smem = sizeof(double) * ((size_t)MHDG_STAGES * ST_DBL + SSm<C>::total + TSm<C>::total +
+  const size_t smem = sizeof(double) * ((size_t)stages_of<C>(0) * ST_DBL + SSm<C>::total + TSm<C>::total +
                                         (cls <= (size_t)C::D * C::n ? cls : 2 * cls));
   return sizes && tables && f.kind == 0 && smem <= 227 * 1024 && al(b.face_state_trace) && al(b.face_trace_trace) &&
          al(b.face_trace_state) && al(b.wdgdq_vol) && al(b.wdgdq_face) && al(f.lu) && al(f.work);
@@ -960,12 +973,12 @@ static int launch_apply(const mhdg_disc& g, const mhdg_blocks& b, const mhdg_fac
                         double* y_loc, cudaStream_t st) {
   if (!f.work || !g_split) {
     tl_begin(TL_APPLY_FUSED, st);
-    const int rc0 = launch_stream<C, MHDG_STAGES, 0>(g, b, f, x, y_loc, st);
+    const int rc0 = launch_stream<C, stages_of<C>(0), 0>(g, b, f, x, y_loc, st);
     tl_end(TL_APPLY_FUSED, st);
     return rc0;
   }
   tl_begin(TL_APPLY_PRE, st);
-  int rc = launch_stream<C, MHDG_STAGES, 1>(g, b, f, x, y_loc, st);
+  int rc = launch_stream<C, stages_of<C>(1), 1>(g, b, f, x, y_loc, st);
   tl_end(TL_APPLY_PRE, st);
   if (rc) return rc;
   tl_begin(TL_APPLY_SI, st);
@@ -973,7 +986,7 @@ static int launch_apply(const mhdg_disc& g, const mhdg_blocks& b, const mhdg_fac
   tl_end(TL_APPLY_SI, st);
   if (rc) return rc;
   tl_begin(TL_APPLY_POST, st);
-  rc = launch_stream<C, MHDG_STAGES, 2>(g, b, f, x, y_loc, st);
+  rc = launch_stream<C, stages_of<C>(2), 2>(g, b, f, x, y_loc, st);
   tl_end(TL_APPLY_POST, st);
   return rc;
 }

@@ -62,3 +62,12 @@ for name, split, stream in (("split", 1, 1), ("fused", 0, 1), ("generic", 1, 0))
           f"{b_mac * disc.n_mac / ms / 1e6:.0f} GB/s (B_ref) = {b_mac * disc.n_mac / ms / 1e6 / 6533.2:.3f}")
 L.mhdg_set_apply_split(1)
 L.mhdg_set_stream_enabled(1)
+kb = bench.apply_kernel_bytes(disc)
+with _lib.Timeline(256) as tl:
+    for _ in range(10):
+        cond.apply_trace(x)
+    torch.cuda.synchronize()
+for k, v in tl.ms.items():
+    ms = v / tl.counts[k]
+    extra = f", {kb[k] / ms / 1e6:.0f} GB/s = {kb[k] / ms / 1e6 / 6533.2:.2f}" if k in kb else ""
+    print(f"  {k:12s} {ms:.3f} ms{extra}")

@@ -19,11 +19,23 @@ from paper_2402_11361_b200.condense import CondensedSchur  # noqa: E402
 
 L = _lib.lib()
 L.mhdg_stream_profile.argtypes = [C.c_void_p, C.c_int]
-case, disc = bench.c2_discretization()
-u, uhat = bench.c2_state(case, disc)
+if len(sys.argv) > 1 and sys.argv[1] == "c3":  # 3D TGV, 16^3 x 6 macros, m=2, p=2
+    from paper_2402_11361_b200.cases import TgvCase
+    from paper_2402_11361_b200.discretization import Discretization
+    from paper_2402_11361_b200.mesh import build_cube_mesh
+
+    case = TgvCase(reynolds=1600.0, mach=0.1)
+    disc = Discretization(build_cube_mesh(case.domain, 16, 2, periodic=(True, True, True)), 2, case.params)
+    u, uhat = disc.nodal_interpolant(case.initial_state)
+    ctx = A.StageContext(50.0, torch.zeros((disc.n_mac, disc.L, disc.ns), dtype=torch.float64, device="cuda"),
+                         float("inf"), 0.02)
+else:
+    case, disc = bench.c2_discretization()
+    u, uhat = bench.c2_state(case, disc)
+    ctx = A.StageContext.steady(1.0)
 f = A.FieldState(torch.as_tensor(u, device="cuda"), None, torch.as_tensor(uhat, device="cuda"))
 f.q = A.gradient_refresh(disc, f.u, f.uhat)
-blocks, _ = A.jacobian(disc, f, A.StageContext.steady(1.0))
+blocks, _ = A.jacobian(disc, f, ctx)
 cond = CondensedSchur.build(blocks)
 x = torch.randn(disc.n_trace, dtype=torch.float64, device="cuda")
 cond.apply_trace(x)
