@@ -175,8 +175,8 @@ int mhdg_timeline_end(double *ms, int *counts);
    place, 2 interchanges rows (the earlier kernel).  For A/B measurements. */
 void mhdg_set_factor_variant(int v);
 
-/* Schur-complement kernel: 0 (default) FP64 tensor cores (DMMA), 1 shared-memory
-   row blocks, 2 per-macro FFMA.  For A/B measurements. */
+/* Schur-complement kernel: 0 (default) FP64 tensor cores (DMMA), otherwise the
+   per-macro FFMA kernel.  For A/B measurements. */
 void mhdg_set_schur_variant(int v);
 
 /* 1 (default): split apply (pre / S^-1 stream / post kernels) when `work` is

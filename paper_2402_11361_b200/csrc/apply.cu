@@ -8,7 +8,6 @@
 // k_grad_refresh  Discretization.gradient_refresh (assembly.py:247-252)
 // k_lu_solve      CondensedSchur._schur_solve (condense.py:80-83) with LU factors
 #include "local_ops.cuh"
-#include "lu_solve.cuh"
 #include "tiled_inv.cuh"
 
 namespace mhdg {
@@ -16,7 +15,7 @@ namespace mhdg {
 constexpr int APPLY_THREADS = 256;
 
 struct ApplySmem {
-  int xl, z, y, cfgz, acc, tmp, dblk, big, vv, wv, cv, wf, z2, cfg2, total;
+  int xl, z, y, cfgz, acc, tmp, big, vv, wv, cv, wf, z2, cfg2, total;
 };
 
 template <int D>
@@ -30,7 +29,6 @@ __host__ __device__ inline ApplySmem apply_smem(const Sz& s) {
   m.cfgz = o; o += s.ltr;
   m.acc = o; o += s.ltr;
   m.tmp = o; o += (s.n > s.ltr ? s.n : s.ltr);
-  m.dblk = o; o += TRI_NB * (TRI_NB + 1);
   m.big = o;
   const int nwf = NF * s.n_tri * s.nqf * NS;
   // phase C: vv | wv | cv | wf     phase E: z2 | wf | cfg2
@@ -57,7 +55,7 @@ __global__ void __launch_bounds__(APPLY_THREADS) k_apply_local(mhdg_disc g, mhdg
   const ApplySmem o = apply_smem<D>(sz);
   const int mac = blockIdx.x;
   double *xl = sm + o.xl, *z = sm + o.z, *y = sm + o.y, *cfgz = sm + o.cfgz, *acc = sm + o.acc,
-         *tmp = sm + o.tmp, *dblk = sm + o.dblk;
+         *tmp = sm + o.tmp;
 
   const int* gat = g.gather + (size_t)mac * sz.ltr;
   for (int i = threadIdx.x; i < sz.ltr; i += blockDim.x) xl[i] = __ldg(x + __ldg(gat + i));
@@ -108,8 +106,7 @@ __global__ void __launch_bounds__(APPLY_THREADS) k_rhs_local(mhdg_disc g, mhdg_b
   const Sz sz = make_sz<D>(g);
   const ApplySmem o = apply_smem<D>(sz);
   const int mac = blockIdx.x;
-  double *zr = sm + o.z, *y = sm + o.y, *cfgz = sm + o.cfgz, *acc = sm + o.acc, *tmp = sm + o.tmp,
-         *dblk = sm + o.dblk;
+  double *zr = sm + o.z, *y = sm + o.y, *cfgz = sm + o.cfgz, *acc = sm + o.acc, *tmp = sm + o.tmp;
   mass_solve<D>(g, sz, mac, R_grad + (size_t)mac * D * sz.L * NS, zr);
   for (int i = threadIdx.x; i < sz.n; i += blockDim.x) y[i] = __ldg(R_state + (size_t)mac * sz.n + i);
   __syncthreads();
@@ -147,8 +144,7 @@ __global__ void __launch_bounds__(APPLY_THREADS) k_recover(mhdg_disc g, mhdg_blo
   const ApplySmem o = apply_smem<D>(sz);
   const int mac = blockIdx.x;
   // reuse the apply layout: z -> z, cfgz -> (face sums), extra vectors after o.total
-  double *xl = sm + o.xl, *z = sm + o.z, *y = sm + o.y, *cfg = sm + o.cfgz, *tmp = sm + o.tmp,
-         *dblk = sm + o.dblk;
+  double *xl = sm + o.xl, *z = sm + o.z, *y = sm + o.y, *cfg = sm + o.cfgz, *tmp = sm + o.tmp;
   double *zr = sm + o.total, *w = zr + D * sz.L * NS;
   const int* gat = g.gather + (size_t)mac * sz.ltr;
   for (int i = threadIdx.x; i < sz.ltr; i += blockDim.x) xl[i] = __ldg(dtrace + __ldg(gat + i));
@@ -197,13 +193,12 @@ __global__ void __launch_bounds__(APPLY_THREADS) k_lu_solve(int n, mhdg_factors 
                                                             double* __restrict__ yout) {
   extern __shared__ double sm[];
   const int mac = blockIdx.x;
-  double *y = sm, *tmp = y + n, *dblk = tmp + n;
+  double *y = sm, *tmp = y + n;
   for (int i = threadIdx.x; i < n; i += blockDim.x) y[i] = b[(size_t)mac * n + i];
   __syncthreads();
   factor_solve_cta(fac, mac, n, y, tmp);
   for (int i = threadIdx.x; i < n; i += blockDim.x) y[i] = tmp[i];
   __syncthreads();
-  (void)dblk;
   for (int i = threadIdx.x; i < n; i += blockDim.x) yout[(size_t)mac * n + i] = y[i];
 }
 
@@ -266,7 +261,7 @@ int grad_refresh(const mhdg_disc& g, const double* u, const double* uhat, double
 
 int lu_solve(const mhdg_disc& g, const mhdg_factors& f, const double* bvec, double* y, cudaStream_t st) {
   const int n = g.L * g.ns;
-  const size_t bytes = sizeof(double) * (2 * n + TRI_NB * (TRI_NB + 1));
+  const size_t bytes = sizeof(double) * 2 * n;
   set_smem(k_lu_solve, bytes);
   k_lu_solve<<<g.n_mac, APPLY_THREADS, bytes, st>>>(n, f, bvec, y);
   return launch_ok();

@@ -28,7 +28,6 @@ int icgs(int n, int j, const double* V, long long ldv, double* w, double* out, d
 long long icgs_scratch_size(int n);
 size_t gj_smem_bytes(int n);
 int apply_stream(const mhdg_disc&, const mhdg_blocks&, const mhdg_factors&, const double*, double*, cudaStream_t);
-size_t lu_smem_bytes(int n);
 }  // namespace mhdg
 
 using namespace mhdg;

@@ -1,16 +1,17 @@
 // Second-layer static condensation on the device.
 //
-// k_schur   S = state_state - A_uq A_qq^-1 A_qu   (_schur_correction,
-//           condense.py:130-158).  Per sub-element (and face sub-element) the
-//           correction is one GEMM  X[(a,s,r), j] = sum_{(q,l)} T1[(a,s,r),(q,l)] VW[(q,l), j]
-//           with T1 = sum_k gphys W (the dG/dq stash) and
-//           VW[q,l,j] = sum_r inv_jac[r,l] PM[q,r,j], PM = phi M^-1 D (a
-//           macro-independent table), scattered into the rows of the
-//           sub-element's nodes.
-// k_lu      in-place LU with partial pivoting of each macro's S (replaces the
-//           reference's np.linalg.inv, condense.py:66-69; FactorizationError on
-//           an exactly zero pivot).  Right-looking, 32-column panels in shared
-//           memory, 64x64 register-tiled trailing updates.
+// k_schur_mma  S = state_state - A_uq A_qq^-1 A_qu (_schur_correction,
+//              condense.py:130-158) on the FP64 tensor cores; k_schur is the
+//              per-macro FFMA fallback (and A/B reference).
+// k_gj3        explicit S^-1 (np.linalg.inv, condense.py:62-70) by Gauss-Jordan
+//              with partial pivoting, pivots kept in place, DMMA updates;
+//              k_pack_inv_rows tiles it for the apply (tiled_inv.cuh).  k_gj2
+//              (row interchanges) and k_gj (32-column FFMA panels, any n that
+//              fits) are the A/B variant and the large-n fallback.
+// k_lu3        batched LU with partial pivoting (pivots in place), packed into
+//              block-triangular solve order by k_pack_lu3 (packed_lu.cuh): the
+//              MHDG_FACTOR=lu option.
+// FactorizationError on an exactly zero pivot.
 #include "common.cuh"
 #include "local_ops.cuh"
 #include "packed_lu.cuh"
@@ -141,169 +142,6 @@ __global__ void __launch_bounds__(SCHUR_THREADS) k_schur(mhdg_disc g, mhdg_block
   }
 }
 
-// --------------------------------------------------------------------------
-// k_schur_rb: the same correction, one CTA per (macro, block of SRB_NODES
-// lattice nodes).  The block's rows of S start from state_state in shared
-// memory, every (face) sub-element touching the block adds its rows there in
-// the order k_schur uses (so S is bitwise identical), and the rows are
-// written once: S costs one read of state_state and one write instead of a
-// read-modify-write of the touched rows per sub-element.
-// --------------------------------------------------------------------------
-constexpr int SRB_NODES = 4;
-
-// Cb rows of local nodes `ia` (lr[i] = local element node index, tr[i] = block row node)
-template <int D>
-__device__ __forceinline__ void schur_tile_rb(const double* T1, const double* VW, int m, int kk, int L, double* Cb,
-                                              int n, const int* tr, double sign) {
-  constexpr int NS = D + 2;
-  const int nas = m * NS, nj = (L + 3) / 4;
-  for (int task = threadIdx.x; task < nas * nj; task += blockDim.x) {
-    const int as = task / nj, j0 = (task - as * nj) * 4;
-    double acc[4][NS];
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-#pragma unroll
-      for (int r = 0; r < NS; ++r) acc[u][r] = 0.0;
-    for (int k = 0; k < kk; ++k) {
-      double tv[NS], vw[4];
-#pragma unroll
-      for (int r = 0; r < NS; ++r) tv[r] = T1[(r * nas + as) * kk + k];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) vw[u] = (j0 + u < L) ? VW[k * L + j0 + u] : 0.0;
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int r = 0; r < NS; ++r) acc[u][r] += tv[r] * vw[u];
-    }
-    double* out = Cb + (size_t)(tr[as / NS] * NS + as % NS) * n + j0 * NS;
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (j0 + u < L) {
-#pragma unroll
-        for (int r = 0; r < NS; ++r) out[u * NS + r] += sign * acc[u][r];
-      }
-  }
-}
-
-template <int D>
-__global__ void __launch_bounds__(SCHUR_THREADS, 2) k_schur_rb(mhdg_disc g, mhdg_blocks b, double* __restrict__ S) {
-  extern __shared__ double sm[];
-  constexpr int NS = D + 2, NF = D + 1;
-  const Sz sz = make_sz<D>(g);
-  const int nrb = (sz.L + SRB_NODES - 1) / SRB_NODES;
-  const int mac = blockIdx.x / nrb, rb = blockIdx.x - mac * nrb;
-  const int I0 = rb * SRB_NODES, nI = min(SRB_NODES, sz.L - I0);
-  const int n = sz.n, L = sz.L, tid = threadIdx.x;
-  const double* ij = g.inv_jac + (size_t)mac * D * D;
-  const int kv = sz.nq * D, kf = sz.nqf * D, kmax = kv > kf ? kv : kf;
-  double* Cb = sm;                              // SRB_NODES*NS rows x n
-  double* VW = Cb + (size_t)SRB_NODES * NS * n;  // kmax x L
-  double* T1 = VW + (size_t)kmax * L;           // NS x (SRB_NODES*NS) x kmax
-  __shared__ int la[SRB_NODES], tr[SRB_NODES], cnt;
-
-  {  // the block's rows of state_state (contiguous, 16-byte vectors)
-    const double2* src = reinterpret_cast<const double2*>(b.state_state + ((size_t)mac * n + (size_t)I0 * NS) * n);
-    double2* dst = reinterpret_cast<double2*>(Cb);
-    const int nv = nI * NS * n / 2;
-    for (int i = tid; i < nv; i += blockDim.x) dst[i] = src[i];
-  }
-
-  // ---- volume sub-elements ----
-  for (int K = 0; K < sz.n_sub; ++K) {
-    if (tid == 0) {
-      int c = 0;
-      for (int a = 0; a < sz.nloc; ++a) {
-        const int I = __ldg(g.sub_conn + K * sz.nloc + a) - I0;
-        if (I >= 0 && I < nI) {
-          la[c] = a;
-          tr[c] = I;
-          ++c;
-        }
-      }
-      cnt = c;
-    }
-    __syncthreads();
-    const int m = cnt;
-    if (m == 0) continue;
-    for (int idx = tid; idx < kv * L; idx += blockDim.x) {
-      const int j = idx % L, ql = idx / L, l = ql % D, q = ql / D;
-      const double* pm = g.pm_vol + (((size_t)K * sz.nq + q) * D) * L + j;
-      double a = 0.0;
-#pragma unroll
-      for (int r = 0; r < D; ++r) a += __ldg(ij + r * D + l) * __ldg(pm + r * L);
-      VW[idx] = a;
-    }
-    const int nas = m * NS;
-    for (int idx = tid; idx < NS * nas * kv; idx += blockDim.x) {
-      const int ql = idx % kv, rest = idx / kv, as = rest % nas, rr = rest / nas;
-      const int s = as % NS, a = la[as / NS], l = ql % D, q = ql / D;
-      const double* gr = g.grad_ref + (((size_t)K * sz.nq + q) * sz.nloc + a) * D;
-      const double* W = b.wdgdq_vol + ((((size_t)mac * sz.n_sub + K) * sz.nq + q) * D * D) * NS * NS;
-      double acc = 0.0;
-#pragma unroll
-      for (int k = 0; k < D; ++k) {
-        double gp = 0.0;
-#pragma unroll
-        for (int r = 0; r < D; ++r) gp += __ldg(gr + r) * __ldg(ij + r * D + k);
-        acc += gp * __ldg(W + ((k * D + l) * NS + s) * NS + rr);
-      }
-      T1[idx] = acc;
-    }
-    __syncthreads();
-    schur_tile_rb<D>(T1, VW, m, kv, L, Cb, n, tr, 1.0);
-    __syncthreads();
-  }
-  // ---- face sub-elements ----
-  for (int f = 0; f < NF; ++f) {
-    for (int T = 0; T < sz.n_tri; ++T) {
-      if (tid == 0) {
-        int c = 0;
-        for (int a = 0; a < sz.nlocf; ++a) {
-          const int I = __ldg(g.face_vol_nodes + f * sz.Lf + __ldg(g.tri_conn + T * sz.nlocf + a)) - I0;
-          if (I >= 0 && I < nI) {
-            la[c] = a;
-            tr[c] = I;
-            ++c;
-          }
-        }
-        cnt = c;
-      }
-      __syncthreads();
-      const int m = cnt;
-      if (m == 0) continue;
-      for (int idx = tid; idx < kf * L; idx += blockDim.x) {
-        const int j = idx % L, ql = idx / L, l = ql % D, q = ql / D;
-        const double* pm = g.pm_face + ((((size_t)f * sz.n_tri + T) * sz.nqf + q) * D) * L + j;
-        double a = 0.0;
-#pragma unroll
-        for (int r = 0; r < D; ++r) a += __ldg(ij + r * D + l) * __ldg(pm + r * L);
-        VW[idx] = a;
-      }
-      const int nas = m * NS;
-      for (int idx = tid; idx < NS * nas * kf; idx += blockDim.x) {
-        const int ql = idx % kf, rest = idx / kf, as = rest % nas, rr = rest / nas;
-        const int s = as % NS, a = la[as / NS], l = ql % D, q = ql / D;
-        const double* W = b.wdgdq_face +
-                          ((((size_t)mac * NF + f) * sz.n_tri * sz.nqf + T * sz.nqf + q) * D + l) * NS * NS;
-        T1[idx] = __ldg(W + s * NS + rr) * __ldg(g.phi_face + q * sz.nlocf + a);
-      }
-      __syncthreads();
-      schur_tile_rb<D>(T1, VW, m, kf, L, Cb, n, tr, -1.0);
-      __syncthreads();
-    }
-  }
-  {
-    double2* dst = reinterpret_cast<double2*>(S + ((size_t)mac * n + (size_t)I0 * NS) * n);
-    const double2* src = reinterpret_cast<const double2*>(Cb);
-    const int nv = nI * NS * n / 2;
-    for (int i = tid; i < nv; i += blockDim.x) dst[i] = src[i];
-  }
-}
-
-// --------------------------------------------------------------------------
-// batched LU with partial pivoting
-// --------------------------------------------------------------------------
-
 __device__ __forceinline__ void block_argmax(double v, int i, double* rv, int* ri, double* outv, int* outi) {
   // max |v|, ties -> smallest index (LAPACK idamax semantics)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -328,225 +166,6 @@ __device__ __forceinline__ void block_argmax(double v, int i, double* rv, int* r
   }
   __syncthreads();
 }
-
-__global__ void __launch_bounds__(LU_THREADS) k_lu(int n, double* __restrict__ LU, int* __restrict__ perm,
-                                                   int* status) {
-  extern __shared__ double sm[];
-  constexpr int PW = LU_NB + 1;  // padded panel row
-  const int mac = blockIdx.x, tid = threadIdx.x;
-  double* A = LU + (size_t)mac * n * n;
-  int* pm = perm + (size_t)mac * n;
-  double* P = sm;                               // n x PW panel
-  double* Ut = P + (size_t)n * PW;              // LU_NB x 64 U12 tile
-  double* Ar = Ut + LU_NB * 64;                 // LU_NB x 64 staged A12 tile
-  double* Li = Ar + LU_NB * 64;                 // LU_NB x PW  L11^-1
-  double* red_v = Li + LU_NB * PW;              // 32
-  int* red_i = (int*)(red_v + 32);              // 32
-  int* piv = red_i + 32;                        // LU_NB
-  double* bcast = (double*)(piv + LU_NB + 2);   // 2 (aligned below)
-  int* bidx = (int*)(bcast + 2);
-  for (int i = tid; i < n; i += blockDim.x) pm[i] = i;
-  bool singular = false;
-
-  for (int k0 = 0; k0 < n; k0 += LU_NB) {
-    const int nb = min(LU_NB, n - k0), m = n - k0;
-    for (int idx = tid; idx < m * nb; idx += blockDim.x) {
-      const int i = idx / nb, c = idx - i * nb;
-      P[i * PW + c] = A[(size_t)(k0 + i) * n + k0 + c];
-    }
-    __syncthreads();
-    for (int j = 0; j < nb; ++j) {
-      // pivot search over panel rows j..m-1 of column j
-      double best = -1.0;
-      int bi = 0x7fffffff;
-      for (int i = j + tid; i < m; i += blockDim.x) {
-        const double v = fabs(P[i * PW + j]);
-        if (v > best || (v == best && i < bi)) { best = v; bi = i; }
-      }
-      block_argmax(best, bi, red_v, red_i, bcast, bidx);
-      const int p = *bidx;
-      if (tid == 0) piv[j] = p;
-      if (*bcast == 0.0) singular = true;
-      if (p != j) {
-        for (int c = tid; c < nb; c += blockDim.x) {
-          const double t = P[j * PW + c];
-          P[j * PW + c] = P[p * PW + c];
-          P[p * PW + c] = t;
-        }
-      }
-      __syncthreads();
-      const double dinv = singular ? 0.0 : 1.0 / P[j * PW + j];
-      for (int i = j + 1 + tid; i < m; i += blockDim.x) P[i * PW + j] *= dinv;
-      __syncthreads();
-      // rank-1 update of the remaining panel columns
-      const int w = nb - j - 1;
-      if (w > 0) {
-        for (int idx = tid; idx < (m - j - 1) * w; idx += blockDim.x) {
-          const int i = j + 1 + idx / w, c = j + 1 + idx % w;
-          P[i * PW + c] -= P[i * PW + j] * P[j * PW + c];
-        }
-      }
-      __syncthreads();
-    }
-    // write the panel back; apply the panel's interchanges to the other columns
-    for (int idx = tid; idx < m * nb; idx += blockDim.x) {
-      const int i = idx / nb, c = idx - i * nb;
-      A[(size_t)(k0 + i) * n + k0 + c] = P[i * PW + c];
-    }
-    for (int j = 0; j < nb; ++j) {
-      const int p = piv[j];
-      if (p == j) continue;
-      const size_t r1 = (size_t)(k0 + j) * n, r2 = (size_t)(k0 + p) * n;
-      for (int c = tid; c < n - nb; c += blockDim.x) {
-        const int cc = c < k0 ? c : c + nb;
-        const double t = A[r1 + cc];
-        A[r1 + cc] = A[r2 + cc];
-        A[r2 + cc] = t;
-      }
-      if (tid == 0) {
-        const int t = pm[k0 + j];
-        pm[k0 + j] = pm[k0 + p];
-        pm[k0 + p] = t;
-      }
-      __syncthreads();
-    }
-    __syncthreads();
-    const int c0 = k0 + nb;
-    if (c0 >= n) break;
-    // Li = L11^-1 (unit lower), one column per thread
-    for (int c = tid; c < LU_NB; c += blockDim.x) {
-      for (int i = 0; i < LU_NB; ++i) Li[i * PW + c] = (i == c) ? 1.0 : 0.0;
-      for (int i = c + 1; i < nb; ++i) {
-        double acc = 0.0;
-        for (int k = c; k < i; ++k) acc += P[i * PW + k] * Li[k * PW + c];
-        Li[i * PW + c] = -acc;
-      }
-    }
-    __syncthreads();
-    // per 64-column tile: U12 = Li A12 (staged in smem), then A22 -= L21 U12
-    const int rows = n - c0;
-    const int tx = tid & 15, ty = tid >> 4;
-    for (int tc = 0; tc < rows; tc += 64) {
-      const int wc = min(64, rows - tc);
-      for (int idx = tid; idx < LU_NB * 64; idx += blockDim.x) {
-        const int r = idx / 64, c = idx % 64;
-        Ar[r * 64 + c] = (c < wc && r < nb) ? A[(size_t)(k0 + r) * n + c0 + tc + c] : 0.0;
-      }
-      __syncthreads();
-      for (int idx = tid; idx < LU_NB * 64; idx += blockDim.x) {
-        const int r = idx / 64, c = idx % 64;
-        double acc = 0.0;
-        for (int k = 0; k <= r; ++k) acc += Li[r * PW + k] * Ar[k * 64 + c];
-        Ut[r * 64 + c] = acc;
-        if (c < wc && r < nb) A[(size_t)(k0 + r) * n + c0 + tc + c] = acc;
-      }
-      __syncthreads();
-      for (int tr = 0; tr < rows; tr += 64) {
-        double acc[4][4];
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-          for (int bq = 0; bq < 4; ++bq) acc[a][bq] = 0.0;
-        for (int k = 0; k < nb; ++k) {
-          double lv[4], uv[4];
-#pragma unroll
-          for (int a = 0; a < 4; ++a) {
-            const int i = tr + ty + 16 * a;
-            lv[a] = i < rows ? P[(nb + i) * PW + k] : 0.0;
-          }
-#pragma unroll
-          for (int bq = 0; bq < 4; ++bq) uv[bq] = Ut[k * 64 + tx + 16 * bq];
-#pragma unroll
-          for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int bq = 0; bq < 4; ++bq) acc[a][bq] += lv[a] * uv[bq];
-        }
-#pragma unroll
-        for (int a = 0; a < 4; ++a) {
-          const int i = tr + ty + 16 * a;
-          if (i >= rows) continue;
-#pragma unroll
-          for (int bq = 0; bq < 4; ++bq) {
-            const int c = tx + 16 * bq;
-            if (c < wc) A[(size_t)(c0 + i) * n + c0 + tc + c] -= acc[a][bq];
-          }
-        }
-      }
-      __syncthreads();
-    }
-  }
-  if (singular && tid == 0) set_status(status, MHDG_ERR_FACTORIZATION, mac, 0, 0.0);
-}
-
-// --------------------------------------------------------------------------
-// pack: factored n x n (scratch) -> packed solve layout with inverted diagonal
-// tiles (packed_lu.cuh)
-// --------------------------------------------------------------------------
-
-__global__ void __launch_bounds__(256) k_pack(int n, const double* __restrict__ F, double* __restrict__ out) {
-  extern __shared__ double pk_sm[];
-  double(*T)[PLU_NB + 1] = reinterpret_cast<double(*)[PLU_NB + 1]>(pk_sm);
-  double(*X)[PLU_NB + 1] = reinterpret_cast<double(*)[PLU_NB + 1]>(pk_sm + PLU_NB * (PLU_NB + 1));
-  const int mac = blockIdx.x, tid = threadIdx.x;
-  const double* A = F + (size_t)mac * n * n;
-  double* O = out + (size_t)mac * plu_size(n);
-  const int nblk = plu_nblk(n);
-  for (int b = 0; b < nblk; ++b) {
-    const PluOffsets o = plu_offsets(n, b);
-    const int nb = o.nb, r0 = o.r0;
-    for (int idx = tid; idx < nb * o.ncol_fwd; idx += blockDim.x) {
-      const int r = idx / o.ncol_fwd, c = idx % o.ncol_fwd;
-      O[o.fwd_panel + plu_panel_idx(nb, o.ncol_fwd, r, c)] = A[(size_t)(r0 + r) * n + c];
-    }
-    for (int idx = tid; idx < nb * o.ncol_bwd; idx += blockDim.x) {
-      const int r = idx / o.ncol_bwd, c = idx % o.ncol_bwd;
-      O[o.bwd_panel + plu_panel_idx(nb, o.ncol_bwd, r, c)] = A[(size_t)(r0 + r) * n + r0 + nb + c];
-    }
-    for (int idx = tid; idx < nb * nb; idx += blockDim.x) {
-      const int r = idx / nb, c = idx % nb;
-      T[r][c] = A[(size_t)(r0 + r) * n + r0 + c];
-    }
-    __syncthreads();
-    if (tid < nb) {  // inverse of the unit lower tile, column tid
-      const int c = tid;
-      X[c][c] = 1.0;
-      for (int i = c + 1; i < nb; ++i) {
-        double acc = 0.0;
-        for (int k = c; k < i; ++k) acc += T[i][k] * X[k][c];
-        X[i][c] = -acc;
-      }
-    }
-    __syncthreads();
-    for (int idx = tid; idx < nb * nb; idx += blockDim.x) {
-      const int r = idx / nb, c = idx % nb;
-      if (c < r) O[o.fwd_diag + plu_lo(r, c)] = X[r][c];
-    }
-    __syncthreads();
-    if (tid < nb) {  // inverse of the upper tile, column tid
-      const int c = tid;
-      X[c][c] = 1.0 / T[c][c];
-      for (int i = c - 1; i >= 0; --i) {
-        double acc = 0.0;
-        for (int k = i + 1; k <= c; ++k) acc += T[i][k] * X[k][c];
-        X[i][c] = -acc / T[i][i];
-      }
-    }
-    __syncthreads();
-    for (int idx = tid; idx < nb * nb; idx += blockDim.x) {
-      const int r = idx / nb, c = idx % nb;
-      if (c >= r) O[o.bwd_diag + plu_up(nb, r, c)] = X[r][c];
-    }
-    if (tid == 0) {  // zero the even-size padding of the last (narrow) tiles and triangles
-      if ((nb * (nb - 1) / 2) & 1) O[o.fwd_diag + nb * (nb - 1) / 2] = 0.0;
-      if ((nb * (nb + 1) / 2) & 1) O[o.bwd_diag + nb * (nb + 1) / 2] = 0.0;
-      const int wf = o.ncol_fwd % PLU_TW, wb = o.ncol_bwd % PLU_TW;
-      if ((nb * wf) & 1) O[o.fwd_diag - 1] = 0.0;
-      if ((nb * wb) & 1) O[o.bwd_diag - 1] = 0.0;
-    }
-    __syncthreads();
-  }
-}
-
 
 // --------------------------------------------------------------------------
 // batched in-place Gauss-Jordan inversion with partial pivoting
@@ -1388,39 +1007,8 @@ __global__ void __launch_bounds__(512, 1) k_gj3(int n, double* __restrict__ S, i
   if (singular && tid == 0) set_status(status, MHDG_ERR_FACTORIZATION, mac, 0, 0.0);
 }
 
-// (P A)^-1 stored with row k in physical row piv[k] -> A^-1 in the tiled layout:
-// A^-1[i][j] = M[piv[i]][inv[j]], inv = piv^-1.
-__global__ void __launch_bounds__(256) k_pack_inv_gather(int n, const double* __restrict__ F,
-                                                         const int* __restrict__ piv, double* __restrict__ out) {
-  extern __shared__ int pp[];  // piv | inv
-  int* inv = pp + n;
-  const int mac = blockIdx.x;
-  const double* A = F + (size_t)mac * n * n;
-  double* O = out + (size_t)mac * ti_size(n);
-  for (int k = threadIdx.x; k < n; k += blockDim.x) {
-    const int p = piv[(size_t)mac * n + k];
-    pp[k] = p;
-    inv[p] = k;
-  }
-  __syncthreads();
-  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
-    const int r = idx / n, c = idx % n;
-    O[ti_idx(n, r, c)] = A[(size_t)pp[r] * n + inv[c]];
-  }
-  if (threadIdx.x == 0) {
-    for (int b = 0; b < ti_nblk(n); ++b) {
-      const int nb = ti_rows(n, b);
-      long long o = ti_block_off(n, b);
-      for (int c = 0; c < n; c += TI_CW) {
-        const int w = (n - c) < TI_CW ? n - c : TI_CW;
-        if (((long long)nb * w) & 1) O[o + (long long)nb * w] = 0.0;
-        o += ti_even((long long)nb * w);
-      }
-    }
-  }
-}
-
-// Same output as k_pack_inv_gather, row by row: each warp stages source row p_i
+// (P A)^-1 stored with row k in physical row piv[k] -> A^-1 in the tiled layout,
+// A^-1[i][j] = M[piv[i]][inv[j]], inv = piv^-1, row by row: each warp stages source row p_i
 // in shared memory with coalesced loads and writes the permuted row into its
 // 64-row block, one contiguous 32-column tile row per lane group.
 __global__ void __launch_bounds__(256) k_pack_inv_rows(int n, const double* __restrict__ F,
@@ -2114,7 +1702,7 @@ int inv_factor(int n, int n_mac, double* scratch, double* tiled, int* status, cu
 // host launchers
 // --------------------------------------------------------------------------
 
-int g_schur_variant = 0;  // 0: tensor cores, 1: row blocks, 2: per-macro FFMA (A/B knob)
+int g_schur_variant = 0;  // 0: tensor cores, else per-macro FFMA (A/B knob)
 
 template <int D>
 int schur_matrix(const mhdg_disc& g, const mhdg_blocks& b, double* S, cudaStream_t st) {
@@ -2133,34 +1721,9 @@ int schur_matrix(const mhdg_disc& g, const mhdg_blocks& b, double* S, cudaStream
       return launch_ok();
     }
   }
-  if (g_schur_variant <= 1 && (n * SRB_NODES * NS) % 2 == 0 && n % 2 == 0) {  // row-block kernel
-    const size_t rb = sizeof(double) * ((size_t)SRB_NODES * NS * n + (size_t)kmax * g.L + (size_t)NS * SRB_NODES * NS * kmax);
-    if (rb <= 227 * 1024) {
-      if (rb > 48 * 1024) cudaFuncSetAttribute(k_schur_rb<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rb);
-      const int nrb = (g.L + SRB_NODES - 1) / SRB_NODES;
-      k_schur_rb<D><<<g.n_mac * nrb, SCHUR_THREADS, rb, st>>>(g, b, S);
-      return launch_ok();
-    }
-  }
   const size_t bytes = sizeof(double) * ((size_t)NS * rmax * kmax + (size_t)kmax * g.L);
   if (bytes > 48 * 1024) cudaFuncSetAttribute(k_schur<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   k_schur<D><<<g.n_mac, SCHUR_THREADS, bytes, st>>>(g, b, S);
-  return launch_ok();
-}
-
-size_t lu_smem_bytes(int n) {
-  return sizeof(double) * ((size_t)n * (LU_NB + 1) + 2 * LU_NB * 64 + LU_NB * (LU_NB + 1) + 32 + 8) + sizeof(int) * (32 + LU_NB + 8) + 64;
-}
-
-int lu_factor(int n, int n_mac, double* scratch, double* packed, int* perm, int* status, cudaStream_t st) {
-  const size_t bytes = lu_smem_bytes(n);
-  if (bytes > 48 * 1024) cudaFuncSetAttribute(k_lu, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  k_lu<<<n_mac, LU_THREADS, bytes, st>>>(n, scratch, perm, status);
-  int rc = launch_ok();
-  if (rc) return rc;
-  const size_t pbytes = sizeof(double) * 2 * PLU_NB * (PLU_NB + 1);
-  cudaFuncSetAttribute(k_pack, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pbytes);
-  k_pack<<<n_mac, 256, pbytes, st>>>(n, scratch, packed);
   return launch_ok();
 }
 
