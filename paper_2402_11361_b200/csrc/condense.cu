@@ -1485,6 +1485,7 @@ __global__ void __launch_bounds__(NT, 2) k_lu3(int n, double* __restrict__ S, in
     constexpr int RPP = (NT / 64) * 16;       // rows per pass of the trailing product
     constexpr int TPT = (16 * TC + NT - 1) / NT;  // TRSM entries per thread and 16-row block
     for (int tc = 0; tc < nright; tc += TC) {
+      GJT(t6);
       const int wct = min(TC, nright - tc), cbase = k0 + nb + tc;
       for (int idx = tid; idx < NB * TC; idx += NT) {
         const int k = idx / TC, cc = idx % TC;
@@ -1531,6 +1532,8 @@ __global__ void __launch_bounds__(NT, 2) k_lu3(int n, double* __restrict__ S, in
         const int k = idx / wct, cc = idx % wct;
         A[(size_t)rows[ppos[k]] * n + cbase + cc] = Bt[k * BS + cc];
       }
+      GJADD(6, t6);
+      GJT(t7);
       // C -= L21 U12 over the panel's other rows: warp (wm, wn) owns 16 rows x 3 column tiles
       for (int tr = 0; tr < m; tr += RPP) {
         double acc[2][3][2];
@@ -1577,6 +1580,7 @@ __global__ void __launch_bounds__(NT, 2) k_lu3(int n, double* __restrict__ S, in
             }
       }
       __syncthreads();
+      GJADD(7, t7);
     }
     GJADD(4, t_up);
     GJT(t5);

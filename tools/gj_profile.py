@@ -34,5 +34,5 @@ buf = (C.c_ulonglong * 8)()
 L.mhdg_gj_profile(buf, 0)
 a = np.array(buf, dtype=np.float64) / disc.n_mac
 print(f"condense {e0.elapsed_time(e1):.1f} ms; cycles per macro (thread 0):")
-for nm, v in zip(["panel load", "subpanel GJ steps", "subpanel DMMA", "row swaps", "big update", "write back"], a):
+for nm, v in zip(["panel load", "subpanel GJ steps", "subpanel DMMA", "row swaps", "big update", "write back", "  (LU: stage+U12)", "  (LU: trailing)"], a):
     print(f"  {nm:18s} {v:10.0f}")
