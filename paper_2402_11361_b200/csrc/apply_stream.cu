@@ -181,24 +181,28 @@ struct Sched {
   }
 };
 
-template <class C>
-struct SSm {  // consumer work layout (doubles), after the ring
+// consumer work layout (doubles), after the ring; arrays a part does not use get
+// no space (pre: x, z, y1, A_hh x, face terms, W results; post: y2, z2, A_hu y2, ...)
+template <class C, int PART = 0>
+struct SSm {
+  static constexpr bool PRE = PART != 2, POST = PART != 1;
   static constexpr int xl = 0;
-  static constexpr int z = xl + C::LTR;  // z, later z2
+  static constexpr int z = xl + (PRE ? C::LTR : 0);  // z, later z2
   static constexpr int y = z + C::D * C::n;
   static constexpr int t = y + C::n;
-  static constexpr int rfst = t + C::n;
-  static constexpr int ftt = rfst + C::LTR;
+  static constexpr int rfst = t + (PART == 0 ? C::n : 0);
+  static constexpr int ftt = rfst + (PRE ? C::LTR : 0);
   static constexpr int fts = ftt + C::LTR;
-  static constexpr int cfgz = fts + C::LTR;
+  static constexpr int cfgz = fts + (POST ? C::LTR : 0);
   static constexpr int yf = cfgz + C::LTR;
-  static constexpr int wfz = yf + C::LTR;
-  static constexpr int wf2 = wfz + C::NPF * C::NS;
-  static constexpr int vv = wf2 + C::NPF * C::NS;  // one 32-double scratch per consumer warp
+  static constexpr int wfz = yf + (POST ? C::LTR : 0);
+  static constexpr int wf2 = wfz + (PRE ? C::NPF * C::NS : 0);
+  static constexpr int vv = wf2 + (POST ? C::NPF * C::NS : 0);  // one 32-double scratch per consumer warp
   static constexpr int cv = vv + (NCONS / 32) * 32;
-  static constexpr int tg = cv + C::NSUB * C::NLOC * C::NS;  // Gf x | W_vol results | M^-1 D y
-  static constexpr int TGN0 = C::NF * C::n;
-  static constexpr int TGN = TGN0 > C::NPV * C::D * C::NS ? TGN0 : C::NPV * C::D * C::NS;
+  static constexpr int tg = cv + (PRE ? C::NSUB * C::NLOC * C::NS : 0);  // Gf x | W_vol results | M^-1 D y
+  static constexpr int TGPRE = C::NF * C::n > C::NPV * C::D * C::NS ? C::NF * C::n : C::NPV * C::D * C::NS;
+  static constexpr int TGPOST = C::D * C::NFN * C::NS;
+  static constexpr int TGN = PART == 1 ? TGPRE : PART == 2 ? TGPOST : (TGPRE > TGPOST ? TGPRE : TGPOST);
   static constexpr int total = ceven(tg + TGN);
 };
 
@@ -291,7 +295,7 @@ struct Work {
 };
 
 template <class C, int STAGES, int PART>
-__global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 || C::D == 3 ? 1 : 2)) k_apply_stream(mhdg_disc g, mhdg_blocks bk, mhdg_factors fac,
+__global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 ? 1 : 2)) k_apply_stream(mhdg_disc g, mhdg_blocks bk, mhdg_factors fac,
                                                              const double* __restrict__ x,
                                                              double* __restrict__ y_loc, int pref_ahead) {
   constexpr int D = C::D, NS = C::NS, NF = C::NF, L = C::L, LF = C::LF, BS = C::BS, LTR = C::LTR, n = C::n;
@@ -301,7 +305,7 @@ __global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 || C::D == 3 ? 1 : 
   __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES];
   __shared__ Piece pieces[MAXP];
   __shared__ int npieces;
-  using S = SSm<C>;
+  using S = SSm<C, PART>;
   using TS = TSm<C>;
   double* ring = smem;
   double* W = smem + STAGES * ST_DBL;
@@ -346,7 +350,7 @@ __global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 || C::D == 3 ? 1 : 
     }
     for (int i = tid; i <= LF; i += nt) Ti[TS::fn_ptr + i] = g.fn_ptr[i];
     for (int i = tid; i < NSUB; i += nt) Ti[TS::gcls_of + i] = g.grad_cls_of[i];
-    if (PART != 2)
+    if (PART != 2 && D == 2)  // 3D reads its (larger) class tables through L1
       for (int i = tid; i < g.n_grad_cls * TS::CLS; i += nt) Gc[i] = g.grad_cls[i];
   }
   __syncthreads();
@@ -500,29 +504,61 @@ __global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 || C::D == 3 ? 1 : 
     // y1 = -A_uh x + A_uq z (needs rfst, the W_vol results, the W_face(z) stash);
     // leaves y1 in y and the face term g = A_hq z / scale in cfgz
     auto make_y1 = [&]() {
-      // cv[K][a][s] = sum_q sum_k gphys[K,q,a,k] w[K,q][k][s], gphys = grad_ref[K] inv_jac:
-      // gphys per gradient class once per macro (in z, dead by now, when it fits; else after the
-      // classes), then one dot per output
-      double* Gp = g.n_grad_cls * TS::CLS <= D * n ? z : Gc + g.n_grad_cls * TS::CLS;
-      for (int idx = tid; idx < g.n_grad_cls * TS::CLS; idx += NCONS) {
-        const int k = idx % D, base = idx - k;
-        double gp = 0.0;
+      // cv[K][a][s] = sum_q sum_k gphys[K,q,a,k] w[K,q][k][s], gphys = grad_ref[K] inv_jac
+      if constexpr (D == 3) {
+        // 3D: w'[q][r][s] = sum_k inv_jac[r][k] w[q][k][s] in place, then
+        // cv = sum_{q,r} G_cls[q][a][r] w'[q][r][s] with the class tables read through L1
+        constexpr int DN = D * NS;
+        for (int idx = tid; idx < C::NPV * NS; idx += NCONS) {
+          const int pt = idx / NS, s = idx - pt * NS;
+          double w[D];
 #pragma unroll
-        for (int r2 = 0; r2 < D; ++r2) gp += Gc[base + r2] * ij[r2][k];
-        Gp[idx] = gp;
-      }
-      cbar();
-      for (int idx = tid; idx < NSUB * NLOC * NS; idx += NCONS) {
-        const int s = idx % NS, a = (idx / NS) % NLOC, K = idx / (NS * NLOC);
-        const double* G = Gp + gco[K] * TS::CLS + a * D;
-        const double* w = wv + K * NQ * D * NS + s;
-        double a0 = 0.0, a1 = 0.0;
+          for (int k = 0; k < D; ++k) w[k] = wv[pt * DN + k * NS + s];
 #pragma unroll
-        for (int q = 0; q < NQ; ++q) {
+          for (int r = 0; r < D; ++r) {
+            double v = 0.0;
 #pragma unroll
-          for (int k = 0; k < D; ++k) ((q & 1) ? a1 : a0) += G[q * NLOC * D + k] * w[(q * D + k) * NS];
+            for (int k = 0; k < D; ++k) v += ij[r][k] * w[k];
+            wv[pt * DN + r * NS + s] = v;
+          }
         }
-        cv[idx] = a0 + a1;
+        cbar();
+        for (int idx = tid; idx < NSUB * NLOC * NS; idx += NCONS) {
+          const int s = idx % NS, a = (idx / NS) % NLOC, K = idx / (NS * NLOC);
+          const double* G = g.grad_cls + (size_t)gco[K] * TS::CLS + a * D;
+          const double* w = wv + K * NQ * DN + s;
+          double a0 = 0.0, a1 = 0.0;
+#pragma unroll 3
+          for (int q = 0; q < NQ; ++q) {
+#pragma unroll
+            for (int r = 0; r < D; ++r) ((q & 1) ? a1 : a0) += __ldg(G + q * NLOC * D + r) * w[(q * D + r) * NS];
+          }
+          cv[idx] = a0 + a1;
+        }
+      } else {
+        // gphys per gradient class once per macro (in z, dead by now, when it fits; else after the
+        // classes), then one dot per output
+        double* Gp = g.n_grad_cls * TS::CLS <= D * n ? z : Gc + g.n_grad_cls * TS::CLS;
+        for (int idx = tid; idx < g.n_grad_cls * TS::CLS; idx += NCONS) {
+          const int k = idx % D, base = idx - k;
+          double gp = 0.0;
+#pragma unroll
+          for (int r2 = 0; r2 < D; ++r2) gp += Gc[base + r2] * ij[r2][k];
+          Gp[idx] = gp;
+        }
+        cbar();
+        for (int idx = tid; idx < NSUB * NLOC * NS; idx += NCONS) {
+          const int s = idx % NS, a = (idx / NS) % NLOC, K = idx / (NS * NLOC);
+          const double* G = Gp + gco[K] * TS::CLS + a * D;
+          const double* w = wv + K * NQ * D * NS + s;
+          double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) {
+#pragma unroll
+            for (int k = 0; k < D; ++k) ((q & 1) ? a1 : a0) += G[q * NLOC * D + k] * w[(q * D + k) * NS];
+          }
+          cv[idx] = a0 + a1;
+        }
       }
       if (tid < LTR) {
         const int idx = tid, s = idx % NS, gg = (idx / NS) % LF, f = idx / BS;
@@ -1098,13 +1134,13 @@ static int count_pieces() {
   return k;
 }
 
-// ring stages per kernel: 2D runs two CTAs per SM with MHDG_STAGES each; the 3D
-// work area allows one CTA per SM only, which then gets a deeper ring
+// ring stages per kernel (all instantiations run two CTAs per SM; 3D keeps its
+// class tables in global memory and the parts' work areas apart to fit)
 #ifndef MHDG_STAGES_3D_PRE
-#define MHDG_STAGES_3D_PRE 5
+#define MHDG_STAGES_3D_PRE 3
 #endif
 #ifndef MHDG_STAGES_3D_POST
-#define MHDG_STAGES_3D_POST 7
+#define MHDG_STAGES_3D_POST 3
 #endif
 template <class C>
 __host__ __device__ constexpr int stages_of(int part) {
@@ -1127,8 +1163,8 @@ static bool stream_ok(const mhdg_disc& g, const mhdg_blocks& b, const mhdg_facto
                      ((C::NPF * C::NWF) % 2 == 0);
   const bool tables = g.n_grad_cls >= 1 && g.grad_cls && g.grad_cls_of && g.node_to_face && g.minv_d_face &&
                       g.n_face_nodes == C::NFN;
-  const size_t cls = (size_t)g.n_grad_cls * TSm<C>::CLS;
-  const size_t smem = sizeof(double) * ((size_t)stages_of<C>(0) * ST_DBL + SSm<C>::total + TSm<C>::total +
+  const size_t cls = C::D == 2 ? (size_t)g.n_grad_cls * TSm<C>::CLS : 0;
+  const size_t smem = sizeof(double) * ((size_t)stages_of<C>(0) * ST_DBL + SSm<C, 0>::total + TSm<C>::total +
                                         (cls <= (size_t)C::D * C::n ? cls : 2 * cls));
   return sizes && tables && (f.kind == 0 || (f.kind == 1 && f.work && g_split)) && smem <= 227 * 1024 &&
          al(b.face_state_trace) && al(b.face_trace_trace) &&
@@ -1137,8 +1173,9 @@ static bool stream_ok(const mhdg_disc& g, const mhdg_blocks& b, const mhdg_facto
 
 template <class C, int STAGES, int PART>
 static size_t stream_smem(const mhdg_disc& g) {
-  const size_t cls = (size_t)g.n_grad_cls * TSm<C>::CLS;  // classes (+ per-macro gphys unless it fits in z)
-  return sizeof(double) * ((size_t)STAGES * ST_DBL + SSm<C>::total + TSm<C>::total +
+  // 2D: class tables (+ per-macro gphys unless it fits in z) in shared memory; 3D: none
+  const size_t cls = C::D == 2 ? (size_t)g.n_grad_cls * TSm<C>::CLS : 0;
+  return sizeof(double) * ((size_t)STAGES * ST_DBL + SSm<C, PART>::total + TSm<C>::total +
                            (PART != 2 ? (cls <= (size_t)C::D * C::n ? cls : 2 * cls) : 0));
 }
 
