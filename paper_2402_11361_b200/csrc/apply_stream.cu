@@ -1142,9 +1142,13 @@ static int count_pieces() {
 #ifndef MHDG_STAGES_3D_POST
 #define MHDG_STAGES_3D_POST 3
 #endif
+#ifndef MHDG_STAGES_2D_POST
+#define MHDG_STAGES_2D_POST 5
+#endif
 template <class C>
 __host__ __device__ constexpr int stages_of(int part) {
-  return C::D == 2 ? MHDG_STAGES : (part == 2 ? MHDG_STAGES_3D_POST : (part == 1 ? MHDG_STAGES_3D_PRE : MHDG_STAGES));
+  return C::D == 2 ? (part == 2 ? MHDG_STAGES_2D_POST : MHDG_STAGES)
+                   : (part == 2 ? MHDG_STAGES_3D_POST : (part == 1 ? MHDG_STAGES_3D_PRE : MHDG_STAGES));
 }
 
 static int g_split = 1;
