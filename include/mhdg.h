@@ -175,6 +175,11 @@ int mhdg_timeline_end(double *ms, int *counts);
    place, 2 interchanges rows (the earlier kernel).  For A/B measurements. */
 void mhdg_set_factor_variant(int v);
 
+/* Batched LU kernel of the packed-LU factor kind: 4 (default) register
+   sub-panels + warp-chunked DMMA trailing updates, 3 the earlier kernel.
+   For A/B measurements. */
+void mhdg_set_lu_variant(int v);
+
 /* Schur-complement kernel: 0 (default) FP64 tensor cores (DMMA), otherwise the
    per-macro FFMA kernel.  For A/B measurements. */
 void mhdg_set_schur_variant(int v);

@@ -23,6 +23,7 @@ int inv_factor(int n, int n_mac, double* scratch, double* tiled, int* status, cu
 int inv_factor2(int n, int n_mac, double* scratch, int* piv, double* tiled, int* status, cudaStream_t st);
 int inv_factor3(int n, int n_mac, double* scratch, int* piv, double* tiled, int* status, cudaStream_t st);
 int lu_factor3(int n, int n_mac, double* scratch, int* piv, double* packed, int* status, cudaStream_t st);
+int lu_factor4(int n, int n_mac, double* scratch, int* piv, double* packed, int* status, cudaStream_t st);
 extern int g_schur_variant;
 int icgs(int n, int j, const double* V, long long ldv, double* w, double* out, double* scratch, cudaStream_t st);
 long long icgs_scratch_size(int n);
@@ -169,12 +170,15 @@ int mhdg_schur_matrix(const mhdg_disc* g, const mhdg_blocks* b, const mhdg_facto
 
 static int g_factor_variant = 3;
 void mhdg_set_factor_variant(int v) { g_factor_variant = v; }
+static int g_lu_variant = 4;
+void mhdg_set_lu_variant(int v) { g_lu_variant = v; }
 void mhdg_set_schur_variant(int v) { mhdg::g_schur_variant = v; }
 
 int mhdg_lu_factor(const mhdg_disc* g, const mhdg_factors* f, int* status, void* st) {
   const int n = g->L * g->ns;
-  if (f->kind == 1) {  // packed LU (k_lu3)
-    const int rc1 = lu_factor3(n, g->n_mac, f->scratch, f->perm, f->lu, status, S(st));
+  if (f->kind == 1) {  // packed LU (k_lu4; k_lu3 behind mhdg_set_lu_variant(3))
+    const int rc1 = g_lu_variant == 3 ? lu_factor3(n, g->n_mac, f->scratch, f->perm, f->lu, status, S(st))
+                                      : lu_factor4(n, g->n_mac, f->scratch, f->perm, f->lu, status, S(st));
     return rc1 < 0 ? MHDG_ERR_CONFIG : rc1;
   }
   // DMMA panel-64 Gauss-Jordan when its panel fits shared memory (without row interchanges

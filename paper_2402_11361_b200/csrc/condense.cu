@@ -13,6 +13,7 @@
 //              MHDG_FACTOR=lu option.
 // FactorizationError on an exactly zero pivot.
 #include "common.cuh"
+#include "dmma.cuh"
 #include "local_ops.cuh"
 #include "packed_lu.cuh"
 #include "tiled_inv.cuh"
@@ -383,11 +384,6 @@ extern "C" int mhdg_gj_profile(unsigned long long* out, int reset) {
 #define GJADD(k, v)
 #endif
 
-__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
-               : "+d"(d0), "+d"(d1)
-               : "d"(a), "d"(b));
-}
 
 size_t gj2_smem_bytes(int n) {
   return sizeof(double) * ((size_t)n * GJ2_PW + GJ2_NB * GJ2_BS + 32 + 8) + sizeof(int) * (32 + 8) + 64;
@@ -1672,6 +1668,16 @@ __global__ void __launch_bounds__(256) k_pack_lu3(int n, const double* __restric
 #define MHDG_LU_NT 256
 #endif
 
+// in-place LU (pivot rows in place) -> packed solve layout
+int pack_lu(int n, int n_mac, const double* scratch, const int* piv, double* packed, cudaStream_t st) {
+  const size_t pbytes = sizeof(double) * 2 * PLU_NB * (PLU_NB + 1) + sizeof(int) * n;
+  cudaFuncSetAttribute(k_pack_lu3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pbytes);
+  tl_begin(TL_PACK, st);
+  k_pack_lu3<<<n_mac, 256, pbytes, st>>>(n, scratch, piv, packed);
+  tl_end(TL_PACK, st);
+  return launch_ok();
+}
+
 int lu_factor3(int n, int n_mac, double* scratch, int* piv, double* packed, int* status, cudaStream_t st) {
   using L3 = Lu3<MHDG_LU_NB, MHDG_LU_NT>;
   const size_t bytes = L3::smem_bytes(n);
@@ -1683,12 +1689,7 @@ int lu_factor3(int n, int n_mac, double* scratch, int* piv, double* packed, int*
   tl_end(TL_FACTOR, st);
   int rc = launch_ok();
   if (rc) return rc;
-  const size_t pbytes = sizeof(double) * 2 * PLU_NB * (PLU_NB + 1) + sizeof(int) * n;
-  cudaFuncSetAttribute(k_pack_lu3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pbytes);
-  tl_begin(TL_PACK, st);
-  k_pack_lu3<<<n_mac, 256, pbytes, st>>>(n, scratch, piv, packed);
-  tl_end(TL_PACK, st);
-  return launch_ok();
+  return pack_lu(n, n_mac, scratch, piv, packed, st);
 }
 
 int inv_factor(int n, int n_mac, double* scratch, double* tiled, int* status, cudaStream_t st) {

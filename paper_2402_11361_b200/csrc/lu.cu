@@ -1,0 +1,479 @@
+// Batched LU with partial pivoting of the condensed local systems S
+// (the factorisation the paper's Remark asks for; the
+// reference's np.linalg.inv at condense.py:62-70 is getrf + getri, and the
+// canonical F_cond of SURVEY 8d counts this getrf part, (2/3) n^3).
+//
+// k_lu4: one CTA per macro, two CTAs per SM so one macro's pivot chain runs
+// under the other's tensor-core updates.  Right-looking, 32-column panels:
+//   * the panel (all not-yet-pivoted rows x 32 columns) sits in shared memory
+//     (XOR-swizzled rows, conflict-free both row-per-thread and as DMMA
+//     A fragments);
+//   * it is factored in 16-column sub-panels held in registers, one row per
+//     thread: a pivot step is one warp argmax (value and row packed into one
+//     64-bit key), one CTA barrier, and register-only row updates; each
+//     warp's candidate row is published with its key, so no second barrier
+//     is needed to broadcast the pivot row;
+//   * between the two sub-panels: a 16-step triangular solve for the pivot
+//     rows and a DMMA rank-16 update of the other rows;
+//   * trailing update, one 16-column chunk per warp, no CTA barrier:
+//     U12 = inv(L11) A12 on DMMA (inv(L11) formed once per panel), U12
+//     turned into B fragments with shuffles, then C -= L21 U12 over all
+//     remaining rows with C read-modified-written in global memory (L2).
+// Pivots stay in place (logical row k = physical row piv[k]; rows are never
+// moved), the output contract of k_lu3: k_pack_lu3 packs it for the apply.
+// FactorizationError on an exactly zero pivot (scipy's lu_factor / LAPACK
+// getrf report singular U).
+#include "common.cuh"
+#include "dmma.cuh"
+#include "packed_lu.cuh"
+
+namespace mhdg {
+
+#ifdef MHDG_STREAM_PROFILE
+__device__ unsigned long long g_lu4prof[8];
+#define LUT(v) long long v = clock64()
+#define LUADD(k, v) if (threadIdx.x == 0) atomicAdd(&g_lu4prof[k], (unsigned long long)(clock64() - (v)))
+extern "C" int mhdg_lu4_profile(unsigned long long* out, int reset) {
+  if (out) cudaMemcpyFromSymbol(out, g_lu4prof, sizeof(g_lu4prof));
+  if (reset) {
+    unsigned long long z[8] = {};
+    cudaMemcpyToSymbol(g_lu4prof, z, sizeof(z));
+  }
+  return 0;
+}
+#else
+#define LUT(v)
+#define LUADD(k, v)
+#endif
+
+// 8-byte global -> shared async copy (src_bytes = 0 zero-fills)
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, int src_bytes) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+namespace lu4 {
+constexpr int NB = 32;       // panel width
+constexpr int SW = 16;       // register sub-panel width
+constexpr int PS = 36;       // panel row stride (= 4 mod 16): conflict-free DMMA A fragments
+constexpr int CW = 16;       // trailing-update column chunk per warp
+constexpr int SWP = SW + 2;  // candidate slot: SW row values, the reciprocal, padding
+
+// argmax key: |v| with the low 9 mantissa bits replaced by (511 - row), so the
+// largest key is the largest magnitude, ties (to 2^-43) going to the lowest row
+__device__ __forceinline__ unsigned long long pkey(double v, int r) {
+  return ((unsigned long long)__double_as_longlong(fabs(v)) & ~0x1FFull) | (unsigned long long)(511 - r);
+}
+__device__ __forceinline__ int key_row(unsigned long long k) { return 511 - (int)(k & 0x1FFull); }
+
+template <int NT>
+size_t smem_bytes(int n) {
+  constexpr int NW = NT / 32;
+  return sizeof(double) * ((size_t)n * PS + 2 * NW * SWP) + sizeof(unsigned long long) * 2 * NW +
+         sizeof(unsigned short) * 2 * (size_t)n + (size_t)n;
+}
+}  // namespace lu4
+
+// C -= L21 U12 for one 16-column chunk over the m remaining rows (list rl), 16 rows per
+// pass with the next three passes' C in flight.  VEC: 16-byte C accesses (full chunk, even n).
+template <bool VEC>
+__device__ __forceinline__ void trail_pass_loop(double* __restrict__ A, int n, int c0, int cw, int m,
+                                                const unsigned short* rl, const double* P, int t4, int g,
+                                                const double (&bf)[lu4::NB / 4][2]) {
+  using namespace lu4;
+  const int rlast = rl[m - 1];
+  auto load = [&](int t, double (&c)[2][2][2], int (&rr)[2], bool (&ok)[2]) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      ok[h] = t + 8 * h + g < m;
+      rr[h] = ok[h] ? rl[t + 8 * h + g] : rlast;
+      const double* src = A + (size_t)rr[h] * n + c0 + 2 * t4;
+#pragma unroll
+      for (int ct = 0; ct < 2; ++ct) {
+        if (VEC) {
+          const double2 v = ok[h] ? *reinterpret_cast<const double2*>(src + 8 * ct) : make_double2(0.0, 0.0);
+          c[h][ct][0] = v.x;
+          c[h][ct][1] = v.y;
+        } else {
+#pragma unroll
+          for (int e = 0; e < 2; ++e) c[h][ct][e] = (ok[h] && 8 * ct + 2 * t4 + e < cw) ? src[8 * ct + e] : 0.0;
+        }
+      }
+    }
+  };
+  auto pass = [&](double (&c)[2][2][2], const int (&rr)[2], const bool (&ok)[2]) {
+    const double* pa0 = P + rr[0] * PS + t4;
+    const double* pa1 = P + rr[1] * PS + t4;
+#pragma unroll
+    for (int ks = 0; ks < NB / 4; ++ks) {
+      const double a0 = pa0[4 * ks], a1 = pa1[4 * ks];
+#pragma unroll
+      for (int ct = 0; ct < 2; ++ct) {
+        dmma_8x8x4(c[0][ct][0], c[0][ct][1], a0, bf[ks][ct]);
+        dmma_8x8x4(c[1][ct][0], c[1][ct][1], a1, bf[ks][ct]);
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      if (ok[h]) {
+        double* dst = A + (size_t)rr[h] * n + c0 + 2 * t4;
+#pragma unroll
+        for (int ct = 0; ct < 2; ++ct) {
+          if (VEC) {
+            *reinterpret_cast<double2*>(dst + 8 * ct) = make_double2(c[h][ct][0], c[h][ct][1]);
+          } else {
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+              if (8 * ct + 2 * t4 + e < cw) dst[8 * ct + e] = c[h][ct][e];
+          }
+        }
+      }
+  };
+  // four register stages: C of the next three passes is in flight during a pass
+  double s0[2][2][2], s1[2][2][2], s2[2][2][2], s3[2][2][2];
+  int r0[2], r1[2], r2[2], r3[2];
+  bool o0[2], o1[2], o2[2], o3[2];
+  load(0, s0, r0, o0);
+  load(16, s1, r1, o1);
+  load(32, s2, r2, o2);
+  for (int t = 0; t < m; t += 64) {
+    load(t + 48, s3, r3, o3);
+    pass(s0, r0, o0);
+    if (t + 16 >= m) break;
+    load(t + 64, s0, r0, o0);
+    pass(s1, r1, o1);
+    if (t + 32 >= m) break;
+    load(t + 80, s1, r1, o1);
+    pass(s2, r2, o2);
+    if (t + 48 >= m) break;
+    load(t + 96, s2, r2, o2);
+    pass(s3, r3, o3);
+  }
+}
+
+template <int NT, int RPT>
+__global__ void __launch_bounds__(NT, 2) k_lu4(int n, double* __restrict__ S, int* __restrict__ piv_out,
+                                               int* status) {
+  using namespace lu4;
+  constexpr int NW = NT / 32;
+  extern __shared__ double sm[];
+  double* P = sm;                                   // n x PS: the panel, physical rows
+  double* cv = P + (size_t)n * PS;                  // [2][NW][SWP] candidate pivot rows
+  unsigned long long* ck = reinterpret_cast<unsigned long long*>(cv + 2 * NW * SWP);  // [2][NW] their keys
+  unsigned short* npl = reinterpret_cast<unsigned short*>(ck + 2 * NW);  // [2][n] not-yet-pivoted rows
+  unsigned char* rflag = reinterpret_cast<unsigned char*>(npl + 2 * n);   // n: 1 = pivot row
+  __shared__ int pv[NB];                            // this panel's pivot rows, logical order
+  __shared__ int wcnt[NW];
+  const int mac = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  double* A = S + (size_t)mac * n * n;
+  int* pivg = piv_out + (size_t)mac * n;
+  bool singular = false;
+  for (int i = tid; i < n; i += NT) {
+    npl[i] = (unsigned short)i;
+    rflag[i] = 0;
+  }
+  int m = n, lb = 0;
+  __syncthreads();
+
+  for (int k0 = 0; k0 < n; k0 += NB) {
+    const int nb = min(NB, n - k0);
+    const unsigned short* np = npl + lb * n;
+    LUT(pt0);
+    // ---- panel: the m not-yet-pivoted rows, columns k0 .. k0+nb-1 (zero beyond) ----
+    for (int i = warp; i < m; i += NW) {
+      const int r = np[i];
+      cp_async8(P + r * PS + lane, A + (size_t)r * n + k0 + (lane < nb ? lane : 0), lane < nb ? 8 : 0);
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    LUADD(0, pt0);
+
+    for (int js = 0; js < nb; js += SW) {
+      LUT(pt1);
+      double x[RPT][SW];
+      bool act[RPT], act0[RPT];
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) {
+        const int r = tid + NT * i;
+        act[i] = r < n && !rflag[r];
+        act0[i] = act[i];
+#pragma unroll
+        for (int c = 0; c < SW; ++c) x[i][c] = act[i] ? P[r * PS + js + c] : 0.0;
+      }
+#pragma unroll
+      for (int jj = 0; jj < SW; ++jj) {
+        const int j = js + jj;
+        if (j >= nb) break;
+        // this thread's best row for column j, and its reciprocal (speculative: only the
+        // winner's is used; formed here, off the post-barrier path)
+        unsigned long long key = 0;
+        double xv = 0.0;
+#pragma unroll
+        for (int i = 0; i < RPT; ++i)
+          if (act[i]) {
+            const unsigned long long kk = pkey(x[i][jj], tid + NT * i);
+            if (kk > key) {
+              key = kk;
+              xv = x[i][jj];
+            }
+          }
+        const double rcp = 1.0 / xv;
+        // warp argmax of the 64-bit key: max of the high words, then of the low words among ties
+        const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+        const unsigned mh = __reduce_max_sync(MHDG_FULL, hi);
+        const unsigned tie = __ballot_sync(MHDG_FULL, hi == mh);
+        unsigned ml = 0;
+        if (hi == mh) ml = __reduce_max_sync(tie, lo);
+        const int par = j & 1;
+        const unsigned win = __ballot_sync(MHDG_FULL, hi == mh && lo == ml);
+        if (hi == mh && lo == ml) {  // this lane holds the warp's candidate (or none: key 0)
+          double* slot = cv + (par * NW + warp) * SWP;
+#pragma unroll
+          for (int i = 0; i < RPT; ++i)
+            if (act[i] && key_row(key) == tid + NT * i) {
+#pragma unroll
+              for (int c = jj; c < SW; ++c) slot[c] = x[i][c];
+            }
+          slot[SW] = rcp;
+          if (lane == __ffs(win) - 1) ck[par * NW + warp] = key;
+        }
+        __syncthreads();
+        // CTA argmax over the warps' keys (broadcast loads); the pivot row's warp follows from
+        // its index (row r belongs to thread r mod NT)
+        unsigned long long best = 0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+          const unsigned long long kk = ck[par * NW + w];
+          best = kk > best ? kk : best;
+        }
+        const int p = key_row(best);
+        const double* prow = cv + (par * NW + (p % NT) / 32) * SWP;
+        const double pd = prow[jj];
+        if (pd == 0.0) singular = true;
+        const double d = pd == 0.0 ? 0.0 : prow[SW];
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+          if (!act[i]) continue;
+          if (tid + NT * i == p) {
+            act[i] = false;  // the pivot row keeps its values: L left of jj, U from jj on
+            continue;
+          }
+          const double l = x[i][jj] * d;
+          x[i][jj] = l;
+#pragma unroll
+          for (int c = jj + 1; c < SW; ++c) x[i][c] -= l * prow[c];
+        }
+        if (tid == 0) {
+          pv[j] = p;
+          pivg[k0 + j] = p;
+          rflag[p] = 1;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < RPT; ++i)
+        if (act0[i]) {
+          const int r = tid + NT * i;
+#pragma unroll
+          for (int c = 0; c < SW; ++c) P[r * PS + js + c] = x[i][c];
+        }
+      __syncthreads();
+      LUADD(1, pt1);
+      LUT(pt2);
+      if (js + SW < nb) {
+        // (a) U rows of this sub-panel's pivots on the panel's remaining columns
+        if (warp == 0 && lane < nb - js - SW) {
+          const int c = js + SW + lane;
+          double u[SW];
+#pragma unroll
+          for (int jj = 0; jj < SW; ++jj) {
+            const double* pr = P + pv[js + jj] * PS;
+            double v = pr[c];
+#pragma unroll
+            for (int i = 0; i < jj; ++i) v -= pr[js + i] * u[i];
+            u[jj] = v;
+            P[pv[js + jj] * PS + c] = v;
+          }
+        }
+        __syncthreads();
+        // (b) rank-SW DMMA update of the other rows on columns js+SW .. NB-1
+        {
+          double bf[SW / 4][2];
+#pragma unroll
+          for (int ks = 0; ks < SW / 4; ++ks)
+#pragma unroll
+            for (int ct = 0; ct < 2; ++ct) bf[ks][ct] = -P[pv[js + 4 * ks + t4] * PS + js + SW + 8 * ct + g];
+          for (int t = warp * 8; t < m; t += NW * 8) {
+            const bool ok = t + g < m;
+            const int r = np[ok ? t + g : 0];
+            const bool st = ok && !rflag[r];
+            double* pr = P + r * PS;
+            double c[2][2];
+#pragma unroll
+            for (int ct = 0; ct < 2; ++ct)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) c[ct][e] = pr[js + SW + 8 * ct + 2 * t4 + e];
+#pragma unroll
+            for (int ks = 0; ks < SW / 4; ++ks) {
+              const double a = pr[js + 4 * ks + t4];
+#pragma unroll
+              for (int ct = 0; ct < 2; ++ct) dmma_8x8x4(c[ct][0], c[ct][1], a, bf[ks][ct]);
+            }
+            if (st) {
+#pragma unroll
+              for (int ct = 0; ct < 2; ++ct)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) pr[js + SW + 8 * ct + 2 * t4 + e] = c[ct][e];
+            }
+          }
+        }
+        __syncthreads();
+      }
+      LUADD(2, pt2);
+    }
+
+    LUT(pt3);
+    // ---- write the factored panel back; list of the rows still unpivoted; inv(L11) ----
+#pragma unroll 4
+    for (int i = warp; i < m; i += NW) {
+      const int r = np[i];
+      if (lane < nb) A[(size_t)r * n + k0 + lane] = P[r * PS + lane];
+    }
+    unsigned short* np2 = npl + (lb ^ 1) * n;
+    {
+      int done_cnt = 0;
+      for (int base = 0; base < m; base += NT) {
+        const int i = base + tid;
+        const bool keep = i < m && !rflag[np[i]];
+        const unsigned bal = __ballot_sync(MHDG_FULL, keep);
+        if (lane == 0) wcnt[warp] = __popc(bal);
+        __syncthreads();
+        int off = done_cnt, tot = 0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+          const int cw = wcnt[w];
+          off += w < warp ? cw : 0;
+          tot += cw;
+        }
+        if (keep) np2[off + __popc(bal & ((1u << lane) - 1u))] = np[i];
+        done_cnt += tot;
+        __syncthreads();
+      }
+    }
+    {
+      // inv(L11): warp w forms columns w, w + NW, ... (lane = row), then, once every warp
+      // has read L11, stores them over the pivot rows of the panel (already written back)
+      constexpr int CPW = (NB + NW - 1) / NW;
+      double xc[CPW];
+#pragma unroll
+      for (int cc = 0; cc < CPW; ++cc) xc[cc] = (lane == warp + NW * cc && lane < nb) ? 1.0 : 0.0;
+      const int prl = lane < nb ? pv[lane] : 0;
+      for (int k = 0; k < nb - 1; ++k) {
+        const double lik = (lane > k && lane < nb) ? P[prl * PS + k] : 0.0;
+#pragma unroll
+        for (int cc = 0; cc < CPW; ++cc) xc[cc] -= lik * __shfl_sync(MHDG_FULL, xc[cc], k);
+      }
+      __syncthreads();
+      if (lane < nb) {
+#pragma unroll
+        for (int cc = 0; cc < CPW; ++cc)
+          if (warp + NW * cc < NB) P[prl * PS + warp + NW * cc] = xc[cc];
+      }
+    }
+    m -= nb;
+    lb ^= 1;
+    __syncthreads();
+    LUADD(3, pt3);
+    LUT(pt4);
+
+    // ---- trailing update, one CW-column chunk per warp (no CTA barrier) ----
+    const int ct0 = k0 + nb;
+    const int nchunks = (n - ct0 + CW - 1) / CW;
+    const double* Lirow[NB / 8];  // inv(L11) row 8 rt + g lives in pivot row pv[8 rt + g]
+#pragma unroll
+    for (int rt = 0; rt < NB / 8; ++rt) Lirow[rt] = P + pv[8 * rt + g] * PS + t4;
+    for (int q = warp; q < nchunks; q += NW) {
+      const int c0 = ct0 + q * CW, cw = min(CW, n - c0);
+      // U12 chunk = inv(L11) A12 (A12 = this panel's pivot rows; nb = NB whenever columns remain)
+      double u[NB / 8][2][2];
+#pragma unroll
+      for (int rt = 0; rt < NB / 8; ++rt)
+#pragma unroll
+        for (int ct = 0; ct < 2; ++ct) u[rt][ct][0] = u[rt][ct][1] = 0.0;
+      {
+        double b[NB / 4][2];
+#pragma unroll
+        for (int ks = 0; ks < NB / 4; ++ks) {
+          const double* src = A + (size_t)pv[4 * ks + t4] * n + c0;
+#pragma unroll
+          for (int ct = 0; ct < 2; ++ct) b[ks][ct] = 8 * ct + g < cw ? src[8 * ct + g] : 0.0;
+        }
+#pragma unroll
+        for (int ks = 0; ks < NB / 4; ++ks)
+#pragma unroll
+          for (int rt = 0; rt < NB / 8; ++rt) {
+            const double a = Lirow[rt][4 * ks];
+#pragma unroll
+            for (int ct = 0; ct < 2; ++ct) dmma_8x8x4(u[rt][ct][0], u[rt][ct][1], a, b[ks][ct]);
+          }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int rt = 0; rt < NB / 8; ++rt) {
+        double* dst = A + (size_t)pv[8 * rt + g] * n + c0;
+#pragma unroll
+        for (int ct = 0; ct < 2; ++ct)
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+            if (8 * ct + 2 * t4 + e < cw) dst[8 * ct + 2 * t4 + e] = u[rt][ct][e];
+      }
+      // -U12 as B fragments: bf[ks][ct] = -U[4 ks + t4][8 ct + g]
+      double bf[NB / 4][2];
+      {
+        const int src_hi = g >> 1;
+#pragma unroll
+        for (int ks = 0; ks < NB / 4; ++ks) {
+          const int src = (4 * (ks & 1) + t4) * 4 + src_hi;
+#pragma unroll
+          for (int ct = 0; ct < 2; ++ct) {
+            const double v0 = __shfl_sync(MHDG_FULL, u[ks >> 1][ct][0], src);
+            const double v1 = __shfl_sync(MHDG_FULL, u[ks >> 1][ct][1], src);
+            bf[ks][ct] = -((g & 1) ? v1 : v0);
+          }
+        }
+      }
+      // C -= L21 U12 over the remaining rows, 16 rows per pass, next pass's C prefetched
+      if (m > 0) {
+        if (cw == CW && (n & 1) == 0)
+          trail_pass_loop<true>(A, n, c0, cw, m, np2, P, t4, g, bf);
+        else
+          trail_pass_loop<false>(A, n, c0, cw, m, np2, P, t4, g, bf);
+      }
+    }
+    LUADD(4, pt4);
+    LUT(pt5);
+    __syncthreads();
+    LUADD(5, pt5);
+  }
+  if (singular && tid == 0) set_status(status, MHDG_ERR_FACTORIZATION, mac, 0, 0.0);
+}
+
+int pack_lu(int n, int n_mac, const double* scratch, const int* piv, double* packed, cudaStream_t st);
+
+int lu_factor4(int n, int n_mac, double* scratch, int* piv, double* packed, int* status, cudaStream_t st) {
+  constexpr int NT = 192;
+  if (n > 2 * NT) return -1;
+  const size_t bytes = lu4::smem_bytes<NT>(n);
+  if (bytes > 227 * 1024) return -1;
+  auto kern = n <= NT ? k_lu4<NT, 1> : k_lu4<NT, 2>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  tl_begin(TL_FACTOR, st);
+  kern<<<n_mac, NT, bytes, st>>>(n, scratch, piv, status);
+  tl_end(TL_FACTOR, st);
+  int rc = launch_ok();
+  if (rc) return rc;
+  return pack_lu(n, n_mac, scratch, piv, packed, st);
+}
+
+}  // namespace mhdg

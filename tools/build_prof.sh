@@ -1,12 +1,16 @@
 #!/bin/sh
-# Builds tools/prof/libmhdg_prof.so: libmhdg with the streamed-apply cycle
-# counters (-DMHDG_STREAM_PROFILE) and GJ phase counters, for tools/*_profile.py.
+# Builds tools/prof/libmhdg_prof.so: libmhdg with cycle counters
+# (-DMHDG_STREAM_PROFILE: streamed-apply, GJ and LU phase counters) compiled into
+# the sources listed in $PROF (default: all), for tools/*_profile.py.
 set -e
 cd "$(dirname "$0")/../paper_2402_11361_b200/csrc"
 mkdir -p ../../tools/prof/build
-for s in capi apply apply_stream condense precond assemble krylov; do
+PROF=${PROF:-"capi apply apply_stream condense lu precond assemble krylov"}
+for s in capi apply apply_stream condense lu precond assemble krylov; do
+  D=""
+  case " $PROF " in *" $s "*) D="-DMHDG_STREAM_PROFILE -DMHDG_GJ_PROFILE" ;; esac
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC \
-    --expt-relaxed-constexpr -DMHDG_STREAM_PROFILE -DMHDG_GJ_PROFILE -c $s.cu -o ../../tools/prof/build/$s.o &
+    --expt-relaxed-constexpr $D -c $s.cu -o ../../tools/prof/build/$s.o &
 done
 wait
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o ../../tools/prof/libmhdg_prof.so ../../tools/prof/build/*.o -lcudart
