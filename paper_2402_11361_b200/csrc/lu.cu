@@ -459,7 +459,136 @@ __global__ void __launch_bounds__(NT, 2) k_lu4(int n, double* __restrict__ S, in
   if (singular && tid == 0) set_status(status, MHDG_ERR_FACTORIZATION, mac, 0, 0.0);
 }
 
-int pack_lu(int n, int n_mac, const double* scratch, const int* piv, double* packed, cudaStream_t st);
+// --------------------------------------------------------------------------
+// k_pack_lu4: in-place LU (pivot rows in place) -> the packed solve layout of
+// packed_lu.cuh.  One CTA per macro, per 64-row block:
+//   * panels: one warp per logical row, lane = column, so every 32-column tile
+//     row is one coalesced read of the row's physical copy and one coalesced
+//     write;
+//   * diagonal block: staged in shared memory, inv(L_bb) (unit lower) and
+//     inv(U_bb) = inv(unit upper) D^-1 by column sweeps over all threads with
+//     the columns in registers (one barrier per step), written as packed
+//     triangles.
+// --------------------------------------------------------------------------
+namespace pk4 {
+constexpr int NT = 256, TS = PLU_NB + 1, MAXSEG = 12;  // n <= 32 MAXSEG
+}
+
+// Column sweep for the inverse of a unit triangular nb x nb block (nb <= 64) held in
+// T (LOWER: strict lower part; else Uh[i][k] = T[i][k] rd[i], strict upper part).
+// Thread (c, grp) keeps rows grp, grp + NG, ... of column c of X in registers; the
+// final row k is broadcast through xr (double-buffered: one barrier per step).
+template <bool LOWER>
+__device__ __forceinline__ void tri_sweep(const double* T, const double* rd, int nb, int c, int grp, double* xr,
+                                          double (&x)[PLU_NB / (pk4::NT / PLU_NB)]) {
+  using namespace pk4;
+  constexpr int NG = NT / PLU_NB, R = PLU_NB / NG;
+#pragma unroll
+  for (int s = 0; s < R; ++s) x[s] = grp + NG * s == c ? 1.0 : 0.0;
+#pragma unroll
+  for (int kk = 0; kk < PLU_NB; ++kk) {
+    const int k = LOWER ? kk : PLU_NB - 1 - kk;
+    if (k >= nb) continue;  // uniform
+    double* row = xr + (kk & 1) * PLU_NB;
+    if (grp == (k % NG)) row[c] = x[k / NG];
+    __syncthreads();
+    const double xk = row[c];
+    if (LOWER ? c <= k : c >= k) {
+#pragma unroll
+      for (int s = 0; s < R; ++s) {
+        const int i = grp + NG * s;
+        if (LOWER ? (i > k && i < nb) : (i < k)) x[s] -= (LOWER ? T[i * TS + k] : T[i * TS + k] * rd[i]) * xk;
+      }
+    }
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(pk4::NT, 3) k_pack_lu4(int n, const double* __restrict__ F,
+                                                      const int* __restrict__ piv, double* __restrict__ out) {
+  using namespace pk4;
+  extern __shared__ double pk_sm[];
+  double* T = pk_sm;                    // PLU_NB x TS: diagonal block (logical rows)
+  double* rd = T + PLU_NB * TS;         // PLU_NB: 1 / U[k][k]
+  double* xr = rd + PLU_NB;             // [2][PLU_NB]: row k of X, broadcast per sweep step
+  int* pr = reinterpret_cast<int*>(xr + 2 * PLU_NB);
+  const int mac = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double* A = F + (size_t)mac * n * n;
+  double* O = out + (size_t)mac * plu_size(n);
+  for (int i = tid; i < n; i += NT) pr[i] = piv[(size_t)mac * n + i];
+  __syncthreads();
+  const int nblk = plu_nblk(n);
+  const int c = tid & (PLU_NB - 1), grp = tid / PLU_NB;  // column and row group of the sweeps
+  constexpr int NG = NT / PLU_NB;
+  for (int b = 0; b < nblk; ++b) {
+    const PluOffsets o = plu_offsets(n, b);
+    const int nb = o.nb, r0 = o.r0;
+    // panels and the diagonal block, row by row: the whole physical row is read in
+    // 32-column segments (all loads in flight), each segment then goes to its piece
+    for (int r = warp; r < nb; r += NT / 32) {
+      const double* src = A + (size_t)pr[r0 + r] * n;
+      double v[MAXSEG];
+#pragma unroll
+      for (int j = 0; j < MAXSEG; ++j) v[j] = 32 * j + lane < n ? src[32 * j + lane] : 0.0;
+#pragma unroll
+      for (int j = 0; j < MAXSEG; ++j) {
+        const int col = 32 * j;
+        if (col >= n) break;
+        if (col < r0) {
+          O[o.fwd_panel + (long long)col * nb + (long long)r * PLU_TW + lane] = v[j];
+        } else if (col < r0 + nb) {
+          if (col + lane < r0 + nb) T[r * TS + col - r0 + lane] = v[j];
+        } else {
+          const int w = min(PLU_TW, n - col);
+          if (lane < w) O[o.bwd_panel + (long long)(col - r0 - nb) * nb + (long long)r * w + lane] = v[j];
+        }
+      }
+    }
+    __syncthreads();
+    if (tid < nb) rd[tid] = 1.0 / T[tid * TS + tid];
+    __syncthreads();
+    double x[PLU_NB / NG];  // X[grp + NG s][c]
+    // inv(L_bb): X = I; X[i][c] -= L[i][k] X[k][c] for i > k, c <= k, k ascending
+    tri_sweep<true>(T, rd, nb, c, grp, xr, x);
+    if (c < nb) {
+#pragma unroll
+      for (int s2 = 0; s2 < PLU_NB / NG; ++s2) {
+        const int i = grp + NG * s2;
+        if (i < nb && c < i) O[o.fwd_diag + plu_lo(i, c)] = x[s2];
+      }
+    }
+    // inv(U_bb) = inv(Uh) D^-1, Uh = D^-1 U unit upper: X[i][c] -= Uh[i][k] X[k][c] for
+    // i < k <= c, k descending
+    tri_sweep<false>(T, rd, nb, c, grp, xr, x);
+    if (c < nb) {
+#pragma unroll
+      for (int s2 = 0; s2 < PLU_NB / NG; ++s2) {
+        const int i = grp + NG * s2;
+        if (i <= c) O[o.bwd_diag + plu_up(nb, i, c)] = x[s2] * rd[c];
+      }
+    }
+    if (tid == 0) {  // zero the even-size padding of the last (narrow) tiles and triangles
+      if ((nb * (nb - 1) / 2) & 1) O[o.fwd_diag + nb * (nb - 1) / 2] = 0.0;
+      if ((nb * (nb + 1) / 2) & 1) O[o.bwd_diag + nb * (nb + 1) / 2] = 0.0;
+      const int wf = o.ncol_fwd % PLU_TW, wb = o.ncol_bwd % PLU_TW;
+      if ((nb * wf) & 1) O[o.fwd_diag - 1] = 0.0;
+      if ((nb * wb) & 1) O[o.bwd_diag - 1] = 0.0;
+    }
+    __syncthreads();
+  }
+}
+
+static int pack_lu4(int n, int n_mac, const double* scratch, const int* piv, double* packed, cudaStream_t st) {
+  if (n > 32 * pk4::MAXSEG) return -1;
+  const size_t bytes = sizeof(double) * (PLU_NB * pk4::TS + 3 * PLU_NB) + sizeof(int) * n;
+  cudaFuncSetAttribute(k_pack_lu4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  tl_begin(TL_PACK, st);
+  k_pack_lu4<<<n_mac, pk4::NT, bytes, st>>>(n, scratch, piv, packed);
+  tl_end(TL_PACK, st);
+  return launch_ok();
+}
+
+
 
 int lu_factor4(int n, int n_mac, double* scratch, int* piv, double* packed, int* status, cudaStream_t st) {
   constexpr int NT = 192;
@@ -473,7 +602,7 @@ int lu_factor4(int n, int n_mac, double* scratch, int* piv, double* packed, int*
   tl_end(TL_FACTOR, st);
   int rc = launch_ok();
   if (rc) return rc;
-  return pack_lu(n, n_mac, scratch, piv, packed, st);
+  return pack_lu4(n, n_mac, scratch, piv, packed, st);
 }
 
 }  // namespace mhdg
