@@ -107,12 +107,14 @@ def apply_kernel_bytes(disc):
 
 def condense_executed_flops_per_macro(disc):
     """Flops the condensation kernels execute per macro: the Schur GEMMs on the
-    tensor cores (k_schur_mma) and the explicit Gauss-Jordan inverse (2 n^3)."""
+    tensor cores (k_schur_mma) and the factorization: batched LU ((2/3) n^3,
+    the default factor kind) or the explicit Gauss-Jordan inverse (2 n^3)."""
+    from paper_2402_11361_b200 import condense as CD
     d, ns, nf, L = disc.dim, disc.ns, disc.nf, disc.L
     rm = disc.rm
     schur = 2 * (rm.n_loc * ns * ns) * (rm.n_quad * d) * L * rm.n_sub
     schur += 2 * (rm.n_loc_face * ns * ns) * (rm.n_quad_face * d) * L * nf * rm.n_tri
-    return {"schur": schur, "factor": 2 * (L * ns) ** 3}
+    return {"schur": schur, "factor": (2 if CD.FACTOR == "inverse" else 2.0 / 3.0) * (L * ns) ** 3}
 
 
 def condense_flops_per_macro(disc):
@@ -453,7 +455,10 @@ def run_gpu(args, rank, world):
             entry.update({"algorithmic_bytes_per_launch": kbytes[k], "achieved_gbs": gbs, "frac": gbs / hbm})
         kernels[k] = entry
     dom = max(kern_s, key=kern_s.get)  # dominant kernel by time
-    dom_name = {"apply_si": "k_si_stream<2,4,3> (TMA-streamed S^-1 apply)",
+    from paper_2402_11361_b200 import condense as CD
+    lu = CD.FACTOR == "lu"
+    dom_name = {"apply_si": "k_lu_warp<2,4,3> (packed-LU forward/back substitution)" if lu
+                else "k_si_stream<2,4,3> (TMA-streamed S^-1 apply)",
                 "apply_pre": "k_apply_stream<2,4,3,pre>", "apply_post": "k_apply_stream<2,4,3,post>",
                 "apply_fused": "k_apply_stream<2,4,3,fused>", "apply_generic": "k_apply_local<2>"}.get(dom, dom)
     dom_bytes = kbytes.get(dom, b_mac * disc.n_mac)
@@ -483,7 +488,8 @@ def run_gpu(args, rank, world):
                      "share_of_step": kern_s[dom] / (t_apply / K),
                      "timing": "CUDA events around every library kernel on its stream (mhdg_timeline)",
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"},
-        "apply_local": {"what": "pre + S^-1 stream + post kernels against B_ref (SURVEY 8d)",
+        "apply_local": {"what": ("pre + LU solve + post kernels" if lu else "pre + S^-1 stream + post kernels")
+                                + " against B_ref (SURVEY 8d)",
                         "achieved": achieved_local, "unit": "GB/s", "frac": achieved_local / hbm,
                         "algorithmic_bytes_per_launch": b_mac * disc.n_mac, "seconds": k_apply,
                         "traffic": traffic.get("apply_local_dram_bytes_per_launch")},
@@ -496,8 +502,9 @@ def run_gpu(args, rank, world):
                                   "peak_source": "cuBLAS DGEMM 8192^3 measured in this run"},
                      "executed": {"flops_per_macro": fx, "achieved_tflops": exec_tf,
                                   "frac": (exec_tf / fp64) if fp64 else None,
-                                  "note": "S^-1 is formed explicitly (the reference's np.linalg.inv): 2 n^3, "
-                                          "3x the LU term of F_cond"}},
+                                  "note": "factor kind %s: " % CD.FACTOR
+                                          + ("batched LU with partial pivoting, (2/3) n^3 (the F_cond term)" if lu
+                                             else "explicit S^-1 (the reference's np.linalg.inv), 2 n^3")}},
         "assembly": {"metric": "macro-elements assembled/s (Jacobian + residual)", "value": disc.n_mac / t_asm,
                      "seconds": t_asm, "kernel_seconds": t_asm_k},
         "e2e": {"value": n_dofs_job / t_e2e, "unit": "DOF-applies/s",

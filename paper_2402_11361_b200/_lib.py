@@ -11,7 +11,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmhdg.so")
+# MHDG_LIB: an alternative build of the same library (A/B measurements of compile-time variants)
+LIB_PATH = os.environ.get("MHDG_LIB") or os.path.join(HERE, "libmhdg.so")
 
 MHDG_OK = 0
 MHDG_ERR_ADMISSIBILITY = 1

@@ -20,9 +20,10 @@ from .assembly import LocalBlocks, raise_status
 from .device import current_stream
 
 
-# S factor kept per macro: "inverse" (explicit S^-1 by Gauss-Jordan, as the
-# reference's np.linalg.inv) or "lu" (packed LU with partial pivoting)
-FACTOR = os.environ.get("MHDG_FACTOR", "inverse")
+# S factor kept per macro: "lu" (default: batched LU with partial pivoting, packed for
+# the forward/back substitution of the apply, as BASELINE's north_star asks) or
+# "inverse" (explicit S^-1 by Gauss-Jordan, what the reference's np.linalg.inv stores)
+FACTOR = os.environ.get("MHDG_FACTOR", "lu")
 FACTOR_KINDS = {"inverse": 0, "lu": 1}
 
 
@@ -34,7 +35,7 @@ class CondensedSchur:
     def __init__(self, blocks: LocalBlocks, lu: torch.Tensor, perm: torch.Tensor, scratch: torch.Tensor,
                  work: torch.Tensor | None = None):
         self.blocks = blocks
-        self.lu = lu  # S^-1 per macro, tiled (csrc/tiled_inv.cuh)
+        self.lu = lu  # per macro: packed LU (csrc/packed_lu.cuh) or tiled S^-1 (csrc/tiled_inv.cuh)
         self.perm = perm
         self.scratch = scratch  # S before inversion
         self.work = work  # hand-off vectors of the split apply (pre -> S^-1 stream -> post)

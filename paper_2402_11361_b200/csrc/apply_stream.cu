@@ -895,224 +895,133 @@ __global__ void __launch_bounds__(NCT + 32) k_si_stream(int n_mac, const double*
 }
 
 // ---------------------------------------------------------------------------
-// LU stream (split apply, middle kernel, packed-LU factors): y2 = U^-1 L^-1 P y1.
+// LU solve (split apply, middle kernel, packed-LU factors): y2 = U^-1 L^-1 P y1.
 //
-// Per macro, pieces in the packed order of packed_lu.cuh: y1 (the pivot rows
-// are read directly: their per-macro base is not 16-byte aligned for every n),
-// then forward blocks b = 0.. (L panel tiles, inv(L_bb) strict lower) and
-// backward blocks b = nblk-1.. (U panel tiles, inv(U_bb) upper).  A block step
-// accumulates its panel tiles like k_si_stream (warp w owns rows 8w.., lane l
-// column l of every tile), reduces, and after a named barrier applies the
-// inverted diagonal triangle; the solution is kept in shared memory.  The
-// per-block dependency stays inside a macro, so a CTA walks whole macros and
-// several CTAs per SM hide each other's barriers.
+// One warp per macro, no CTA barriers: lane l owns rows l and l + 32 of every
+// 64-row block.  The packed factor is column-major inside panels and
+// triangles (packed_lu.cuh), so per column a warp reads its block rows with
+// one coalesced 256-byte access; the block's right-hand side and solution
+// stay in the warp's slice of shared memory.  A block step is a panel GEMV
+// (sixteen columns of loads in flight per lane), a warp-synchronous hand-off
+// and the inverted diagonal triangle; many warps per SM keep HBM busy while
+// each walks its macro's dependent block steps.
 // ---------------------------------------------------------------------------
-struct LuPiece {
-  int kind;  // 0 y1, 1 perm, 2 panel tile, 3 triangle
-  int b, fwd, tile;
-  long long off;  // doubles from the macro's factor base (kind 2, 3)
-  int cnt;        // doubles (even)
-  int w;          // tile width (kind 2), c0 = first column of the tile
-  int c0;
+constexpr int LUW_NT = 128;
+
+struct LuBlk {
+  long long fwd_panel, fwd_diag, bwd_panel, bwd_diag;
+  int nb, r0, ncol_fwd, ncol_bwd;
 };
 
-template <int N>
-struct LuSched {
-  static constexpr int NBLK = (N + PLU_NB - 1) / PLU_NB;
-  int stage = 0, b = 0, t = -1;  // stage 0: y1, 1: perm, 2: forward, 3: backward
-  __host__ __device__ bool next(LuPiece& p) {
-    if (stage == 0) {
-      p.kind = 0;
-      p.cnt = (N + 1) & ~1;
-      stage = 1;
-      return true;
+// rows lane and lane + 32 of an nb-row column-major panel times x[c0 .. c0 + ncol)
+__device__ __forceinline__ void luw_panel(const double* __restrict__ P, int nb, int ncol, const double* x, int lane,
+                                          double& a0, double& a1) {
+  const bool v0 = lane < nb, v1 = lane + 32 < nb;
+  int c = 0;
+  for (; c + 16 <= ncol; c += 16) {
+    double t0[16], t1[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      t0[k] = v0 ? __ldcs(P + (size_t)(c + k) * nb + lane) : 0.0;
+      t1[k] = v1 ? __ldcs(P + (size_t)(c + k) * nb + lane + 32) : 0.0;
     }
-    if (stage == 1) {
-      stage = 2;
-      b = 0;
-      t = 0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const double xv = x[c + k];
+      a0 += t0[k] * xv;
+      a1 += t1[k] * xv;
     }
-    while (stage == 2 || stage == 3) {
-      const bool fwd = stage == 2;
-      const PluOffsets o = plu_offsets(N, b);
-      const int ncol = fwd ? o.ncol_fwd : o.ncol_bwd;
-      const int ntile = (ncol + PLU_TW - 1) / PLU_TW;
-      p.b = b;
-      p.fwd = fwd;
-      if (t < ntile) {
-        const int c0 = t * PLU_TW, w = (ncol - c0) < PLU_TW ? ncol - c0 : PLU_TW;
-        p.kind = 2;
-        p.tile = t;
-        p.w = w;
-        p.c0 = (fwd ? 0 : o.r0 + o.nb) + c0;
-        p.off = (fwd ? o.fwd_panel : o.bwd_panel) + (long long)t * o.nb * PLU_TW;
-        p.cnt = (int)even_ll((long long)o.nb * w);
-        ++t;
-        return true;
-      }
-      if (t == ntile) {
-        p.kind = 3;
-        p.off = fwd ? o.fwd_diag : o.bwd_diag;
-        p.cnt = (int)even_ll(fwd ? (long long)o.nb * (o.nb - 1) / 2 : (long long)o.nb * (o.nb + 1) / 2);
-        ++t;
-        return true;
-      }
-      t = 0;
-      if (fwd) {
-        if (++b == NBLK) { stage = 3; b = NBLK - 1; }
-      } else {
-        if (--b < 0) { stage = 4; }
-      }
-    }
-    return false;
   }
-};
-
-template <class C, int STAGES, int NCT>
-__global__ void __launch_bounds__(NCT + 32) k_lu_stream(int n_mac, const double* __restrict__ F,
-                                                       const int* __restrict__ perm, double* __restrict__ work) {
-  constexpr int n = C::n, NP = (n + 1) & ~1, NW = NCT / 32, SRW = PLU_NB / NW;
-  static_assert(SRW * NW == PLU_NB && PLU_TW == 32, "LU stream mapping");
-  static_assert(NP <= ST_DBL, "y1 must fit one ring stage");
-  extern __shared__ __align__(128) double smem[];
-  __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES];
-  double* ring = smem;
-  double* ybuf = smem + STAGES * ST_DBL;  // NP: solution (logical order)
-  double* tmp = ybuf + NP;               // PLU_NB: block right-hand side
-  int* pv = reinterpret_cast<int*>(tmp + PLU_NB);  // n + 3: pivot rows
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const long long FS = plu_size(n);
-  if (tid == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], NW);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
-
-  if (warp == NW) {  // producer
-    if (lane == 0) {
-      int it = 0;
-      for (int mac = blockIdx.x; mac < n_mac; mac += gridDim.x) {
-        LuSched<n> sc;
-        LuPiece p;
-        while (sc.next(p)) {
-          const int s = it % STAGES;
-          if (it >= STAGES) mbar_wait(&empty_bar[s], ((it / STAGES) + 1) & 1);
-          const void* src =
-              p.kind == 0 ? (const void*)Work<C>::y1(work, mac) : (const void*)(F + (size_t)mac * FS + p.off);
-          const uint32_t bytes = (uint32_t)p.cnt * 8u;
-          mbar_arrive_expect_tx(&full_bar[s], bytes);
-          bulk_g2s(ring + s * ST_DBL, src, bytes, &full_bar[s]);
-          ++it;
-        }
-      }
-    }
-    return;
-  }
-
-  int it = 0;
-  auto wait_stage = [&]() -> const double* {
-    const int s = it % STAGES;
-    mbar_wait(&full_bar[s], (it / STAGES) & 1);
-    return ring + s * ST_DBL;
-  };
-  auto release = [&]() {
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty_bar[it % STAGES]);
-    ++it;
-  };
-  for (int mac = blockIdx.x; mac < n_mac; mac += gridDim.x) {
-    named_bar(1, NCT);  // previous macro's solution read
-    for (int i = tid; i < n; i += NCT) pv[i] = __ldg(perm + (size_t)mac * n + i);
-    const double* y1s = wait_stage();  // y1 (natural order)
-    for (int i = tid; i < n; i += NCT) ybuf[i] = y1s[i];
-    release();
-    named_bar(1, NCT);
-    double yp[(NP + NCT - 1) / NCT];
-#pragma unroll
-    for (int k = 0; k < (NP + NCT - 1) / NCT; ++k) yp[k] = (tid + k * NCT < n) ? ybuf[pv[tid + k * NCT]] : 0.0;
-    named_bar(1, NCT);
-#pragma unroll
-    for (int k = 0; k < (NP + NCT - 1) / NCT; ++k)
-      if (tid + k * NCT < n) ybuf[tid + k * NCT] = yp[k];  // (P y1), logical order
-    named_bar(1, NCT);
-
-    LuSched<n> sc;
-    LuPiece p;
-    sc.next(p);  // y1
-    double acc[SRW];
-#pragma unroll
-    for (int j = 0; j < SRW; ++j) acc[j] = 0.0;
-    const int r0w = SRW * warp;
-    while (sc.next(p)) {
-      const PluOffsets o = plu_offsets(n, p.b);
-      const int nb = o.nb;
-      if (p.kind == 2) {  // panel tile: acc[row] += T[row][c] x[c0 + c]
-        const double* T = wait_stage();
-        if (lane < p.w) {
-          const double xv = ybuf[p.c0 + lane];
-#pragma unroll
-          for (int j = 0; j < SRW; ++j)
-            if (r0w + j < nb) acc[j] += T[(r0w + j) * p.w + lane] * xv;
-        }
-        release();
-      } else {  // triangle: finish the block
-#pragma unroll
-        for (int j = 0; j < SRW; ++j) {
-          double v = acc[j];
-#pragma unroll
-          for (int oo = 16; oo > 0; oo >>= 1) v += __shfl_xor_sync(MHDG_FULL, v, oo);
-          if (lane == j && r0w + j < nb) tmp[r0w + j] = ybuf[o.r0 + r0w + j] - v;
-          acc[j] = 0.0;
-        }
-        named_bar(1, NCT);  // tmp complete
-        const double* Tr = wait_stage();
-#pragma unroll
-        for (int j = 0; j < SRW; ++j) {
-          const int r = r0w + j;
-          double v = 0.0;
-          if (r < nb) {
-            if (p.fwd) {  // y = tmp + invL_strict tmp
-              for (int c = lane; c < r; c += 32) v += Tr[plu_lo(r, c)] * tmp[c];
-            } else {      // x = invU tmp (upper incl. diagonal)
-              for (int c = r + lane; c < nb; c += 32) v += Tr[plu_up(nb, r, c)] * tmp[c];
-            }
-          }
-#pragma unroll
-          for (int oo = 16; oo > 0; oo >>= 1) v += __shfl_xor_sync(MHDG_FULL, v, oo);
-          if (lane == j && r < nb) ybuf[o.r0 + r] = p.fwd ? tmp[r] + v : v;
-        }
-        release();
-        named_bar(1, NCT);  // block solution visible before the next block reads it
-      }
-    }
-    double* y2 = Work<C>::y2(work, n_mac, mac);
-    for (int i = tid; i < n; i += NCT) y2[i] = ybuf[i];
+  for (; c < ncol; ++c) {
+    const double xv = x[c];
+    if (v0) a0 += __ldcs(P + (size_t)c * nb + lane) * xv;
+    if (v1) a1 += __ldcs(P + (size_t)c * nb + lane + 32) * xv;
   }
 }
 
-#ifndef MHDG_LU_STAGES
-#define MHDG_LU_STAGES 3
-#endif
+template <class C>
+__global__ void __launch_bounds__(LUW_NT) k_lu_warp(int n_mac, const double* __restrict__ F,
+                                                    const int* __restrict__ perm, double* __restrict__ work) {
+  constexpr int n = C::n, NP = ceven(n), NBLK = (n + PLU_NB - 1) / PLU_NB, NWP = LUW_NT / 32;
+  extern __shared__ __align__(16) double smw[];
+  __shared__ LuBlk blk[NBLK];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid < NBLK) {
+    const PluOffsets o = plu_offsets(n, tid);
+    blk[tid] = LuBlk{o.fwd_panel, o.fwd_diag, o.bwd_panel, o.bwd_diag, o.nb, o.r0, o.ncol_fwd, o.ncol_bwd};
+  }
+  __syncthreads();
+  double* yb = smw + warp * (NP + PLU_NB);  // solution, logical order
+  double* tb = yb + NP;                     // block right-hand side
+  const long long FS = plu_size(n);
+  for (int mac = blockIdx.x * NWP + warp; mac < n_mac; mac += gridDim.x * NWP) {
+    const double* y1 = Work<C>::y1(work, mac);
+    const int* pm = perm + (size_t)mac * n;
+    for (int k = lane; k < n; k += 32) yb[k] = y1[__ldg(pm + k)];  // P y1
+    __syncwarp();
+    const double* Fm = F + (size_t)mac * FS;
+    for (int b = 0; b < NBLK; ++b) {  // forward: y_b = inv(L_bb) (y_b - L[b, :b] y_:b)
+      const LuBlk o = blk[b];
+      double a0 = 0.0, a1 = 0.0;
+      luw_panel(Fm + o.fwd_panel, o.nb, o.ncol_fwd, yb, lane, a0, a1);
+      if (lane < o.nb) tb[lane] = yb[o.r0 + lane] - a0;
+      if (lane + 32 < o.nb) tb[lane + 32] = yb[o.r0 + lane + 32] - a1;
+      __syncwarp();
+      double v0 = lane < o.nb ? tb[lane] : 0.0, v1 = lane + 32 < o.nb ? tb[lane + 32] : 0.0;
+      const double* Tl = Fm + o.fwd_diag;
+#pragma unroll 8
+      for (int c = 0; c < o.nb - 1; ++c) {  // column c of inv(L_bb): rows c+1 .. nb-1
+        const double* col = Tl + plu_lo_col(o.nb, c) - c - 1;
+        const double tc = tb[c];
+        if (lane > c && lane < o.nb) v0 += __ldcs(col + lane) * tc;
+        if (lane + 32 > c && lane + 32 < o.nb) v1 += __ldcs(col + lane + 32) * tc;
+      }
+      if (lane < o.nb) yb[o.r0 + lane] = v0;
+      if (lane + 32 < o.nb) yb[o.r0 + lane + 32] = v1;
+      __syncwarp();
+    }
+    for (int b = NBLK - 1; b >= 0; --b) {  // backward: x_b = inv(U_bb) (y_b - U[b, b+1:] x_b+1:)
+      const LuBlk o = blk[b];
+      double a0 = 0.0, a1 = 0.0;
+      luw_panel(Fm + o.bwd_panel, o.nb, o.ncol_bwd, yb + o.r0 + o.nb, lane, a0, a1);
+      if (lane < o.nb) tb[lane] = yb[o.r0 + lane] - a0;
+      if (lane + 32 < o.nb) tb[lane + 32] = yb[o.r0 + lane + 32] - a1;
+      __syncwarp();
+      double v0 = 0.0, v1 = 0.0;
+      const double* Tu = Fm + o.bwd_diag;
+#pragma unroll 8
+      for (int c = 0; c < o.nb; ++c) {  // column c of inv(U_bb): rows 0 .. c
+        const double* col = Tu + c * (c + 1) / 2;
+        const double tc = tb[c];
+        if (lane <= c) v0 += __ldcs(col + lane) * tc;
+        if (lane + 32 <= c) v1 += __ldcs(col + lane + 32) * tc;
+      }
+      if (lane < o.nb) yb[o.r0 + lane] = v0;
+      if (lane + 32 < o.nb) yb[o.r0 + lane + 32] = v1;
+      __syncwarp();
+    }
+    double* y2 = Work<C>::y2(work, n_mac, mac);
+    for (int k = lane; k < n; k += 32) y2[k] = yb[k];
+    __syncwarp();
+  }
+}
 
 template <class C>
 static int launch_lu_stream(const mhdg_disc& g, const mhdg_factors& f, cudaStream_t st) {
-  constexpr int STG = MHDG_LU_STAGES, NCT = 256;
-  const size_t bytes = sizeof(double) * ((size_t)STG * ST_DBL + ((C::n + 1) & ~1) + PLU_NB) + sizeof(int) * (C::n + 4);
-  auto kern = k_lu_stream<C, STG, NCT>;
+  const size_t bytes = sizeof(double) * (LUW_NT / 32) * (ceven(C::n) + PLU_NB);
+  auto kern = k_lu_warp<C>;
   static int ctas = 0;
   if (!ctas) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     int dev = 0, sms = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, NCT + 32, bytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, LUW_NT, bytes);
     ctas = sms * (per > 0 ? per : 1);
   }
-  const int grid = g.n_mac < ctas ? g.n_mac : ctas;
-  kern<<<grid, NCT + 32, bytes, st>>>(g.n_mac, f.lu, f.perm, f.work);
+  const int need = (g.n_mac + LUW_NT / 32 - 1) / (LUW_NT / 32);
+  const int grid = need < ctas ? need : ctas;
+  kern<<<grid, LUW_NT, bytes, st>>>(g.n_mac, f.lu, f.perm, f.work);
   return launch_ok();
 }
 

@@ -9,7 +9,7 @@
 //              (row interchanges) and k_gj (32-column FFMA panels, any n that
 //              fits) are the A/B variant and the large-n fallback.
 // k_lu3        batched LU with partial pivoting (pivots in place), packed into
-//              block-triangular solve order by k_pack_lu3 (packed_lu.cuh): the
+//              block-triangular solve order by k_pack_lu4 (packed_lu.cuh): the
 //              MHDG_FACTOR=lu option.
 // FactorizationError on an exactly zero pivot.
 #include "common.cuh"
@@ -1591,76 +1591,6 @@ __global__ void __launch_bounds__(NT, 2) k_lu3(int n, double* __restrict__ S, in
   if (singular && tid == 0) set_status(status, MHDG_ERR_FACTORIZATION, mac, 0, 0.0);
 }
 
-// in-place LU with pivot rows in place -> packed solve layout (packed_lu.cuh):
-// logical row r = physical row piv[r]; diagonal tiles inverted.
-__global__ void __launch_bounds__(256) k_pack_lu3(int n, const double* __restrict__ F, const int* __restrict__ piv,
-                                                  double* __restrict__ out) {
-  extern __shared__ double pk_sm[];
-  double(*T)[PLU_NB + 1] = reinterpret_cast<double(*)[PLU_NB + 1]>(pk_sm);
-  double(*X)[PLU_NB + 1] = reinterpret_cast<double(*)[PLU_NB + 1]>(pk_sm + PLU_NB * (PLU_NB + 1));
-  int* pr = reinterpret_cast<int*>(pk_sm + 2 * PLU_NB * (PLU_NB + 1));
-  const int mac = blockIdx.x, tid = threadIdx.x;
-  const double* A = F + (size_t)mac * n * n;
-  double* O = out + (size_t)mac * plu_size(n);
-  for (int i = tid; i < n; i += blockDim.x) pr[i] = piv[(size_t)mac * n + i];
-  __syncthreads();
-  const int nblk = plu_nblk(n);
-  for (int b = 0; b < nblk; ++b) {
-    const PluOffsets o = plu_offsets(n, b);
-    const int nb = o.nb, r0 = o.r0;
-    for (int idx = tid; idx < nb * o.ncol_fwd; idx += blockDim.x) {
-      const int r = idx / o.ncol_fwd, c = idx % o.ncol_fwd;
-      O[o.fwd_panel + plu_panel_idx(nb, o.ncol_fwd, r, c)] = A[(size_t)pr[r0 + r] * n + c];
-    }
-    for (int idx = tid; idx < nb * o.ncol_bwd; idx += blockDim.x) {
-      const int r = idx / o.ncol_bwd, c = idx % o.ncol_bwd;
-      O[o.bwd_panel + plu_panel_idx(nb, o.ncol_bwd, r, c)] = A[(size_t)pr[r0 + r] * n + r0 + nb + c];
-    }
-    for (int idx = tid; idx < nb * nb; idx += blockDim.x) {
-      const int r = idx / nb, c = idx % nb;
-      T[r][c] = A[(size_t)pr[r0 + r] * n + r0 + c];
-    }
-    __syncthreads();
-    if (tid < nb) {  // inverse of the unit lower tile, column tid
-      const int c = tid;
-      X[c][c] = 1.0;
-      for (int i = c + 1; i < nb; ++i) {
-        double acc = 0.0;
-        for (int k = c; k < i; ++k) acc += T[i][k] * X[k][c];
-        X[i][c] = -acc;
-      }
-    }
-    __syncthreads();
-    for (int idx = tid; idx < nb * nb; idx += blockDim.x) {
-      const int r = idx / nb, c = idx % nb;
-      if (c < r) O[o.fwd_diag + plu_lo(r, c)] = X[r][c];
-    }
-    __syncthreads();
-    if (tid < nb) {  // inverse of the upper tile, column tid
-      const int c = tid;
-      X[c][c] = 1.0 / T[c][c];
-      for (int i = c - 1; i >= 0; --i) {
-        double acc = 0.0;
-        for (int k = i + 1; k <= c; ++k) acc += T[i][k] * X[k][c];
-        X[i][c] = -acc / T[i][i];
-      }
-    }
-    __syncthreads();
-    for (int idx = tid; idx < nb * nb; idx += blockDim.x) {
-      const int r = idx / nb, c = idx % nb;
-      if (c >= r) O[o.bwd_diag + plu_up(nb, r, c)] = X[r][c];
-    }
-    if (tid == 0) {  // zero the even-size padding of the last (narrow) tiles and triangles
-      if ((nb * (nb - 1) / 2) & 1) O[o.fwd_diag + nb * (nb - 1) / 2] = 0.0;
-      if ((nb * (nb + 1) / 2) & 1) O[o.bwd_diag + nb * (nb + 1) / 2] = 0.0;
-      const int wf = o.ncol_fwd % PLU_TW, wb = o.ncol_bwd % PLU_TW;
-      if ((nb * wf) & 1) O[o.fwd_diag - 1] = 0.0;
-      if ((nb * wb) & 1) O[o.bwd_diag - 1] = 0.0;
-    }
-    __syncthreads();
-  }
-}
-
 #ifndef MHDG_LU_NB
 #define MHDG_LU_NB 24
 #endif
@@ -1668,15 +1598,8 @@ __global__ void __launch_bounds__(256) k_pack_lu3(int n, const double* __restric
 #define MHDG_LU_NT 256
 #endif
 
-// in-place LU (pivot rows in place) -> packed solve layout
-int pack_lu(int n, int n_mac, const double* scratch, const int* piv, double* packed, cudaStream_t st) {
-  const size_t pbytes = sizeof(double) * 2 * PLU_NB * (PLU_NB + 1) + sizeof(int) * n;
-  cudaFuncSetAttribute(k_pack_lu3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pbytes);
-  tl_begin(TL_PACK, st);
-  k_pack_lu3<<<n_mac, 256, pbytes, st>>>(n, scratch, piv, packed);
-  tl_end(TL_PACK, st);
-  return launch_ok();
-}
+// packs an in-place LU (pivot rows in place) into the solve layout (lu.cu)
+int pack_lu4(int n, int n_mac, const double* scratch, const int* piv, double* packed, cudaStream_t st);
 
 int lu_factor3(int n, int n_mac, double* scratch, int* piv, double* packed, int* status, cudaStream_t st) {
   using L3 = Lu3<MHDG_LU_NB, MHDG_LU_NT>;
@@ -1689,7 +1612,7 @@ int lu_factor3(int n, int n_mac, double* scratch, int* piv, double* packed, int*
   tl_end(TL_FACTOR, st);
   int rc = launch_ok();
   if (rc) return rc;
-  return pack_lu(n, n_mac, scratch, piv, packed, st);
+  return pack_lu4(n, n_mac, scratch, piv, packed, st);
 }
 
 int inv_factor(int n, int n_mac, double* scratch, double* tiled, int* status, cudaStream_t st) {

@@ -20,7 +20,7 @@
 //     turned into B fragments with shuffles, then C -= L21 U12 over all
 //     remaining rows with C read-modified-written in global memory (L2).
 // Pivots stay in place (logical row k = physical row piv[k]; rows are never
-// moved), the output contract of k_lu3: k_pack_lu3 packs it for the apply.
+// moved), the output contract of k_lu3: k_pack_lu4 packs it for the apply.
 // FactorizationError on an exactly zero pivot (scipy's lu_factor / LAPACK
 // getrf report singular U).
 #include "common.cuh"
@@ -462,16 +462,16 @@ __global__ void __launch_bounds__(NT, 2) k_lu4(int n, double* __restrict__ S, in
 // --------------------------------------------------------------------------
 // k_pack_lu4: in-place LU (pivot rows in place) -> the packed solve layout of
 // packed_lu.cuh.  One CTA per macro, per 64-row block:
-//   * panels: one warp per logical row, lane = column, so every 32-column tile
-//     row is one coalesced read of the row's physical copy and one coalesced
-//     write;
+//   * panels: each 32-column segment of the block's 64 rows is staged in shared
+//     memory with coalesced reads of the physical rows and written column-major
+//     (the layout of packed_lu.cuh) with coalesced writes;
 //   * diagonal block: staged in shared memory, inv(L_bb) (unit lower) and
 //     inv(U_bb) = inv(unit upper) D^-1 by column sweeps over all threads with
 //     the columns in registers (one barrier per step), written as packed
 //     triangles.
 // --------------------------------------------------------------------------
 namespace pk4 {
-constexpr int NT = 256, TS = PLU_NB + 1, MAXSEG = 12;  // n <= 32 MAXSEG
+constexpr int NT = 256, TS = PLU_NB + 1;
 }
 
 // Column sweep for the inverse of a unit triangular nb x nb block (nb <= 64) held in
@@ -505,11 +505,12 @@ __device__ __forceinline__ void tri_sweep(const double* T, const double* rd, int
 }
 
 __global__ void __launch_bounds__(pk4::NT, 3) k_pack_lu4(int n, const double* __restrict__ F,
-                                                      const int* __restrict__ piv, double* __restrict__ out) {
+                                                         const int* __restrict__ piv, double* __restrict__ out) {
   using namespace pk4;
   extern __shared__ double pk_sm[];
   double* T = pk_sm;                    // PLU_NB x TS: diagonal block (logical rows)
-  double* rd = T + PLU_NB * TS;         // PLU_NB: 1 / U[k][k]
+  double* X = T + PLU_NB * TS;          // PLU_NB x TS: an inverse; first 32 columns: tile staging
+  double* rd = X + PLU_NB * TS;         // PLU_NB: 1 / U[k][k]
   double* xr = rd + PLU_NB;             // [2][PLU_NB]: row k of X, broadcast per sweep step
   int* pr = reinterpret_cast<int*>(xr + 2 * PLU_NB);
   const int mac = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -519,53 +520,56 @@ __global__ void __launch_bounds__(pk4::NT, 3) k_pack_lu4(int n, const double* __
   __syncthreads();
   const int nblk = plu_nblk(n);
   const int c = tid & (PLU_NB - 1), grp = tid / PLU_NB;  // column and row group of the sweeps
-  constexpr int NG = NT / PLU_NB;
+  constexpr int NG = NT / PLU_NB, RPW = PLU_NB / (NT / 32);
   for (int b = 0; b < nblk; ++b) {
     const PluOffsets o = plu_offsets(n, b);
     const int nb = o.nb, r0 = o.r0;
-    // panels and the diagonal block, row by row: the whole physical row is read in
-    // 32-column segments (all loads in flight), each segment then goes to its piece
-    for (int r = warp; r < nb; r += NT / 32) {
-      const double* src = A + (size_t)pr[r0 + r] * n;
-      double v[MAXSEG];
+    // 32-column segments of the block's rows: staged row-wise (coalesced reads of the
+    // physical rows), written column-major (coalesced writes of the packed tiles)
+    for (int col = 0; col < n; col += PLU_TW) {
+      double v[RPW];
 #pragma unroll
-      for (int j = 0; j < MAXSEG; ++j) v[j] = 32 * j + lane < n ? src[32 * j + lane] : 0.0;
-#pragma unroll
-      for (int j = 0; j < MAXSEG; ++j) {
-        const int col = 32 * j;
-        if (col >= n) break;
-        if (col < r0) {
-          O[o.fwd_panel + (long long)col * nb + (long long)r * PLU_TW + lane] = v[j];
-        } else if (col < r0 + nb) {
-          if (col + lane < r0 + nb) T[r * TS + col - r0 + lane] = v[j];
-        } else {
-          const int w = min(PLU_TW, n - col);
-          if (lane < w) O[o.bwd_panel + (long long)(col - r0 - nb) * nb + (long long)r * w + lane] = v[j];
-        }
+      for (int k = 0; k < RPW; ++k) {
+        const int r = warp + (NT / 32) * k;
+        v[k] = (r < nb && col + lane < n) ? A[(size_t)pr[r0 + r] * n + col + lane] : 0.0;
       }
+#pragma unroll
+      for (int k = 0; k < RPW; ++k) X[(warp + (NT / 32) * k) * TS + lane] = v[k];
+      __syncthreads();
+      const int w = min(PLU_TW, n - col), r = tid & (PLU_NB - 1);
+      if (col >= r0 && col < r0 + nb) {
+        for (int cc = grp; cc < w; cc += NG)
+          if (r < nb && col + cc < r0 + nb) T[r * TS + col - r0 + cc] = X[r * TS + cc];
+      } else {
+        double* dst = col < r0 ? O + o.fwd_panel + (long long)col * nb : O + o.bwd_panel + (long long)(col - r0 - nb) * nb;
+        for (int cc = grp; cc < w; cc += NG)
+          if (r < nb) dst[cc * nb + r] = X[r * TS + cc];
+      }
+      __syncthreads();
     }
-    __syncthreads();
     if (tid < nb) rd[tid] = 1.0 / T[tid * TS + tid];
     __syncthreads();
     double x[PLU_NB / NG];  // X[grp + NG s][c]
     // inv(L_bb): X = I; X[i][c] -= L[i][k] X[k][c] for i > k, c <= k, k ascending
     tri_sweep<true>(T, rd, nb, c, grp, xr, x);
-    if (c < nb) {
 #pragma unroll
-      for (int s2 = 0; s2 < PLU_NB / NG; ++s2) {
-        const int i = grp + NG * s2;
-        if (i < nb && c < i) O[o.fwd_diag + plu_lo(i, c)] = x[s2];
-      }
+    for (int s2 = 0; s2 < PLU_NB / NG; ++s2) X[(grp + NG * s2) * TS + c] = x[s2];
+    __syncthreads();
+    {
+      const int r = tid & (PLU_NB - 1);
+      for (int cc = grp; cc < nb - 1; cc += NG)
+        if (r > cc && r < nb) O[o.fwd_diag + plu_lo(nb, r, cc)] = X[r * TS + cc];
     }
     // inv(U_bb) = inv(Uh) D^-1, Uh = D^-1 U unit upper: X[i][c] -= Uh[i][k] X[k][c] for
     // i < k <= c, k descending
     tri_sweep<false>(T, rd, nb, c, grp, xr, x);
-    if (c < nb) {
 #pragma unroll
-      for (int s2 = 0; s2 < PLU_NB / NG; ++s2) {
-        const int i = grp + NG * s2;
-        if (i <= c) O[o.bwd_diag + plu_up(nb, i, c)] = x[s2] * rd[c];
-      }
+    for (int s2 = 0; s2 < PLU_NB / NG; ++s2) X[(grp + NG * s2) * TS + c] = x[s2];
+    __syncthreads();
+    {
+      const int r = tid & (PLU_NB - 1);
+      for (int cc = grp; cc < nb; cc += NG)
+        if (r <= cc) O[o.bwd_diag + plu_up(r, cc)] = X[r * TS + cc] * rd[cc];
     }
     if (tid == 0) {  // zero the even-size padding of the last (narrow) tiles and triangles
       if ((nb * (nb - 1) / 2) & 1) O[o.fwd_diag + nb * (nb - 1) / 2] = 0.0;
@@ -578,9 +582,8 @@ __global__ void __launch_bounds__(pk4::NT, 3) k_pack_lu4(int n, const double* __
   }
 }
 
-static int pack_lu4(int n, int n_mac, const double* scratch, const int* piv, double* packed, cudaStream_t st) {
-  if (n > 32 * pk4::MAXSEG) return -1;
-  const size_t bytes = sizeof(double) * (PLU_NB * pk4::TS + 3 * PLU_NB) + sizeof(int) * n;
+int pack_lu4(int n, int n_mac, const double* scratch, const int* piv, double* packed, cudaStream_t st) {
+  const size_t bytes = sizeof(double) * (2 * PLU_NB * pk4::TS + 3 * PLU_NB) + sizeof(int) * n;
   cudaFuncSetAttribute(k_pack_lu4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   tl_begin(TL_PACK, st);
   k_pack_lu4<<<n_mac, pk4::NT, bytes, st>>>(n, scratch, piv, packed);

@@ -1,17 +1,20 @@
-// Packed LU factor layout consumed by the streaming trace apply.
+// Packed LU factor layout consumed by the trace apply.
 //
 // After LU with partial pivoting (P S = L U, L unit lower), each macro's
 // factor is re-laid out in the order the two triangular solves read it, in
 // 64-row blocks b = 0..nblk-1 (nb_b rows each):
-//   forward  section, b ascending : [ L[b, 0:32b] panel | inv(L_bb) strict lower, packed ]
-//   backward section, b descending: [ U[b, 32b+nb_b:n] panel | inv(U_bb) upper incl. diag, packed ]
+//   forward  section, b ascending : [ L[b, 0:64b] panel | inv(L_bb) strict lower ]
+//   backward section, b descending: [ U[b, 64b+nb_b:n] panel | inv(U_bb) upper incl. diag ]
 // A panel (nb_b rows x ncol) is stored as consecutive column tiles of
-// PLU_TW = 32 columns (the last one narrower), each tile row-major with its
-// own width as row stride, so one tile is one contiguous bulk copy holding
-// every row of the block.  Every tile / triangle is padded to an even number
-// of doubles so each piece is a 16-byte aligned bulk copy.
-// The diagonal tiles are stored inverted, so the solve is a sequence of
-// GEMVs: y_b = inv(L_bb) (y_b - L[b,:b] y_:b), and likewise backwards.
+// PLU_TW = 32 columns (the last one narrower); inside a tile the layout is
+// column-major (element (r, c) at c * nb_b + r), and the triangles are
+// column-major too (column c of inv(L_bb): rows c+1..nb_b-1; of inv(U_bb):
+// rows 0..c).  So a warp walking a block reads, per column, consecutive rows:
+// one coalesced access per column, each lane owning rows of the block.
+// Every tile / triangle is padded to an even number of doubles (16-byte
+// aligned pieces).  The diagonal tiles are stored inverted, so the solve is a
+// sequence of GEMVs: y_b = inv(L_bb) (y_b - L[b,:b] y_:b), and likewise
+// backwards.
 #pragma once
 #include "common.cuh"
 
@@ -80,16 +83,16 @@ __host__ __device__ inline long long plu_size(int n) {
 }
 
 // offset of element (r, c) inside a tiled panel of nb rows x ncol columns
-__host__ __device__ __forceinline__ long long plu_panel_idx(int nb, int ncol, int r, int c) {
-  const int j = c / PLU_TW, c0 = j * PLU_TW;
-  const int w = (ncol - c0) < PLU_TW ? ncol - c0 : PLU_TW;
-  // all tiles before j are full width (even size nb*PLU_TW)
-  return (long long)j * nb * PLU_TW + (long long)r * w + (c - c0);
+__host__ __device__ __forceinline__ long long plu_panel_idx(int nb, int r, int c) {
+  // all tiles before c's are full width (even size nb*PLU_TW); column-major inside a tile
+  return (long long)c * nb + r;
 }
 
-// packed strict-lower index (r > c) and upper-incl-diag index (c >= r)
-__host__ __device__ __forceinline__ int plu_lo(int r, int c) { return r * (r - 1) / 2 + c; }
-__host__ __device__ __forceinline__ int plu_up(int nb, int r, int c) { return r * nb - r * (r - 1) / 2 + (c - r); }
+// column starts of the packed triangles: strict lower (column c: rows c+1..nb-1) and
+// upper incl. diagonal (column c: rows 0..c)
+__host__ __device__ __forceinline__ int plu_lo_col(int nb, int c) { return c * (nb - 1) - c * (c - 1) / 2; }
+__host__ __device__ __forceinline__ int plu_lo(int nb, int r, int c) { return plu_lo_col(nb, c) + (r - c - 1); }
+__host__ __device__ __forceinline__ int plu_up(int r, int c) { return c * (c + 1) / 2 + r; }
 
 // CTA-wide in-place y <- U^-1 L^-1 P y with a packed factor (synchronous loads).
 // y, t: shared vectors of length n.
@@ -105,15 +108,14 @@ __device__ inline void plu_solve_cta(const double* __restrict__ F, const int* __
     const PluOffsets o = plu_offsets(n, b);
     for (int r = warp; r < o.nb; r += nw) {
       double acc = 0.0;
-      for (int c = lane; c < o.ncol_fwd; c += 32)
-        acc += __ldg(F + o.fwd_panel + plu_panel_idx(o.nb, o.ncol_fwd, r, c)) * y[c];
+      for (int c = lane; c < o.ncol_fwd; c += 32) acc += __ldg(F + o.fwd_panel + plu_panel_idx(o.nb, r, c)) * y[c];
       acc = warp_sum(acc);
       if (lane == 0) t[r] = y[o.r0 + r] - acc;
     }
     __syncthreads();
     for (int r = tid; r < o.nb; r += blockDim.x) {
       double acc = t[r];
-      for (int c = 0; c < r; ++c) acc += __ldg(F + o.fwd_diag + plu_lo(r, c)) * t[c];
+      for (int c = 0; c < r; ++c) acc += __ldg(F + o.fwd_diag + plu_lo(o.nb, r, c)) * t[c];
       y[o.r0 + r] = acc;
     }
     __syncthreads();
@@ -124,14 +126,14 @@ __device__ inline void plu_solve_cta(const double* __restrict__ F, const int* __
     for (int r = warp; r < o.nb; r += nw) {
       double acc = 0.0;
       for (int c = lane; c < o.ncol_bwd; c += 32)
-        acc += __ldg(F + o.bwd_panel + plu_panel_idx(o.nb, o.ncol_bwd, r, c)) * y[c0 + c];
+        acc += __ldg(F + o.bwd_panel + plu_panel_idx(o.nb, r, c)) * y[c0 + c];
       acc = warp_sum(acc);
       if (lane == 0) t[r] = y[o.r0 + r] - acc;
     }
     __syncthreads();
     for (int r = tid; r < o.nb; r += blockDim.x) {
       double acc = 0.0;
-      for (int c = r; c < o.nb; ++c) acc += __ldg(F + o.bwd_diag + plu_up(o.nb, r, c)) * t[c];
+      for (int c = r; c < o.nb; ++c) acc += __ldg(F + o.bwd_diag + plu_up(r, c)) * t[c];
       y[o.r0 + r] = acc;
     }
     __syncthreads();

@@ -101,19 +101,21 @@ def test_c1_plane_couette_ptc_vs_oracle():
     assert r_dev <= 1e-10  # ptc_steady_solve's target; measured 2.68e-11 (oracle run: 3.73e-11)
 
 
-def test_dirk33_step_with_lu_factors():
-    """The DIRK33 golden step with packed-LU condensation factors."""
+@pytest.mark.parametrize("kind", ["lu", "inverse"])
+def test_dirk33_step_with_factor_kind(kind):
+    """The DIRK33 golden step with packed-LU (default) and explicit-inverse condensation factors."""
     need_gpu()
     from paper_2402_11361_b200 import condense as CD
 
     g = load_golden("dirk_tgv_m2p2")
     d = Discretization(build_cube_mesh(TGV.domain, 1, 2, periodic=(True,) * 3), 2, TGV.params)
     f = A.to_device_fields(d, g["u0"], g["q0"], g["uhat0"])
+    old = CD.FACTOR
     try:
-        CD.FACTOR = "lu"
+        CD.FACTOR = kind
         sts, _ = S.dirk_advance(d, f, float(g["dt"]), S.DirkTableau.dirk33())
     finally:
-        CD.FACTOR = "inverse"
+        CD.FACTOR = old
     assert [s.iterations for s in sts] == list(g["newton"])
     assert all(abs(a - b) <= 1 for a, b in zip([s.krylov_iterations for s in sts], g["krylov"]))
     assert rel_err(host(f.u), g["u"]) < 1e-8

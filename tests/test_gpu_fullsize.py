@@ -81,7 +81,9 @@ def test_full_size_apply_properties(cfg):
     assert _rel(y_fused, y_gen) < 1e-10, cfg
     # linearity
     y12 = cond.apply_trace(2.0 * x1 - 3.0 * x2)
-    assert _rel(y12, 2.0 * y_split - 3.0 * cond.apply_trace(x2)) < 1e-12
+    # 1e-11: the LU forward/back substitution rounds at cond(S) * eps level (cond(S) ~ 1e6
+    # at m=4, p=3); the explicit-inverse GEMV stays below 1e-12
+    assert _rel(y12, 2.0 * y_split - 3.0 * cond.apply_trace(x2)) < 1e-11
     # rhs / recover consistency: the Newton correction (du, dq, dx) of the full
     # local system with dx = x1 satisfies A_hat dx - b = (trace residual of the
     # recovered correction), i.e. apply_trace(x) - rhs is linear in x with the
