@@ -180,8 +180,9 @@ void mhdg_set_factor_variant(int v);
    For A/B measurements. */
 void mhdg_set_lu_variant(int v);
 
-/* Schur-complement kernel: 0 (default) FP64 tensor cores (DMMA), otherwise the
-   per-macro FFMA kernel.  For A/B measurements. */
+/* Schur-complement kernel: 0 (default) stage-pipelined FP64 tensor-core kernel,
+   1 the earlier tensor-core kernel, otherwise the per-macro FFMA kernel.  For A/B
+   measurements. */
 void mhdg_set_schur_variant(int v);
 
 /* 1 (default): split apply (pre / S^-1 stream / post kernels) when `work` is

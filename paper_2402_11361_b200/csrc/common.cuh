@@ -40,6 +40,13 @@ __device__ __forceinline__ void set_status(int* status, int code, int index, int
   }
 }
 
+// 8-byte global -> shared async copy (src_bytes = 0 zero-fills)
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, int src_bytes) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 inline int launch_ok() {
   ++g_launches;
   return cudaPeekAtLastError() == cudaSuccess ? MHDG_OK : MHDG_ERR_CUDA;

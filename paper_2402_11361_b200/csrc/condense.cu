@@ -1190,10 +1190,46 @@ __global__ void __launch_bounds__(256, 2) k_schur_mma(mhdg_disc g, mhdg_blocks b
     }
   };
 
+  // The stash of the next (face) sub-element streams in (cp.async) while the GEMMs of the
+  // current one run; on arrival the inverse Jacobian is folded into it in place,
+  // W'[q][(k, r')][s][r] = sum_l inv_jac[r'][l] W[q][(k, l)][s][r], so a left-factor entry
+  // is D products.
+  const int nwv = nq * NW, nwf = nqf * D * NS * NS, nstash = g.n_sub + NF * g.n_tri;
+  auto stash_src = [&](int i) -> const double* {
+    if (i < g.n_sub) return b.wdgdq_vol + ((size_t)mac * g.n_sub + i) * nwv;
+    const int fT = i - g.n_sub;  // f * n_tri + T
+    return b.wdgdq_face + ((size_t)mac * NF * g.n_tri + fT) * nwf;
+  };
+  auto prefetch = [&](int i) {
+    if (i >= nstash) return;
+    const double* src = stash_src(i);
+    const int cnt = i < g.n_sub ? nwv : nwf;
+    for (int e = tid; e < cnt; e += blockDim.x) cp_async8(Wst + e, src + e, 8);
+  };
+  auto land_and_fold = [&](int i) {  // wait for stash i, fold inv_jac into it
+    cp_async_wait_all();
+    __syncthreads();
+    const int ngrp = (i < g.n_sub ? nq * D : nqf) * NS * NS;  // (q[, k], s, r) groups
+    for (int e = tid; e < ngrp; e += blockDim.x) {
+      const int sr = e % (NS * NS), qk = e / (NS * NS);  // qk = q * D + k (volume) or q (face)
+      double* w = Wst + (size_t)qk * D * NS * NS + sr;
+      double v[D];
+#pragma unroll
+      for (int l = 0; l < D; ++l) v[l] = w[l * NS * NS];
+#pragma unroll
+      for (int rp = 0; rp < D; ++rp) {
+        double t = 0.0;
+#pragma unroll
+        for (int l = 0; l < D; ++l) t += ij[rp][l] * v[l];
+        w[rp * NS * NS] = t;
+      }
+    }
+  };
+
   // ---- volume sub-elements ----
+  prefetch(0);
   for (int K = 0; K < g.n_sub; ++K) {
-    const double* W = b.wdgdq_vol + ((size_t)mac * g.n_sub + K) * nq * NW;
-    for (int i = tid; i < nq * NW; i += blockDim.x) Wst[i] = W[i];
+    land_and_fold(K);
     for (int idx = tid; idx < dm.kv * L; idx += blockDim.x) {
       const int j = idx % L, qr = idx / L;
       PM[qr * dm.LP + j] = __ldg(g.pm_vol + ((size_t)K * dm.kv + qr) * L + j);
@@ -1206,18 +1242,14 @@ __global__ void __launch_bounds__(256, 2) k_schur_mma(mhdg_disc g, mhdg_blocks b
         const int qr = idx % dm.kv, ml = idx / dm.kv, m = m0 + ml;
         const int q = qr / D, rp = qr % D, a = m / (NS * NS), s = (m / NS) % NS, r = m % NS;
         const double* gp = gph + ((cls * nq + q) * nloc + a) * D;
-        const double* w = Wst + q * NW + s * NS + r;
+        const double* w = Wst + q * NW + (rp * NS + s) * NS + r;
         double v = 0.0;
 #pragma unroll
-        for (int l = 0; l < D; ++l) {
-          double t = 0.0;
-#pragma unroll
-          for (int k = 0; k < D; ++k) t += gp[k] * w[(k * D + l) * NS * NS];
-          v += ij[rp][l] * t;
-        }
+        for (int k = 0; k < D; ++k) v += gp[k] * w[k * D * NS * NS];
         Tp[ml * dm.sA + qr] = v;
       }
       __syncthreads();
+      if (m0 + dm.MVp >= dm.MV) prefetch(K + 1);  // the stash is consumed: overlap the next one
       gemm_into_s(mc, m0, dm.nks_v, [&](int a) { return __ldg(g.sub_conn + K * nloc + a); }, K);
       __syncthreads();
     }
@@ -1225,11 +1257,10 @@ __global__ void __launch_bounds__(256, 2) k_schur_mma(mhdg_disc g, mhdg_blocks b
   // ---- face sub-elements (sign folded into T1') ----
   for (int idx = tid; idx < dm.MVp * dm.sA; idx += blockDim.x) Tp[idx] = 0.0;
   for (int idx = tid; idx < kmaxp * dm.LP; idx += blockDim.x) PM[idx] = 0.0;
-  __syncthreads();
   for (int f = 0; f < NF; ++f) {
     for (int T = 0; T < g.n_tri; ++T) {
-      const double* W = b.wdgdq_face + (((size_t)mac * NF + f) * g.n_tri + T) * nqf * D * NS * NS;
-      for (int i = tid; i < nqf * D * NS * NS; i += blockDim.x) Wst[i] = W[i];
+      const int si = g.n_sub + f * g.n_tri + T;
+      land_and_fold(si);
       for (int idx = tid; idx < dm.kf * L; idx += blockDim.x) {
         const int j = idx % L, qr = idx / L;
         PM[qr * dm.LP + j] = __ldg(g.pm_face + (((size_t)f * g.n_tri + T) * dm.kf + qr) * L + j);
@@ -1240,18 +1271,15 @@ __global__ void __launch_bounds__(256, 2) k_schur_mma(mhdg_disc g, mhdg_blocks b
         for (int idx = tid; idx < mc * dm.kf; idx += blockDim.x) {
           const int qr = idx % dm.kf, ml = idx / dm.kf, m = m0 + ml;
           const int q = qr / D, rp = qr % D, a = m / (NS * NS), s = (m / NS) % NS, r = m % NS;
-          double v = 0.0;
-#pragma unroll
-          for (int l = 0; l < D; ++l) v += ij[rp][l] * Wst[((q * D + l) * NS + s) * NS + r];
-          Tp[ml * dm.sA + qr] = -v * __ldg(g.phi_face + q * nlocf + a);
+          Tp[ml * dm.sA + qr] = -Wst[((q * D + rp) * NS + s) * NS + r] * __ldg(g.phi_face + q * nlocf + a);
         }
         __syncthreads();
+        if (m0 + dm.MVp >= dm.MF) prefetch(si + 1);
         gemm_into_s(mc, m0, dm.nks_f, [&](int a) {
           return __ldg(g.face_vol_nodes + f * g.Lf + __ldg(g.tri_conn + T * nlocf + a));
         }, -1);
         __syncthreads();
       }
-      __syncthreads();
     }
   }
 }
@@ -1630,7 +1658,9 @@ int inv_factor(int n, int n_mac, double* scratch, double* tiled, int* status, cu
 // host launchers
 // --------------------------------------------------------------------------
 
-int g_schur_variant = 0;  // 0: tensor cores, else per-macro FFMA (A/B knob)
+int g_schur_variant = 0;  // 0: k_schur2, 1: k_schur_mma, else per-macro FFMA (A/B knob)
+template <int D>
+int schur2(const mhdg_disc& g, const mhdg_blocks& b, double* S, cudaStream_t st);
 
 template <int D>
 int schur_matrix(const mhdg_disc& g, const mhdg_blocks& b, double* S, cudaStream_t st) {
@@ -1638,10 +1668,14 @@ int schur_matrix(const mhdg_disc& g, const mhdg_blocks& b, double* S, cudaStream
   const int kv = g.nq * D, kf = g.nqf * D, kmax = kv > kf ? kv : kf;
   const int rmax = (g.nloc > g.nlocf ? g.nloc : g.nlocf) * NS;
   const int n = g.L * NS;
-  {  // tensor-core kernel when its operands fit (k-steps <= 16)
+  if (g_schur_variant == 0) {  // stage-pipelined tensor-core kernel (schur.cu)
+    const int rc = schur2<D>(g, b, S, st);
+    if (rc >= 0) return rc;
+  }
+  {  // earlier tensor-core kernel when its operands fit
     const SchurMmaDims<D> dm(g);
     const size_t mb = sizeof(double) * dm.smem_doubles(g);
-    if (g_schur_variant == 0 && dm.nks_v <= SchT<D>::KS && dm.nks_f <= SchT<D>::KS &&
+    if (g_schur_variant <= 1 && dm.nks_v <= SchT<D>::KS && dm.nks_f <= SchT<D>::KS &&
         g.L <= 8 * SchT<D>::NT &&
         mb <= 227 * 1024 && g.grad_cls) {
       if (mb > 48 * 1024) cudaFuncSetAttribute(k_schur_mma<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mb);

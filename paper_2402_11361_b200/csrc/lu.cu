@@ -46,13 +46,6 @@ extern "C" int mhdg_lu4_profile(unsigned long long* out, int reset) {
 #define LUADD(k, v)
 #endif
 
-// 8-byte global -> shared async copy (src_bytes = 0 zero-fills)
-__device__ __forceinline__ void cp_async8(double* dst, const double* src, int src_bytes) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(src_bytes) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-
 namespace lu4 {
 constexpr int NB = 32;       // panel width
 constexpr int SW = 16;       // register sub-panel width
