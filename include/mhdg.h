@@ -180,6 +180,10 @@ void mhdg_set_factor_variant(int v);
    For A/B measurements. */
 void mhdg_set_lu_variant(int v);
 
+/* Panel width of k_lu4: 32 (default; 192 threads, two CTAs per SM) or 64 (one CTA
+   per SM; threads 256 or 384).  For A/B measurements. */
+void mhdg_set_lu_panel(int nb, int threads);
+
 /* Schur-complement kernel: 0 (default) stage-pipelined FP64 tensor-core kernel,
    1 the earlier tensor-core kernel, otherwise the per-macro FFMA kernel.  For A/B
    measurements. */

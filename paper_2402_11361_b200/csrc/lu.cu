@@ -47,11 +47,12 @@ extern "C" int mhdg_lu4_profile(unsigned long long* out, int reset) {
 #endif
 
 namespace lu4 {
-constexpr int NB = 32;       // panel width
 constexpr int SW = 16;       // register sub-panel width
-constexpr int PS = 36;       // panel row stride (= 4 mod 16): conflict-free DMMA A fragments
 constexpr int CW = 16;       // trailing-update column chunk per warp
 constexpr int SWP = SW + 2;  // candidate slot: SW row values, the reciprocal, padding
+// panel row stride for panel width NB (= 4 mod 16): conflict-free DMMA A fragments
+template <int NB>
+constexpr int pstride() { return NB + 4; }
 
 // argmax key: |v| with the low 9 mantissa bits replaced by (511 - row), so the
 // largest key is the largest magnitude, ties (to 2^-43) going to the lowest row
@@ -60,21 +61,22 @@ __device__ __forceinline__ unsigned long long pkey(double v, int r) {
 }
 __device__ __forceinline__ int key_row(unsigned long long k) { return 511 - (int)(k & 0x1FFull); }
 
-template <int NT>
+template <int NB, int NT>
 size_t smem_bytes(int n) {
   constexpr int NW = NT / 32;
-  return sizeof(double) * ((size_t)n * PS + 2 * NW * SWP) + sizeof(unsigned long long) * 2 * NW +
+  return sizeof(double) * ((size_t)n * pstride<NB>() + 2 * NW * SWP) + sizeof(unsigned long long) * 2 * NW +
          sizeof(unsigned short) * 2 * (size_t)n + (size_t)n;
 }
 }  // namespace lu4
 
 // C -= L21 U12 for one 16-column chunk over the m remaining rows (list rl), 16 rows per
 // pass with the next three passes' C in flight.  VEC: 16-byte C accesses (full chunk, even n).
-template <bool VEC>
+template <int NB, bool VEC>
 __device__ __forceinline__ void trail_pass_loop(double* __restrict__ A, int n, int c0, int cw, int m,
                                                 const unsigned short* rl, const double* P, int t4, int g,
-                                                const double (&bf)[lu4::NB / 4][2]) {
+                                                const double (&bf)[NB / 4][2]) {
   using namespace lu4;
+  constexpr int PS = pstride<NB>();
   const int rlast = rl[m - 1];
   auto load = [&](int t, double (&c)[2][2][2], int (&rr)[2], bool (&ok)[2]) {
 #pragma unroll
@@ -145,11 +147,11 @@ __device__ __forceinline__ void trail_pass_loop(double* __restrict__ A, int n, i
   }
 }
 
-template <int NT, int RPT>
-__global__ void __launch_bounds__(NT, 2) k_lu4(int n, double* __restrict__ S, int* __restrict__ piv_out,
-                                               int* status) {
+template <int NB, int NT, int RPT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_lu4(int n, double* __restrict__ S, int* __restrict__ piv_out,
+                                                  int* status) {
   using namespace lu4;
-  constexpr int NW = NT / 32;
+  constexpr int NW = NT / 32, PS = pstride<NB>(), NH = NB / 32;  // NH: 32-column halves of a panel
   extern __shared__ double sm[];
   double* P = sm;                                   // n x PS: the panel, physical rows
   double* cv = P + (size_t)n * PS;                  // [2][NW][SWP] candidate pivot rows
@@ -177,7 +179,11 @@ __global__ void __launch_bounds__(NT, 2) k_lu4(int n, double* __restrict__ S, in
     // ---- panel: the m not-yet-pivoted rows, columns k0 .. k0+nb-1 (zero beyond) ----
     for (int i = warp; i < m; i += NW) {
       const int r = np[i];
-      cp_async8(P + r * PS + lane, A + (size_t)r * n + k0 + (lane < nb ? lane : 0), lane < nb ? 8 : 0);
+#pragma unroll
+      for (int h = 0; h < NH; ++h) {
+        const int c = 32 * h + lane;
+        cp_async8(P + r * PS + c, A + (size_t)r * n + k0 + (c < nb ? c : 0), c < nb ? 8 : 0);
+      }
     }
     cp_async_wait_all();
     __syncthreads();
@@ -276,27 +282,28 @@ __global__ void __launch_bounds__(NT, 2) k_lu4(int n, double* __restrict__ S, in
       LUT(pt2);
       if (js + SW < nb) {
         // (a) U rows of this sub-panel's pivots on the panel's remaining columns
-        if (warp == 0 && lane < nb - js - SW) {
-          const int c = js + SW + lane;
-          double u[SW];
+        if (warp == 0) {
+          for (int c = js + SW + lane; c < nb; c += 32) {
+            double u[SW];
 #pragma unroll
-          for (int jj = 0; jj < SW; ++jj) {
-            const double* pr = P + pv[js + jj] * PS;
-            double v = pr[c];
+            for (int jj = 0; jj < SW; ++jj) {
+              const double* pr = P + pv[js + jj] * PS;
+              double v = pr[c];
 #pragma unroll
-            for (int i = 0; i < jj; ++i) v -= pr[js + i] * u[i];
-            u[jj] = v;
-            P[pv[js + jj] * PS + c] = v;
+              for (int i = 0; i < jj; ++i) v -= pr[js + i] * u[i];
+              u[jj] = v;
+              P[pv[js + jj] * PS + c] = v;
+            }
           }
         }
         __syncthreads();
-        // (b) rank-SW DMMA update of the other rows on columns js+SW .. NB-1
-        {
+        // (b) rank-SW DMMA update of the other rows on columns js+SW .. NB-1, 16 at a time
+        for (int cg = js + SW; cg < NB; cg += 16) {
           double bf[SW / 4][2];
 #pragma unroll
           for (int ks = 0; ks < SW / 4; ++ks)
 #pragma unroll
-            for (int ct = 0; ct < 2; ++ct) bf[ks][ct] = -P[pv[js + 4 * ks + t4] * PS + js + SW + 8 * ct + g];
+            for (int ct = 0; ct < 2; ++ct) bf[ks][ct] = -P[pv[js + 4 * ks + t4] * PS + cg + 8 * ct + g];
           for (int t = warp * 8; t < m; t += NW * 8) {
             const bool ok = t + g < m;
             const int r = np[ok ? t + g : 0];
@@ -306,7 +313,7 @@ __global__ void __launch_bounds__(NT, 2) k_lu4(int n, double* __restrict__ S, in
 #pragma unroll
             for (int ct = 0; ct < 2; ++ct)
 #pragma unroll
-              for (int e = 0; e < 2; ++e) c[ct][e] = pr[js + SW + 8 * ct + 2 * t4 + e];
+              for (int e = 0; e < 2; ++e) c[ct][e] = pr[cg + 8 * ct + 2 * t4 + e];
 #pragma unroll
             for (int ks = 0; ks < SW / 4; ++ks) {
               const double a = pr[js + 4 * ks + t4];
@@ -317,7 +324,7 @@ __global__ void __launch_bounds__(NT, 2) k_lu4(int n, double* __restrict__ S, in
 #pragma unroll
               for (int ct = 0; ct < 2; ++ct)
 #pragma unroll
-                for (int e = 0; e < 2; ++e) pr[js + SW + 8 * ct + 2 * t4 + e] = c[ct][e];
+                for (int e = 0; e < 2; ++e) pr[cg + 8 * ct + 2 * t4 + e] = c[ct][e];
             }
           }
         }
@@ -331,7 +338,9 @@ __global__ void __launch_bounds__(NT, 2) k_lu4(int n, double* __restrict__ S, in
 #pragma unroll 4
     for (int i = warp; i < m; i += NW) {
       const int r = np[i];
-      if (lane < nb) A[(size_t)r * n + k0 + lane] = P[r * PS + lane];
+#pragma unroll
+      for (int h = 0; h < NH; ++h)
+        if (32 * h + lane < nb) A[(size_t)r * n + k0 + 32 * h + lane] = P[r * PS + 32 * h + lane];
     }
     unsigned short* np2 = npl + (lb ^ 1) * n;
     {
@@ -355,24 +364,42 @@ __global__ void __launch_bounds__(NT, 2) k_lu4(int n, double* __restrict__ S, in
       }
     }
     {
-      // inv(L11): warp w forms columns w, w + NW, ... (lane = row), then, once every warp
-      // has read L11, stores them over the pivot rows of the panel (already written back)
+      // inv(L11): warp w forms columns w, w + NW, ... (lane = rows lane + 32 h), then, once
+      // every warp has read L11, stores them over the pivot rows of the panel (written back)
       constexpr int CPW = (NB + NW - 1) / NW;
-      double xc[CPW];
+      double xc[CPW][NH];
 #pragma unroll
-      for (int cc = 0; cc < CPW; ++cc) xc[cc] = (lane == warp + NW * cc && lane < nb) ? 1.0 : 0.0;
-      const int prl = lane < nb ? pv[lane] : 0;
+      for (int cc = 0; cc < CPW; ++cc)
+#pragma unroll
+        for (int h = 0; h < NH; ++h) xc[cc][h] = (32 * h + lane == warp + NW * cc && 32 * h + lane < nb) ? 1.0 : 0.0;
+      int prl[NH];
+#pragma unroll
+      for (int h = 0; h < NH; ++h) prl[h] = 32 * h + lane < nb ? pv[32 * h + lane] : 0;
       for (int k = 0; k < nb - 1; ++k) {
-        const double lik = (lane > k && lane < nb) ? P[prl * PS + k] : 0.0;
+        double lik[NH];
 #pragma unroll
-        for (int cc = 0; cc < CPW; ++cc) xc[cc] -= lik * __shfl_sync(MHDG_FULL, xc[cc], k);
+        for (int h = 0; h < NH; ++h) {
+          const int row = 32 * h + lane;
+          lik[h] = (row > k && row < nb) ? P[prl[h] * PS + k] : 0.0;
+        }
+#pragma unroll
+        for (int cc = 0; cc < CPW; ++cc) {
+          double src = xc[cc][0];
+#pragma unroll
+          for (int h = 1; h < NH; ++h) src = (k >> 5) == h ? xc[cc][h] : src;
+          const double xk = __shfl_sync(MHDG_FULL, src, k & 31);
+#pragma unroll
+          for (int h = 0; h < NH; ++h) xc[cc][h] -= lik[h] * xk;
+        }
       }
       __syncthreads();
-      if (lane < nb) {
 #pragma unroll
-        for (int cc = 0; cc < CPW; ++cc)
-          if (warp + NW * cc < NB) P[prl * PS + warp + NW * cc] = xc[cc];
-      }
+      for (int h = 0; h < NH; ++h)
+        if (32 * h + lane < nb) {
+#pragma unroll
+          for (int cc = 0; cc < CPW; ++cc)
+            if (warp + NW * cc < NB) P[prl[h] * PS + warp + NW * cc] = xc[cc][h];
+        }
     }
     m -= nb;
     lb ^= 1;
@@ -439,9 +466,9 @@ __global__ void __launch_bounds__(NT, 2) k_lu4(int n, double* __restrict__ S, in
       // C -= L21 U12 over the remaining rows, 16 rows per pass, next pass's C prefetched
       if (m > 0) {
         if (cw == CW && (n & 1) == 0)
-          trail_pass_loop<true>(A, n, c0, cw, m, np2, P, t4, g, bf);
+          trail_pass_loop<NB, true>(A, n, c0, cw, m, np2, P, t4, g, bf);
         else
-          trail_pass_loop<false>(A, n, c0, cw, m, np2, P, t4, g, bf);
+          trail_pass_loop<NB, false>(A, n, c0, cw, m, np2, P, t4, g, bf);
       }
     }
     LUADD(4, pt4);
@@ -586,16 +613,32 @@ int pack_lu4(int n, int n_mac, const double* scratch, const int* piv, double* pa
 
 
 
-int lu_factor4(int n, int n_mac, double* scratch, int* piv, double* packed, int* status, cudaStream_t st) {
-  constexpr int NT = 192;
+static int g_lu_nb = 32, g_lu_nt = 0;
+extern "C" void mhdg_set_lu_panel(int nb, int threads) {
+  g_lu_nb = nb == 64 ? 64 : 32;
+  g_lu_nt = threads;
+}
+
+template <int NB, int NT, int MINB>
+static int launch_lu4(int n, int n_mac, double* scratch, int* piv, int* status, cudaStream_t st) {
   if (n > 2 * NT) return -1;
-  const size_t bytes = lu4::smem_bytes<NT>(n);
+  const size_t bytes = lu4::smem_bytes<NB, NT>(n);
   if (bytes > 227 * 1024) return -1;
-  auto kern = n <= NT ? k_lu4<NT, 1> : k_lu4<NT, 2>;
+  auto kern = n <= NT ? k_lu4<NB, NT, 1, MINB> : k_lu4<NB, NT, 2, MINB>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   tl_begin(TL_FACTOR, st);
   kern<<<n_mac, NT, bytes, st>>>(n, scratch, piv, status);
   tl_end(TL_FACTOR, st);
+  return 0;
+}
+
+int lu_factor4(int n, int n_mac, double* scratch, int* piv, double* packed, int* status, cudaStream_t st) {
+  // 32-column panels, two CTAs per SM (one's pivot chain under the other's updates), or
+  // 64-column panels, one CTA per SM (half the trailing-update traffic)
+  const int rc0 = g_lu_nb != 64   ? launch_lu4<32, 192, 2>(n, n_mac, scratch, piv, status, st)
+                  : g_lu_nt == 384 ? launch_lu4<64, 384, 1>(n, n_mac, scratch, piv, status, st)
+                                   : launch_lu4<64, 256, 1>(n, n_mac, scratch, piv, status, st);
+  if (rc0 < 0) return -1;
   int rc = launch_ok();
   if (rc) return rc;
   return pack_lu4(n, n_mac, scratch, piv, packed, st);

@@ -19,10 +19,13 @@ f.q = A.gradient_refresh(disc, f.u, f.uhat)
 blocks, _ = A.jacobian(disc, f, A.StageContext.steady(1.0))
 x = torch.randn(disc.n_trace, dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(0))
 out = {}
-for label, kind, var in (("inverse", "inverse", 0), ("lu3", "lu", 3), ("lu4", "lu", 4), ("lu4b", "lu", 4)):
+VARIANTS = (("inverse", "inverse", 0, 32, 0), ("lu3", "lu", 3, 32, 0), ("lu4", "lu", 4, 32, 0),
+            ("lu4b", "lu", 4, 32, 0), ("lu4_64x256", "lu", 4, 64, 256), ("lu4_64x384", "lu", 4, 64, 384))
+for label, kind, var, nb, nt in VARIANTS:
     CD.FACTOR = kind
     if var:
         L.mhdg_set_lu_variant(var)
+        L.mhdg_set_lu_panel(nb, nt)
     cond = CD.CondensedSchur.allocate(blocks)
     st = disc.device.status_buffer()
     cond.refactor_async(st)
@@ -50,3 +53,4 @@ ref = out["inverse"]
 for k, v in out.items():
     print(f"{k}: vs inverse rel diff {float((v - ref).abs().max() / ref.abs().max()):.2e}")
 print("lu4 run-to-run equal:", bool(torch.equal(out["lu4"], out["lu4b"])))
+L.mhdg_set_lu_panel(32, 0)
