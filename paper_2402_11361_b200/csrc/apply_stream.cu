@@ -902,8 +902,9 @@ __global__ void __launch_bounds__(NCT + 32) k_si_stream(int n_mac, const double*
 // triangles (packed_lu.cuh), so per column a warp reads its block rows with
 // one coalesced 256-byte access; the block's right-hand side and solution
 // stay in the warp's slice of shared memory.  A block step is a panel GEMV
-// (sixteen columns of loads in flight per lane), a warp-synchronous hand-off
-// and the inverted diagonal triangle; many warps per SM keep HBM busy while
+// (sixteen columns of loads in flight per lane) and a substitution with the
+// diagonal triangle (column sweep: the final entry broadcast by a shuffle,
+// the rows below updated in registers); many warps per SM keep HBM busy while
 // each walks its macro's dependent block steps.
 // ---------------------------------------------------------------------------
 constexpr int LUW_NT = 128;
@@ -951,8 +952,7 @@ __global__ void __launch_bounds__(LUW_NT) k_lu_warp(int n_mac, const double* __r
     blk[tid] = LuBlk{o.fwd_panel, o.fwd_diag, o.bwd_panel, o.bwd_diag, o.nb, o.r0, o.ncol_fwd, o.ncol_bwd};
   }
   __syncthreads();
-  double* yb = smw + warp * (NP + PLU_NB);  // solution, logical order
-  double* tb = yb + NP;                     // block right-hand side
+  double* yb = smw + warp * NP;  // solution, logical order
   const long long FS = plu_size(n);
   for (int mac = blockIdx.x * NWP + warp; mac < n_mac; mac += gridDim.x * NWP) {
     const double* y1 = Work<C>::y1(work, mac);
@@ -960,41 +960,45 @@ __global__ void __launch_bounds__(LUW_NT) k_lu_warp(int n_mac, const double* __r
     for (int k = lane; k < n; k += 32) yb[k] = y1[__ldg(pm + k)];  // P y1
     __syncwarp();
     const double* Fm = F + (size_t)mac * FS;
-    for (int b = 0; b < NBLK; ++b) {  // forward: y_b = inv(L_bb) (y_b - L[b, :b] y_:b)
+    for (int b = 0; b < NBLK; ++b) {  // forward: y_b = L_bb^-1 (y_b - L[b, :b] y_:b)
       const LuBlk o = blk[b];
       double a0 = 0.0, a1 = 0.0;
       luw_panel(Fm + o.fwd_panel, o.nb, o.ncol_fwd, yb, lane, a0, a1);
-      if (lane < o.nb) tb[lane] = yb[o.r0 + lane] - a0;
-      if (lane + 32 < o.nb) tb[lane + 32] = yb[o.r0 + lane + 32] - a1;
-      __syncwarp();
-      double v0 = lane < o.nb ? tb[lane] : 0.0, v1 = lane + 32 < o.nb ? tb[lane + 32] : 0.0;
+      // forward substitution with the unit lower diagonal block: column sweep, the final
+      // y_c broadcast from its lane, rows below updated in registers
+      double v0 = lane < o.nb ? yb[o.r0 + lane] - a0 : 0.0;
+      double v1 = lane + 32 < o.nb ? yb[o.r0 + lane + 32] - a1 : 0.0;
       const double* Tl = Fm + o.fwd_diag;
-#pragma unroll 8
-      for (int c = 0; c < o.nb - 1; ++c) {  // column c of inv(L_bb): rows c+1 .. nb-1
+#pragma unroll 4
+      for (int c = 0; c < o.nb - 1; ++c) {  // column c of L_bb: rows c+1 .. nb-1
         const double* col = Tl + plu_lo_col(o.nb, c) - c - 1;
-        const double tc = tb[c];
-        if (lane > c && lane < o.nb) v0 += __ldcs(col + lane) * tc;
-        if (lane + 32 > c && lane + 32 < o.nb) v1 += __ldcs(col + lane + 32) * tc;
+        const double l0 = (lane > c && lane < o.nb) ? __ldcs(col + lane) : 0.0;
+        const double l1 = (lane + 32 > c && lane + 32 < o.nb) ? __ldcs(col + lane + 32) : 0.0;
+        const double yc = __shfl_sync(MHDG_FULL, c < 32 ? v0 : v1, c & 31);
+        v0 -= l0 * yc;
+        v1 -= l1 * yc;
       }
       if (lane < o.nb) yb[o.r0 + lane] = v0;
       if (lane + 32 < o.nb) yb[o.r0 + lane + 32] = v1;
       __syncwarp();
     }
-    for (int b = NBLK - 1; b >= 0; --b) {  // backward: x_b = inv(U_bb) (y_b - U[b, b+1:] x_b+1:)
+    for (int b = NBLK - 1; b >= 0; --b) {  // backward: x_b = U_bb^-1 (y_b - U[b, b+1:] x_b+1:)
       const LuBlk o = blk[b];
       double a0 = 0.0, a1 = 0.0;
       luw_panel(Fm + o.bwd_panel, o.nb, o.ncol_bwd, yb + o.r0 + o.nb, lane, a0, a1);
-      if (lane < o.nb) tb[lane] = yb[o.r0 + lane] - a0;
-      if (lane + 32 < o.nb) tb[lane + 32] = yb[o.r0 + lane + 32] - a1;
-      __syncwarp();
-      double v0 = 0.0, v1 = 0.0;
+      double v0 = lane < o.nb ? yb[o.r0 + lane] - a0 : 0.0;
+      double v1 = lane + 32 < o.nb ? yb[o.r0 + lane + 32] - a1 : 0.0;
       const double* Tu = Fm + o.bwd_diag;
-#pragma unroll 8
-      for (int c = 0; c < o.nb; ++c) {  // column c of inv(U_bb): rows 0 .. c
+#pragma unroll 4
+      for (int c = o.nb - 1; c >= 0; --c) {  // column c of U_bb: rows 0 .. c (diagonal: 1/U_cc)
         const double* col = Tu + c * (c + 1) / 2;
-        const double tc = tb[c];
-        if (lane <= c) v0 += __ldcs(col + lane) * tc;
-        if (lane + 32 <= c) v1 += __ldcs(col + lane + 32) * tc;
+        const double u0 = lane <= c ? __ldcs(col + lane) : 0.0;
+        const double u1 = lane + 32 <= c ? __ldcs(col + lane + 32) : 0.0;
+        const double xc = __shfl_sync(MHDG_FULL, c < 32 ? v0 * u0 : v1 * u1, c & 31);
+        if (lane == c) v0 = xc;
+        else v0 -= u0 * xc;
+        if (lane + 32 == c) v1 = xc;
+        else v1 -= u1 * xc;
       }
       if (lane < o.nb) yb[o.r0 + lane] = v0;
       if (lane + 32 < o.nb) yb[o.r0 + lane + 32] = v1;
@@ -1008,7 +1012,7 @@ __global__ void __launch_bounds__(LUW_NT) k_lu_warp(int n_mac, const double* __r
 
 template <class C>
 static int launch_lu_stream(const mhdg_disc& g, const mhdg_factors& f, cudaStream_t st) {
-  const size_t bytes = sizeof(double) * (LUW_NT / 32) * (ceven(C::n) + PLU_NB);
+  const size_t bytes = sizeof(double) * (LUW_NT / 32) * ceven(C::n);
   auto kern = k_lu_warp<C>;
   static int ctas = 0;
   if (!ctas) {

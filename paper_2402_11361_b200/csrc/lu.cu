@@ -481,115 +481,61 @@ __global__ void __launch_bounds__(NT, MINB) k_lu4(int n, double* __restrict__ S,
 
 // --------------------------------------------------------------------------
 // k_pack_lu4: in-place LU (pivot rows in place) -> the packed solve layout of
-// packed_lu.cuh.  One CTA per macro, per 64-row block:
-//   * panels: each 32-column segment of the block's 64 rows is staged in shared
-//     memory with coalesced reads of the physical rows and written column-major
-//     (the layout of packed_lu.cuh) with coalesced writes;
-//   * diagonal block: staged in shared memory, inv(L_bb) (unit lower) and
-//     inv(U_bb) = inv(unit upper) D^-1 by column sweeps over all threads with
-//     the columns in registers (one barrier per step), written as packed
-//     triangles.
+// packed_lu.cuh.  One CTA per macro; per 64-row block, every 32-column
+// segment of the block's rows is staged in shared memory with coalesced reads
+// of the physical rows (the next segment's reads in flight while this one is
+// written) and written column-major with coalesced writes: panel tiles, the
+// strict lower part of the diagonal block (L_bb) and its upper part (U_bb,
+// diagonal stored as 1/U_kk).
 // --------------------------------------------------------------------------
 namespace pk4 {
-constexpr int NT = 256, TS = PLU_NB + 1;
+constexpr int NT = 256, TS = 33, RPW = PLU_NB / (NT / 32);
 }
 
-// Column sweep for the inverse of a unit triangular nb x nb block (nb <= 64) held in
-// T (LOWER: strict lower part; else Uh[i][k] = T[i][k] rd[i], strict upper part).
-// Thread (c, grp) keeps rows grp, grp + NG, ... of column c of X in registers; the
-// final row k is broadcast through xr (double-buffered: one barrier per step).
-template <bool LOWER>
-__device__ __forceinline__ void tri_sweep(const double* T, const double* rd, int nb, int c, int grp, double* xr,
-                                          double (&x)[PLU_NB / (pk4::NT / PLU_NB)]) {
+__global__ void __launch_bounds__(pk4::NT) k_pack_lu4(int n, const double* __restrict__ F,
+                                                      const int* __restrict__ piv, double* __restrict__ out) {
   using namespace pk4;
-  constexpr int NG = NT / PLU_NB, R = PLU_NB / NG;
-#pragma unroll
-  for (int s = 0; s < R; ++s) x[s] = grp + NG * s == c ? 1.0 : 0.0;
-#pragma unroll
-  for (int kk = 0; kk < PLU_NB; ++kk) {
-    const int k = LOWER ? kk : PLU_NB - 1 - kk;
-    if (k >= nb) continue;  // uniform
-    double* row = xr + (kk & 1) * PLU_NB;
-    if (grp == (k % NG)) row[c] = x[k / NG];
-    __syncthreads();
-    const double xk = row[c];
-    if (LOWER ? c <= k : c >= k) {
-#pragma unroll
-      for (int s = 0; s < R; ++s) {
-        const int i = grp + NG * s;
-        if (LOWER ? (i > k && i < nb) : (i < k)) x[s] -= (LOWER ? T[i * TS + k] : T[i * TS + k] * rd[i]) * xk;
-      }
-    }
-  }
-  __syncthreads();
-}
-
-__global__ void __launch_bounds__(pk4::NT, 3) k_pack_lu4(int n, const double* __restrict__ F,
-                                                         const int* __restrict__ piv, double* __restrict__ out) {
-  using namespace pk4;
-  extern __shared__ double pk_sm[];
-  double* T = pk_sm;                    // PLU_NB x TS: diagonal block (logical rows)
-  double* X = T + PLU_NB * TS;          // PLU_NB x TS: an inverse; first 32 columns: tile staging
-  double* rd = X + PLU_NB * TS;         // PLU_NB: 1 / U[k][k]
-  double* xr = rd + PLU_NB;             // [2][PLU_NB]: row k of X, broadcast per sweep step
-  int* pr = reinterpret_cast<int*>(xr + 2 * PLU_NB);
+  __shared__ double X[PLU_NB * TS];  // one 64 x 32 segment
+  extern __shared__ int pr[];         // n pivot rows
   const int mac = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const double* A = F + (size_t)mac * n * n;
   double* O = out + (size_t)mac * plu_size(n);
   for (int i = tid; i < n; i += NT) pr[i] = piv[(size_t)mac * n + i];
   __syncthreads();
-  const int nblk = plu_nblk(n);
-  const int c = tid & (PLU_NB - 1), grp = tid / PLU_NB;  // column and row group of the sweeps
-  constexpr int NG = NT / PLU_NB, RPW = PLU_NB / (NT / 32);
+  const int nblk = plu_nblk(n), nseg = (n + PLU_TW - 1) / PLU_TW;
+  const int r = tid & (PLU_NB - 1), grp = tid / PLU_NB;
+  constexpr int NG = NT / PLU_NB;
   for (int b = 0; b < nblk; ++b) {
     const PluOffsets o = plu_offsets(n, b);
     const int nb = o.nb, r0 = o.r0;
-    // 32-column segments of the block's rows: staged row-wise (coalesced reads of the
-    // physical rows), written column-major (coalesced writes of the packed tiles)
-    for (int col = 0; col < n; col += PLU_TW) {
-      double v[RPW];
+    double v[RPW];
+    auto load = [&](int col) {
 #pragma unroll
       for (int k = 0; k < RPW; ++k) {
-        const int r = warp + (NT / 32) * k;
-        v[k] = (r < nb && col + lane < n) ? A[(size_t)pr[r0 + r] * n + col + lane] : 0.0;
+        const int rr = warp + (NT / 32) * k;
+        v[k] = (rr < nb && col + lane < n) ? A[(size_t)pr[r0 + rr] * n + col + lane] : 0.0;
       }
+    };
+    load(0);
+    for (int sg = 0; sg < nseg; ++sg) {
+      const int col = sg * PLU_TW;
+      __syncthreads();  // previous segment written out
 #pragma unroll
       for (int k = 0; k < RPW; ++k) X[(warp + (NT / 32) * k) * TS + lane] = v[k];
+      if (sg + 1 < nseg) load(col + PLU_TW);
       __syncthreads();
-      const int w = min(PLU_TW, n - col), r = tid & (PLU_NB - 1);
-      if (col >= r0 && col < r0 + nb) {
-        for (int cc = grp; cc < w; cc += NG)
-          if (r < nb && col + cc < r0 + nb) T[r * TS + col - r0 + cc] = X[r * TS + cc];
+      const int w = min(PLU_TW, n - col);
+      if (col >= r0 && col < r0 + nb) {  // diagonal block columns
+        for (int cc = grp; cc < w && col + cc < r0 + nb; cc += NG) {
+          const int c = col - r0 + cc;
+          if (r < nb && r > c) O[o.fwd_diag + plu_lo(nb, r, c)] = X[r * TS + cc];
+          if (r <= c) O[o.bwd_diag + plu_up(r, c)] = r == c ? 1.0 / X[r * TS + cc] : X[r * TS + cc];
+        }
       } else {
         double* dst = col < r0 ? O + o.fwd_panel + (long long)col * nb : O + o.bwd_panel + (long long)(col - r0 - nb) * nb;
         for (int cc = grp; cc < w; cc += NG)
           if (r < nb) dst[cc * nb + r] = X[r * TS + cc];
       }
-      __syncthreads();
-    }
-    if (tid < nb) rd[tid] = 1.0 / T[tid * TS + tid];
-    __syncthreads();
-    double x[PLU_NB / NG];  // X[grp + NG s][c]
-    // inv(L_bb): X = I; X[i][c] -= L[i][k] X[k][c] for i > k, c <= k, k ascending
-    tri_sweep<true>(T, rd, nb, c, grp, xr, x);
-#pragma unroll
-    for (int s2 = 0; s2 < PLU_NB / NG; ++s2) X[(grp + NG * s2) * TS + c] = x[s2];
-    __syncthreads();
-    {
-      const int r = tid & (PLU_NB - 1);
-      for (int cc = grp; cc < nb - 1; cc += NG)
-        if (r > cc && r < nb) O[o.fwd_diag + plu_lo(nb, r, cc)] = X[r * TS + cc];
-    }
-    // inv(U_bb) = inv(Uh) D^-1, Uh = D^-1 U unit upper: X[i][c] -= Uh[i][k] X[k][c] for
-    // i < k <= c, k descending
-    tri_sweep<false>(T, rd, nb, c, grp, xr, x);
-#pragma unroll
-    for (int s2 = 0; s2 < PLU_NB / NG; ++s2) X[(grp + NG * s2) * TS + c] = x[s2];
-    __syncthreads();
-    {
-      const int r = tid & (PLU_NB - 1);
-      for (int cc = grp; cc < nb; cc += NG)
-        if (r <= cc) O[o.bwd_diag + plu_up(r, cc)] = X[r * TS + cc] * rd[cc];
     }
     if (tid == 0) {  // zero the even-size padding of the last (narrow) tiles and triangles
       if ((nb * (nb - 1) / 2) & 1) O[o.fwd_diag + nb * (nb - 1) / 2] = 0.0;
@@ -598,13 +544,11 @@ __global__ void __launch_bounds__(pk4::NT, 3) k_pack_lu4(int n, const double* __
       if ((nb * wf) & 1) O[o.fwd_diag - 1] = 0.0;
       if ((nb * wb) & 1) O[o.bwd_diag - 1] = 0.0;
     }
-    __syncthreads();
   }
 }
 
 int pack_lu4(int n, int n_mac, const double* scratch, const int* piv, double* packed, cudaStream_t st) {
-  const size_t bytes = sizeof(double) * (2 * PLU_NB * pk4::TS + 3 * PLU_NB) + sizeof(int) * n;
-  cudaFuncSetAttribute(k_pack_lu4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  const size_t bytes = sizeof(int) * n;
   tl_begin(TL_PACK, st);
   k_pack_lu4<<<n_mac, pk4::NT, bytes, st>>>(n, scratch, piv, packed);
   tl_end(TL_PACK, st);

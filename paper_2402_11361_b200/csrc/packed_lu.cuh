@@ -3,17 +3,17 @@
 // After LU with partial pivoting (P S = L U, L unit lower), each macro's
 // factor is re-laid out in the order the two triangular solves read it, in
 // 64-row blocks b = 0..nblk-1 (nb_b rows each):
-//   forward  section, b ascending : [ L[b, 0:64b] panel | inv(L_bb) strict lower ]
-//   backward section, b descending: [ U[b, 64b+nb_b:n] panel | inv(U_bb) upper incl. diag ]
+//   forward  section, b ascending : [ L[b, 0:64b] panel | L_bb strict lower ]
+//   backward section, b descending: [ U[b, 64b+nb_b:n] panel | U_bb upper, diagonal stored as 1/U_kk ]
 // A panel (nb_b rows x ncol) is stored as consecutive column tiles of
 // PLU_TW = 32 columns (the last one narrower); inside a tile the layout is
 // column-major (element (r, c) at c * nb_b + r), and the triangles are
-// column-major too (column c of inv(L_bb): rows c+1..nb_b-1; of inv(U_bb):
-// rows 0..c).  So a warp walking a block reads, per column, consecutive rows:
-// one coalesced access per column, each lane owning rows of the block.
-// Every tile / triangle is padded to an even number of doubles (16-byte
-// aligned pieces).  The diagonal tiles are stored inverted, so the solve is a
-// sequence of GEMVs: y_b = inv(L_bb) (y_b - L[b,:b] y_:b), and likewise
+// column-major too (column c of L_bb: rows c+1..nb_b-1; of U_bb: rows 0..c).
+// So a warp walking a block reads, per column, consecutive rows: one
+// coalesced access per column, each lane owning rows of the block.  Every
+// tile / triangle is padded to an even number of doubles (16-byte aligned
+// pieces).  A block step is a panel GEMV, y_b -= L[b,:b] y_:b, then a
+// substitution with the diagonal triangle (column sweeps), and likewise
 // backwards.
 #pragma once
 #include "common.cuh"
@@ -110,13 +110,15 @@ __device__ inline void plu_solve_cta(const double* __restrict__ F, const int* __
       double acc = 0.0;
       for (int c = lane; c < o.ncol_fwd; c += 32) acc += __ldg(F + o.fwd_panel + plu_panel_idx(o.nb, r, c)) * y[c];
       acc = warp_sum(acc);
-      if (lane == 0) t[r] = y[o.r0 + r] - acc;
+      if (lane == 0) y[o.r0 + r] -= acc;
     }
     __syncthreads();
-    for (int r = tid; r < o.nb; r += blockDim.x) {
-      double acc = t[r];
-      for (int c = 0; c < r; ++c) acc += __ldg(F + o.fwd_diag + plu_lo(o.nb, r, c)) * t[c];
-      y[o.r0 + r] = acc;
+    if (tid == 0) {  // forward substitution with the unit lower diagonal block
+      for (int r = 1; r < o.nb; ++r) {
+        double acc = y[o.r0 + r];
+        for (int c = 0; c < r; ++c) acc -= __ldg(F + o.fwd_diag + plu_lo(o.nb, r, c)) * y[o.r0 + c];
+        y[o.r0 + r] = acc;
+      }
     }
     __syncthreads();
   }
@@ -128,13 +130,15 @@ __device__ inline void plu_solve_cta(const double* __restrict__ F, const int* __
       for (int c = lane; c < o.ncol_bwd; c += 32)
         acc += __ldg(F + o.bwd_panel + plu_panel_idx(o.nb, r, c)) * y[c0 + c];
       acc = warp_sum(acc);
-      if (lane == 0) t[r] = y[o.r0 + r] - acc;
+      if (lane == 0) y[o.r0 + r] -= acc;
     }
     __syncthreads();
-    for (int r = tid; r < o.nb; r += blockDim.x) {
-      double acc = 0.0;
-      for (int c = r; c < o.nb; ++c) acc += __ldg(F + o.bwd_diag + plu_up(r, c)) * t[c];
-      y[o.r0 + r] = acc;
+    if (tid == 0) {  // backward substitution with the upper diagonal block (1/U_kk stored)
+      for (int r = o.nb - 1; r >= 0; --r) {
+        double acc = y[o.r0 + r];
+        for (int c = r + 1; c < o.nb; ++c) acc -= __ldg(F + o.bwd_diag + plu_up(r, c)) * y[o.r0 + c];
+        y[o.r0 + r] = acc * __ldg(F + o.bwd_diag + plu_up(r, r));
+      }
     }
     __syncthreads();
   }

@@ -60,10 +60,13 @@ def test_ptc_couette_vs_reference():
     assert rel_err(host(f.uhat), g["uhat"]) < 1e-8
 
 
-def test_c1_plane_couette_ptc_vs_oracle():
+@pytest.mark.parametrize("kind", ["lu", "inverse"])
+def test_c1_plane_couette_ptc_vs_oracle(kind):
     """BASELINE configs[0] (C1) end to end on the device: PTC + FGMRES to 1e-10
-    from the seeded IC, against the oracle's run (oracle/make_c1_golden.py)."""
+    from the seeded IC, against the oracle's run (oracle/make_c1_golden.py), with the
+    packed-LU (default) and explicit-inverse condensation factors."""
     need_gpu()
+    from paper_2402_11361_b200 import condense as CD
     from paper_2402_11361_b200.cases import CouettePlane2D
     from paper_2402_11361_b200.mesh import build_square_mesh
 
@@ -72,9 +75,28 @@ def test_c1_plane_couette_ptc_vs_oracle():
     mesh = build_square_mesh(case.domain, (8, 4), 2, periodic=(True, False))
     d = Discretization(mesh, 2, case.params, bcs=case.boundary_conditions())
     f = A.to_device_fields(d, g["u0"], g["q0"], g["uhat0"])
-    st, _ = S.ptc_steady_solve(d, f, rel_tol=1e-10)
-    assert abs(st.iterations - int(g["newton"])) <= 1  # measured: 8 vs 8
-    assert abs(st.krylov_iterations - int(g["krylov"])) <= 1  # measured: 2879 vs 2879
+    old = CD.FACTOR
+    try:
+        CD.FACTOR = kind
+        st, _ = S.ptc_steady_solve(d, f, rel_tol=1e-10)
+    finally:
+        CD.FACTOR = old
+    # The first Newton residuals agree with the oracle's to 3 digits; from the fourth on the
+    # PTC trajectory differs by the FGMRES truncation (~2% per step, in both device factor
+    # kinds), so the step that crosses the 1e-10 target can move by one.  Measured: inverse
+    # 8 Newton / 2879 FGMRES (oracle 8 / 2879); LU 7 / 2479 (residual 3.4e-10 -> 8.3e-11 at
+    # step 7 vs the oracle's 5.6e-10 -> 1.4e-10), i.e. one Newton step and its ~400 FGMRES
+    # iterations fewer.
+    for a, b in zip(st.residuals[:3], g["residuals"][:3]):
+        assert abs(a - b) <= 1e-3 * b
+    assert abs(st.iterations - int(g["newton"])) <= 1
+    if kind == "inverse":
+        assert abs(st.krylov_iterations - int(g["krylov"])) <= 1
+    else:
+        # at most one Newton step's FGMRES iterations apart (a late PTC step takes ~400,
+        # 1.25x the run's average of 360)
+        per_step = 1.25 * int(g["krylov"]) / int(g["newton"])
+        assert abs(st.krylov_iterations - int(g["krylov"])) <= per_step * abs(st.iterations - int(g["newton"])) + 1
     assert st.residuals[-1] <= max(1e-10, 1e-10 * st.residuals[0])  # ptc_steady_solve's target (abs_tol 1e-10)
     # Steady Couette between isothermal walls in a periodic channel fixes velocity and
     # temperature but not the pressure/density level (PTC does not conserve mass, so
@@ -92,8 +114,8 @@ def test_c1_plane_couette_ptc_vs_oracle():
     rho_d, v_d, T_d = prim(host(f.u))
     rho_o, v_o, T_o = prim(g["u"])
     assert rel_err(T_d, T_o) < 1e-8  # measured 1.1e-9
-    ratio = rho_d / rho_o  # measured: uniform offset -3.7e-7, spread 3.3e-10
-    assert ratio.std() < 1e-9 * ratio.mean()
+    ratio = rho_d / rho_o  # measured: uniform offset -3.7e-7, spread 3.3e-10 (inverse), 1.0e-9 (LU:
+    assert ratio.std() < 5e-9 * ratio.mean()  # stops one step earlier, residual 8.3e-11)
     # the weakly determined density level leaks into v = m / rho at the 1e-8 level (measured 1.6e-8)
     assert np.abs(v_d - v_o).max() < 5e-8 * np.abs(v_o).max()
     of = O.Fields(host(f.u), host(f.q), host(f.uhat))
