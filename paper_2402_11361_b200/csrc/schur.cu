@@ -26,8 +26,15 @@ struct Sch2 {
   static constexpr int NS = D + 2, NW = D * D * NS * NS, NWF = D * NS * NS;
   static constexpr int NT = D == 2 ? 12 : 5;   // n-tiles: L <= 8 NT
   static constexpr int KS = D == 2 ? 8 : 21;   // k-steps: nq D <= 4 KS
-  static constexpr int NWARP = D == 2 ? 8 : 16;
-  static constexpr int MINB = D == 2 ? 2 : 1;  // CTAs per SM the registers are budgeted for
+#ifndef MHDG_SCHUR3_NBUF
+#define MHDG_SCHUR3_NBUF 1
+#endif
+  // 2D: two stage buffers (stage i+1 streams in during stage i), 8 warps, 2 CTAs per SM;
+  // 3D: one stage buffer (a 3D stash is 48 KB) so two CTAs share an SM and cover each
+  // other's loads
+  static constexpr int NBUF = D == 2 ? 2 : MHDG_SCHUR3_NBUF;
+  static constexpr int NWARP = (D == 2 || NBUF == 1) ? 8 : 16;
+  static constexpr int MINB = (D == 2 || NBUF == 1) ? 2 : 1;  // CTAs per SM the registers are budgeted for
 };
 
 struct Sch2Dims {
@@ -44,11 +51,14 @@ struct Sch2Dims {
     while (d.LP % 16 != 4) d.LP += 4;
     const int wv = g.nq * C::NW, wf = g.nqf * C::NWF;
     d.wmax = ((wv > wf ? wv : wf) + 1) & ~1;
-    d.stage = d.wmax + 4 * C::KS * d.LP;
+    // + padding: the last B fragments of a row read up to 8 NT - LP columns past it
+    // (columns >= L are never stored; the padding is zero)
+    d.stage = d.wmax + 4 * C::KS * d.LP + 8 * C::NT;
     d.ngph = (g.n_grad_cls * g.nq * g.nloc * D + 1) & ~1;
     return d;
   }
-  size_t smem_bytes() const { return sizeof(double) * ((size_t)ngph + 2 * (size_t)stage); }
+  template <int D>
+  size_t smem_bytes() const { return sizeof(double) * ((size_t)ngph + Sch2<D>::NBUF * (size_t)stage); }
 };
 
 template <int D>
@@ -74,7 +84,7 @@ __global__ void __launch_bounds__(Sch2<D>::NWARP * 32, Sch2<D>::MINB) k_schur2(m
 
   auto prefetch = [&](int i) {
     if (i >= nstage) return;
-    double* W = stg + (size_t)(i & 1) * dm.stage;
+    double* W = stg + (size_t)(i % C::NBUF) * dm.stage;
     double* PM = W + dm.wmax;
     const double* wsrc;
     const double* psrc;
@@ -99,7 +109,7 @@ __global__ void __launch_bounds__(Sch2<D>::NWARP * 32, Sch2<D>::MINB) k_schur2(m
   };
 
   // PM padding (rows >= kv, columns >= L) must be finite: zero both stages once
-  for (int e = tid; e < 2 * dm.stage; e += NT_THREADS) stg[e] = 0.0;
+  for (int e = tid; e < C::NBUF * dm.stage; e += NT_THREADS) stg[e] = 0.0;
   __syncthreads();
   prefetch(0);
   // physical gradients per class (geometry folded in once per macro)
@@ -112,11 +122,15 @@ __global__ void __launch_bounds__(Sch2<D>::NWARP * 32, Sch2<D>::MINB) k_schur2(m
   }
 
   for (int i = 0; i < nstage; ++i) {
+    if (C::NBUF == 1 && i > 0) {
+      __syncthreads();  // stage i-1 consumed: its buffer takes stage i
+      prefetch(i);
+    }
     cp_async_wait_all();
     __syncthreads();  // stage i landed; stage i-1 consumed (its buffer is free)
-    prefetch(i + 1);
+    if (C::NBUF > 1) prefetch(i + 1);
     const bool vol = i < nvol;
-    double* W = stg + (size_t)(i & 1) * dm.stage;
+    double* W = stg + (size_t)(i % C::NBUF) * dm.stage;
     const double* PM = W + dm.wmax;
     {  // fold inv_jac into the stash in place: W'[..(k, r')..] = sum_l ij[r'][l] W[..(k, l)..]
       const int ngrp = (vol ? nq * D : nqf) * NS * NS;
@@ -140,41 +154,57 @@ __global__ void __launch_bounds__(Sch2<D>::NWARP * 32, Sch2<D>::MINB) k_schur2(m
     const int kdim = vol ? dm.kv : dm.kf, nks = vol ? dm.ksv : dm.ksf;
     const int K = i, fT = i - nvol, f = fT / (g.n_tri > 0 ? g.n_tri : 1), T = fT - f * g.n_tri;
     const int cls = vol ? __ldg(g.grad_cls_of + K) : 0;
-    for (int mt = warp; mt * 8 < rows; mt += NWP) {
+    // S row of an 8-row tile's output row, and where its accumulators start from
+    struct Row {
+      double* srow;
+      const double* crow;
+      int a, s, r;
+      bool ok;
+    };
+    auto row_of = [&](int mt) {
+      Row q;
       const int m = mt * 8 + g8;
-      const bool mok = m < rows;
-      const int a = mok ? m / (NS * NS) : 0, s = (m / NS) % NS, r = m % NS;
-      // S row of this thread's output row, and where its accumulators start from
+      q.ok = m < rows;
+      q.a = q.ok ? m / (NS * NS) : 0;
+      q.s = (m / NS) % NS;
+      q.r = m % NS;
       int node;
       bool first = false;
       if (vol) {
-        node = __ldg(g.sub_conn + K * nloc + a);
+        node = __ldg(g.sub_conn + K * nloc + q.a);
         first = __ldg(g.vn_sub + __ldg(g.vn_ptr + node)) / nloc == K;
       } else {
-        node = __ldg(g.face_vol_nodes + f * g.Lf + __ldg(g.tri_conn + T * nlocf + a));
+        node = __ldg(g.face_vol_nodes + f * g.Lf + __ldg(g.tri_conn + T * nlocf + q.a));
       }
-      double* srow = Sm + (size_t)(node * NS + s) * n + r;
-      const double* crow = first ? SSm + (size_t)(node * NS + s) * n + r : srow;
-      double c[NT][2];
+      q.srow = Sm + (size_t)(node * NS + q.s) * n + q.r;
+      q.crow = first ? SSm + (size_t)(node * NS + q.s) * n + q.r : q.srow;
+      return q;
+    };
+    auto load_c = [&](const Row& q, double (&c)[NT][2]) {
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
         const int j0 = nt * 8 + 2 * t4;
-        c[nt][0] = (mok && j0 < L) ? crow[j0 * NS] : 0.0;
-        c[nt][1] = (mok && j0 + 1 < L) ? crow[(j0 + 1) * NS] : 0.0;
+        c[nt][0] = (q.ok && j0 < L) ? q.crow[j0 * NS] : 0.0;
+        c[nt][1] = (q.ok && j0 + 1 < L) ? q.crow[(j0 + 1) * NS] : 0.0;
       }
+    };
+    for (int mt = warp; mt * 8 < rows; mt += NWP) {
+      const Row q = row_of(mt);
+      double c[NT][2];
+      load_c(q, c);
       // A fragments of this row: T1[m][(q, r') = 4 ks + t4]
       double af[KS];
       if (vol) {
-        const double* gp = gph + (size_t)(cls * nq) * nloc * D + a * D;
-        const double* w = W + (s * NS + r);
+        const double* gp = gph + (size_t)(cls * nq) * nloc * D + q.a * D;
+        const double* w = W + (q.s * NS + q.r);
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks) {
           const int kq = 4 * ks + t4;
           double v = 0.0;
-          if (mok && ks < nks && kq < kdim) {
-            const int q = kq / D, rp = kq - q * D;
-            const double* gq = gp + (size_t)q * nloc * D;
-            const double* wq = w + (size_t)q * NW + rp * NS * NS;
+          if (q.ok && ks < nks && kq < kdim) {
+            const int qq = kq / D, rp = kq - qq * D;
+            const double* gq = gp + (size_t)qq * nloc * D;
+            const double* wq = w + (size_t)qq * NW + rp * NS * NS;
 #pragma unroll
             for (int k = 0; k < D; ++k) v += gq[k] * wq[k * D * NS * NS];
           }
@@ -185,9 +215,9 @@ __global__ void __launch_bounds__(Sch2<D>::NWARP * 32, Sch2<D>::MINB) k_schur2(m
         for (int ks = 0; ks < KS; ++ks) {
           const int kq = 4 * ks + t4;
           double v = 0.0;
-          if (mok && ks < nks && kq < kdim) {
-            const int q = kq / D, rp = kq - q * D;
-            v = -W[((q * D + rp) * NS + s) * NS + r] * __ldg(g.phi_face + q * nlocf + a);
+          if (q.ok && ks < nks && kq < kdim) {
+            const int qq = kq / D, rp = kq - qq * D;
+            v = -W[((qq * D + rp) * NS + q.s) * NS + q.r] * __ldg(g.phi_face + qq * nlocf + q.a);
           }
           af[ks] = v;
         }
@@ -202,8 +232,8 @@ __global__ void __launch_bounds__(Sch2<D>::NWARP * 32, Sch2<D>::MINB) k_schur2(m
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
         const int j0 = nt * 8 + 2 * t4;
-        if (mok && j0 < L) srow[j0 * NS] = c[nt][0];
-        if (mok && j0 + 1 < L) srow[(j0 + 1) * NS] = c[nt][1];
+        if (q.ok && j0 < L) q.srow[j0 * NS] = c[nt][0];
+        if (q.ok && j0 + 1 < L) q.srow[(j0 + 1) * NS] = c[nt][1];
       }
     }
   }
@@ -214,7 +244,7 @@ template <int D>
 int schur2(const mhdg_disc& g, const mhdg_blocks& b, double* S, cudaStream_t st) {
   using C = Sch2<D>;
   const Sch2Dims dm = Sch2Dims::make<D>(g);
-  const size_t bytes = dm.smem_bytes();
+  const size_t bytes = dm.smem_bytes<D>();
   if (!g.grad_cls || g.L > 8 * C::NT || dm.ksv > C::KS || dm.ksf > C::KS || bytes > 227 * 1024) return -1;
   cudaFuncSetAttribute(k_schur2<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   k_schur2<D><<<g.n_mac, C::NWARP * 32, bytes, st>>>(g, b, dm, S);
