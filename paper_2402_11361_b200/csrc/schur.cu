@@ -38,7 +38,7 @@ struct Sch2 {
 };
 
 struct Sch2Dims {
-  int kv, kf, ksv, ksf, LP, wmax, stage, ngph;
+  int kv, kf, ksv, ksf, LP, wmax, pmrows, stage, ngph, kfp, rpn;
   template <int D>
   static Sch2Dims make(const mhdg_disc& g) {
     using C = Sch2<D>;
@@ -49,11 +49,16 @@ struct Sch2Dims {
     d.ksf = (d.kf + 3) / 4;
     d.LP = (g.L + 3) / 4 * 4;
     while (d.LP % 16 != 4) d.LP += 4;
-    const int wv = g.nq * C::NW, wf = g.nqf * C::NWF;
+    // a face stage holds all n_tri sub-faces of one face: stashes back to back, tables at
+    // rows T kfp + k (kfp = 4 ksf: each sub-face starts on a k-step)
+    d.kfp = 4 * d.ksf;
+    d.rpn = (C::NS * C::NS + 7) / 8 * 8;  // face-stage rows per face node (8-row tiles stay on one node)
+    const int wv = g.nq * C::NW, wf = g.n_tri * g.nqf * C::NWF;
     d.wmax = ((wv > wf ? wv : wf) + 1) & ~1;
+    d.pmrows = 4 * C::KS > g.n_tri * d.kfp ? 4 * C::KS : g.n_tri * d.kfp;
     // + padding: the last B fragments of a row read up to 8 NT - LP columns past it
     // (columns >= L are never stored; the padding is zero)
-    d.stage = d.wmax + 4 * C::KS * d.LP + 8 * C::NT;
+    d.stage = d.wmax + d.pmrows * d.LP + 8 * C::NT;
     d.ngph = (g.n_grad_cls * g.nq * g.nloc * D + 1) & ~1;
     return d;
   }
@@ -80,7 +85,22 @@ __global__ void __launch_bounds__(Sch2<D>::NWARP * 32, Sch2<D>::MINB) k_schur2(m
   for (int a = 0; a < D; ++a)
 #pragma unroll
     for (int c = 0; c < D; ++c) ij[a][c] = __ldg(g.inv_jac + (size_t)mac * D * D + a * D + c);
-  const int nvol = g.n_sub, nstage = g.n_sub + NF * g.n_tri;
+  const int nvol = g.n_sub, nstage = g.n_sub + NF;  // volume sub-elements, then one stage per face
+  // face-lattice incidence: node g lies in sub-faces finc_T[g][k] as local node finc_a[g][k]
+  constexpr int MAXINC = 8;
+  __shared__ unsigned char finc_T[64][MAXINC], finc_a[64][MAXINC], finc_n[64];
+  if (tid == 0) {
+    for (int gg = 0; gg < g.Lf && gg < 64; ++gg) finc_n[gg] = 0;
+    for (int T = 0; T < g.n_tri; ++T)
+      for (int a = 0; a < nlocf; ++a) {
+        const int gg = __ldg(g.tri_conn + T * nlocf + a);
+        if (gg < 64 && finc_n[gg] < MAXINC) {
+          finc_T[gg][finc_n[gg]] = (unsigned char)T;
+          finc_a[gg][finc_n[gg]] = (unsigned char)a;
+          ++finc_n[gg];
+        }
+      }
+  }
 
   auto prefetch = [&](int i) {
     if (i >= nstage) return;
@@ -95,16 +115,17 @@ __global__ void __launch_bounds__(Sch2<D>::NWARP * 32, Sch2<D>::MINB) k_schur2(m
       psrc = g.pm_vol + (size_t)i * dm.kv * L;
       kk = dm.kv;
     } else {
-      const int fT = i - nvol;
-      wsrc = b.wdgdq_face + ((size_t)mac * NF * g.n_tri + fT) * nqf * NWF;
-      wcnt = nqf * NWF;
-      psrc = g.pm_face + (size_t)fT * dm.kf * L;
-      kk = dm.kf;
+      const int f = i - nvol;
+      wsrc = b.wdgdq_face + ((size_t)mac * NF + f) * g.n_tri * nqf * NWF;
+      wcnt = g.n_tri * nqf * NWF;
+      psrc = g.pm_face + (size_t)f * g.n_tri * dm.kf * L;
+      kk = g.n_tri * dm.kf;
     }
     for (int e = tid; e < wcnt; e += NT_THREADS) cp_async8(W + e, wsrc + e, 8);
     for (int e = tid; e < kk * L; e += NT_THREADS) {
       const int row = e / L, j = e - row * L;
-      cp_async8(PM + row * dm.LP + j, psrc + e, 8);
+      const int prow = i < nvol ? row : (row / dm.kf) * dm.kfp + row % dm.kf;
+      cp_async8(PM + prow * dm.LP + j, psrc + e, 8);
     }
   };
 
@@ -133,7 +154,7 @@ __global__ void __launch_bounds__(Sch2<D>::NWARP * 32, Sch2<D>::MINB) k_schur2(m
     double* W = stg + (size_t)(i % C::NBUF) * dm.stage;
     const double* PM = W + dm.wmax;
     {  // fold inv_jac into the stash in place: W'[..(k, r')..] = sum_l ij[r'][l] W[..(k, l)..]
-      const int ngrp = (vol ? nq * D : nqf) * NS * NS;
+      const int ngrp = (vol ? nq * D : g.n_tri * nqf) * NS * NS;
       for (int e = tid; e < ngrp; e += NT_THREADS) {
         const int sr = e % (NS * NS), qk = e / (NS * NS);
         double* w = W + (size_t)qk * D * NS * NS + sr;
@@ -150,90 +171,105 @@ __global__ void __launch_bounds__(Sch2<D>::NWARP * 32, Sch2<D>::MINB) k_schur2(m
       }
     }
     __syncthreads();
-    const int rows = (vol ? nloc : nlocf) * NS * NS;
-    const int kdim = vol ? dm.kv : dm.kf, nks = vol ? dm.ksv : dm.ksf;
-    const int K = i, fT = i - nvol, f = fT / (g.n_tri > 0 ? g.n_tri : 1), T = fT - f * g.n_tri;
-    const int cls = vol ? __ldg(g.grad_cls_of + K) : 0;
-    // S row of an 8-row tile's output row, and where its accumulators start from
-    struct Row {
-      double* srow;
-      const double* crow;
-      int a, s, r;
-      bool ok;
-    };
-    auto row_of = [&](int mt) {
-      Row q;
-      const int m = mt * 8 + g8;
-      q.ok = m < rows;
-      q.a = q.ok ? m / (NS * NS) : 0;
-      q.s = (m / NS) % NS;
-      q.r = m % NS;
-      int node;
-      bool first = false;
-      if (vol) {
-        node = __ldg(g.sub_conn + K * nloc + q.a);
-        first = __ldg(g.vn_sub + __ldg(g.vn_ptr + node)) / nloc == K;
-      } else {
-        node = __ldg(g.face_vol_nodes + f * g.Lf + __ldg(g.tri_conn + T * nlocf + q.a));
-      }
-      q.srow = Sm + (size_t)(node * NS + q.s) * n + q.r;
-      q.crow = first ? SSm + (size_t)(node * NS + q.s) * n + q.r : q.srow;
-      return q;
-    };
-    auto load_c = [&](const Row& q, double (&c)[NT][2]) {
+    if (vol) {
+      const int rows = nloc * NS * NS;
+      const int K = i;
+      const int cls = __ldg(g.grad_cls_of + K);
+      for (int mt = warp; mt * 8 < rows; mt += NWP) {
+        const int m = mt * 8 + g8;
+        const bool mok = m < rows;
+        const int a = mok ? m / (NS * NS) : 0, s = (m / NS) % NS, r = m % NS;
+        // S row of this thread's output row, and where its accumulators start from
+        const int node = __ldg(g.sub_conn + K * nloc + a);
+        const bool first = __ldg(g.vn_sub + __ldg(g.vn_ptr + node)) / nloc == K;
+        double* srow = Sm + (size_t)(node * NS + s) * n + r;
+        const double* crow = first ? SSm + (size_t)(node * NS + s) * n + r : srow;
+        double c[NT][2];
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        const int j0 = nt * 8 + 2 * t4;
-        c[nt][0] = (q.ok && j0 < L) ? q.crow[j0 * NS] : 0.0;
-        c[nt][1] = (q.ok && j0 + 1 < L) ? q.crow[(j0 + 1) * NS] : 0.0;
-      }
-    };
-    for (int mt = warp; mt * 8 < rows; mt += NWP) {
-      const Row q = row_of(mt);
-      double c[NT][2];
-      load_c(q, c);
-      // A fragments of this row: T1[m][(q, r') = 4 ks + t4]
-      double af[KS];
-      if (vol) {
-        const double* gp = gph + (size_t)(cls * nq) * nloc * D + q.a * D;
-        const double* w = W + (q.s * NS + q.r);
+        for (int nt = 0; nt < NT; ++nt) {
+          const int j0 = nt * 8 + 2 * t4;
+          c[nt][0] = (mok && j0 < L) ? crow[j0 * NS] : 0.0;
+          c[nt][1] = (mok && j0 + 1 < L) ? crow[(j0 + 1) * NS] : 0.0;
+        }
+        // A fragments of this row: T1[m][(q, r') = 4 ks + t4]
+        double af[KS];
+        const double* gp = gph + (size_t)(cls * nq) * nloc * D + a * D;
+        const double* w = W + (s * NS + r);
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks) {
           const int kq = 4 * ks + t4;
           double v = 0.0;
-          if (q.ok && ks < nks && kq < kdim) {
-            const int qq = kq / D, rp = kq - qq * D;
-            const double* gq = gp + (size_t)qq * nloc * D;
-            const double* wq = w + (size_t)qq * NW + rp * NS * NS;
+          if (mok && ks < dm.ksv && kq < dm.kv) {
+            const int q = kq / D, rp = kq - q * D;
+            const double* gq = gp + (size_t)q * nloc * D;
+            const double* wq = w + (size_t)q * NW + rp * NS * NS;
 #pragma unroll
             for (int k = 0; k < D; ++k) v += gq[k] * wq[k * D * NS * NS];
           }
           af[ks] = v;
         }
-      } else {
 #pragma unroll
-        for (int ks = 0; ks < KS; ++ks) {
-          const int kq = 4 * ks + t4;
-          double v = 0.0;
-          if (q.ok && ks < nks && kq < kdim) {
-            const int qq = kq / D, rp = kq - qq * D;
-            v = -W[((qq * D + rp) * NS + q.s) * NS + q.r] * __ldg(g.phi_face + qq * nlocf + q.a);
+        for (int ks = 0; ks < KS; ++ks)
+          if (ks < dm.ksv) {
+            const double* pb = PM + (4 * ks + t4) * dm.LP + g8;
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(c[nt][0], c[nt][1], af[ks], pb[nt * 8]);
           }
-          af[ks] = v;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const int j0 = nt * 8 + 2 * t4;
+          if (mok && j0 < L) srow[j0 * NS] = c[nt][0];
+          if (mok && j0 + 1 < L) srow[(j0 + 1) * NS] = c[nt][1];
         }
       }
+    } else {
+      // face f, all sub-faces at once: rows (face node gg, s, r), rpn rows per node, so an
+      // 8-row tile stays on one node and sums its sub-faces in order (T ascending: the
+      // reference's accumulation order), -W'_T[q][r'][s][r] phi_face[q][a] against PM_T
+      const int f = i - nvol;
+      constexpr int KSF = 8;  // face k-steps per sub-face (kf <= 32)
+      for (int mt = warp; mt * 8 < g.Lf * dm.rpn; mt += NWP) {
+        const int gg = (mt * 8) / dm.rpn, sr = mt * 8 - gg * dm.rpn + g8;
+        const bool mok = sr < NS * NS;
+        const int s = mok ? sr / NS : 0, r = mok ? sr % NS : 0;
+        const int node = __ldg(g.face_vol_nodes + f * g.Lf + gg);
+        double* srow = Sm + (size_t)(node * NS + s) * n + r;
+        double c[NT][2];
 #pragma unroll
-      for (int ks = 0; ks < KS; ++ks)
-        if (ks < nks) {
-          const double* pb = PM + (4 * ks + t4) * dm.LP + g8;
+        for (int nt = 0; nt < NT; ++nt) {
+          const int j0 = nt * 8 + 2 * t4;
+          c[nt][0] = (mok && j0 < L) ? srow[j0 * NS] : 0.0;
+          c[nt][1] = (mok && j0 + 1 < L) ? srow[(j0 + 1) * NS] : 0.0;
+        }
+        const int ninc = finc_n[gg];
+        for (int e = 0; e < ninc; ++e) {
+          const int T = finc_T[gg][e], a = finc_a[gg][e];
+          const double* WT = W + (size_t)T * nqf * NWF;
+          double af[KSF];
 #pragma unroll
-          for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(c[nt][0], c[nt][1], af[ks], pb[nt * 8]);
+          for (int ks = 0; ks < KSF; ++ks) {
+            const int kq = 4 * ks + t4;
+            double v = 0.0;
+            if (mok && ks < dm.ksf && kq < dm.kf) {
+              const int q = kq / D, rp = kq - q * D;
+              v = -WT[((q * D + rp) * NS + s) * NS + r] * __ldg(g.phi_face + q * nlocf + a);
+            }
+            af[ks] = v;
+          }
+#pragma unroll
+          for (int ks = 0; ks < KSF; ++ks)
+            if (ks < dm.ksf) {
+              const double* pb = PM + (T * dm.kfp + 4 * ks + t4) * dm.LP + g8;
+#pragma unroll
+              for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(c[nt][0], c[nt][1], af[ks], pb[nt * 8]);
+            }
         }
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        const int j0 = nt * 8 + 2 * t4;
-        if (q.ok && j0 < L) q.srow[j0 * NS] = c[nt][0];
-        if (q.ok && j0 + 1 < L) q.srow[(j0 + 1) * NS] = c[nt][1];
+        for (int nt = 0; nt < NT; ++nt) {
+          const int j0 = nt * 8 + 2 * t4;
+          if (mok && j0 < L) srow[j0 * NS] = c[nt][0];
+          if (mok && j0 + 1 < L) srow[(j0 + 1) * NS] = c[nt][1];
+        }
       }
     }
   }
@@ -245,7 +281,8 @@ int schur2(const mhdg_disc& g, const mhdg_blocks& b, double* S, cudaStream_t st)
   using C = Sch2<D>;
   const Sch2Dims dm = Sch2Dims::make<D>(g);
   const size_t bytes = dm.smem_bytes<D>();
-  if (!g.grad_cls || g.L > 8 * C::NT || dm.ksv > C::KS || dm.ksf > C::KS || bytes > 227 * 1024) return -1;
+  if (!g.grad_cls || g.L > 8 * C::NT || dm.ksv > C::KS || dm.ksf > 8 || g.Lf > 64 || bytes > 227 * 1024)
+    return -1;
   cudaFuncSetAttribute(k_schur2<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   k_schur2<D><<<g.n_mac, C::NWARP * 32, bytes, st>>>(g, b, dm, S);
   return launch_ok();
