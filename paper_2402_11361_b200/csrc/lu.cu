@@ -413,7 +413,21 @@ __global__ void __launch_bounds__(NT, MINB) k_lu4(int n, double* __restrict__ S,
     const double* Lirow[NB / 8];  // inv(L11) row 8 rt + g lives in pivot row pv[8 rt + g]
 #pragma unroll
     for (int rt = 0; rt < NB / 8; ++rt) Lirow[rt] = P + pv[8 * rt + g] * PS + t4;
-    for (int q = warp; q < nchunks; q += NW) {
+    // Units of work: one chunk per warp, except that the r = nchunks mod NW chunks of the
+    // last round are split by rows over NW / r warps each (when that is >= 2), so the
+    // warps finish together.  The parts of a split chunk read A12 before a named barrier
+    // (ids 1..r); only part 0 then overwrites it with U12.
+    const int rlast = nchunks % NW, nparts = rlast > 0 ? NW / rlast : 1;
+    const int nfull = nparts >= 2 ? nchunks - rlast : nchunks;
+    const int nunits = nfull + (nparts >= 2 ? rlast * nparts : 0);
+    for (int un = warp; un < nunits; un += NW) {
+      int q = un, part = 0, np_ = 1;
+      if (un >= nfull) {
+        const int v = un - nfull;
+        q = nfull + v / nparts;
+        part = v % nparts;
+        np_ = nparts;
+      }
       const int c0 = ct0 + q * CW, cw = min(CW, n - c0);
       // U12 chunk = inv(L11) A12 (A12 = this panel's pivot rows; nb = NB whenever columns remain)
       double u[NB / 8][2][2];
@@ -439,8 +453,11 @@ __global__ void __launch_bounds__(NT, MINB) k_lu4(int n, double* __restrict__ S,
           }
       }
       __syncwarp();
+      if (np_ > 1)  // every part has read A12
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + q - nfull), "r"(32 * np_) : "memory");
 #pragma unroll
       for (int rt = 0; rt < NB / 8; ++rt) {
+        if (part != 0) break;
         double* dst = A + (size_t)pv[8 * rt + g] * n + c0;
 #pragma unroll
         for (int ct = 0; ct < 2; ++ct)
@@ -464,11 +481,13 @@ __global__ void __launch_bounds__(NT, MINB) k_lu4(int n, double* __restrict__ S,
         }
       }
       // C -= L21 U12 over the remaining rows, 16 rows per pass, next pass's C prefetched
-      if (m > 0) {
+      const int npass = (m + 15) / 16, pb = npass * part / np_, pe = npass * (part + 1) / np_;
+      const int mb = 16 * pb, mp = min(m, 16 * pe) - mb;  // this part's rows of the list
+      if (mp > 0) {
         if (cw == CW && (n & 1) == 0)
-          trail_pass_loop<NB, true>(A, n, c0, cw, m, np2, P, t4, g, bf);
+          trail_pass_loop<NB, true>(A, n, c0, cw, mp, np2 + mb, P, t4, g, bf);
         else
-          trail_pass_loop<NB, false>(A, n, c0, cw, m, np2, P, t4, g, bf);
+          trail_pass_loop<NB, false>(A, n, c0, cw, mp, np2 + mb, P, t4, g, bf);
       }
     }
     LUADD(4, pt4);
