@@ -598,7 +598,10 @@ static int launch_lu4(int n, int n_mac, double* scratch, int* piv, int* status, 
 int lu_factor4(int n, int n_mac, double* scratch, int* piv, double* packed, int* status, cudaStream_t st) {
   // 32-column panels, two CTAs per SM (one's pivot chain under the other's updates), or
   // 64-column panels, one CTA per SM (half the trailing-update traffic)
-  const int rc0 = g_lu_nb != 64   ? launch_lu4<32, 192, 2>(n, n_mac, scratch, piv, status, st)
+#ifndef MHDG_LU4_NT
+#define MHDG_LU4_NT 192
+#endif
+  const int rc0 = g_lu_nb != 64   ? launch_lu4<32, MHDG_LU4_NT, 2>(n, n_mac, scratch, piv, status, st)
                   : g_lu_nt == 384 ? launch_lu4<64, 384, 1>(n, n_mac, scratch, piv, status, st)
                                    : launch_lu4<64, 256, 1>(n, n_mac, scratch, piv, status, st);
   if (rc0 < 0) return -1;

@@ -34,7 +34,10 @@ struct Sch2 {
   // other's loads
   static constexpr int NBUF = D == 2 ? 2 : MHDG_SCHUR3_NBUF;
   static constexpr int NWARP = (D == 2 || NBUF == 1) ? 8 : 16;
-  static constexpr int MINB = (D == 2 || NBUF == 1) ? 2 : 1;  // CTAs per SM the registers are budgeted for
+#ifndef MHDG_SCHUR2_MINB2D
+#define MHDG_SCHUR2_MINB2D 2
+#endif
+  static constexpr int MINB = D == 2 ? MHDG_SCHUR2_MINB2D : (NBUF == 1 ? 2 : 1);  // CTAs per SM (register budget)
 };
 
 struct Sch2Dims {
