@@ -184,6 +184,11 @@ void mhdg_set_lu_variant(int v);
    per SM; threads 256 or 384).  For A/B measurements. */
 void mhdg_set_lu_panel(int nb, int threads);
 
+/* L2 priority of k_lu4's trailing-update traffic: evict_last on the macros with
+   mac % mode != 0 (mode >= 2; default 2 = every other macro), on all (1) or none
+   (0).  For A/B measurements. */
+void mhdg_set_lu_l2mode(int mode);
+
 /* Schur-complement kernel: 0 (default) stage-pipelined FP64 tensor-core kernel,
    1 the earlier tensor-core kernel, otherwise the per-macro FFMA kernel.  For A/B
    measurements. */

@@ -116,6 +116,8 @@ def lib():
         L.mhdg_set_lu_variant.restype = None
         L.mhdg_set_lu_panel.argtypes = [C.c_int, C.c_int]
         L.mhdg_set_lu_panel.restype = None
+        L.mhdg_set_lu_l2mode.argtypes = [C.c_int]
+        L.mhdg_set_lu_l2mode.restype = None
         L.mhdg_set_schur_variant.argtypes = [C.c_int]
         L.mhdg_set_schur_variant.restype = None
         L.mhdg_icgs.argtypes = [C.c_int, C.c_int, _dp, C.c_longlong, _dp, _dp, _dp, _dp]
@@ -136,7 +138,7 @@ EXPORTED = (
     "mhdg_gradient_refresh", "mhdg_precond_build", "mhdg_precond_apply", "mhdg_launch_count",
     "mhdg_packed_lu_size", "mhdg_set_stream_enabled", "mhdg_precond_build_ext", "mhdg_side_blocks",
     "mhdg_apply_work_size", "mhdg_set_apply_split", "mhdg_set_factor_variant", "mhdg_set_lu_variant", "mhdg_set_lu_panel",
-    "mhdg_set_schur_variant", "mhdg_timeline_begin", "mhdg_timeline_end", "mhdg_icgs", "mhdg_icgs_scratch_size",
+    "mhdg_set_lu_l2mode", "mhdg_set_schur_variant", "mhdg_timeline_begin", "mhdg_timeline_end", "mhdg_icgs", "mhdg_icgs_scratch_size",
 )
 
 

@@ -71,10 +71,33 @@ size_t smem_bytes(int n) {
 
 // C -= L21 U12 for one 16-column chunk over the m remaining rows (list rl), 16 rows per
 // pass with the next three passes' C in flight.  VEC: 16-byte C accesses (full chunk, even n).
+#ifndef MHDG_LU_L2MODE
+#define MHDG_LU_L2MODE 2
+#endif
+
+__device__ __forceinline__ double2 ld_hint(const double* p, unsigned long long pol) {
+  double2 v;
+  asm volatile("ld.global.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_hint(double* p, double2 v, unsigned long long pol) {
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y), "l"(pol) : "memory");
+}
+__device__ __forceinline__ unsigned long long l2_policy(int mode) {
+  unsigned long long pol;
+  if (mode == 1)
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  else if (mode == 2)
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
 template <int NB, bool VEC>
 __device__ __forceinline__ void trail_pass_loop(double* __restrict__ A, int n, int c0, int cw, int m,
                                                 const unsigned short* rl, const double* P, int t4, int g,
-                                                const double (&bf)[NB / 4][2]) {
+                                                const double (&bf)[NB / 4][2], unsigned long long pol) {
   using namespace lu4;
   constexpr int PS = pstride<NB>();
   const int rlast = rl[m - 1];
@@ -87,7 +110,7 @@ __device__ __forceinline__ void trail_pass_loop(double* __restrict__ A, int n, i
 #pragma unroll
       for (int ct = 0; ct < 2; ++ct) {
         if (VEC) {
-          const double2 v = ok[h] ? *reinterpret_cast<const double2*>(src + 8 * ct) : make_double2(0.0, 0.0);
+          const double2 v = ok[h] ? ld_hint(src + 8 * ct, pol) : make_double2(0.0, 0.0);
           c[h][ct][0] = v.x;
           c[h][ct][1] = v.y;
         } else {
@@ -116,7 +139,7 @@ __device__ __forceinline__ void trail_pass_loop(double* __restrict__ A, int n, i
 #pragma unroll
         for (int ct = 0; ct < 2; ++ct) {
           if (VEC) {
-            *reinterpret_cast<double2*>(dst + 8 * ct) = make_double2(c[h][ct][0], c[h][ct][1]);
+            st_hint(dst + 8 * ct, make_double2(c[h][ct][0], c[h][ct][1]), pol);
           } else {
 #pragma unroll
             for (int e = 0; e < 2; ++e)
@@ -149,7 +172,7 @@ __device__ __forceinline__ void trail_pass_loop(double* __restrict__ A, int n, i
 
 template <int NB, int NT, int RPT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) k_lu4(int n, double* __restrict__ S, int* __restrict__ piv_out,
-                                                  int* status) {
+                                                  int* status, int l2mode) {
   using namespace lu4;
   constexpr int NW = NT / 32, PS = pstride<NB>(), NH = NB / 32;  // NH: 32-column halves of a panel
   extern __shared__ double sm[];
@@ -170,6 +193,12 @@ __global__ void __launch_bounds__(NT, MINB) k_lu4(int n, double* __restrict__ S,
     rflag[i] = 0;
   }
   int m = n, lb = 0;
+  // L2 priority of the trailing-update C traffic: evict_last on the macros with
+  // mac % l2mode != 0 (l2mode >= 2), on all (1) or none (0).  The trailing matrices of all
+  // resident macros together are about the L2 size and are swept cyclically, so under LRU
+  // every macro's lines get evicted; keeping a fraction of the macros resident recovers
+  // their hits.
+  const unsigned long long pol = l2_policy(l2mode == 1 || (l2mode >= 2 && mac % l2mode != 0) ? 1 : 0);
   __syncthreads();
 
   for (int k0 = 0; k0 < n; k0 += NB) {
@@ -485,9 +514,9 @@ __global__ void __launch_bounds__(NT, MINB) k_lu4(int n, double* __restrict__ S,
       const int mb = 16 * pb, mp = min(m, 16 * pe) - mb;  // this part's rows of the list
       if (mp > 0) {
         if (cw == CW && (n & 1) == 0)
-          trail_pass_loop<NB, true>(A, n, c0, cw, mp, np2 + mb, P, t4, g, bf);
+          trail_pass_loop<NB, true>(A, n, c0, cw, mp, np2 + mb, P, t4, g, bf, pol);
         else
-          trail_pass_loop<NB, false>(A, n, c0, cw, mp, np2 + mb, P, t4, g, bf);
+          trail_pass_loop<NB, false>(A, n, c0, cw, mp, np2 + mb, P, t4, g, bf, pol);
       }
     }
     LUADD(4, pt4);
@@ -576,7 +605,8 @@ int pack_lu4(int n, int n_mac, const double* scratch, const int* piv, double* pa
 
 
 
-static int g_lu_nb = 32, g_lu_nt = 0;
+static int g_lu_nb = 32, g_lu_nt = 0, g_lu_l2mode = MHDG_LU_L2MODE;
+extern "C" void mhdg_set_lu_l2mode(int m) { g_lu_l2mode = m; }
 extern "C" void mhdg_set_lu_panel(int nb, int threads) {
   g_lu_nb = nb == 64 ? 64 : 32;
   g_lu_nt = threads;
@@ -590,7 +620,7 @@ static int launch_lu4(int n, int n_mac, double* scratch, int* piv, int* status, 
   auto kern = n <= NT ? k_lu4<NB, NT, 1, MINB> : k_lu4<NB, NT, 2, MINB>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   tl_begin(TL_FACTOR, st);
-  kern<<<n_mac, NT, bytes, st>>>(n, scratch, piv, status);
+  kern<<<n_mac, NT, bytes, st>>>(n, scratch, piv, status, g_lu_l2mode);
   tl_end(TL_FACTOR, st);
   return 0;
 }

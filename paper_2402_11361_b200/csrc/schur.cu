@@ -33,7 +33,10 @@ struct Sch2 {
   // 3D: one stage buffer (a 3D stash is 48 KB) so two CTAs share an SM and cover each
   // other's loads
   static constexpr int NBUF = D == 2 ? 2 : MHDG_SCHUR3_NBUF;
-  static constexpr int NWARP = (D == 2 || NBUF == 1) ? 8 : 16;
+#ifndef MHDG_SCHUR2_NW2D
+#define MHDG_SCHUR2_NW2D 8
+#endif
+  static constexpr int NWARP = D == 2 ? MHDG_SCHUR2_NW2D : (NBUF == 1 ? 8 : 16);
 #ifndef MHDG_SCHUR2_MINB2D
 #define MHDG_SCHUR2_MINB2D 2
 #endif
