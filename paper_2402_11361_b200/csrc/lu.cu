@@ -75,25 +75,6 @@ size_t smem_bytes(int n) {
 #define MHDG_LU_L2MODE 2
 #endif
 
-__device__ __forceinline__ double2 ld_hint(const double* p, unsigned long long pol) {
-  double2 v;
-  asm volatile("ld.global.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
-  return v;
-}
-__device__ __forceinline__ void st_hint(double* p, double2 v, unsigned long long pol) {
-  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y), "l"(pol) : "memory");
-}
-__device__ __forceinline__ unsigned long long l2_policy(int mode) {
-  unsigned long long pol;
-  if (mode == 1)
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-  else if (mode == 2)
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  else
-    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-
 template <int NB, bool VEC>
 __device__ __forceinline__ void trail_pass_loop(double* __restrict__ A, int n, int c0, int cw, int m,
                                                 const unsigned short* rl, const double* P, int t4, int g,
