@@ -30,7 +30,7 @@ import numpy as np
 import scipy.linalg
 from scipy.optimize import brentq
 
-from paper_2402_11361_b200.discretization import DIRICHLET, WALL
+from paper_2402_11361_b200.discretization import ADIABATIC, DIRICHLET, WALL
 from paper_2402_11361_b200.physics import AdmissibilityError
 
 from . import pointwise as pw
@@ -272,6 +272,10 @@ def _face_terms(disc, fields, uh_loc, want_jac, frozen, R_U, R_T_loc, blocks, ne
                     if kind == DIRICHLET:
                         xq = disc.face_quad_coords(lf, T)[sel]
                         bhat = uh_pt[sel] - data(xq.reshape(-1, d)).reshape(-1, nqf, ns)
+                    elif kind == ADIABATIC:  # rho_hat - rho, m_hat, E_hat - E
+                        bhat = uh_pt[sel].copy()
+                        bhat[..., 0] -= u_pt[sel][..., 0]
+                        bhat[..., E] -= u_pt[sel][..., E]
                     else:
                         e_w, u_w = data
                         uh = uh_pt[sel]
@@ -314,6 +318,8 @@ def _face_terms(disc, fields, uh_loc, want_jac, frozen, R_U, R_T_loc, blocks, ne
                         Khh[1:E, 0] = -u_w
                         Khh[E, 0] = -(e_w + 0.5 * float(u_w @ u_w))
                         Kuu[0, 0] = -1.0
+                    elif kind == ADIABATIC:
+                        Kuu[0, 0] = Kuu[E, E] = -1.0
                     ttt[sel] = np.einsum("mqab,st->masbt", proj[sel], Khh).reshape(-1, nl, nl)
                     tst[sel] = np.einsum("mqab,st->masbt", proj[sel], Kuu).reshape(-1, nl, nl)
             blocks.face_trace_state[:, lf][:, rc[:, None], rc[None, :]] += tst

@@ -10,6 +10,10 @@ reference cannot run:
   T_w = 1 (BASELINE leaves the wall temperatures unspecified).
 * ``UniformFlow2D`` -- C2: uniform flow rho=1, v=(1, 0.3), P=1/(gamma M^2) with
   flow scaling as CouetteCase (Re_acoustic = Re_flow = Re, mach_ref = M).
+* ``SphereCase`` -- C4 (3D, the reference has neither the mesh nor the wall
+  BC): steady flow past a unit-diameter sphere on the O-grid of
+  ``mesh.build_sphere_ogrid_mesh``; adiabatic no-slip sphere, free-stream
+  Dirichlet far field.
 """
 
 from __future__ import annotations
@@ -194,3 +198,29 @@ class UniformFlow2D:
         n = len(np.asarray(x))
         return conserved(np.ones(n), np.tile(np.asarray(self.velocity, float), (n, 1)),
                          np.full(n, self.pressure), self.params)
+
+
+@dataclass
+class SphereCase:
+    """C4: free stream |v| = M along x past a unit-diameter sphere at Re (based on the
+    diameter).  Acoustic scaling as TgvCase (rho = 1, c = 1, P = 1/gamma,
+    Re_acoustic = Re/M); BASELINE does not give Pr, 0.72 as C1/C2."""
+
+    reynolds: float = 100.0
+    mach: float = 0.2
+    gamma: float = 1.4
+    prandtl: float = 0.72
+    params: FlowParams = field(init=False)
+
+    def __post_init__(self):
+        self.params = FlowParams(gamma=self.gamma, prandtl=self.prandtl,
+                                 reynolds_acoustic=self.reynolds / self.mach, mach_ref=self.mach)
+
+    def freestream(self, x):
+        n = len(np.asarray(x))
+        v = np.zeros((n, 3))
+        v[:, 0] = self.mach
+        return conserved(np.ones(n), v, np.full(n, 1.0 / self.gamma), self.params)
+
+    def boundary_conditions(self):
+        return {"sphere": ("adiabatic_noslip_wall", None), "farfield": ("dirichlet_state", self.freestream)}

@@ -438,6 +438,8 @@ __global__ void __launch_bounds__(ASM_THREADS)
           else if (s <= D) v = fuh[idx] - rh * u_w[s - 1];
           else v = fuh[qq * NS + E] - rh * e_tot;
           fbh[idx] = v;
+        } else if (kind == 3) {  // adiabatic no-slip wall: rho_hat - rho, m_hat, E_hat - E
+          fbh[idx] = (s == 0 || s == E) ? fuh[idx] - fu[idx] : fuh[idx];
         }
       }
       __syncthreads();
@@ -481,6 +483,8 @@ __global__ void __launch_bounds__(ASM_THREADS)
               if (t == 0 && s >= 1 && s <= D) khh = -u_w[s - 1];
               if (t == 0 && s == E) khh = -e_tot;
               if (s == 0 && t == 0) kuu = -1.0;
+            } else if (kind == 3) {
+              if (s == t && (s == 0 || s == E)) kuu = -1.0;
             }
             tst = pr * kuu;
             ttt = pr * khh;

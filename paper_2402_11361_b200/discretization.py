@@ -21,6 +21,11 @@ from .refmacro import FACE_CORNERS, SIMPLEX_VERTICES, ref_macro
 
 DIRICHLET = 1
 WALL = 2
+# adiabatic no-slip wall (BASELINE config 4; the reference has none, physics.py:201):
+# rho_hat = rho, m_hat = 0 as the reference's wall (assembly.py:546-550), and the
+# energy row E_hat = E (interior total energy, so T_hat = T and the stabilised heat
+# flux through the wall vanishes) in place of the isothermal E_hat = rho_hat e_w
+ADIABATIC = 3
 
 
 class ConfigError(ValueError):
@@ -109,6 +114,8 @@ class Discretization:
                 T_w, vel = data
                 self.bc_data[code] = (WALL, (float(T_w) / (g * (g - 1.0)),
                                              np.asarray(vel, dtype=float).reshape(d)))
+            elif kind == "adiabatic_noslip_wall":
+                self.bc_data[code] = (ADIABATIC, None)
             else:
                 raise ConfigError(f"unknown boundary kind {kind!r}")
         fk = mesh.face_kind[mesh.faces_of_macro]
@@ -192,6 +199,8 @@ class Discretization:
             if kind == WALL:
                 wall_e[sel] = data[0]
                 wall_u[sel] = data[1]
+                continue
+            if kind == ADIABATIC:
                 continue
             for lf in range(self.nf):
                 macs = np.nonzero(sel[:, lf])[0]

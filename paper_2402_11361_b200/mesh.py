@@ -22,7 +22,8 @@ INTERIOR = 0
 BOUNDARY = 1
 PERIODIC = 2
 
-BOUNDARY_LABELS = ("x0", "x1", "y0", "y1", "z0", "z1")
+# box planes (codes 0-5, the reference's labels) and the O-grid's two spheres (6, 7)
+BOUNDARY_LABELS = ("x0", "x1", "y0", "y1", "z0", "z1", "sphere", "farfield")
 
 
 @dataclass
@@ -110,8 +111,10 @@ def _orient_positive(tets, vertices):
     return tets
 
 
-def build_faces(vertices, tets, lo, hi, periodic, tol):
-    """Face skeleton in the reference's order (mesh.py:132-225), any dim."""
+def build_faces(vertices, tets, lo, hi, periodic, tol, classify=None):
+    """Face skeleton in the reference's order (mesh.py:132-225), any dim.
+    classify(face vertex coords (d, d)) -> label code replaces the box-plane
+    tags (mesh.py:144-151) for meshes that are not boxes."""
     d = tets.shape[1] - 1
     corners = FACE_CORNERS[d]
     nm = len(tets)
@@ -158,11 +161,11 @@ def build_faces(vertices, tets, lo, hi, periodic, tol):
             continue
         i0 = incs[0]
         g0 = tuple(flat[i0])
-        code = bcode(g0)
+        code = bcode(g0) if classify is None else int(classify(vertices[list(g0)]))
         if code < 0:
             raise AssertionError("single-incidence face not on the box boundary")
         ax = code // 2
-        if not periodic[ax]:
+        if classify is not None or not periodic[ax]:
             recs.append(((i0 // (d + 1), -1), (i0 % (d + 1), -1), BOUNDARY, code, g0, None,
                          np.zeros(d)))
             continue
@@ -256,6 +259,68 @@ def build_square_mesh(domain, n_cells, m: int, periodic=(False, False)) -> Macro
     tris = _orient_positive(tris.reshape(-1, 3), vertices)
     faces = build_faces(vertices, tris, lo, hi, tuple(periodic), float(min(hx, hy)) * 1e-8)
     return MacroMesh(vertices, tris, m, *faces)
+
+
+def build_sphere_ogrid_mesh(n_r: int, n_theta: int, n_phi: int, m: int, r_in: float = 0.5,
+                            r_out: float = 20.0, grading: float = 1.15) -> MacroMesh:
+    """O-grid around a sphere (BASELINE config 4; the reference meshes boxes only,
+    mesh.py:144-151): n_r radial shells geometrically graded (ratio `grading`) from
+    r_in to r_out, x n_theta polar x n_phi azimuthal cells in spherical coordinates,
+    each cell split into 6 Kuhn tets in (r, theta, phi) index space, as
+    build_cube_mesh does (mesh.py:263-266); cells r-major, so contiguous macro
+    slabs are radial shells.
+
+    Poles: the cells touching the polar axis are wedges (their theta = 0 or pi
+    corners coincide for every phi).  The axis vertices are shared and the Kuhn
+    tets with a repeated vertex (three of the six in a wedge cell, zero volume)
+    are dropped; the other three tile the wedge conformingly, since a dropped
+    tet's two non-degenerate faces coincide and become the interface of the two
+    neighbouring tets.  phi wraps through the vertex numbering (no periodic faces).
+    Boundary labels: "sphere" (r = r_in) and "farfield" (r = r_out)."""
+    if n_r < 1 or n_theta < 2 or n_phi < 3 or m < 1:
+        raise ValueError("need n_r >= 1, n_theta >= 2, n_phi >= 3, m >= 1")
+    if not (0.0 < r_in < r_out) or grading <= 0.0:
+        raise ValueError("need 0 < r_in < r_out and grading > 0")
+    w = grading ** np.arange(n_r)
+    r = r_in + (r_out - r_in) * np.concatenate([[0.0], np.cumsum(w)]) / np.sum(w)
+    th = np.pi * np.arange(n_theta + 1) / n_theta
+    ph = 2.0 * np.pi * np.arange(n_phi) / n_phi
+    # vertex ids: interior theta rings (i, j = 1..n_theta-1, k) then the two axis points per radius
+    nt_in = n_theta - 1
+    ring = np.arange((n_r + 1) * nt_in * n_phi).reshape(n_r + 1, nt_in, n_phi)
+    north = ring.size + np.arange(n_r + 1)
+    south = north[-1] + 1 + np.arange(n_r + 1)
+    R, T, P = np.meshgrid(r, th[1:-1], ph, indexing="ij")
+    xyz = np.stack([R * np.sin(T) * np.cos(P), R * np.sin(T) * np.sin(P), R * np.cos(T)], -1).reshape(-1, 3)
+    axis = lambda z: np.stack([np.zeros_like(r), np.zeros_like(r), z * r], -1)
+    vertices = np.concatenate([xyz, axis(1.0), axis(-1.0)])
+
+    def vid(i, j, k):
+        k = k % n_phi
+        return np.where(j == 0, north[i], np.where(j == n_theta, south[i], ring[i, np.clip(j - 1, 0, nt_in - 1), k]))
+
+    cells = np.array(list(itertools.product(range(n_r), range(n_theta), range(n_phi))), dtype=np.int64)
+    tets = []
+    for off in _kuhn_cell_tets():
+        c = cells[:, None, :] + off[None, :, :]
+        tets.append(vid(c[..., 0], c[..., 1], c[..., 2]))
+    tets = np.stack(tets, axis=1).reshape(-1, 4)  # cell-major, 6 Kuhn tets per cell
+    srt = np.sort(tets, axis=1)
+    tets = tets[np.all(srt[:, 1:] != srt[:, :-1], axis=1)]
+    tets = _orient_positive(tets, vertices)
+    tol = 1e-8 * float(r[1] - r[0])
+
+    def classify(P):
+        rr = np.linalg.norm(P, axis=1)
+        if np.all(np.abs(rr - r_in) < tol * 10):
+            return BOUNDARY_LABELS.index("sphere")
+        if np.all(np.abs(rr - r_out) < tol * 1e3):
+            return BOUNDARY_LABELS.index("farfield")
+        return -1
+
+    lo, hi = vertices.min(axis=0), vertices.max(axis=0)
+    faces = build_faces(vertices, tets, lo, hi, (False, False, False), tol, classify=classify)
+    return MacroMesh(vertices, tets, m, *faces)
 
 
 def count_dofs(mesh: MacroMesh, p: int, n_s: int | None = None):
