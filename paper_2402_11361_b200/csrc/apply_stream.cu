@@ -1189,6 +1189,10 @@ int apply_stream(const mhdg_disc& g, const mhdg_blocks& b, const mhdg_factors& f
   if (stream_ok<Cfg<3, 2, 2>>(g, b, f)) return launch_apply<Cfg<3, 2, 2>>(g, b, f, x, y_loc, st);
   if (stream_ok<Cfg<3, 1, 2>>(g, b, f)) return launch_apply<Cfg<3, 1, 2>>(g, b, f, x, y_loc, st);
   if (stream_ok<Cfg<3, 2, 1>>(g, b, f)) return launch_apply<Cfg<3, 2, 1>>(g, b, f, x, y_loc, st);
+  // the rest of the C5 (m, p) sweep (BASELINE configs[4])
+  if (stream_ok<Cfg<3, 1, 1>>(g, b, f)) return launch_apply<Cfg<3, 1, 1>>(g, b, f, x, y_loc, st);
+  if (stream_ok<Cfg<3, 1, 3>>(g, b, f)) return launch_apply<Cfg<3, 1, 3>>(g, b, f, x, y_loc, st);
+  if (stream_ok<Cfg<3, 4, 1>>(g, b, f)) return launch_apply<Cfg<3, 4, 1>>(g, b, f, x, y_loc, st);
   return -1;
 }
 
