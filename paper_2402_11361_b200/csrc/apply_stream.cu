@@ -377,6 +377,18 @@ __global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 ? 1 : 2)) k_apply_s
           default: return fac.lu + (size_t)mac * PK + p.off;  // S^-1 tiles
         }
       };
+      // W_vol segments of an odd number of doubles (3D m = 1, p = 2: 27 x 225) leave every
+      // other macro's base 8-byte aligned: those pieces are copied from one double earlier
+      // (bulk copies need 16-byte alignment) and read from stage + 1
+      constexpr bool WV_ODD = (C::NPV * C::NW) & 1;
+      auto span = [&](int mac, const Piece& p, const double*& src, uint32_t& bytes) {
+        src = src_of(mac, p);
+        bytes = (uint32_t)p.cnt * 8u;
+        if (WV_ODD && p.kind == K_WV && (mac & 1)) {
+          src -= 1;
+          bytes = (uint32_t)ceven(p.nu * C::NW + 1) * 8u;
+        }
+      };
       int pm = blockIdx.x, pp = 0, pref = 0;  // prefetch cursor (macro, piece), pieces issued
       int it = 0;
       for (int mac = blockIdx.x; mac < g.n_mac; mac += gridDim.x) {
@@ -385,14 +397,21 @@ __global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 ? 1 : 2)) k_apply_s
           const int s = it % STAGES;
           while (pref < it + pref_ahead && pm < g.n_mac) {
             const Piece& q = pieces[pp];
-            if (q.kind != K_GF && q.kind != K_MD && q.cnt) bulk_prefetch_l2(src_of(pm, q), (uint32_t)q.cnt * 8u);
+            if (q.kind != K_GF && q.kind != K_MD && q.cnt) {
+              const double* src;
+              uint32_t nbytes;
+              span(pm, q, src, nbytes);
+              bulk_prefetch_l2(src, nbytes);
+            }
             ++pref;
             if (++pp == np) { pp = 0; pm += gridDim.x; }
           }
           if (it >= STAGES) mbar_wait(&empty_bar[s], ((it / STAGES) + 1) & 1);
-          const uint32_t bytes = (uint32_t)p.cnt * 8u;
+          const double* src;
+          uint32_t bytes;
+          span(mac, p, src, bytes);
           mbar_arrive_expect_tx(&full_bar[s], bytes);
-          if (bytes) bulk_g2s(ring + s * ST_DBL, src_of(mac, p), bytes, &full_bar[s]);
+          if (bytes) bulk_g2s(ring + s * ST_DBL, src, bytes, &full_bar[s]);
           ++it;
         }
       }
@@ -636,7 +655,9 @@ __global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 ? 1 : 2)) k_apply_s
       if (tid == 0) { PROF_ADD(K_FTT, 1, t3); }
       PROF_T(t4);
       seg_loop<C::NPV, SC::WV_ALIGN ? SC::WV_PER : units_per_piece(C::NW)>(
-          rg, lane, [&](const double* A, int u0, int nu) { wcontract(A, u0, nu, false, false); });
+          rg, lane, [&](const double* A, int u0, int nu) {
+            wcontract(A + (((C::NPV * C::NW) & 1) && (mac & 1) ? 1 : 0), u0, nu, false, false);
+          });
       if (tid == 0) { PROF_ADD(K_WV, 1, t4); }
       PROF_T(t5);
       seg_loop<C::NPF, units_per_piece(C::NWF)>(
@@ -1076,8 +1097,7 @@ static bool stream_ok(const mhdg_disc& g, const mhdg_blocks& b, const mhdg_facto
     return false;
   // 16-byte alignment of every per-macro segment base
   auto al = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
-  const bool sizes = ((C::NF * C::BS * C::BS) % 2 == 0) && ((C::NPV * C::NW) % 2 == 0) &&
-                     ((C::NPF * C::NWF) % 2 == 0);
+  const bool sizes = ((C::NF * C::BS * C::BS) % 2 == 0) && ((C::NPF * C::NWF) % 2 == 0);  // W_vol: either
   const bool tables = g.n_grad_cls >= 1 && g.grad_cls && g.grad_cls_of && g.node_to_face && g.minv_d_face &&
                       g.n_face_nodes == C::NFN;
   const size_t cls = C::D == 2 ? (size_t)g.n_grad_cls * TSm<C>::CLS : 0;

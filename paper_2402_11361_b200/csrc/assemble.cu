@@ -34,7 +34,9 @@ struct AsmSmem {
 };
 
 template <int D>
-__host__ __device__ inline AsmSmem<D> asm_smem(const Sz& s) {
+__host__ __device__ inline AsmSmem<D> asm_smem(const Sz& s0, int nqc) {
+  Sz s = s0;
+  s.nq = nqc;  // the volume per-point work arrays hold one chunk of points
   constexpr int NS = D + 2, NF = D + 1;
   constexpr int PRIM = (int)((sizeof(Prim<D>) + 7) / 8);
   AsmSmem<D> m;
@@ -110,11 +112,11 @@ __global__ void __launch_bounds__(ASM_THREADS)
     k_assemble(mhdg_disc g, mhdg_flow flow, mhdg_stage stage, const double* __restrict__ u,
                const double* __restrict__ q, const double* __restrict__ uhat, double* __restrict__ R_grad,
                double* __restrict__ R_state, double* __restrict__ R_tl, int want_jac, mhdg_blocks bk,
-               mhdg_frozen fo, mhdg_frozen fi, int use_frozen, int* status) {
+               mhdg_frozen fo, mhdg_frozen fi, int use_frozen, int* status, int nqc) {
   extern __shared__ double sm[];
   constexpr int NS = D + 2, NF = D + 1, E = D + 1;
   const Sz sz = make_sz<D>(g);
-  const AsmSmem<D> o = asm_smem<D>(sz);
+  const AsmSmem<D> o = asm_smem<D>(sz, nqc);
   const FlowC fl = make_flow<D>(flow);
   const int mac = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
   const int n = sz.n, L = sz.L, Lf = sz.Lf, nq = sz.nq, nloc = sz.nloc, nqf = sz.nqf, nlocf = sz.nlocf;
@@ -202,20 +204,24 @@ __global__ void __launch_bounds__(ASM_THREADS)
   __syncthreads();
 
   // ---- volume terms, one sub-element at a time (assembly.py:409-475) ------
+  // quadrature points in chunks of nqc (= nq unless the per-point work arrays would
+  // exceed shared memory, e.g. 3D p = 3); sums over points accumulate chunk by chunk
   const int nA = D * NS * NS;
   for (int K = 0; K < sz.n_sub; ++K) {
     const int* conn = g.sub_conn + K * nloc;
-    for (int idx = tid; idx < nq * nloc * D; idx += nt) {
+    for (int q0 = 0; q0 < nq; q0 += nqc) {
+    const int nc = min(nqc, nq - q0);
+    for (int idx = tid; idx < nc * nloc * D; idx += nt) {
       const int k = idx % D, a = (idx / D) % nloc, qq = idx / (D * nloc);
-      const double* gr = g.grad_ref + (((size_t)K * nq + qq) * nloc + a) * D;
+      const double* gr = g.grad_ref + (((size_t)K * nq + q0 + qq) * nloc + a) * D;
       double v = 0.0;
 #pragma unroll
       for (int r = 0; r < D; ++r) v += gr[r] * ij[r * D + k];
       gph[idx] = v;  // gphys[q][a][k]
     }
-    for (int qq = tid; qq < nq; qq += nt) {
+    for (int qq = tid; qq < nc; qq += nt) {
       double uu[NS], qv[D * NS];
-      interp_point<D>(g.phi_vol + qq * nloc, nloc, conn, nullptr, us, 0, qs, L, uu, qv);
+      interp_point<D>(g.phi_vol + (q0 + qq) * nloc, nloc, conn, nullptr, us, 0, qs, L, uu, qv);
 #pragma unroll
       for (int s = 0; s < NS; ++s) upt[qq * NS + s] = uu[s];
 #pragma unroll
@@ -224,16 +230,16 @@ __global__ void __launch_bounds__(ASM_THREADS)
       if (bad) set_status(status, MHDG_ERR_ADMISSIBILITY, mac, bad - 1, uu[0]);
       const Prim<D> p = prim<D>(uu, fl);
       prv[qq] = p;
-      wq[qq] = g.w_ref[K * nq + qq] * det;
-      const size_t fidx = ((size_t)mac * sz.n_sub + K) * nq + qq;
+      wq[qq] = g.w_ref[K * nq + q0 + qq] * det;
+      const size_t fidx = ((size_t)mac * sz.n_sub + K) * nq + q0 + qq;
       tq[qq] = use_frozen ? fi.supg_tau[fidx] : supg_tau<D>(p, fl, g.h_sub[mac * sz.n_sub + K], inv_sdt);
       if (want_jac) fo.supg_tau[fidx] = tq[qq];
     }
     __syncthreads();
     // pointwise Jacobians and fluxes, one entry per thread
-    for (int idx = tid; idx < nq * nA; idx += nt) {
+    for (int idx = tid; idx < nc * nA; idx += nt) {
       const int qq = idx / nA, e = idx % nA, t = e % NS, s = (e / NS) % NS, k = e / (NS * NS);
-      const size_t fidx = (((size_t)mac * sz.n_sub + K) * nq + qq) * nA + e;
+      const size_t fidx = (((size_t)mac * sz.n_sub + K) * nq + q0 + qq) * nA + e;
       const double a = euler_jac<D>(prv[qq], fl, k, s, t);
       As[idx] = use_frozen ? fi.supg_jac[fidx] : a;
       if (want_jac) {
@@ -241,14 +247,14 @@ __global__ void __launch_bounds__(ASM_THREADS)
         fo.supg_jac[fidx] = a;
       }
     }
-    for (int idx = tid; idx < nq * NS * D; idx += nt) {
+    for (int idx = tid; idx < nc * NS * D; idx += nt) {
       const int qq = idx / (NS * D), k = idx % D, s = (idx / D) % NS;
       FG[idx] = euler_flux<D>(prv[qq], upt + qq * NS, s, k) + visc_flux<D>(prv[qq], fl, qpt + qq * D * NS, s, k);
     }
     if (want_jac) {
       const int nW = D * D * NS * NS;
-      double* Wd = bk.wdgdq_vol + (((size_t)mac * sz.n_sub + K) * nq) * nW;
-      for (int idx = tid; idx < nq * nW; idx += nt) {
+      double* Wd = bk.wdgdq_vol + (((size_t)mac * sz.n_sub + K) * nq + q0) * nW;
+      for (int idx = tid; idx < nc * nW; idx += nt) {
         const int qq = idx / nW, e = idx % nW, t = e % NS, s = (e / NS) % NS, l = (e / (NS * NS)) % D,
                   k = e / (D * NS * NS);
         Wd[idx] = wq[qq] * visc_dgdq<D>(prv[qq], fl, k, l, s, t);
@@ -256,7 +262,7 @@ __global__ void __launch_bounds__(ASM_THREADS)
     }
     __syncthreads();
     // strong SUPG residual and the per-point residual vector Pp[q][k][s]
-    for (int qq = tid; qq < nq; qq += nt) {
+    for (int qq = tid; qq < nc; qq += nt) {
       double gu[D][NS], tdp[NS];
 #pragma unroll
       for (int t = 0; t < NS; ++t) {
@@ -273,7 +279,7 @@ __global__ void __launch_bounds__(ASM_THREADS)
           for (int t = 0; t < NS; ++t) gu[k][t] += gp * us[node * NS + t];
         }
         if (temporal) {
-          const double ph = g.phi_vol[qq * nloc + a];
+          const double ph = g.phi_vol[(q0 + qq) * nloc + a];
 #pragma unroll
           for (int t = 0; t < NS; ++t) tdp[t] += ph * td[node * NS + t];
         }
@@ -300,7 +306,7 @@ __global__ void __launch_bounds__(ASM_THREADS)
           Pp[(qq * D + k) * NS + s] = -w * FG[(qq * NS + s) * D + k] + wt * acc;
         }
       if (g.source) {
-        const double* src = g.source + (((size_t)mac * sz.n_sub + K) * nq + qq) * NS;
+        const double* src = g.source + (((size_t)mac * sz.n_sub + K) * nq + q0 + qq) * NS;
 #pragma unroll
         for (int s = 0; s < NS; ++s) sw[qq * NS + s] = -w * src[s];
       }
@@ -309,16 +315,16 @@ __global__ void __launch_bounds__(ASM_THREADS)
     for (int idx = tid; idx < nloc * NS; idx += nt) {
       const int s = idx % NS, a = idx / NS;
       double acc = 0.0;
-      for (int qq = 0; qq < nq; ++qq) {
+      for (int qq = 0; qq < nc; ++qq) {
 #pragma unroll
         for (int k = 0; k < D; ++k) acc += gph[(qq * nloc + a) * D + k] * Pp[(qq * D + k) * NS + s];
-        if (g.source) acc += g.phi_vol[qq * nloc + a] * sw[qq * NS + s];
+        if (g.source) acc += g.phi_vol[(q0 + qq) * nloc + a] * sw[qq * NS + s];
       }
-      cvol[(K * nloc + a) * NS + s] = acc;
+      cvol[(K * nloc + a) * NS + s] = q0 == 0 ? acc : cvol[(K * nloc + a) * NS + s] + acc;
     }
     if (want_jac) {
       const int nw = nloc * NS * NS;
-      for (int idx = tid; idx < nq * nw; idx += nt) {
+      for (int idx = tid; idx < nc * nw; idx += nt) {
         const int qq = idx / nw, e = idx % nw, s = e % NS, uu = (e / NS) % NS, a = e / (NS * NS);
         double acc = 0.0;
 #pragma unroll
@@ -333,7 +339,7 @@ __global__ void __launch_bounds__(ASM_THREADS)
       for (int idx = tid; idx < nr * nr; idx += nt) {
         const int t = idx % NS, b = (idx / NS) % nloc, s = (idx / nr) % NS, a = idx / (nr * NS);
         double acc = 0.0;
-        for (int qq = 0; qq < nq; ++qq) {
+        for (int qq = 0; qq < nc; ++qq) {
           const double w = wq[qq], wt = w * tq[qq];
           double y = 0.0;
 #pragma unroll
@@ -344,12 +350,13 @@ __global__ void __launch_bounds__(ASM_THREADS)
 #pragma unroll
           for (int uu = 0; uu < NS; ++uu)
             z += W1[(qq * nloc + a) * W1S<D>() + uu * NS + s] * W1[(qq * nloc + b) * W1S<D>() + uu * NS + t];
-          acc += y * g.phi_vol[qq * nloc + b] + wt * z;
+          acc += y * g.phi_vol[(q0 + qq) * nloc + b] + wt * z;
         }
         SSm[(size_t)(conn[a] * NS + s) * n + conn[b] * NS + t] += acc;
       }
     }
     __syncthreads();
+    }  // point chunks
   }
 
   // ---- face terms (assembly.py:477-612) -----------------------------------
@@ -529,7 +536,9 @@ int assemble(const mhdg_disc& g, const mhdg_flow& fl, const mhdg_stage& sg, cons
              const double* uhat, double* Rg, double* Ru, double* Rtl, double* Rt, int want_jac, const mhdg_blocks* b,
              const mhdg_frozen* fo, const mhdg_frozen* fi, int* status, cudaStream_t st) {
   const Sz sz = make_sz<D>(g);
-  const size_t bytes = sizeof(double) * asm_smem<D>(sz).total;
+  int nqc = sz.nq;  // largest point chunk whose work arrays fit shared memory
+  while (nqc > 1 && sizeof(double) * asm_smem<D>(sz, nqc).total > 227 * 1024) nqc = (nqc + 1) / 2;
+  const size_t bytes = sizeof(double) * asm_smem<D>(sz, nqc).total;
   if (bytes > 227 * 1024) return MHDG_ERR_CONFIG;
   if (bytes > 48 * 1024) cudaFuncSetAttribute(k_assemble<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   mhdg_blocks bb{};
@@ -541,7 +550,7 @@ int assemble(const mhdg_disc& g, const mhdg_flow& fl, const mhdg_stage& sg, cons
   }
   if (fi) fzi = *fi;
   k_assemble<D><<<g.n_mac, ASM_THREADS, bytes, st>>>(g, fl, sg, u, q, uhat, Rg, Ru, Rtl, want_jac, bb, fzo, fzi,
-                                                     fi ? 1 : 0, status);
+                                                     fi ? 1 : 0, status, nqc);
   int rc = launch_ok();
   if (rc) return rc;
   return face_reduce(g, Rtl, nullptr, 0.0, Rt, st);
