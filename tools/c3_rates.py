@@ -24,6 +24,8 @@ f = A.FieldState(torch.as_tensor(u, device="cuda"), None, torch.as_tensor(uhat, 
 f.q = A.gradient_refresh(disc, f.u, f.uhat)
 ctx = A.StageContext(50.0, torch.zeros_like(f.u), np.inf, 0.02)
 L = _lib.lib()
+if os.environ.get("MHDG_PREF"):  # A/B: L2 prefetch lookahead of the streamed kernels (pieces)
+    L.mhdg_set_stream_prefetch(int(os.environ["MHDG_PREF"]))
 blocks, _ = A.jacobian(disc, f, ctx)
 del blocks
 torch.cuda.synchronize()
