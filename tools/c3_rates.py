@@ -42,6 +42,7 @@ with _lib.Timeline(16) as tc:
 A.raise_status(st, "condense")
 x = torch.randn(disc.n_trace, dtype=torch.float64, device="cuda")
 b_mac = bench.algorithmic_bytes_per_macro(disc)
+HBM = float(bench.measured_peaks().get("hbm_gbs", 6533.2))  # GB/s, as bench.py
 print(f"C3: {disc.n_mac} macros, n_trace {disc.n_trace}, B_ref {b_mac / 1e3:.1f} KB/macro, "
       f"{b_mac * disc.n_mac / 1e9:.2f} GB/apply")
 print(f"assembly kernel {ta.ms.get('assemble', 0):.2f} ms = {disc.n_mac / ta.ms.get('assemble', 1) * 1e3:.3g} macros/s")
@@ -61,7 +62,7 @@ for name, split, stream in (("split", 1, 1), ("fused", 0, 1), ("generic", 1, 0))
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 10
     print(f"apply {name:8s} {ms:.3f} ms = {disc.n_trace / ms * 1e3:.3g} DOF-applies/s, "
-          f"{b_mac * disc.n_mac / ms / 1e6:.0f} GB/s (B_ref) = {b_mac * disc.n_mac / ms / 1e6 / 6533.2:.3f}")
+          f"{b_mac * disc.n_mac / ms / 1e6:.0f} GB/s (B_ref) = {b_mac * disc.n_mac / ms / 1e6 / HBM:.3f}")
 L.mhdg_set_apply_split(1)
 L.mhdg_set_stream_enabled(1)
 kb = bench.apply_kernel_bytes(disc)
@@ -71,5 +72,5 @@ with _lib.Timeline(256) as tl:
     torch.cuda.synchronize()
 for k, v in tl.ms.items():
     ms = v / tl.counts[k]
-    extra = f", {kb[k] / ms / 1e6:.0f} GB/s = {kb[k] / ms / 1e6 / 6533.2:.2f}" if k in kb else ""
+    extra = f", {kb[k] / ms / 1e6:.0f} GB/s = {kb[k] / ms / 1e6 / HBM:.2f}" if k in kb else ""
     print(f"  {k:12s} {ms:.3f} ms{extra}")
