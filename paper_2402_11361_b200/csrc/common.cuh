@@ -45,6 +45,11 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src, int sr
   const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(src_bytes) : "memory");
 }
+// 16-byte global -> shared async copy through L2 only (src_bytes = 0 zero-fills)
+__device__ __forceinline__ void cp_async16(double* dst, const double* src, int src_bytes) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(src_bytes) : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // global loads / stores with an L2 eviction-priority policy (createpolicy)

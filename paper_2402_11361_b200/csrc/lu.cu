@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(NT, MINB) k_lu4(int n, double* __restrict__ S,
                                                   int* status, int l2mode) {
   using namespace lu4;
   constexpr int NW = NT / 32, PS = pstride<NB>(), NH = NB / 32;  // NH: 32-column halves of a panel
-  extern __shared__ double sm[];
+  extern __shared__ __align__(16) double sm[];
   double* P = sm;                                   // n x PS: the panel, physical rows
   double* cv = P + (size_t)n * PS;                  // [2][NW][SWP] candidate pivot rows
   unsigned long long* ck = reinterpret_cast<unsigned long long*>(cv + 2 * NW * SWP);  // [2][NW] their keys
@@ -190,12 +190,23 @@ __global__ void __launch_bounds__(NT, MINB) k_lu4(int n, double* __restrict__ S,
     const unsigned short* np = npl + lb * n;
     LUT(pt0);
     // ---- panel: the m not-yet-pivoted rows, columns k0 .. k0+nb-1 (zero beyond) ----
-    for (int i = warp; i < m; i += NW) {
-      const int r = np[i];
+    if ((n & 1) == 0) {  // 16-byte copies, two rows per warp pass (rows and k0 even)
+      for (int i = 2 * warp + (lane >> 4); i < m; i += 2 * NW) {
+        const int r = np[i];
 #pragma unroll
-      for (int h = 0; h < NH; ++h) {
-        const int c = 32 * h + lane;
-        cp_async8(P + r * PS + c, A + (size_t)r * n + k0 + (c < nb ? c : 0), c < nb ? 8 : 0);
+        for (int h = 0; h < NH; ++h) {
+          const int c = 32 * h + 2 * (lane & 15);
+          cp_async16(P + r * PS + c, A + (size_t)r * n + k0 + (c < nb ? c : 0), c < nb ? 16 : 0);
+        }
+      }
+    } else {
+      for (int i = warp; i < m; i += NW) {
+        const int r = np[i];
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+          const int c = 32 * h + lane;
+          cp_async8(P + r * PS + c, A + (size_t)r * n + k0 + (c < nb ? c : 0), c < nb ? 8 : 0);
+        }
       }
     }
     cp_async_wait_all();
@@ -212,7 +223,11 @@ __global__ void __launch_bounds__(NT, MINB) k_lu4(int n, double* __restrict__ S,
         act[i] = r < n && !rflag[r];
         act0[i] = act[i];
 #pragma unroll
-        for (int c = 0; c < SW; ++c) x[i][c] = act[i] ? P[r * PS + js + c] : 0.0;
+        for (int c = 0; c < SW; c += 2) {  // 16-byte loads (PS and js even)
+          const double2 v = act[i] ? *reinterpret_cast<const double2*>(P + r * PS + js + c) : make_double2(0.0, 0.0);
+          x[i][c] = v.x;
+          x[i][c + 1] = v.y;
+        }
       }
 #pragma unroll
       for (int jj = 0; jj < SW; ++jj) {
@@ -246,7 +261,8 @@ __global__ void __launch_bounds__(NT, MINB) k_lu4(int n, double* __restrict__ S,
           for (int i = 0; i < RPT; ++i)
             if (act[i] && key_row(key) == tid + NT * i) {
 #pragma unroll
-              for (int c = jj; c < SW; ++c) slot[c] = x[i][c];
+              for (int c = jj & ~1; c < SW; c += 2)  // from column jj (the pair's first entry is unused)
+                *reinterpret_cast<double2*>(slot + c) = make_double2(x[i][c], x[i][c + 1]);
             }
           slot[SW] = rcp;
           if (lane == __ffs(win) - 1) ck[par * NW + warp] = key;
@@ -262,9 +278,18 @@ __global__ void __launch_bounds__(NT, MINB) k_lu4(int n, double* __restrict__ S,
         }
         const int p = key_row(best);
         const double* prow = cv + (par * NW + (p % NT) / 32) * SWP;
-        const double pd = prow[jj];
+        // the pivot row from column jj and its reciprocal in 16-byte loads (slots are 16-byte
+        // aligned: SWP and the panel region are even); 26.1 -> 25.6 ms at C2
+        double pr[SW + 2];
+#pragma unroll
+        for (int c = jj & ~1; c < SW + 2; c += 2) {
+          const double2 v = *reinterpret_cast<const double2*>(prow + c);
+          pr[c] = v.x;
+          pr[c + 1] = v.y;
+        }
+        const double pd = pr[jj];
         if (pd == 0.0) singular = true;
-        const double d = pd == 0.0 ? 0.0 : prow[SW];
+        const double d = pd == 0.0 ? 0.0 : pr[SW];
 #pragma unroll
         for (int i = 0; i < RPT; ++i) {
           if (!act[i]) continue;
@@ -275,7 +300,7 @@ __global__ void __launch_bounds__(NT, MINB) k_lu4(int n, double* __restrict__ S,
           const double l = x[i][jj] * d;
           x[i][jj] = l;
 #pragma unroll
-          for (int c = jj + 1; c < SW; ++c) x[i][c] -= l * prow[c];
+          for (int c = jj + 1; c < SW; ++c) x[i][c] -= l * pr[c];
         }
         if (tid == 0) {
           pv[j] = p;
@@ -288,7 +313,8 @@ __global__ void __launch_bounds__(NT, MINB) k_lu4(int n, double* __restrict__ S,
         if (act0[i]) {
           const int r = tid + NT * i;
 #pragma unroll
-          for (int c = 0; c < SW; ++c) P[r * PS + js + c] = x[i][c];
+          for (int c = 0; c < SW; c += 2)
+            *reinterpret_cast<double2*>(P + r * PS + js + c) = make_double2(x[i][c], x[i][c + 1]);
         }
       __syncthreads();
       LUADD(1, pt1);
@@ -324,9 +350,11 @@ __global__ void __launch_bounds__(NT, MINB) k_lu4(int n, double* __restrict__ S,
             double* pr = P + r * PS;
             double c[2][2];
 #pragma unroll
-            for (int ct = 0; ct < 2; ++ct)
-#pragma unroll
-              for (int e = 0; e < 2; ++e) c[ct][e] = pr[cg + 8 * ct + 2 * t4 + e];
+            for (int ct = 0; ct < 2; ++ct) {
+              const double2 v = *reinterpret_cast<const double2*>(pr + cg + 8 * ct + 2 * t4);
+              c[ct][0] = v.x;
+              c[ct][1] = v.y;
+            }
 #pragma unroll
             for (int ks = 0; ks < SW / 4; ++ks) {
               const double a = pr[js + 4 * ks + t4];
@@ -336,8 +364,7 @@ __global__ void __launch_bounds__(NT, MINB) k_lu4(int n, double* __restrict__ S,
             if (st) {
 #pragma unroll
               for (int ct = 0; ct < 2; ++ct)
-#pragma unroll
-                for (int e = 0; e < 2; ++e) pr[cg + 8 * ct + 2 * t4 + e] = c[ct][e];
+                *reinterpret_cast<double2*>(pr + cg + 8 * ct + 2 * t4) = make_double2(c[ct][0], c[ct][1]);
             }
           }
         }
@@ -349,11 +376,23 @@ __global__ void __launch_bounds__(NT, MINB) k_lu4(int n, double* __restrict__ S,
     LUT(pt3);
     // ---- write the factored panel back; list of the rows still unpivoted; inv(L11) ----
 #pragma unroll 4
-    for (int i = warp; i < m; i += NW) {
-      const int r = np[i];
+    if ((n & 1) == 0) {  // 16-byte stores, two rows per warp pass
+      for (int i = 2 * warp + (lane >> 4); i < m; i += 2 * NW) {
+        const int r = np[i];
 #pragma unroll
-      for (int h = 0; h < NH; ++h)
-        if (32 * h + lane < nb) st_hint1(A + (size_t)r * n + k0 + 32 * h + lane, P[r * PS + 32 * h + lane], pol_final);
+        for (int h = 0; h < NH; ++h) {
+          const int c = 32 * h + 2 * (lane & 15);
+          if (c < nb)
+            st_hint(A + (size_t)r * n + k0 + c, *reinterpret_cast<const double2*>(P + r * PS + c), pol_final);
+        }
+      }
+    } else {
+      for (int i = warp; i < m; i += NW) {
+        const int r = np[i];
+#pragma unroll
+        for (int h = 0; h < NH; ++h)
+          if (32 * h + lane < nb) st_hint1(A + (size_t)r * n + k0 + 32 * h + lane, P[r * PS + 32 * h + lane], pol_final);
+      }
     }
     unsigned short* np2 = npl + (lb ^ 1) * n;
     {
