@@ -20,7 +20,14 @@
 
 namespace mhdg {
 
-constexpr int ASM_THREADS = 256;
+// threads per CTA (one macro per CTA; the work arrays fill shared memory, so one CTA per
+// SM in 3D): measured 2D 256 (512: 18.3 -> 32.2 ms at C2), 3D 768 (256: 224 ms, 384: 188,
+// 512: 170, 768: 159, 1024: 158 with 128 bytes of spills, at C3)
+#ifndef MHDG_ASM_THREADS_3D
+#define MHDG_ASM_THREADS_3D 768
+#endif
+template <int D>
+__host__ __device__ constexpr int asm_threads() { return D == 2 ? 256 : MHDG_ASM_THREADS_3D; }
 
 // W1[q][a] blocks (NS x NS) are stored with stride NS*NS + 4 (2D: 20 doubles): the
 // SUPG product reads W1[q][b][u][t] across (b, t) lanes without bank conflicts
@@ -108,7 +115,7 @@ __device__ __forceinline__ void interp_point(const double* ph, int nb, const int
 }
 
 template <int D>
-__global__ void __launch_bounds__(ASM_THREADS)
+__global__ void __launch_bounds__(asm_threads<D>())
     k_assemble(mhdg_disc g, mhdg_flow flow, mhdg_stage stage, const double* __restrict__ u,
                const double* __restrict__ q, const double* __restrict__ uhat, double* __restrict__ R_grad,
                double* __restrict__ R_state, double* __restrict__ R_tl, int want_jac, mhdg_blocks bk,
@@ -549,7 +556,7 @@ int assemble(const mhdg_disc& g, const mhdg_flow& fl, const mhdg_stage& sg, cons
     fzo = *fo;
   }
   if (fi) fzi = *fi;
-  k_assemble<D><<<g.n_mac, ASM_THREADS, bytes, st>>>(g, fl, sg, u, q, uhat, Rg, Ru, Rtl, want_jac, bb, fzo, fzi,
+  k_assemble<D><<<g.n_mac, asm_threads<D>(), bytes, st>>>(g, fl, sg, u, q, uhat, Rg, Ru, Rtl, want_jac, bb, fzo, fzi,
                                                      fi ? 1 : 0, status, nqc);
   int rc = launch_ok();
   if (rc) return rc;
