@@ -30,6 +30,13 @@ struct Sch2 {
   static constexpr int NT = D == 2 ? 12 : 5;   // n-tiles: L <= 8 NT
   static constexpr int KS = D == 2 ? 8 : 21;   // k-steps: nq D <= 4 KS
   static constexpr int KSF = D == 2 ? 8 : 12;  // face k-steps per sub-face: nqf D <= 4 KSF (3D p <= 3)
+#ifndef MHDG_SCHUR_KB3
+#define MHDG_SCHUR_KB3 7
+#endif
+#ifndef MHDG_SCHUR_KB2
+#define MHDG_SCHUR_KB2 8
+#endif
+  static constexpr int KB = D == 2 ? MHDG_SCHUR_KB2 : MHDG_SCHUR_KB3;  // A-fragment k-steps formed at once (divides KS)
 #ifndef MHDG_SCHUR3_NBUF
 #define MHDG_SCHUR3_NBUF 1
 #endif
@@ -230,30 +237,35 @@ __global__ void __launch_bounds__(Sch2<D>::NWARP * 32, Sch2<D>::MINB) k_schur2(m
           c[nt][0] = (mok && j0 < L) ? crow[j0 * NS] : 0.0;
           c[nt][1] = (mok && j0 + 1 < L) ? crow[(j0 + 1) * NS] : 0.0;
         }
-        // A fragments of this row: T1[m][(q, r') = 4 ks + t4]
-        double af[KS];
+        // A fragments of this row, T1[m][(q, r') = 4 ks + t4], formed KB k-steps at a time (3D:
+        // the 21 k-steps at once spilled registers inside this loop)
         const double* gp = gph + (size_t)(cls * nq) * nloc * D + a * D;
         const double* w = W + (s * NS + r);
+        constexpr int KB = C::KB;
 #pragma unroll
-        for (int ks = 0; ks < KS; ++ks) {
-          const int kq = 4 * ks + t4;
-          double v = 0.0;
-          if (mok && ks < ksv && kq < kvs) {
-            const int q = kq / D, rp = kq - q * D;  // slice-local point; q0 + q in the tables
-            const double* gq = gp + (size_t)(q0 + q) * nloc * D;
-            const double* wq = w + (size_t)q * NW + rp * NS * NS;
+        for (int kb = 0; kb < KS; kb += KB) {
+          double af[KB];
 #pragma unroll
-            for (int k = 0; k < D; ++k) v += gq[k] * wq[k * D * NS * NS];
+          for (int kk = 0; kk < KB; ++kk) {
+            const int ks = kb + kk, kq = 4 * ks + t4;
+            double v = 0.0;
+            if (mok && ks < ksv && kq < kvs) {
+              const int q = kq / D, rp = kq - q * D;  // slice-local point; q0 + q in the tables
+              const double* gq = gp + (size_t)(q0 + q) * nloc * D;
+              const double* wq = w + (size_t)q * NW + rp * NS * NS;
+#pragma unroll
+              for (int k = 0; k < D; ++k) v += gq[k] * wq[k * D * NS * NS];
+            }
+            af[kk] = v;
           }
-          af[ks] = v;
+#pragma unroll
+          for (int kk = 0; kk < KB; ++kk)
+            if (kb + kk < ksv) {
+              const double* pb = PM + (4 * (kb + kk) + t4) * dm.LP + g8;
+#pragma unroll
+              for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(c[nt][0], c[nt][1], af[kk], pb[nt * 8]);
+            }
         }
-#pragma unroll
-        for (int ks = 0; ks < KS; ++ks)
-          if (ks < ksv) {
-            const double* pb = PM + (4 * ks + t4) * dm.LP + g8;
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(c[nt][0], c[nt][1], af[ks], pb[nt * 8]);
-          }
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
           const int j0 = nt * 8 + 2 * t4;
