@@ -32,6 +32,8 @@ class FactorizationError(RuntimeError):
 
 
 class CondensedSchur:
+    capturable = True  # apply_trace only launches kernels on the current stream (CUDA-graph safe)
+
     def __init__(self, blocks: LocalBlocks, lu: torch.Tensor, perm: torch.Tensor, scratch: torch.Tensor,
                  work: torch.Tensor | None = None):
         self.blocks = blocks

@@ -31,3 +31,45 @@ def test_fused_icgs_matches_reference_formulation(n, j):
     # deterministic
     h_b, hv_b, w_b = K._icgs_device(V, j, w)
     assert np.array_equal(h_b, h_dev) and hv_b == hv_dev and torch.equal(w_b, w_dev)
+
+
+def _c1_operator():
+    from paper_2402_11361_b200 import assembly as A
+    from paper_2402_11361_b200.cases import CouettePlane2D
+    from paper_2402_11361_b200.condense import CondensedSchur
+    from paper_2402_11361_b200.discretization import Discretization
+    from paper_2402_11361_b200.mesh import build_square_mesh
+
+    case = CouettePlane2D()
+    d = Discretization(build_square_mesh(case.domain, (8, 4), 2, periodic=(True, False)), 2, case.params,
+                       bcs=case.boundary_conditions())
+    u, uhat = d.nodal_interpolant(case.exact_state)
+    rng = np.random.default_rng(0)
+    u = u + rng.uniform(-1e-3, 1e-3, u.shape)
+    f = A.FieldState(torch.as_tensor(u, device="cuda"), None, torch.as_tensor(uhat, device="cuda"))
+    f.q = A.gradient_refresh(d, f.u, f.uhat)
+    blocks, _ = A.jacobian(d, f, A.StageContext.steady(1.0))
+    return d, CondensedSchur.build(blocks)
+
+
+@pytest.mark.parametrize("solver", ["fgmres", "gmres"])
+def test_graph_captured_arnoldi_steps_are_bitwise_eager(solver, monkeypatch):
+    """The CUDA-graph path of the Arnoldi steps (K._StepGraphs) replays the eager step's
+    kernels on persistent buffers: same solution bit for bit, same iteration and matvec
+    counts, at C1 size (BASELINE configs[0]) over several restarts."""
+    need_gpu()
+    d, cond = _c1_operator()
+    b = torch.as_tensor(np.random.default_rng(3).standard_normal(d.n_trace), device="cuda")
+    cfg = K.KrylovConfig(restart=12, max_iter=200, rel_tol=1e-9, inner_iter=6)
+    runs = {}
+    for on in (False, True):
+        monkeypatch.setattr(K, "KRYLOV_GRAPHS", on)
+        res, nmv = K.solve_trace_system(cond, b, cfg, solver)
+        runs[on] = (res, nmv)
+    (r0, n0), (r1, n1) = runs[False], runs[True]
+    assert r0.iterations == r1.iterations and n0 == n1 and r0.converged == r1.converged
+    assert torch.equal(r0.x, r1.x)
+    assert r0.history == r1.history or all(
+        (a[0] == c[0] and (a[1] == c[1] or (a[1] != a[1] and c[1] != c[1])) and a[2] == c[2])
+        for a, c in zip(r0.history, r1.history))
+    assert r0.iterations > cfg.restart  # the persistent bases are reused across restarts
