@@ -46,3 +46,47 @@ for on in [False, True] * 2:  # the first pair warms up the library and the allo
                       "solve_matvecs": nmv, "us_per_matvec": round(1e6 * t_solve / nmv, 1),
                       "ptc_s": round(t_ptc, 3), "newton": st.iterations, "krylov": st.krylov_iterations,
                       "final_residual": st.residuals[-1]}), flush=True)
+
+# breakdown of one inner step at C1: graph replay + sync, host Givens, eager pieces
+K.KRYLOV_GRAPHS = True
+op, cnt = K.make_counted(cond.apply_trace, capturable=True)
+pre = K.block_precond_build(cond)
+ws = K._StepGraphs(20, d.n_trace, b.device, cnt, False)
+V = ws.V
+V.copy_(torch.randn_like(V))
+body = lambda i: K._icgs_launch(V, i, pre(op(V[i])))  # noqa: E731
+for j in range(8):
+    ws.run(j, body)
+torch.cuda.synchronize()
+
+
+def tm(fn, reps=500):
+    fn()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        fn()
+    torch.cuda.synchronize()
+    return round(1e6 * (time.perf_counter() - t0) / reps, 1)
+
+
+g7 = ws.graphs[7][0]
+out = ws.graphs[7][1][1]
+H = np.random.rand(21, 20)
+cs, sn, gg = np.zeros(20), np.zeros(20), np.zeros(21)
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(200):
+    g7.replay()
+e1.record()
+torch.cuda.synchronize()
+print(json.dumps({
+    "replay_only_us": tm(lambda: g7.replay()),
+    "replay_gpu_us_back_to_back": round(1e3 * e0.elapsed_time(e1) / 200, 1),
+    "replay_fetch_us": tm(lambda: (g7.replay(), K._icgs_fetch(out, 7, d.n_trace))),
+    "eager_step_fetch_us": tm(lambda: K._icgs_fetch(body(7)[1], 7, d.n_trace)),
+    "apply_eager_us": tm(lambda: op(V[3])),
+    "precond_eager_us": tm(lambda: pre(V[3])),
+    "givens_j10_us": tm(lambda: K._givens(H, cs, sn, gg, 10)),
+    "v_update_us": tm(lambda: V.__setitem__(9, V[8] / 1.7)),
+}), flush=True)
