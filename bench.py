@@ -440,6 +440,47 @@ def run_gpu(args, rank, world):
     if dist:
         t_e2e = _max_over_ranks(dist, t_e2e)
 
+    # ---- stored local operators (B_A representation, csrc/ahat.cu): formation + applies ----
+    stored = None
+    if ddisc is None and not args.no_stored:
+        torch.cuda.synchronize()
+        f0, f1 = ev(), ev()
+        f0.record()
+        at = cond.form_local_operators()
+        f1.record()
+        f1.synchronize()
+        t_form = f0.elapsed_time(f1) / 1e3
+        for i in range(W):
+            cond.apply_trace(xs[i], out=y)
+        torch.cuda.synchronize()
+        s0, s1 = ev(), ev()
+        with _lib.Timeline(4 * K + 16) as tl_st:
+            s0.record()
+            for i in range(K):
+                cond.apply_trace(xs[W + i], out=y)
+            s1.record()
+            s1.synchronize()
+        t_st = s0.elapsed_time(s1) / 1e3
+        k_st = tl_st.ms["apply_ahat"] / tl_st.counts["apply_ahat"] / 1e3
+        ltr = disc.nf * disc.Lf * disc.ns
+        b_st = (8 * ltr * ltr + 12 * ltr) * disc.n_mac  # blocks + gathered x and indices + y_loc
+        cond.ahat = None
+        y_mf = cond.apply_trace(xs[0]).clone()
+        cond.ahat = at
+        y_st = cond.apply_trace(xs[0])
+        rel = float((y_st - y_mf).abs().max() / y_mf.abs().max())
+        stored = {"what": "per-macro condensed trace blocks A^{T_i} (B_A, SURVEY 8d), formed once per "
+                          "condensation from ltr unit-trace local applies; apply = batched GEMV k_ahat_gemv + "
+                          "face reduce. Not the headline (value is the matrix-free B_ref apply).",
+                  "value": n_own * K / t_st, "unit": "DOF-applies/s", "ms_per_step": 1e3 * t_st / K,
+                  "form_seconds": t_form,
+                  "break_even_applies": t_form / max(1e-12, t_apply / K - t_st / K),
+                  "kernel": "k_ahat_gemv", "avg_launch_s": k_st, "algorithmic_bytes_per_launch": b_st,
+                  "achieved_gbs": b_st / k_st / 1e9,
+                  "max_rel_diff_vs_matrix_free": rel}
+        del at
+        cond.ahat = None
+
     peaks = measured_peaks()
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     fp64 = fp64_gemm_peak(torch) if rank == 0 else None
@@ -507,11 +548,15 @@ def run_gpu(args, rank, world):
                                              else "explicit S^-1 (the reference's np.linalg.inv), 2 n^3")}},
         "assembly": {"metric": "macro-elements assembled/s (Jacobian + residual)", "value": disc.n_mac / t_asm,
                      "seconds": t_asm, "kernel_seconds": t_asm_k},
+        "apply_stored": stored,
         "e2e": {"value": n_dofs_job / t_e2e, "unit": "DOF-applies/s",
                 "h2d_bytes_per_step": 8 * n_dofs_job, "d2h_bytes_per_step": 8 * n_dofs_job},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
+    if stored is not None:
+        stored["frac"] = stored["achieved_gbs"] / hbm
+        stored["traffic"] = traffic.get("apply_ahat_dram_bytes_per_launch")
     if rank == 0 and not args.no_cpu_baseline:
         v, sdisc, dt = cpu_apply_rate(8, 10, 1)
         line["cpu_baseline"] = {"value": v, "unit": "DOF-applies/s", "cores": 1, "kind": "port",
@@ -531,6 +576,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-stored", action="store_true", help="skip the stored-operator (B_A) side measurement")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -234,6 +234,21 @@ int mhdg_apply_trace(const mhdg_disc *disc, const mhdg_blocks *blocks, const mhd
 int mhdg_apply_trace_local(const mhdg_disc *disc, const mhdg_blocks *blocks,
                            const mhdg_factors *fac, const double *x, double *y_loc, void *stream);
 
+/* Stored local trace operators (B_A representation, csrc/ahat.cu): A^T[m][k][:] = column k
+ * of macro m's condensed trace block (the apply of the unit local trace e_k), for
+ * k < nf*Lf*ns; the blocks the reference's dense_trace_operator assembles
+ * (condense.py:269-290).  at: n_mac*ltr*ltr; x_loc, y_loc: n_mac*ltr scratch; ident:
+ * n_mac*ltr ints of scratch.  Runs ltr local applies. */
+int mhdg_ahat_form(const mhdg_disc *disc, const mhdg_blocks *blocks, const mhdg_factors *fac,
+                   double *at, double *x_loc, double *y_loc, int *ident, void *stream);
+
+/* y = A_hat x from the stored blocks (replaces CondensedSchur.apply_trace,
+ * condense.py:91-103): batched GEMV + face reduction.  y_loc: n_mac*ltr scratch. */
+int mhdg_ahat_apply(const mhdg_disc *disc, const double *at, const double *x, double *y,
+                    double *y_loc, void *stream);
+int mhdg_ahat_apply_local(const mhdg_disc *disc, const double *at, const double *x,
+                          double *y_loc, void *stream);
+
 /* y[dof] = sum of the (one or two) local contributions, in flat-index order. */
 int mhdg_face_reduce(const mhdg_disc *disc, const double *y_loc, double *y, void *stream);
 

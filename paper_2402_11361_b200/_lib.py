@@ -95,6 +95,9 @@ def lib():
             "mhdg_precond_apply": [P(Disc), _dp, _dp, _dp, _dp],
             "mhdg_precond_build_ext": [P(Disc), P(Blocks), _dp, _dp, _dp, _dp],
             "mhdg_side_blocks": [P(Disc), P(Blocks), _dp, _dp, C.c_int, _dp, _dp],
+            "mhdg_ahat_form": [P(Disc), P(Blocks), P(Factors), _dp, _dp, _dp, _dp, _dp],
+            "mhdg_ahat_apply": [P(Disc), _dp, _dp, _dp, _dp, _dp],
+            "mhdg_ahat_apply_local": [P(Disc), _dp, _dp, _dp, _dp],
         }
         for name, args in sigs.items():
             fn = getattr(L, name)
@@ -139,11 +142,12 @@ EXPORTED = (
     "mhdg_packed_lu_size", "mhdg_set_stream_enabled", "mhdg_precond_build_ext", "mhdg_side_blocks",
     "mhdg_apply_work_size", "mhdg_set_apply_split", "mhdg_set_factor_variant", "mhdg_set_lu_variant", "mhdg_set_lu_panel",
     "mhdg_set_lu_l2mode", "mhdg_set_schur_variant", "mhdg_timeline_begin", "mhdg_timeline_end", "mhdg_icgs", "mhdg_icgs_scratch_size",
+    "mhdg_ahat_form", "mhdg_ahat_apply", "mhdg_ahat_apply_local",
 )
 
 
 TIMELINE_SLOTS = ("apply_pre", "apply_si", "apply_post", "apply_fused", "apply_generic", "face_reduce",
-                  "schur", "factor", "pack", "assemble")
+                  "schur", "factor", "pack", "assemble", "apply_ahat")
 
 
 class Timeline:

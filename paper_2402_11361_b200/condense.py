@@ -25,6 +25,11 @@ from .device import current_stream
 # "inverse" (explicit S^-1 by Gauss-Jordan, what the reference's np.linalg.inv stores)
 FACTOR = os.environ.get("MHDG_FACTOR", "lu")
 FACTOR_KINDS = {"inverse": 0, "lu": 1}
+# Trace-operator representation used by apply_trace: "matrix_free" (default: the
+# reference's stored-operator algorithm, B_ref bytes per apply) or "stored" (each macro's
+# condensed trace block A^{T_i}, formed once per condensation by ltr local applies, then
+# one batched GEMV per apply: B_A bytes; csrc/ahat.cu)
+APPLY_REPR = os.environ.get("MHDG_APPLY_REPR", "matrix_free")
 
 
 class FactorizationError(RuntimeError):
@@ -46,6 +51,7 @@ class CondensedSchur:
         fac.work = _lib.ptr(work) if work is not None else None
         fac.kind = FACTOR_KINDS[FACTOR]
         self._fac = fac
+        self.ahat = None  # (n_mac, ltr, ltr) column-major local trace blocks when formed
         dd = blocks.disc.device
         self._y_loc = torch.empty(dd.n_local_trace, dtype=torch.float64, device=dd.device)
 
@@ -74,6 +80,28 @@ class CondensedSchur:
         rc = _lib.lib().mhdg_condense(dd.c, self.blocks.c, self._fac, _lib.ptr(status), current_stream())
         _lib.check(rc, "mhdg_condense")
         raise_status(status, "condense")
+        self.ahat = None
+        if APPLY_REPR == "stored":
+            self.form_local_operators()
+        elif APPLY_REPR != "matrix_free":
+            raise ValueError(f"MHDG_APPLY_REPR={APPLY_REPR!r}: expected 'matrix_free' or 'stored'")
+
+    def form_local_operators(self) -> torch.Tensor:
+        """Per-macro condensed trace blocks A^{T_i} (what dense_trace_operator,
+        condense.py:269-291, assembles), column k = the local apply of the unit trace
+        e_k; stored column-major.  Afterwards apply_trace reads these blocks only."""
+        disc = self.disc
+        dd = disc.device
+        ltr = disc.nf * disc.Lf * disc.ns
+        self.ahat = None
+        at = torch.empty((disc.n_mac, ltr, ltr), dtype=torch.float64, device=dd.device)
+        x_loc = torch.empty(disc.n_mac * ltr, dtype=torch.float64, device=dd.device)
+        ident = torch.empty(disc.n_mac * ltr, dtype=torch.int32, device=dd.device)
+        rc = _lib.lib().mhdg_ahat_form(dd.c, self.blocks.c, self._fac, _lib.ptr(at), _lib.ptr(x_loc),
+                                       _lib.ptr(self._y_loc), _lib.ptr(ident), current_stream())
+        _lib.check(rc, "mhdg_ahat_form")
+        self.ahat = at
+        return at
 
     def refactor_async(self, status: torch.Tensor) -> None:
         """Same as refactor() without the host synchronisation (benchmarks)."""
@@ -108,6 +136,11 @@ class CondensedSchur:
         """Matrix-free action of the reduced trace operator (condense.py:91-103)."""
         dd = self.disc.device
         y = torch.empty_like(x) if out is None else out
+        if self.ahat is not None:
+            rc = _lib.lib().mhdg_ahat_apply(dd.c, _lib.ptr(self.ahat), _lib.ptr(x), _lib.ptr(y),
+                                            _lib.ptr(self._y_loc), current_stream())
+            _lib.check(rc, "mhdg_ahat_apply")
+            return y
         rc = _lib.lib().mhdg_apply_trace(dd.c, self.blocks.c, self._fac, _lib.ptr(x), _lib.ptr(y),
                                          _lib.ptr(self._y_loc), current_stream())
         _lib.check(rc, "mhdg_apply_trace")
@@ -115,8 +148,12 @@ class CondensedSchur:
 
     def apply_trace_local(self, x: torch.Tensor) -> torch.Tensor:
         dd = self.disc.device
-        rc = _lib.lib().mhdg_apply_trace_local(dd.c, self.blocks.c, self._fac, _lib.ptr(x),
-                                               _lib.ptr(self._y_loc), current_stream())
+        if self.ahat is not None:
+            rc = _lib.lib().mhdg_ahat_apply_local(dd.c, _lib.ptr(self.ahat), _lib.ptr(x), _lib.ptr(self._y_loc),
+                                                  current_stream())
+        else:
+            rc = _lib.lib().mhdg_apply_trace_local(dd.c, self.blocks.c, self._fac, _lib.ptr(x),
+                                                   _lib.ptr(self._y_loc), current_stream())
         _lib.check(rc, "mhdg_apply_trace_local")
         return self._y_loc.view(self.disc.n_mac, self.disc.nf, self.disc.Lf, self.disc.ns).clone()
 

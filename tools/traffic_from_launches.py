@@ -22,7 +22,8 @@ def slot(name):
         return {"1": "apply_pre", "2": "apply_post", "0": "apply_fused"}.get(part)
     for pat, key in (("k_lu_warp", "apply_si"), ("k_si_stream", "apply_si"), ("k_schur2", "schur"),
                      ("k_schur_mma", "schur"), ("k_pack_lu4", "pack"), ("k_pack_inv_rows", "pack"),
-                     ("k_lu4", "factor"), ("k_gj3", "factor"), ("k_face_reduce", "face_reduce")):
+                     ("k_lu4", "factor"), ("k_gj3", "factor"), ("k_face_reduce", "face_reduce"),
+                     ("k_ahat_gemv", "apply_ahat")):
         if pat in name:
             return key
     return None
