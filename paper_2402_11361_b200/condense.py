@@ -28,7 +28,9 @@ FACTOR_KINDS = {"inverse": 0, "lu": 1}
 # Trace-operator representation used by apply_trace: "matrix_free" (default: the
 # reference's stored-operator algorithm, B_ref bytes per apply) or "stored" (each macro's
 # condensed trace block A^{T_i}, formed once per condensation by ltr local applies, then
-# one batched GEMV per apply: B_A bytes; csrc/ahat.cu)
+# one batched GEMV per apply: B_A bytes; csrc/ahat.cu) or "auto"
+# (matrix-free until ltr applies have run on this condensation -- about what forming the
+# blocks costs -- then stored: never more than twice the cheaper choice in hindsight)
 APPLY_REPR = os.environ.get("MHDG_APPLY_REPR", "matrix_free")
 
 
@@ -52,6 +54,7 @@ class CondensedSchur:
         fac.kind = FACTOR_KINDS[FACTOR]
         self._fac = fac
         self.ahat = None  # (n_mac, ltr, ltr) column-major local trace blocks when formed
+        self._n_applies = 0
         dd = blocks.disc.device
         self._y_loc = torch.empty(dd.n_local_trace, dtype=torch.float64, device=dd.device)
 
@@ -81,10 +84,24 @@ class CondensedSchur:
         _lib.check(rc, "mhdg_condense")
         raise_status(status, "condense")
         self.ahat = None
+        self._n_applies = 0
         if APPLY_REPR == "stored":
             self.form_local_operators()
-        elif APPLY_REPR != "matrix_free":
-            raise ValueError(f"MHDG_APPLY_REPR={APPLY_REPR!r}: expected 'matrix_free' or 'stored'")
+        elif APPLY_REPR not in ("matrix_free", "auto"):
+            raise ValueError(f"MHDG_APPLY_REPR={APPLY_REPR!r}: expected 'matrix_free', 'stored' or 'auto'")
+
+    def note_applies(self, k: int = 1) -> bool:
+        """Count applies on this condensation; under MHDG_APPLY_REPR=auto form the stored
+        blocks once ltr applies have run.  Returns True when the representation changed
+        (callers holding CUDA graphs of the apply recapture).  Never forms inside a capture."""
+        self._n_applies += k
+        if APPLY_REPR != "auto" or self.ahat is not None or torch.cuda.is_current_stream_capturing():
+            return False
+        disc = self.disc
+        if self._n_applies < disc.nf * disc.Lf * disc.ns:
+            return False
+        self.form_local_operators()
+        return True
 
     def form_local_operators(self) -> torch.Tensor:
         """Per-macro condensed trace blocks A^{T_i} (what dense_trace_operator,
@@ -136,6 +153,7 @@ class CondensedSchur:
         """Matrix-free action of the reduced trace operator (condense.py:91-103)."""
         dd = self.disc.device
         y = torch.empty_like(x) if out is None else out
+        self.note_applies(1)
         if self.ahat is not None:
             rc = _lib.lib().mhdg_ahat_apply(dd.c, _lib.ptr(self.ahat), _lib.ptr(x), _lib.ptr(y),
                                             _lib.ptr(self._y_loc), current_stream())

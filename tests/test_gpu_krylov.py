@@ -73,3 +73,23 @@ def test_graph_captured_arnoldi_steps_are_bitwise_eager(solver, monkeypatch):
         (a[0] == c[0] and (a[1] == c[1] or (a[1] != a[1] and c[1] != c[1])) and a[2] == c[2])
         for a, c in zip(r0.history, r1.history))
     assert r0.iterations > cfg.restart  # the persistent bases are reused across restarts
+
+
+def test_auto_stored_representation_mid_solve(monkeypatch):
+    """MHDG_APPLY_REPR=auto: the stored local blocks are formed after ltr applies, in the
+    middle of the FGMRES solve (graphs recaptured against the new apply); the solve agrees
+    with the matrix-free one (iterations within 1, solution to 1e-8)."""
+    need_gpu()
+    from paper_2402_11361_b200 import condense as CD
+
+    d, cond = _c1_operator()
+    b = torch.as_tensor(np.random.default_rng(5).standard_normal(d.n_trace), device="cuda")
+    cfg = K.KrylovConfig(rel_tol=1e-10, max_iter=400)
+    r0, n0 = K.solve_trace_system(cond, b, cfg, "fgmres")
+    assert cond.ahat is None
+    monkeypatch.setattr(CD, "APPLY_REPR", "auto")
+    cond._n_applies = 0
+    r1, n1 = K.solve_trace_system(cond, b, cfg, "fgmres")
+    assert cond.ahat is not None and n1 > d.nf * d.Lf * d.ns
+    assert abs(r0.iterations - r1.iterations) <= 1 and r1.converged
+    assert float((r1.x - r0.x).abs().max() / r0.x.abs().max()) < 1e-8

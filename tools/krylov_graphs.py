@@ -25,8 +25,11 @@ g = load_golden("c1_ptc_oracle")
 case = CouettePlane2D()
 d = Discretization(build_square_mesh(case.domain, (8, 4), 2, periodic=(True, False)), 2, case.params,
                    bcs=case.boundary_conditions())
-for on in [False, True] * 2:  # the first pair warms up the library and the allocator
+from paper_2402_11361_b200 import condense as CD  # noqa: E402
+
+for on, repr_ in [(False, "matrix_free"), (True, "matrix_free")] * 2 + [(True, "auto"), (False, "auto")]:
     K.KRYLOV_GRAPHS = on
+    CD.APPLY_REPR = repr_
     f = A.to_device_fields(d, g["u0"], g["q0"], g["uhat0"])
     blocks, _ = A.jacobian(d, f, A.StageContext.steady(1.0))
     cond = CondensedSchur.build(blocks)
@@ -42,13 +45,15 @@ for on in [False, True] * 2:  # the first pair warms up the library and the allo
     st, _ = S.ptc_steady_solve(d, f, rel_tol=1e-10)
     torch.cuda.synchronize()
     t_ptc = time.perf_counter() - t0
-    print(json.dumps({"graphs": on, "solve_s": round(t_solve, 4), "solve_fgmres_iters": res.iterations,
+    print(json.dumps({"graphs": on, "apply_repr": repr_, "solve_s": round(t_solve, 4), "solve_fgmres_iters": res.iterations,
                       "solve_matvecs": nmv, "us_per_matvec": round(1e6 * t_solve / nmv, 1),
                       "ptc_s": round(t_ptc, 3), "newton": st.iterations, "krylov": st.krylov_iterations,
                       "final_residual": st.residuals[-1]}), flush=True)
 
 # breakdown of one inner step at C1: graph replay + sync, host Givens, eager pieces
 K.KRYLOV_GRAPHS = True
+CD.APPLY_REPR = "matrix_free"
+cond.ahat = None
 op, cnt = K.make_counted(cond.apply_trace, capturable=True)
 pre = K.block_precond_build(cond)
 ws = K._StepGraphs(20, d.n_trace, b.device, cnt, False)
