@@ -74,3 +74,28 @@ for k, v in tl.ms.items():
     ms = v / tl.counts[k]
     extra = f", {kb[k] / ms / 1e6:.0f} GB/s = {kb[k] / ms / 1e6 / HBM:.2f}" if k in kb else ""
     print(f"  {k:12s} {ms:.3f} ms{extra}")
+
+# stored local operators (B_A): formation time, apply rate, agreement with the matrix-free apply
+if os.environ.get("MHDG_C3_STORED", "1") != "0":
+    y_mf = cond.apply_trace(x).clone()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    at = cond.form_local_operators()
+    e1.record()
+    torch.cuda.synchronize()
+    t_form = e0.elapsed_time(e1)
+    ltr = disc.nf * disc.Lf * disc.ns
+    b_st = (8 * ltr * ltr + 12 * ltr) * disc.n_mac
+    for _ in range(2):
+        y_st = cond.apply_trace(x)
+    torch.cuda.synchronize()
+    rel = float((y_st - y_mf).abs().max() / y_mf.abs().max())
+    e0.record()
+    for _ in range(10):
+        cond.apply_trace(x)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 10
+    print(f"apply stored   {ms:.3f} ms = {disc.n_trace / ms * 1e3:.3g} DOF-applies/s, {b_st / ms / 1e6:.0f} GB/s "
+          f"(B_A {b_st / disc.n_mac / 1e3:.1f} KB/macro) = {b_st / ms / 1e6 / HBM:.3f}; formation {t_form:.1f} ms; "
+          f"max rel diff vs matrix-free {rel:.2e}")
