@@ -546,13 +546,16 @@ __global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 ? 1 : 2)) k_apply_s
           const int s = idx % NS, a = (idx / NS) % NLOC, K = idx / (NS * NLOC);
           const double* G = g.grad_cls + (size_t)gco[K] * TS::CLS + a * D;
           const double* w = wv + K * NQ * DN + s;
-          double a0 = 0.0, a1 = 0.0;
-#pragma unroll 3
+          double ar[D] = {};  // one chain per direction r: D independent FMA chains
+#pragma unroll 9
           for (int q = 0; q < NQ; ++q) {
 #pragma unroll
-            for (int r = 0; r < D; ++r) ((q & 1) ? a1 : a0) += __ldg(G + q * NLOC * D + r) * w[(q * D + r) * NS];
+            for (int r = 0; r < D; ++r) ar[r] += __ldg(G + q * NLOC * D + r) * w[(q * D + r) * NS];
           }
-          cv[idx] = a0 + a1;
+          double sum = ar[0];
+#pragma unroll
+          for (int r = 1; r < D; ++r) sum += ar[r];
+          cv[idx] = sum;
         }
       } else {
         // gphys per gradient class once per macro (in z, dead by now, when it fits; else after the
