@@ -83,6 +83,10 @@ class CondensedSchur:
         rc = _lib.lib().mhdg_condense(dd.c, self.blocks.c, self._fac, _lib.ptr(status), current_stream())
         _lib.check(rc, "mhdg_condense")
         raise_status(status, "condense")
+        self._reset_representation()
+
+    def _reset_representation(self) -> None:
+        """New factors: drop stale stored blocks; form them again under MHDG_APPLY_REPR=stored."""
         self.ahat = None
         self._n_applies = 0
         if APPLY_REPR == "stored":
@@ -125,6 +129,7 @@ class CondensedSchur:
         dd = self.disc.device
         rc = _lib.lib().mhdg_condense(dd.c, self.blocks.c, self._fac, _lib.ptr(status), current_stream())
         _lib.check(rc, "mhdg_condense")
+        self._reset_representation()
 
     @property
     def disc(self):
