@@ -197,6 +197,12 @@ def test_streamed_apply_3d_m1_vs_oracle(p_deg):
             x = rng.standard_normal(d.n_trace)
             assert rel_err(host(cond.apply_trace(dev(x))), ocond.apply_trace(x)) < 1e-9
     assert "apply_pre" in tl.ms and "apply_generic" not in tl.ms  # the streamed kernels ran
+    cond.form_local_operators()  # stored blocks from these streamed kernels (odd W_vol segments at p = 2)
+    with _lib.Timeline(16) as tl:
+        for _ in range(2):
+            x = rng.standard_normal(d.n_trace)
+            assert rel_err(host(cond.apply_trace(dev(x))), ocond.apply_trace(x)) < 1e-9
+    assert "apply_ahat" in tl.ms and "apply_pre" not in tl.ms
 
 
 @pytest.mark.parametrize("name", sorted(OP_CASES))
