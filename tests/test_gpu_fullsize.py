@@ -84,6 +84,12 @@ def test_full_size_apply_properties(cfg):
     # 1e-11: the LU forward/back substitution rounds at cond(S) * eps level (cond(S) ~ 1e6
     # at m=4, p=3); the explicit-inverse GEMV stays below 1e-12
     assert _rel(y12, 2.0 * y_split - 3.0 * cond.apply_trace(x2)) < 1e-11
+    if cfg == "C2":  # stored local operators at full size (1.6 GB of blocks): same operator
+        cond.form_local_operators()
+        y_st = cond.apply_trace(x1).clone()
+        assert torch.equal(y_st, cond.apply_trace(x1))
+        assert _rel(y_st, y_split) < 1e-10
+        cond.ahat = None
     # rhs / recover consistency: the Newton correction (du, dq, dx) of the full
     # local system with dx = x1 satisfies A_hat dx - b = (trace residual of the
     # recovered correction), i.e. apply_trace(x) - rhs is linear in x with the
