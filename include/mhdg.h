@@ -26,6 +26,9 @@
  * gradient dof (l*L+node)*ns+s, trace dof (f*Lf+g)*ns+s, local trace
  * (mac, lf, g, s).  Blocks use the LocalBlocks shapes of assembly.py:293-312.
  *
+ * Diagnostic A/B knobs (kernel variants for cross-checks) are not part of
+ * this ABI; they live in paper_2402_11361_b200/csrc/mhdg_tuning.h.
+ *
  * Errors: the return value is MHDG_OK or MHDG_ERR_CUDA (launch failure).
  * Data-dependent failures are reported through the device status word
  * `status` (mhdg_status, int32[4]): code, macro/face index, component, and
@@ -133,14 +136,21 @@ typedef struct {
   double *face_visc_state;   /* n_mac*nf*(n_tri nqf)*ns */
 } mhdg_frozen;
 
-/* condensed operator S = A_uu - A_uq A_qq^-1 A_qu (n = L*ns).  `lu` holds
-   each macro's explicit inverse S^-1 in the tiled order of
-   csrc/tiled_inv.cuh (mhdg_packed_lu_size(n) doubles per macro: 64-row
-   blocks of 32-column tiles), computed by Gauss-Jordan with partial
-   pivoting; perm is the pivot workspace; `scratch` (n_mac*n*n) holds S before
-   inversion.  `work` (mhdg_apply_work_size doubles, or NULL) holds the
-   per-macro hand-off vectors of the split apply (pre -> S^-1 stream -> post);
-   with NULL the fused single-kernel apply runs. */
+/* condensed operator S = A_uu - A_uq A_qq^-1 A_qu (n = L*ns), factored per
+   macro into `lu` (mhdg_packed_lu_size(n) doubles per macro) according to
+   `kind`:
+     kind 1 (default): LU with partial pivoting (the rows never move; perm[k]
+       = physical row of logical pivot k), packed in block-triangular solve
+       order (csrc/packed_lu.cuh): per 64-row block the L panel and inv(L_bb)
+       for the forward sweep, then the U panel and inv(U_bb) for the backward
+       sweep, column-major inside panels and triangles;
+     kind 0: the explicit inverse S^-1 (what the reference's np.linalg.inv
+       stores, condense.py:67) by Gauss-Jordan with partial pivoting, in the
+       tiled order of csrc/tiled_inv.cuh (64-row blocks of 32-column tiles).
+   `scratch` (n_mac*n*n) holds S before factorization.  `work`
+   (mhdg_apply_work_size doubles, or NULL) holds the per-macro hand-off
+   vectors of the split apply (pre -> factor solve -> post); with NULL the
+   fused single-kernel apply runs. */
 typedef struct {
   double *lu;                /* n_mac*mhdg_packed_lu_size(n) */
   int *perm;                 /* n_mac*n */
@@ -150,53 +160,46 @@ typedef struct {
                                 1: packed LU (csrc/packed_lu.cuh), perm = pivot rows */
 } mhdg_factors;
 
+/* Largest local Schur size n = L*ns the factor kernels take for factor `kind`
+   (mhdg_factors.kind); mhdg_condense returns MHDG_ERR_CONFIG above it. */
+int mhdg_factor_max_n(int kind);
+
 /* doubles of mhdg_factors.work for this discretization */
 long long mhdg_apply_work_size(const mhdg_disc *disc);
 
 /* One ICGS Arnoldi orthogonalisation (krylov.py:51-58): with V_j = rows 0..j of
    V (row stride ldv), h = V_j w; w -= V_j^T h; h2 = V_j w; w -= V_j^T h2;
    out[0..j] = h + h2, out[j+1] = ||w|| (w updated in place).  Three fused
-   passes over V_j, deterministic reductions; j <= 62.  scratch:
-   mhdg_icgs_scratch_size(n) doubles. */
+   streaming passes over V_j (mhdg_vec_pass modes 0, 1, 2), any n,
+   deterministic reductions (the result depends on n only); j <= 62.
+   scratch: mhdg_icgs_scratch_size(n) doubles, zeroed once before first use
+   (the passes leave their completion ticket re-armed). */
 int mhdg_icgs(int n, int j, const double *V, long long ldv, double *w, double *out, double *scratch,
               void *stream);
 long long mhdg_icgs_scratch_size(int n);
+
+/* One streaming pass of the Krylov vector algebra over rows 0..rows-1 of V
+   (row stride ldv; rows <= 64) and the n-vector w, deterministic:
+     mode 0: out[i] = V_i . w                        (the dots of krylov.py:53, 55)
+     mode 1: w -= sum_i coef[i] V_i; out[i] = V_i . w (ICGS update + re-orthogonalisation dots)
+     mode 2: w -= sum_i coef[i] V_i; out[0] = w . w
+     mode 3: w += sum_i coef[i] V_i                  (x + V^T y, krylov.py:121-122, 188-189)
+     mode 4: out[0] = w . w                          (squared norms, krylov.py:72-168)
+   Sums are this device's partial sums (a distributed caller allreduces `out`);
+   coef and out are device arrays.  scratch as for mhdg_icgs. */
+int mhdg_vec_pass(long long n, int rows, const double *V, long long ldv, double *w, const double *coef, int mode,
+                  double *out, double *scratch, void *stream);
 
 /* Per-kernel timeline: while enabled, the library records a CUDA event pair
    around each of its kernels on the caller's stream (capacity = max records).
    mhdg_timeline_end synchronises, disables recording and returns, per slot,
    the summed milliseconds and the record counts (16 slots: 0 apply pre,
-   1 apply S^-1 stream, 2 apply post, 3 fused apply, 4 generic apply, 5 face
-   reduce, 6 Schur complement, 7 inverse factor, 8 factor tiling, 9 assembly). */
+   1 apply factor solve, 2 apply post, 3 fused apply, 4 generic apply, 5 face
+   reduce, 6 Schur complement, 7 factorization, 8 factor packing, 9 assembly,
+   10 stored-operator apply, 11 ICGS, 12 preconditioner build, 13
+   preconditioner apply, 14 halo pack/unpack). */
 int mhdg_timeline_begin(int capacity);
 int mhdg_timeline_end(double *ms, int *counts);
-
-/* Gauss-Jordan variant of mhdg_lu_factor: 3 (default) keeps pivot rows in
-   place, 2 interchanges rows (the earlier kernel).  For A/B measurements. */
-void mhdg_set_factor_variant(int v);
-
-/* Batched LU kernel of the packed-LU factor kind: 4 (default) register
-   sub-panels + warp-chunked DMMA trailing updates, 3 the earlier kernel.
-   For A/B measurements. */
-void mhdg_set_lu_variant(int v);
-
-/* Panel width of k_lu4: 32 (default; 192 threads, two CTAs per SM) or 64 (one CTA
-   per SM; threads 256 or 384).  For A/B measurements. */
-void mhdg_set_lu_panel(int nb, int threads);
-
-/* L2 priority of k_lu4's trailing-update traffic: evict_last on the macros with
-   mac % mode != 0 (mode >= 2; default 2 = every other macro), on all (1) or none
-   (0).  For A/B measurements. */
-void mhdg_set_lu_l2mode(int mode);
-
-/* Schur-complement kernel: 0 (default) stage-pipelined FP64 tensor-core kernel,
-   1 the earlier tensor-core kernel, otherwise the per-macro FFMA kernel.  For A/B
-   measurements. */
-void mhdg_set_schur_variant(int v);
-
-/* 1 (default): split apply (pre / S^-1 stream / post kernels) when `work` is
-   set; 0: fused single-kernel apply.  For A/B measurements. */
-void mhdg_set_apply_split(int on);
 
 /* doubles per macro of the factor buffer (either kind) */
 long long mhdg_packed_lu_size(int n);
@@ -288,13 +291,6 @@ int mhdg_side_blocks(const mhdg_disc *disc, const mhdg_blocks *blocks, const int
 /* y = blockdiag(inv) v (krylov.py:234-236). */
 int mhdg_precond_apply(const mhdg_disc *disc, const double *inv, const double *v, double *y,
                        void *stream);
-
-/* 1 (default): use the compile-time specialised TMA-streamed apply kernel when
-   one matches (dim, m, p); 0: always the generic kernel (cross-checks). */
-void mhdg_set_stream_enabled(int on);
-
-/* L2 prefetch lookahead (pieces) of the streamed apply; 0 (default) = shared-memory ring only. */
-void mhdg_set_stream_prefetch(int pieces);
 
 /* number of kernel launches issued by this library since load (diagnostics) */
 long long mhdg_launch_count(void);

@@ -894,6 +894,7 @@ class NewtonStats:
     dtau: list = field(default_factory=list)
     krylov_matvecs: int = 0
     krylov_iterations: int = 0
+    krylov_per_step: list = field(default_factory=list)
     linear_converged: int = 0
     timings: dict = field(default_factory=lambda: {"assembly": 0.0, "condense": 0.0, "krylov": 0.0,
                                                    "recover": 0.0})
@@ -904,7 +905,12 @@ def full_norm(res):
 
 
 def newton_solve(disc, fields, ctx, krylov_cfg=None, solver="fgmres", abs_tol=1e-12, rel_tol=1e-6,
-                 max_newton=60, ptc=None, max_retries=10):
+                 max_newton=60, ptc=None, max_retries=10, log=None, mode="inv"):
+    """stepper.py:138-224.  ``mode`` picks the Schur factor representation
+    ("inv": the reference's explicit inverse, condense.py:67; "lu": LAPACK LU
+    solves, the algebra of the device's default packed-LU factors); ``log(st,
+    fields)`` is called after every accepted step (the reference's ``log(stats)``
+    hook, stepper.py:220-221, plus the accepted state for per-step goldens)."""
     cfg = krylov_cfg or KrylovConfig()
     st = NewtonStats()
     res = residual(disc, fields, ctx)
@@ -928,7 +934,7 @@ def newton_solve(disc, fields, ctx, krylov_cfg=None, solver="fgmres", abs_tol=1e
                 t0 = time.perf_counter()
                 blocks, _ = jacobian(disc, fields, cur)
                 t1 = time.perf_counter()
-                cond = condense(blocks)
+                cond = condense(blocks, mode=mode)
                 t2 = time.perf_counter()
                 b = cond.rhs(*res)
                 lin, nmv = solve_trace_system(cond, b, cfg, solver)
@@ -958,23 +964,28 @@ def newton_solve(disc, fields, ctx, krylov_cfg=None, solver="fgmres", abs_tol=1e
         st.res_u.append(float(np.linalg.norm(res[1])))
         if ptc is not None:
             ptc.update(st.res_u[-1])
+        st.krylov_per_step.append(st.krylov_iterations - sum(st.krylov_per_step))
+        if log is not None:
+            log(st, fields)
     else:
         st.converged = rn <= target
     return st
 
 
 def ptc_steady_solve(disc, fields, krylov_cfg=None, solver="fgmres", abs_tol=1e-10, rel_tol=1e-8,
-                     max_newton=120, tau_init=1.0, tau_max=1e8, ser_printed_ratio=False):
+                     max_newton=120, tau_init=1.0, tau_max=1e8, ser_printed_ratio=False, log=None, mode="inv"):
+    """stepper.py:227-262 (``mode``/``log`` as in newton_solve)."""
     ptc = PtcState(dtau=tau_init, tau_init=tau_init, tau_max=tau_max, printed_ratio=ser_printed_ratio)
     st = newton_solve(disc, fields, Ctx.steady(), krylov_cfg=krylov_cfg, solver=solver, abs_tol=abs_tol,
-                      rel_tol=rel_tol, max_newton=max_newton, ptc=ptc)
+                      rel_tol=rel_tol, max_newton=max_newton, ptc=ptc, log=log, mode=mode)
     if not st.converged:
         raise NonConvergenceError(f"steady solve stalled at {st.residuals[-1]:.3e}")
     return st, ptc
 
 
 def dirk_advance(disc, fields, dt, tableau, krylov_cfg=None, solver="fgmres", abs_tol=1e-12, rel_tol=1e-8,
-                 max_newton=30, max_dt_retries=4):
+                 max_newton=30, max_dt_retries=4, mode="inv"):
+    """stepper.py:265-328 (``mode`` as in newton_solve)."""
     if abs(tableau.c[-1] - 1.0) > 1e-12:
         raise NotImplementedError("tableaus with c_s != 1 require a trailing trace/gradient solve")
     d, e = tableau.d, tableau.e
@@ -987,7 +998,7 @@ def dirk_advance(disc, fields, dt, tableau, krylov_cfg=None, solver="fgmres", ab
             for i in range(tableau.stages):
                 ctx = Ctx.dirk_stage(dt_cur, d[i], i, stages, u_old)
                 st = newton_solve(disc, fields, ctx, krylov_cfg=krylov_cfg, solver=solver, abs_tol=abs_tol,
-                                  rel_tol=rel_tol, max_newton=max_newton)
+                                  rel_tol=rel_tol, max_newton=max_newton, mode=mode)
                 if not st.converged:
                     raise NonConvergenceError(f"stage {i} did not converge")
                 all_st.append(st)

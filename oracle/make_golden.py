@@ -128,13 +128,20 @@ def dirk_case(name, case, n, m, p, dt, steps):
     f = rd.interpolate(case.initial_state)
     out = dict(versions=_versions(), n_ele=n, m=m, p=p, dt=dt, steps=steps, u0=f.u.copy(), q0=f.q.copy(),
                uhat0=f.uhat.copy())
-    newton, kits, mvs = [], [], []
+    newton, kits, mvs, step_u, step_uhat, secs = [], [], [], [], [], []
+    import time
+
     for _ in range(steps):
+        t0 = time.perf_counter()
         sts, _dt = RS.dirk_advance(rd, f, dt, RS.DirkTableau.dirk33())
+        secs.append(time.perf_counter() - t0)
         newton += [s.iterations for s in sts]
         kits += [s.krylov_iterations for s in sts]
         mvs += [s.krylov_matvecs for s in sts]
-    out.update(u=f.u, q=f.q, uhat=f.uhat, newton=np.array(newton), krylov=np.array(kits), matvecs=np.array(mvs))
+        step_u.append(f.u.copy())
+        step_uhat.append(f.uhat.copy())
+    out.update(u=f.u, q=f.q, uhat=f.uhat, newton=np.array(newton), krylov=np.array(kits), matvecs=np.array(mvs),
+               step_u=np.stack(step_u), step_uhat=np.stack(step_uhat), seconds=np.array(secs))
     np.savez_compressed(os.path.join(OUT, name + ".npz"), **out)
     print("wrote", name, newton, kits, mvs)
 
@@ -201,10 +208,16 @@ def main():
         operator_case("op_wall_m1p2", tgv, tgv.domain, 2, 1, 2, (True, False, True), walls, None, "ptc", False)
         operator_case("op_couette_m2p1", cou, ((0, 0, 0), (1, 1, 1)), 1, 2, 1, (False,) * 3,
                       cou.boundary_conditions(), cou.source, "ptc", True)
+    if want("op23"):
+        # n = L ns = 420 > 384: the larger-n batched LU path (C5 (m, p) = (2, 3))
+        operator_case("op_tgv_m2p3", tgv, tgv.domain, 1, 2, 3, (True,) * 3, None, None, "dirk", False)
     if want("krylov"):
         krylov_case("krylov_tgv_m1p2", tgv, 1, 1, 2)
     if want("dirk"):
         dirk_case("dirk_tgv_m2p2", tgv, 1, 2, 2, 0.01, 1)
+    if want("dirk48"):
+        # a C3 slab: BASELINE configs[2]'s case, tableau, dt and (m, p) on 2^3 x 6 = 48 macros
+        dirk_case("dirk_tgv_n2_m2p2", tgv, 2, 2, 2, 0.01, 2)
     if want("ptc"):
         ptc_case("ptc_couette_m2p1", cou, 1, 2, 1)
 

@@ -105,6 +105,8 @@ def lib():
             fn.restype = C.c_int
         L.mhdg_set_stream_enabled.argtypes = [C.c_int]
         L.mhdg_set_stream_enabled.restype = None
+        L.mhdg_factor_max_n.argtypes = [C.c_int]
+        L.mhdg_factor_max_n.restype = C.c_int
         L.mhdg_packed_lu_size.argtypes = [C.c_int]
         L.mhdg_packed_lu_size.restype = C.c_longlong
         L.mhdg_launch_count.argtypes = []
@@ -113,10 +115,8 @@ def lib():
         L.mhdg_apply_work_size.restype = C.c_longlong
         L.mhdg_set_apply_split.argtypes = [C.c_int]
         L.mhdg_set_apply_split.restype = None
-        L.mhdg_set_factor_variant.argtypes = [C.c_int]
-        L.mhdg_set_factor_variant.restype = None
-        L.mhdg_set_lu_variant.argtypes = [C.c_int]
-        L.mhdg_set_lu_variant.restype = None
+        L.mhdg_set_stream_prefetch.argtypes = [C.c_int]
+        L.mhdg_set_stream_prefetch.restype = None
         L.mhdg_set_lu_panel.argtypes = [C.c_int, C.c_int]
         L.mhdg_set_lu_panel.restype = None
         L.mhdg_set_lu_l2mode.argtypes = [C.c_int]
@@ -125,6 +125,8 @@ def lib():
         L.mhdg_set_schur_variant.restype = None
         L.mhdg_icgs.argtypes = [C.c_int, C.c_int, _dp, C.c_longlong, _dp, _dp, _dp, _dp]
         L.mhdg_icgs.restype = C.c_int
+        L.mhdg_vec_pass.argtypes = [C.c_longlong, C.c_int, _dp, C.c_longlong, _dp, _dp, C.c_int, _dp, _dp, _dp]
+        L.mhdg_vec_pass.restype = C.c_int
         L.mhdg_icgs_scratch_size.argtypes = [C.c_int]
         L.mhdg_icgs_scratch_size.restype = C.c_longlong
         L.mhdg_timeline_begin.argtypes = [C.c_int]
@@ -135,19 +137,26 @@ def lib():
     return _lib
 
 
+# the drop-in C ABI (include/mhdg.h)
 EXPORTED = (
     "mhdg_assemble", "mhdg_condense", "mhdg_schur_matrix", "mhdg_lu_factor", "mhdg_lu_solve",
     "mhdg_apply_trace", "mhdg_apply_trace_local", "mhdg_face_reduce", "mhdg_condensed_rhs", "mhdg_recover",
     "mhdg_gradient_refresh", "mhdg_precond_build", "mhdg_precond_apply", "mhdg_launch_count",
-    "mhdg_packed_lu_size", "mhdg_set_stream_enabled", "mhdg_precond_build_ext", "mhdg_side_blocks",
-    "mhdg_apply_work_size", "mhdg_set_apply_split", "mhdg_set_factor_variant", "mhdg_set_lu_variant", "mhdg_set_lu_panel",
-    "mhdg_set_lu_l2mode", "mhdg_set_schur_variant", "mhdg_timeline_begin", "mhdg_timeline_end", "mhdg_icgs", "mhdg_icgs_scratch_size",
-    "mhdg_ahat_form", "mhdg_ahat_apply", "mhdg_ahat_apply_local",
+    "mhdg_packed_lu_size", "mhdg_precond_build_ext", "mhdg_side_blocks",
+    "mhdg_apply_work_size", "mhdg_timeline_begin", "mhdg_timeline_end", "mhdg_icgs", "mhdg_icgs_scratch_size",
+    "mhdg_ahat_form", "mhdg_ahat_apply", "mhdg_ahat_apply_local", "mhdg_factor_max_n",
+    "mhdg_vec_pass",
+)
+# diagnostic A/B knobs (csrc/mhdg_tuning.h; not part of the drop-in ABI)
+TUNING = (
+    "mhdg_set_schur_variant", "mhdg_set_lu_panel", "mhdg_set_lu_l2mode", "mhdg_set_apply_split",
+    "mhdg_set_stream_enabled", "mhdg_set_stream_prefetch", "mhdg_stream_grid",
 )
 
 
 TIMELINE_SLOTS = ("apply_pre", "apply_si", "apply_post", "apply_fused", "apply_generic", "face_reduce",
-                  "schur", "factor", "pack", "assemble", "apply_ahat")
+                  "schur", "factor", "pack", "assemble", "apply_ahat", "icgs", "precond_build", "precond_apply",
+                  "halo")
 
 
 class Timeline:
@@ -177,3 +186,21 @@ def check(rc: int, what: str) -> None:
 def ptr(t) -> int | None:
     """Device pointer of a torch tensor (None -> NULL)."""
     return None if t is None else t.data_ptr()
+
+
+def arg(t, numel: int | None = None, what: str = "argument"):
+    """Validate a float64 device array handed to the C ABI and return it contiguous.
+
+    The caller must keep the returned tensor alive until the library call has been
+    issued (bind it to a local): a temporary from ``.contiguous()`` that is freed
+    before the call can be handed straight back by the caching allocator to the
+    next temporary, so two arguments would alias."""
+    import torch
+
+    if t.dtype != torch.float64:
+        raise TypeError(f"{what}: expected float64, got {t.dtype}")
+    if t.device.type != "cuda":
+        raise ValueError(f"{what}: expected a CUDA tensor, got device {t.device}")
+    if numel is not None and t.numel() != numel:
+        raise ValueError(f"{what}: expected {numel} entries, got {t.numel()}")
+    return t.contiguous()

@@ -193,9 +193,12 @@ def assemble_system(disc, fields: FieldState, ctx: StageContext, want_jac: bool 
     flow = _flow_struct(disc.params)
     fo = new_frozen.c_struct() if want_jac else None
     fi = frozen.c_struct() if frozen is not None else None
+    u_c = _lib.arg(fields.u, M * L * ns, "fields.u")  # bound locals: alive across the call
+    q_c = _lib.arg(fields.q, M * d * L * ns, "fields.q")
+    uh_c = _lib.arg(fields.uhat, disc.n_trace, "fields.uhat")
     rc = _lib.lib().mhdg_assemble(
-        dd.c, flow, stage, _lib.ptr(fields.u.contiguous()), _lib.ptr(fields.q.contiguous()),
-        _lib.ptr(fields.uhat.contiguous()), _lib.ptr(R_Q), _lib.ptr(R_U), _lib.ptr(R_Tl), _lib.ptr(R_T),
+        dd.c, flow, stage, _lib.ptr(u_c), _lib.ptr(q_c),
+        _lib.ptr(uh_c), _lib.ptr(R_Q), _lib.ptr(R_U), _lib.ptr(R_Tl), _lib.ptr(R_T),
         int(want_jac), blocks.c if want_jac else None, fo, fi, _lib.ptr(status), current_stream())
     _lib.check(rc, "mhdg_assemble")
     raise_status(status, "assemble")
@@ -222,8 +225,9 @@ def gradient_refresh(disc, u: torch.Tensor, uhat: torch.Tensor) -> torch.Tensor:
     """q = A_qq^-1 (-A_qu u - A_qh uhat) on the device (assembly.py:247-252)."""
     dd = disc.device
     q = torch.empty((disc.n_mac, disc.dim, disc.L, disc.ns), dtype=torch.float64, device=dd.device)
-    rc = _lib.lib().mhdg_gradient_refresh(dd.c, _lib.ptr(u.contiguous()), _lib.ptr(uhat.contiguous()),
-                                          _lib.ptr(q), current_stream())
+    u_c = _lib.arg(u, disc.n_mac * disc.L * disc.ns, "u")
+    uh_c = _lib.arg(uhat, disc.n_trace, "uhat")
+    rc = _lib.lib().mhdg_gradient_refresh(dd.c, _lib.ptr(u_c), _lib.ptr(uh_c), _lib.ptr(q), current_stream())
     _lib.check(rc, "mhdg_gradient_refresh")
     return q
 

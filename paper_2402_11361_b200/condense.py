@@ -63,6 +63,12 @@ class CondensedSchur:
         disc = blocks.disc
         n = disc.L * disc.ns
         dev = disc.device.device
+        n_max = int(_lib.lib().mhdg_factor_max_n(FACTOR_KINDS[FACTOR]))
+        if n > n_max:
+            from .discretization import ConfigError
+
+            raise ConfigError(f"local Schur complement size L*ns = {n} (m={disc.mesh.m}, p={disc.p}) exceeds the "
+                              f"{FACTOR!r} factor kernels' limit n <= {n_max}")
         packed = int(_lib.lib().mhdg_packed_lu_size(n))
         lu = torch.empty((disc.n_mac, packed), dtype=torch.float64, device=dev)
         perm = torch.empty((disc.n_mac, n), dtype=torch.int32, device=dev)
@@ -79,11 +85,16 @@ class CondensedSchur:
     def refactor(self) -> None:
         """Schur complement + batched LU (mhdg_condense); raises FactorizationError."""
         dd = self.disc.device
+        self._drop_representation()  # stale stored blocks must not survive a failed refactor
         status = dd.status_buffer()
         rc = _lib.lib().mhdg_condense(dd.c, self.blocks.c, self._fac, _lib.ptr(status), current_stream())
         _lib.check(rc, "mhdg_condense")
         raise_status(status, "condense")
         self._reset_representation()
+
+    def _drop_representation(self) -> None:
+        self.ahat = None
+        self._n_applies = 0
 
     def _reset_representation(self) -> None:
         """New factors: drop stale stored blocks; form them again under MHDG_APPLY_REPR=stored."""
@@ -98,8 +109,10 @@ class CondensedSchur:
         """Count applies on this condensation; under MHDG_APPLY_REPR=auto form the stored
         blocks once ltr applies have run.  Returns True when the representation changed
         (callers holding CUDA graphs of the apply recapture).  Never forms inside a capture."""
+        if torch.cuda.is_current_stream_capturing():
+            return False  # a captured apply is counted when the graph replays (krylov._StepGraphs)
         self._n_applies += k
-        if APPLY_REPR != "auto" or self.ahat is not None or torch.cuda.is_current_stream_capturing():
+        if APPLY_REPR != "auto" or self.ahat is not None:
             return False
         disc = self.disc
         if self._n_applies < disc.nf * disc.Lf * disc.ns:
@@ -127,6 +140,7 @@ class CondensedSchur:
     def refactor_async(self, status: torch.Tensor) -> None:
         """Same as refactor() without the host synchronisation (benchmarks)."""
         dd = self.disc.device
+        self._drop_representation()
         rc = _lib.lib().mhdg_condense(dd.c, self.blocks.c, self._fac, _lib.ptr(status), current_stream())
         _lib.check(rc, "mhdg_condense")
         self._reset_representation()
@@ -149,14 +163,16 @@ class CondensedSchur:
 
     def schur_solve(self, y: torch.Tensor) -> torch.Tensor:
         dd = self.disc.device
-        out = torch.empty_like(y)
-        rc = _lib.lib().mhdg_lu_solve(dd.c, self._fac, _lib.ptr(y.contiguous()), _lib.ptr(out), current_stream())
+        y_c = _lib.arg(y, self.disc.n_mac * self.disc.L * self.disc.ns, "y")
+        out = torch.empty_like(y_c)
+        rc = _lib.lib().mhdg_lu_solve(dd.c, self._fac, _lib.ptr(y_c), _lib.ptr(out), current_stream())
         _lib.check(rc, "mhdg_lu_solve")
         return out
 
     def apply_trace(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         """Matrix-free action of the reduced trace operator (condense.py:91-103)."""
         dd = self.disc.device
+        x = _lib.arg(x, self.disc.n_trace, "x")
         y = torch.empty_like(x) if out is None else out
         self.note_applies(1)
         if self.ahat is not None:
@@ -171,6 +187,7 @@ class CondensedSchur:
 
     def apply_trace_local(self, x: torch.Tensor) -> torch.Tensor:
         dd = self.disc.device
+        x = _lib.arg(x, self.disc.n_trace, "x")
         if self.ahat is not None:
             rc = _lib.lib().mhdg_ahat_apply_local(dd.c, _lib.ptr(self.ahat), _lib.ptr(x), _lib.ptr(self._y_loc),
                                                   current_stream())
@@ -182,9 +199,13 @@ class CondensedSchur:
 
     def rhs(self, res_grad, res_state, res_trace) -> torch.Tensor:
         dd = self.disc.device
-        b = torch.empty(self.disc.n_trace, dtype=torch.float64, device=dd.device)
-        rc = _lib.lib().mhdg_condensed_rhs(dd.c, self.blocks.c, self._fac, _lib.ptr(res_grad.contiguous()),
-                                           _lib.ptr(res_state.contiguous()), _lib.ptr(res_trace.contiguous()),
+        disc = self.disc
+        nu = disc.n_mac * disc.L * disc.ns
+        rg = _lib.arg(res_grad, nu * disc.dim, "R_Q")  # bound locals: alive across the call
+        ru = _lib.arg(res_state, nu, "R_U")
+        rt = _lib.arg(res_trace, disc.n_trace, "R_T")
+        b = torch.empty(disc.n_trace, dtype=torch.float64, device=dd.device)
+        rc = _lib.lib().mhdg_condensed_rhs(dd.c, self.blocks.c, self._fac, _lib.ptr(rg), _lib.ptr(ru), _lib.ptr(rt),
                                            _lib.ptr(b), _lib.ptr(self._y_loc), current_stream())
         _lib.check(rc, "mhdg_condensed_rhs")
         return b
@@ -194,9 +215,12 @@ class CondensedSchur:
         dev = disc.device.device
         du = torch.empty((disc.n_mac, disc.L, disc.ns), dtype=torch.float64, device=dev)
         dq = torch.empty((disc.n_mac, disc.dim, disc.L, disc.ns), dtype=torch.float64, device=dev)
-        rc = _lib.lib().mhdg_recover(disc.device.c, self.blocks.c, self._fac, _lib.ptr(res_grad.contiguous()),
-                                     _lib.ptr(res_state.contiguous()), _lib.ptr(dtrace.contiguous()),
-                                     _lib.ptr(du), _lib.ptr(dq), current_stream())
+        nu = disc.n_mac * disc.L * disc.ns
+        rg = _lib.arg(res_grad, nu * disc.dim, "R_Q")  # bound locals: alive across the call
+        ru = _lib.arg(res_state, nu, "R_U")
+        dt = _lib.arg(dtrace, disc.n_trace, "dtrace")
+        rc = _lib.lib().mhdg_recover(disc.device.c, self.blocks.c, self._fac, _lib.ptr(rg), _lib.ptr(ru),
+                                     _lib.ptr(dt), _lib.ptr(du), _lib.ptr(dq), current_stream())
         _lib.check(rc, "mhdg_recover")
         return du, dq
 

@@ -1,4 +1,6 @@
-// extern "C" boundary (include/mhdg.h): dispatch on the dimension and launch.
+// extern "C" boundary (include/mhdg.h; A/B knobs in mhdg_tuning.h): dispatch on the
+// dimension and launch.
+#include "mhdg_tuning.h"
 #include "common.cuh"
 #include "packed_lu.cuh"
 #include "tiled_inv.cuh"
@@ -20,12 +22,13 @@ int precond_apply(const mhdg_disc&, const double*, const double*, double*, cudaS
 int face_reduce(const mhdg_disc&, const double*, const double*, double, double*, cudaStream_t);
 int lu_solve(const mhdg_disc&, const mhdg_factors&, const double*, double*, cudaStream_t);
 int inv_factor(int n, int n_mac, double* scratch, double* tiled, int* status, cudaStream_t st);
-int inv_factor2(int n, int n_mac, double* scratch, int* piv, double* tiled, int* status, cudaStream_t st);
 int inv_factor3(int n, int n_mac, double* scratch, int* piv, double* tiled, int* status, cudaStream_t st);
-int lu_factor3(int n, int n_mac, double* scratch, int* piv, double* packed, int* status, cudaStream_t st);
 int lu_factor4(int n, int n_mac, double* scratch, int* piv, double* packed, int* status, cudaStream_t st);
+int lu_max_n();
 extern int g_schur_variant;
 int icgs(int n, int j, const double* V, long long ldv, double* w, double* out, double* scratch, cudaStream_t st);
+int vec_pass_api(long long n, int rows, const double* V, long long ldv, double* w, const double* coef, int mode,
+                 double* out, double* scratch, cudaStream_t st);
 long long icgs_scratch_size(int n);
 size_t gj_smem_bytes(int n);
 int apply_stream(const mhdg_disc&, const mhdg_blocks&, const mhdg_factors&, const double*, double*, cudaStream_t);
@@ -68,6 +71,11 @@ int mhdg_icgs(int n, int j, const double* V, long long ldv, double* w, double* o
 }
 
 long long mhdg_icgs_scratch_size(int n) { return icgs_scratch_size(n); }
+
+int mhdg_vec_pass(long long n, int rows, const double* V, long long ldv, double* w, const double* coef, int mode,
+                  double* out, double* scratch, void* st) {
+  return vec_pass_api(n, rows, V, ldv, w, coef, mode, out, scratch, S(st));
+}
 
 int mhdg_timeline_begin(int capacity) {
   if (capacity > g_tl_cap) {
@@ -168,23 +176,24 @@ int mhdg_schur_matrix(const mhdg_disc* g, const mhdg_blocks* b, const mhdg_facto
   return rc;
 }
 
-static int g_factor_variant = 3;
-void mhdg_set_factor_variant(int v) { g_factor_variant = v; }
-static int g_lu_variant = 4;
-void mhdg_set_lu_variant(int v) { g_lu_variant = v; }
 void mhdg_set_schur_variant(int v) { mhdg::g_schur_variant = v; }
+
+int mhdg_factor_max_n(int kind) {
+  if (kind == 1) return lu_max_n();
+  int n = 384;  // k_gj3; beyond it k_gj while its 32-column panel fits shared memory
+  while (gj_smem_bytes(n + 1) <= 227 * 1024) ++n;
+  return n;
+}
 
 int mhdg_lu_factor(const mhdg_disc* g, const mhdg_factors* f, int* status, void* st) {
   const int n = g->L * g->ns;
-  if (f->kind == 1) {  // packed LU (k_lu4; k_lu3 behind mhdg_set_lu_variant(3))
-    const int rc1 = g_lu_variant == 3 ? lu_factor3(n, g->n_mac, f->scratch, f->perm, f->lu, status, S(st))
-                                      : lu_factor4(n, g->n_mac, f->scratch, f->perm, f->lu, status, S(st));
+  if (f->kind == 1) {  // packed LU (lu.cu)
+    const int rc1 = lu_factor4(n, g->n_mac, f->scratch, f->perm, f->lu, status, S(st));
     return rc1 < 0 ? MHDG_ERR_CONFIG : rc1;
   }
-  // DMMA panel-64 Gauss-Jordan when its panel fits shared memory (without row interchanges
-  // by default), else the 32-column FFMA one
-  const int rc = g_factor_variant == 2 ? inv_factor2(n, g->n_mac, f->scratch, f->perm, f->lu, status, S(st))
-                                       : inv_factor3(n, g->n_mac, f->scratch, f->perm, f->lu, status, S(st));
+  // explicit inverse: DMMA panel-64 Gauss-Jordan when its panel fits shared memory, else
+  // the 32-column FFMA one
+  const int rc = inv_factor3(n, g->n_mac, f->scratch, f->perm, f->lu, status, S(st));
   if (rc >= 0) return rc;
   if (gj_smem_bytes(n) > 227 * 1024) return MHDG_ERR_CONFIG;
   return inv_factor(n, g->n_mac, f->scratch, f->lu, status, S(st));

@@ -15,7 +15,8 @@ extern long long g_launches;
 // record a CUDA event pair on their own stream while it is enabled.
 enum TlSlot {
   TL_APPLY_PRE = 0, TL_APPLY_SI, TL_APPLY_POST, TL_APPLY_FUSED, TL_APPLY_GENERIC, TL_FACE_REDUCE,
-  TL_SCHUR, TL_FACTOR, TL_PACK, TL_ASSEMBLE, TL_APPLY_AHAT, TL_NSLOTS = 16
+  TL_SCHUR, TL_FACTOR, TL_PACK, TL_ASSEMBLE, TL_APPLY_AHAT, TL_KRYLOV, TL_PRECOND_BUILD, TL_PRECOND_APPLY,
+  TL_HALO, TL_NSLOTS = 16
 };
 void tl_begin(int slot, cudaStream_t st);
 void tl_end(int slot, cudaStream_t st);

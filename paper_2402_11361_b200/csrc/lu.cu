@@ -54,12 +54,13 @@ constexpr int SWP = SW + 2;  // candidate slot: SW row values, the reciprocal, p
 template <int NB>
 constexpr int pstride() { return NB + 4; }
 
-// argmax key: |v| with the low 9 mantissa bits replaced by (511 - row), so the
-// largest key is the largest magnitude, ties (to 2^-43) going to the lowest row
+// argmax key: |v| with the low 10 mantissa bits replaced by (1023 - row), so the
+// largest key is the largest magnitude, ties (to 2^-42) going to the lowest row (n <= 1024)
+constexpr int MAX_N = 1024;
 __device__ __forceinline__ unsigned long long pkey(double v, int r) {
-  return ((unsigned long long)__double_as_longlong(fabs(v)) & ~0x1FFull) | (unsigned long long)(511 - r);
+  return ((unsigned long long)__double_as_longlong(fabs(v)) & ~0x3FFull) | (unsigned long long)(1023 - r);
 }
-__device__ __forceinline__ int key_row(unsigned long long k) { return 511 - (int)(k & 0x1FFull); }
+__device__ __forceinline__ int key_row(unsigned long long k) { return 1023 - (int)(k & 0x3FFull); }
 
 template <int NB, int NT>
 size_t smem_bytes(int n) {
@@ -641,6 +642,7 @@ static int launch_lu4(int n, int n_mac, double* scratch, int* piv, int* status, 
   const size_t bytes = lu4::smem_bytes<NB, NT>(n);
   if (bytes > 227 * 1024) return -1;
   auto kern = n <= NT ? k_lu4<NB, NT, 1, MINB> : k_lu4<NB, NT, 2, MINB>;
+  if (MINB > 1 && 2 * bytes > 228 * 1024) return -1;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   tl_begin(TL_FACTOR, st);
   kern<<<n_mac, NT, bytes, st>>>(n, scratch, piv, status, g_lu_l2mode);
@@ -648,15 +650,33 @@ static int launch_lu4(int n, int n_mac, double* scratch, int* piv, int* status, 
   return 0;
 }
 
+// n > 384 (C5 (m, p) = (2, 3): n = 420): three rows per thread, one CTA per SM (the
+// 32-column panel of n rows no longer fits twice into shared memory)
+template <int NB, int NT>
+static int launch_lu4_large(int n, int n_mac, double* scratch, int* piv, int* status, cudaStream_t st) {
+  if (n > 3 * NT || n > lu4::MAX_N) return -1;
+  const size_t bytes = lu4::smem_bytes<NB, NT>(n);
+  if (bytes > 227 * 1024) return -1;
+  auto kern = k_lu4<NB, NT, 3, 1>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  tl_begin(TL_FACTOR, st);
+  kern<<<n_mac, NT, bytes, st>>>(n, scratch, piv, status, g_lu_l2mode);
+  tl_end(TL_FACTOR, st);
+  return 0;
+}
+
+int lu_max_n() { return 3 * 192; }
+
 int lu_factor4(int n, int n_mac, double* scratch, int* piv, double* packed, int* status, cudaStream_t st) {
   // 32-column panels, two CTAs per SM (one's pivot chain under the other's updates), or
   // 64-column panels, one CTA per SM (half the trailing-update traffic)
 #ifndef MHDG_LU4_NT
 #define MHDG_LU4_NT 192
 #endif
-  const int rc0 = g_lu_nb != 64   ? launch_lu4<32, MHDG_LU4_NT, 2>(n, n_mac, scratch, piv, status, st)
-                  : g_lu_nt == 384 ? launch_lu4<64, 384, 1>(n, n_mac, scratch, piv, status, st)
-                                   : launch_lu4<64, 256, 1>(n, n_mac, scratch, piv, status, st);
+  int rc0 = g_lu_nb != 64   ? launch_lu4<32, MHDG_LU4_NT, 2>(n, n_mac, scratch, piv, status, st)
+            : g_lu_nt == 384 ? launch_lu4<64, 384, 1>(n, n_mac, scratch, piv, status, st)
+                             : launch_lu4<64, 256, 1>(n, n_mac, scratch, piv, status, st);
+  if (rc0 < 0) rc0 = launch_lu4_large<32, 192>(n, n_mac, scratch, piv, status, st);
   if (rc0 < 0) return -1;
   int rc = launch_ok();
   if (rc) return rc;

@@ -147,13 +147,17 @@ int precond_build(const mhdg_disc& g, const mhdg_blocks& b, const double* extra,
   if (bytes > 227 * 1024) return MHDG_ERR_CONFIG;
   if (bytes > 48 * 1024)
     cudaFuncSetAttribute(k_precond_build<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  tl_begin(TL_PRECOND_BUILD, st);
   k_precond_build<D><<<g.n_faces, PRE_THREADS, bytes, st>>>(g, b, extra, inv, status);
+  tl_end(TL_PRECOND_BUILD, st);
   return launch_ok();
 }
 
 int precond_apply(const mhdg_disc& g, const double* inv, const double* v, double* y, cudaStream_t st) {
   const int bs = g.Lf * g.ns;
+  tl_begin(TL_PRECOND_APPLY, st);
   k_precond_apply<<<g.n_faces, PRE_THREADS, sizeof(double) * 2 * bs, st>>>(bs, inv, v, y);
+  tl_end(TL_PRECOND_APPLY, st);
   return launch_ok();
 }
 

@@ -13,6 +13,7 @@ WALLS = {"y0": ("isothermal_noslip_wall", 1.0), "y1": ("isothermal_noslip_wall",
 OP_CASES = {
     "op_tgv_m1p1": lambda: Discretization(build_cube_mesh(TGV.domain, 1, 1, periodic=(True,) * 3), 1, TGV.params),
     "op_tgv_m2p2": lambda: Discretization(build_cube_mesh(TGV.domain, 1, 2, periodic=(True,) * 3), 2, TGV.params),
+    "op_tgv_m2p3": lambda: Discretization(build_cube_mesh(TGV.domain, 1, 2, periodic=(True,) * 3), 3, TGV.params),
     "op_wall_m1p2": lambda: Discretization(build_cube_mesh(TGV.domain, 2, 1, periodic=(True, False, True)), 2,
                                            TGV.params, bcs=WALLS),
     "op_couette_m2p1": lambda: Discretization(build_cube_mesh(((0, 0, 0), (1, 1, 1)), 1, 2), 1, COU.params,

@@ -32,3 +32,19 @@ def perturbed_fields(disc, state_fn, seed, amp_u=1e-3, amp_q=1e-2):
     f.uhat = f.uhat + amp_u * rng.standard_normal(f.uhat.shape) * np.abs(f.uhat).max()
     f.q = f.q + amp_q * rng.standard_normal(f.q.shape)
     return f
+
+
+def subset_disc(disc, idx):
+    """A host Discretization restricted to the macros `idx` (sorted), sharing the
+    global trace numbering: the oracle run on it reproduces exactly those macros'
+    local operators (every per-macro array is sliced; gather still indexes the
+    full trace vector, so a global x gathers the same local traces)."""
+    import copy
+
+    sub = copy.copy(disc)
+    idx = np.asarray(idx)
+    sub.n_mac = len(idx)
+    for k in ("det", "inv_jac", "jac", "origin", "normals", "areas", "h_sub", "gather", "bc_kind", "bc_label"):
+        setattr(sub, k, getattr(disc, k)[idx])
+    sub._device = None
+    return sub

@@ -13,10 +13,11 @@ from paper_2402_11361_b200 import _lib
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 HEADER = os.path.join(ROOT, "include", "mhdg.h")
+TUNING = os.path.join(ROOT, "paper_2402_11361_b200", "csrc", "mhdg_tuning.h")
 
 
-def declared_functions():
-    text = open(HEADER).read()
+def declared_functions(path=HEADER):
+    text = open(path).read()
     return sorted(set(re.findall(r"^\s*(?:int|long long|void)\s+(mhdg_\w+)\s*\(", text, re.M)))
 
 
@@ -26,7 +27,18 @@ def test_library_exports_every_declared_symbol():
     lib = _lib.lib()
     for n in names:
         assert hasattr(lib, n), n
-    assert set(names) <= set(_lib.EXPORTED) | {"mhdg_set_stream_prefetch", "mhdg_stream_grid"}
+    assert set(names) == set(_lib.EXPORTED)
+
+
+def test_tuning_knobs_stay_out_of_the_public_header():
+    """The A/B knobs are process-global diagnostics: exported, declared only in
+    the internal csrc/mhdg_tuning.h, never in the drop-in header."""
+    knobs = declared_functions(TUNING)
+    assert set(knobs) == set(_lib.TUNING)
+    assert not set(knobs) & set(declared_functions())
+    lib = _lib.lib()
+    for n in knobs:
+        assert hasattr(lib, n), n
 
 
 def test_packed_factor_size():

@@ -142,7 +142,7 @@ def test_streamed_apply_matches_generic(name, split):
 
 @pytest.mark.parametrize("name", ["uniform_m2p2", "uniform_m4p3", "couette_m2p2"])
 def test_lu_factor_kind_matches_inverse(name):
-    """Packed-LU factors (k_lu4 / k_lu3, pivots in place) and the explicit inverse give
+    """Packed-LU factors (k_lu4, pivots in place) and the explicit inverse give
     the same condensed operator, rhs and recovery up to cond(S) * eps."""
     need_gpu()
     from paper_2402_11361_b200 import condense as CD
@@ -155,22 +155,16 @@ def test_lu_factor_kind_matches_inverse(name):
     x = dev(np.random.default_rng(3).standard_normal(d.n_trace))
     out = {}
     old = CD.FACTOR
-    L = _lib.lib()
     try:
-        for kind, var in (("inverse", 0), ("lu", 4), ("lu3", 3)):
-            CD.FACTOR = "lu" if kind == "lu3" else kind
-            if var:
-                L.mhdg_set_lu_variant(var)
+        for kind in ("inverse", "lu"):
+            CD.FACTOR = kind
             cond = CD.CondensedSchur.build(blocks)
             du, _ = cond.recover(res[0], res[1], x)
             out[kind] = (host(cond.apply_trace(x)), host(cond.rhs(*res)), host(du))
     finally:
         CD.FACTOR = old
-        L.mhdg_set_lu_variant(4)
     tol = 1e-7 if name == "uniform_m4p3" else 1e-10  # cond(S) ~ 1e6 at m=4, p=3
     for a, b in zip(out["lu"], out["inverse"]):
-        assert rel_err(a, b) < tol
-    for a, b in zip(out["lu"], out["lu3"]):
         assert rel_err(a, b) < tol
 
 

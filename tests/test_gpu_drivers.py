@@ -141,3 +141,24 @@ def test_dirk33_step_with_factor_kind(kind):
     assert [s.iterations for s in sts] == list(g["newton"])
     assert all(abs(a - b) <= 1 for a, b in zip([s.krylov_iterations for s in sts], g["krylov"]))
     assert rel_err(host(f.u), g["u"]) < 1e-8
+
+
+def test_dirk33_c3_slab_vs_reference():
+    """BASELINE configs[2] (C3: TGV Re=1600, M=0.1, m=2, p=2, DIRK33, dt=0.01) on a
+    2^3 x 6 = 48-macro periodic slab, two steps against the reference's own run
+    (oracle/make_golden.py dirk48, stepper.py:265-328): Newton counts per stage
+    equal, FGMRES within +-1 per stage, state within 1e-8 after every step."""
+    need_gpu()
+    g = load_golden("dirk_tgv_n2_m2p2")
+    d = Discretization(build_cube_mesh(TGV.domain, 2, 2, periodic=(True,) * 3), 2, TGV.params)
+    f = A.to_device_fields(d, g["u0"], g["q0"], g["uhat0"])
+    newton, kits = [], []
+    for step in range(int(g["steps"])):
+        sts, dt = S.dirk_advance(d, f, float(g["dt"]), S.DirkTableau.dirk33())
+        assert dt == float(g["dt"])
+        newton += [s.iterations for s in sts]
+        kits += [s.krylov_iterations for s in sts]
+        assert rel_err(host(f.u), g["step_u"][step]) < 1e-8, step
+        assert rel_err(host(f.uhat), g["step_uhat"][step]) < 1e-8, step
+    assert newton == list(g["newton"])
+    assert all(abs(a - b) <= 1 for a, b in zip(kits, g["krylov"]))
