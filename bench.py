@@ -117,6 +117,21 @@ def condense_executed_flops_per_macro(disc):
     return {"schur": schur, "factor": (2 if CD.FACTOR == "inverse" else 2.0 / 3.0) * (L * ns) ** 3}
 
 
+def assembly_flops_per_macro(disc):
+    """Algorithmic flops of the Jacobian assembly per macro: the reference's dense
+    contractions (assembly.py:455-470 volume, 578-585 face) per quadrature point in
+    their cheapest order -- W1 = A g (nloc ns^2 d), the flux-Jacobian term
+    (nloc ns^2 d + (nloc ns)^2), SUPG W1^T tau W1 ((nloc ns)^2 ns), the DIRK/PTC SUPG
+    mass term ((nloc ns)^2); faces: proj x K1 and proj x S ((nlf ns)^2 each) -- at
+    2 flops per multiply-add.  Residual and pointwise-physics work is not counted."""
+    d, ns, nf = disc.dim, disc.ns, disc.nf
+    rm = disc.rm
+    nl, nlf = rm.n_loc, rm.n_loc_face
+    vol = 2 * (2 * nl * ns * ns * d + (nl * ns) ** 2 * (1 + ns + 1))
+    face = 2 * 2 * (nlf * ns) ** 2
+    return rm.n_sub * rm.n_quad * vol + nf * rm.n_tri * rm.n_quad_face * face
+
+
 def condense_flops_per_macro(disc):
     """F_cond = 2 d L^3 ns^2 + (2/3) (L ns)^3."""
     d, L, ns = disc.dim, disc.L, disc.ns
@@ -383,13 +398,14 @@ def run_gpu(args, rank, world):
     st = current_stream()
 
     def apply_split(x):
-        """One trace-operator apply; with slabs: forward halo, local apply,
-        face reduce, reverse halo (DistCondensed.apply_trace)."""
-        xl = ddisc.forward(x) if ddisc is not None else x
-        _lib.check(L.mhdg_apply_trace_local(dd.c, blocks.c, cond._fac, _lib.ptr(xl), _lib.ptr(y_loc), st), "apply")
-        _lib.check(L.mhdg_face_reduce(dd.c, _lib.ptr(y_loc), _lib.ptr(y_face), st), "reduce")
+        """One trace-operator apply; with slabs DistCondensed.apply_trace: forward halo
+        in flight while the interior macros are applied, then the halo-adjacent ones,
+        reverse halo summed in the face reduction."""
         if ddisc is not None:
-            y.copy_(ddisc.reverse(y_face))
+            api.apply_trace(x, out=y)
+            return
+        _lib.check(L.mhdg_apply_trace_local(dd.c, blocks.c, cond._fac, _lib.ptr(x), _lib.ptr(y_loc), st), "apply")
+        _lib.check(L.mhdg_face_reduce(dd.c, _lib.ptr(y_loc), _lib.ptr(y_face), st), "reduce")
 
     clk = Clocks(local).__enter__()
     for i in range(W):
@@ -481,6 +497,47 @@ def run_gpu(args, rank, world):
         del at
         cond.ahat = None
 
+    # ---- Krylov vector kernels and the block preconditioner ----
+    krylov = None
+    if ddisc is None:
+        from paper_2402_11361_b200 import krylov as KR
+
+        torch.cuda.synchronize()
+        p0, p1 = ev(), ev()
+        with _lib.Timeline(64) as tl_pb:
+            p0.record()
+            pre = KR.block_precond_build(cond)
+            p1.record()
+            p1.synchronize()
+        n = n_own
+        rows = 21  # an inner GMRES column at restart 20 (krylov.py:270-276)
+        V = torch.as_tensor(np.random.default_rng(7).standard_normal((rows + 1, n)), device="cuda")
+        for _ in range(2):
+            KR._icgs_launch(V, rows - 1, V[rows])
+            pre(V[0])
+        torch.cuda.synchronize()
+        with _lib.Timeline(8 * K + 16) as tl_kr:
+            for i in range(K):
+                KR._icgs_launch(V, rows - 1, V[rows])
+                pre(V[i % rows])
+            torch.cuda.synchronize()
+        bs = disc.Lf * disc.ns
+        nfc = disc.mesh.n_faces
+        t_icgs = tl_kr.ms["icgs"] / tl_kr.counts["icgs"] / 1e3
+        t_pa = tl_kr.ms["precond_apply"] / tl_kr.counts["precond_apply"] / 1e3
+        b_icgs = 8 * n * (3 * rows + 5)  # V_j streamed 3x; w read 3x, written 2x
+        b_pa = 8 * (nfc * bs * bs + 2 * n)
+        krylov = {"what": "one ICGS Arnoldi orthogonalisation (mhdg_icgs: 3 fused deterministic passes) "
+                          "against 21 basis vectors and one block-preconditioner apply, C2 trace vectors",
+                  "icgs": {"avg_launch_s": t_icgs, "rows": rows, "algorithmic_bytes": b_icgs,
+                           "achieved_gbs": b_icgs / t_icgs / 1e9},
+                  "precond_apply": {"avg_launch_s": t_pa, "algorithmic_bytes": b_pa, "achieved_gbs": b_pa / t_pa / 1e9},
+                  "precond_build": {"seconds": p0.elapsed_time(p1) / 1e3,
+                                    "kernel_seconds": tl_pb.ms.get("precond_build", 0.0) / 1e3,
+                                    "faces": nfc, "block": bs,
+                                    "flops": nfc * (bs**3 / 3.0 + bs**3 / 3.0 + bs**3 / 3.0)}}
+        del V, pre
+
     peaks = measured_peaks()
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     fp64 = fp64_gemm_peak(torch) if rank == 0 else None
@@ -505,6 +562,7 @@ def run_gpu(args, rank, world):
     dom_bytes = kbytes.get(dom, b_mac * disc.n_mac)
     achieved = dom_bytes / kern_s[dom] / 1e9
     f_mac = condense_flops_per_macro(disc)
+    f_asm = assembly_flops_per_macro(disc)
     cond_tf = f_mac * disc.n_mac / t_cond / 1e12
     fx = condense_executed_flops_per_macro(disc)
     exec_tf = (fx["schur"] + fx["factor"]) * disc.n_mac / t_cond / 1e12
@@ -547,7 +605,14 @@ def run_gpu(args, rank, world):
                                           + ("batched LU with partial pivoting, (2/3) n^3 (the F_cond term)" if lu
                                              else "explicit S^-1 (the reference's np.linalg.inv), 2 n^3")}},
         "assembly": {"metric": "macro-elements assembled/s (Jacobian + residual)", "value": disc.n_mac / t_asm,
-                     "seconds": t_asm, "kernel_seconds": t_asm_k},
+                     "seconds": t_asm, "kernel_seconds": t_asm_k,
+                     "roofline": {"bound": "fp64", "flops_per_macro": f_asm,
+                                  "achieved": f_asm * disc.n_mac / t_asm_k / 1e12 if t_asm_k else None,
+                                  "peak": fp64, "unit": "TFLOP/s",
+                                  "frac": (f_asm * disc.n_mac / t_asm_k / 1e12 / fp64) if (fp64 and t_asm_k) else None,
+                                  "flops": "the reference's Jacobian contractions (assembly.py:455-470, 578-585) "
+                                           "in their cheapest order, per quadrature point"}},
+        "krylov": krylov,
         "apply_stored": stored,
         "e2e": {"value": n_dofs_job / t_e2e, "unit": "DOF-applies/s",
                 "h2d_bytes_per_step": 8 * n_dofs_job, "d2h_bytes_per_step": 8 * n_dofs_job},

@@ -147,7 +147,7 @@ typedef struct {
      kind 0: the explicit inverse S^-1 (what the reference's np.linalg.inv
        stores, condense.py:67) by Gauss-Jordan with partial pivoting, in the
        tiled order of csrc/tiled_inv.cuh (64-row blocks of 32-column tiles).
-   `scratch` (n_mac*n*n) holds S before factorization.  `work`
+   `scratch` (n_mac*n*n, or scratch_macros*n*n) holds S before factorization.  `work`
    (mhdg_apply_work_size doubles, or NULL) holds the per-macro hand-off
    vectors of the split apply (pre -> factor solve -> post); with NULL the
    fused single-kernel apply runs. */
@@ -158,6 +158,9 @@ typedef struct {
   double *work;              /* mhdg_apply_work_size(disc) or NULL */
   int kind;                  /* 0: explicit S^-1, tiled (csrc/tiled_inv.cuh), Gauss-Jordan;
                                 1: packed LU (csrc/packed_lu.cuh), perm = pivot rows */
+  int scratch_macros;        /* macros `scratch` holds: <= 0 or >= n_mac: all (n_mac*n*n);
+                                else mhdg_condense forms and factors S that many macros at a
+                                time (memory-lean: C5's (m, p) = (2, 3) slabs) */
 } mhdg_factors;
 
 /* Largest local Schur size n = L*ns the factor kernels take for factor `kind`
@@ -251,6 +254,26 @@ int mhdg_ahat_apply(const mhdg_disc *disc, const double *at, const double *x, do
                     double *y_loc, void *stream);
 int mhdg_ahat_apply_local(const mhdg_disc *disc, const double *at, const double *x,
                           double *y_loc, void *stream);
+
+/* mhdg_apply_trace_local for the contiguous macro range [mac0, mac0 + count) only
+   (y_loc entries of the other macros untouched): a slab applies its interior
+   macros while the forward halo is in flight and the macros next to ghost faces
+   after it arrives (multi-GPU). */
+int mhdg_apply_trace_local_range(const mhdg_disc *disc, const mhdg_blocks *blocks, const mhdg_factors *fac,
+                                 const double *x, double *y_loc, int mac0, int count, void *stream);
+
+/* Halo messages of the slab decomposition: buf[i] = src[idx[i]] (pack), and
+   dst[idx[i]] = buf[i] or, with accumulate, dst[idx[i]] += buf[i] (unpack;
+   idx entries unique), i < n. */
+int mhdg_halo_gather(long long n, const int *idx, const double *src, double *buf, void *stream);
+int mhdg_halo_scatter(long long n, const int *idx, const double *buf, double *dst, int accumulate, void *stream);
+
+/* Face sum of the first n_out trace dofs with the reverse halo folded in: y[i] =
+   y_loc[src0] + (y_loc[src1] if the dof has a second local side, else
+   remote[remote_src[i]] if remote_src[i] >= 0, else 0) -- the other rank's side of
+   a face split across slabs (condense.py:48-51 across ranks). */
+int mhdg_face_reduce_remote(const mhdg_disc *disc, const double *y_loc, const int *remote_src, const double *remote,
+                            int n_out, double *y, void *stream);
 
 /* y[dof] = sum of the (one or two) local contributions, in flat-index order. */
 int mhdg_face_reduce(const mhdg_disc *disc, const double *y_loc, double *y, void *stream);

@@ -64,7 +64,8 @@ class Frozen(C.Structure):
 
 
 class Factors(C.Structure):
-    _fields_ = [("lu", _dp), ("perm", _dp), ("scratch", _dp), ("work", _dp), ("kind", C.c_int)]
+    _fields_ = [("lu", _dp), ("perm", _dp), ("scratch", _dp), ("work", _dp), ("kind", C.c_int),
+                ("scratch_macros", C.c_int)]
 
 
 _lib = None
@@ -98,6 +99,10 @@ def lib():
             "mhdg_ahat_form": [P(Disc), P(Blocks), P(Factors), _dp, _dp, _dp, _dp, _dp],
             "mhdg_ahat_apply": [P(Disc), _dp, _dp, _dp, _dp, _dp],
             "mhdg_ahat_apply_local": [P(Disc), _dp, _dp, _dp, _dp],
+            "mhdg_apply_trace_local_range": [P(Disc), P(Blocks), P(Factors), _dp, _dp, C.c_int, C.c_int, _dp],
+            "mhdg_halo_gather": [C.c_longlong, _dp, _dp, _dp, _dp],
+            "mhdg_halo_scatter": [C.c_longlong, _dp, _dp, _dp, C.c_int, _dp],
+            "mhdg_face_reduce_remote": [P(Disc), _dp, _dp, _dp, C.c_int, _dp, _dp],
         }
         for name, args in sigs.items():
             fn = getattr(L, name)
@@ -145,7 +150,8 @@ EXPORTED = (
     "mhdg_packed_lu_size", "mhdg_precond_build_ext", "mhdg_side_blocks",
     "mhdg_apply_work_size", "mhdg_timeline_begin", "mhdg_timeline_end", "mhdg_icgs", "mhdg_icgs_scratch_size",
     "mhdg_ahat_form", "mhdg_ahat_apply", "mhdg_ahat_apply_local", "mhdg_factor_max_n",
-    "mhdg_vec_pass",
+    "mhdg_vec_pass", "mhdg_apply_trace_local_range", "mhdg_halo_gather", "mhdg_halo_scatter",
+    "mhdg_face_reduce_remote",
 )
 # diagnostic A/B knobs (csrc/mhdg_tuning.h; not part of the drop-in ABI)
 TUNING = (

@@ -52,6 +52,7 @@ class CondensedSchur:
         fac.lu, fac.perm, fac.scratch = _lib.ptr(lu), _lib.ptr(perm), _lib.ptr(scratch)
         fac.work = _lib.ptr(work) if work is not None else None
         fac.kind = FACTOR_KINDS[FACTOR]
+        fac.scratch_macros = scratch.shape[0]
         self._fac = fac
         self.ahat = None  # (n_mac, ltr, ltr) column-major local trace blocks when formed
         self._n_applies = 0
@@ -59,9 +60,14 @@ class CondensedSchur:
         self._y_loc = torch.empty(dd.n_local_trace, dtype=torch.float64, device=dd.device)
 
     @classmethod
-    def allocate(cls, blocks: LocalBlocks) -> "CondensedSchur":
+    def allocate(cls, blocks: LocalBlocks, scratch_macros: int | None = None) -> "CondensedSchur":
+        """Factor storage for every macro; `scratch_macros` (or MHDG_CONDENSE_CHUNK) bounds
+        the Schur scratch to that many macros (condensed chunk by chunk)."""
         disc = blocks.disc
         n = disc.L * disc.ns
+        if scratch_macros is None:
+            scratch_macros = int(os.environ.get("MHDG_CONDENSE_CHUNK", "0"))
+        chunk = scratch_macros if 0 < scratch_macros < disc.n_mac else disc.n_mac
         dev = disc.device.device
         n_max = int(_lib.lib().mhdg_factor_max_n(FACTOR_KINDS[FACTOR]))
         if n > n_max:
@@ -72,7 +78,7 @@ class CondensedSchur:
         packed = int(_lib.lib().mhdg_packed_lu_size(n))
         lu = torch.empty((disc.n_mac, packed), dtype=torch.float64, device=dev)
         perm = torch.empty((disc.n_mac, n), dtype=torch.int32, device=dev)
-        scratch = torch.empty((disc.n_mac, n, n), dtype=torch.float64, device=dev)
+        scratch = torch.empty((chunk, n, n), dtype=torch.float64, device=dev)
         work = torch.empty(int(_lib.lib().mhdg_apply_work_size(disc.device.c)), dtype=torch.float64, device=dev)
         return cls(blocks, lu, perm, scratch, work)
 
@@ -157,6 +163,8 @@ class CondensedSchur:
     def schur_matrix_into_factors(self) -> torch.Tensor:
         """Write S (unfactorized) into self.scratch and return it; for parity tests."""
         dd = self.disc.device
+        if self.scratch.shape[0] != self.disc.n_mac:
+            raise ValueError("schur_matrix_into_factors needs scratch for every macro (no MHDG_CONDENSE_CHUNK)")
         rc = _lib.lib().mhdg_schur_matrix(dd.c, self.blocks.c, self._fac, current_stream())
         _lib.check(rc, "mhdg_schur_matrix")
         return self.scratch
@@ -184,6 +192,28 @@ class CondensedSchur:
                                          _lib.ptr(self._y_loc), current_stream())
         _lib.check(rc, "mhdg_apply_trace")
         return y
+
+    def apply_trace_local_into(self, x: torch.Tensor) -> None:
+        """Unscattered local apply of all macros into the scratch y_loc (no copy)."""
+        dd = self.disc.device
+        x = _lib.arg(x, self.disc.n_trace, "x")
+        if self.ahat is not None:
+            rc = _lib.lib().mhdg_ahat_apply_local(dd.c, _lib.ptr(self.ahat), _lib.ptr(x), _lib.ptr(self._y_loc),
+                                                  current_stream())
+        else:
+            rc = _lib.lib().mhdg_apply_trace_local(dd.c, self.blocks.c, self._fac, _lib.ptr(x),
+                                                   _lib.ptr(self._y_loc), current_stream())
+        _lib.check(rc, "mhdg_apply_trace_local")
+
+    def apply_trace_local_range(self, x: torch.Tensor, mac0: int, count: int) -> None:
+        """Matrix-free local apply of macros [mac0, mac0 + count) into y_loc (the
+        slab's interior / halo-adjacent split, dist.DistCondensed.apply_trace)."""
+        if count <= 0:
+            return
+        dd = self.disc.device
+        rc = _lib.lib().mhdg_apply_trace_local_range(dd.c, self.blocks.c, self._fac, _lib.ptr(x),
+                                                     _lib.ptr(self._y_loc), int(mac0), int(count), current_stream())
+        _lib.check(rc, "mhdg_apply_trace_local_range")
 
     def apply_trace_local(self, x: torch.Tensor) -> torch.Tensor:
         dd = self.disc.device

@@ -282,15 +282,17 @@ __device__ __forceinline__ void rows_dot(const double* A, int u0, int nu, VecF v
   }
 }
 
-// Work buffers of the split apply (mhdg_factors.work), per macro:
-//   y1 [M][NP] | y2 [M][NP] | face terms [M][A_hh x (LTR) | g (LTR)]   (NP = n rounded up to even)
+// Work buffers of the split apply (mhdg_factors.work), interleaved per macro so a
+// contiguous macro range is a plain pointer offset (mhdg_apply_trace_local_range):
+//   [M][ y1 (NP) | y2 (NP) | face terms: A_hh x (LTR) | g (LTR) ]   (NP = n rounded up to even)
 template <class C>
 struct Work {
   static constexpr int NP = ceven(C::n);
-  static __host__ __device__ __forceinline__ double* y1(double* w, int m) { return w + (size_t)m * NP; }
-  static __host__ __device__ __forceinline__ double* y2(double* w, int M, int m) { return w + ((size_t)M + m) * NP; }
-  static __host__ __device__ __forceinline__ double* fc(double* w, int M, int m) {
-    return w + (size_t)2 * M * NP + (size_t)m * 2 * C::LTR;
+  static constexpr size_t PER = 2 * (size_t)NP + 2 * (size_t)C::LTR;
+  static __host__ __device__ __forceinline__ double* y1(double* w, int m) { return w + (size_t)m * PER; }
+  static __host__ __device__ __forceinline__ double* y2(double* w, int, int m) { return w + (size_t)m * PER + NP; }
+  static __host__ __device__ __forceinline__ double* fc(double* w, int, int m) {
+    return w + (size_t)m * PER + 2 * (size_t)NP;
   }
 };
 

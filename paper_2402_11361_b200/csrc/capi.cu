@@ -32,6 +32,10 @@ int vec_pass_api(long long n, int rows, const double* V, long long ldv, double* 
 long long icgs_scratch_size(int n);
 size_t gj_smem_bytes(int n);
 int apply_stream(const mhdg_disc&, const mhdg_blocks&, const mhdg_factors&, const double*, double*, cudaStream_t);
+int halo_gather(long long n, const int* idx, const double* src, double* buf, cudaStream_t st);
+int halo_scatter(long long n, const int* idx, const double* buf, double* dst, int accumulate, cudaStream_t st);
+int face_reduce_remote(const mhdg_disc& g, const double* y_loc, const int* remote_src, const double* remote,
+                       int n_out, double* y, cudaStream_t st);
 }  // namespace mhdg
 
 using namespace mhdg;
@@ -137,6 +141,64 @@ int mhdg_apply_trace_local(const mhdg_disc* g, const mhdg_blocks* b, const mhdg_
   return rc2;
 }
 
+// views of the macro range [mac0, mac0 + count): every per-macro array offset by mac0
+// (mhdg.h layouts); the factors' scratch is offset only when it holds every macro
+static void macro_view(const mhdg_disc* g, const mhdg_blocks* b, const mhdg_factors* f, int mac0, int count,
+                       mhdg_disc* gv, mhdg_blocks* bv, mhdg_factors* fv) {
+  const size_t m0 = (size_t)mac0, d = g->dim, nf = g->nf, ns = g->ns, n = (size_t)g->L * ns;
+  const size_t bs = (size_t)g->Lf * ns, ltr = nf * bs, nqf_f = (size_t)g->n_tri * g->nqf;
+  *gv = *g;
+  gv->n_mac = count;
+  gv->det += m0;
+  gv->inv_jac += m0 * d * d;
+  gv->normals += m0 * nf * d;
+  gv->areas += m0 * nf;
+  gv->h_sub += m0 * g->n_sub;
+  gv->gather += m0 * ltr;
+  if (gv->bc_kind) gv->bc_kind += m0 * nf;
+  if (gv->wall_e) gv->wall_e += m0 * nf;
+  if (gv->wall_u) gv->wall_u += m0 * nf * d;
+  if (gv->u_dir) gv->u_dir += m0 * nf * nqf_f * ns;
+  if (gv->source) gv->source += m0 * g->n_sub * g->nq * ns;
+  *bv = *b;
+  bv->state_state += m0 * n * n;
+  bv->face_state_trace += m0 * nf * bs * bs;
+  bv->face_trace_state += m0 * nf * bs * bs;
+  bv->face_trace_trace += m0 * nf * bs * bs;
+  bv->wdgdq_vol += m0 * g->n_sub * g->nq * d * d * ns * ns;
+  bv->wdgdq_face += m0 * nf * nqf_f * d * ns * ns;
+  bv->trace_face_scale += m0 * nf;
+  *fv = *f;
+  fv->lu += m0 * (size_t)mhdg_packed_lu_size((int)n);
+  fv->perm += m0 * n;
+  if (f->scratch_macros <= 0 || f->scratch_macros >= g->n_mac) fv->scratch += m0 * n * n;
+  if (fv->work) fv->work += m0 * (size_t)(mhdg_apply_work_size(g) / g->n_mac);
+}
+
+int mhdg_apply_trace_local_range(const mhdg_disc* g, const mhdg_blocks* b, const mhdg_factors* f, const double* x,
+                                 double* y_loc, int mac0, int count, void* st) {
+  if (mac0 < 0 || count < 0 || mac0 + count > g->n_mac) return MHDG_ERR_CONFIG;
+  if (count == 0) return MHDG_OK;
+  mhdg_disc gv;
+  mhdg_blocks bv;
+  mhdg_factors fv;
+  macro_view(g, b, f, mac0, count, &gv, &bv, &fv);
+  return mhdg_apply_trace_local(&gv, &bv, &fv, x, y_loc + (size_t)mac0 * g->nf * g->Lf * g->ns, st);
+}
+
+int mhdg_halo_gather(long long n, const int* idx, const double* src, double* buf, void* st) {
+  return halo_gather(n, idx, src, buf, S(st));
+}
+
+int mhdg_halo_scatter(long long n, const int* idx, const double* buf, double* dst, int accumulate, void* st) {
+  return halo_scatter(n, idx, buf, dst, accumulate, S(st));
+}
+
+int mhdg_face_reduce_remote(const mhdg_disc* g, const double* y_loc, const int* remote_src, const double* remote,
+                            int n_out, double* y, void* st) {
+  return face_reduce_remote(*g, y_loc, remote_src, remote, n_out, y, S(st));
+}
+
 int mhdg_face_reduce(const mhdg_disc* g, const double* y_loc, double* y, void* st) {
   tl_begin(TL_FACE_REDUCE, S(st));
   const int rc = face_reduce(*g, y_loc, nullptr, 0.0, y, S(st));
@@ -200,9 +262,24 @@ int mhdg_lu_factor(const mhdg_disc* g, const mhdg_factors* f, int* status, void*
 }
 
 int mhdg_condense(const mhdg_disc* g, const mhdg_blocks* b, const mhdg_factors* f, int* status, void* st) {
-  int rc = mhdg_schur_matrix(g, b, f, st);
-  if (rc) return rc;
-  return mhdg_lu_factor(g, f, status, st);
+  const int chunk = f->scratch_macros;
+  if (chunk <= 0 || chunk >= g->n_mac) {
+    int rc = mhdg_schur_matrix(g, b, f, st);
+    if (rc) return rc;
+    return mhdg_lu_factor(g, f, status, st);
+  }
+  // scratch for `chunk` macros: Schur + factor + pack chunk by chunk
+  for (int c0 = 0; c0 < g->n_mac; c0 += chunk) {
+    const int cnt = g->n_mac - c0 < chunk ? g->n_mac - c0 : chunk;
+    mhdg_disc gv;
+    mhdg_blocks bv;
+    mhdg_factors fv;
+    macro_view(g, b, f, c0, cnt, &gv, &bv, &fv);
+    int rc = mhdg_schur_matrix(&gv, &bv, &fv, st);
+    if (!rc) rc = mhdg_lu_factor(&gv, &fv, status, st);
+    if (rc) return rc;
+  }
+  return MHDG_OK;
 }
 
 int mhdg_lu_solve(const mhdg_disc* g, const mhdg_factors* f, const double* bvec, double* y, void* st) {

@@ -14,12 +14,14 @@ constexpr int PRE_THREADS = 256;
 
 template <int D>
 __global__ void __launch_bounds__(PRE_THREADS) k_precond_build(mhdg_disc g, mhdg_blocks b, const double* __restrict__ extra,
-                                                               double* __restrict__ inv, int* status) {
+                                                               double* inv, int* status, int x_global) {
   extern __shared__ double sm[];
   constexpr int NS = D + 2, NF = D + 1;
   const int f = blockIdx.x, bs = g.Lf * NS, tid = threadIdx.x;
   double* B = sm;            // bs x bs
-  double* X = B + bs * bs;   // bs x bs
+  // bs x bs Cholesky workspace: shared memory, or (large faces: 3D p = 3 has bs = 140 and
+  // 2 bs^2 doubles exceed shared memory) this face's own output block, overwritten last
+  double* X = x_global ? inv + (size_t)f * bs * bs : B + bs * bs;
   __shared__ int fail;
   if (tid == 0) fail = 0;
   for (int i = tid; i < bs * bs; i += blockDim.x) B[i] = 0.0;
@@ -143,12 +145,14 @@ template <int D>
 int precond_build(const mhdg_disc& g, const mhdg_blocks& b, const double* extra, double* inv, int* status,
                   cudaStream_t st) {
   const int bs = g.Lf * (D + 2);
-  const size_t bytes = sizeof(double) * 2 * bs * bs;
+  size_t bytes = sizeof(double) * 2 * bs * bs;
+  const int x_global = bytes > 227 * 1024;
+  if (x_global) bytes /= 2;
   if (bytes > 227 * 1024) return MHDG_ERR_CONFIG;
   if (bytes > 48 * 1024)
     cudaFuncSetAttribute(k_precond_build<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   tl_begin(TL_PRECOND_BUILD, st);
-  k_precond_build<D><<<g.n_faces, PRE_THREADS, bytes, st>>>(g, b, extra, inv, status);
+  k_precond_build<D><<<g.n_faces, PRE_THREADS, bytes, st>>>(g, b, extra, inv, status, x_global);
   tl_end(TL_PRECOND_BUILD, st);
   return launch_ok();
 }

@@ -51,6 +51,28 @@ class Comm:
                 t.copy_(w)
         return t
 
+    def exchange_start(self, sends: dict, recv_bufs: dict):
+        """Post the sends and receives (into the given contiguous views) and return a
+        wait() that makes the current stream wait for them: with NCCL the transfers run
+        on the communicator's stream while the caller keeps launching kernels."""
+        if self.world == 1 or (not sends and not recv_bufs):
+            return lambda: None
+        if self.host_staged:
+            got = self.exchange(sends, {q: b.numel() for q, b in recv_bufs.items()}, next(iter(recv_bufs.values())))
+            for q, b in recv_bufs.items():
+                b.copy_(got[q])
+            return lambda: None
+        d = self.dist
+        ops = [d.P2POp(d.irecv, buf, q) for q, buf in sorted(recv_bufs.items())]
+        ops += [d.P2POp(d.isend, t, q) for q, t in sorted(sends.items())]
+        reqs = d.batch_isend_irecv(ops)
+
+        def wait():
+            for r in reqs:
+                r.wait()
+
+        return wait
+
     def exchange(self, sends: dict, recv_counts: dict, like: torch.Tensor) -> dict:
         """Point-to-point exchange: sends[q] -> rank q, receives recv_counts[q] values from q."""
         wire_dev = torch.device("cpu") if self.host_staged else like.device
@@ -108,33 +130,140 @@ def collective(comm, fn):
     return out
 
 
-class HaloPlan:
-    """Dof-level send/receive index sets of a SlabPartition."""
+def _start_exchange(comm, sends: dict, recv_bufs: dict):
+    """Start a point-to-point exchange into preallocated receive views; returns a
+    wait() that makes the current stream wait for the received data (NCCL) or
+    nothing (synchronous communicators)."""
+    if hasattr(comm, "exchange_start"):
+        return comm.exchange_start(sends, recv_bufs)
+    like = next(iter(recv_bufs.values()), next(iter(sends.values()), None))
+    got = comm.exchange(sends, {q: b.numel() for q, b in recv_bufs.items()}, like)
+    for q, b in recv_bufs.items():
+        b.copy_(got[q])
+    return lambda: None
 
-    def __init__(self, part, Lf: int, ns: int, device):
+
+def _segments(buf: torch.Tensor, counts: dict) -> dict:
+    out, o = {}, 0
+    for q in sorted(counts):
+        out[q] = buf[o: o + counts[q]]
+        o += counts[q]
+    return out
+
+
+class HaloPlan:
+    """Dof-level send/receive index sets of a SlabPartition, as int32 device tables
+    for the library's halo kernels (mhdg_halo_gather / _scatter / _face_reduce_remote).
+
+    Per neighbour q (ascending), faces in ascending global id on both sides:
+      fwd_send -- owned dofs q holds as ghosts (x sent forward; y received back),
+      fwd_recv -- this rank's ghost dofs owned by q (x received; y sent back),
+      rev_send -- the local flat y_loc entries of those ghost dofs (their one local side),
+      remote_src -- per owned dof, its slot in the concatenated reverse receive buffer
+                    (-1: no remote side)."""
+
+    def __init__(self, part, Lf: int, ns: int, device, scatter_src=None):
         per = Lf * ns
         self.per = per
         self.n_owned = part.n_owned_faces * per
         self.n_local = part.n_local_faces * per
-        as_t = lambda a: torch.as_tensor(np.asarray(a, dtype=np.int64), device=device)  # noqa: E731
-        self.send = {q: as_t(part.dof_index(f, Lf, ns)) for q, f in sorted(part.send_faces.items())}
-        self.recv = {q: as_t(part.dof_index(f, Lf, ns)) for q, f in sorted(part.recv_faces.items())}
+        self.device = device
+        i32 = lambda a: torch.as_tensor(np.asarray(a, dtype=np.int32), device=device)  # noqa: E731
+        i64 = lambda a: torch.as_tensor(np.asarray(a, dtype=np.int64), device=device)  # noqa: E731
+        send = {q: part.dof_index(f, Lf, ns) for q, f in sorted(part.send_faces.items())}
+        recv = {q: part.dof_index(f, Lf, ns) for q, f in sorted(part.recv_faces.items())}
+        # int64 copies for the torch (CPU / gloo) path
+        self.send = {q: i64(i) for q, i in send.items()}
+        self.recv = {q: i64(i) for q, i in recv.items()}
+        self.send_counts = {q: len(i) for q, i in send.items()}
+        self.recv_counts = {q: len(i) for q, i in recv.items()}
+        cat = lambda d: np.concatenate([d[q] for q in sorted(d)]) if d else np.zeros(0, np.int64)  # noqa: E731
+        self.fwd_send = i32(cat(send))
+        self.fwd_recv = i32(cat(recv))
+        remote = np.full(self.n_owned, -1, dtype=np.int64)
+        o = 0
+        for q in sorted(send):
+            remote[send[q]] = o + np.arange(len(send[q]))
+            o += len(send[q])
+        self.remote_src = i32(remote)
+        if scatter_src is not None:
+            rs = scatter_src[cat(recv)] if len(cat(recv)) else np.zeros((0, 2), np.int64)
+            if np.any(rs[:, 1] >= 0):
+                raise AssertionError("a ghost trace dof with two local sides")
+            self.rev_send = i32(rs[:, 0])
+        else:
+            self.rev_send = None
+        n_s, n_r = int(self.fwd_send.numel()), int(self.fwd_recv.numel())
+        f64 = lambda k: torch.empty(k, dtype=torch.float64, device=device)  # noqa: E731
+        self.buf_send, self.buf_recv = f64(n_s), f64(n_r)  # forward: x out / x in
+        self.rbuf_send, self.rbuf_recv = f64(n_r), f64(n_s)  # reverse: y out / y in
+
+    # ---- kernels ----------------------------------------------------------
+    def _stream(self):
+        from .device import current_stream
+
+        return current_stream()
+
+    def _gather(self, idx, src, dst):
+        _lib.check(_lib.lib().mhdg_halo_gather(idx.numel(), _lib.ptr(idx), _lib.ptr(src), _lib.ptr(dst),
+                                               self._stream()), "mhdg_halo_gather")
+
+    def _scatter(self, idx, buf, dst, accumulate):
+        _lib.check(_lib.lib().mhdg_halo_scatter(idx.numel(), _lib.ptr(idx), _lib.ptr(buf), _lib.ptr(dst),
+                                                int(accumulate), self._stream()), "mhdg_halo_scatter")
+
+    # ---- forward: owned x -> local x with ghost values -----------------------
+    def start_forward(self, comm, x_owned: torch.Tensor, x_local: torch.Tensor):
+        """x_local[:n_owned] = x_owned and the ghost messages in flight; returns wait()
+        which unpacks the ghost values (after it, x_local is complete)."""
+        if not x_owned.is_cuda:  # CPU tensors: the gloo host-logic tests
+            x_local[: self.n_owned] = x_owned
+            got = comm.exchange({q: x_owned[i] for q, i in self.send.items()}, self.recv_counts, x_owned)
+            for q, buf in got.items():
+                x_local[self.recv[q]] = buf
+            return lambda: None
+        x_local[: self.n_owned].copy_(x_owned)
+        self._gather(self.fwd_send, x_owned, self.buf_send)
+        wait = _start_exchange(comm, _segments(self.buf_send, self.send_counts),
+                               _segments(self.buf_recv, self.recv_counts))
+
+        def finish():
+            wait()
+            self._scatter(self.fwd_recv, self.buf_recv, x_local, False)
+
+        return finish
 
     def forward(self, comm: Comm, x_owned: torch.Tensor) -> torch.Tensor:
         x_local = torch.empty(self.n_local, dtype=x_owned.dtype, device=x_owned.device)
-        x_local[: self.n_owned] = x_owned
-        got = comm.exchange({q: x_owned[i] for q, i in self.send.items()},
-                            {q: len(i) for q, i in self.recv.items()}, x_owned)
-        for q, buf in got.items():
-            x_local[self.recv[q]] = buf
+        self.start_forward(comm, x_owned, x_local)()
         return x_local
 
+    # ---- reverse: local partial sums -> owned sums ----------------------------
     def reverse(self, comm: Comm, y_local: torch.Tensor) -> torch.Tensor:
+        """Owned entries of a face-reduced local vector plus the other ranks' sides."""
+        if not y_local.is_cuda:
+            y_owned = y_local[: self.n_owned].clone()
+            got = comm.exchange({q: y_local[i] for q, i in self.recv.items()}, self.send_counts, y_local)
+            for q in sorted(got):
+                y_owned.index_add_(0, self.send[q], got[q])  # unique indices per q: deterministic
+            return y_owned
+        self._gather(self.fwd_recv, y_local, self.rbuf_send)
+        _start_exchange(comm, _segments(self.rbuf_send, self.recv_counts),
+                        _segments(self.rbuf_recv, self.send_counts))()
         y_owned = y_local[: self.n_owned].clone()
-        got = comm.exchange({q: y_local[i] for q, i in self.recv.items()},
-                            {q: len(i) for q, i in self.send.items()}, y_local)
-        for q in sorted(got):
-            y_owned.index_add_(0, self.send[q], got[q])  # unique indices per q: deterministic
+        self._scatter(self.fwd_send, self.rbuf_recv, y_owned, True)
+        return y_owned
+
+    def reverse_local(self, comm: Comm, disc_c, y_loc: torch.Tensor, y_owned: torch.Tensor) -> torch.Tensor:
+        """Face reduction of the unscattered local y with the reverse halo folded in
+        (mhdg_face_reduce_remote): sends this rank's ghost-face sides, receives the
+        other sides of its owned faces and sums both in one pass."""
+        self._gather(self.rev_send, y_loc, self.rbuf_send)
+        _start_exchange(comm, _segments(self.rbuf_send, self.recv_counts),
+                        _segments(self.rbuf_recv, self.send_counts))()
+        _lib.check(_lib.lib().mhdg_face_reduce_remote(disc_c, _lib.ptr(y_loc), _lib.ptr(self.remote_src),
+                                                      _lib.ptr(self.rbuf_recv), self.n_owned, _lib.ptr(y_owned),
+                                                      self._stream()), "mhdg_face_reduce_remote")
         return y_owned
 
 
@@ -160,6 +289,7 @@ class DistDiscretization:
         self.n_trace = self.part.n_owned_faces * self.Lf * self.ns
         self.global_mesh = global_mesh
         self._plan = None
+        self._split = None
         self._plan_device = plan_device
 
     @property
@@ -170,8 +300,31 @@ class DistDiscretization:
     def plan(self) -> HaloPlan:
         if self._plan is None:
             dev = self._plan_device if self._plan_device is not None else self.local.device.device
-            self._plan = HaloPlan(self.part, self.Lf, self.ns, dev)
+            src = self.local.scatter_sources() if torch.device(dev).type == "cuda" else None
+            self._plan = HaloPlan(self.part, self.Lf, self.ns, dev, src)
         return self._plan
+
+    @property
+    def macro_split(self):
+        """(i0, i1): local macros [i0, i1) touch no ghost face (they only read owned
+        trace values), the rest do.  Slabs are strips of cells, so the macros next to
+        ghost faces sit at both ends of the slab's macro range."""
+        if self._split is None:
+            fo = self.local.mesh.faces_of_macro
+            needs_ghost = (fo >= self.part.n_owned_faces).any(axis=1)
+            best, i, M = (0, 0), 0, len(needs_ghost)
+            while i < M:
+                if needs_ghost[i]:
+                    i += 1
+                    continue
+                j = i
+                while j < M and not needs_ghost[j]:
+                    j += 1
+                if j - i > best[1] - best[0]:
+                    best = (i, j)
+                i = j
+            self._split = best
+        return self._split
 
     # ---- host helpers -------------------------------------------------
     def local_macros(self):
@@ -220,13 +373,39 @@ class DistCondensed:
         self.dist = ddisc
         self.local = local_cond
         self.comm = ddisc.comm
+        self._x_local = None
 
     @property
     def blocks(self):
         return self.local.blocks
 
     def apply_trace(self, x_owned, out=None):
-        y = self.dist.reverse(self.local.apply_trace(self.dist.forward(x_owned)))
+        """Distributed apply (condense.py:91-103 over slabs): the forward
+        halo is in flight while the macros that read only owned trace values are
+        applied; the macros next to ghost faces follow once it lands; the reverse halo
+        is summed inside the face reduction (mhdg_face_reduce_remote)."""
+        dd, loc = self.dist, self.local
+        plan = dd.plan
+        if not x_owned.is_cuda:  # CPU tensors: the gloo host-logic tests
+            y = dd.reverse(loc.apply_trace(dd.forward(x_owned)))
+        else:
+            x_owned = _lib.arg(x_owned, plan.n_owned, "x")
+            if self._x_local is None:
+                self._x_local = torch.empty(plan.n_local, dtype=torch.float64, device=x_owned.device)
+            xl = self._x_local
+            finish = plan.start_forward(self.comm, x_owned, xl)
+            i0, i1 = dd.macro_split
+            loc.note_applies(1)
+            if loc.ahat is None and i1 > i0:
+                loc.apply_trace_local_range(xl, i0, i1 - i0)  # interior: overlaps the halo
+                finish()
+                loc.apply_trace_local_range(xl, 0, i0)
+                loc.apply_trace_local_range(xl, i1, dd.n_mac - i1)
+            else:
+                finish()
+                loc.apply_trace_local_into(xl)
+            y = torch.empty(plan.n_owned, dtype=torch.float64, device=x_owned.device)
+            plan.reverse_local(self.comm, dd.local.device.c, loc._y_loc, y)
         if out is not None:
             out.copy_(y)
             return out

@@ -62,48 +62,63 @@ def test_ptc_couette_vs_reference():
 
 @pytest.mark.parametrize("kind", ["lu", "inverse"])
 def test_c1_plane_couette_ptc_vs_oracle(kind):
-    """BASELINE configs[0] (C1) end to end on the device: PTC + FGMRES to 1e-10
-    from the seeded IC, against the oracle's run (oracle/make_c1_golden.py), with the
-    packed-LU (default) and explicit-inverse condensation factors."""
+    """BASELINE configs[0] (C1) end to end on the device: PTC + FGMRES to 1e-10 from
+    the seeded IC, against the oracle run with the same factor algebra
+    (oracle/make_c1_golden.py: "lu" = LAPACK LU solves, "inverse" = the reference's
+    explicit inverse, condense.py:67), step by step.
+
+    Every Newton step after the first ends at FGMRES's 400-iteration cap with the
+    linear system unconverged, so rounding-level differences are amplified by the
+    truncated Krylov solve: the oracle's own LU and inverse runs -- solves accurate to
+    1e-14 on these S -- already differ by 7e-7 in the state after step 2 and settle on
+    a uniform density offset of 2.4e-7 (steady Couette between isothermal walls in a
+    periodic channel leaves the density level free; PTC does not conserve mass).
+    Bounds: Newton +-1; per-step FGMRES +-1 on every common step; the state after
+    step 1 within 1e-8; after later common steps within 10x the oracle pair's own
+    spread at that step; final temperature and velocity within max(1e-8, 10x the
+    pair's spread); the final state a converged solution of the oracle's residual.  oracle/c1_ensemble.py records the
+    spread of Newton counts under 1e-14 initial-state noise (profiles/r2_c1_ensemble_*)."""
     need_gpu()
     from paper_2402_11361_b200 import condense as CD
     from paper_2402_11361_b200.cases import CouettePlane2D
     from paper_2402_11361_b200.mesh import build_square_mesh
+    import oracle.hdg_oracle as O
 
-    g = load_golden("c1_ptc_oracle")
+    g = load_golden("c1_ptc_oracle_lu" if kind == "lu" else "c1_ptc_oracle")
+    g_other = load_golden("c1_ptc_oracle" if kind == "lu" else "c1_ptc_oracle_lu")
     case = CouettePlane2D()
     mesh = build_square_mesh(case.domain, (8, 4), 2, periodic=(True, False))
     d = Discretization(mesh, 2, case.params, bcs=case.boundary_conditions())
     f = A.to_device_fields(d, g["u0"], g["q0"], g["uhat0"])
+    steps_u, steps_uhat, per_step = [], [], []
+
+    def log(st):
+        steps_u.append(host(f.u))
+        steps_uhat.append(host(f.uhat))
+        per_step.append(st.krylov_iterations - sum(per_step))
+
     old = CD.FACTOR
     try:
         CD.FACTOR = kind
-        st, _ = S.ptc_steady_solve(d, f, rel_tol=1e-10)
+        st, _ = S.ptc_steady_solve(d, f, rel_tol=1e-10, log=log)
     finally:
         CD.FACTOR = old
-    # The first Newton residuals agree with the oracle's to 3 digits; from the fourth on the
-    # PTC trajectory differs by the FGMRES truncation (~2% per step, in both device factor
-    # kinds), so the step that crosses the 1e-10 target can move by one.  Measured: inverse
-    # 8 Newton / 2879 FGMRES (oracle 8 / 2879); LU 7 / 2479 (residual 3.4e-10 -> 8.3e-11 at
-    # step 7 vs the oracle's 5.6e-10 -> 1.4e-10), i.e. one Newton step and its ~400 FGMRES
-    # iterations fewer.
-    for a, b in zip(st.residuals[:3], g["residuals"][:3]):
-        assert abs(a - b) <= 1e-3 * b
+    print(kind, "device newton", st.iterations, "fgmres", st.krylov_iterations, per_step,
+          "oracle", int(g["newton"]), int(g["krylov"]), list(g["krylov_per_step"]))
     assert abs(st.iterations - int(g["newton"])) <= 1
-    if kind == "inverse":
-        assert abs(st.krylov_iterations - int(g["krylov"])) <= 1
-    else:
-        # at most one Newton step's FGMRES iterations apart (a late PTC step takes ~400,
-        # 1.25x the run's average of 360)
-        per_step = 1.25 * int(g["krylov"]) / int(g["newton"])
-        assert abs(st.krylov_iterations - int(g["krylov"])) <= per_step * abs(st.iterations - int(g["newton"])) + 1
+    common = min(st.iterations, int(g["newton"]))
+    for k in range(common):
+        assert abs(per_step[k] - int(g["krylov_per_step"][k])) <= 1, k
+    assert abs(st.residuals[1] - g["residuals"][1]) <= 1e-8 * g["residuals"][1]  # step 1: before any cap
+    for k in range(common):
+        du = rel_err(steps_u[k], g["steps_u"][k])
+        duh = rel_err(steps_uhat[k], g["steps_uhat"][k])
+        pair = max(rel_err(g_other["steps_u"][k], g["steps_u"][k]),
+                   rel_err(g_other["steps_uhat"][k], g["steps_uhat"][k]))
+        print(f"  step {k + 1}: state vs oracle {du:.2e} / {duh:.2e}; oracle LU vs inverse {pair:.2e}")
+        tol = 1e-8 if k == 0 else max(1e-8, 10.0 * pair)
+        assert du < tol and duh < tol, (k, du, duh, pair)
     assert st.residuals[-1] <= max(1e-10, 1e-10 * st.residuals[0])  # ptc_steady_solve's target (abs_tol 1e-10)
-    # Steady Couette between isothermal walls in a periodic channel fixes velocity and
-    # temperature but not the pressure/density level (PTC does not conserve mass, so
-    # runs land on different members of that one-parameter family): compare the
-    # invariants, check the density offset is a uniform scale, and check the device
-    # state is a converged solution of the oracle's own residual.
-    import oracle.hdg_oracle as O
 
     def prim(u):
         rho, m, E = u[..., 0], u[..., 1:3], u[..., 3]
@@ -113,14 +128,19 @@ def test_c1_plane_couette_ptc_vs_oracle(kind):
 
     rho_d, v_d, T_d = prim(host(f.u))
     rho_o, v_o, T_o = prim(g["u"])
-    assert rel_err(T_d, T_o) < 1e-8  # measured 1.1e-9
-    ratio = rho_d / rho_o  # measured: uniform offset -3.7e-7, spread 3.3e-10 (inverse), 1.0e-9 (LU:
-    assert ratio.std() < 5e-9 * ratio.mean()  # stops one step earlier, residual 8.3e-11)
-    # the weakly determined density level leaks into v = m / rho at the 1e-8 level (measured 1.6e-8)
-    assert np.abs(v_d - v_o).max() < 5e-8 * np.abs(v_o).max()
+    rho_p, v_p, T_p = prim(g_other["u"])
+    # the free density level leaks into v = m / rho: bound v and T by the oracle pair's
+    # own final spread too (pair: 3.6e-9 in v, 2.7e-10 in T; device runs measured
+    # 1.1e-8 / 1.3e-8 in v, 7.5e-10 / 9.2e-10 in T)
+    for name, a, b, c in (("T", T_d, T_o, T_p), ("v", v_d, v_o, v_p)):
+        e, pair = rel_err(a, b), rel_err(c, b)
+        print(f"  final {name}: vs oracle {e:.2e}; oracle LU vs inverse {pair:.2e}")
+        assert e < max(1e-8, 10.0 * pair), (name, e, pair)
+    ratio = rho_d / rho_o  # the free density level: a uniform scale
+    assert ratio.std() < 1e-8 * ratio.mean()
     of = O.Fields(host(f.u), host(f.q), host(f.uhat))
     r_dev = np.sqrt(sum(float((r * r).sum()) for r in O.residual(d, of, O.Ctx.steady())))
-    assert r_dev <= 1e-10  # ptc_steady_solve's target; measured 2.68e-11 (oracle run: 3.73e-11)
+    assert r_dev <= 1e-10
 
 
 @pytest.mark.parametrize("kind", ["lu", "inverse"])
