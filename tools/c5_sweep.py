@@ -5,8 +5,10 @@ batched LU, timed), then 200 trace-operator applies on x ~ N(0, 1) (seed 1, time
 
 Combos whose device data exceed one GPU run the rank-0 slab of a P-GPU contiguous
 slab partition (the macros this GPU would own with P = 2, 4, 8 GPUs; partition.py),
-the smallest P that fits; "n_gpus_needed" says which.  Combos beyond 8 GPUs or the
-kernels' compile-time limits (LU for L ns <= 384) are listed as such.
+the smallest P that fits; "n_gpus_needed" says which.  The Schur scratch is bounded
+to CHUNK macros (condensed chunk by chunk, mhdg_factors.scratch_macros) so the
+resident data are the blocks plus the packed factors.  Combos beyond 8 GPUs or the
+factor kernels' limit (mhdg_factor_max_n) are listed as such.
 
     python tools/c5_sweep.py [n_ele_1d]   (default 32)     -> one JSON line per combo
 """
@@ -32,7 +34,8 @@ from paper_2402_11361_b200.partition import partition_mesh  # noqa: E402
 from paper_2402_11361_b200.refmacro import lattice_size  # noqa: E402
 
 N1D = int(sys.argv[1]) if len(sys.argv) > 1 else 32
-BUDGET = 150e9  # bytes of device data per GPU (of ~180 GB HBM3e)
+BUDGET = 160e9  # bytes of device data per GPU (of ~180 GB HBM3e)
+CHUNK = 4096  # macros of Schur scratch
 L_ = _lib.lib()
 
 
@@ -44,18 +47,19 @@ def bytes_per_macro(m, p):
     nq, nqf = (p + 1) ** d, (p + 1) ** (d - 1)
     n = L * ns
     blk = n * n + 3 * nf * (Lf * ns) ** 2 + m**d * nq * d * d * ns * ns + nf * m ** (d - 1) * nqf * d * ns * ns
-    return 8 * (blk + 2.1 * n * n + 8 * n + 20 * L * ns)
+    return 8 * (blk + 1.1 * n * n + 8 * n + 20 * L * ns)  # + the packed factor (scratch: CHUNK macros)
 
 
 def run(m, p):
     n = lattice_size(3, m * p) * 5
     out = {"m": m, "p": p, "L_ns": n}
-    if n > 384:
-        out["status"] = "not run: L ns > 384 (batched LU kernel limit)"
+    n_max = int(L_.mhdg_factor_max_n(1))
+    if n > n_max:
+        out["status"] = f"not run: L ns > {n_max} (batched LU kernel limit)"
         return out
     case = TgvCase(reynolds=1600.0, mach=0.1)
     gmesh = build_cube_mesh(case.domain, N1D, m, periodic=(True, True, True))
-    need = gmesh.n_macro * bytes_per_macro(m, p)
+    need = gmesh.n_macro * bytes_per_macro(m, p) + 8 * CHUNK * n * n
     P = 1
     while need / P > BUDGET:
         P *= 2
@@ -72,7 +76,7 @@ def run(m, p):
     blocks, _ = A.jacobian(disc, f, ctx)
     del f
     torch.cuda.synchronize()
-    cond = CondensedSchur.allocate(blocks)
+    cond = CondensedSchur.allocate(blocks, scratch_macros=CHUNK)
     st = disc.device.status_buffer()
     cond.refactor_async(st)
     torch.cuda.synchronize()
