@@ -68,8 +68,8 @@ __global__ void __launch_bounds__(KV_T) k_vec_pass(long long n, int rows, const 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nb = gridDim.x;
   const KvScratch sc(scratch, nb);
   const long long base = (long long)blockIdx.x * KV_SL + tid;
-  if (UPD)
-    for (int i = tid; i < rows; i += KV_T) cs[i] = coef[i];
+  if (UPD)  // coefficients, zero-padded to a multiple of KV_R rows
+    for (int i = tid; i < KV_MAXR; i += KV_T) cs[i] = i < rows ? coef[i] : 0.0;
   double wr[KV_E];
   bool ok[KV_E];
 #pragma unroll
@@ -83,12 +83,18 @@ __global__ void __launch_bounds__(KV_T) k_vec_pass(long long n, int rows, const 
     double s[KV_E];
 #pragma unroll
     for (int k = 0; k < KV_E; ++k) s[k] = 0.0;
-    for (int i = 0; i < rows; ++i) {
-      const double c = cs[i];
-      const double* vr = V + (long long)i * ldv + base;
+    for (int i0 = 0; i0 < rows; i0 += KV_R) {  // KV_R rows of loads in flight, then the FMAs in row order
+      double vv[KV_R][KV_E];
 #pragma unroll
-      for (int k = 0; k < KV_E; ++k)
-        if (ok[k]) s[k] += c * vr[(long long)k * KV_T];
+      for (int r = 0; r < KV_R; ++r) {
+        const double* vr = V + (long long)(i0 + r) * ldv + base;
+#pragma unroll
+        for (int k = 0; k < KV_E; ++k) vv[r][k] = (i0 + r < rows && ok[k]) ? vr[(long long)k * KV_T] : 0.0;
+      }
+#pragma unroll
+      for (int r = 0; r < KV_R; ++r)
+#pragma unroll
+        for (int k = 0; k < KV_E; ++k) s[k] += cs[i0 + r] * vv[r][k];
     }
 #pragma unroll
     for (int k = 0; k < KV_E; ++k) {
