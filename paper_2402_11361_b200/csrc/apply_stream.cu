@@ -473,8 +473,10 @@ __global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 ? 1 : 2)) k_apply_s
         if (on) {
           const int tt = j % NS, l = j / NS;
           double a = 0.0;
-          if (!face) {  // v[l][tt] = sum_b phi[q][b] z[l][conn[K][b]][tt], formed ahead in wv
-            a = wv[(u0 + pl) * DN + j];
+          if (!face) {  // v[l][tt] = sum_b phi[q][b] z[l][conn[K][b]][tt]
+            const int pt = u0 + pl, K = pt / NQ, q = pt % NQ;
+#pragma unroll
+            for (int b = 0; b < NLOC; ++b) a += phs[q * NLOC + b] * z[(l * L + conn[K * NLOC + b]) * NS + tt];
           } else {
             const double* zs = second ? z2 : z;
             const int lstride = second ? C::NFN : L;
@@ -495,15 +497,15 @@ __global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 ? 1 : 2)) k_apply_s
             const double* w = A + pl * C::NW + k * D * NS * NS + s * NS;
             const double* v = vw + pi * DN;
             const int rot = (pi * D + k) % DN;
-            double a0 = 0.0, a1 = 0.0;  // two chains
+            double a = 0.0;
 #pragma unroll
             for (int i = 0; i < DN; ++i) {
               int ii = i + rot;
               if (ii >= DN) ii -= DN;
               const int l = ii / NS, tt = ii - l * NS;
-              ((i & 1) ? a1 : a0) += w[l * NS * NS + tt] * v[ii];
+              a += w[l * NS * NS + tt] * v[ii];
             }
-            wv[(u0 + pl) * DN + j] = a0 + a1;  // in place: this lane's v entry was copied to vw
+            wv[(u0 + pl) * DN + j] = a;
           }
         } else if (on && j < NS) {
           const int s = j;
@@ -643,19 +645,6 @@ __global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 ? 1 : 2)) k_apply_s
         }
       }
       cbar();  // z complete; tg free for the W_vol results
-      {  // v[pt][l][tt] = sum_b phi[q][b] z[l][conn[K][b]][tt] for every volume point, all warps,
-         // ahead of the W_vol stash (the W_vol passes then only contract: W v, in place)
-        constexpr int DN = D * NS;
-        for (int idx = tid; idx < C::NPV * DN; idx += NCONS) {
-          const int pt = idx / DN, j = idx - pt * DN, l = j / NS, tt = j - l * NS, K = pt / NQ, q = pt - K * NQ;
-          double a0 = 0.0, a1 = 0.0;
-#pragma unroll
-          for (int b = 0; b < NLOC; ++b)
-            ((b & 1) ? a1 : a0) += phs[q * NLOC + b] * z[(l * L + conn[K * NLOC + b]) * NS + tt];
-          wv[idx] = a0 + a1;
-        }
-      }
-      cbar();
       if (tid == 0) { PROF_ADD(K_FST, 2, t1); }
       PROF_T(t2);
       seg_loop<NF * BS, units_per_piece(BS)>(rg, lane, [&](const double* A, int u0, int nu) {
