@@ -247,9 +247,29 @@ __device__ unsigned long long g_prof[16][3];
 constexpr int MAXP = 256;  // pieces per macro (checked on the host)
 
 // First group >= g0 that warp `warp` owns when groups are dealt round-robin
-// by global index: consecutive pieces of one kind keep all warps busy.
-__device__ __forceinline__ int first_group(int g0, int warp) {
-  return g0 + ((warp - g0 % NWARP_C) % NWARP_C + NWARP_C) % NWARP_C;
+// by global index over nw warps: consecutive pieces of one kind keep all warps busy.
+__device__ __forceinline__ int first_group(int g0, int warp, int nw = NWARP_C) {
+  return g0 + ((warp - g0 % nw) % nw + nw) % nw;
+}
+
+// The stash contractions (W_vol, W_face) hold ~10 quadrature points per ring stage:
+// fewer point groups than consumer warps, and every group a dependent FMA chain.
+// SPLIT consumption: the two halves of the consumer warps take alternate pieces, so
+// two stages are contracted at once; every warp still waits for and releases every
+// stage (the empty barrier counts all consumer warps), a warp skipping a piece only
+// waits for it to land first.
+constexpr int WSPLIT = 2;
+template <int NROWS, int PER, class R, class Body>
+__device__ __forceinline__ void seg_loop_split(R& rg, int lane, int warp, Body&& body) {
+  constexpr int NWH = NWARP_C / WSPLIT;
+  const int half = warp / NWH, wid = warp - half * NWH;
+  int k = 0;
+#pragma unroll 1
+  for (int u0 = 0; u0 < NROWS; u0 += PER, ++k) {
+    const double* A = rg.wait();
+    if (k % WSPLIT == half) body(A, u0, (NROWS - u0) < PER ? NROWS - u0 : PER, wid, NWH);
+    rg.release(lane);
+  }
 }
 
 // acc_r = sum_c A[r][c] vec_r[c] for rows u0 .. u0+nu-1 of a staged piece, LPR
@@ -463,11 +483,11 @@ __global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 ? 1 : 2)) k_apply_s
 
     // W_vol / W_face contraction of one piece: v = phi z (gathered), out = W v.
     // Point groups of PPI points per warp pass, dealt to warps by global index.
-    auto wcontract = [&](const double* A, int u0, int nu, bool face, bool second) {
+    auto wcontract = [&](const double* A, int u0, int nu, bool face, bool second, int wid, int nw) {
       constexpr int DN = D * NS, PPI = 32 / DN;
       const int pi = lane / DN, j = lane % DN;
       const int ngrp = (nu + PPI - 1) / PPI;
-      for (int grp = first_group(u0 / PPI, warp) - u0 / PPI; grp < ngrp; grp += NWARP_C) {
+      for (int grp = first_group(u0 / PPI, wid, nw) - u0 / PPI; grp < ngrp; grp += nw) {
         const int pl = grp * PPI + pi;
         const bool on = pi < PPI && pl < nu;
         if (on) {
@@ -659,14 +679,16 @@ __global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 ? 1 : 2)) k_apply_s
       });
       if (tid == 0) { PROF_ADD(K_FTT, 1, t3); }
       PROF_T(t4);
-      seg_loop<C::NPV, SC::WV_ALIGN ? SC::WV_PER : units_per_piece(C::NW)>(
-          rg, lane, [&](const double* A, int u0, int nu) {
-            wcontract(A + (((C::NPV * C::NW) & 1) && (mac & 1) ? 1 : 0), u0, nu, false, false);
+      seg_loop_split<C::NPV, SC::WV_ALIGN ? SC::WV_PER : units_per_piece(C::NW)>(
+          rg, lane, warp, [&](const double* A, int u0, int nu, int wid, int nw) {
+            wcontract(A + (((C::NPV * C::NW) & 1) && (mac & 1) ? 1 : 0), u0, nu, false, false, wid, nw);
           });
       if (tid == 0) { PROF_ADD(K_WV, 1, t4); }
       PROF_T(t5);
-      seg_loop<C::NPF, units_per_piece(C::NWF)>(
-          rg, lane, [&](const double* A, int u0, int nu) { wcontract(A, u0, nu, true, false); });
+      seg_loop_split<C::NPF, units_per_piece(C::NWF)>(
+          rg, lane, warp, [&](const double* A, int u0, int nu, int wid, int nw) {
+            wcontract(A, u0, nu, true, false, wid, nw);
+          });
       if (tid == 0) { PROF_ADD(K_WFZ, 1, t5); }
       PROF_T(t6);
       cbar();  // rfst, W_vol results, W_face(z) stash complete
@@ -783,8 +805,10 @@ __global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 ? 1 : 2)) k_apply_s
     cbar();  // z2 and yf complete
     if (tid == 0) { PROF_ADD(K_WF2, 2, t10); }
     PROF_T(t11);
-    seg_loop<C::NPF, units_per_piece(C::NWF)>(
-        rg, lane, [&](const double* A, int u0, int nu) { wcontract(A, u0, nu, true, true); });
+    seg_loop_split<C::NPF, units_per_piece(C::NWF)>(
+        rg, lane, warp, [&](const double* A, int u0, int nu, int wid, int nw) {
+          wcontract(A, u0, nu, true, true, wid, nw);
+        });
     seg_loop<NF * BS, units_per_piece(BS)>(rg, lane, [&](const double* A, int u0, int nu) {
       rows_dot<4, BS>(A, u0, nu, [&](int rl) { return yf + ((u0 + rl) / BS) * BS; },
                       [&](int rl, double acc) { fts[u0 + rl] = acc; });
