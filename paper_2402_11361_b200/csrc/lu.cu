@@ -154,7 +154,7 @@ __device__ __forceinline__ void trail_pass_loop(double* __restrict__ A, int n, i
 
 template <int NB, int NT, int RPT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) k_lu4(int n, double* __restrict__ S, int* __restrict__ piv_out,
-                                                  int* status, int l2mode) {
+                                                  int* status, int l2mode, int n_mac) {
   using namespace lu4;
   constexpr int NW = NT / 32, PS = pstride<NB>(), NH = NB / 32;  // NH: 32-column halves of a panel
   extern __shared__ __align__(16) double sm[];
@@ -165,8 +165,12 @@ __global__ void __launch_bounds__(NT, MINB) k_lu4(int n, double* __restrict__ S,
   unsigned char* rflag = reinterpret_cast<unsigned char*>(npl + 2 * n);   // n: 1 = pivot row
   __shared__ int pv[NB];                            // this panel's pivot rows, logical order
   __shared__ int wcnt[NW];
-  const int mac = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t4 = lane & 3;
+  // grid = n_mac (one macro per CTA) or persistent (fewer CTAs walk the macros: fewer
+  // trailing matrices resident at once, so they stay in L2)
+#pragma unroll 1
+  for (int mac = blockIdx.x; mac < n_mac; mac += gridDim.x) {
   double* A = S + (size_t)mac * n * n;
   int* pivg = piv_out + (size_t)mac * n;
   bool singular = false;
@@ -549,6 +553,8 @@ __global__ void __launch_bounds__(NT, MINB) k_lu4(int n, double* __restrict__ S,
     LUADD(5, pt5);
   }
   if (singular && tid == 0) set_status(status, MHDG_ERR_FACTORIZATION, mac, 0, 0.0);
+  __syncthreads();  // the next macro reuses the shared panel and row lists
+  }
 }
 
 // --------------------------------------------------------------------------
@@ -629,8 +635,10 @@ int pack_lu4(int n, int n_mac, const double* scratch, const int* piv, double* pa
 
 
 
-static int g_lu_nb = 32, g_lu_nt = 0, g_lu_l2mode = MHDG_LU_L2MODE;
+static int g_lu_nb = 32, g_lu_nt = 0, g_lu_l2mode = MHDG_LU_L2MODE, g_lu_grid = 0;
 extern "C" void mhdg_set_lu_l2mode(int m) { g_lu_l2mode = m; }
+extern "C" void mhdg_set_lu_grid(int ctas) { g_lu_grid = ctas; }
+static inline int lu_grid(int n_mac) { return g_lu_grid > 0 && g_lu_grid < n_mac ? g_lu_grid : n_mac; }
 extern "C" void mhdg_set_lu_panel(int nb, int threads) {
   g_lu_nb = nb == 64 ? 64 : 32;
   g_lu_nt = threads;
@@ -645,7 +653,7 @@ static int launch_lu4(int n, int n_mac, double* scratch, int* piv, int* status, 
   if (MINB > 1 && 2 * bytes > 228 * 1024) return -1;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   tl_begin(TL_FACTOR, st);
-  kern<<<n_mac, NT, bytes, st>>>(n, scratch, piv, status, g_lu_l2mode);
+  kern<<<lu_grid(n_mac), NT, bytes, st>>>(n, scratch, piv, status, g_lu_l2mode, n_mac);
   tl_end(TL_FACTOR, st);
   return 0;
 }
@@ -660,7 +668,7 @@ static int launch_lu4_large(int n, int n_mac, double* scratch, int* piv, int* st
   auto kern = k_lu4<NB, NT, 3, 1>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   tl_begin(TL_FACTOR, st);
-  kern<<<n_mac, NT, bytes, st>>>(n, scratch, piv, status, g_lu_l2mode);
+  kern<<<lu_grid(n_mac), NT, bytes, st>>>(n, scratch, piv, status, g_lu_l2mode, n_mac);
   tl_end(TL_FACTOR, st);
   return 0;
 }

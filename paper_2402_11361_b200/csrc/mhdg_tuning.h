@@ -26,6 +26,10 @@ void mhdg_set_lu_panel(int nb, int threads);
    mac % mode != 0 (mode >= 2; default 2 = every other macro), on all (1) or none (0). */
 void mhdg_set_lu_l2mode(int mode);
 
+/* Persistent grid of k_lu4: ctas > 0 launches that many CTAs walking the macros
+   (fewer trailing matrices resident at once); 0 (default): one CTA per macro. */
+void mhdg_set_lu_grid(int ctas);
+
 /* 1 (default): split apply (pre / factor solve / post kernels) when `work` is set;
    0: fused single-kernel apply. */
 void mhdg_set_apply_split(int on);
