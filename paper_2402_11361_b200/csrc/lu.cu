@@ -639,18 +639,24 @@ static int g_lu_nb = 32, g_lu_nt = 0, g_lu_l2mode = MHDG_LU_L2MODE, g_lu_grid = 
 extern "C" void mhdg_set_lu_l2mode(int m) { g_lu_l2mode = m; }
 extern "C" void mhdg_set_lu_grid(int ctas) { g_lu_grid = ctas; }
 static inline int lu_grid(int n_mac) { return g_lu_grid > 0 && g_lu_grid < n_mac ? g_lu_grid : n_mac; }
+// n <= 192 (C3's n = 175 and the smaller C5 combos): CTAs of 32 / 64 / 96 threads (n <= 64 /
+// 128 / 192), two rows per thread, 8 / 6 / 4 CTAs per SM -- the factorisation is bound by each
+// macro's pivot chain, so more macros in flight per SM (C3: 15.6 -> 13.5 ms; A/B knob)
+static int g_lu_small = 2;
+extern "C" void mhdg_set_lu_small(int on) { g_lu_small = on; }
 extern "C" void mhdg_set_lu_panel(int nb, int threads) {
   g_lu_nb = nb == 64 ? 64 : 32;
   g_lu_nt = threads;
 }
 
-template <int NB, int NT, int MINB>
+template <int NB, int NT, int MINB, int MAXRPT = 2>
 static int launch_lu4(int n, int n_mac, double* scratch, int* piv, int* status, cudaStream_t st) {
-  if (n > 2 * NT) return -1;
+  if (n > MAXRPT * NT) return -1;
   const size_t bytes = lu4::smem_bytes<NB, NT>(n);
   if (bytes > 227 * 1024) return -1;
-  auto kern = n <= NT ? k_lu4<NB, NT, 1, MINB> : k_lu4<NB, NT, 2, MINB>;
-  if (MINB > 1 && 2 * bytes > 228 * 1024) return -1;
+  auto kern = n <= NT ? k_lu4<NB, NT, 1, MINB> : n <= 2 * NT || MAXRPT < 3 ? k_lu4<NB, NT, 2, MINB>
+                                                                           : k_lu4<NB, NT, MAXRPT, MINB>;
+  if (MINB > 1 && MINB * (bytes + 1024) > 228 * 1024) return -1;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   tl_begin(TL_FACTOR, st);
   kern<<<lu_grid(n_mac), NT, bytes, st>>>(n, scratch, piv, status, g_lu_l2mode, n_mac);
@@ -681,9 +687,18 @@ int lu_factor4(int n, int n_mac, double* scratch, int* piv, double* packed, int*
 #ifndef MHDG_LU4_NT
 #define MHDG_LU4_NT 192
 #endif
-  int rc0 = g_lu_nb != 64   ? launch_lu4<32, MHDG_LU4_NT, 2>(n, n_mac, scratch, piv, status, st)
-            : g_lu_nt == 384 ? launch_lu4<64, 384, 1>(n, n_mac, scratch, piv, status, st)
-                             : launch_lu4<64, 256, 1>(n, n_mac, scratch, piv, status, st);
+  int rc0 = -1;
+  if (g_lu_small && g_lu_nb != 64) {  // smaller CTAs, more macros per SM, while 2 rows per thread cover n
+    if (n <= 64) rc0 = launch_lu4<32, 32, 8>(n, n_mac, scratch, piv, status, st);
+    else if (n <= 128) rc0 = launch_lu4<32, 64, 6>(n, n_mac, scratch, piv, status, st);
+    else if (n <= 192)
+      rc0 = g_lu_small == 2 ? launch_lu4<32, 64, 4, 3>(n, n_mac, scratch, piv, status, st)
+                            : launch_lu4<32, 96, 4>(n, n_mac, scratch, piv, status, st);
+  }
+  if (rc0 < 0)
+    rc0 = g_lu_nb != 64   ? launch_lu4<32, MHDG_LU4_NT, 2>(n, n_mac, scratch, piv, status, st)
+          : g_lu_nt == 384 ? launch_lu4<64, 384, 1>(n, n_mac, scratch, piv, status, st)
+                           : launch_lu4<64, 256, 1>(n, n_mac, scratch, piv, status, st);
   if (rc0 < 0) rc0 = launch_lu4_large<32, 192>(n, n_mac, scratch, piv, status, st);
   if (rc0 < 0) return -1;
   int rc = launch_ok();

@@ -30,6 +30,11 @@ void mhdg_set_lu_l2mode(int mode);
    (fewer trailing matrices resident at once); 0 (default): one CTA per macro. */
 void mhdg_set_lu_grid(int ctas);
 
+/* LU kernel shape for n <= 192: 2 (default) CTAs of 32 / 64 / 64 threads for n <= 64 / 128 / 192
+   (2 / 2 / 3 rows per thread, 8 / 6 / 4 CTAs per SM); 1: as 2 but 96 threads for n <= 192;
+   0: the 192-thread, two-CTAs-per-SM kernel. */
+void mhdg_set_lu_small(int on);
+
 /* 1 (default): split apply (pre / factor solve / post kernels) when `work` is set;
    0: fused single-kernel apply. */
 void mhdg_set_apply_split(int on);
