@@ -247,3 +247,46 @@ def test_stored_local_operators_2d_c1_matches_matrix_free():
     for x, ymf in zip(xs, y_mf):
         assert rel_err(host(cond.apply_trace(x)), ymf) < 1e-12
     assert torch.equal(cond.apply_trace(xs[0]), cond.apply_trace(xs[0]))
+
+
+@pytest.mark.parametrize("name", ["uniform_m4p3", "couette_m2p2"])
+def test_chunked_condensation_and_range_apply(name):
+    """mhdg_factors.scratch_macros (Schur + LU + pack chunk by chunk) gives bitwise the
+    factors of the one-shot condensation, and the local apply over macro ranges
+    (mhdg_apply_trace_local_range, the slab overlap) equals the full local apply."""
+    need_gpu()
+    d, fn, ctx = _cases_2d()[name]
+    of = perturbed_fields(d, fn, 33)
+    ob, _ = O.jacobian(d, of, ctx)
+    blocks = upload_blocks(d, ob)
+    full = CondensedSchur.build(blocks)
+    chunked = CondensedSchur.allocate(blocks, scratch_macros=3)
+    assert chunked.scratch.shape[0] == 3
+    chunked.refactor()
+    assert torch.equal(full.lu, chunked.lu) and torch.equal(full.perm, chunked.perm)
+    x = dev(np.random.default_rng(4).standard_normal(d.n_trace))
+    y_full = full.apply_trace_local(x)
+    for cuts in ((0, 1, d.n_mac), (0, d.n_mac // 2, d.n_mac), (0, 3, 5, d.n_mac)):
+        full._y_loc.zero_()
+        for a, b in zip(cuts[:-1], cuts[1:]):
+            full.apply_trace_local_range(x, a, b - a)
+        assert torch.equal(full._y_loc.view_as(y_full), y_full), cuts
+
+
+def test_factor_size_limit_raises_config_error():
+    """L ns above the factor kernels' limit (mhdg_factor_max_n) raises ConfigError at
+    allocation instead of a launch failure."""
+    need_gpu()
+    from paper_2402_11361_b200.condense import FACTOR, FACTOR_KINDS
+    from paper_2402_11361_b200.discretization import ConfigError
+
+    n_max = int(_lib.lib().mhdg_factor_max_n(FACTOR_KINDS[FACTOR]))
+    assert n_max >= 420
+    c2 = UniformFlow2D()
+    d = Discretization(build_square_mesh(c2.domain, 1, 8, periodic=(True, True)), 4, c2.params)  # L ns = 2244
+    assert d.L * d.ns > n_max
+    from paper_2402_11361_b200.assembly import LocalBlocks
+
+    blocks = LocalBlocks.empty(d)
+    with pytest.raises(ConfigError):
+        CondensedSchur.allocate(blocks)

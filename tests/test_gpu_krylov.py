@@ -93,3 +93,41 @@ def test_auto_stored_representation_mid_solve(monkeypatch):
     assert cond.ahat is not None and n1 > d.nf * d.Lf * d.ns
     assert abs(r0.iterations - r1.iterations) <= 1 and r1.converged
     assert float((r1.x - r0.x).abs().max() / r0.x.abs().max()) < 1e-8
+
+
+@pytest.mark.parametrize("n,rows", [(1, 1), (1000, 7), (638976, 21), (3686400, 9)])
+def test_vec_pass_modes_match_torch(n, rows):
+    """mhdg_vec_pass (csrc/krylov.cu), every mode, at sizes up to C3's trace length:
+    dots, update + dots, update + norm, combine (x += V^T y), norm -- against torch
+    float64, and bitwise deterministic."""
+    need_gpu()
+    g = torch.Generator(device="cuda").manual_seed(n + rows)
+    V = torch.randn(rows + 1, n, dtype=torch.float64, device="cuda", generator=g)
+    w0 = torch.randn(n, dtype=torch.float64, device="cuda", generator=g)
+    c = torch.randn(rows, dtype=torch.float64, device="cuda", generator=g)
+    out = torch.empty(64, dtype=torch.float64, device="cuda")
+    Vr = V[:rows]
+
+    def run(mode):
+        w = w0.clone()
+        K._vec_pass(n, rows, V, w, c, mode, out)
+        torch.cuda.synchronize()
+        return w, out.clone()
+
+    tol = lambda ref: 1e-12 * max(1.0, float(ref.abs().max()))  # noqa: E731
+    w, o = run(0)
+    assert torch.equal(w, w0) and float((o[:rows] - Vr @ w0).abs().max()) <= tol(Vr @ w0) * n ** 0.5
+    upd = w0 - Vr.T @ c
+    w, o = run(1)
+    assert float((w - upd).abs().max()) <= tol(upd)
+    assert float((o[:rows] - Vr @ upd).abs().max()) <= tol(Vr @ upd) * n ** 0.5
+    w, o = run(2)
+    assert abs(float(o[0]) - float(upd @ upd)) <= 1e-12 * float(upd @ upd)
+    w, o = run(3)
+    comb = w0 + Vr.T @ c
+    assert float((w - comb).abs().max()) <= tol(comb)
+    w, o = run(4)
+    assert abs(float(o[0]) - float(w0 @ w0)) <= 1e-12 * float(w0 @ w0)
+    for mode in range(5):  # deterministic
+        a, b = run(mode), run(mode)
+        assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
