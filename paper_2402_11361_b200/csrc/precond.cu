@@ -81,17 +81,27 @@ __global__ void __launch_bounds__(PRE_THREADS) k_precond_build(mhdg_disc g, mhdg
     if (tid == 0) set_status(status, MHDG_ERR_PRECONDITIONER, f, 0, 0.0);
     return;
   }
-  // B <- L^-1 (lower), one column per thread
-  for (int c = tid; c < bs; c += blockDim.x) {
-    for (int i = 0; i < c; ++i) B[i * bs + c] = 0.0;
-    B[c * bs + c] = 1.0 / X[c * bs + c];
-    for (int i = c + 1; i < bs; ++i) {
-      double acc = 0.0;
-      for (int k = c; k < i; ++k) acc += X[i * bs + k] * B[k * bs + c];
-      B[i * bs + c] = -acc / X[i * bs + i];
-    }
+  // B <- L^-1 (lower) by forward elimination on the identity, all threads per step:
+  // step k scales row k by 1 / L_kk, then removes L_ik x row k from the rows below.  Each
+  // entry accumulates its terms in the same order (k ascending) and is divided once, as the
+  // column-by-column substitution does, so the result is bitwise that of the serial
+  // per-column loop -- with bs steps of parallel work instead of one thread per column.
+  for (int idx = tid; idx < bs * bs; idx += blockDim.x) {
+    const int r = idx / bs, c = idx - r * bs;
+    B[idx] = (r == c) ? 1.0 : 0.0;
   }
   __syncthreads();
+  for (int k = 0; k < bs; ++k) {
+    const double lkk = X[k * bs + k];
+    for (int c = tid; c <= k; c += blockDim.x) B[k * bs + c] = c == k ? 1.0 / lkk : B[k * bs + c] / lkk;
+    __syncthreads();
+    const int rows = bs - k - 1, cols = k + 1;
+    for (int idx = tid; idx < rows * cols; idx += blockDim.x) {
+      const int i = k + 1 + idx / cols, c = idx - (idx / cols) * cols;
+      B[i * bs + c] -= X[i * bs + k] * B[k * bs + c];
+    }
+    __syncthreads();
+  }
   // inv = L^-T L^-1
   double* out = inv + (size_t)f * bs * bs;
   for (int idx = tid; idx < bs * bs; idx += blockDim.x) {
