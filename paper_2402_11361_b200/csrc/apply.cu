@@ -202,6 +202,69 @@ __global__ void __launch_bounds__(APPLY_THREADS) k_lu_solve(int n, mhdg_factors 
   for (int i = threadIdx.x; i < n; i += blockDim.x) yout[(size_t)mac * n + i] = y[i];
 }
 
+// zr = A_qq^-1 R_Q for every macro (the first step of rhs / recover, condense.py:105-127),
+// into global memory for the streamed rhs / recovery (apply_stream.cu: cond_stream)
+template <int D>
+__global__ void __launch_bounds__(APPLY_THREADS) k_mass_solve(mhdg_disc g, const double* __restrict__ R_grad,
+                                                              double* __restrict__ zr) {
+  constexpr int NS = D + 2;
+  const Sz sz = make_sz<D>(g);
+  const size_t off = (size_t)blockIdx.x * D * sz.L * NS;
+  mass_solve<D>(g, sz, blockIdx.x, R_grad + off, zr + off);
+}
+
+// The tail of the streamed recovery: du = y2 (the factor solve's output in the split
+// apply's work buffer), dq = -zr - A_qq^-1 A_qu du - A_qq^-1 A_qh dtrace (condense.py:112-127)
+template <int D>
+__global__ void __launch_bounds__(APPLY_THREADS) k_recover_dq(mhdg_disc g, const double* __restrict__ dtrace,
+                                                              const double* __restrict__ zr,
+                                                              const double* __restrict__ y2, long long y2_stride,
+                                                              double* __restrict__ du, double* __restrict__ dq) {
+  extern __shared__ double sm[];
+  constexpr int NS = D + 2;
+  const Sz sz = make_sz<D>(g);
+  const int mac = blockIdx.x;
+  double *xl = sm, *y = xl + sz.ltr, *z = y + sz.n, *z2 = z + D * sz.L * NS;
+  const int* gat = g.gather + (size_t)mac * sz.ltr;
+  const double* y2m = y2 + (size_t)mac * y2_stride;
+  for (int i = threadIdx.x; i < sz.ltr; i += blockDim.x) xl[i] = __ldg(dtrace + __ldg(gat + i));
+  for (int i = threadIdx.x; i < sz.n; i += blockDim.x) {
+    const double v = y2m[i];
+    y[i] = v;
+    du[(size_t)mac * sz.n + i] = v;
+  }
+  __syncthreads();
+  grad_trace_solve<D>(g, sz, mac, xl, z, false, 1.0);
+  grad_state_solve<D>(g, sz, mac, y, z2, false, 1.0);
+  __syncthreads();
+  const double* zrm = zr + (size_t)mac * D * sz.L * NS;
+  for (int i = threadIdx.x; i < D * sz.L * NS; i += blockDim.x)
+    dq[(size_t)mac * D * sz.L * NS + i] = (-zrm[i] - z2[i]) - z[i];
+}
+
+template <int D>
+int mass_solve_all(const mhdg_disc& g, const double* R_grad, double* zr, cudaStream_t st) {
+  k_mass_solve<D><<<g.n_mac, APPLY_THREADS, 0, st>>>(g, R_grad, zr);
+  return launch_ok();
+}
+
+template <int D>
+int recover_dq(const mhdg_disc& g, const double* dtrace, const double* zr, const double* y2, long long y2_stride,
+               double* du, double* dq, cudaStream_t st) {
+  const Sz sz = make_sz<D>(g);
+  const size_t bytes = sizeof(double) * ((size_t)sz.ltr + sz.n + 2 * (size_t)D * sz.L * (D + 2));
+  if (bytes > 48 * 1024) cudaFuncSetAttribute(k_recover_dq<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  k_recover_dq<D><<<g.n_mac, APPLY_THREADS, bytes, st>>>(g, dtrace, zr, y2, y2_stride, du, dq);
+  return launch_ok();
+}
+
+template int mass_solve_all<2>(const mhdg_disc&, const double*, double*, cudaStream_t);
+template int mass_solve_all<3>(const mhdg_disc&, const double*, double*, cudaStream_t);
+template int recover_dq<2>(const mhdg_disc&, const double*, const double*, const double*, long long, double*, double*,
+                           cudaStream_t);
+template int recover_dq<3>(const mhdg_disc&, const double*, const double*, const double*, long long, double*, double*,
+                           cudaStream_t);
+
 // ---------------------------------------------------------------------------
 // host launchers
 // ---------------------------------------------------------------------------

@@ -316,10 +316,21 @@ struct Work {
   }
 };
 
+// Extra inputs that turn the pre part into the condensed rhs / recovery (condense.py:105-127):
+// x == nullptr reads a zero trace; z += z_sign * z_add (the per-macro A_qq^-1 R_Q, layout
+// (mac, l, node, s)); y1 += y1_sign * y1_add (R_U) before the hand-off.  All zero: the apply.
+struct StreamIn {
+  const double* z_add;
+  double z_sign;
+  const double* y1_add;
+  double y1_sign;
+};
+
 template <class C, int STAGES, int PART>
 __global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 ? 1 : 2)) k_apply_stream(mhdg_disc g, mhdg_blocks bk, mhdg_factors fac,
                                                              const double* __restrict__ x,
-                                                             double* __restrict__ y_loc, int pref_ahead) {
+                                                             double* __restrict__ y_loc, int pref_ahead,
+                                                             StreamIn sin) {
   constexpr int D = C::D, NS = C::NS, NF = C::NF, L = C::L, LF = C::LF, BS = C::BS, LTR = C::LTR, n = C::n;
   constexpr int NLOC = C::NLOC, NQ = C::NQ, NLOCF = C::NLOCF, NQF = C::NQF, NTRI = C::NTRI, NSUB = C::NSUB;
   static_assert(LTR <= NCONS, "one local trace entry per consumer thread");
@@ -461,7 +472,7 @@ __global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 ? 1 : 2)) k_apply_s
 
   // this thread's trace entry of the next macro, gathered one macro ahead
   double x_next = 0.0;
-  if (PART != 2 && tid < LTR && blockIdx.x < g.n_mac)
+  if (PART != 2 && tid < LTR && blockIdx.x < g.n_mac && x)
     x_next = __ldg(x + __ldg(g.gather + (size_t)blockIdx.x * LTR + tid));
 
   for (int mac = blockIdx.x; mac < g.n_mac; mac += gridDim.x) {
@@ -476,7 +487,7 @@ __global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 ? 1 : 2)) k_apply_s
     if (PART != 2 && tid < LTR) {
       xl[tid] = x_next;
       const int nm = mac + gridDim.x;
-      if (nm < g.n_mac) x_next = __ldg(x + __ldg(g.gather + (size_t)nm * LTR + tid));
+      if (nm < g.n_mac && x) x_next = __ldg(x + __ldg(g.gather + (size_t)nm * LTR + tid));
     }
     cbar();  // xl complete; the previous macro's readers of every work array are done
     if (tid == 0) { PROF_ADD(13, 2, t_start); }
@@ -660,8 +671,14 @@ __global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 ? 1 : 2)) k_apply_s
 #pragma unroll
             for (int l = 0; l < D; ++l) acc[l] += cfl[f][l] * tv;
           }
+          if (PART == 1 && sin.z_add) {
+            const double* za = sin.z_add + (size_t)mac * D * n + idx;
 #pragma unroll
-          for (int l = 0; l < D; ++l) z[l * n + idx] = acc[l];
+            for (int l = 0; l < D; ++l) z[l * n + idx] = acc[l] + sin.z_sign * __ldg(za + l * n);
+          } else {
+#pragma unroll
+            for (int l = 0; l < D; ++l) z[l * n + idx] = acc[l];
+          }
         }
       }
       cbar();  // z complete; tg free for the W_vol results
@@ -698,7 +715,12 @@ __global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 ? 1 : 2)) k_apply_s
     if (PART == 1) {  // hand y1 and the face terms to the S^-1 stream / post kernels
       PROF_T(t_wb);
       double* y1g = Work<C>::y1(fac.work, mac);
-      for (int i = tid; i < n; i += NCONS) y1g[i] = y[i];
+      if (sin.y1_add) {
+        const double* ya = sin.y1_add + (size_t)mac * n;
+        for (int i = tid; i < n; i += NCONS) y1g[i] = y[i] + sin.y1_sign * __ldg(ya + i);
+      } else {
+        for (int i = tid; i < n; i += NCONS) y1g[i] = y[i];
+      }
       double* fc = Work<C>::fc(fac.work, g.n_mac, mac);
       if (tid < LTR) {
         fc[tid] = ftt[tid];
@@ -1149,7 +1171,7 @@ static size_t stream_smem(const mhdg_disc& g) {
 
 template <class C, int STAGES, int PART>
 static int launch_stream(const mhdg_disc& g, const mhdg_blocks& b, const mhdg_factors& f, const double* x,
-                         double* y_loc, cudaStream_t st) {
+                         double* y_loc, cudaStream_t st, StreamIn sin = StreamIn{nullptr, 0.0, nullptr, 0.0}) {
   const size_t bytes = stream_smem<C, STAGES, PART>(g);
   if (bytes > 227 * 1024) return MHDG_ERR_CONFIG;
   auto kern = k_apply_stream<C, STAGES, PART>;
@@ -1165,7 +1187,7 @@ static int launch_stream(const mhdg_disc& g, const mhdg_blocks& b, const mhdg_fa
   const int grid = g.n_mac < ctas ? g.n_mac : ctas;
   g_stream_grid = grid;
   const int pref = g_pref_ahead >= 0 ? g_pref_ahead : 4;
-  kern<<<grid, NCONS + 32, bytes, st>>>(g, b, f, x, y_loc, pref);
+  kern<<<grid, NCONS + 32, bytes, st>>>(g, b, f, x, y_loc, pref, sin);
   return launch_ok();
 }
 
@@ -1232,6 +1254,62 @@ extern "C" int mhdg_stream_profile(unsigned long long* out, int reset) {
   return 0;
 }
 #endif
+
+template <int D> int mass_solve_all(const mhdg_disc&, const double*, double*, cudaStream_t);
+template <int D> int recover_dq(const mhdg_disc&, const double*, const double*, const double*, long long, double*,
+                                double*, cudaStream_t);
+
+// Condensed rhs and recovery (condense.py:105-127) on the split apply's kernels:
+//   rhs:      zr = A_qq^-1 R_Q; pre with x = 0, z = -zr, y1 + R_U  -> t2 = S^-1 (R_U - A_uq zr)
+//             -> post: b_loc = A_hu t2 - A_hq A_qq^-1 A_qu t2 + A_hq zr;
+//   recover:  zr; pre with x = dtrace, z += zr, y1 - R_U -> du = S^-1 (A_uq zr - R_U + y1(dtrace))
+//             -> k_recover_dq: dq = -zr - A_qq^-1 A_qu du - A_qq^-1 A_qh dtrace.
+// zr lives in the factors' Schur scratch (dead after the factorization).
+template <class C>
+static int cond_stream_impl(const mhdg_disc& g, const mhdg_blocks& b, const mhdg_factors& f, bool rhs,
+                            const double* Rg, const double* Ru, const double* dtrace, double* y_loc, double* du,
+                            double* dq, cudaStream_t st) {
+  double* zr = f.scratch;
+  int rc = mass_solve_all<C::D>(g, Rg, zr, st);
+  if (rc) return rc;
+  const StreamIn sin = rhs ? StreamIn{zr, -1.0, Ru, 1.0} : StreamIn{zr, 1.0, Ru, -1.0};
+  tl_begin(TL_APPLY_PRE, st);
+  rc = launch_stream<C, stages_of<C>(1), 1>(g, b, f, rhs ? nullptr : dtrace, y_loc, st, sin);
+  tl_end(TL_APPLY_PRE, st);
+  if (rc) return rc;
+  tl_begin(TL_APPLY_SI, st);
+  rc = launch_lu_stream<C>(g, f, st);
+  tl_end(TL_APPLY_SI, st);
+  if (rc) return rc;
+  if (rhs) {
+    tl_begin(TL_APPLY_POST, st);
+    rc = launch_stream<C, stages_of<C>(2), 2>(g, b, f, nullptr, y_loc, st);
+    tl_end(TL_APPLY_POST, st);
+    return rc;
+  }
+  return recover_dq<C::D>(g, dtrace, zr, Work<C>::y2(f.work, g.n_mac, 0), (long long)Work<C>::PER, du, dq, st);
+}
+
+// -1 when no streamed instantiation matches or the scratch cannot hold zr (generic kernels)
+int cond_stream(const mhdg_disc& g, const mhdg_blocks& b, const mhdg_factors& f, bool rhs, const double* Rg,
+                const double* Ru, const double* dtrace, double* y_loc, double* du, double* dq, cudaStream_t st) {
+  if (f.kind != 1 || !f.work || !f.scratch || !g_split) return -1;
+  const long long n = (long long)g.L * g.ns;
+  const long long cap = (f.scratch_macros > 0 && f.scratch_macros < g.n_mac ? f.scratch_macros : g.n_mac) * n * n;
+  if (cap < (long long)g.n_mac * g.dim * n) return -1;
+#define MHDG_COND(D_, M_, P_) \
+  if (stream_ok<Cfg<D_, M_, P_>>(g, b, f)) return cond_stream_impl<Cfg<D_, M_, P_>>(g, b, f, rhs, Rg, Ru, dtrace, y_loc, du, dq, st);
+  MHDG_COND(2, 4, 3)
+  MHDG_COND(2, 2, 2)
+  MHDG_COND(3, 2, 2)
+  MHDG_COND(3, 1, 2)
+  MHDG_COND(3, 2, 1)
+  MHDG_COND(3, 1, 1)
+  MHDG_COND(3, 1, 3)
+  MHDG_COND(3, 4, 1)
+#undef MHDG_COND
+  return -1;
+}
 
 // returns -1 when no streamed instantiation matches (caller uses k_apply_local)
 int apply_stream(const mhdg_disc& g, const mhdg_blocks& b, const mhdg_factors& f, const double* x, double* y_loc,

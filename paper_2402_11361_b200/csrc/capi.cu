@@ -32,6 +32,8 @@ int vec_pass_api(long long n, int rows, const double* V, long long ldv, double* 
 long long icgs_scratch_size(int n);
 size_t gj_smem_bytes(int n);
 int apply_stream(const mhdg_disc&, const mhdg_blocks&, const mhdg_factors&, const double*, double*, cudaStream_t);
+int cond_stream(const mhdg_disc& g, const mhdg_blocks& b, const mhdg_factors& f, bool rhs, const double* Rg,
+                const double* Ru, const double* dtrace, double* y_loc, double* du, double* dq, cudaStream_t st);
 int halo_gather(long long n, const int* idx, const double* src, double* buf, cudaStream_t st);
 int halo_scatter(long long n, const int* idx, const double* buf, double* dst, int accumulate, cudaStream_t st);
 int face_reduce_remote(const mhdg_disc& g, const double* y_loc, const int* remote_src, const double* remote,
@@ -215,6 +217,12 @@ int mhdg_apply_trace(const mhdg_disc* g, const mhdg_blocks* b, const mhdg_factor
 
 int mhdg_condensed_rhs(const mhdg_disc* g, const mhdg_blocks* b, const mhdg_factors* f, const double* Rg,
                        const double* Ru, const double* Rt, double* bvec, double* b_loc, void* st) {
+  // the split apply's streamed kernels when an instantiation matches, else the generic kernel
+  if (g_stream_enabled) {
+    const int rs = cond_stream(*g, *b, *f, true, Rg, Ru, nullptr, b_loc, nullptr, nullptr, S(st));
+    if (rs > 0) return rs;
+    if (rs == 0) return face_reduce(*g, b_loc, Rt, -1.0, bvec, S(st));
+  }
   int rc = DISPATCH(g, rhs_local<2>(*g, *b, *f, Rg, Ru, b_loc, S(st)), rhs_local<3>(*g, *b, *f, Rg, Ru, b_loc, S(st)));
   if (rc) return rc;
   return face_reduce(*g, b_loc, Rt, -1.0, bvec, S(st));
@@ -222,6 +230,11 @@ int mhdg_condensed_rhs(const mhdg_disc* g, const mhdg_blocks* b, const mhdg_fact
 
 int mhdg_recover(const mhdg_disc* g, const mhdg_blocks* b, const mhdg_factors* f, const double* Rg,
                  const double* Ru, const double* dtr, double* du, double* dq, void* st) {
+  if (g_stream_enabled) {
+    // the streamed pre part writes its face terms into the work buffer only; y_loc is unused
+    const int rs = cond_stream(*g, *b, *f, false, Rg, Ru, dtr, nullptr, du, dq, S(st));
+    if (rs >= 0) return rs;
+  }
   return DISPATCH(g, recover<2>(*g, *b, *f, Rg, Ru, dtr, du, dq, S(st)),
                   recover<3>(*g, *b, *f, Rg, Ru, dtr, du, dq, S(st)));
 }

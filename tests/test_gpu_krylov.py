@@ -105,7 +105,7 @@ def test_vec_pass_modes_match_torch(n, rows):
     V = torch.randn(rows + 1, n, dtype=torch.float64, device="cuda", generator=g)
     w0 = torch.randn(n, dtype=torch.float64, device="cuda", generator=g)
     c = torch.randn(rows, dtype=torch.float64, device="cuda", generator=g)
-    out = torch.empty(64, dtype=torch.float64, device="cuda")
+    out = torch.zeros(64, dtype=torch.float64, device="cuda")
     Vr = V[:rows]
 
     def run(mode):
@@ -128,6 +128,7 @@ def test_vec_pass_modes_match_torch(n, rows):
     assert float((w - comb).abs().max()) <= tol(comb)
     w, o = run(4)
     assert abs(float(o[0]) - float(w0 @ w0)) <= 1e-12 * float(w0 @ w0)
-    for mode in range(5):  # deterministic
+    for mode in range(5):  # deterministic (the outputs each mode writes)
         a, b = run(mode), run(mode)
-        assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+        k = {0: rows, 1: rows, 2: 1, 3: 0, 4: 1}[mode]
+        assert torch.equal(a[0], b[0]) and torch.equal(a[1][:k], b[1][:k])
