@@ -980,6 +980,10 @@ __global__ void __launch_bounds__(NCT + 32) k_si_stream(int n_mac, const double*
 // each walks its macro's dependent block steps.
 // ---------------------------------------------------------------------------
 constexpr int LUW_NT = 128;
+#ifndef MHDG_LUW_CH
+#define MHDG_LUW_CH 8
+#endif
+constexpr int LUW_CH = MHDG_LUW_CH;  // triangle columns per prefetch chunk
 
 struct LuBlk {
   long long fwd_panel, fwd_diag, bwd_panel, bwd_diag;
@@ -1041,14 +1045,36 @@ __global__ void __launch_bounds__(LUW_NT) k_lu_warp(int n_mac, const double* __r
       double v0 = lane < o.nb ? yb[o.r0 + lane] - a0 : 0.0;
       double v1 = lane + 32 < o.nb ? yb[o.r0 + lane + 32] - a1 : 0.0;
       const double* Tl = Fm + o.fwd_diag;
-#pragma unroll 4
-      for (int c = 0; c < o.nb - 1; ++c) {  // column c of L_bb: rows c+1 .. nb-1
-        const double* col = Tl + plu_lo_col(o.nb, c) - c - 1;
-        const double l0 = (lane > c && lane < o.nb) ? __ldcs(col + lane) : 0.0;
-        const double l1 = (lane + 32 > c && lane + 32 < o.nb) ? __ldcs(col + lane + 32) : 0.0;
-        const double yc = __shfl_sync(MHDG_FULL, c < 32 ? v0 : v1, c & 31);
-        v0 -= l0 * yc;
-        v1 -= l1 * yc;
+      {  // columns in chunks of LUW_CH, the next chunk's loads in flight during this one's sweep
+        const int nc = o.nb - 1;
+        auto ld = [&](int c0, double (&l0)[LUW_CH], double (&l1)[LUW_CH]) {
+#pragma unroll
+          for (int k = 0; k < LUW_CH; ++k) {
+            const int c = c0 + k;
+            const double* col = Tl + plu_lo_col(o.nb, c) - c - 1;
+            l0[k] = (c < nc && lane > c && lane < o.nb) ? __ldcs(col + lane) : 0.0;
+            l1[k] = (c < nc && lane + 32 > c && lane + 32 < o.nb) ? __ldcs(col + lane + 32) : 0.0;
+          }
+        };
+        auto sweep = [&](int c0, const double (&l0)[LUW_CH], const double (&l1)[LUW_CH]) {
+#pragma unroll
+          for (int k = 0; k < LUW_CH; ++k) {  // column c of L_bb: rows c+1 .. nb-1
+            const int c = c0 + k;
+            if (c < nc) {
+              const double yc = __shfl_sync(MHDG_FULL, c < 32 ? v0 : v1, c & 31);
+              v0 -= l0[k] * yc;
+              v1 -= l1[k] * yc;
+            }
+          }
+        };
+        double pa0[LUW_CH], pa1[LUW_CH], pb0[LUW_CH], pb1[LUW_CH];
+        ld(0, pa0, pa1);
+        for (int c0 = 0; c0 < nc; c0 += 2 * LUW_CH) {
+          ld(c0 + LUW_CH, pb0, pb1);
+          sweep(c0, pa0, pa1);
+          ld(c0 + 2 * LUW_CH, pa0, pa1);
+          sweep(c0 + LUW_CH, pb0, pb1);
+        }
       }
       if (lane < o.nb) yb[o.r0 + lane] = v0;
       if (lane + 32 < o.nb) yb[o.r0 + lane + 32] = v1;
@@ -1061,16 +1087,37 @@ __global__ void __launch_bounds__(LUW_NT) k_lu_warp(int n_mac, const double* __r
       double v0 = lane < o.nb ? yb[o.r0 + lane] - a0 : 0.0;
       double v1 = lane + 32 < o.nb ? yb[o.r0 + lane + 32] - a1 : 0.0;
       const double* Tu = Fm + o.bwd_diag;
-#pragma unroll 4
-      for (int c = o.nb - 1; c >= 0; --c) {  // column c of U_bb: rows 0 .. c (diagonal: 1/U_cc)
-        const double* col = Tu + c * (c + 1) / 2;
-        const double u0 = lane <= c ? __ldcs(col + lane) : 0.0;
-        const double u1 = lane + 32 <= c ? __ldcs(col + lane + 32) : 0.0;
-        const double xc = __shfl_sync(MHDG_FULL, c < 32 ? v0 * u0 : v1 * u1, c & 31);
-        if (lane == c) v0 = xc;
-        else v0 -= u0 * xc;
-        if (lane + 32 == c) v1 = xc;
-        else v1 -= u1 * xc;
+      {  // columns nb-1 .. 0 in chunks, the next chunk's loads in flight
+        auto ld = [&](int c0, double (&u0)[LUW_CH], double (&u1)[LUW_CH]) {
+#pragma unroll
+          for (int k = 0; k < LUW_CH; ++k) {
+            const int c = c0 - k;
+            const double* col = Tu + (c >= 0 ? c * (c + 1) / 2 : 0);
+            u0[k] = (c >= 0 && lane <= c) ? __ldcs(col + lane) : 0.0;
+            u1[k] = (c >= 0 && lane + 32 <= c) ? __ldcs(col + lane + 32) : 0.0;
+          }
+        };
+        auto sweep = [&](int c0, const double (&u0)[LUW_CH], const double (&u1)[LUW_CH]) {
+#pragma unroll
+          for (int k = 0; k < LUW_CH; ++k) {  // column c of U_bb: rows 0 .. c (diagonal: 1/U_cc)
+            const int c = c0 - k;
+            if (c >= 0) {
+              const double xc = __shfl_sync(MHDG_FULL, c < 32 ? v0 * u0[k] : v1 * u1[k], c & 31);
+              if (lane == c) v0 = xc;
+              else v0 -= u0[k] * xc;
+              if (lane + 32 == c) v1 = xc;
+              else v1 -= u1[k] * xc;
+            }
+          }
+        };
+        double pa0[LUW_CH], pa1[LUW_CH], pb0[LUW_CH], pb1[LUW_CH];
+        ld(o.nb - 1, pa0, pa1);
+        for (int c0 = o.nb - 1; c0 >= 0; c0 -= 2 * LUW_CH) {
+          ld(c0 - LUW_CH, pb0, pb1);
+          sweep(c0, pa0, pa1);
+          ld(c0 - 2 * LUW_CH, pa0, pa1);
+          sweep(c0 - LUW_CH, pb0, pb1);
+        }
       }
       if (lane < o.nb) yb[o.r0 + lane] = v0;
       if (lane + 32 < o.nb) yb[o.r0 + lane + 32] = v1;
