@@ -15,6 +15,7 @@
 // (pointwise.cuh), so the stash stores are coalesced.  Every accumulation runs
 // in a fixed order (sub-element loop, inverse-incidence gathers): results are
 // bitwise reproducible run to run.
+#include "dmma.cuh"
 #include "local_ops.cuh"
 #include "pointwise.cuh"
 
@@ -29,6 +30,22 @@ namespace mhdg {
 template <int D>
 __host__ __device__ constexpr int asm_threads() { return D == 2 ? 256 : MHDG_ASM_THREADS_3D; }
 
+// The state_state contraction of a sub-element on the FP64 tensor cores (3D; the 2D loop
+// measured faster on the FP64 pipe): W1 is then stored as the K x N matrix
+// W1T[(q, u)][(a, s)] with row stride w1t_ld (= 4 mod 16: conflict-free DMMA fragments) and
+// the sub-element's (nloc NS)^2 block is summed in the shared-memory tile Csm.
+#ifndef MHDG_ASM_DMMA_2D
+#define MHDG_ASM_DMMA_2D 0
+#endif
+template <int D>
+__host__ __device__ constexpr bool asm_dmma() { return D == 3 || MHDG_ASM_DMMA_2D; }
+__host__ __device__ inline int w1t_ld(int nr) {
+  int ld = (nr + 3) & ~3;
+  while (ld % 16 != 4) ld += 4;
+  return ld;
+}
+__host__ __device__ inline int csm_ld(int nr) { return (nr + 3) & ~1; }
+
 // W1[q][a] blocks (NS x NS) are stored with stride NS*NS + 4 (2D: 20 doubles): the
 // SUPG product reads W1[q][b][u][t] across (b, t) lanes without bank conflicts
 template <int D>
@@ -36,7 +53,7 @@ __host__ __device__ constexpr int W1S() { return (D + 2) * (D + 2) + 4; }
 
 template <int D>
 struct AsmSmem {
-  int us, qs, uh, td, tf, gph, upt, qpt, wq, tq, prv, As, Adu, FG, Pp, sw, W1, cvol;
+  int us, qs, uh, td, tf, gph, upt, qpt, wq, tq, prv, As, Adu, FG, Pp, sw, W1, csm, cvol;
   int fuh, fu, fq, fuv, fw, fpr, fpv, fS, fK1, ffn, fbh, cf, ctr, total;
 };
 
@@ -67,7 +84,8 @@ __host__ __device__ inline AsmSmem<D> asm_smem(const Sz& s0, int nqc) {
   TAKE(FG, s.nq * NS * D)
   TAKE(Pp, s.nq * D * NS)
   TAKE(sw, s.nq * NS)
-  TAKE(W1, s.nq * s.nloc * W1S<D>())
+  TAKE(W1, asm_dmma<D>() ? s.nq * NS * w1t_ld(s.nloc * NS) : s.nq * s.nloc * W1S<D>())
+  TAKE(csm, asm_dmma<D>() ? s.nloc * NS * csm_ld(s.nloc * NS) : 0)
   TAKE(cvol, s.n_sub * s.nloc * NS)
   TAKE(fuh, s.nqf * NS)
   TAKE(fu, s.nqf * NS)
@@ -331,6 +349,107 @@ __global__ void __launch_bounds__(asm_threads<D>())
     }
     if (want_jac) {
       const int nw = nloc * NS * NS;
+      double* SSm = bk.state_state + (size_t)mac * n * n;
+      const int nr = nloc * NS;
+      if constexpr (asm_dmma<D>()) {
+        const int wld = w1t_ld(nr), cld = csm_ld(nr);
+        double* Csm = sm + o.csm;
+        for (int idx = tid; idx < nc * nw; idx += nt) {
+          const int s = idx % NS, a = (idx / NS) % nloc, uu = (idx / nr) % NS, qq = idx / nw;
+          double acc = 0.0;
+#pragma unroll
+          for (int k = 0; k < D; ++k) acc += As[((qq * D + k) * NS + uu) * NS + s] * gph[(qq * nloc + a) * D + k];
+          W1[(qq * NS + uu) * wld + a * NS + s] = acc;  // W1T[(q, u)][(a, s)]
+        }
+        __syncthreads();
+        // contrib[(a,s),(b,t)] = sum_{(q,u)} (w tau W1T[(q,u)][(a,s)]) W1T[(q,u)][(b,t)]        (GEMM 2)
+        //                      + sum_q Y[q][(a,s,t)] phi[q][b],                                 (GEMM 1)
+        //   Y = -w sum_k Adu[q,k,s,t] gphys[q,a,k] + dt_coeff w tau W1T[(q,t)][(a,s)]   (assembly.py:465-470)
+        const int warp = tid >> 5, lane = tid & 31, g8 = lane >> 2, t4 = lane & 3, nwarp = nt >> 5;
+        const int mtl = (nr + 7) / 8;
+        constexpr int NH = 4;  // n-tiles per unit of GEMM 2 (the A fragment is used NH times)
+        const int nun = mtl * ((mtl + NH - 1) / NH), K2 = nc * NS, ks2 = (K2 + 3) / 4;
+        for (int un = warp; un < nun; un += nwarp) {
+          const int mt = un % mtl, n0 = (un / mtl) * NH;
+          const int m = mt * 8 + g8;
+          const bool mok = m < nr;
+          int colB[NH];
+          bool nok[NH];
+#pragma unroll
+          for (int h = 0; h < NH; ++h) {
+            const int nn = (n0 + h) * 8 + g8;
+            nok[h] = nn < nr;
+            colB[h] = nok[h] ? nn : 0;
+          }
+          double c[NH][2];
+#pragma unroll
+          for (int h = 0; h < NH; ++h) c[h][0] = c[h][1] = 0.0;
+          for (int ks = 0; ks < ks2; ++ks) {
+            const int kk = 4 * ks + t4;
+            const bool kok = kk < K2;
+            const int qq = kok ? kk / NS : 0;
+            const double* wr = W1 + (kok ? kk : 0) * wld;
+            const double af = (mok && kok) ? wq[qq] * tq[qq] * wr[m] : 0.0;
+#pragma unroll
+            for (int h = 0; h < NH; ++h) {
+              const double bf = (kok && nok[h]) ? wr[colB[h]] : 0.0;
+              dmma_8x8x4(c[h][0], c[h][1], af, bf);
+            }
+          }
+#pragma unroll
+          for (int h = 0; h < NH; ++h)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int col = (n0 + h) * 8 + 2 * t4 + e;
+              if (mok && col < nr) Csm[m * cld + col] = c[h][e];
+            }
+        }
+        __syncthreads();
+        const int mt1 = (nw + 7) / 8, ks1 = (nc + 3) / 4;
+        constexpr int NB1 = 3;  // b-tiles: nloc <= 24
+        const int nb1 = (nloc + 7) / 8;
+        for (int un = warp; un < mt1; un += nwarp) {
+          const int m = un * 8 + g8;
+          const bool mok = m < nw;
+          const int a = mok ? m / (NS * NS) : 0, s = (m / NS) % NS, t = m % NS;
+          double c[NB1][2];
+#pragma unroll
+          for (int h = 0; h < NB1; ++h) c[h][0] = c[h][1] = 0.0;
+          for (int ks = 0; ks < ks1; ++ks) {
+            const int qq = 4 * ks + t4;
+            const bool kok = qq < nc;
+            double af = 0.0;
+            if (mok && kok) {
+              double y = 0.0;
+#pragma unroll
+              for (int k = 0; k < D; ++k) y += Adu[((qq * D + k) * NS + s) * NS + t] * gph[(qq * nloc + a) * D + k];
+              const double w = wq[qq];
+              y = -w * y;
+              if (stage.dt_coeff != 0.0) y += stage.dt_coeff * (w * tq[qq]) * W1[(qq * NS + t) * wld + a * NS + s];
+              af = y;
+            }
+#pragma unroll
+            for (int h = 0; h < NB1; ++h)
+              if (h < nb1) {
+                const int bb = h * 8 + g8;
+                const double bf = (kok && bb < nloc) ? __ldg(g.phi_vol + (q0 + qq) * nloc + bb) : 0.0;
+                dmma_8x8x4(c[h][0], c[h][1], af, bf);
+              }
+          }
+#pragma unroll
+          for (int h = 0; h < NB1; ++h)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int bb = h * 8 + 2 * t4 + e;
+              if (mok && h < nb1 && bb < nloc) Csm[(a * NS + s) * cld + bb * NS + t] += c[h][e];
+            }
+        }
+        __syncthreads();
+        for (int idx = tid; idx < nr * nr; idx += nt) {
+          const int cb = idx % nr, rb = idx / nr, t = cb % NS, b = cb / NS, s = rb % NS, a = rb / NS;
+          SSm[(size_t)(conn[a] * NS + s) * n + conn[b] * NS + t] += Csm[rb * cld + cb];
+        }
+      } else {
       for (int idx = tid; idx < nc * nw; idx += nt) {
         const int qq = idx / nw, e = idx % nw, s = e % NS, uu = (e / NS) % NS, a = e / (NS * NS);
         double acc = 0.0;
@@ -341,8 +460,6 @@ __global__ void __launch_bounds__(asm_threads<D>())
       __syncthreads();
       // contrib[a,s,b,t] = -sum w Adu[k,s,t] gphys[a,k] phi[b] + sum w tau W1[a,u,s] W1[b,u,t]
       //                    + dt_coeff sum w tau W1[a,t,s] phi[b]          (assembly.py:465-470)
-      double* SSm = bk.state_state + (size_t)mac * n * n;
-      const int nr = nloc * NS;
       for (int idx = tid; idx < nr * nr; idx += nt) {
         const int t = idx % NS, b = (idx / NS) % nloc, s = (idx / nr) % NS, a = idx / (nr * NS);
         double acc = 0.0;
@@ -360,6 +477,7 @@ __global__ void __launch_bounds__(asm_threads<D>())
           acc += y * g.phi_vol[(q0 + qq) * nloc + b] + wt * z;
         }
         SSm[(size_t)(conn[a] * NS + s) * n + conn[b] * NS + t] += acc;
+      }
       }
     }
     __syncthreads();

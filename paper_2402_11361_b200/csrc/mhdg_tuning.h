@@ -47,6 +47,10 @@ void mhdg_set_stream_enabled(int on);
    shared-memory ring only. */
 void mhdg_set_stream_prefetch(int pieces);
 
+/* Face-block preconditioner build: 0 (default) the register-tile Gauss-Jordan sweep for
+   face blocks up to 144 dofs; 1: the shared-memory Cholesky + triangular inverse. */
+void mhdg_set_precond_variant(int v);
+
 /* CTAs per launch of the last streamed pre/post kernel (diagnostics). */
 int mhdg_stream_grid(void);
 

@@ -12,6 +12,10 @@ namespace mhdg {
 
 constexpr int PRE_THREADS = 256;
 
+static int g_precond_variant = 0;
+extern "C" void mhdg_set_precond_variant(int v) { g_precond_variant = v; }
+static bool precond_shared_build() { return g_precond_variant == 1; }
+
 template <int D>
 __global__ void __launch_bounds__(PRE_THREADS) k_precond_build(mhdg_disc g, mhdg_blocks b, const double* __restrict__ extra,
                                                                double* inv, int* status, int x_global) {
@@ -113,6 +117,147 @@ __global__ void __launch_bounds__(PRE_THREADS) k_precond_build(mhdg_disc g, mhdg
   }
 }
 
+// k_precond_build_reg: the same face block inverted in registers.  The 16 x 16 threads of a
+// CTA hold B_f as T x T tiles each (entry (ti + 16 a, tj + 16 b)) and run an in-place
+// Gauss-Jordan sweep without pivoting (B_f is symmetric positive definite; the pivots are
+// the Cholesky pivots L_kk^2, so the positive-definiteness test is the same): step k
+// publishes row k and column k through a double-buffered shared-memory line (one barrier
+// per step), then every thread does T^2 FMAs on its registers.  One bs^2 shared-memory
+// block stages the coalesced loads into canonical order and the inverse for coalesced
+// stores.  bs <= 16 T.
+template <int D, int T>
+__global__ void __launch_bounds__(PRE_THREADS, T <= 5 ? 3 : 1)
+    k_precond_build_reg(mhdg_disc g, mhdg_blocks b, const double* __restrict__ extra, double* __restrict__ inv,
+                        int* status) {
+  constexpr int NS = D + 2, NF = D + 1, W = 16 * T;
+  const int f = blockIdx.x, bs = g.Lf * NS, tid = threadIdx.x, ti = tid >> 4, tj = tid & 15;
+  extern __shared__ double sm[];  // bs x ld staging block: B_f in canonical order, later the inverse
+  const int ld = bs | 1;          // odd row stride: the transposed reads are conflict-free
+  __shared__ __align__(16) double rowb[2][W], colb[2][W];
+  __shared__ int perm[W];
+  int m0 = g.face_macros[2 * f], m1 = g.face_macros[2 * f + 1];
+  int l0 = g.face_locals[2 * f], l1 = g.face_locals[2 * f + 1];
+  if (m1 >= 0 && (m1 * NF + l1) < (m0 * NF + l0)) {  // sides in flat (mac, lf) order, as np.add.at
+    int t = m0; m0 = m1; m1 = t;
+    t = l0; l0 = l1; l1 = t;
+  }
+  // coalesced reads of each side's block, scattered into canonical order in shared memory
+  bool first = true;
+  const float rbs = 1.0f / (float)bs;
+  for (int side = 0; side < 2; ++side) {
+    const int mac = side ? m1 : m0, lf = side ? l1 : l0;
+    if (mac < 0) continue;
+    const int* gat = g.gather + ((size_t)mac * NF + lf) * bs;
+    const double* As = b.face_trace_trace + ((size_t)mac * NF + lf) * bs * bs;
+    __syncthreads();  // the previous side's perm reads and block writes are done
+    for (int r = tid; r < bs; r += PRE_THREADS) perm[r] = __ldg(gat + r) - f * bs;
+    __syncthreads();
+    // the block read linearly, LB loads in flight per thread, then scattered
+    constexpr int LB = 12;
+    for (int e0 = tid; e0 < bs * bs; e0 += PRE_THREADS * LB) {
+      double v[LB];
+#pragma unroll
+      for (int u = 0; u < LB; ++u) {
+        const int idx = e0 + PRE_THREADS * u;
+        v[u] = idx < bs * bs ? __ldg(As + idx) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < LB; ++u) {
+        const int idx = e0 + PRE_THREADS * u;
+        if (idx < bs * bs) {
+          const int r = __float2int_rd(((float)idx + 0.5f) * rbs), c = idx - r * bs;  // exact: idx < 2^15
+          double* d = sm + perm[r] * ld + perm[c];
+          *d = first ? v[u] : *d + v[u];  // each (pr, pc) hit once per side: no race
+        }
+      }
+    }
+    first = false;
+  }
+  __syncthreads();
+  if (extra) {  // the face's other side, held by another rank, already in canonical order
+    const double* ex = extra + (size_t)f * bs * bs;
+    for (int r = tid >> 5; r < bs; r += PRE_THREADS / 32)
+      for (int c = tid & 31; c < bs; c += 32) sm[r * ld + c] += __ldg(ex + r * bs + c);
+    __syncthreads();
+  }
+  double A[T][T];
+#pragma unroll
+  for (int a = 0; a < T; ++a)
+#pragma unroll
+    for (int c = 0; c < T; ++c) {
+      const int i = ti + 16 * a, j = tj + 16 * c;
+      A[a][c] = (i < bs && j < bs) ? 0.5 * (sm[i * ld + j] + sm[j * ld + i]) : 0.0;
+    }
+  bool bad = false;
+#pragma unroll
+  for (int ka = 0; ka < T; ++ka) {
+    for (int kk = 0; kk < 16; ++kk) {
+      const int k = 16 * ka + kk;
+      if (k >= bs) break;
+      double* rb = rowb[k & 1];
+      double* cb = colb[k & 1];
+      if (ti == kk) {
+#pragma unroll
+        for (int c = 0; c < T; ++c) rb[tj + 16 * c] = A[ka][c];
+      }
+      if (tj == kk) {
+#pragma unroll
+        for (int a = 0; a < T; ++a) cb[ti + 16 * a] = A[a][ka];
+      }
+      __syncthreads();
+      const double p = rb[k];
+      if (!(p > 0.0)) {  // uniform over the CTA
+        bad = true;
+        break;
+      }
+      const double ip = 1.0 / p;
+      double cc[T], rr[T];
+#pragma unroll
+      for (int a = 0; a < T; ++a) {
+        cc[a] = -cb[ti + 16 * a] * ip;
+        rr[a] = rb[tj + 16 * a];
+      }
+      if (ti == kk) cc[ka] = ip;
+      if (tj == kk) rr[ka] = 1.0;
+#pragma unroll
+      for (int a = 0; a < T; ++a)
+#pragma unroll
+        for (int c = 0; c < T; ++c) {
+          double old = A[a][c];
+          if ((a == ka && ti == kk) || (c == ka && tj == kk)) old = 0.0;
+          A[a][c] = fma(cc[a], rr[c], old);
+        }
+    }
+    if (bad) break;
+  }
+  if (bad) {
+    if (tid == 0) set_status(status, MHDG_ERR_PRECONDITIONER, f, 0, 0.0);
+    return;
+  }
+  __syncthreads();  // every thread has taken its tile of B_f out of the staging block
+#pragma unroll
+  for (int a = 0; a < T; ++a)
+#pragma unroll
+    for (int c = 0; c < T; ++c) {
+      const int i = ti + 16 * a, j = tj + 16 * c;
+      if (i < bs && j < bs) sm[i * ld + j] = A[a][c];
+    }
+  __syncthreads();
+  double* out = inv + (size_t)f * bs * bs;
+  for (int r = tid >> 5; r < bs; r += PRE_THREADS / 32)
+    for (int c = tid & 31; c < bs; c += 32) out[r * bs + c] = sm[r * ld + c];
+}
+
+template <int D, int T>
+static void launch_build_reg(const mhdg_disc& g, const mhdg_blocks& b, const double* extra, double* inv, int* status,
+                             cudaStream_t st) {
+  const int bs = g.Lf * (D + 2);
+  const size_t bytes = sizeof(double) * bs * (bs | 1);
+  if (bytes > 48 * 1024)
+    cudaFuncSetAttribute(k_precond_build_reg<D, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  k_precond_build_reg<D, T><<<g.n_faces, PRE_THREADS, bytes, st>>>(g, b, extra, inv, status);
+}
+
 __global__ void __launch_bounds__(PRE_THREADS) k_precond_apply(int bs, const double* __restrict__ inv,
                                                                const double* __restrict__ v, double* __restrict__ y) {
   extern __shared__ double sm[];
@@ -155,6 +300,18 @@ template <int D>
 int precond_build(const mhdg_disc& g, const mhdg_blocks& b, const double* extra, double* inv, int* status,
                   cudaStream_t st) {
   const int bs = g.Lf * (D + 2);
+  if (bs <= 144 && !precond_shared_build()) {  // register-tile sweep (no bs^2 shared-memory block)
+    tl_begin(TL_PRECOND_BUILD, st);
+    if (bs <= 16) launch_build_reg<D, 1>(g, b, extra, inv, status, st);
+    else if (bs <= 32) launch_build_reg<D, 2>(g, b, extra, inv, status, st);
+    else if (bs <= 48) launch_build_reg<D, 3>(g, b, extra, inv, status, st);
+    else if (bs <= 64) launch_build_reg<D, 4>(g, b, extra, inv, status, st);
+    else if (bs <= 80) launch_build_reg<D, 5>(g, b, extra, inv, status, st);
+    else if (bs <= 112) launch_build_reg<D, 7>(g, b, extra, inv, status, st);
+    else launch_build_reg<D, 9>(g, b, extra, inv, status, st);
+    tl_end(TL_PRECOND_BUILD, st);
+    return launch_ok();
+  }
   size_t bytes = sizeof(double) * 2 * bs * bs;
   const int x_global = bytes > 227 * 1024;
   if (x_global) bytes /= 2;
