@@ -25,10 +25,17 @@ namespace mhdg {
 // SM in 3D): measured 2D 256 (512: 18.3 -> 32.2 ms at C2), 3D 768 (256: 224 ms, 384: 188,
 // 512: 170, 768: 159, 1024: 158 with 128 bytes of spills, at C3)
 #ifndef MHDG_ASM_THREADS_3D
-#define MHDG_ASM_THREADS_3D 768
+#define MHDG_ASM_THREADS_3D 384
+#endif
+#ifndef MHDG_ASM_CTAS_3D
+#define MHDG_ASM_CTAS_3D 2
 #endif
 template <int D>
 __host__ __device__ constexpr int asm_threads() { return D == 2 ? 256 : MHDG_ASM_THREADS_3D; }
+// 3D: CTAs per SM the shared-memory budget is cut for (the volume points go in chunks that
+// fit): the serial phases of one macro run under the parallel phases of another
+template <int D>
+__host__ __device__ constexpr int asm_ctas() { return D == 2 ? 1 : MHDG_ASM_CTAS_3D; }
 
 // The state_state contraction of a sub-element on the FP64 tensor cores (3D; the 2D loop
 // measured faster on the FP64 pipe): W1 is then stored as the K x N matrix
@@ -68,11 +75,17 @@ __host__ __device__ inline AsmSmem<D> asm_smem(const Sz& s0, int nqc) {
 #define TAKE(field, cnt) \
   m.field = o;           \
   o += (cnt);
+  // kept for the whole macro
   TAKE(us, s.n)
   TAKE(qs, D * s.n)
   TAKE(uh, s.ltr)
   TAKE(td, s.n)
   TAKE(tf, s.ltr)
+  TAKE(cvol, s.n_sub * s.nloc * NS)
+  TAKE(cf, NF * s.n_tri * s.nlocf * NS)
+  TAKE(ctr, NF * s.n_tri * s.nlocf * NS)
+  // volume work arrays (one chunk of points of one sub-element) ...
+  const int work = o;
   TAKE(gph, s.nq * s.nloc * D)
   TAKE(upt, s.nq * NS)
   TAKE(qpt, s.nq * D * NS)
@@ -86,7 +99,9 @@ __host__ __device__ inline AsmSmem<D> asm_smem(const Sz& s0, int nqc) {
   TAKE(sw, s.nq * NS)
   TAKE(W1, asm_dmma<D>() ? s.nq * NS * w1t_ld(s.nloc * NS) : s.nq * s.nloc * W1S<D>())
   TAKE(csm, asm_dmma<D>() ? s.nloc * NS * csm_ld(s.nloc * NS) : 0)
-  TAKE(cvol, s.n_sub * s.nloc * NS)
+  const int vol_end = o;
+  // ... share their memory with the face work arrays (one sub-face)
+  o = work;
   TAKE(fuh, s.nqf * NS)
   TAKE(fu, s.nqf * NS)
   TAKE(fq, s.nqf * D * NS)
@@ -98,8 +113,7 @@ __host__ __device__ inline AsmSmem<D> asm_smem(const Sz& s0, int nqc) {
   TAKE(fK1, s.nqf * NS * NS)
   TAKE(ffn, s.nqf * NS)
   TAKE(fbh, s.nqf * NS)
-  TAKE(cf, NF * s.n_tri * s.nlocf * NS)
-  TAKE(ctr, NF * s.n_tri * s.nlocf * NS)
+  if (o < vol_end) o = vol_end;
 #undef TAKE
   m.total = o;
   return m;
@@ -133,7 +147,7 @@ __device__ __forceinline__ void interp_point(const double* ph, int nb, const int
 }
 
 template <int D>
-__global__ void __launch_bounds__(asm_threads<D>())
+__global__ void __launch_bounds__(asm_threads<D>(), asm_ctas<D>())
     k_assemble(mhdg_disc g, mhdg_flow flow, mhdg_stage stage, const double* __restrict__ u,
                const double* __restrict__ q, const double* __restrict__ uhat, double* __restrict__ R_grad,
                double* __restrict__ R_state, double* __restrict__ R_tl, int want_jac, mhdg_blocks bk,
@@ -401,7 +415,7 @@ __global__ void __launch_bounds__(asm_threads<D>())
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
               const int col = (n0 + h) * 8 + 2 * t4 + e;
-              if (mok && col < nr) Csm[m * cld + col] = c[h][e];
+              if (mok && col < nr) Csm[m * cld + col] = q0 == 0 ? c[h][e] : Csm[m * cld + col] + c[h][e];
             }
         }
         __syncthreads();
@@ -444,10 +458,12 @@ __global__ void __launch_bounds__(asm_threads<D>())
               if (mok && h < nb1 && bb < nloc) Csm[(a * NS + s) * cld + bb * NS + t] += c[h][e];
             }
         }
-        __syncthreads();
-        for (int idx = tid; idx < nr * nr; idx += nt) {
-          const int cb = idx % nr, rb = idx / nr, t = cb % NS, b = cb / NS, s = rb % NS, a = rb / NS;
-          SSm[(size_t)(conn[a] * NS + s) * n + conn[b] * NS + t] += Csm[rb * cld + cb];
+        if (q0 + nqc >= nq) {  // the sub-element's block is complete (summed over the point chunks in Csm)
+          __syncthreads();
+          for (int idx = tid; idx < nr * nr; idx += nt) {
+            const int cb = idx % nr, rb = idx / nr, t = cb % NS, b = cb / NS, s = rb % NS, a = rb / NS;
+            SSm[(size_t)(conn[a] * NS + s) * n + conn[b] * NS + t] += Csm[rb * cld + cb];
+          }
         }
       } else {
       for (int idx = tid; idx < nc * nw; idx += nt) {
@@ -662,7 +678,13 @@ int assemble(const mhdg_disc& g, const mhdg_flow& fl, const mhdg_stage& sg, cons
              const mhdg_frozen* fo, const mhdg_frozen* fi, int* status, cudaStream_t st) {
   const Sz sz = make_sz<D>(g);
   int nqc = sz.nq;  // largest point chunk whose work arrays fit shared memory
-  while (nqc > 1 && sizeof(double) * asm_smem<D>(sz, nqc).total > 227 * 1024) nqc = (nqc + 1) / 2;
+  // budget per CTA: 227 KB, or the SM's 228 KB (1 KB reserved per CTA) over asm_ctas CTAs
+  const size_t budget = asm_ctas<D>() > 1 ? (228 * 1024) / asm_ctas<D>() - 1024 : 227 * 1024;
+  while (nqc > 1 && sizeof(double) * asm_smem<D>(sz, nqc).total > budget) nqc = (nqc + 1) / 2;
+  if (sizeof(double) * asm_smem<D>(sz, nqc).total > budget) {  // no chunk fits the shared budget: one CTA per SM
+    nqc = sz.nq;
+    while (nqc > 1 && sizeof(double) * asm_smem<D>(sz, nqc).total > 227 * 1024) nqc = (nqc + 1) / 2;
+  }
   const size_t bytes = sizeof(double) * asm_smem<D>(sz, nqc).total;
   if (bytes > 227 * 1024) return MHDG_ERR_CONFIG;
   if (bytes > 48 * 1024) cudaFuncSetAttribute(k_assemble<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
