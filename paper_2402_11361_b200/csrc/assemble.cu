@@ -36,6 +36,10 @@ __host__ __device__ constexpr int asm_threads() { return D == 2 ? 256 : MHDG_ASM
 // fit): the serial phases of one macro run under the parallel phases of another
 template <int D>
 __host__ __device__ constexpr int asm_ctas() { return D == 2 ? 1 : MHDG_ASM_CTAS_3D; }
+// register budget (CTAs per SM in __launch_bounds__): the 2D work arrays are small enough
+// for three CTAs per SM (C2: 64 KB each)
+template <int D>
+__host__ __device__ constexpr int asm_min_ctas() { return D == 2 ? 3 : MHDG_ASM_CTAS_3D; }
 
 // The state_state contraction of a sub-element on the FP64 tensor cores (3D; the 2D loop
 // measured faster on the FP64 pipe): W1 is then stored as the K x N matrix
@@ -58,6 +62,8 @@ __host__ __device__ inline int csm_ld(int nr) { return (nr + 3) & ~1; }
 template <int D>
 __host__ __device__ constexpr int W1S() { return (D + 2) * (D + 2) + 4; }
 
+constexpr int ASM_MAXFLOC = 1024;  // n_tri x Lf entries of the sub-face node table
+
 template <int D>
 struct AsmSmem {
   int us, qs, uh, td, tf, gph, upt, qpt, wq, tq, prv, As, Adu, FG, Pp, sw, W1, csm, cvol;
@@ -65,7 +71,7 @@ struct AsmSmem {
 };
 
 template <int D>
-__host__ __device__ inline AsmSmem<D> asm_smem(const Sz& s0, int nqc) {
+__host__ __device__ inline AsmSmem<D> asm_smem(const Sz& s0, int nqc, int nfg) {
   Sz s = s0;
   s.nq = nqc;  // the volume per-point work arrays hold one chunk of points
   constexpr int NS = D + 2, NF = D + 1;
@@ -100,8 +106,10 @@ __host__ __device__ inline AsmSmem<D> asm_smem(const Sz& s0, int nqc) {
   TAKE(W1, asm_dmma<D>() ? s.nq * NS * w1t_ld(s.nloc * NS) : s.nq * s.nloc * W1S<D>())
   TAKE(csm, asm_dmma<D>() ? s.nloc * NS * csm_ld(s.nloc * NS) : 0)
   const int vol_end = o;
-  // ... share their memory with the face work arrays (one sub-face)
+  // ... share their memory with the face work arrays (all sub-faces of nfg faces)
   o = work;
+  const int nqf_one = s.nqf;
+  s.nqf = nfg * s.n_tri * nqf_one;
   TAKE(fuh, s.nqf * NS)
   TAKE(fu, s.nqf * NS)
   TAKE(fq, s.nqf * D * NS)
@@ -114,6 +122,7 @@ __host__ __device__ inline AsmSmem<D> asm_smem(const Sz& s0, int nqc) {
   TAKE(ffn, s.nqf * NS)
   TAKE(fbh, s.nqf * NS)
   if (o < vol_end) o = vol_end;
+  s.nqf = nqf_one;
 #undef TAKE
   m.total = o;
   return m;
@@ -147,15 +156,15 @@ __device__ __forceinline__ void interp_point(const double* ph, int nb, const int
 }
 
 template <int D>
-__global__ void __launch_bounds__(asm_threads<D>(), asm_ctas<D>())
+__global__ void __launch_bounds__(asm_threads<D>(), asm_min_ctas<D>())
     k_assemble(mhdg_disc g, mhdg_flow flow, mhdg_stage stage, const double* __restrict__ u,
                const double* __restrict__ q, const double* __restrict__ uhat, double* __restrict__ R_grad,
                double* __restrict__ R_state, double* __restrict__ R_tl, int want_jac, mhdg_blocks bk,
-               mhdg_frozen fo, mhdg_frozen fi, int use_frozen, int* status, int nqc) {
+               mhdg_frozen fo, mhdg_frozen fi, int use_frozen, int* status, int nqc, int nfg) {
   extern __shared__ double sm[];
   constexpr int NS = D + 2, NF = D + 1, E = D + 1;
   const Sz sz = make_sz<D>(g);
-  const AsmSmem<D> o = asm_smem<D>(sz, nqc);
+  const AsmSmem<D> o = asm_smem<D>(sz, nqc, nfg);
   const FlowC fl = make_flow<D>(flow);
   const int mac = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
   const int n = sz.n, L = sz.L, Lf = sz.Lf, nq = sz.nq, nloc = sz.nloc, nqf = sz.nqf, nlocf = sz.nlocf;
@@ -170,6 +179,15 @@ __global__ void __launch_bounds__(asm_threads<D>(), asm_ctas<D>())
   double *As = sm + o.As, *Adu = sm + o.Adu, *FG = sm + o.FG, *Pp = sm + o.Pp, *sw = sm + o.sw;
   double *W1 = sm + o.W1, *cvol = sm + o.cvol;
 
+  // face lattice node -> local node of sub-face T (or -1)
+  __shared__ short floc[ASM_MAXFLOC];
+  for (int i = tid; i < sz.n_tri * Lf; i += nt) {
+    const int T = i / Lf, gg = i - T * Lf;
+    short a = -1;
+    for (int k = 0; k < nlocf; ++k)
+      if (g.tri_conn[T * nlocf + k] == gg) a = (short)k;
+    floc[i] = a;
+  }
   // ---- load state ---------------------------------------------------------
   for (int i = tid; i < n; i += nt) us[i] = u[(size_t)mac * n + i];
   for (int i = tid; i < D * n; i += nt) qs[i] = q[(size_t)mac * D * n + i];
@@ -231,12 +249,6 @@ __global__ void __launch_bounds__(asm_threads<D>(), asm_ctas<D>())
           row[c] = (s == t && coeff != 0.0) ? coeff * det * g.mass[I * L + J] : 0.0;
         }
       }
-    }
-    const size_t fb = (size_t)NF * sz.bs * sz.bs;
-    for (size_t i = tid; i < fb; i += nt) {
-      bk.face_state_trace[(size_t)mac * fb + i] = 0.0;
-      bk.face_trace_state[(size_t)mac * fb + i] = 0.0;
-      bk.face_trace_trace[(size_t)mac * fb + i] = 0.0;
     }
     if (tid < NF) bk.trace_face_scale[mac * NF + tid] = g.bc_kind[mac * NF + tid] > 0 ? 0.0 : 1.0;
   }
@@ -501,125 +513,166 @@ __global__ void __launch_bounds__(asm_threads<D>(), asm_ctas<D>())
   }
 
   // ---- face terms (assembly.py:477-612) -----------------------------------
+  // All sub-faces of a group of nfg faces go through the per-point phases together (point
+  // p = ((f - f0) n_tri + T) nqf + qq); the face blocks are then formed entry by entry, each
+  // entry summing its sub-faces in order (T ascending, as the reference accumulates) and
+  // written once -- no zero fill and no read-modify-write of the three face blocks.
   double *fuh = sm + o.fuh, *fu = sm + o.fu, *fq = sm + o.fq, *fuv = sm + o.fuv, *fw = sm + o.fw;
   Prim<D>* fpr = (Prim<D>*)(sm + o.fpr);
   Prim<D>* fpv = (Prim<D>*)(sm + o.fpv);
   double *fS = sm + o.fS, *fK1 = sm + o.fK1, *ffn = sm + o.ffn, *fbh = sm + o.fbh, *cf = sm + o.cf,
          *ctr = sm + o.ctr;
   const int nqt = sz.n_tri * nqf;
-  for (int f = 0; f < NF; ++f) {
-    const int kind = g.bc_kind[mac * NF + f];
-    const double* nv = g.normals + (mac * NF + f) * D;
-    const int* fvn = g.face_vol_nodes + f * Lf;
-    const double e_w = g.wall_e[mac * NF + f];
-    const double* u_w = g.wall_u + (mac * NF + f) * D;
-    double uw2 = 0.0;
-#pragma unroll
-    for (int i = 0; i < D; ++i) uw2 += u_w[i] * u_w[i];
-    const double e_tot = e_w + 0.5 * uw2;
-    for (int T = 0; T < sz.n_tri; ++T) {
+  constexpr int NC = (2 + D) * NS;  // interpolated components per face point: uhat, u, q
+  for (int f0 = 0; f0 < NF; f0 += nfg) {
+    const int nfa = min(nfg, NF - f0), npt = nfa * nqt;
+    // interpolation to the face points, one component per thread
+    for (int idx = tid; idx < npt * NC; idx += nt) {
+      const int comp = idx % NC, pp = idx / NC, qq = pp % nqf, T = (pp / nqf) % sz.n_tri, f = f0 + pp / nqt;
+      const double* ph = g.phi_face + qq * nlocf;
       const int* tc = g.tri_conn + T * nlocf;
-      const size_t pbase = ((size_t)mac * NF + f) * nqt + T * nqf;  // face point index (frozen / stash)
-      for (int qq = tid; qq < nqf; qq += nt) {
-        double a_uh[NS], a_u[NS], a_q[D * NS];
-        const double* ph = g.phi_face + qq * nlocf;
-        interp_point<D>(ph, nlocf, tc, nullptr, uh + f * Lf * NS, 0, qs, L, a_uh, nullptr);
-        interp_point<D>(ph, nlocf, tc, fvn, us, 0, qs, L, a_u, a_q);
-        const int bad = admissible_code<D>(a_uh, fl.gamma);
-        if (bad) set_status(status, MHDG_ERR_ADMISSIBILITY, mac, bad - 1, a_uh[0]);
-#pragma unroll
-        for (int s = 0; s < NS; ++s) {
-          fuh[qq * NS + s] = a_uh[s];
-          fu[qq * NS + s] = a_u[s];
-          fuv[qq * NS + s] = use_frozen ? fi.face_visc_state[(pbase + qq) * NS + s] : a_uh[s];
-          if (want_jac) fo.face_visc_state[(pbase + qq) * NS + s] = a_uh[s];
-        }
-#pragma unroll
-        for (int s = 0; s < D * NS; ++s) fq[qq * D * NS + s] = a_q[s];
-        fpr[qq] = prim<D>(a_uh, fl);
-        fpv[qq] = prim<D>(fuv + qq * NS, fl);
-        fw[qq] = g.w_face_ref[T * nqf + qq] * (g.face_fac * g.areas[mac * NF + f]);
+      double acc = 0.0;
+      if (comp < NS) {
+        const double* src = uh + f * Lf * NS + comp;
+        for (int a = 0; a < nlocf; ++a) acc += ph[a] * src[tc[a] * NS];
+        fuh[pp * NS + comp] = acc;
+      } else {
+        const int* fvn = g.face_vol_nodes + f * Lf;
+        const int c2 = comp - NS;
+        const double* src = c2 < NS ? us + c2 : qs + (size_t)((c2 - NS) / NS) * n + (c2 - NS) % NS;
+        for (int a = 0; a < nlocf; ++a) acc += ph[a] * src[fvn[tc[a]] * NS];
+        if (c2 < NS) fu[pp * NS + c2] = acc;
+        else fq[pp * D * NS + (c2 - NS)] = acc;
       }
-      __syncthreads();
-      for (int idx = tid; idx < nqf * NS * NS; idx += nt) {
-        const int qq = idx / (NS * NS), s = (idx / NS) % NS, t = idx % NS;
-        const double S = use_frozen ? fi.face_stab[(pbase + qq) * NS * NS + s * NS + t]
-                                    : ((s == t) ? stab_diag<D>(fpr[qq], fl, nv, s) : 0.0);
-        fS[idx] = S;
-        if (want_jac) {
-          fo.face_stab[(pbase + qq) * NS * NS + s * NS + t] = S;
-          double an = 0.0;
+    }
+    __syncthreads();
+    for (int pp = tid; pp < npt; pp += nt) {
+      const int qq = pp % nqf, T = (pp / nqf) % sz.n_tri, f = f0 + pp / nqt;
+      const size_t pg = ((size_t)mac * NF + f) * nqt + T * nqf + qq;  // face point index (frozen / stash)
+      double a_uh[NS];
 #pragma unroll
-          for (int k = 0; k < D; ++k) an += euler_jac<D>(fpr[qq], fl, k, s, t) * nv[k];
-          fK1[idx] = an - S;  // d(flux.n)/d uhat, viscous uhat-dependence dropped
-        }
+      for (int s = 0; s < NS; ++s) a_uh[s] = fuh[pp * NS + s];
+      const int bad = admissible_code<D>(a_uh, fl.gamma);
+      if (bad) set_status(status, MHDG_ERR_ADMISSIBILITY, mac, bad - 1, a_uh[0]);
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        fuv[pp * NS + s] = use_frozen ? fi.face_visc_state[pg * NS + s] : a_uh[s];
+        if (want_jac) fo.face_visc_state[pg * NS + s] = a_uh[s];
       }
+      fpr[pp] = prim<D>(a_uh, fl);
+      fpv[pp] = use_frozen ? prim<D>(fuv + pp * NS, fl) : fpr[pp];
+      fw[pp] = g.w_face_ref[T * nqf + qq] * (g.face_fac * g.areas[mac * NF + f]);
+    }
+    __syncthreads();
+    for (int idx = tid; idx < npt * NS * NS; idx += nt) {
+      const int pp = idx / (NS * NS), s = (idx / NS) % NS, t = idx % NS, f = f0 + pp / nqt;
+      const size_t pg = ((size_t)mac * NF + f) * nqt + pp % nqt;
+      const double* nv = g.normals + (mac * NF + f) * D;
+      const double S = use_frozen ? fi.face_stab[pg * NS * NS + s * NS + t]
+                                  : ((s == t) ? stab_diag<D>(fpr[pp], fl, nv, s) : 0.0);
+      fS[idx] = S;
       if (want_jac) {
-        const int nW = D * NS * NS;
-        double* Wf = bk.wdgdq_face + pbase * nW;
-        for (int idx = tid; idx < nqf * nW; idx += nt) {
-          const int qq = idx / nW, e = idx % nW, t = e % NS, s = (e / NS) % NS, l = e / (NS * NS);
-          double acc = 0.0;
+        fo.face_stab[pg * NS * NS + s * NS + t] = S;
+        double an = 0.0;
 #pragma unroll
-          for (int k = 0; k < D; ++k) acc += visc_dgdq<D>(fpv[qq], fl, k, l, s, t) * nv[k];
-          Wf[idx] = fw[qq] * acc;
-        }
+        for (int k = 0; k < D; ++k) an += euler_jac<D>(fpr[pp], fl, k, s, t) * nv[k];
+        fK1[idx] = an - S;  // d(flux.n)/d uhat, viscous uhat-dependence dropped
       }
-      __syncthreads();
-      for (int idx = tid; idx < nqf * NS; idx += nt) {
-        const int qq = idx / NS, s = idx % NS;
-        double fn = 0.0;
+    }
+    if (want_jac) {
+      const int nW = D * NS * NS;
+      double* Wf = bk.wdgdq_face + (((size_t)mac * NF + f0) * nqt) * nW;  // the group's points are contiguous
+      for (int idx = tid; idx < npt * nW; idx += nt) {
+        const int pp = idx / nW, e = idx % nW, t = e % NS, s = (e / NS) % NS, l = e / (NS * NS), f = f0 + pp / nqt;
+        const double* nv = g.normals + (mac * NF + f) * D;
+        double acc = 0.0;
 #pragma unroll
-        for (int k = 0; k < D; ++k)
-          fn += (euler_flux<D>(fpr[qq], fuh + qq * NS, s, k) + visc_flux<D>(fpv[qq], fl, fq + qq * D * NS, s, k)) *
-                nv[k];
-        double sa = 0.0;
+        for (int k = 0; k < D; ++k) acc += visc_dgdq<D>(fpv[pp], fl, k, l, s, t) * nv[k];
+        Wf[idx] = fw[pp] * acc;
+      }
+    }
+    __syncthreads();
+    for (int idx = tid; idx < npt * NS; idx += nt) {
+      const int pp = idx / NS, s = idx % NS, f = f0 + pp / nqt;
+      const int kind = g.bc_kind[mac * NF + f];
+      const double* nv = g.normals + (mac * NF + f) * D;
+      double fn = 0.0;
 #pragma unroll
-        for (int t = 0; t < NS; ++t) sa += fS[(qq * NS + s) * NS + t] * (fu[qq * NS + t] - fuh[qq * NS + t]);
-        ffn[idx] = fn + sa;
-        if (kind == 1) {  // Dirichlet: uhat - u_D
-          fbh[idx] = fuh[idx] - g.u_dir[(pbase + qq) * NS + s];
-        } else if (kind == 2) {  // isothermal wall (moving with u_w)
-          const double rh = fuh[qq * NS];
-          double v;
-          if (s == 0) v = rh - fu[qq * NS];
-          else if (s <= D) v = fuh[idx] - rh * u_w[s - 1];
-          else v = fuh[qq * NS + E] - rh * e_tot;
-          fbh[idx] = v;
-        } else if (kind == 3) {  // adiabatic no-slip wall: rho_hat - rho, m_hat, E_hat - E
-          fbh[idx] = (s == 0 || s == E) ? fuh[idx] - fu[idx] : fuh[idx];
-        }
+      for (int k = 0; k < D; ++k)
+        fn += (euler_flux<D>(fpr[pp], fuh + pp * NS, s, k) + visc_flux<D>(fpv[pp], fl, fq + pp * D * NS, s, k)) *
+              nv[k];
+      double sa = 0.0;
+#pragma unroll
+      for (int t = 0; t < NS; ++t) sa += fS[(pp * NS + s) * NS + t] * (fu[pp * NS + t] - fuh[pp * NS + t]);
+      ffn[idx] = fn + sa;
+      if (kind == 1) {  // Dirichlet: uhat - u_D
+        const size_t pg = ((size_t)mac * NF + f) * nqt + pp % nqt;
+        fbh[idx] = fuh[idx] - g.u_dir[pg * NS + s];
+      } else if (kind == 2) {  // isothermal wall (moving with u_w)
+        const double* u_w = g.wall_u + (mac * NF + f) * D;
+        double uw2 = 0.0;
+#pragma unroll
+        for (int i = 0; i < D; ++i) uw2 += u_w[i] * u_w[i];
+        const double e_tot = g.wall_e[mac * NF + f] + 0.5 * uw2;
+        const double rh = fuh[pp * NS];
+        double v;
+        if (s == 0) v = rh - fu[pp * NS];
+        else if (s <= D) v = fuh[idx] - rh * u_w[s - 1];
+        else v = fuh[pp * NS + E] - rh * e_tot;
+        fbh[idx] = v;
+      } else if (kind == 3) {  // adiabatic no-slip wall: rho_hat - rho, m_hat, E_hat - E
+        fbh[idx] = (s == 0 || s == E) ? fuh[idx] - fu[idx] : fuh[idx];
       }
-      __syncthreads();
-      // projections onto the face sub-element's nodes
-      for (int idx = tid; idx < nlocf * NS; idx += nt) {
-        const int s = idx % NS, a = idx / NS;
-        double acc = 0.0, accb = 0.0;
-        for (int qq = 0; qq < nqf; ++qq) {
-          const double wp = fw[qq] * g.phi_face[qq * nlocf + a];
-          acc += wp * ffn[qq * NS + s];
-          if (kind > 0) accb += wp * fbh[qq * NS + s];
-        }
-        const int slot = ((f * sz.n_tri + T) * nlocf + a) * NS + s;
-        cf[slot] = acc;
-        ctr[slot] = kind > 0 ? accb : -acc;
+    }
+    __syncthreads();
+    // projections onto the face sub-elements' nodes
+    for (int idx = tid; idx < nfa * sz.n_tri * nlocf * NS; idx += nt) {
+      const int s = idx % NS, a = (idx / NS) % nlocf, T = (idx / (NS * nlocf)) % sz.n_tri,
+                fl_ = idx / (NS * nlocf * sz.n_tri), f = f0 + fl_;
+      const int kind = g.bc_kind[mac * NF + f];
+      const int p0 = (fl_ * sz.n_tri + T) * nqf;
+      double acc = 0.0, accb = 0.0;
+      for (int qq = 0; qq < nqf; ++qq) {
+        const double wp = fw[p0 + qq] * g.phi_face[qq * nlocf + a];
+        acc += wp * ffn[(p0 + qq) * NS + s];
+        if (kind > 0) accb += wp * fbh[(p0 + qq) * NS + s];
       }
-      if (want_jac) {
-        const int nr = nlocf * NS;
-        double* SSm = bk.state_state + (size_t)mac * n * n;
+      const int slot = ((f * sz.n_tri + T) * nlocf + a) * NS + s;
+      cf[slot] = acc;
+      ctr[slot] = kind > 0 ? accb : -acc;
+    }
+    if (want_jac) {
+      double* SSm = bk.state_state + (size_t)mac * n * n;
+      for (int fl_ = 0; fl_ < nfa; ++fl_) {  // faces in turn: they share state_state entries on their common edges
+        const int f = f0 + fl_;
+        const int kind = g.bc_kind[mac * NF + f];
+        const int* fvn = g.face_vol_nodes + f * Lf;
+        const double* u_w = g.wall_u + (mac * NF + f) * D;
+        double uw2 = 0.0;
+#pragma unroll
+        for (int i = 0; i < D; ++i) uw2 += u_w[i] * u_w[i];
+        const double e_tot = g.wall_e[mac * NF + f] + 0.5 * uw2;
         const size_t fboff = ((size_t)mac * NF + f) * sz.bs * sz.bs;
-        for (int idx = tid; idx < nr * nr; idx += nt) {
-          const int t = idx % NS, b = (idx / NS) % nlocf, s = (idx / nr) % NS, a = idx / (nr * NS);
+        for (int idx = tid; idx < sz.bs * sz.bs; idx += nt) {
+          const int cl = idx % sz.bs, rl = idx / sz.bs, t = cl % NS, gc = cl / NS, s = rl % NS, gr = rl / NS;
           double ust = 0.0, uss = 0.0, pr = 0.0;
-          for (int qq = 0; qq < nqf; ++qq) {
-            const double p = fw[qq] * g.phi_face[qq * nlocf + a] * g.phi_face[qq * nlocf + b];
-            ust += p * fK1[(qq * NS + s) * NS + t];
-            uss += p * fS[(qq * NS + s) * NS + t];
-            pr += p;
+          bool any = false;
+          for (int T = 0; T < sz.n_tri; ++T) {
+            const int a = floc[T * Lf + gr], b = floc[T * Lf + gc];
+            if (a < 0 || b < 0) continue;
+            any = true;
+            const int p0 = (fl_ * sz.n_tri + T) * nqf;
+            double ust_T = 0.0, uss_T = 0.0, pr_T = 0.0;
+            for (int qq = 0; qq < nqf; ++qq) {
+              const double pq = fw[p0 + qq] * g.phi_face[qq * nlocf + a] * g.phi_face[qq * nlocf + b];
+              ust_T += pq * fK1[((p0 + qq) * NS + s) * NS + t];
+              uss_T += pq * fS[((p0 + qq) * NS + s) * NS + t];
+              pr_T += pq;
+            }
+            ust += ust_T;
+            uss += uss_T;
+            pr += pr_T;
           }
-          const int rl = tc[a] * NS + s, cl = tc[b] * NS + t;
-          bk.face_state_trace[fboff + (size_t)rl * sz.bs + cl] += ust;
-          SSm[(size_t)(fvn[tc[a]] * NS + s) * n + fvn[tc[b]] * NS + t] += uss;
           double tst, ttt;
           if (kind == 0) {
             tst = -uss;
@@ -637,12 +690,15 @@ __global__ void __launch_bounds__(asm_threads<D>(), asm_ctas<D>())
             tst = pr * kuu;
             ttt = pr * khh;
           }
-          bk.face_trace_state[fboff + (size_t)rl * sz.bs + cl] += tst;
-          bk.face_trace_trace[fboff + (size_t)rl * sz.bs + cl] += ttt;
+          bk.face_state_trace[fboff + idx] = ust;
+          bk.face_trace_state[fboff + idx] = tst;
+          bk.face_trace_trace[fboff + idx] = ttt;
+          if (any) SSm[(size_t)(fvn[gr] * NS + s) * n + fvn[gc] * NS + t] += uss;
         }
+        __syncthreads();
       }
-      __syncthreads();
     }
+    __syncthreads();
   }
 
   // ---- R_U and the local trace residual ------------------------------------
@@ -677,16 +733,19 @@ int assemble(const mhdg_disc& g, const mhdg_flow& fl, const mhdg_stage& sg, cons
              const double* uhat, double* Rg, double* Ru, double* Rtl, double* Rt, int want_jac, const mhdg_blocks* b,
              const mhdg_frozen* fo, const mhdg_frozen* fi, int* status, cudaStream_t st) {
   const Sz sz = make_sz<D>(g);
-  int nqc = sz.nq;  // largest point chunk whose work arrays fit shared memory
   // budget per CTA: 227 KB, or the SM's 228 KB (1 KB reserved per CTA) over asm_ctas CTAs
-  const size_t budget = asm_ctas<D>() > 1 ? (228 * 1024) / asm_ctas<D>() - 1024 : 227 * 1024;
-  while (nqc > 1 && sizeof(double) * asm_smem<D>(sz, nqc).total > budget) nqc = (nqc + 1) / 2;
-  if (sizeof(double) * asm_smem<D>(sz, nqc).total > budget) {  // no chunk fits the shared budget: one CTA per SM
+  size_t budget = asm_ctas<D>() > 1 ? (228 * 1024) / asm_ctas<D>() - 1024 : 227 * 1024;
+  int nqc = sz.nq;  // largest point chunk whose work arrays fit shared memory
+  while (nqc > 1 && sizeof(double) * asm_smem<D>(sz, nqc, 1).total > budget) nqc = (nqc + 1) / 2;
+  if (sizeof(double) * asm_smem<D>(sz, nqc, 1).total > budget) {  // no chunk fits the shared budget: one CTA per SM
+    budget = 227 * 1024;
     nqc = sz.nq;
-    while (nqc > 1 && sizeof(double) * asm_smem<D>(sz, nqc).total > 227 * 1024) nqc = (nqc + 1) / 2;
+    while (nqc > 1 && sizeof(double) * asm_smem<D>(sz, nqc, 1).total > budget) nqc = (nqc + 1) / 2;
   }
-  const size_t bytes = sizeof(double) * asm_smem<D>(sz, nqc).total;
-  if (bytes > 227 * 1024) return MHDG_ERR_CONFIG;
+  if (sizeof(double) * asm_smem<D>(sz, nqc, 1).total > budget || sz.n_tri * sz.Lf > ASM_MAXFLOC) return MHDG_ERR_CONFIG;
+  int nfg = D + 1;  // faces per group of the face phases: as many as fit beside the kept arrays
+  while (nfg > 1 && sizeof(double) * asm_smem<D>(sz, nqc, nfg).total > budget) --nfg;
+  const size_t bytes = sizeof(double) * asm_smem<D>(sz, nqc, nfg).total;
   if (bytes > 48 * 1024) cudaFuncSetAttribute(k_assemble<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   mhdg_blocks bb{};
   mhdg_frozen fzo{}, fzi{};
@@ -697,7 +756,7 @@ int assemble(const mhdg_disc& g, const mhdg_flow& fl, const mhdg_stage& sg, cons
   }
   if (fi) fzi = *fi;
   k_assemble<D><<<g.n_mac, asm_threads<D>(), bytes, st>>>(g, fl, sg, u, q, uhat, Rg, Ru, Rtl, want_jac, bb, fzo, fzi,
-                                                     fi ? 1 : 0, status, nqc);
+                                                     fi ? 1 : 0, status, nqc, nfg);
   int rc = launch_ok();
   if (rc) return rc;
   return face_reduce(g, Rtl, nullptr, 0.0, Rt, st);
