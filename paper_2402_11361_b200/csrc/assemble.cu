@@ -15,6 +15,8 @@
 // (pointwise.cuh), so the stash stores are coalesced.  Every accumulation runs
 // in a fixed order (sub-element loop, inverse-incidence gathers): results are
 // bitwise reproducible run to run.
+#include <type_traits>
+
 #include "dmma.cuh"
 #include "local_ops.cuh"
 #include "pointwise.cuh"
@@ -61,6 +63,25 @@ __host__ __device__ inline int csm_ld(int nr) { return (nr + 3) & ~1; }
 // SUPG product reads W1[q][b][u][t] across (b, t) lanes without bank conflicts
 template <int D>
 __host__ __device__ constexpr int W1S() { return (D + 2) * (D + 2) + 4; }
+
+// f(integral_constant<int, c>) for the runtime c in [0, N)
+template <int I, int N>
+struct StaticSwitch {
+  template <class F>
+  static __device__ __forceinline__ void run(int c, F& f) {
+    if (c == I) f(std::integral_constant<int, I>{});
+    else StaticSwitch<I + 1, N>::run(c, f);
+  }
+};
+template <int N>
+struct StaticSwitch<N, N> {
+  template <class F>
+  static __device__ __forceinline__ void run(int, F&) {}
+};
+template <int N, class F>
+__device__ __forceinline__ void static_switch(int c, F f) {
+  StaticSwitch<0, N>::run(c, f);
+}
 
 constexpr int ASM_MAXFLOC = 1024;  // n_tri x Lf entries of the sub-face node table
 
@@ -287,28 +308,49 @@ __global__ void __launch_bounds__(asm_threads<D>(), asm_min_ctas<D>())
       if (want_jac) fo.supg_tau[fidx] = tq[qq];
     }
     __syncthreads();
-    // pointwise Jacobians and fluxes, one entry per thread
-    for (int idx = tid; idx < nc * nA; idx += nt) {
-      const int qq = idx / nA, e = idx % nA, t = e % NS, s = (e / NS) % NS, k = e / (NS * NS);
-      const size_t fidx = (((size_t)mac * sz.n_sub + K) * nq + q0 + qq) * nA + e;
-      const double a = euler_jac<D>(prv[qq], fl, k, s, t);
-      As[idx] = use_frozen ? fi.supg_jac[fidx] : a;
-      if (want_jac) {
-        Adu[idx] = a + visc_dgdu<D>(prv[qq], fl, qpt + qq * D * NS, k, s, t);
-        fo.supg_jac[fidx] = a;
-      }
-    }
-    for (int idx = tid; idx < nc * NS * D; idx += nt) {
-      const int qq = idx / (NS * D), k = idx % D, s = (idx / D) % NS;
-      FG[idx] = euler_flux<D>(prv[qq], upt + qq * NS, s, k) + visc_flux<D>(prv[qq], fl, qpt + qq * D * NS, s, k);
-    }
-    if (want_jac) {
-      const int nW = D * D * NS * NS;
-      double* Wd = bk.wdgdq_vol + (((size_t)mac * sz.n_sub + K) * nq + q0) * nW;
-      for (int idx = tid; idx < nc * nW; idx += nt) {
-        const int qq = idx / nW, e = idx % nW, t = e % NS, s = (e / NS) % NS, l = (e / (NS * NS)) % D,
-                  k = e / (D * NS * NS);
-        Wd[idx] = wq[qq] * visc_dgdq<D>(prv[qq], fl, k, l, s, t);
+    // pointwise Jacobians and fluxes.  An item is (case, point) with the case -- a (k, l) block
+    // of the stash or a (k, s) row of the Euler / viscous state Jacobians -- uniform over
+    // (most of) a warp and the lanes over points, so the entry indices are compile-time inside
+    // a case (the pointwise functions fold to straight-line code).
+    {
+      const int ncase = (want_jac ? D * D : 0) + D * NS;
+      constexpr int nW = D * D * NS * NS;
+      for (int idx = tid; idx < ncase * nc; idx += nt) {
+        const int cs = idx / nc, qq = idx - cs * nc;
+        const Prim<D> pr = prv[qq];
+        const size_t pidx = ((size_t)mac * sz.n_sub + K) * nq + q0 + qq;
+        const int c0 = want_jac ? cs : cs + D * D;
+        if (c0 < D * D) {
+          double* Wd = bk.wdgdq_vol + pidx * nW + c0 * NS * NS;
+          const double w = wq[qq];
+          static_switch<D * D>(c0, [&](auto kl) {
+            constexpr int k = decltype(kl)::value / D, l = decltype(kl)::value % D;
+#pragma unroll
+            for (int s = 0; s < NS; ++s)
+#pragma unroll
+              for (int t = 0; t < NS; ++t) Wd[s * NS + t] = w * visc_dgdq<D>(pr, fl, k, l, s, t);
+          });
+        } else {
+          const int c1 = c0 - D * D;  // k * NS + s
+          const double* qp = qpt + qq * D * NS;
+          const double* up = upt + qq * NS;
+          double* Ar = As + qq * nA + c1 * NS;
+          double* Adr = Adu + qq * nA + c1 * NS;
+          const size_t fidx = pidx * nA + c1 * NS;
+          static_switch<D * NS>(c1, [&](auto ks) {
+            constexpr int k = decltype(ks)::value / NS, sr = decltype(ks)::value % NS;
+#pragma unroll
+            for (int t = 0; t < NS; ++t) {
+              const double a = euler_jac<D>(pr, fl, k, sr, t);
+              Ar[t] = use_frozen ? fi.supg_jac[fidx + t] : a;
+              if (want_jac) {
+                Adr[t] = a + visc_dgdu<D>(pr, fl, qp, k, sr, t);
+                fo.supg_jac[fidx + t] = a;
+              }
+            }
+            FG[(qq * NS + sr) * D + k] = euler_flux<D>(pr, up, sr, k) + visc_flux<D>(pr, fl, qp, sr, k);
+          });
+        }
       }
     }
     __syncthreads();
