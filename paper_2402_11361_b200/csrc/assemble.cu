@@ -87,7 +87,7 @@ constexpr int ASM_MAXFLOC = 1024;  // n_tri x Lf entries of the sub-face node ta
 
 template <int D>
 struct AsmSmem {
-  int us, qs, uh, td, tf, gph, upt, qpt, wq, tq, prv, As, Adu, FG, Pp, sw, W1, csm, cvol;
+  int us, qs, uh, td, tf, gph, upt, qpt, wq, tq, prv, As, Adu, FG, Pp, sw, gus, tdps, rs, W1, csm, cvol;
   int fuh, fu, fq, fuv, fw, fpr, fpv, fS, fK1, ffn, fbh, cf, ctr, total;
 };
 
@@ -124,6 +124,9 @@ __host__ __device__ inline AsmSmem<D> asm_smem(const Sz& s0, int nqc, int nfg) {
   TAKE(FG, s.nq * NS * D)
   TAKE(Pp, s.nq * D * NS)
   TAKE(sw, s.nq * NS)
+  TAKE(gus, s.nq * D * NS)
+  TAKE(tdps, s.nq * NS)
+  TAKE(rs, s.nq * NS)
   TAKE(W1, asm_dmma<D>() ? s.nq * NS * w1t_ld(s.nloc * NS) : s.nq * s.nloc * W1S<D>())
   TAKE(csm, asm_dmma<D>() ? s.nloc * NS * csm_ld(s.nloc * NS) : 0)
   const int vol_end = o;
@@ -198,7 +201,7 @@ __global__ void __launch_bounds__(asm_threads<D>(), asm_min_ctas<D>())
   double *gph = sm + o.gph, *upt = sm + o.upt, *qpt = sm + o.qpt, *wq = sm + o.wq, *tq = sm + o.tq;
   Prim<D>* prv = (Prim<D>*)(sm + o.prv);
   double *As = sm + o.As, *Adu = sm + o.Adu, *FG = sm + o.FG, *Pp = sm + o.Pp, *sw = sm + o.sw;
-  double *W1 = sm + o.W1, *cvol = sm + o.cvol;
+  double *W1 = sm + o.W1, *cvol = sm + o.cvol, *gus = sm + o.gus, *tdps = sm + o.tdps, *rs = sm + o.rs;
 
   // face lattice node -> local node of sub-face T (or -1)
   __shared__ short floc[ASM_MAXFLOC];
@@ -291,13 +294,21 @@ __global__ void __launch_bounds__(asm_threads<D>(), asm_min_ctas<D>())
       for (int r = 0; r < D; ++r) v += gr[r] * ij[r * D + k];
       gph[idx] = v;  // gphys[q][a][k]
     }
+    // state and gradient at the points, one component per thread (nodes in order, as interp_point)
+    for (int idx = tid; idx < nc * (1 + D) * NS; idx += nt) {
+      const int c = idx % ((1 + D) * NS), qq = idx / ((1 + D) * NS);
+      const double* ph = g.phi_vol + (q0 + qq) * nloc;
+      const double* src = c < NS ? us + c : qs + (size_t)((c - NS) / NS) * n + (c - NS) % NS;
+      double acc = 0.0;
+      for (int a = 0; a < nloc; ++a) acc += ph[a] * src[conn[a] * NS];
+      if (c < NS) upt[qq * NS + c] = acc;
+      else qpt[qq * D * NS + (c - NS)] = acc;
+    }
+    __syncthreads();
     for (int qq = tid; qq < nc; qq += nt) {
-      double uu[NS], qv[D * NS];
-      interp_point<D>(g.phi_vol + (q0 + qq) * nloc, nloc, conn, nullptr, us, 0, qs, L, uu, qv);
+      double uu[NS];
 #pragma unroll
-      for (int s = 0; s < NS; ++s) upt[qq * NS + s] = uu[s];
-#pragma unroll
-      for (int s = 0; s < D * NS; ++s) qpt[qq * D * NS + s] = qv[s];
+      for (int s = 0; s < NS; ++s) uu[s] = upt[qq * NS + s];
       const int bad = admissible_code<D>(uu, fl.gamma);
       if (bad) set_status(status, MHDG_ERR_ADMISSIBILITY, mac, bad - 1, uu[0]);
       const Prim<D> p = prim<D>(uu, fl);
@@ -306,6 +317,19 @@ __global__ void __launch_bounds__(asm_threads<D>(), asm_min_ctas<D>())
       const size_t fidx = ((size_t)mac * sz.n_sub + K) * nq + q0 + qq;
       tq[qq] = use_frozen ? fi.supg_tau[fidx] : supg_tau<D>(p, fl, g.h_sub[mac * sz.n_sub + K], inv_sdt);
       if (want_jac) fo.supg_tau[fidx] = tq[qq];
+    }
+    // physical gradient of u (and the temporal term) at the points, for the strong residual
+    for (int idx = tid; idx < nc * (D + 1) * NS; idx += nt) {
+      const int c = idx % ((D + 1) * NS), qq = idx / ((D + 1) * NS), t = c % NS, k = c / NS;
+      double acc = 0.0;
+      if (k < D) {
+        for (int a = 0; a < nloc; ++a) acc += gph[(qq * nloc + a) * D + k] * us[conn[a] * NS + t];
+        gus[(qq * D + k) * NS + t] = acc;
+      } else {
+        if (temporal)
+          for (int a = 0; a < nloc; ++a) acc += g.phi_vol[(q0 + qq) * nloc + a] * td[conn[a] * NS + t];
+        tdps[qq * NS + t] = acc;
+      }
     }
     __syncthreads();
     // pointwise Jacobians and fluxes.  An item is (case, point) with the case -- a (k, l) block
@@ -354,56 +378,33 @@ __global__ void __launch_bounds__(asm_threads<D>(), asm_min_ctas<D>())
       }
     }
     __syncthreads();
-    // strong SUPG residual and the per-point residual vector Pp[q][k][s]
-    for (int qq = tid; qq < nc; qq += nt) {
-      double gu[D][NS], tdp[NS];
-#pragma unroll
-      for (int t = 0; t < NS; ++t) {
-        tdp[t] = 0.0;
-#pragma unroll
-        for (int k = 0; k < D; ++k) gu[k][t] = 0.0;
-      }
-      for (int a = 0; a < nloc; ++a) {
-        const int node = conn[a];
-#pragma unroll
-        for (int k = 0; k < D; ++k) {
-          const double gp = gph[(qq * nloc + a) * D + k];
-#pragma unroll
-          for (int t = 0; t < NS; ++t) gu[k][t] += gp * us[node * NS + t];
-        }
-        if (temporal) {
-          const double ph = g.phi_vol[(q0 + qq) * nloc + a];
-#pragma unroll
-          for (int t = 0; t < NS; ++t) tdp[t] += ph * td[node * NS + t];
-        }
-      }
+    // strong SUPG residual r[q][u] = sum_{k,t} A[k][u][t] gu[k][t] + td, then the per-point
+    // residual vector Pp[q][k][s]
+    for (int idx = tid; idx < nc * NS; idx += nt) {
+      const int uu = idx % NS, qq = idx / NS;
       const double* A = As + qq * nA;
-      double r[NS];
-#pragma unroll
-      for (int uu = 0; uu < NS; ++uu) {
-        double acc = 0.0;
-#pragma unroll
-        for (int k = 0; k < D; ++k)
-#pragma unroll
-          for (int t = 0; t < NS; ++t) acc += A[(k * NS + uu) * NS + t] * gu[k][t];
-        r[uu] = acc + tdp[uu];
-      }
-      const double w = wq[qq], wt = w * tq[qq];
+      double acc = 0.0;
 #pragma unroll
       for (int k = 0; k < D; ++k)
 #pragma unroll
-        for (int s = 0; s < NS; ++s) {
-          double acc = 0.0;
-#pragma unroll
-          for (int uu = 0; uu < NS; ++uu) acc += A[(k * NS + uu) * NS + s] * r[uu];
-          Pp[(qq * D + k) * NS + s] = -w * FG[(qq * NS + s) * D + k] + wt * acc;
-        }
-      if (g.source) {
-        const double* src = g.source + (((size_t)mac * sz.n_sub + K) * nq + q0 + qq) * NS;
-#pragma unroll
-        for (int s = 0; s < NS; ++s) sw[qq * NS + s] = -w * src[s];
-      }
+        for (int t = 0; t < NS; ++t) acc += A[(k * NS + uu) * NS + t] * gus[(qq * D + k) * NS + t];
+      rs[idx] = acc + tdps[idx];
     }
+    __syncthreads();
+    for (int idx = tid; idx < nc * D * NS; idx += nt) {
+      const int s = idx % NS, k = (idx / NS) % D, qq = idx / (D * NS);
+      const double* A = As + qq * nA;
+      const double w = wq[qq], wt = w * tq[qq];
+      double acc = 0.0;
+#pragma unroll
+      for (int uu = 0; uu < NS; ++uu) acc += A[(k * NS + uu) * NS + s] * rs[qq * NS + uu];
+      Pp[(qq * D + k) * NS + s] = -w * FG[(qq * NS + s) * D + k] + wt * acc;
+    }
+    if (g.source)
+      for (int idx = tid; idx < nc * NS; idx += nt) {
+        const int qq = idx / NS;
+        sw[idx] = -wq[qq] * g.source[(((size_t)mac * sz.n_sub + K) * nq + q0) * NS + idx];
+      }
     __syncthreads();
     for (int idx = tid; idx < nloc * NS; idx += nt) {
       const int s = idx % NS, a = idx / NS;
@@ -514,9 +515,22 @@ __global__ void __launch_bounds__(asm_threads<D>(), asm_min_ctas<D>())
         }
         if (q0 + nqc >= nq) {  // the sub-element's block is complete (summed over the point chunks in Csm)
           __syncthreads();
-          for (int idx = tid; idx < nr * nr; idx += nt) {
-            const int cb = idx % nr, rb = idx / nr, t = cb % NS, b = cb / NS, s = rb % NS, a = rb / NS;
-            SSm[(size_t)(conn[a] * NS + s) * n + conn[b] * NS + t] += Csm[rb * cld + cb];
+          constexpr int UB = 4;  // loads in flight per thread
+          for (int i0 = tid; i0 < nr * nr; i0 += UB * nt) {
+            double* pa[UB];
+            double v[UB];
+#pragma unroll
+            for (int u = 0; u < UB; ++u) {
+              const int idx = i0 + u * nt;
+              if (idx < nr * nr) {
+                const int cb = idx % nr, rb = idx / nr, t = cb % NS, b = cb / NS, s = rb % NS, a = rb / NS;
+                pa[u] = SSm + (size_t)(conn[a] * NS + s) * n + conn[b] * NS + t;
+                v[u] = *pa[u] + Csm[rb * cld + cb];
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < UB; ++u)
+              if (i0 + u * nt < nr * nr) *pa[u] = v[u];
           }
         }
       } else {
@@ -606,43 +620,67 @@ __global__ void __launch_bounds__(asm_threads<D>(), asm_min_ctas<D>())
       fw[pp] = g.w_face_ref[T * nqf + qq] * (g.face_fac * g.areas[mac * NF + f]);
     }
     __syncthreads();
-    for (int idx = tid; idx < npt * NS * NS; idx += nt) {
-      const int pp = idx / (NS * NS), s = (idx / NS) % NS, t = idx % NS, f = f0 + pp / nqt;
-      const size_t pg = ((size_t)mac * NF + f) * nqt + pp % nqt;
-      const double* nv = g.normals + (mac * NF + f) * D;
-      const double S = use_frozen ? fi.face_stab[pg * NS * NS + s * NS + t]
-                                  : ((s == t) ? stab_diag<D>(fpr[pp], fl, nv, s) : 0.0);
-      fS[idx] = S;
-      if (want_jac) {
-        fo.face_stab[pg * NS * NS + s * NS + t] = S;
-        double an = 0.0;
+    // stabilisation / flux Jacobian rows and stash rows as (case, point) items: the case (a row
+    // s of S and K1, or a row (l, s) of the stash) is uniform over (most of) a warp, the lanes
+    // run over points, and the entry indices are compile-time inside a case
+    {
+      const int ncase = NS + (want_jac ? D * NS : 0);
+      for (int idx = tid; idx < ncase * npt; idx += nt) {
+        const int cs = idx / npt, pp = idx - cs * npt, f = f0 + pp / nqt;
+        const size_t pg = ((size_t)mac * NF + f) * nqt + pp % nqt;
+        double nv[D];
 #pragma unroll
-        for (int k = 0; k < D; ++k) an += euler_jac<D>(fpr[pp], fl, k, s, t) * nv[k];
-        fK1[idx] = an - S;  // d(flux.n)/d uhat, viscous uhat-dependence dropped
-      }
-    }
-    if (want_jac) {
-      const int nW = D * NS * NS;
-      double* Wf = bk.wdgdq_face + (((size_t)mac * NF + f0) * nqt) * nW;  // the group's points are contiguous
-      for (int idx = tid; idx < npt * nW; idx += nt) {
-        const int pp = idx / nW, e = idx % nW, t = e % NS, s = (e / NS) % NS, l = e / (NS * NS), f = f0 + pp / nqt;
-        const double* nv = g.normals + (mac * NF + f) * D;
-        double acc = 0.0;
+        for (int k = 0; k < D; ++k) nv[k] = g.normals[(mac * NF + f) * D + k];
+        if (cs < NS) {
+          const Prim<D> pr = fpr[pp];
+          static_switch<NS>(cs, [&](auto sc) {
+            constexpr int sr = decltype(sc)::value;
 #pragma unroll
-        for (int k = 0; k < D; ++k) acc += visc_dgdq<D>(fpv[pp], fl, k, l, s, t) * nv[k];
-        Wf[idx] = fw[pp] * acc;
+            for (int t = 0; t < NS; ++t) {
+              const double S = use_frozen ? fi.face_stab[pg * NS * NS + sr * NS + t]
+                                          : ((sr == t) ? stab_diag<D>(pr, fl, nv, sr) : 0.0);
+              fS[(pp * NS + sr) * NS + t] = S;
+              if (want_jac) {
+                fo.face_stab[pg * NS * NS + sr * NS + t] = S;
+                double an = 0.0;
+#pragma unroll
+                for (int k = 0; k < D; ++k) an += euler_jac<D>(pr, fl, k, sr, t) * nv[k];
+                fK1[(pp * NS + sr) * NS + t] = an - S;  // d(flux.n)/d uhat, viscous uhat-dependence dropped
+              }
+            }
+          });
+        } else {
+          const Prim<D> pr = fpv[pp];
+          const double w = fw[pp];
+          double* Wf = bk.wdgdq_face + pg * (D * NS * NS) + (cs - NS) * NS;
+          static_switch<D * NS>(cs - NS, [&](auto lsc) {
+            constexpr int l = decltype(lsc)::value / NS, sr = decltype(lsc)::value % NS;
+#pragma unroll
+            for (int t = 0; t < NS; ++t) {
+              double acc = 0.0;
+#pragma unroll
+              for (int k = 0; k < D; ++k) acc += visc_dgdq<D>(pr, fl, k, l, sr, t) * nv[k];
+              Wf[t] = w * acc;
+            }
+          });
+        }
       }
     }
     __syncthreads();
-    for (int idx = tid; idx < npt * NS; idx += nt) {
-      const int pp = idx / NS, s = idx % NS, f = f0 + pp / nqt;
+    for (int idx0 = tid; idx0 < npt * NS; idx0 += nt) {
+      const int s = idx0 / npt, pp = idx0 - s * npt, f = f0 + pp / nqt, idx = pp * NS + s;  // lanes over points
       const int kind = g.bc_kind[mac * NF + f];
       const double* nv = g.normals + (mac * NF + f) * D;
       double fn = 0.0;
+      {
+        const Prim<D> pr = fpr[pp], pv = fpv[pp];
+        static_switch<NS>(s, [&](auto sc) {
+          constexpr int sr = decltype(sc)::value;
 #pragma unroll
-      for (int k = 0; k < D; ++k)
-        fn += (euler_flux<D>(fpr[pp], fuh + pp * NS, s, k) + visc_flux<D>(fpv[pp], fl, fq + pp * D * NS, s, k)) *
-              nv[k];
+          for (int k = 0; k < D; ++k)
+            fn += (euler_flux<D>(pr, fuh + pp * NS, sr, k) + visc_flux<D>(pv, fl, fq + pp * D * NS, sr, k)) * nv[k];
+        });
+      }
       double sa = 0.0;
 #pragma unroll
       for (int t = 0; t < NS; ++t) sa += fS[(pp * NS + s) * NS + t] * (fu[pp * NS + t] - fuh[pp * NS + t]);
