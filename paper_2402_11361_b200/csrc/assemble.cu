@@ -87,7 +87,7 @@ constexpr int ASM_MAXFLOC = 1024;  // n_tri x Lf entries of the sub-face node ta
 
 template <int D>
 struct AsmSmem {
-  int us, qs, uh, td, tf, gph, upt, qpt, wq, tq, prv, As, Adu, FG, Pp, sw, gus, tdps, rs, W1, csm, cvol;
+  int us, qs, uh, td, tf, gph, upt, qpt, wq, tq, prv, As, Adu, FG, Pp, sw, gus, tdps, rs, wts, W1, csm, cvol;
   int fuh, fu, fq, fuv, fw, fpr, fpv, fS, fK1, ffn, fbh, cf, ctr, total;
 };
 
@@ -127,6 +127,7 @@ __host__ __device__ inline AsmSmem<D> asm_smem(const Sz& s0, int nqc, int nfg) {
   TAKE(gus, s.nq * D * NS)
   TAKE(tdps, s.nq * NS)
   TAKE(rs, s.nq * NS)
+  TAKE(wts, s.nq)
   TAKE(W1, asm_dmma<D>() ? s.nq * NS * w1t_ld(s.nloc * NS) : s.nq * s.nloc * W1S<D>())
   TAKE(csm, asm_dmma<D>() ? s.nloc * NS * csm_ld(s.nloc * NS) : 0)
   const int vol_end = o;
@@ -201,7 +202,7 @@ __global__ void __launch_bounds__(asm_threads<D>(), asm_min_ctas<D>())
   double *gph = sm + o.gph, *upt = sm + o.upt, *qpt = sm + o.qpt, *wq = sm + o.wq, *tq = sm + o.tq;
   Prim<D>* prv = (Prim<D>*)(sm + o.prv);
   double *As = sm + o.As, *Adu = sm + o.Adu, *FG = sm + o.FG, *Pp = sm + o.Pp, *sw = sm + o.sw;
-  double *W1 = sm + o.W1, *cvol = sm + o.cvol, *gus = sm + o.gus, *tdps = sm + o.tdps, *rs = sm + o.rs;
+  double *W1 = sm + o.W1, *cvol = sm + o.cvol, *gus = sm + o.gus, *tdps = sm + o.tdps, *rs = sm + o.rs, *wts = sm + o.wts;
 
   // face lattice node -> local node of sub-face T (or -1)
   __shared__ short floc[ASM_MAXFLOC];
@@ -317,6 +318,7 @@ __global__ void __launch_bounds__(asm_threads<D>(), asm_min_ctas<D>())
       const size_t fidx = ((size_t)mac * sz.n_sub + K) * nq + q0 + qq;
       tq[qq] = use_frozen ? fi.supg_tau[fidx] : supg_tau<D>(p, fl, g.h_sub[mac * sz.n_sub + K], inv_sdt);
       if (want_jac) fo.supg_tau[fidx] = tq[qq];
+      wts[qq] = wq[qq] * tq[qq];
     }
     // physical gradient of u (and the temporal term) at the points, for the strong residual
     for (int idx = tid; idx < nc * (D + 1) * NS; idx += nt) {
@@ -423,55 +425,60 @@ __global__ void __launch_bounds__(asm_threads<D>(), asm_min_ctas<D>())
       if constexpr (asm_dmma<D>()) {
         const int wld = w1t_ld(nr), cld = csm_ld(nr);
         double* Csm = sm + o.csm;
-        for (int idx = tid; idx < nc * nw; idx += nt) {
-          const int s = idx % NS, a = (idx / NS) % nloc, uu = (idx / nr) % NS, qq = idx / nw;
-          double acc = 0.0;
+        const int warp = tid >> 5, lane = tid & 31, g8 = lane >> 2, t4 = lane & 3, nwarp = nt >> 5;
+        for (int row = warp; row < nc * NS; row += nwarp) {  // a warp per row (q, u) of W1T: no runtime divisions
+          const int qq = row / NS, uu = row - qq * NS;
+          const double* Aq = As + (qq * D * NS + uu) * NS;
+          const double* gq_ = gph + qq * nloc * D;
+          for (int col = lane; col < nr; col += 32) {
+            const int a = col / NS, s = col - a * NS;
+            double acc = 0.0;
 #pragma unroll
-          for (int k = 0; k < D; ++k) acc += As[((qq * D + k) * NS + uu) * NS + s] * gph[(qq * nloc + a) * D + k];
-          W1[(qq * NS + uu) * wld + a * NS + s] = acc;  // W1T[(q, u)][(a, s)]
+            for (int k = 0; k < D; ++k) acc += Aq[k * NS * NS + s] * gq_[a * D + k];
+            W1[row * wld + col] = acc;  // W1T[(q, u)][(a, s)]
+          }
         }
+        if (q0 + nqc >= nq)  // the rows of state_state this sub-element updates, on their way to L1
+          for (int idx = tid; idx < nr * nloc; idx += nt) {
+            const int b = idx % nloc, rb = idx / nloc, s = rb % NS, a = rb / NS;
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(SSm + (size_t)(conn[a] * NS + s) * n + conn[b] * NS));
+          }
         __syncthreads();
         // contrib[(a,s),(b,t)] = sum_{(q,u)} (w tau W1T[(q,u)][(a,s)]) W1T[(q,u)][(b,t)]        (GEMM 2)
         //                      + sum_q Y[q][(a,s,t)] phi[q][b],                                 (GEMM 1)
         //   Y = -w sum_k Adu[q,k,s,t] gphys[q,a,k] + dt_coeff w tau W1T[(q,t)][(a,s)]   (assembly.py:465-470)
-        const int warp = tid >> 5, lane = tid & 31, g8 = lane >> 2, t4 = lane & 3, nwarp = nt >> 5;
+        // GEMM 2 is symmetric: one 8 x 8 tile (mt <= nt) per unit, mirrored into Csm
         const int mtl = (nr + 7) / 8;
-        constexpr int NH = 4;  // n-tiles per unit of GEMM 2 (the A fragment is used NH times)
-        const int nun = mtl * ((mtl + NH - 1) / NH), K2 = nc * NS, ks2 = (K2 + 3) / 4;
+        const int nun = mtl * (mtl + 1) / 2, K2 = nc * NS, ks2 = (K2 + 3) / 4;
         for (int un = warp; un < nun; un += nwarp) {
-          const int mt = un % mtl, n0 = (un / mtl) * NH;
-          const int m = mt * 8 + g8;
-          const bool mok = m < nr;
-          int colB[NH];
-          bool nok[NH];
-#pragma unroll
-          for (int h = 0; h < NH; ++h) {
-            const int nn = (n0 + h) * 8 + g8;
-            nok[h] = nn < nr;
-            colB[h] = nok[h] ? nn : 0;
+          int mt = 0, rem = un;
+          while (rem >= mtl - mt) {
+            rem -= mtl - mt;
+            ++mt;
           }
-          double c[NH][2];
-#pragma unroll
-          for (int h = 0; h < NH; ++h) c[h][0] = c[h][1] = 0.0;
+          const int ntile = mt + rem;
+          const int m = mt * 8 + g8, nn = ntile * 8 + g8;
+          const bool mok = m < nr, nok = nn < nr;
+          const int mc = mok ? m : 0, ncol = nok ? nn : 0;
+          double c0 = 0.0, c1 = 0.0;
           for (int ks = 0; ks < ks2; ++ks) {
             const int kk = 4 * ks + t4;
             const bool kok = kk < K2;
-            const int qq = kok ? kk / NS : 0;
-            const double* wr = W1 + (kok ? kk : 0) * wld;
-            const double af = (mok && kok) ? wq[qq] * tq[qq] * wr[m] : 0.0;
-#pragma unroll
-            for (int h = 0; h < NH; ++h) {
-              const double bf = (kok && nok[h]) ? wr[colB[h]] : 0.0;
-              dmma_8x8x4(c[h][0], c[h][1], af, bf);
-            }
+            const int kc = kok ? kk : 0;
+            const double* wr = W1 + kc * wld;
+            const double af = (mok && kok) ? wts[kc / NS] * wr[mc] : 0.0;
+            const double bf = (kok && nok) ? wr[ncol] : 0.0;
+            dmma_8x8x4(c0, c1, af, bf);
           }
 #pragma unroll
-          for (int h = 0; h < NH; ++h)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int col = (n0 + h) * 8 + 2 * t4 + e;
-              if (mok && col < nr) Csm[m * cld + col] = q0 == 0 ? c[h][e] : Csm[m * cld + col] + c[h][e];
+          for (int e = 0; e < 2; ++e) {
+            const int col = ntile * 8 + 2 * t4 + e;
+            const double cv = e ? c1 : c0;
+            if (mok && col < nr) {
+              Csm[m * cld + col] = q0 == 0 ? cv : Csm[m * cld + col] + cv;
+              if (ntile != mt) Csm[col * cld + m] = q0 == 0 ? cv : Csm[col * cld + m] + cv;
             }
+          }
         }
         __syncthreads();
         const int mt1 = (nw + 7) / 8, ks1 = (nc + 3) / 4;
