@@ -496,6 +496,44 @@ __global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 ? 1 : 2)) k_apply_s
     // Point groups of PPI points per warp pass, dealt to warps by global index.
     auto wcontract = [&](const double* A, int u0, int nu, bool face, bool second, int wid, int nw) {
       constexpr int DN = D * NS, PPI = 32 / DN;
+      if constexpr (D == 3) {
+        // 3D volume stash: 15 outputs of 15 terms per point and ~8 points per piece -- one point
+        // per warp pass with two lanes per output (lane = 16 h + j; terms i = 2 i' + h, rotated by
+        // 5 s: conflict-free W reads), so every warp of the half works on a piece and the
+        // dependent FMA chains are half as long
+        if (!face) {
+          const int h = lane >> 4, j = lane & 15;
+          const bool jon = j < DN;
+          const int jj = jon ? j : 0, tt0 = jj % NS, l0 = jj / NS;  // v component / output (k, s)
+          for (int pl = first_group(u0, wid, nw) - u0; pl < nu; pl += nw) {
+            const int pt = u0 + pl, K = pt / NQ, q = pt % NQ;
+            double a = 0.0;
+#pragma unroll
+            for (int b = 0; b < NLOC; b += 2)
+              if (b + h < NLOC) a += phs[q * NLOC + b + h] * z[(l0 * L + conn[K * NLOC + b + h]) * NS + tt0];
+            a += __shfl_xor_sync(MHDG_FULL, a, 16);
+            if (h == 0 && jon) vw[j] = a;
+            __syncwarp();
+            const double* w = A + pl * C::NW + l0 * D * NS * NS + tt0 * NS;  // output k = l0, s = tt0
+            double o = 0.0;
+#pragma unroll
+            for (int ip = 0; ip < (DN + 1) / 2; ++ip) {
+              const int i = 2 * ip + h;
+              if (i < DN) {
+                int ii = i + NS * tt0;
+                if (ii >= DN) ii -= DN;
+                if (ii >= DN) ii -= DN;
+                const int l = ii / NS, tt = ii - l * NS;
+                o += w[l * NS * NS + tt] * vw[ii];
+              }
+            }
+            o += __shfl_xor_sync(MHDG_FULL, o, 16);
+            if (h == 0 && jon) wv[pt * DN + j] = o;
+            __syncwarp();
+          }
+          return;
+        }
+      }
       const int pi = lane / DN, j = lane % DN;
       const int ngrp = (nu + PPI - 1) / PPI;
       for (int grp = first_group(u0 / PPI, wid, nw) - u0 / PPI; grp < ngrp; grp += nw) {
