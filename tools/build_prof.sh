@@ -5,8 +5,8 @@
 set -e
 cd "$(dirname "$0")/../paper_2402_11361_b200/csrc"
 mkdir -p ../../tools/prof/build
-PROF=${PROF:-"capi apply apply_stream condense schur lu precond assemble krylov ahat"}
-for s in capi apply apply_stream condense schur lu precond assemble krylov ahat; do
+PROF=${PROF:-"capi apply apply_stream condense schur lu precond assemble krylov ahat halo"}
+for s in capi apply apply_stream condense schur lu precond assemble krylov ahat halo; do
   D=""
   case " $PROF " in *" $s "*) D="-DMHDG_STREAM_PROFILE -DMHDG_GJ_PROFILE" ;; esac
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC \
