@@ -27,6 +27,12 @@ constexpr int SCH2_MAXT = 256;
 template <int D>
 struct Sch2 {
   static constexpr int NS = D + 2, NW = D * D * NS * NS, NWF = D * NS * NS;
+  // shared-memory strides of the stash (doubles): the (s, r) block of gradient direction l at
+  // SR (= 4 mod 16), flux direction k at SK, point q at SQ (= 4 D mod 16), so the A-fragment
+  // reads of a half-warp -- 4 consecutive (s, r) x 4 consecutive (q, r') -- fall in 16
+  // different banks (the dense strides ns^2, D ns^2, D^2 ns^2 gave 2-way (3D) and 4-way (2D)
+  // conflicts); faces: SR per direction, SQF per point
+  static constexpr int SR = D == 2 ? 20 : 28, SK = D * SR, SQ = D == 2 ? 88 : 252, SQF = D == 2 ? 40 : 92;
   static constexpr int NT = D == 2 ? 12 : 5;   // n-tiles: L <= 8 NT
   static constexpr int KS = D == 2 ? 8 : 21;   // k-steps: nq D <= 4 KS
   static constexpr int KSF = D == 2 ? 8 : 12;  // face k-steps per sub-face: nqf D <= 4 KSF (3D p <= 3)
@@ -74,13 +80,13 @@ struct Sch2Dims {
     // rows T kfp + k (kfp = 4 ksf: each sub-face starts on a k-step)
     d.kfp = 4 * d.ksf;
     d.rpn = (C::NS * C::NS + 7) / 8 * 8;  // face-stage rows per face node (8-row tiles stay on one node)
-    const int wv = d.qs * C::NW, wf = g.n_tri * g.nqf * C::NWF;
+    const int wv = d.qs * C::SQ, wf = g.n_tri * g.nqf * C::SQF;
     d.wmax = ((wv > wf ? wv : wf) + 1) & ~1;
     d.pmrows = 4 * C::KS > g.n_tri * d.kfp ? 4 * C::KS : g.n_tri * d.kfp;
     // + padding: the last B fragments of a row read up to 8 NT - LP columns past it
     // (columns >= L are never stored; the padding is zero)
     d.stage = d.wmax + d.pmrows * d.LP + 8 * C::NT;
-    d.ngph = (g.n_grad_cls * g.nq * g.nloc * D + 1) & ~1;
+    d.ngph = (g.nq * g.nloc * D + 1) & ~1;  // one gradient class at a time (the stage's sub-element)
     return d;
   }
   template <int D>
@@ -99,7 +105,7 @@ __global__ void __launch_bounds__(Sch2<D>::NWARP * 32, Sch2<D>::MINB) k_schur2(m
   const int mac = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g8 = lane >> 2, t4 = lane & 3;
   const int L = g.L, n = L * NS, nq = g.nq, nloc = g.nloc, nqf = g.nqf, nlocf = g.nlocf;
-  double* gph = sm;                      // n_grad_cls x nq x nloc x D: physical basis gradients
+  double* gph = sm;                      // nq x nloc x D: physical basis gradients of the stage's class
   double* stg = sm + dm.ngph;            // 2 stages: [W' (wmax) | PM (4 KS x LP)]
   double* Sm = S + (size_t)mac * n * n;
   const double* SSm = b.state_state + (size_t)mac * n * n;
@@ -156,7 +162,18 @@ __global__ void __launch_bounds__(Sch2<D>::NWARP * 32, Sch2<D>::MINB) k_schur2(m
       psrc = g.pm_face + (size_t)f * g.n_tri * dm.kf * L;
       kk = g.n_tri * dm.kf;
     }
-    for (int e = tid; e < wcnt; e += NT_THREADS) cp_async8(W + e, wsrc + e, 8);
+    if (i < nvol) {
+      for (int e = tid; e < wcnt; e += NT_THREADS) {
+        const int pt = e / NW, rem = e - pt * NW, k = rem / (D * NS * NS), l = (rem / (NS * NS)) % D,
+                  sr = rem % (NS * NS);
+        cp_async8(W + pt * C::SQ + k * C::SK + l * C::SR + sr, wsrc + e, 8);
+      }
+    } else {
+      for (int e = tid; e < wcnt; e += NT_THREADS) {
+        const int pt = e / NWF, rem = e - pt * NWF, l = rem / (NS * NS), sr = rem % (NS * NS);
+        cp_async8(W + pt * C::SQF + l * C::SR + sr, wsrc + e, 8);
+      }
+    }
     for (int e = tid; e < kk * L; e += NT_THREADS) {
       const int row = e / L, j = e - row * L;
       const int prow = i < nvol ? row : (row / dm.kf) * dm.kfp + row % dm.kf;
@@ -168,14 +185,6 @@ __global__ void __launch_bounds__(Sch2<D>::NWARP * 32, Sch2<D>::MINB) k_schur2(m
   for (int e = tid; e < C::NBUF * dm.stage; e += NT_THREADS) stg[e] = 0.0;
   __syncthreads();
   prefetch(0);
-  // physical gradients per class (geometry folded in once per macro)
-  for (int idx = tid; idx < g.n_grad_cls * nq * nloc * D; idx += NT_THREADS) {
-    const int k = idx % D, base = idx - k;
-    double v = 0.0;
-#pragma unroll
-    for (int r = 0; r < D; ++r) v += __ldg(g.grad_cls + base + r) * ij[r][k];
-    gph[idx] = v;
-  }
 
   for (int i = 0; i < nstage; ++i) {
     if (C::NBUF == 1 && i > 0) {
@@ -188,20 +197,30 @@ __global__ void __launch_bounds__(Sch2<D>::NWARP * 32, Sch2<D>::MINB) k_schur2(m
     const bool vol = i < nvol;
     double* W = stg + (size_t)(i % C::NBUF) * dm.stage;
     const double* PM = W + dm.wmax;
+    if (vol) {  // physical gradients of this stage's sub-element class (geometry folded in)
+      const double* gc = g.grad_cls + (size_t)__ldg(g.grad_cls_of + (SLICED ? i / dm.nsl : i)) * nq * nloc * D;
+      for (int idx = tid; idx < nq * nloc * D; idx += NT_THREADS) {
+        const int k = idx % D, base = idx - k;
+        double v = 0.0;
+#pragma unroll
+        for (int r = 0; r < D; ++r) v += __ldg(gc + base + r) * ij[r][k];
+        gph[idx] = v;
+      }
+    }
     {  // fold inv_jac into the stash in place: W'[..(k, r')..] = sum_l ij[r'][l] W[..(k, l)..]
       const int ngrp = (vol ? (SLICED ? min(dm.qs, nq - (i % dm.nsl) * dm.qs) : nq) * D : g.n_tri * nqf) * NS * NS;
       for (int e = tid; e < ngrp; e += NT_THREADS) {
-        const int sr = e % (NS * NS), qk = e / (NS * NS);
-        double* w = W + (size_t)qk * D * NS * NS + sr;
+        const int sr = e % (NS * NS), qk = e / (NS * NS);  // volume: qk = q D + k; faces: the point
+        double* w = W + (vol ? (qk / D) * C::SQ + (qk % D) * C::SK : qk * C::SQF) + sr;
         double v[D];
 #pragma unroll
-        for (int l = 0; l < D; ++l) v[l] = w[l * NS * NS];
+        for (int l = 0; l < D; ++l) v[l] = w[l * C::SR];
 #pragma unroll
         for (int rp = 0; rp < D; ++rp) {
           double t = 0.0;
 #pragma unroll
           for (int l = 0; l < D; ++l) t += ij[rp][l] * v[l];
-          w[rp * NS * NS] = t;
+          w[rp * C::SR] = t;
         }
       }
     }
@@ -239,7 +258,7 @@ __global__ void __launch_bounds__(Sch2<D>::NWARP * 32, Sch2<D>::MINB) k_schur2(m
         }
         // A fragments of this row, T1[m][(q, r') = 4 ks + t4], formed KB k-steps at a time (3D:
         // the 21 k-steps at once spilled registers inside this loop)
-        const double* gp = gph + (size_t)(cls * nq) * nloc * D + a * D;
+        const double* gp = gph + a * D;
         const double* w = W + (s * NS + r);
         constexpr int KB = C::KB;
 #pragma unroll
@@ -252,9 +271,9 @@ __global__ void __launch_bounds__(Sch2<D>::NWARP * 32, Sch2<D>::MINB) k_schur2(m
             if (mok && ks < ksv && kq < kvs) {
               const int q = kq / D, rp = kq - q * D;  // slice-local point; q0 + q in the tables
               const double* gq = gp + (size_t)(q0 + q) * nloc * D;
-              const double* wq = w + (size_t)q * NW + rp * NS * NS;
+              const double* wq = w + q * C::SQ + rp * C::SR;
 #pragma unroll
-              for (int k = 0; k < D; ++k) v += gq[k] * wq[k * D * NS * NS];
+              for (int k = 0; k < D; ++k) v += gq[k] * wq[k * C::SK];
             }
             af[kk] = v;
           }
@@ -295,7 +314,7 @@ __global__ void __launch_bounds__(Sch2<D>::NWARP * 32, Sch2<D>::MINB) k_schur2(m
         const int ninc = finc_n[gg];
         for (int e = 0; e < ninc; ++e) {
           const int T = finc_T[gg][e], a = finc_a[gg][e];
-          const double* WT = W + (size_t)T * nqf * NWF;
+          const double* WT = W + T * nqf * C::SQF;
           double af[KSF];
 #pragma unroll
           for (int ks = 0; ks < KSF; ++ks) {
@@ -303,7 +322,7 @@ __global__ void __launch_bounds__(Sch2<D>::NWARP * 32, Sch2<D>::MINB) k_schur2(m
             double v = 0.0;
             if (mok && ks < dm.ksf && kq < dm.kf) {
               const int q = kq / D, rp = kq - q * D;
-              v = -WT[((q * D + rp) * NS + s) * NS + r] * __ldg(g.phi_face + q * nlocf + a);
+              v = -WT[q * C::SQF + rp * C::SR + s * NS + r] * __ldg(g.phi_face + q * nlocf + a);
             }
             af[ks] = v;
           }
