@@ -13,6 +13,7 @@
 //     bytes in flight are set by the ring depth, not by thread count;
 //   * CTAs are persistent (grid = SMs x CTAs/SM) and walk the macros.
 // Results match k_apply_local to rounding; all reductions are in a fixed order.
+#include "dmma.cuh"
 #include "local_ops.cuh"
 #include "packed_lu.cuh"
 #include "tiled_inv.cuh"
@@ -110,7 +111,9 @@ __device__ __forceinline__ void seg_loop(R& rg, int lane, Body&& body) {
 // PART 0 walks the fused apply (all but the hand-off pieces), PART 1 the
 // segments before S^-1 (pre kernel), PART 2 the hand-off pieces and the
 // segments after S^-1 (post kernel).
-template <class C, int PART = 0>
+// MDR: the M^-1 D table stays resident in shared memory (post kernel) instead of streaming
+// through the ring for every macro.
+template <class C, int PART = 0, bool MDR = false>
 struct Sched {
   int seg = 0, i = 0, b = 0, r = 0;
   // W_vol pieces hold whole sub-elements when they fit (one warp pass per point group)
@@ -168,7 +171,7 @@ struct Sched {
             return true;
           }
           break;
-        case 7: if (rows(p, K_MD, C::D * C::NFN, C::L)) return true; break;
+        case 7: if (!MDR && rows(p, K_MD, C::D * C::NFN, C::L)) return true; break;
         case 8: if (rows(p, K_WF2, C::NPF, C::NWF)) return true; break;
         case 9: if (rows(p, K_FTS, C::NF * C::BS, C::BS)) return true; break;
       }
@@ -188,7 +191,7 @@ struct SSm {
   static constexpr bool PRE = PART != 2, POST = PART != 1;
   static constexpr int xl = 0;
   static constexpr int z = xl + (PRE ? C::LTR : 0);  // z, later z2
-  static constexpr int y = z + C::D * C::n;
+  static constexpr int y = z + (PART == 2 ? C::D * C::NFN * C::NS : C::D * C::n);  // post: z2 at the face nodes only
   static constexpr int t = y + C::n;
   static constexpr int rfst = t + (PART == 0 ? C::n : 0);
   static constexpr int ftt = rfst + (PRE ? C::LTR : 0);
@@ -229,6 +232,21 @@ struct TSm {
   static constexpr int total = ndbl + ceven((nint + 1) / 2);     // doubles
   static constexpr int CLS = C::NQ * C::NLOC * C::D;            // doubles per gradient class
 };
+
+// Post kernel with the macro-independent M^-1 D table (D NFN x L doubles: 52 KB at C2) resident
+// in shared memory: streamed through the ring it was 52 of the 135 KB per macro the C2 post
+// kernel moved.  Used when at least two ring stages still fit the two-CTAs-per-SM budget.
+#ifndef MHDG_POST_MDR
+#define MHDG_POST_MDR 1
+#endif
+template <class C>
+__host__ __device__ constexpr int md_table() { return ceven(C::D * C::NFN * C::L); }
+template <class C>
+__host__ __device__ constexpr int post_stages_mdr() {
+  return ((109 * 1024) / 8 - SSm<C, 2>::total - TSm<C>::total - md_table<C>()) / ST_DBL;
+}
+template <class C>
+__host__ __device__ constexpr bool post_mdr() { return MHDG_POST_MDR != 0 && post_stages_mdr<C>() >= 2; }
 
 __device__ __forceinline__ void cbar() { named_bar(1, NCONS); }
 
@@ -340,6 +358,7 @@ __global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 ? 1 : 2)) k_apply_s
   __shared__ int npieces;
   using S = SSm<C, PART>;
   using TS = TSm<C>;
+  constexpr bool MDRES = PART == 2 && post_mdr<C>();
   double* ring = smem;
   double* W = smem + STAGES * ST_DBL;
   double* Td = W + S::total;
@@ -355,7 +374,7 @@ __global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 ? 1 : 2)) k_apply_s
     }
     fence_mbar_init();
     // the piece schedule is identical for every macro: build it once
-    Sched<C, PART> sc;
+    Sched<C, PART, MDRES> sc;
     int np = 0;
     while (np < MAXP && sc.next(pieces[np])) ++np;
     npieces = np;
@@ -385,6 +404,8 @@ __global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 ? 1 : 2)) k_apply_s
     for (int i = tid; i < NSUB; i += nt) Ti[TS::gcls_of + i] = g.grad_cls_of[i];
     if (PART != 2 && D == 2)  // 3D reads its (larger) class tables through L1
       for (int i = tid; i < g.n_grad_cls * TS::CLS; i += nt) Gc[i] = g.grad_cls[i];
+    if (MDRES)  // the M^-1 D table, resident for the whole launch (the post part has no class tables)
+      for (int i = tid; i < D * C::NFN * L; i += nt) Gc[i] = g.minv_d_face[i];
   }
   __syncthreads();
   const int np = npieces;
@@ -467,7 +488,7 @@ __global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 ? 1 : 2)) k_apply_s
   double* wv = tg;   // W_vol contraction results, lifetime: W_vol pieces .. y1
   double* z2 = z;    // z is dead once the W_face(z) pieces are consumed
   double* vw = vv + warp * 32;  // warp-private scratch
-  using SC = Sched<C, PART>;
+  using SC = Sched<C, PART, MDRES>;
   ConsRing<STAGES> rg{smem_u32(full_bar), smem_u32(empty_bar), ring};
 
   // this thread's trace entry of the next macro, gathered one macro ahead
@@ -820,30 +841,40 @@ __global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 ? 1 : 2)) k_apply_s
     }
     // tg[r][i][s] = sum_J (M^-1 D_r)[fnode_i][J] y2[J][s]: lane = (J half, row, s) for groups
     // of MDR rows dealt to warps by global index; the two halves meet in one shuffle
-    seg_loop<D * C::NFN, units_per_piece(L)>(rg, lane, [&](const double* A, int u0, int nu) {
-      constexpr int MDR = 16 / NS, JH = (L + 1) / 2;
-      const int h = lane >> 4, rr = (lane & 15) / NS, s = (lane & 15) % NS;
-      const int g1 = (u0 + nu - 1) / MDR;
-      for (int gg = first_group(u0 / MDR, warp); gg <= g1; gg += NWARP_C) {
-        const int row = gg * MDR + rr;
-        const bool on = rr < MDR && row >= u0 && row < u0 + nu;
-        double a0 = 0.0, a1 = 0.0;
-        if (on) {
-          const int j0 = h * JH, j1 = h ? L : JH;
-          const double* a = A + (row - u0) * L;
-          int J = j0;
+    // On the FP64 tensor cores: 8-row tiles of the table (A fragments straight from shared
+    // memory) against y2 as an L x NS matrix padded to 8 columns; two accumulator chains (even
+    // and odd k-steps), tiles dealt to warps by global index.
+    auto md_rows = [&](const double* A, int u0, int nu) {
+      const int g8 = lane >> 2, t4 = lane & 3;
+      constexpr int KSTEPS = (L + 3) / 4;
+      const int t1 = (u0 + nu - 1) / 8;
+      for (int tt = first_group(u0 / 8, warp); tt <= t1; tt += NWARP_C) {
+        const int row = tt * 8 + g8;
+        const bool on = row >= u0 && row < u0 + nu;
+        const double* a = A + (on ? row - u0 : 0) * L;
+        double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;
 #pragma unroll 4
-          for (; J + 1 < j1; J += 2) {
-            a0 += a[J] * y[J * NS + s];
-            a1 += a[J + 1] * y[(J + 1) * NS + s];
+        for (int ks = 0; ks < KSTEPS; ks += 2) {
+          {
+            const int J = 4 * ks + t4;
+            const double af = (on && J < L) ? a[J] : 0.0;
+            const double bf = (g8 < NS && J < L) ? y[J * NS + g8] : 0.0;
+            dmma_8x8x4(c0, c1, af, bf);
           }
-          if (J < j1) a0 += a[J] * y[J * NS + s];
+          if (ks + 1 < KSTEPS) {
+            const int J = 4 * (ks + 1) + t4;
+            const double af = (on && J < L) ? a[J] : 0.0;
+            const double bf = (g8 < NS && J < L) ? y[J * NS + g8] : 0.0;
+            dmma_8x8x4(e0, e1, af, bf);
+          }
         }
-        double acc = a0 + a1;
-        acc += __shfl_xor_sync(MHDG_FULL, acc, 16);
-        if (on && h == 0) tg[row * NS + s] = acc;
+        const int s0 = 2 * t4;
+        if (on && s0 < NS) tg[row * NS + s0] = c0 + e0;
+        if (on && s0 + 1 < NS) tg[row * NS + s0 + 1] = c1 + e1;
       }
-    });
+    };
+    if constexpr (MDRES) md_rows(Gc, 0, D * C::NFN);  // the resident table, all rows at once
+    else seg_loop<D * C::NFN, units_per_piece(L)>(rg, lane, md_rows);
     if (tid == 0) { PROF_ADD(K_MD, 1, t9); }
     PROF_T(t10);
     cbar();
@@ -1219,8 +1250,10 @@ static int count_pieces() {
 #endif
 template <class C>
 __host__ __device__ constexpr int stages_of(int part) {
-  return C::D == 2 ? (part == 2 ? MHDG_STAGES_2D_POST : MHDG_STAGES)
-                   : (part == 2 ? MHDG_STAGES_3D_POST : (part == 1 ? MHDG_STAGES_3D_PRE : MHDG_STAGES));
+  const int dflt = C::D == 2 ? (part == 2 ? MHDG_STAGES_2D_POST : MHDG_STAGES)
+                             : (part == 2 ? MHDG_STAGES_3D_POST : (part == 1 ? MHDG_STAGES_3D_PRE : MHDG_STAGES));
+  // post part with the resident M^-1 D table: the stages that still fit beside it
+  return part == 2 && post_mdr<C>() && post_stages_mdr<C>() < dflt ? post_stages_mdr<C>() : dflt;
 }
 
 static int g_split = 1;
@@ -1251,7 +1284,8 @@ static size_t stream_smem(const mhdg_disc& g) {
   // 2D: class tables (+ per-macro gphys unless it fits in z) in shared memory; 3D: none
   const size_t cls = C::D == 2 ? (size_t)g.n_grad_cls * TSm<C>::CLS : 0;
   return sizeof(double) * ((size_t)STAGES * ST_DBL + SSm<C, PART>::total + TSm<C>::total +
-                           (PART != 2 ? (cls <= (size_t)C::D * C::n ? cls : 2 * cls) : 0));
+                           (PART != 2 ? (cls <= (size_t)C::D * C::n ? cls : 2 * cls)
+                                      : (post_mdr<C>() ? (size_t)md_table<C>() : 0)));
 }
 
 template <class C, int STAGES, int PART>
