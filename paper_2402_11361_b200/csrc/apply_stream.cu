@@ -650,28 +650,46 @@ __global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 ? 1 : 2)) k_apply_s
           cv[idx] = sum;
         }
       } else {
-        // gphys per gradient class once per macro (in z, dead by now, when it fits; else after the
-        // classes), then one dot per output
-        double* Gp = g.n_grad_cls * TS::CLS <= D * n ? z : Gc + g.n_grad_cls * TS::CLS;
-        for (int idx = tid; idx < g.n_grad_cls * TS::CLS; idx += NCONS) {
-          const int k = idx % D, base = idx - k;
-          double gp = 0.0;
+        // 2D: per sub-element an (NLOC x NQ D) x (NQ D x NS) product on the FP64 tensor cores --
+        // units (K, 8-row tile of a) dealt to the warps; the A fragments are gphys formed on the
+        // fly from the class tables in shared memory and inv_jac, the B fragments the W_vol
+        // results; two accumulator chains (even / odd k-steps).  (3D keeps the FFMA loop: its
+        // class tables are read through L1 and 21 fragment loads in flight do not fit the
+        // register budget -- measured pre 5.02 -> 5.32 ms.)
+        constexpr int DN = D * NS, MT = (NLOC + 7) / 8, KD = NQ * D, KST = (KD + 3) / 4;
+        const int g8 = lane >> 2, t4 = lane & 3;
+        for (int un = warp; un < NSUB * MT; un += NWARP_C) {
+          const int K = un / MT, a = (un - K * MT) * 8 + g8;
+          const bool aok = a < NLOC;
+          const double* G = Gc + gco[K] * TS::CLS + (aok ? a : 0) * D;
+          const double* w = wv + K * NQ * DN + (g8 < NS ? g8 : 0);
+          double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;
+#pragma unroll 2
+          for (int ks = 0; ks < KST; ks += 2) {
 #pragma unroll
-          for (int r2 = 0; r2 < D; ++r2) gp += Gc[base + r2] * ij[r2][k];
-          Gp[idx] = gp;
-        }
-        cbar();
-        for (int idx = tid; idx < NSUB * NLOC * NS; idx += NCONS) {
-          const int s = idx % NS, a = (idx / NS) % NLOC, K = idx / (NS * NLOC);
-          const double* G = Gp + gco[K] * TS::CLS + a * D;
-          const double* w = wv + K * NQ * D * NS + s;
-          double a0 = 0.0, a1 = 0.0;
+            for (int hh = 0; hh < 2; ++hh) {
+              const int kk = 4 * (ks + hh) + t4;
+              if (ks + hh < KST) {
+                const bool kok = kk < KD;
+                const int q = kok ? kk / D : 0, k = kok ? kk - q * D : 0;
+                double af = 0.0;
 #pragma unroll
-          for (int q = 0; q < NQ; ++q) {
+                for (int r = 0; r < D; ++r) {
+                  double ijk = ij[r][0];
 #pragma unroll
-            for (int k = 0; k < D; ++k) ((q & 1) ? a1 : a0) += G[q * NLOC * D + k] * w[(q * D + k) * NS];
+                  for (int k2 = 1; k2 < D; ++k2) ijk = k == k2 ? ij[r][k2] : ijk;
+                  af += G[q * NLOC * D + r] * ijk;
+                }
+                if (!(aok && kok)) af = 0.0;
+                const double bf = (kok && g8 < NS) ? w[q * DN + k * NS] : 0.0;
+                if (hh == 0) dmma_8x8x4(c0, c1, af, bf);
+                else dmma_8x8x4(e0, e1, af, bf);
+              }
+            }
           }
-          cv[idx] = a0 + a1;
+          const int s0 = 2 * t4;
+          if (aok && s0 < NS) cv[(K * NLOC + a) * NS + s0] = c0 + e0;
+          if (aok && s0 + 1 < NS) cv[(K * NLOC + a) * NS + s0 + 1] = c1 + e1;
         }
       }
       if (tid < LTR) {
