@@ -356,6 +356,7 @@ __global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 ? 1 : 2)) k_apply_s
   __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES];
   __shared__ Piece pieces[MAXP];
   __shared__ int npieces;
+  __shared__ double cfls[16];  // z coefficients -(fac / det) area_f n_f,l of the current macro
   using S = SSm<C, PART>;
   using TS = TSm<C>;
   constexpr bool MDRES = PART == 2 && post_mdr<C>();
@@ -505,6 +506,11 @@ __global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 ? 1 : 2)) k_apply_s
     double sc_mine = 0.0;  // trace_face_scale of this thread's face in the final sum
     if (PART != 1 && tid < LTR) sc_mine = __ldg(bk.trace_face_scale + mac * NF + tid / BS);
     PROF_T(t_start);
+    if (PART != 2 && tid >= NCONS - NF * D) {  // the last consumer threads: one z coefficient each
+      const int e = tid - (NCONS - NF * D), f = e / D;
+      cfls[e] = -g.face_fac * __ldg(g.areas + mac * NF + f) / __ldg(g.det + mac) *
+                __ldg(g.normals + (mac * NF + f) * D + e % D);
+    }
     if (PART != 2 && tid < LTR) {
       xl[tid] = x_next;
       const int nm = mac + gridDim.x;
@@ -732,14 +738,13 @@ __global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 ? 1 : 2)) k_apply_s
       if (tid == 0) { PROF_ADD(K_GF, 1, t0); }
       PROF_T(t1);
       cbar();
-      {  // z = A_qq^-1 A_qh x = -(fac/det) sum_f area_f n_f (Gf x_f)
-        const double idet = 1.0 / __ldg(g.det + mac);
+      {  // z = A_qq^-1 A_qh x = -(fac/det) sum_f area_f n_f (Gf x_f); the coefficients were
+         // put in shared memory at the start of the macro (their global loads ran under the Gf phase)
         double cfl[NF][D];
 #pragma unroll
         for (int f = 0; f < NF; ++f)
 #pragma unroll
-          for (int l = 0; l < D; ++l)
-            cfl[f][l] = -g.face_fac * __ldg(g.areas + mac * NF + f) * idet * __ldg(g.normals + (mac * NF + f) * D + l);
+          for (int l = 0; l < D; ++l) cfl[f][l] = cfls[f * D + l];
         for (int idx = tid; idx < n; idx += NCONS) {
           double acc[D] = {};
 #pragma unroll
