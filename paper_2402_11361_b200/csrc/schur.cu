@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(Sch2<D>::NWARP * 32, Sch2<D>::MINB) k_schur2(m
     const bool vol = i < nvol;
     double* W = stg + (size_t)(i % C::NBUF) * dm.stage;
     const double* PM = W + dm.wmax;
-    if (vol) {  // physical gradients of this stage's sub-element class (geometry folded in)
+    if (vol && (!SLICED || i % dm.nsl == 0)) {  // physical gradients of this sub-element's class (geometry folded in)
       const double* gc = g.grad_cls + (size_t)__ldg(g.grad_cls_of + (SLICED ? i / dm.nsl : i)) * nq * nloc * D;
       for (int idx = tid; idx < nq * nloc * D; idx += NT_THREADS) {
         const int k = idx % D, base = idx - k;

@@ -48,6 +48,36 @@ def test_condensed_ops_vs_reference(name):
 
 
 @pytest.mark.parametrize("name", sorted(OP_CASES))
+def test_precond_build_variants_agree(name):
+    """The register-tile Gauss-Jordan sweep (default) and the shared-memory Cholesky +
+    triangular inverse invert the same symmetrised face blocks: inverses equal to rounding,
+    and the sweep's inverse symmetric to rounding."""
+    need_gpu()
+    g = load_golden(name)
+    d = OP_CASES[name]()
+    ob, _ = O.jacobian(d, O.Fields(g["u"], g["q"], g["uhat"]), ctx_of(g, O.Ctx))
+    cond = CondensedSchur.allocate(upload_blocks(d, ob))
+    L = _lib.lib()
+    try:
+        L.mhdg_set_precond_variant(1)
+        chol = block_precond_build(cond).inverse.clone()
+    finally:
+        L.mhdg_set_precond_variant(0)
+    sweep = block_precond_build(cond).inverse
+    scale = float(chol.abs().max())
+    assert float((sweep - chol).abs().max()) < 1e-12 * scale
+    assert float((sweep - sweep.transpose(1, 2)).abs().max()) < 1e-13 * scale
+    # a face block that is not positive definite raises the reference's error class
+    import dataclasses
+
+    from paper_2402_11361_b200.krylov import PreconditionerError
+
+    ob_bad = dataclasses.replace(ob, face_trace_trace=-np.abs(ob.face_trace_trace))
+    with pytest.raises(PreconditionerError):
+        block_precond_build(CondensedSchur.allocate(upload_blocks(d, ob_bad)))
+
+
+@pytest.mark.parametrize("name", sorted(OP_CASES))
 def test_gradient_refresh_vs_oracle(name):
     need_gpu()
     g = load_golden(name)
