@@ -256,10 +256,53 @@ __global__ void __launch_bounds__(Sch2<D>::NWARP * 32, Sch2<D>::MINB) k_schur2(m
           c[nt][0] = (mok && j0 < L) ? crow[j0 * NS] : 0.0;
           c[nt][1] = (mok && j0 + 1 < L) ? crow[(j0 + 1) * NS] : 0.0;
         }
-        // A fragments of this row, T1[m][(q, r') = 4 ks + t4], formed KB k-steps at a time (3D:
-        // the 21 k-steps at once spilled registers inside this loop)
         const double* gp = gph + a * D;
         const double* w = W + (s * NS + r);
+        if constexpr (D == 3) {
+          // 3D: the k index runs over blocks of 4 points, r' inside a block: lane t4 owns point
+          // 4 b + t4 of block b, so every offset is a per-lane base plus a compile-time constant
+          // (no index divisions), a point's gradient entries are loaded once for its D k-steps,
+          // and the lanes' stash / PM rows fall in different banks (SQ = 12, D LP = 12 mod 16)
+          constexpr int NBK = KS / D;
+          const int nqs = SLICED ? min(dm.qs, nq - q0) : nq, nblk = (nqs + 3) / 4;
+          const double* gq0 = gp + (size_t)(q0 + t4) * nloc * D;
+          const double* wq0 = w + t4 * C::SQ;
+          const double* pb0 = PM + (t4 * D) * dm.LP + g8;
+#pragma unroll
+          for (int b = 0; b < NBK; b += 2) {
+            double af[2 * D];
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+              const int bb = b + hh;
+              const bool ok = mok && bb < NBK && 4 * bb + t4 < nqs;
+              double gk[D];
+#pragma unroll
+              for (int k = 0; k < D; ++k) gk[k] = ok ? gq0[4 * bb * nloc * D + k] : 0.0;
+#pragma unroll
+              for (int rp = 0; rp < D; ++rp) {
+                double v = 0.0;
+                if (ok) {
+                  const double* wq = wq0 + 4 * bb * C::SQ + rp * C::SR;
+#pragma unroll
+                  for (int k = 0; k < D; ++k) v += gk[k] * wq[k * C::SK];
+                }
+                af[hh * D + rp] = v;
+              }
+            }
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh)
+              if (b + hh < NBK && b + hh < nblk) {
+#pragma unroll
+                for (int rp = 0; rp < D; ++rp) {
+                  const double* pb = pb0 + (4 * (b + hh) * D + rp) * dm.LP;
+#pragma unroll
+                  for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(c[nt][0], c[nt][1], af[hh * D + rp], pb[nt * 8]);
+                }
+              }
+          }
+        } else {
+        // A fragments of this row, T1[m][(q, r') = 4 ks + t4], formed KB k-steps at a time (3D:
+        // the 21 k-steps at once spilled registers inside this loop)
         constexpr int KB = C::KB;
 #pragma unroll
         for (int kb = 0; kb < KS; kb += KB) {
@@ -284,6 +327,7 @@ __global__ void __launch_bounds__(Sch2<D>::NWARP * 32, Sch2<D>::MINB) k_schur2(m
 #pragma unroll
               for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(c[nt][0], c[nt][1], af[kk], pb[nt * 8]);
             }
+        }
         }
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
