@@ -22,6 +22,7 @@
 namespace mhdg {
 
 constexpr int SCH2_MAXT = 256;
+constexpr int SCH2_MAXPHF = 256;  // nqf x nlocf entries of the face basis table
   // n_sub x nloc entries of the per-CTA node table
 
 template <int D>
@@ -128,6 +129,8 @@ __global__ void __launch_bounds__(Sch2<D>::NWARP * 32, Sch2<D>::MINB) k_schur2(m
   // face-lattice incidence: node g lies in sub-faces finc_T[g][k] as local node finc_a[g][k]
   constexpr int MAXINC = 8;
   __shared__ unsigned char finc_T[64][MAXINC], finc_a[64][MAXINC], finc_n[64];
+  __shared__ double phf[SCH2_MAXPHF];  // phi_face (nqf x nlocf)
+  for (int e = tid; e < nqf * nlocf; e += NT_THREADS) phf[e] = __ldg(g.phi_face + e);
   if (tid == 0) {
     for (int gg = 0; gg < g.Lf && gg < 64; ++gg) finc_n[gg] = 0;
     for (int T = 0; T < g.n_tri; ++T)
@@ -366,7 +369,7 @@ __global__ void __launch_bounds__(Sch2<D>::NWARP * 32, Sch2<D>::MINB) k_schur2(m
             double v = 0.0;
             if (mok && ks < dm.ksf && kq < dm.kf) {
               const int q = kq / D, rp = kq - q * D;
-              v = -WT[q * C::SQF + rp * C::SR + s * NS + r] * __ldg(g.phi_face + q * nlocf + a);
+              v = -WT[q * C::SQF + rp * C::SR + s * NS + r] * phf[q * nlocf + a];
             }
             af[ks] = v;
           }
@@ -396,7 +399,7 @@ int schur2(const mhdg_disc& g, const mhdg_blocks& b, double* S, cudaStream_t st)
   const Sch2Dims dm = Sch2Dims::make<D>(g);
   const size_t bytes = dm.smem_bytes<D>();
   if (!g.grad_cls || g.L > 8 * C::NT || dm.ksv > C::KS || dm.ksf > C::KSF || g.Lf > 64 || bytes > 227 * 1024 ||
-      (D == 2 && g.n_sub * g.nloc > SCH2_MAXT))
+      (D == 2 && g.n_sub * g.nloc > SCH2_MAXT) || g.nqf * g.nlocf > SCH2_MAXPHF)
     return -1;
   auto kern = dm.nsl > 1 ? k_schur2<D, true> : k_schur2<D, false>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
