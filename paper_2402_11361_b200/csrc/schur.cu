@@ -119,9 +119,9 @@ __global__ void __launch_bounds__(Sch2<D>::NWARP * 32, Sch2<D>::MINB) k_schur2(m
   const int nvol = g.n_sub * dm.nsl, nstage = nvol + NF;
   // per (sub-element K, local node a): the macro node and whether K is its first toucher
   // (the tile's S rows start from state_state) -- once per CTA, off the tiles' load chains
-  // (2D only: measured 8.84 -> 8.56 ms at C2; the 3D instantiation is 5% slower with it)
-  __shared__ int tnode[D == 2 ? SCH2_MAXT : 1];
-  for (int e = tid; D == 2 && e < g.n_sub * nloc; e += NWP * 32) {
+  // (measured 8.84 -> 8.56 ms at C2)
+  __shared__ int tnode[SCH2_MAXT];
+  for (int e = tid; e < g.n_sub * nloc; e += NWP * 32) {
     const int node = __ldg(g.sub_conn + e);
     const bool first = __ldg(g.vn_sub + __ldg(g.vn_ptr + node)) / nloc == e / nloc;
     tnode[e] = first ? -1 - node : node;
@@ -241,13 +241,10 @@ __global__ void __launch_bounds__(Sch2<D>::NWARP * 32, Sch2<D>::MINB) k_schur2(m
         // S row of this thread's output row, and where its accumulators start from
         int node;
         bool first;
-        if constexpr (D == 2) {
+        {
           const int tn = tnode[K * nloc + a];
           first = tn < 0;
           node = first ? -1 - tn : tn;
-        } else {
-          node = __ldg(g.sub_conn + K * nloc + a);
-          first = __ldg(g.vn_sub + __ldg(g.vn_ptr + node)) / nloc == K;
         }
         first = first && sl == 0;
         double* srow = Sm + (size_t)(node * NS + s) * n + r;
@@ -399,7 +396,7 @@ int schur2(const mhdg_disc& g, const mhdg_blocks& b, double* S, cudaStream_t st)
   const Sch2Dims dm = Sch2Dims::make<D>(g);
   const size_t bytes = dm.smem_bytes<D>();
   if (!g.grad_cls || g.L > 8 * C::NT || dm.ksv > C::KS || dm.ksf > C::KSF || g.Lf > 64 || bytes > 227 * 1024 ||
-      (D == 2 && g.n_sub * g.nloc > SCH2_MAXT) || g.nqf * g.nlocf > SCH2_MAXPHF)
+      g.n_sub * g.nloc > SCH2_MAXT || g.nqf * g.nlocf > SCH2_MAXPHF)
     return -1;
   auto kern = dm.nsl > 1 ? k_schur2<D, true> : k_schur2<D, false>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
