@@ -92,7 +92,7 @@ struct AsmSmem {
 };
 
 template <int D>
-__host__ __device__ inline AsmSmem<D> asm_smem(const Sz& s0, int nqc, int nfg) {
+__host__ __device__ inline AsmSmem<D> asm_smem(const Sz& s0, int nqc, int nfg, bool jac = true) {
   Sz s = s0;
   s.nq = nqc;  // the volume per-point work arrays hold one chunk of points
   constexpr int NS = D + 2, NF = D + 1;
@@ -120,7 +120,7 @@ __host__ __device__ inline AsmSmem<D> asm_smem(const Sz& s0, int nqc, int nfg) {
   TAKE(tq, s.nq)
   TAKE(prv, s.nq * PRIM)
   TAKE(As, s.nq * D * NS * NS)
-  TAKE(Adu, s.nq * D * NS * NS)
+  TAKE(Adu, jac ? s.nq * D * NS * NS : 0)  // residual-only launches: no Jacobian work arrays
   TAKE(FG, s.nq * NS * D)
   TAKE(Pp, s.nq * D * NS)
   TAKE(sw, s.nq * NS)
@@ -128,8 +128,8 @@ __host__ __device__ inline AsmSmem<D> asm_smem(const Sz& s0, int nqc, int nfg) {
   TAKE(tdps, s.nq * NS)
   TAKE(rs, s.nq * NS)
   TAKE(wts, s.nq)
-  TAKE(W1, asm_dmma<D>() ? s.nq * NS * w1t_ld(s.nloc * NS) : s.nq * s.nloc * W1S<D>())
-  TAKE(csm, asm_dmma<D>() ? s.nloc * NS * csm_ld(s.nloc * NS) : 0)
+  TAKE(W1, !jac ? 0 : asm_dmma<D>() ? s.nq * NS * w1t_ld(s.nloc * NS) : s.nq * s.nloc * W1S<D>())
+  TAKE(csm, jac && asm_dmma<D>() ? s.nloc * NS * csm_ld(s.nloc * NS) : 0)
   const int vol_end = o;
   // ... share their memory with the face work arrays (all sub-faces of nfg faces)
   o = work;
@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(asm_threads<D>(), asm_min_ctas<D>())
   extern __shared__ double sm[];
   constexpr int NS = D + 2, NF = D + 1, E = D + 1;
   const Sz sz = make_sz<D>(g);
-  const AsmSmem<D> o = asm_smem<D>(sz, nqc, nfg);
+  const AsmSmem<D> o = asm_smem<D>(sz, nqc, nfg, want_jac != 0);
   const FlowC fl = make_flow<D>(flow);
   const int mac = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
   const int n = sz.n, L = sz.L, Lf = sz.Lf, nq = sz.nq, nloc = sz.nloc, nqf = sz.nqf, nlocf = sz.nlocf;
@@ -230,6 +230,37 @@ __global__ void __launch_bounds__(asm_threads<D>(), asm_min_ctas<D>())
     tf[idx] = a * (g.face_fac * g.areas[mac * NF + f]);
   }
   __syncthreads();
+  if ((1 + D) * L * L + 2 * D * n <= o.total - o.gph) {
+    // the mass and weak-derivative tables staged through the (still unused) work area: one
+    // round of coalesced loads instead of 4 L dependent L2 reads per entry; the derivative
+    // sums T[r][I][s] are formed once, not once per gradient direction l
+    double *tm = sm + o.gph, *tw = tm + L * L, *sT = tw + D * L * L, *sA = sT + D * n;
+    for (int i = tid; i < L * L; i += nt) tm[i] = g.mass[i];
+    for (int i = tid; i < D * L * L; i += nt) tw[i] = g.weak_deriv[i];
+    __syncthreads();
+    for (int idx = tid; idx < 2 * D * n; idx += nt) {
+      const bool isT = idx < D * n;
+      const int e = isT ? idx : idx - D * n, s = e % NS, I = (e / NS) % L, rl = e / n;
+      const double* row = isT ? tw + ((size_t)rl * L + I) * L : tm + I * L;
+      const double* src = isT ? us + s : qs + rl * n + s;
+      double acc = 0.0;
+      for (int J = 0; J < L; ++J) acc += row[J] * src[J * NS];
+      (isT ? sT : sA)[e] = acc;
+    }
+    __syncthreads();
+    for (int idx = tid; idx < D * n; idx += nt) {
+      const int s = idx % NS, I = (idx / NS) % L, l = idx / n;
+      double b = 0.0;
+#pragma unroll
+      for (int r = 0; r < D; ++r) b += ij[r * D + l] * sT[(r * L + I) * NS + s];
+      double c = 0.0;
+      for (int e = g.vf_ptr[I]; e < g.vf_ptr[I + 1]; ++e) {
+        const int ent = g.vf_ent[e], f = ent / Lf;
+        c -= g.normals[(mac * NF + f) * D + l] * tf[ent * NS + s];
+      }
+      R_grad[(size_t)mac * D * n + idx] = (det * sA[idx] + det * b) + c;
+    }
+  } else {
   for (int idx = tid; idx < D * n; idx += nt) {
     const int s = idx % NS, I = (idx / NS) % L, l = idx / n;
     double a = 0.0;
@@ -250,6 +281,7 @@ __global__ void __launch_bounds__(asm_threads<D>(), asm_min_ctas<D>())
     R_grad[(size_t)mac * D * n + idx] = (det * a + det * b) + c;
   }
 
+  }
   // ---- Jacobian initialisation (mass / PTC term, assembly.py:397-405) -----
   if (want_jac) {
     const double coeff = stage.dt_coeff + (isinf(stage.pseudo_dt) ? 0.0 : 1.0 / stage.pseudo_dt);
@@ -823,16 +855,16 @@ int assemble(const mhdg_disc& g, const mhdg_flow& fl, const mhdg_stage& sg, cons
   // budget per CTA: 227 KB, or the SM's 228 KB (1 KB reserved per CTA) over asm_ctas CTAs
   size_t budget = asm_ctas<D>() > 1 ? (228 * 1024) / asm_ctas<D>() - 1024 : 227 * 1024;
   int nqc = sz.nq;  // largest point chunk whose work arrays fit shared memory
-  while (nqc > 1 && sizeof(double) * asm_smem<D>(sz, nqc, 1).total > budget) nqc = (nqc + 1) / 2;
-  if (sizeof(double) * asm_smem<D>(sz, nqc, 1).total > budget) {  // no chunk fits the shared budget: one CTA per SM
+  while (nqc > 1 && sizeof(double) * asm_smem<D>(sz, nqc, 1, want_jac != 0).total > budget) nqc = (nqc + 1) / 2;
+  if (sizeof(double) * asm_smem<D>(sz, nqc, 1, want_jac != 0).total > budget) {  // no chunk fits the shared budget: one CTA per SM
     budget = 227 * 1024;
     nqc = sz.nq;
-    while (nqc > 1 && sizeof(double) * asm_smem<D>(sz, nqc, 1).total > budget) nqc = (nqc + 1) / 2;
+    while (nqc > 1 && sizeof(double) * asm_smem<D>(sz, nqc, 1, want_jac != 0).total > budget) nqc = (nqc + 1) / 2;
   }
-  if (sizeof(double) * asm_smem<D>(sz, nqc, 1).total > budget || sz.n_tri * sz.Lf > ASM_MAXFLOC) return MHDG_ERR_CONFIG;
+  if (sizeof(double) * asm_smem<D>(sz, nqc, 1, want_jac != 0).total > budget || sz.n_tri * sz.Lf > ASM_MAXFLOC) return MHDG_ERR_CONFIG;
   int nfg = D + 1;  // faces per group of the face phases: as many as fit beside the kept arrays
-  while (nfg > 1 && sizeof(double) * asm_smem<D>(sz, nqc, nfg).total > budget) --nfg;
-  const size_t bytes = sizeof(double) * asm_smem<D>(sz, nqc, nfg).total;
+  while (nfg > 1 && sizeof(double) * asm_smem<D>(sz, nqc, nfg, want_jac != 0).total > budget) --nfg;
+  const size_t bytes = sizeof(double) * asm_smem<D>(sz, nqc, nfg, want_jac != 0).total;
   if (bytes > 48 * 1024) cudaFuncSetAttribute(k_assemble<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   mhdg_blocks bb{};
   mhdg_frozen fzo{}, fzi{};
