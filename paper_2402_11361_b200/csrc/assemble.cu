@@ -32,6 +32,12 @@ namespace mhdg {
 #ifndef MHDG_ASM_CTAS_3D
 #define MHDG_ASM_CTAS_3D 2
 #endif
+#ifndef MHDG_ASM_RES_THREADS_3D
+#define MHDG_ASM_RES_THREADS_3D 320
+#endif
+#ifndef MHDG_ASM_RES_CTAS_3D
+#define MHDG_ASM_RES_CTAS_3D 2
+#endif
 template <int D>
 __host__ __device__ constexpr int asm_threads() { return D == 2 ? 256 : MHDG_ASM_THREADS_3D; }
 // 3D: CTAs per SM the shared-memory budget is cut for (the volume points go in chunks that
@@ -853,7 +859,10 @@ int assemble(const mhdg_disc& g, const mhdg_flow& fl, const mhdg_stage& sg, cons
              const mhdg_frozen* fo, const mhdg_frozen* fi, int* status, cudaStream_t st) {
   const Sz sz = make_sz<D>(g);
   // budget per CTA: 227 KB, or the SM's 228 KB (1 KB reserved per CTA) over asm_ctas CTAs
-  size_t budget = asm_ctas<D>() > 1 ? (228 * 1024) / asm_ctas<D>() - 1024 : 227 * 1024;
+  // 3D residual-only launches: 320 threads (measured at C3: 384 x 2: 13.6 ms, 320 x 2: 11.6, 256 x 2: 12.6, 256 x 3: 14.2)
+  const int ctas = (D == 3 && !want_jac) ? MHDG_ASM_RES_CTAS_3D : asm_ctas<D>();
+  const int threads = (D == 3 && !want_jac) ? MHDG_ASM_RES_THREADS_3D : asm_threads<D>();
+  size_t budget = ctas > 1 ? (228 * 1024) / ctas - 1024 : 227 * 1024;
   int nqc = sz.nq;  // largest point chunk whose work arrays fit shared memory
   while (nqc > 1 && sizeof(double) * asm_smem<D>(sz, nqc, 1, want_jac != 0).total > budget) nqc = (nqc + 1) / 2;
   if (sizeof(double) * asm_smem<D>(sz, nqc, 1, want_jac != 0).total > budget) {  // no chunk fits the shared budget: one CTA per SM
@@ -874,7 +883,7 @@ int assemble(const mhdg_disc& g, const mhdg_flow& fl, const mhdg_stage& sg, cons
     fzo = *fo;
   }
   if (fi) fzi = *fi;
-  k_assemble<D><<<g.n_mac, asm_threads<D>(), bytes, st>>>(g, fl, sg, u, q, uhat, Rg, Ru, Rtl, want_jac, bb, fzo, fzi,
+  k_assemble<D><<<g.n_mac, threads, bytes, st>>>(g, fl, sg, u, q, uhat, Rg, Ru, Rtl, want_jac, bb, fzo, fzi,
                                                      fi ? 1 : 0, status, nqc, nfg);
   int rc = launch_ok();
   if (rc) return rc;
