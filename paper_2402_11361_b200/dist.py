@@ -58,7 +58,10 @@ class Comm:
         if self.world == 1 or (not sends and not recv_bufs):
             return lambda: None
         if self.host_staged:
-            got = self.exchange(sends, {q: b.numel() for q, b in recv_bufs.items()}, next(iter(recv_bufs.values())))
+            like = next(iter(recv_bufs.values()), None)  # a rank may only send (it owns every shared face)
+            if like is None:
+                like = next(iter(sends.values()))
+            got = self.exchange(sends, {q: b.numel() for q, b in recv_bufs.items()}, like)
             for q, b in recv_bufs.items():
                 b.copy_(got[q])
             return lambda: None

@@ -108,6 +108,13 @@ def _worker(rank, world, port, q):
         gcond = O.condense(gblocks)
 
         comm = Comm()
+        # a one-sided exchange (a rank that owns every shared face only sends): rank 0 -> rank 1
+        peer = 1 - rank
+        sends = {peer: torch.arange(3, dtype=torch.float64)} if rank == 0 else {}
+        recv = {peer: torch.empty(3, dtype=torch.float64)} if rank == 1 else {}
+        comm.exchange_start(sends, recv)()
+        if rank == 1:
+            assert recv[peer].tolist() == [0.0, 1.0, 2.0]
         dd = DistDiscretization(gmesh, 1, case.params, bcs=case.boundary_conditions(), comm=comm,
                                 plan_device=torch.device("cpu"))
         part, disc = dd.part, dd.local
