@@ -195,9 +195,9 @@ struct SSm {
   static constexpr int t = y + C::n;
   static constexpr int rfst = t + (PART == 0 ? C::n : 0);
   static constexpr int ftt = rfst + (PRE ? C::LTR : 0);
-  static constexpr int fts = ftt + C::LTR;
+  static constexpr int fts = ftt + (PART == 2 ? 0 : C::LTR);  // post: A_hh x and g stay in registers
   static constexpr int cfgz = fts + (POST ? C::LTR : 0);
-  static constexpr int yf = cfgz + C::LTR;
+  static constexpr int yf = cfgz + (PART == 2 ? 0 : C::LTR);
   static constexpr int wfz = yf + (POST ? C::LTR : 0);
   static constexpr int wf2 = wfz + (PRE ? C::NPF * C::NS : 0);
   static constexpr int vv = wf2 + (POST ? C::NPF * C::NS : 0);  // one 32-double scratch per consumer warp
@@ -504,6 +504,7 @@ __global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 ? 1 : 2)) k_apply_s
 #pragma unroll
       for (int b = 0; b < D; ++b) ij[a][b] = __ldg(g.inv_jac + (size_t)mac * D * D + a * D + b);
     double sc_mine = 0.0;  // trace_face_scale of this thread's face in the final sum
+    double ftt_mine = 0.0, cfgz_mine = 0.0;  // post part: this thread's A_hh x and g entries
     if (PART != 1 && tid < LTR) sc_mine = __ldg(bk.trace_face_scale + mac * NF + tid / BS);
     PROF_T(t_start);
     if (PART != 2 && tid >= NCONS - NF * D) {  // the last consumer threads: one z coefficient each
@@ -849,9 +850,9 @@ __global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 ? 1 : 2)) k_apply_s
         for (int i = tid; i < n; i += NCONS) y[i] = A[i];
       });
       seg_loop<1, 1>(rg, lane, [&](const double* A, int, int) {
-        if (tid < LTR) {
-          ftt[tid] = A[tid];
-          cfgz[tid] = A[LTR + tid];
+        if (tid < LTR) {  // one entry per thread, used by the same thread in the final sum
+          ftt_mine = A[tid];
+          cfgz_mine = A[LTR + tid];
         }
       });
       if (tid == 0) { PROF_ADD(K_Y2, 1, t8); }
@@ -941,7 +942,8 @@ __global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 ? 1 : 2)) k_apply_s
 #pragma unroll
         for (int q = 0; q < NQF; ++q) acc += pfs[q * NLOCF + a] * w[q * NS];
       }
-      y_loc[(size_t)mac * LTR + idx] = ((fts[idx] + sc_mine * acc) + ftt[idx]) + sc_mine * cfgz[idx];
+      y_loc[(size_t)mac * LTR + idx] = ((fts[idx] + sc_mine * acc) + (PART == 2 ? ftt_mine : ftt[idx])) +
+                                       sc_mine * (PART == 2 ? cfgz_mine : cfgz[idx]);
     }
     if (tid == 0) { PROF_ADD(12, 2, t_end); }
   }
