@@ -325,6 +325,19 @@ __global__ void __launch_bounds__(asm_threads<D>(), asm_min_ctas<D>())
     const int* conn = g.sub_conn + K * nloc;
     for (int q0 = 0; q0 < nq; q0 += nqc) {
     const int nc = min(nqc, nq - q0);
+    if constexpr (asm_dmma<D>()) {
+      if (want_jac && q0 == 0) {
+        // the sub-element's block of state_state copied asynchronously into the shared-memory
+        // tile the GEMMs accumulate into (no read-modify-write latency at the end)
+        const int nr = nloc * NS, cld = csm_ld(nr);
+        double* Csm = sm + o.csm;
+        const double* SSm = bk.state_state + (size_t)mac * n * n;
+        for (int idx = tid; idx < nr * nr; idx += nt) {
+          const int cb = idx % nr, rb = idx / nr, t = cb % NS, b = cb / NS, s = rb % NS, a = rb / NS;
+          cp_async8(Csm + rb * cld + cb, SSm + (size_t)(conn[a] * NS + s) * n + conn[b] * NS + t, 8);
+        }
+      }
+    }
     for (int idx = tid; idx < nc * nloc * D; idx += nt) {
       const int k = idx % D, a = (idx / D) % nloc, qq = idx / (D * nloc);
       const double* gr = g.grad_ref + (((size_t)K * nq + q0 + qq) * nloc + a) * D;
@@ -356,7 +369,7 @@ __global__ void __launch_bounds__(asm_threads<D>(), asm_min_ctas<D>())
       const size_t fidx = ((size_t)mac * sz.n_sub + K) * nq + q0 + qq;
       tq[qq] = use_frozen ? fi.supg_tau[fidx] : supg_tau<D>(p, fl, g.h_sub[mac * sz.n_sub + K], inv_sdt);
       if (want_jac) fo.supg_tau[fidx] = tq[qq];
-      wts[qq] = wq[qq] * tq[qq];
+      wts[qq] = sqrt(wq[qq] * tq[qq]);  // W1 rows carry sqrt(w tau): GEMM 2 is then W1s^T W1s
     }
     // physical gradient of u (and the temporal term) at the points, for the strong residual
     for (int idx = tid; idx < nc * (D + 1) * NS; idx += nt) {
@@ -468,19 +481,16 @@ __global__ void __launch_bounds__(asm_threads<D>(), asm_min_ctas<D>())
           const int qq = row / NS, uu = row - qq * NS;
           const double* Aq = As + (qq * D * NS + uu) * NS;
           const double* gq_ = gph + qq * nloc * D;
+          const double swt = wts[qq];
           for (int col = lane; col < nr; col += 32) {
             const int a = col / NS, s = col - a * NS;
             double acc = 0.0;
 #pragma unroll
             for (int k = 0; k < D; ++k) acc += Aq[k * NS * NS + s] * gq_[a * D + k];
-            W1[row * wld + col] = acc;  // W1T[(q, u)][(a, s)]
+            W1[row * wld + col] = acc * swt;  // sqrt(w tau) W1T[(q, u)][(a, s)]
           }
         }
-        if (q0 + nqc >= nq)  // the rows of state_state this sub-element updates, on their way to L1
-          for (int idx = tid; idx < nr * nloc; idx += nt) {
-            const int b = idx % nloc, rb = idx / nloc, s = rb % NS, a = rb / NS;
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(SSm + (size_t)(conn[a] * NS + s) * n + conn[b] * NS));
-          }
+        cp_async_wait_all();  // Csm holds this sub-element's state_state entries (copied since the chunk began)
         __syncthreads();
         // contrib[(a,s),(b,t)] = sum_{(q,u)} (w tau W1T[(q,u)][(a,s)]) W1T[(q,u)][(b,t)]        (GEMM 2)
         //                      + sum_q Y[q][(a,s,t)] phi[q][b],                                 (GEMM 1)
@@ -504,7 +514,7 @@ __global__ void __launch_bounds__(asm_threads<D>(), asm_min_ctas<D>())
             const bool kok = kk < K2;
             const int kc = kok ? kk : 0;
             const double* wr = W1 + kc * wld;
-            const double af = (mok && kok) ? wts[kc / NS] * wr[mc] : 0.0;
+            const double af = (mok && kok) ? wr[mc] : 0.0;
             const double bf = (kok && nok) ? wr[ncol] : 0.0;
             dmma_8x8x4(c0, c1, af, bf);
           }
@@ -513,8 +523,8 @@ __global__ void __launch_bounds__(asm_threads<D>(), asm_min_ctas<D>())
             const int col = ntile * 8 + 2 * t4 + e;
             const double cv = e ? c1 : c0;
             if (mok && col < nr) {
-              Csm[m * cld + col] = q0 == 0 ? cv : Csm[m * cld + col] + cv;
-              if (ntile != mt) Csm[col * cld + m] = q0 == 0 ? cv : Csm[col * cld + m] + cv;
+              Csm[m * cld + col] += cv;
+              if (ntile != mt) Csm[col * cld + m] += cv;
             }
           }
         }
@@ -539,7 +549,7 @@ __global__ void __launch_bounds__(asm_threads<D>(), asm_min_ctas<D>())
               for (int k = 0; k < D; ++k) y += Adu[((qq * D + k) * NS + s) * NS + t] * gph[(qq * nloc + a) * D + k];
               const double w = wq[qq];
               y = -w * y;
-              if (stage.dt_coeff != 0.0) y += stage.dt_coeff * (w * tq[qq]) * W1[(qq * NS + t) * wld + a * NS + s];
+              if (stage.dt_coeff != 0.0) y += stage.dt_coeff * wts[qq] * W1[(qq * NS + t) * wld + a * NS + s];
               af = y;
             }
 #pragma unroll
@@ -560,22 +570,9 @@ __global__ void __launch_bounds__(asm_threads<D>(), asm_min_ctas<D>())
         }
         if (q0 + nqc >= nq) {  // the sub-element's block is complete (summed over the point chunks in Csm)
           __syncthreads();
-          constexpr int UB = 4;  // loads in flight per thread
-          for (int i0 = tid; i0 < nr * nr; i0 += UB * nt) {
-            double* pa[UB];
-            double v[UB];
-#pragma unroll
-            for (int u = 0; u < UB; ++u) {
-              const int idx = i0 + u * nt;
-              if (idx < nr * nr) {
-                const int cb = idx % nr, rb = idx / nr, t = cb % NS, b = cb / NS, s = rb % NS, a = rb / NS;
-                pa[u] = SSm + (size_t)(conn[a] * NS + s) * n + conn[b] * NS + t;
-                v[u] = *pa[u] + Csm[rb * cld + cb];
-              }
-            }
-#pragma unroll
-            for (int u = 0; u < UB; ++u)
-              if (i0 + u * nt < nr * nr) *pa[u] = v[u];
+          for (int idx = tid; idx < nr * nr; idx += nt) {
+            const int cb = idx % nr, rb = idx / nr, t = cb % NS, b = cb / NS, s = rb % NS, a = rb / NS;
+            SSm[(size_t)(conn[a] * NS + s) * n + conn[b] * NS + t] = Csm[rb * cld + cb];
           }
         }
       } else {
@@ -782,10 +779,12 @@ __global__ void __launch_bounds__(asm_threads<D>(), asm_min_ctas<D>())
           const int cl = idx % sz.bs, rl = idx / sz.bs, t = cl % NS, gc = cl / NS, s = rl % NS, gr = rl / NS;
           double ust = 0.0, uss = 0.0, pr = 0.0;
           bool any = false;
+          for (int T = 0; T < sz.n_tri; ++T) any |= floc[T * Lf + gr] >= 0 && floc[T * Lf + gc] >= 0;
+          double* pss = SSm + (size_t)(fvn[gr] * NS + s) * n + fvn[gc] * NS + t;
+          const double ss_old = any ? *pss : 0.0;  // issued before the sums: its latency runs under them
           for (int T = 0; T < sz.n_tri; ++T) {
             const int a = floc[T * Lf + gr], b = floc[T * Lf + gc];
             if (a < 0 || b < 0) continue;
-            any = true;
             const int p0 = (fl_ * sz.n_tri + T) * nqf;
             double ust_T = 0.0, uss_T = 0.0, pr_T = 0.0;
             for (int qq = 0; qq < nqf; ++qq) {
@@ -818,7 +817,7 @@ __global__ void __launch_bounds__(asm_threads<D>(), asm_min_ctas<D>())
           bk.face_state_trace[fboff + idx] = ust;
           bk.face_trace_state[fboff + idx] = tst;
           bk.face_trace_trace[fboff + idx] = ttt;
-          if (any) SSm[(size_t)(fvn[gr] * NS + s) * n + fvn[gc] * NS + t] += uss;
+          if (any) *pss = ss_old + uss;
         }
         __syncthreads();
       }
