@@ -198,17 +198,19 @@ def test_lu_factor_kind_matches_inverse(name):
         assert rel_err(a, b) < tol
 
 
-@pytest.mark.parametrize("p_deg", [2, 3])
-def test_streamed_apply_3d_m1_vs_oracle(p_deg):
-    """C5's 3D m = 1 combos on the streamed apply: p = 2 has an odd W_vol segment per
-    macro (27 x 225 doubles), so every other macro's pieces are copied from one double
-    earlier; p = 3 exercises the point-chunked assembly."""
+@pytest.mark.parametrize("m_sub,p_deg", [(1, 2), (1, 3), (4, 1)])
+def test_streamed_apply_3d_m1_vs_oracle(m_sub, p_deg):
+    """C5's 3D combos without a reference golden on the streamed apply: (1, 2) has an odd
+    W_vol segment per macro (27 x 225 doubles), so every other macro's pieces are copied from
+    one double earlier; (1, 3) exercises the point-chunked assembly; (4, 1) has 64
+    sub-elements and 16 sub-faces per face (the most face-lattice sharing)."""
     need_gpu()
     from golden_cases import TGV
     from paper_2402_11361_b200 import assembly as A
     from paper_2402_11361_b200.mesh import build_cube_mesh
 
-    d = Discretization(build_cube_mesh(TGV.domain, 2, 1, periodic=(True,) * 3), p_deg, TGV.params)
+    d = Discretization(build_cube_mesh(TGV.domain, 2 if m_sub == 1 else 1, m_sub, periodic=(True,) * 3), p_deg,
+                       TGV.params)
     of = perturbed_fields(d, TGV.initial_state, 13)
     ob, _ = O.jacobian(d, of, O.Ctx.steady(2.0))
     gb, _ = A.jacobian(d, A.to_device_fields(d, of.u, of.q, of.uhat), A.StageContext.steady(2.0))
