@@ -497,6 +497,13 @@ __global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 ? 1 : 2)) k_apply_s
   if (PART != 2 && tid < LTR && blockIdx.x < g.n_mac && x)
     x_next = __ldg(x + __ldg(g.gather + (size_t)blockIdx.x * LTR + tid));
 
+  auto zcoef = [&](int m) {  // -(fac / det) area_f n_f,l of macro m for this thread's (f, l)
+    const int e = tid - (NCONS - NF * D), f = e / D;
+    return -g.face_fac * __ldg(g.areas + m * NF + f) / __ldg(g.det + m) * __ldg(g.normals + (m * NF + f) * D + e % D);
+  };
+  double cfl_next = 0.0;
+  if (PART != 2 && tid >= NCONS - NF * D && blockIdx.x < g.n_mac) cfl_next = zcoef(blockIdx.x);
+
   for (int mac = blockIdx.x; mac < g.n_mac; mac += gridDim.x) {
     double ij[D][D];
 #pragma unroll
@@ -507,10 +514,10 @@ __global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 ? 1 : 2)) k_apply_s
     double ftt_mine = 0.0, cfgz_mine = 0.0;  // post part: this thread's A_hh x and g entries
     if (PART != 1 && tid < LTR) sc_mine = __ldg(bk.trace_face_scale + mac * NF + tid / BS);
     PROF_T(t_start);
-    if (PART != 2 && tid >= NCONS - NF * D) {  // the last consumer threads: one z coefficient each
-      const int e = tid - (NCONS - NF * D), f = e / D;
-      cfls[e] = -g.face_fac * __ldg(g.areas + mac * NF + f) / __ldg(g.det + mac) *
-                __ldg(g.normals + (mac * NF + f) * D + e % D);
+    if (PART != 2 && tid >= NCONS - NF * D) {  // the last consumer threads: one z coefficient each,
+      cfls[tid - (NCONS - NF * D)] = cfl_next;      // loaded one macro ahead like the trace entries
+      const int nm = mac + gridDim.x;
+      if (nm < g.n_mac) cfl_next = zcoef(nm);
     }
     if (PART != 2 && tid < LTR) {
       xl[tid] = x_next;
