@@ -611,16 +611,21 @@ __global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 ? 1 : 2)) k_apply_s
             }
             wv[(u0 + pl) * DN + j] = a;
           }
-        } else if (on && j < NS) {
-          const int s = j;
-          const double* w = A + pl * C::NWF + s * NS;
-          const double* v = vw + pi * DN;
+        } else {
+          // out[s] = sum_{l,tt} W[l][s][tt] v[l][tt]: lane (l, s) of the point's DN lanes sums over tt,
+          // the D direction partials meet by shuffles (an NS-term chain instead of D NS)
+          const int s = j % NS, l = j / NS;
           double a = 0.0;
+          if (on) {
+            const double* w = A + pl * C::NWF + l * NS * NS + s * NS;
+            const double* v = vw + pi * DN + l * NS;
 #pragma unroll
-          for (int l = 0; l < D; ++l)
+            for (int tt = 0; tt < NS; ++tt) a += w[tt] * v[tt];
+          }
+          double tot = a;
 #pragma unroll
-            for (int tt = 0; tt < NS; ++tt) a += w[l * NS * NS + tt] * v[l * NS + tt];
-          (second ? wf2 : wfz)[(u0 + pl) * NS + s] = a;
+          for (int ll = 1; ll < D; ++ll) tot += __shfl_down_sync(MHDG_FULL, a, ll * NS);
+          if (on && j < NS) (second ? wf2 : wfz)[(u0 + pl) * NS + s] = tot;
         }
         __syncwarp();
       }
