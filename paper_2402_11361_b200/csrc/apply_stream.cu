@@ -357,6 +357,8 @@ __global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 ? 1 : 2)) k_apply_s
   __shared__ Piece pieces[MAXP];
   __shared__ int npieces;
   __shared__ double cfls[16];  // z coefficients -(fac / det) area_f n_f,l of the current macro
+  // z row of local node b of sub-face T of face f: [0] the volume node, [1] its face-node index
+  __shared__ short fzn[2][C::NF * C::NTRI * C::NLOCF];
   using S = SSm<C, PART>;
   using TS = TSm<C>;
   constexpr bool MDRES = PART == 2 && post_mdr<C>();
@@ -403,6 +405,12 @@ __global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 ? 1 : 2)) k_apply_s
     }
     for (int i = tid; i <= LF; i += nt) Ti[TS::fn_ptr + i] = g.fn_ptr[i];
     for (int i = tid; i < NSUB; i += nt) Ti[TS::gcls_of + i] = g.grad_cls_of[i];
+    for (int i = tid; i < NF * NTRI * NLOCF; i += nt) {
+      const int f = i / (NTRI * NLOCF), tb = i % (NTRI * NLOCF);
+      const int node = g.face_vol_nodes[f * LF + g.tri_conn[tb]];
+      fzn[0][i] = (short)node;
+      fzn[1][i] = (short)g.node_to_face[node];
+    }
     if (PART != 2 && D == 2)  // 3D reads its (larger) class tables through L1
       for (int i = tid; i < g.n_grad_cls * TS::CLS; i += nt) Gc[i] = g.grad_cls[i];
     if (MDRES)  // the M^-1 D table, resident for the whole launch (the post part has no class tables)
@@ -587,8 +595,7 @@ __global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 ? 1 : 2)) k_apply_s
             const int pf = u0 + pl, q = pf % NQF, T = (pf / NQF) % NTRI, f = pf / (NQF * NTRI);
 #pragma unroll
             for (int b = 0; b < NLOCF; ++b) {
-              int node = fvn[f * LF + tconn[T * NLOCF + b]];
-              if (second) node = n2f[node];
+              const int node = fzn[second ? 1 : 0][(f * NTRI + T) * NLOCF + b];  // resolved once per CTA
               a += pfs[q * NLOCF + b] * zs[(l * lstride + node) * NS + tt];
             }
           }
