@@ -360,6 +360,34 @@ __global__ void __launch_bounds__(Sch2<D>::NWARP * 32, Sch2<D>::MINB) k_schur2(m
           const int T = finc_T[gg][e], a = finc_a[gg][e];
           const double* WT = W + T * nqf * C::SQF;
           double af[KSF];
+          if constexpr (D == 3) {
+            // k index by blocks of 4 points, r' inside a block (as the volume stages): lane t4
+            // owns point 4 b + t4, one basis value per point, compile-time offsets, no divisions
+            constexpr int NBF = KSF / D;
+            const int nblk = (nqf + 3) / 4;
+            const double* wq0 = WT + s * NS + r;
+            const double* pb0 = PM + (T * dm.kfp) * dm.LP + g8;
+#pragma unroll
+            for (int bq = 0; bq < NBF; ++bq) {
+              const int q = 4 * bq + t4;
+              const bool ok = mok && bq < nblk && q < nqf;
+              const double ph = ok ? -phf[q * nlocf + a] : 0.0;
+#pragma unroll
+              for (int rp = 0; rp < D; ++rp) af[bq * D + rp] = ok ? wq0[q * C::SQF + rp * C::SR] * ph : 0.0;
+            }
+#pragma unroll
+            for (int bq = 0; bq < NBF; ++bq)
+              if (bq < nblk) {
+                const int qc = min(4 * bq + t4, nqf - 1);  // rows of padded points: any finite row (af = 0)
+#pragma unroll
+                for (int rp = 0; rp < D; ++rp) {
+                  const double* pb = pb0 + (qc * D + rp) * dm.LP;
+#pragma unroll
+                  for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(c[nt][0], c[nt][1], af[bq * D + rp], pb[nt * 8]);
+                }
+              }
+            continue;
+          }
 #pragma unroll
           for (int ks = 0; ks < KSF; ++ks) {
             const int kq = 4 * ks + t4;
