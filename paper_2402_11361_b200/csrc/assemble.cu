@@ -11,10 +11,15 @@
 //   face S), face_state_trace / face_trace_state / face_trace_trace with the
 //   boundary rows, the w*dG/dq stashes and the frozen coefficients
 //   (assembly.py:397-405, 459-475, 556-612).
-// Per-point Jacobian arrays are generated one entry per thread
-// (pointwise.cuh), so the stash stores are coalesced.  Every accumulation runs
-// in a fixed order (sub-element loop, inverse-incidence gathers): results are
-// bitwise reproducible run to run.
+// Per sub-element (and chunk of its quadrature points) the phases between CTA
+// barriers are laid out so that all warps have work: interpolation one component
+// per thread, pointwise Jacobians as (case, point) items whose entry indices are
+// compile-time inside a case (pointwise.cuh folds to straight-line code), the
+// sub-element's state_state contraction as two FP64 tensor-core GEMMs summed in a
+// shared-memory tile (3D), the faces of a group through their per-point phases
+// together with the face blocks formed entry by entry and written once.  Every
+// accumulation runs in a fixed order (sub-element loop, sub-faces ascending,
+// inverse-incidence gathers): results are bitwise reproducible run to run.
 #include <type_traits>
 
 #include "dmma.cuh"

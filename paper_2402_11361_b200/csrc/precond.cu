@@ -1,10 +1,13 @@
 // Face-block preconditioner (krylov.py:194-238).
 //
-// k_precond_build: one CTA per skeleton face: B_f = sum over the face's sides
-// (flat (mac, lf) order, as np.add.at) of P^T face_trace_trace P, with P the
-// side's canonical node permutation (recovered from `gather`); symmetrise,
-// Cholesky (PreconditionerError naming the face if not positive definite),
-// explicit inverse via L^-T L^-1 as cho_solve(., I) does.
+// One CTA per skeleton face: B_f = sum over the face's sides (flat (mac, lf)
+// order, as np.add.at) of P^T face_trace_trace P, with P the side's canonical
+// node permutation (recovered from `gather`), symmetrised and inverted
+// (PreconditionerError naming the face if not positive definite):
+//   k_precond_build_reg (default, face blocks up to 144 dofs): in-place
+//     Gauss-Jordan sweep on register tiles, the pivots are the Cholesky pivots;
+//   k_precond_build (larger blocks, or mhdg_set_precond_variant(1)): Cholesky in
+//     shared memory and the explicit inverse L^-T L^-1 as cho_solve(., I) does.
 // k_precond_apply: y_f = inv_f v_f, one CTA per face.
 #include "common.cuh"
 
