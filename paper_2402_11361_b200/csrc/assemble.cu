@@ -54,26 +54,15 @@ __host__ __device__ constexpr int asm_ctas() { return D == 2 ? 1 : MHDG_ASM_CTAS
 template <int D>
 __host__ __device__ constexpr int asm_min_ctas() { return D == 2 ? 3 : MHDG_ASM_CTAS_3D; }
 
-// The state_state contraction of a sub-element on the FP64 tensor cores (3D; the 2D loop
-// measured faster on the FP64 pipe): W1 is then stored as the K x N matrix
-// W1T[(q, u)][(a, s)] with row stride w1t_ld (= 4 mod 16: conflict-free DMMA fragments) and
-// the sub-element's (nloc NS)^2 block is summed in the shared-memory tile Csm.
-#ifndef MHDG_ASM_DMMA_2D
-#define MHDG_ASM_DMMA_2D 0
-#endif
-template <int D>
-__host__ __device__ constexpr bool asm_dmma() { return D == 3 || MHDG_ASM_DMMA_2D; }
+// The state_state contraction of a sub-element runs on the FP64 tensor cores: W1 is stored as
+// the K x N matrix W1T[(q, u)][(a, s)] with row stride w1t_ld (= 4 mod 16: conflict-free DMMA
+// fragments) and the sub-element's (nloc NS)^2 block is summed in the shared-memory tile Csm.
 __host__ __device__ inline int w1t_ld(int nr) {
   int ld = (nr + 3) & ~3;
   while (ld % 16 != 4) ld += 4;
   return ld;
 }
 __host__ __device__ inline int csm_ld(int nr) { return (nr + 3) & ~1; }
-
-// W1[q][a] blocks (NS x NS) are stored with stride NS*NS + 4 (2D: 20 doubles): the
-// SUPG product reads W1[q][b][u][t] across (b, t) lanes without bank conflicts
-template <int D>
-__host__ __device__ constexpr int W1S() { return (D + 2) * (D + 2) + 4; }
 
 // f(integral_constant<int, c>) for the runtime c in [0, N)
 template <int I, int N>
@@ -139,8 +128,8 @@ __host__ __device__ inline AsmSmem<D> asm_smem(const Sz& s0, int nqc, int nfg, b
   TAKE(tdps, s.nq * NS)
   TAKE(rs, s.nq * NS)
   TAKE(wts, s.nq)
-  TAKE(W1, !jac ? 0 : asm_dmma<D>() ? s.nq * NS * w1t_ld(s.nloc * NS) : s.nq * s.nloc * W1S<D>())
-  TAKE(csm, jac && asm_dmma<D>() ? s.nloc * NS * csm_ld(s.nloc * NS) : 0)
+  TAKE(W1, jac ? s.nq * NS * w1t_ld(s.nloc * NS) : 0)
+  TAKE(csm, jac ? s.nloc * NS * csm_ld(s.nloc * NS) : 0)
   const int vol_end = o;
   // ... share their memory with the face work arrays (all sub-faces of nfg faces)
   o = work;
@@ -330,7 +319,7 @@ __global__ void __launch_bounds__(asm_threads<D>(), asm_min_ctas<D>())
     const int* conn = g.sub_conn + K * nloc;
     for (int q0 = 0; q0 < nq; q0 += nqc) {
     const int nc = min(nqc, nq - q0);
-    if constexpr (asm_dmma<D>()) {
+    {
       if (want_jac && q0 == 0) {
         // the sub-element's block of state_state copied asynchronously into the shared-memory
         // tile the GEMMs accumulate into (no read-modify-write latency at the end)
@@ -478,7 +467,7 @@ __global__ void __launch_bounds__(asm_threads<D>(), asm_min_ctas<D>())
       const int nw = nloc * NS * NS;
       double* SSm = bk.state_state + (size_t)mac * n * n;
       const int nr = nloc * NS;
-      if constexpr (asm_dmma<D>()) {
+      {
         const int wld = w1t_ld(nr), cld = csm_ld(nr);
         double* Csm = sm + o.csm;
         const int warp = tid >> 5, lane = tid & 31, g8 = lane >> 2, t4 = lane & 3, nwarp = nt >> 5;
@@ -580,35 +569,6 @@ __global__ void __launch_bounds__(asm_threads<D>(), asm_min_ctas<D>())
             SSm[(size_t)(conn[a] * NS + s) * n + conn[b] * NS + t] = Csm[rb * cld + cb];
           }
         }
-      } else {
-      for (int idx = tid; idx < nc * nw; idx += nt) {
-        const int qq = idx / nw, e = idx % nw, s = e % NS, uu = (e / NS) % NS, a = e / (NS * NS);
-        double acc = 0.0;
-#pragma unroll
-        for (int k = 0; k < D; ++k) acc += As[((qq * D + k) * NS + uu) * NS + s] * gph[(qq * nloc + a) * D + k];
-        W1[(qq * nloc + a) * W1S<D>() + uu * NS + s] = acc;  // W1[q][a][u][s]
-      }
-      __syncthreads();
-      // contrib[a,s,b,t] = -sum w Adu[k,s,t] gphys[a,k] phi[b] + sum w tau W1[a,u,s] W1[b,u,t]
-      //                    + dt_coeff sum w tau W1[a,t,s] phi[b]          (assembly.py:465-470)
-      for (int idx = tid; idx < nr * nr; idx += nt) {
-        const int t = idx % NS, b = (idx / NS) % nloc, s = (idx / nr) % NS, a = idx / (nr * NS);
-        double acc = 0.0;
-        for (int qq = 0; qq < nc; ++qq) {
-          const double w = wq[qq], wt = w * tq[qq];
-          double y = 0.0;
-#pragma unroll
-          for (int k = 0; k < D; ++k) y += Adu[((qq * D + k) * NS + s) * NS + t] * gph[(qq * nloc + a) * D + k];
-          y = -w * y;
-          if (stage.dt_coeff != 0.0) y += stage.dt_coeff * wt * W1[(qq * nloc + a) * W1S<D>() + t * NS + s];
-          double z = 0.0;
-#pragma unroll
-          for (int uu = 0; uu < NS; ++uu)
-            z += W1[(qq * nloc + a) * W1S<D>() + uu * NS + s] * W1[(qq * nloc + b) * W1S<D>() + uu * NS + t];
-          acc += y * g.phi_vol[(q0 + qq) * nloc + b] + wt * z;
-        }
-        SSm[(size_t)(conn[a] * NS + s) * n + conn[b] * NS + t] += acc;
-      }
       }
     }
     __syncthreads();
