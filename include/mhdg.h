@@ -315,6 +315,56 @@ int mhdg_side_blocks(const mhdg_disc *disc, const mhdg_blocks *blocks, const int
 int mhdg_precond_apply(const mhdg_disc *disc, const double *inv, const double *v, double *y,
                        void *stream);
 
+/* ---- Coupling-recompute representation (B_min: "store only
+   S^-1 and transformation data").  Only the S factors (and the face preconditioner) stay
+   resident; the coupling blocks the trace operator needs (condense.py:91-127) are re-formed
+   from the linearisation state (u, q, uhat) one window of macros at a time.  In every call
+   `blocks_w` (and `frozen_w`, R_*_w) hold the window [mac0, mac0 + count) only, while the
+   factors and all other vectors are whole-mesh arrays; fac->scratch must hold at least
+   `count` macros (n*n doubles each). ---- */
+
+/* mhdg_assemble restricted to the window.  want_jac: 0 residuals only, 1 residuals +
+   blocks + frozen coefficients, 2 couplings only (face blocks, dG/dq stashes and
+   trace_face_scale; no state_state, no frozen output, no residual vectors: R_*_w and
+   frozen_w may be NULL).  No R_trace face sum (call mhdg_face_reduce on whole-mesh data).
+   Status macro indices are window-relative. */
+int mhdg_assemble_window(const mhdg_disc *disc, const mhdg_flow *flow, const mhdg_stage *stage,
+                         const double *u, const double *q, const double *uhat,
+                         double *R_grad_w, double *R_state_w, double *R_trace_loc_w, int want_jac,
+                         const mhdg_blocks *blocks_w, const mhdg_frozen *frozen_w, int mac0, int count,
+                         int *status, void *stream);
+
+/* mhdg_condense for the window's macros: S from blocks_w, factors written at their
+   whole-mesh positions. */
+int mhdg_condense_window(const mhdg_disc *disc, const mhdg_blocks *blocks_w, const mhdg_factors *fac,
+                         int mac0, int count, int *status, void *stream);
+
+/* mhdg_apply_trace_local for the window (y_loc: whole-mesh array, the window's part written). */
+int mhdg_apply_trace_local_window(const mhdg_disc *disc, const mhdg_blocks *blocks_w, const mhdg_factors *fac,
+                                  const double *x, double *y_loc, int mac0, int count, void *stream);
+
+/* Local part of mhdg_condensed_rhs for the window (R_grad, R_state, b_loc whole-mesh);
+   finish with mhdg_face_reduce_axpy(b_loc, R_trace, -1). */
+int mhdg_condensed_rhs_local_window(const mhdg_disc *disc, const mhdg_blocks *blocks_w, const mhdg_factors *fac,
+                                    const double *R_grad, const double *R_state, double *b_loc,
+                                    int mac0, int count, void *stream);
+
+/* mhdg_recover for the window (all vectors whole-mesh). */
+int mhdg_recover_window(const mhdg_disc *disc, const mhdg_blocks *blocks_w, const mhdg_factors *fac,
+                        const double *R_grad, const double *R_state, const double *dtrace,
+                        double *du, double *dq, int mac0, int count, void *stream);
+
+/* sums[f] += P^T face_trace_trace P of the window's sides of every face f (sums:
+   n_faces*bs*bs, zeroed before the first window; windows in ascending order give the
+   bitwise sum mhdg_precond_build forms), then mhdg_precond_build_sums inverts them. */
+int mhdg_face_sum_window(const mhdg_disc *disc, const mhdg_blocks *blocks_w, double *sums, int mac0, int count,
+                         void *stream);
+int mhdg_precond_build_sums(const mhdg_disc *disc, const double *sums, double *inv, int *status, void *stream);
+
+/* y[dof] = face sum of y_loc (as mhdg_face_reduce) + alpha * add[dof] (add may be NULL). */
+int mhdg_face_reduce_axpy(const mhdg_disc *disc, const double *y_loc, const double *add, double alpha,
+                          double *y, void *stream);
+
 /* number of kernel launches issued by this library since load (diagnostics) */
 long long mhdg_launch_count(void);
 

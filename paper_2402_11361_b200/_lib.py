@@ -103,6 +103,15 @@ def lib():
             "mhdg_halo_gather": [C.c_longlong, _dp, _dp, _dp, _dp],
             "mhdg_halo_scatter": [C.c_longlong, _dp, _dp, _dp, C.c_int, _dp],
             "mhdg_face_reduce_remote": [P(Disc), _dp, _dp, _dp, C.c_int, _dp, _dp],
+            "mhdg_assemble_window": [P(Disc), P(Flow), P(Stage), _dp, _dp, _dp, _dp, _dp, _dp, C.c_int, P(Blocks),
+                                     P(Frozen), C.c_int, C.c_int, _dp, _dp],
+            "mhdg_condense_window": [P(Disc), P(Blocks), P(Factors), C.c_int, C.c_int, _dp, _dp],
+            "mhdg_apply_trace_local_window": [P(Disc), P(Blocks), P(Factors), _dp, _dp, C.c_int, C.c_int, _dp],
+            "mhdg_condensed_rhs_local_window": [P(Disc), P(Blocks), P(Factors), _dp, _dp, _dp, C.c_int, C.c_int, _dp],
+            "mhdg_recover_window": [P(Disc), P(Blocks), P(Factors), _dp, _dp, _dp, _dp, _dp, C.c_int, C.c_int, _dp],
+            "mhdg_face_sum_window": [P(Disc), P(Blocks), _dp, C.c_int, C.c_int, _dp],
+            "mhdg_precond_build_sums": [P(Disc), _dp, _dp, _dp, _dp],
+            "mhdg_face_reduce_axpy": [P(Disc), _dp, _dp, C.c_double, _dp, _dp],
         }
         for name, args in sigs.items():
             fn = getattr(L, name)
@@ -157,7 +166,9 @@ EXPORTED = (
     "mhdg_apply_work_size", "mhdg_timeline_begin", "mhdg_timeline_end", "mhdg_icgs", "mhdg_icgs_scratch_size",
     "mhdg_ahat_form", "mhdg_ahat_apply", "mhdg_ahat_apply_local", "mhdg_factor_max_n",
     "mhdg_vec_pass", "mhdg_apply_trace_local_range", "mhdg_halo_gather", "mhdg_halo_scatter",
-    "mhdg_face_reduce_remote",
+    "mhdg_face_reduce_remote", "mhdg_assemble_window", "mhdg_condense_window", "mhdg_apply_trace_local_window",
+    "mhdg_condensed_rhs_local_window", "mhdg_recover_window", "mhdg_face_sum_window", "mhdg_precond_build_sums",
+    "mhdg_face_reduce_axpy",
 )
 # diagnostic A/B knobs (csrc/mhdg_tuning.h; not part of the drop-in ABI)
 TUNING = (

@@ -11,6 +11,7 @@ mhdg_assemble (paper_2402_11361_b200/csrc/assemble.cu).
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -73,8 +74,8 @@ class FrozenCoeffs:
         return c
 
     @classmethod
-    def empty(cls, disc):
-        rm, M, d, ns, nf = disc.rm, disc.n_mac, disc.dim, disc.ns, disc.nf
+    def empty(cls, disc, n_mac: int | None = None):
+        rm, M, d, ns, nf = disc.rm, disc.n_mac if n_mac is None else n_mac, disc.dim, disc.ns, disc.nf
         dev = disc.device.device
         nqt = rm.n_tri * rm.n_quad_face
         z = lambda *s: torch.empty(s, dtype=torch.float64, device=dev)  # noqa: E731
@@ -95,11 +96,13 @@ class LocalBlocks:
         self._c = None
 
     @classmethod
-    def empty(cls, disc):
-        rm, M, d, ns, nf, L, Lf = disc.rm, disc.n_mac, disc.dim, disc.ns, disc.nf, disc.L, disc.Lf
+    def empty(cls, disc, n_mac: int | None = None, with_state_state: bool = True):
+        """Uninitialised blocks for every macro, or (coupling-recompute windows) for `n_mac`
+        macros, optionally without state_state (a NULL pointer in the C struct)."""
+        rm, M, d, ns, nf, L, Lf = disc.rm, disc.n_mac if n_mac is None else n_mac, disc.dim, disc.ns, disc.nf, disc.L, disc.Lf
         dev = disc.device.device
         z = lambda *s: torch.empty(s, dtype=torch.float64, device=dev)  # noqa: E731
-        return cls(disc, state_state=z(M, L * ns, L * ns), face_state_trace=z(M, nf, Lf * ns, Lf * ns),
+        return cls(disc, state_state=z(M, L * ns, L * ns) if with_state_state else None, face_state_trace=z(M, nf, Lf * ns, Lf * ns),
                    face_trace_state=z(M, nf, Lf * ns, Lf * ns), face_trace_trace=z(M, nf, Lf * ns, Lf * ns),
                    wdgdq_vol=z(M, rm.n_sub, rm.n_quad, d, d, ns, ns),
                    wdgdq_face=z(M, nf, rm.n_tri * rm.n_quad_face, d, ns, ns), trace_face_scale=z(M, nf))
@@ -117,7 +120,7 @@ class LocalBlocks:
             c = _lib.Blocks()
             for k in self.KEYS:
                 t = getattr(self, k)
-                assert t.is_contiguous() and t.dtype == torch.float64
+                assert t is None or (t.is_contiguous() and t.dtype == torch.float64)
                 setattr(c, k, _lib.ptr(t))
             self._c = c
         return self._c
@@ -132,6 +135,42 @@ class LocalBlocks:
 
     def to_host(self) -> dict:
         return {k: getattr(self, k).cpu().numpy() for k in self.KEYS}
+
+
+# MHDG_APPLY_REPR=recompute (or jacobian(..., recompute=True)): jacobian() returns the
+# linearisation point instead of assembled blocks (the coupling-recompute representation)
+# macros per window (MHDG_RECOMPUTE_CHUNK, read when the blocks are created)
+RECOMPUTE_CHUNK = 4096
+
+
+class RecomputeBlocks:
+    """The linearisation point (u, q, uhat, stage context) standing in for LocalBlocks under
+    the coupling-recompute representation (B_min; "store
+    only S^-1 and transformation data"): condense() factors S window by window from it and
+    the condensed operator re-forms the coupling blocks of a window of `chunk` macros
+    before each local apply (condense.CondensedRecompute).  Per macro it keeps (1 + d) L ns
+    doubles instead of the blocks' (L ns)^2 + 3 nf (Lf ns)^2 + stashes."""
+
+    def __init__(self, disc, fields: FieldState, ctx: StageContext, chunk: int | None = None):
+        self.disc = disc
+        cp = lambda t: t.detach().clone(memory_format=torch.contiguous_format)  # noqa: E731
+        self.u, self.q, self.uhat = cp(fields.u), cp(fields.q), cp(fields.uhat)
+        self.ctx = ctx
+        chunk = chunk or int(os.environ.get("MHDG_RECOMPUTE_CHUNK", RECOMPUTE_CHUNK))
+        self.chunk = max(1, min(int(chunk), disc.n_mac))
+        self.stage, self._hist_keep = _stage_struct(ctx, disc)
+        self.flow = _flow_struct(disc.params)
+
+    def assemble_window(self, mac0: int, count: int, want_jac: int, window: LocalBlocks, status,
+                        frozen: FrozenCoeffs | None = None, res=(None, None, None)) -> None:
+        """mhdg_assemble_window for macros [mac0, mac0 + count): want_jac = 1 blocks + frozen
+        coefficients + residual vectors (all window-sized), 2 the couplings only."""
+        rc = _lib.lib().mhdg_assemble_window(
+            self.disc.device.c, self.flow, self.stage, _lib.ptr(self.u), _lib.ptr(self.q), _lib.ptr(self.uhat),
+            _lib.ptr(res[0]), _lib.ptr(res[1]), _lib.ptr(res[2]), int(want_jac), window.c,
+            frozen.c_struct() if frozen is not None else None, int(mac0), int(count), _lib.ptr(status),
+            current_stream())
+        _lib.check(rc, "mhdg_assemble_window")
 
 
 def raise_status(status: torch.Tensor, what: str) -> None:
@@ -214,9 +253,17 @@ def residual(disc, fields, ctx, frozen: FrozenCoeffs | None = None):
     return assemble_system(disc, fields, ctx, want_jac=False, frozen=frozen)
 
 
-def jacobian(disc, fields, ctx):
+def jacobian(disc, fields, ctx, recompute: bool | None = None):
+    """Blocks + frozen coefficients (assembly.py:626-629).  With `recompute` (default:
+    MHDG_APPLY_REPR=recompute) the blocks are a RecomputeBlocks -- nothing is assembled
+    here, condense() and the condensed operator form windows of blocks on demand -- and
+    no frozen coefficients are returned."""
     if getattr(disc, "is_distributed", False):
         return disc.jacobian(fields, ctx)
+    if recompute is None:
+        recompute = os.environ.get("MHDG_APPLY_REPR", "matrix_free") == "recompute"
+    if recompute:
+        return RecomputeBlocks(disc, fields, ctx), None
     _, blocks, frozen = assemble_system(disc, fields, ctx, want_jac=True)
     return blocks, frozen
 

@@ -16,7 +16,7 @@ import os
 import torch
 
 from . import _lib
-from .assembly import LocalBlocks, raise_status
+from .assembly import FrozenCoeffs, LocalBlocks, RecomputeBlocks, raise_status
 from .device import current_stream
 
 
@@ -30,7 +30,10 @@ FACTOR_KINDS = {"inverse": 0, "lu": 1}
 # condensed trace block A^{T_i}, formed once per condensation by ltr local applies, then
 # one batched GEMV per apply: B_A bytes; csrc/ahat.cu) or "auto"
 # (matrix-free until ltr applies have run on this condensation -- about what forming the
-# blocks costs -- then stored: never more than twice the cheaper choice in hindsight)
+# blocks costs -- then stored: never more than twice the cheaper choice in hindsight) or
+# "recompute" (B_min: only the S factors and the face
+# preconditioner stay resident; jacobian() returns the linearisation point and the coupling
+# blocks are re-formed window by window for every apply -- CondensedRecompute below)
 APPLY_REPR = os.environ.get("MHDG_APPLY_REPR", "matrix_free")
 
 
@@ -108,8 +111,8 @@ class CondensedSchur:
         self._n_applies = 0
         if APPLY_REPR == "stored":
             self.form_local_operators()
-        elif APPLY_REPR not in ("matrix_free", "auto"):
-            raise ValueError(f"MHDG_APPLY_REPR={APPLY_REPR!r}: expected 'matrix_free', 'stored' or 'auto'")
+        elif APPLY_REPR not in ("matrix_free", "auto", "recompute"):
+            raise ValueError(f"MHDG_APPLY_REPR={APPLY_REPR!r}: expected 'matrix_free', 'stored', 'auto' or 'recompute'")
 
     def note_applies(self, k: int = 1) -> bool:
         """Count applies on this condensation; under MHDG_APPLY_REPR=auto form the stored
@@ -255,6 +258,166 @@ class CondensedSchur:
         return du, dq
 
 
+class CondensedRecompute(CondensedSchur):
+    """CondensedSchur under the coupling-recompute representation (B_min; PAPER.md:550
+    "store only S^-1 and transformation data"): per macro only the packed
+    LU of S, its pivots and the hand-off vectors stay resident -- (L ns)^2 + O(L ns)
+    doubles -- next to the linearisation point (u, q, uhat).  build() walks the macros in
+    windows of `blocks.chunk`: assemble the window's Jacobian blocks, form and factor S
+    into its whole-mesh slot, add the window's trace-trace blocks to the per-face
+    preconditioner sums.  apply_trace / rhs / recover re-form a window's coupling blocks
+    (mhdg_assemble_window, want_jac = 2: face blocks and dG/dq stashes only) right before
+    the window's local kernels read them, so the data the apply streams from HBM per
+    macro drops from B_ref to about B_min plus the window buffer's L2-resident traffic,
+    at the price of the pointwise Jacobians per apply.  Results are those of
+    CondensedSchur bit for bit (same kernels on the same block values)."""
+
+    capturable = True
+
+    def __init__(self, blocks: RecomputeBlocks):
+        disc = blocks.disc
+        n = disc.L * disc.ns
+        dev = disc.device.device
+        n_max = int(_lib.lib().mhdg_factor_max_n(FACTOR_KINDS[FACTOR]))
+        if n > n_max:
+            from .discretization import ConfigError
+
+            raise ConfigError(f"local Schur complement size L*ns = {n} exceeds the {FACTOR!r} factor kernels' "
+                              f"limit n <= {n_max}")
+        packed = int(_lib.lib().mhdg_packed_lu_size(n))
+        lu = torch.empty((disc.n_mac, packed), dtype=torch.float64, device=dev)
+        perm = torch.empty((disc.n_mac, n), dtype=torch.int32, device=dev)
+        scratch = torch.empty((blocks.chunk, n, n), dtype=torch.float64, device=dev)
+        work = torch.empty(int(_lib.lib().mhdg_apply_work_size(disc.device.c)), dtype=torch.float64, device=dev)
+        super().__init__(blocks, lu, perm, scratch, work)
+        self.window = None  # coupling blocks of one window (no state_state)
+        self.precond_inverse = None
+
+    @classmethod
+    def build(cls, blocks: RecomputeBlocks) -> "CondensedRecompute":
+        self = cls(blocks)
+        self.refactor()
+        return self
+
+    def _windows(self):
+        M, C = self.disc.n_mac, self.blocks.chunk
+        return [(m0, min(C, M - m0)) for m0 in range(0, M, C)]
+
+    def refactor(self) -> None:
+        rb, disc = self.blocks, self.disc
+        dd = disc.device
+        dev, C, d, n = dd.device, rb.chunk, disc.dim, disc.L * disc.ns
+        bs = disc.Lf * disc.ns
+        self.window = self.precond_inverse = None
+        win = LocalBlocks.empty(disc, n_mac=C)
+        fro = FrozenCoeffs.empty(disc, n_mac=C)
+        z = lambda k: torch.empty(k, dtype=torch.float64, device=dev)  # noqa: E731
+        res = (z(C * d * n), z(C * n), z(C * disc.nf * bs))
+        sums = torch.zeros((disc.mesh.n_faces, bs, bs), dtype=torch.float64, device=dev)
+        status = dd.status_buffer()
+        L, st = _lib.lib(), current_stream()
+        for m0, cnt in self._windows():
+            rb.assemble_window(m0, cnt, 1, win, status, frozen=fro, res=res)
+            _lib.check(L.mhdg_condense_window(dd.c, win.c, self._fac, m0, cnt, _lib.ptr(status), st),
+                       "mhdg_condense_window")
+            _lib.check(L.mhdg_face_sum_window(dd.c, win.c, _lib.ptr(sums), m0, cnt, st), "mhdg_face_sum_window")
+        raise_status(status, "condense")
+        del fro, res
+        inv = torch.empty_like(sums)
+        _lib.check(L.mhdg_precond_build_sums(dd.c, _lib.ptr(sums), _lib.ptr(inv), _lib.ptr(status), st),
+                   "mhdg_precond_build_sums")
+        self._precond_status = status  # checked when the preconditioner is asked for (krylov.py:194-238)
+        self.precond_inverse = inv
+        del sums
+        self.window = LocalBlocks(disc, **{k: (None if k == "state_state" else getattr(win, k))
+                                           for k in LocalBlocks.KEYS})
+        del win
+        self._n_applies = 0
+
+    def refactor_async(self, status: torch.Tensor) -> None:
+        raise NotImplementedError("the coupling-recompute representation condenses window by window (refactor())")
+
+    def block_precond_build(self):
+        from .krylov import BlockPreconditioner
+
+        raise_status(self._precond_status, "precond_build")
+        return BlockPreconditioner(self, inverse=self.precond_inverse)
+
+    def note_applies(self, k: int = 1) -> bool:
+        if not torch.cuda.is_current_stream_capturing():
+            self._n_applies += k
+        return False
+
+    def form_local_operators(self):
+        raise NotImplementedError("stored local operators need resident blocks (MHDG_APPLY_REPR=stored)")
+
+    def schur_matrix_into_factors(self):
+        raise NotImplementedError("S is formed and factored window by window under the recompute representation")
+
+    def _local(self, call) -> None:
+        """Re-form each window's couplings, then run `call(m0, cnt)` on it (stream order
+        keeps the one window buffer consistent)."""
+        status = None  # the linearisation point was admissible when the factors were built
+        for m0, cnt in self._windows():
+            self.blocks.assemble_window(m0, cnt, 2, self.window, status)
+            call(m0, cnt)
+
+    def apply_trace_local_into(self, x: torch.Tensor) -> None:
+        dd = self.disc.device
+        x = _lib.arg(x, self.disc.n_trace, "x")
+        L, st = _lib.lib(), current_stream()
+        self._local(lambda m0, cnt: _lib.check(
+            L.mhdg_apply_trace_local_window(dd.c, self.window.c, self._fac, _lib.ptr(x), _lib.ptr(self._y_loc),
+                                            m0, cnt, st), "mhdg_apply_trace_local_window"))
+
+    def apply_trace(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        x = _lib.arg(x, self.disc.n_trace, "x")
+        y = torch.empty_like(x) if out is None else out
+        self.note_applies(1)
+        self.apply_trace_local_into(x)
+        _lib.check(_lib.lib().mhdg_face_reduce(self.disc.device.c, _lib.ptr(self._y_loc), _lib.ptr(y),
+                                               current_stream()), "mhdg_face_reduce")
+        return y
+
+    def apply_trace_local(self, x: torch.Tensor) -> torch.Tensor:
+        self.apply_trace_local_into(x)
+        return self._y_loc.view(self.disc.n_mac, self.disc.nf, self.disc.Lf, self.disc.ns).clone()
+
+    def apply_trace_local_range(self, x, mac0, count):
+        raise NotImplementedError("slab ranges are not combined with the recompute representation")
+
+    def rhs(self, res_grad, res_state, res_trace) -> torch.Tensor:
+        disc = self.disc
+        dd = disc.device
+        nu = disc.n_mac * disc.L * disc.ns
+        rg = _lib.arg(res_grad, nu * disc.dim, "R_Q")
+        ru = _lib.arg(res_state, nu, "R_U")
+        rt = _lib.arg(res_trace, disc.n_trace, "R_T")
+        b = torch.empty(disc.n_trace, dtype=torch.float64, device=dd.device)
+        L, st = _lib.lib(), current_stream()
+        self._local(lambda m0, cnt: _lib.check(
+            L.mhdg_condensed_rhs_local_window(dd.c, self.window.c, self._fac, _lib.ptr(rg), _lib.ptr(ru),
+                                              _lib.ptr(self._y_loc), m0, cnt, st), "mhdg_condensed_rhs_local_window"))
+        _lib.check(L.mhdg_face_reduce_axpy(dd.c, _lib.ptr(self._y_loc), _lib.ptr(rt), -1.0, _lib.ptr(b), st),
+                   "mhdg_face_reduce_axpy")
+        return b
+
+    def recover(self, res_grad, res_state, dtrace):
+        disc = self.disc
+        dd = disc.device
+        du = torch.empty((disc.n_mac, disc.L, disc.ns), dtype=torch.float64, device=dd.device)
+        dq = torch.empty((disc.n_mac, disc.dim, disc.L, disc.ns), dtype=torch.float64, device=dd.device)
+        nu = disc.n_mac * disc.L * disc.ns
+        rg = _lib.arg(res_grad, nu * disc.dim, "R_Q")
+        ru = _lib.arg(res_state, nu, "R_U")
+        dt = _lib.arg(dtrace, disc.n_trace, "dtrace")
+        L, st = _lib.lib(), current_stream()
+        self._local(lambda m0, cnt: _lib.check(
+            L.mhdg_recover_window(dd.c, self.window.c, self._fac, _lib.ptr(rg), _lib.ptr(ru), _lib.ptr(dt),
+                                  _lib.ptr(du), _lib.ptr(dq), m0, cnt, st), "mhdg_recover_window"))
+        return du, dq
+
+
 def condense(blocks: LocalBlocks, path: str = "schur") -> CondensedSchur:
     """condense.py:261-266; only the second-layer path runs on the device (the
     one-shot 'standard' path is a CPU oracle in the reference)."""
@@ -264,4 +427,6 @@ def condense(blocks: LocalBlocks, path: str = "schur") -> CondensedSchur:
         from .dist import condense_distributed
 
         return condense_distributed(blocks, path)
+    if isinstance(blocks, RecomputeBlocks):
+        return CondensedRecompute.build(blocks)
     return CondensedSchur.build(blocks)

@@ -196,6 +196,10 @@ __global__ void __launch_bounds__(asm_threads<D>(), asm_min_ctas<D>())
   const double det = g.det[mac];
   const double* ij = g.inv_jac + (size_t)mac * D * D;
   const bool temporal = stage.dt_coeff != 0.0 || stage.hist != nullptr;
+  // want_jac == 2: couplings only (face blocks and dG/dq stashes, what the trace apply streams);
+  // no state_state, no frozen coefficients, no residual vectors (the coupling-recompute
+  // representation re-forms them per apply from (u, q, uhat), condense.py RecomputeBlocks)
+  const bool want_ss = want_jac == 1, want_res = want_jac != 2;
   const double inv_sdt = isinf(stage.supg_dt) ? 0.0 : 1.0 / stage.supg_dt;
 
   double *us = sm + o.us, *qs = sm + o.qs, *uh = sm + o.uh, *td = sm + o.td, *tf = sm + o.tf;
@@ -223,6 +227,7 @@ __global__ void __launch_bounds__(asm_threads<D>(), asm_min_ctas<D>())
       td[i] = stage.hist ? stage.dt_coeff * us[i] + stage.hist[(size_t)mac * n + i] : stage.dt_coeff * us[i];
 
   // ---- gradient equation residual (linear, assembly.py:360-365) -----------
+  if (want_res) {
   for (int idx = tid; idx < sz.ltr; idx += nt) {
     const int s = idx % NS, gg = (idx / NS) % Lf, f = idx / sz.bs;
     double a = 0.0;
@@ -282,8 +287,10 @@ __global__ void __launch_bounds__(asm_threads<D>(), asm_min_ctas<D>())
   }
 
   }
+  }  // want_res
   // ---- Jacobian initialisation (mass / PTC term, assembly.py:397-405) -----
-  if (want_jac) {
+  if (want_jac == 2 && tid < NF) bk.trace_face_scale[mac * NF + tid] = g.bc_kind[mac * NF + tid] > 0 ? 0.0 : 1.0;
+  if (want_ss) {
     const double coeff = stage.dt_coeff + (isinf(stage.pseudo_dt) ? 0.0 : 1.0 / stage.pseudo_dt);
     double* SSm = bk.state_state + (size_t)mac * n * n;
     const int lane = tid & 31, nwarp = nt >> 5;
@@ -320,7 +327,7 @@ __global__ void __launch_bounds__(asm_threads<D>(), asm_min_ctas<D>())
     for (int q0 = 0; q0 < nq; q0 += nqc) {
     const int nc = min(nqc, nq - q0);
     {
-      if (want_jac && q0 == 0) {
+      if (want_ss && q0 == 0) {
         // the sub-element's block of state_state copied asynchronously into the shared-memory
         // tile the GEMMs accumulate into (no read-modify-write latency at the end)
         const int nr = nloc * NS, cld = csm_ld(nr);
@@ -362,7 +369,7 @@ __global__ void __launch_bounds__(asm_threads<D>(), asm_min_ctas<D>())
       wq[qq] = g.w_ref[K * nq + q0 + qq] * det;
       const size_t fidx = ((size_t)mac * sz.n_sub + K) * nq + q0 + qq;
       tq[qq] = use_frozen ? fi.supg_tau[fidx] : supg_tau<D>(p, fl, g.h_sub[mac * sz.n_sub + K], inv_sdt);
-      if (want_jac) fo.supg_tau[fidx] = tq[qq];
+      if (want_ss) fo.supg_tau[fidx] = tq[qq];
       wts[qq] = sqrt(wq[qq] * tq[qq]);  // W1 rows carry sqrt(w tau): GEMM 2 is then W1s^T W1s
     }
     // physical gradient of u (and the temporal term) at the points, for the strong residual
@@ -384,7 +391,7 @@ __global__ void __launch_bounds__(asm_threads<D>(), asm_min_ctas<D>())
     // (most of) a warp and the lanes over points, so the entry indices are compile-time inside
     // a case (the pointwise functions fold to straight-line code).
     {
-      const int ncase = (want_jac ? D * D : 0) + D * NS;
+      const int ncase = (want_jac ? D * D : 0) + (want_res ? D * NS : 0);
       constexpr int nW = D * D * NS * NS;
       for (int idx = tid; idx < ncase * nc; idx += nt) {
         const int cs = idx / nc, qq = idx - cs * nc;
@@ -414,7 +421,7 @@ __global__ void __launch_bounds__(asm_threads<D>(), asm_min_ctas<D>())
             for (int t = 0; t < NS; ++t) {
               const double a = euler_jac<D>(pr, fl, k, sr, t);
               Ar[t] = use_frozen ? fi.supg_jac[fidx + t] : a;
-              if (want_jac) {
+              if (want_ss) {
                 Adr[t] = a + visc_dgdu<D>(pr, fl, qp, k, sr, t);
                 fo.supg_jac[fidx + t] = a;
               }
@@ -425,6 +432,7 @@ __global__ void __launch_bounds__(asm_threads<D>(), asm_min_ctas<D>())
       }
     }
     __syncthreads();
+    if (!want_res) continue;  // couplings only: the stash rows of this chunk are written
     // strong SUPG residual r[q][u] = sum_{k,t} A[k][u][t] gu[k][t] + td, then the per-point
     // residual vector Pp[q][k][s]
     for (int idx = tid; idx < nc * NS; idx += nt) {
@@ -463,7 +471,7 @@ __global__ void __launch_bounds__(asm_threads<D>(), asm_min_ctas<D>())
       }
       cvol[(K * nloc + a) * NS + s] = q0 == 0 ? acc : cvol[(K * nloc + a) * NS + s] + acc;
     }
-    if (want_jac) {
+    if (want_ss) {
       const int nw = nloc * NS * NS;
       double* SSm = bk.state_state + (size_t)mac * n * n;
       const int nr = nloc * NS;
@@ -620,7 +628,7 @@ __global__ void __launch_bounds__(asm_threads<D>(), asm_min_ctas<D>())
 #pragma unroll
       for (int s = 0; s < NS; ++s) {
         fuv[pp * NS + s] = use_frozen ? fi.face_visc_state[pg * NS + s] : a_uh[s];
-        if (want_jac) fo.face_visc_state[pg * NS + s] = a_uh[s];
+        if (want_ss) fo.face_visc_state[pg * NS + s] = a_uh[s];
       }
       fpr[pp] = prim<D>(a_uh, fl);
       fpv[pp] = use_frozen ? prim<D>(fuv + pp * NS, fl) : fpr[pp];
@@ -648,7 +656,7 @@ __global__ void __launch_bounds__(asm_threads<D>(), asm_min_ctas<D>())
                                           : ((sr == t) ? stab_diag<D>(pr, fl, nv, sr) : 0.0);
               fS[(pp * NS + sr) * NS + t] = S;
               if (want_jac) {
-                fo.face_stab[pg * NS * NS + sr * NS + t] = S;
+                if (want_ss) fo.face_stab[pg * NS * NS + sr * NS + t] = S;
                 double an = 0.0;
 #pragma unroll
                 for (int k = 0; k < D; ++k) an += euler_jac<D>(pr, fl, k, sr, t) * nv[k];
@@ -674,7 +682,7 @@ __global__ void __launch_bounds__(asm_threads<D>(), asm_min_ctas<D>())
       }
     }
     __syncthreads();
-    for (int idx0 = tid; idx0 < npt * NS; idx0 += nt) {
+    for (int idx0 = want_res ? tid : npt * NS; idx0 < npt * NS; idx0 += nt) {
       const int s = idx0 / npt, pp = idx0 - s * npt, f = f0 + pp / nqt, idx = pp * NS + s;  // lanes over points
       const int kind = g.bc_kind[mac * NF + f];
       const double* nv = g.normals + (mac * NF + f) * D;
@@ -713,7 +721,7 @@ __global__ void __launch_bounds__(asm_threads<D>(), asm_min_ctas<D>())
     }
     __syncthreads();
     // projections onto the face sub-elements' nodes
-    for (int idx = tid; idx < nfa * sz.n_tri * nlocf * NS; idx += nt) {
+    for (int idx = want_res ? tid : nfa * sz.n_tri * nlocf * NS; idx < nfa * sz.n_tri * nlocf * NS; idx += nt) {
       const int s = idx % NS, a = (idx / NS) % nlocf, T = (idx / (NS * nlocf)) % sz.n_tri,
                 fl_ = idx / (NS * nlocf * sz.n_tri), f = f0 + fl_;
       const int kind = g.bc_kind[mac * NF + f];
@@ -744,7 +752,7 @@ __global__ void __launch_bounds__(asm_threads<D>(), asm_min_ctas<D>())
           const int cl = idx % sz.bs, rl = idx / sz.bs, t = cl % NS, gc = cl / NS, s = rl % NS, gr = rl / NS;
           double ust = 0.0, uss = 0.0, pr = 0.0;
           bool any = false;
-          for (int T = 0; T < sz.n_tri; ++T) any |= floc[T * Lf + gr] >= 0 && floc[T * Lf + gc] >= 0;
+          for (int T = 0; T < sz.n_tri; ++T) any |= want_ss && floc[T * Lf + gr] >= 0 && floc[T * Lf + gc] >= 0;
           double* pss = SSm + (size_t)(fvn[gr] * NS + s) * n + fvn[gc] * NS + t;
           const double ss_old = any ? *pss : 0.0;  // issued before the sums: its latency runs under them
           for (int T = 0; T < sz.n_tri; ++T) {
@@ -791,6 +799,7 @@ __global__ void __launch_bounds__(asm_threads<D>(), asm_min_ctas<D>())
   }
 
   // ---- R_U and the local trace residual ------------------------------------
+  if (!want_res) return;
   for (int idx = tid; idx < n; idx += nt) {
     const int I = idx / NS, s = idx % NS;
     double acc = 0.0;
@@ -842,16 +851,16 @@ int assemble(const mhdg_disc& g, const mhdg_flow& fl, const mhdg_stage& sg, cons
   mhdg_blocks bb{};
   mhdg_frozen fzo{}, fzi{};
   if (want_jac) {
-    if (!b || !fo) return MHDG_ERR_CONFIG;
+    if (!b || (want_jac == 1 && !fo)) return MHDG_ERR_CONFIG;
     bb = *b;
-    fzo = *fo;
+    if (fo) fzo = *fo;
   }
   if (fi) fzi = *fi;
   k_assemble<D><<<g.n_mac, threads, bytes, st>>>(g, fl, sg, u, q, uhat, Rg, Ru, Rtl, want_jac, bb, fzo, fzi,
                                                      fi ? 1 : 0, status, nqc, nfg);
   int rc = launch_ok();
   if (rc) return rc;
-  return face_reduce(g, Rtl, nullptr, 0.0, Rt, st);
+  return Rt ? face_reduce(g, Rtl, nullptr, 0.0, Rt, st) : MHDG_OK;
 }
 
 template int assemble<2>(const mhdg_disc&, const mhdg_flow&, const mhdg_stage&, const double*, const double*,

@@ -17,6 +17,7 @@ template <int D> int assemble(const mhdg_disc&, const mhdg_flow&, const mhdg_sta
                               const double*, double*, double*, double*, double*, int, const mhdg_blocks*,
                               const mhdg_frozen*, const mhdg_frozen*, int*, cudaStream_t);
 template <int D> int precond_build(const mhdg_disc&, const mhdg_blocks&, const double*, double*, int*, cudaStream_t);
+template <int D> int face_sum_window(const mhdg_disc&, const mhdg_blocks&, int, int, double*, cudaStream_t);
 template <int D> int side_blocks(const mhdg_disc&, const mhdg_blocks&, const int*, const int*, int, double*, cudaStream_t);
 int precond_apply(const mhdg_disc&, const double*, const double*, double*, cudaStream_t);
 int face_reduce(const mhdg_disc&, const double*, const double*, double, double*, cudaStream_t);
@@ -145,8 +146,10 @@ int mhdg_apply_trace_local(const mhdg_disc* g, const mhdg_blocks* b, const mhdg_
 
 // views of the macro range [mac0, mac0 + count): every per-macro array offset by mac0
 // (mhdg.h layouts); the factors' scratch is offset only when it holds every macro
+// blocks_resident = false: `b` already holds the window only (the coupling-recompute
+// representation's chunk buffers), so it is not offset
 static void macro_view(const mhdg_disc* g, const mhdg_blocks* b, const mhdg_factors* f, int mac0, int count,
-                       mhdg_disc* gv, mhdg_blocks* bv, mhdg_factors* fv) {
+                       mhdg_disc* gv, mhdg_blocks* bv, mhdg_factors* fv, bool blocks_resident = true) {
   const size_t m0 = (size_t)mac0, d = g->dim, nf = g->nf, ns = g->ns, n = (size_t)g->L * ns;
   const size_t bs = (size_t)g->Lf * ns, ltr = nf * bs, nqf_f = (size_t)g->n_tri * g->nqf;
   *gv = *g;
@@ -163,6 +166,7 @@ static void macro_view(const mhdg_disc* g, const mhdg_blocks* b, const mhdg_fact
   if (gv->u_dir) gv->u_dir += m0 * nf * nqf_f * ns;
   if (gv->source) gv->source += m0 * g->n_sub * g->nq * ns;
   *bv = *b;
+  if (blocks_resident) {
   bv->state_state += m0 * n * n;
   bv->face_state_trace += m0 * nf * bs * bs;
   bv->face_trace_state += m0 * nf * bs * bs;
@@ -170,6 +174,7 @@ static void macro_view(const mhdg_disc* g, const mhdg_blocks* b, const mhdg_fact
   bv->wdgdq_vol += m0 * g->n_sub * g->nq * d * d * ns * ns;
   bv->wdgdq_face += m0 * nf * nqf_f * d * ns * ns;
   bv->trace_face_scale += m0 * nf;
+  }
   *fv = *f;
   fv->lu += m0 * (size_t)mhdg_packed_lu_size((int)n);
   fv->perm += m0 * n;
@@ -186,6 +191,118 @@ int mhdg_apply_trace_local_range(const mhdg_disc* g, const mhdg_blocks* b, const
   mhdg_factors fv;
   macro_view(g, b, f, mac0, count, &gv, &bv, &fv);
   return mhdg_apply_trace_local(&gv, &bv, &fv, x, y_loc + (size_t)mac0 * g->nf * g->Lf * g->ns, st);
+}
+
+// ---- coupling-recompute representation (B_min): window entry points ----
+// `bw` holds the blocks of macros [mac0, mac0 + count) only; factors and vectors are whole-mesh.
+static bool window_ok(const mhdg_disc* g, int mac0, int count) {
+  return mac0 >= 0 && count >= 0 && mac0 + count <= g->n_mac;
+}
+
+int mhdg_assemble_window(const mhdg_disc* g, const mhdg_flow* fl, const mhdg_stage* sg, const double* u, const double* q,
+                         const double* uhat, double* Rg_w, double* Ru_w, double* Rtl_w, int want_jac,
+                         const mhdg_blocks* bw, const mhdg_frozen* fo_w, int mac0, int count, int* status, void* st) {
+  if (!window_ok(g, mac0, count)) return MHDG_ERR_CONFIG;
+  if (count == 0) return MHDG_OK;
+  mhdg_disc gv;
+  mhdg_blocks bv;
+  mhdg_factors fv{}, f0{};
+  const mhdg_blocks b0{};
+  macro_view(g, bw ? bw : &b0, &f0, mac0, count, &gv, &bv, &fv, false);
+  const size_t n = (size_t)g->L * g->ns;
+  mhdg_stage sv = *sg;
+  if (sv.hist) sv.hist += (size_t)mac0 * n;
+  tl_begin(TL_ASSEMBLE, S(st));
+  const double *uw = u + (size_t)mac0 * n, *qw = q + (size_t)mac0 * g->dim * n;
+  const int rc = DISPATCH(g, assemble<2>(gv, *fl, sv, uw, qw, uhat, Rg_w, Ru_w, Rtl_w, nullptr, want_jac, bw ? &bv : nullptr,
+                                         fo_w, nullptr, status, S(st)),
+                          assemble<3>(gv, *fl, sv, uw, qw, uhat, Rg_w, Ru_w, Rtl_w, nullptr, want_jac, bw ? &bv : nullptr,
+                                      fo_w, nullptr, status, S(st)));
+  tl_end(TL_ASSEMBLE, S(st));
+  return rc;
+}
+
+int mhdg_condense_window(const mhdg_disc* g, const mhdg_blocks* bw, const mhdg_factors* f, int mac0, int count,
+                         int* status, void* st) {
+  if (!window_ok(g, mac0, count)) return MHDG_ERR_CONFIG;
+  if (count == 0) return MHDG_OK;
+  if (f->scratch_macros > 0 && f->scratch_macros < count) return MHDG_ERR_CONFIG;
+  mhdg_disc gv;
+  mhdg_blocks bv;
+  mhdg_factors fv;
+  macro_view(g, bw, f, mac0, count, &gv, &bv, &fv, false);
+  fv.scratch_macros = 0;  // the view's scratch holds the whole window
+  int rc = mhdg_schur_matrix(&gv, &bv, &fv, st);
+  if (!rc) rc = mhdg_lu_factor(&gv, &fv, status, st);
+  return rc;
+}
+
+int mhdg_apply_trace_local_window(const mhdg_disc* g, const mhdg_blocks* bw, const mhdg_factors* f, const double* x,
+                                  double* y_loc, int mac0, int count, void* st) {
+  if (!window_ok(g, mac0, count)) return MHDG_ERR_CONFIG;
+  if (count == 0) return MHDG_OK;
+  mhdg_disc gv;
+  mhdg_blocks bv;
+  mhdg_factors fv;
+  macro_view(g, bw, f, mac0, count, &gv, &bv, &fv, false);
+  return mhdg_apply_trace_local(&gv, &bv, &fv, x, y_loc + (size_t)mac0 * g->nf * g->Lf * g->ns, st);
+}
+
+int mhdg_condensed_rhs_local_window(const mhdg_disc* g, const mhdg_blocks* bw, const mhdg_factors* f, const double* Rg,
+                                    const double* Ru, double* b_loc, int mac0, int count, void* st) {
+  if (!window_ok(g, mac0, count)) return MHDG_ERR_CONFIG;
+  if (count == 0) return MHDG_OK;
+  mhdg_disc gv;
+  mhdg_blocks bv;
+  mhdg_factors fv;
+  macro_view(g, bw, f, mac0, count, &gv, &bv, &fv, false);
+  fv.scratch_macros = 0;
+  const size_t n = (size_t)g->L * g->ns, ltr = (size_t)g->nf * g->Lf * g->ns;
+  const double *rg = Rg + (size_t)mac0 * g->dim * n, *ru = Ru + (size_t)mac0 * n;
+  double* bl = b_loc + (size_t)mac0 * ltr;
+  if (g_stream_enabled) {
+    const int rs = cond_stream(gv, bv, fv, true, rg, ru, nullptr, bl, nullptr, nullptr, S(st));
+    if (rs >= 0) return rs;
+  }
+  return DISPATCH(g, rhs_local<2>(gv, bv, fv, rg, ru, bl, S(st)), rhs_local<3>(gv, bv, fv, rg, ru, bl, S(st)));
+}
+
+int mhdg_recover_window(const mhdg_disc* g, const mhdg_blocks* bw, const mhdg_factors* f, const double* Rg,
+                        const double* Ru, const double* dtr, double* du, double* dq, int mac0, int count, void* st) {
+  if (!window_ok(g, mac0, count)) return MHDG_ERR_CONFIG;
+  if (count == 0) return MHDG_OK;
+  mhdg_disc gv;
+  mhdg_blocks bv;
+  mhdg_factors fv;
+  macro_view(g, bw, f, mac0, count, &gv, &bv, &fv, false);
+  fv.scratch_macros = 0;
+  const size_t n = (size_t)g->L * g->ns;
+  const double *rg = Rg + (size_t)mac0 * g->dim * n, *ru = Ru + (size_t)mac0 * n;
+  double *duw = du + (size_t)mac0 * n, *dqw = dq + (size_t)mac0 * g->dim * n;
+  if (g_stream_enabled) {
+    const int rs = cond_stream(gv, bv, fv, false, rg, ru, dtr, nullptr, duw, dqw, S(st));
+    if (rs >= 0) return rs;
+  }
+  return DISPATCH(g, recover<2>(gv, bv, fv, rg, ru, dtr, duw, dqw, S(st)),
+                  recover<3>(gv, bv, fv, rg, ru, dtr, duw, dqw, S(st)));
+}
+
+int mhdg_face_sum_window(const mhdg_disc* g, const mhdg_blocks* bw, double* sums, int mac0, int count, void* st) {
+  if (!window_ok(g, mac0, count)) return MHDG_ERR_CONFIG;
+  if (count == 0) return MHDG_OK;
+  return DISPATCH(g, face_sum_window<2>(*g, *bw, mac0, count, sums, S(st)),
+                  face_sum_window<3>(*g, *bw, mac0, count, sums, S(st)));
+}
+
+int mhdg_precond_build_sums(const mhdg_disc* g, const double* sums, double* inv, int* status, void* st) {
+  const mhdg_blocks none{};
+  return DISPATCH(g, precond_build<2>(*g, none, sums, inv, status, S(st)),
+                  precond_build<3>(*g, none, sums, inv, status, S(st)));
+}
+
+int mhdg_face_reduce_axpy(const mhdg_disc* g, const double* y_loc, const double* add, double alpha, double* y,
+                          void* st) {
+  return face_reduce(*g, y_loc, add, alpha, y, S(st));
 }
 
 int mhdg_halo_gather(long long n, const int* idx, const double* src, double* buf, void* st) {

@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(PRE_THREADS) k_precond_build(mhdg_disc g, mhdg
   }
   for (int side = 0; side < 2; ++side) {
     const int mac = side ? m1 : m0, lf = side ? l1 : l0;
-    if (mac < 0) continue;
+    if (mac < 0 || !b.face_trace_trace) continue;  // no resident blocks: `extra` holds the whole face sum
     const int* gat = g.gather + ((size_t)mac * NF + lf) * bs;
     const double* A = b.face_trace_trace + ((size_t)mac * NF + lf) * bs * bs;
     for (int idx = tid; idx < bs * bs; idx += blockDim.x) {
@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(PRE_THREADS, T <= 5 ? 3 : 1)
   const float rbs = 1.0f / (float)bs;
   for (int side = 0; side < 2; ++side) {
     const int mac = side ? m1 : m0, lf = side ? l1 : l0;
-    if (mac < 0) continue;
+    if (mac < 0 || !b.face_trace_trace) continue;  // no resident blocks: `extra` holds the whole face sum
     const int* gat = g.gather + ((size_t)mac * NF + lf) * bs;
     const double* As = b.face_trace_trace + ((size_t)mac * NF + lf) * bs * bs;
     __syncthreads();  // the previous side's perm reads and block writes are done
@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(PRE_THREADS, T <= 5 ? 3 : 1)
   if (extra) {  // the face's other side, held by another rank, already in canonical order
     const double* ex = extra + (size_t)f * bs * bs;
     for (int r = tid >> 5; r < bs; r += PRE_THREADS / 32)
-      for (int c = tid & 31; c < bs; c += 32) sm[r * ld + c] += __ldg(ex + r * bs + c);
+      for (int c = tid & 31; c < bs; c += 32) sm[r * ld + c] = first ? __ldg(ex + r * bs + c) : sm[r * ld + c] + __ldg(ex + r * bs + c);
     __syncthreads();
   }
   double A[T][T];
@@ -288,6 +288,43 @@ __global__ void k_side_blocks(mhdg_disc g, mhdg_blocks b, const int* __restrict_
     out[(size_t)i * bs * bs + (gat[r] - base) * bs + (gat[c] - base)] = A[idx];
   }
 }
+
+// sums[f] += P^T face_trace_trace[mac, lf] P for the sides (mac, lf) of face f with mac in the
+// window [mac0, mac0 + count), in flat (mac, lf) order; `b` holds the window's blocks only.
+// Windows visited one after the other on a stream leave in sums[f] the same two-term sum
+// as k_precond_build forms (a + b is commutative; the first term is added to zero).
+template <int D>
+__global__ void __launch_bounds__(PRE_THREADS) k_face_sum_window(mhdg_disc g, mhdg_blocks b, int mac0, int count,
+                                                                 double* __restrict__ sums) {
+  constexpr int NS = D + 2, NF = D + 1;
+  const int f = blockIdx.x, bs = g.Lf * NS;
+  int m0 = g.face_macros[2 * f], m1 = g.face_macros[2 * f + 1];
+  int l0 = g.face_locals[2 * f], l1 = g.face_locals[2 * f + 1];
+  if (m1 >= 0 && (m1 * NF + l1) < (m0 * NF + l0)) {
+    int t = m0; m0 = m1; m1 = t;
+    t = l0; l0 = l1; l1 = t;
+  }
+  double* out = sums + (size_t)f * bs * bs;
+  for (int side = 0; side < 2; ++side) {
+    const int mac = side ? m1 : m0, lf = side ? l1 : l0;
+    if (mac < mac0 || mac >= mac0 + count) continue;
+    const int* gat = g.gather + ((size_t)mac * NF + lf) * bs;
+    const double* A = b.face_trace_trace + ((size_t)(mac - mac0) * NF + lf) * bs * bs;
+    for (int idx = threadIdx.x; idx < bs * bs; idx += blockDim.x) {
+      const int r = idx / bs, c = idx - r * bs;
+      out[(gat[r] - f * bs) * bs + (gat[c] - f * bs)] += A[idx];  // each entry hit once per side
+    }
+    __syncthreads();
+  }
+}
+
+template <int D>
+int face_sum_window(const mhdg_disc& g, const mhdg_blocks& b, int mac0, int count, double* sums, cudaStream_t st) {
+  k_face_sum_window<D><<<g.n_faces, PRE_THREADS, 0, st>>>(g, b, mac0, count, sums);
+  return launch_ok();
+}
+template int face_sum_window<2>(const mhdg_disc&, const mhdg_blocks&, int, int, double*, cudaStream_t);
+template int face_sum_window<3>(const mhdg_disc&, const mhdg_blocks&, int, int, double*, cudaStream_t);
 
 template <int D>
 int side_blocks(const mhdg_disc& g, const mhdg_blocks& b, const int* macs, const int* lfs, int count, double* out,
