@@ -141,6 +141,8 @@ def lib():
         L.mhdg_set_lu_l2mode.restype = None
         L.mhdg_set_precond_variant.argtypes = [C.c_int]
         L.mhdg_set_precond_variant.restype = None
+        L.mhdg_set_couplings_kernel.argtypes = [C.c_int]
+        L.mhdg_set_couplings_kernel.restype = None
         L.mhdg_set_schur_variant.argtypes = [C.c_int]
         L.mhdg_set_schur_variant.restype = None
         L.mhdg_icgs.argtypes = [C.c_int, C.c_int, _dp, C.c_longlong, _dp, _dp, _dp, _dp]
@@ -174,6 +176,7 @@ EXPORTED = (
 TUNING = (
     "mhdg_set_schur_variant", "mhdg_set_lu_panel", "mhdg_set_lu_l2mode", "mhdg_set_lu_grid", "mhdg_set_lu_small", "mhdg_set_apply_split",
     "mhdg_set_stream_enabled", "mhdg_set_stream_prefetch", "mhdg_stream_grid", "mhdg_set_precond_variant",
+    "mhdg_set_couplings_kernel",
 )
 
 

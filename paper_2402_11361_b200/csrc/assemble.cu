@@ -824,6 +824,253 @@ __global__ void __launch_bounds__(asm_threads<D>(), asm_min_ctas<D>())
   }
 }
 
+// ---- couplings only (want_jac == 2): the data the trace apply streams ------------------
+// The coupling-recompute representation (B_min) re-forms, per apply and
+// per window of macros, exactly the blocks the apply reads: the w dG/dq stashes (volume and
+// face) and the three face blocks, from (u, uhat) alone -- none of them depends on q.  A
+// dedicated kernel instead of k_assemble's Jacobian path: no residual phases, no
+// state_state, small shared memory (several CTAs per SM).  Every value is formed by the
+// same expressions in the same order as in k_assemble, so the blocks are bitwise equal.
+//   volume: prims at all points, then (case, point) items write tiles of CPL_TP points to
+//     shared memory that leave as linear coalesced stores;
+//   faces, one at a time: prims, (case, point) items for S, d(flux.n)/d uhat and the stash
+//     (tile -> linear stores), then the face blocks as (node pair, row s) items: the
+//     quadrature weight products are formed once per 5 (= NS) entries and each thread
+//     writes NS consecutive doubles of the three blocks.
+constexpr int CPL_THREADS = 256, CPL_TP = 16;
+static int g_couplings_kernel = 1;  // A/B: 0 = k_assemble's couplings-only path
+extern "C" void mhdg_set_couplings_kernel(int on) { g_couplings_kernel = on; }
+
+template <int D>
+struct CplSmem {
+  int us, uh, prv, wq, tile, fpr, fw, wphi, fSd, fK1, ftile, total;
+};
+
+template <int D>
+__host__ __device__ inline CplSmem<D> cpl_smem(const Sz& s) {
+  constexpr int NS = D + 2;
+  constexpr int PRIM = (int)((sizeof(Prim<D>) + 7) / 8);
+  CplSmem<D> m;
+  int o = 0;
+  m.us = o, o += s.n;
+  m.uh = o, o += s.ltr;
+  const int work = o, npv = s.n_sub * s.nq, npf = s.n_tri * s.nqf;
+  m.prv = o, o += npv * PRIM;
+  m.wq = o, o += npv;
+  m.tile = o, o += CPL_TP * D * D * NS * NS;
+  const int vol_end = o;
+  o = work;  // the face arrays (one face at a time) share the volume arrays' memory
+  m.fpr = o, o += npf * PRIM;
+  m.fw = o, o += npf;
+  m.wphi = o, o += npf * s.nlocf;
+  m.fSd = o, o += npf * NS;
+  m.fK1 = o, o += npf * NS * NS;
+  m.ftile = o, o += npf * D * NS * NS;
+  m.total = o > vol_end ? o : vol_end;
+  return m;
+}
+
+template <int D>
+__global__ void __launch_bounds__(CPL_THREADS, 3) k_couplings(mhdg_disc g, mhdg_flow flow, const double* __restrict__ u,
+                                                           const double* __restrict__ uhat, mhdg_blocks bk) {
+  extern __shared__ double sm[];
+  constexpr int NS = D + 2, NF = D + 1, E = D + 1, NW = D * D * NS * NS, NWF = D * NS * NS;
+  const Sz sz = make_sz<D>(g);
+  const CplSmem<D> o = cpl_smem<D>(sz);
+  const FlowC fl = make_flow<D>(flow);
+  const int mac = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+  const int n = sz.n, Lf = sz.Lf, nq = sz.nq, nloc = sz.nloc, nqf = sz.nqf, nlocf = sz.nlocf, bs = sz.bs;
+  const double det = g.det[mac];
+  double *us = sm + o.us, *uh = sm + o.uh, *wq = sm + o.wq, *tile = sm + o.tile;
+  Prim<D>* prv = (Prim<D>*)(sm + o.prv);
+  __shared__ short floc[ASM_MAXFLOC];
+  for (int i = tid; i < sz.n_tri * Lf; i += nt) {
+    const int T = i / Lf, gg = i - T * Lf;
+    short a = -1;
+    for (int k = 0; k < nlocf; ++k)
+      if (g.tri_conn[T * nlocf + k] == gg) a = (short)k;
+    floc[i] = a;
+  }
+  for (int i = tid; i < n; i += nt) us[i] = u[(size_t)mac * n + i];
+  for (int i = tid; i < sz.ltr; i += nt) uh[i] = uhat[g.gather[(size_t)mac * sz.ltr + i]];
+  if (tid < NF) bk.trace_face_scale[mac * NF + tid] = g.bc_kind[mac * NF + tid] > 0 ? 0.0 : 1.0;
+  __syncthreads();
+  // ---- volume stash (assembly.py:459-463) ------------------------------------------------
+  const int npv = sz.n_sub * nq;
+  for (int P = tid; P < npv; P += nt) {
+    const int K = P / nq, qq = P - K * nq;
+    const int* conn = g.sub_conn + K * nloc;
+    const double* ph = g.phi_vol + qq * nloc;
+    double uu[NS];
+#pragma unroll
+    for (int c = 0; c < NS; ++c) {
+      double acc = 0.0;
+      for (int a = 0; a < nloc; ++a) acc += ph[a] * us[conn[a] * NS + c];
+      uu[c] = acc;
+    }
+    prv[P] = prim<D>(uu, fl);
+    wq[P] = g.w_ref[P] * det;
+  }
+  __syncthreads();
+  double* Wv = bk.wdgdq_vol + (size_t)mac * npv * NW;
+  for (int p0 = 0; p0 < npv; p0 += CPL_TP) {
+    const int tp = min(CPL_TP, npv - p0);
+    for (int idx = tid; idx < D * D * tp; idx += nt) {
+      const int cs = idx / tp, pp = idx - cs * tp;
+      const Prim<D> pr = prv[p0 + pp];
+      const double w = wq[p0 + pp];
+      double* Wd = tile + pp * NW + cs * NS * NS;
+      static_switch<D * D>(cs, [&](auto kl) {
+        constexpr int k = decltype(kl)::value / D, l = decltype(kl)::value % D;
+#pragma unroll
+        for (int s = 0; s < NS; ++s)
+#pragma unroll
+          for (int t = 0; t < NS; ++t) Wd[s * NS + t] = w * visc_dgdq<D>(pr, fl, k, l, s, t);
+      });
+    }
+    __syncthreads();
+    double* dst = Wv + (size_t)p0 * NW;
+    for (int i = tid; i < tp * NW; i += nt) dst[i] = tile[i];
+    __syncthreads();
+  }
+  // ---- faces (assembly.py:556-612), one at a time ----------------------------------------
+  Prim<D>* fpr = (Prim<D>*)(sm + o.fpr);
+  double *fw = sm + o.fw, *wphi = sm + o.wphi, *fSd = sm + o.fSd, *fK1 = sm + o.fK1, *ftile = sm + o.ftile;
+  const int nqt = sz.n_tri * nqf;
+  for (int f = 0; f < NF; ++f) {
+    const double fscale = g.face_fac * g.areas[mac * NF + f];
+    for (int pp = tid; pp < nqt; pp += nt) {
+      const int T = pp / nqf, qq = pp - T * nqf;
+      const double* ph = g.phi_face + qq * nlocf;
+      const int* tc = g.tri_conn + T * nlocf;
+      double a_uh[NS];
+#pragma unroll
+      for (int c = 0; c < NS; ++c) {
+        const double* src = uh + f * Lf * NS + c;
+        double acc = 0.0;
+        for (int a = 0; a < nlocf; ++a) acc += ph[a] * src[tc[a] * NS];
+        a_uh[c] = acc;
+      }
+      fpr[pp] = prim<D>(a_uh, fl);
+      const double w = g.w_face_ref[T * nqf + qq] * fscale;
+      fw[pp] = w;
+      for (int a = 0; a < nlocf; ++a) wphi[pp * nlocf + a] = w * ph[a];
+    }
+    __syncthreads();
+    double nv[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) nv[k] = g.normals[(mac * NF + f) * D + k];
+    for (int idx = tid; idx < (NS + D * NS) * nqt; idx += nt) {
+      const int cs = idx / nqt, pp = idx - cs * nqt;
+      const Prim<D> pr = fpr[pp];
+      if (cs < NS) {
+        static_switch<NS>(cs, [&](auto sc) {
+          constexpr int sr = decltype(sc)::value;
+#pragma unroll
+          for (int t = 0; t < NS; ++t) {
+            const double S = (sr == t) ? stab_diag<D>(pr, fl, nv, sr) : 0.0;
+            if (sr == t) fSd[pp * NS + sr] = S;
+            double an = 0.0;
+#pragma unroll
+            for (int k = 0; k < D; ++k) an += euler_jac<D>(pr, fl, k, sr, t) * nv[k];
+            fK1[(pp * NS + sr) * NS + t] = an - S;
+          }
+        });
+      } else {
+        const double w = fw[pp];
+        double* Wf = ftile + pp * NWF + (cs - NS) * NS;
+        static_switch<D * NS>(cs - NS, [&](auto lsc) {
+          constexpr int l = decltype(lsc)::value / NS, sr = decltype(lsc)::value % NS;
+#pragma unroll
+          for (int t = 0; t < NS; ++t) {
+            double acc = 0.0;
+#pragma unroll
+            for (int k = 0; k < D; ++k) acc += visc_dgdq<D>(pr, fl, k, l, sr, t) * nv[k];
+            Wf[t] = w * acc;
+          }
+        });
+      }
+    }
+    __syncthreads();
+    {
+      double* dst = bk.wdgdq_face + ((size_t)mac * NF + f) * nqt * NWF;
+      for (int i = tid; i < nqt * NWF; i += nt) dst[i] = ftile[i];
+    }
+    // face blocks: item (node pair (gr, gc), row s) -> entries (gr NS + s, gc NS + t), t < NS
+    const int kind = g.bc_kind[mac * NF + f];
+    const double* u_w = g.wall_u + (mac * NF + f) * D;
+    double uw2 = 0.0;
+#pragma unroll
+    for (int i = 0; i < D; ++i) uw2 += u_w[i] * u_w[i];
+    const double e_tot = g.wall_e[mac * NF + f] + 0.5 * uw2;
+    const size_t fboff = ((size_t)mac * NF + f) * bs * bs;
+    for (int it = tid; it < Lf * Lf * NS; it += nt) {
+      const int s = it % NS, pair = it / NS, gc = pair % Lf, gr = pair / Lf;
+      double ust[NS], uss = 0.0, pr = 0.0;
+#pragma unroll
+      for (int t = 0; t < NS; ++t) ust[t] = 0.0;
+      for (int T = 0; T < sz.n_tri; ++T) {
+        const int a = floc[T * Lf + gr], b = floc[T * Lf + gc];
+        if (a < 0 || b < 0) continue;
+        const int p0 = T * nqf;
+        double ust_T[NS], uss_T = 0.0, pr_T = 0.0;
+#pragma unroll
+        for (int t = 0; t < NS; ++t) ust_T[t] = 0.0;
+        for (int qq = 0; qq < nqf; ++qq) {
+          const double pq = wphi[(p0 + qq) * nlocf + a] * g.phi_face[qq * nlocf + b];
+          const double* k1 = fK1 + ((p0 + qq) * NS + s) * NS;
+#pragma unroll
+          for (int t = 0; t < NS; ++t) ust_T[t] += pq * k1[t];
+          uss_T += pq * fSd[(p0 + qq) * NS + s];
+          pr_T += pq;
+        }
+#pragma unroll
+        for (int t = 0; t < NS; ++t) ust[t] += ust_T[t];
+        uss += uss_T;
+        pr += pr_T;
+      }
+      const size_t row = fboff + (size_t)(gr * NS + s) * bs + gc * NS;
+#pragma unroll
+      for (int t = 0; t < NS; ++t) {
+        // S is diagonal here (no frozen coefficients): the off-diagonal sums of k_assemble are
+        // sums of pq * 0.0, i.e. +0.0
+        const double uss_t = (s == t) ? uss : 0.0;
+        double tst, ttt;
+        if (kind == 0) {
+          tst = -uss_t;
+          ttt = -ust[t];
+        } else {
+          double khh = (s == t) ? 1.0 : 0.0, kuu = 0.0;
+          if (kind == 2) {
+            if (t == 0 && s >= 1 && s <= D) khh = -u_w[s - 1];
+            if (t == 0 && s == E) khh = -e_tot;
+            if (s == 0 && t == 0) kuu = -1.0;
+          } else if (kind == 3) {
+            if (s == t && (s == 0 || s == E)) kuu = -1.0;
+          }
+          tst = pr * kuu;
+          ttt = pr * khh;
+        }
+        bk.face_state_trace[row + t] = ust[t];
+        bk.face_trace_state[row + t] = tst;
+        bk.face_trace_trace[row + t] = ttt;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <int D>
+static int launch_couplings(const mhdg_disc& g, const mhdg_flow& fl, const double* u, const double* uhat,
+                            const mhdg_blocks& b, cudaStream_t st) {
+  const Sz sz = make_sz<D>(g);
+  const size_t bytes = sizeof(double) * cpl_smem<D>(sz).total;
+  if (bytes > 227 * 1024 || sz.n_tri * sz.Lf > ASM_MAXFLOC) return -1;
+  if (bytes > 48 * 1024) cudaFuncSetAttribute(k_couplings<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  k_couplings<D><<<g.n_mac, CPL_THREADS, bytes, st>>>(g, fl, u, uhat, b);
+  return launch_ok();
+}
+
 int face_reduce(const mhdg_disc&, const double*, const double*, double, double*, cudaStream_t);
 
 template <int D>
@@ -831,6 +1078,10 @@ int assemble(const mhdg_disc& g, const mhdg_flow& fl, const mhdg_stage& sg, cons
              const double* uhat, double* Rg, double* Ru, double* Rtl, double* Rt, int want_jac, const mhdg_blocks* b,
              const mhdg_frozen* fo, const mhdg_frozen* fi, int* status, cudaStream_t st) {
   const Sz sz = make_sz<D>(g);
+  if (want_jac == 2 && b && !fi && g_couplings_kernel) {  // couplings only: the dedicated kernel when it fits
+    const int rc2 = launch_couplings<D>(g, fl, u, uhat, *b, st);
+    if (rc2 >= 0) return rc2;
+  }
   // budget per CTA: 227 KB, or the SM's 228 KB (1 KB reserved per CTA) over asm_ctas CTAs
   // 3D residual-only launches: 320 threads (measured at C3: 384 x 2: 13.6 ms, 320 x 2: 11.6, 256 x 2: 12.6, 256 x 3: 14.2)
   const int ctas = (D == 3 && !want_jac) ? MHDG_ASM_RES_CTAS_3D : asm_ctas<D>();

@@ -51,6 +51,10 @@ void mhdg_set_stream_prefetch(int pieces);
    face blocks up to 144 dofs; 1: the shared-memory Cholesky + triangular inverse. */
 void mhdg_set_precond_variant(int v);
 
+/* Couplings-only assembly (mhdg_assemble_window, want_jac = 2): 1 (default) the dedicated
+   k_couplings kernel; 0: k_assemble's Jacobian path with the state_state work skipped. */
+void mhdg_set_couplings_kernel(int on);
+
 /* CTAs per launch of the last streamed pre/post kernel (diagnostics). */
 int mhdg_stream_grid(void);
 

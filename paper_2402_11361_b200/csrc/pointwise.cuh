@@ -90,7 +90,9 @@ __device__ __forceinline__ double euler_jac(const Prim<D>& p, const FlowC& f, in
     }
     return i == k ? f.g1 : 0.0;
   }
-  if (t == 0) return p.v[k] * (f.g1 * p.kin - p.H);
+  // explicit FMA: left to the compiler, g1 kin - H is contracted in some inlining contexts and
+  // not in others (k_assemble vs k_couplings differed by 1 ulp in this entry)
+  if (t == 0) return p.v[k] * __fma_rn(f.g1, p.kin, -p.H);
   if (t <= D) {
     const int j = t - 1;
     return (j == k ? p.H : 0.0) - f.g1 * p.v[j] * p.v[k];

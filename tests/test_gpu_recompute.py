@@ -47,10 +47,22 @@ def _c2_patch():
     return disc, f, A.StageContext.steady(1.0)
 
 
-@pytest.mark.parametrize("cfg,chunk", [("tgv", 20), ("tgv", 48), ("c2", 48)])
-def test_recompute_equals_resident_bitwise(cfg, chunk):
+@pytest.fixture
+def couplings_kernel(request):
+    """The couplings-only assembly: the dedicated k_couplings kernel (1, default) or
+    k_assemble's Jacobian path with the state_state work skipped (0)."""
+    from paper_2402_11361_b200 import _lib
+
+    _lib.lib().mhdg_set_couplings_kernel(request.param)
+    yield request.param
+    _lib.lib().mhdg_set_couplings_kernel(1)
+
+
+@pytest.mark.parametrize("couplings_kernel", [1, 0], indirect=True)
+@pytest.mark.parametrize("cfg,chunk", [("tgv", 20), ("tgv", 48), ("c2", 48), ("tgv13", 7)])
+def test_recompute_equals_resident_bitwise(cfg, chunk, couplings_kernel):
     need_gpu()
-    disc, f, ctx = _tgv() if cfg == "tgv" else _c2_patch()
+    disc, f, ctx = _c2_patch() if cfg == "c2" else (_tgv(1, 1, 3) if cfg == "tgv13" else _tgv())
     res = A.residual(disc, f, ctx)
     blocks, _ = A.jacobian(disc, f, ctx, recompute=False)
     ref = CondensedSchur.build(blocks)
