@@ -274,10 +274,11 @@ class CondensedRecompute(CondensedSchur):
 
     capturable = True
 
-    def __init__(self, blocks: RecomputeBlocks):
+    def __init__(self, blocks: RecomputeBlocks, precond: bool = True):
         disc = blocks.disc
         n = disc.L * disc.ns
         dev = disc.device.device
+        self._with_precond = precond  # False: the face preconditioner is built when first asked for
         n_max = int(_lib.lib().mhdg_factor_max_n(FACTOR_KINDS[FACTOR]))
         if n > n_max:
             from .discretization import ConfigError
@@ -294,8 +295,8 @@ class CondensedRecompute(CondensedSchur):
         self.precond_inverse = None
 
     @classmethod
-    def build(cls, blocks: RecomputeBlocks) -> "CondensedRecompute":
-        self = cls(blocks)
+    def build(cls, blocks: RecomputeBlocks, precond: bool = True) -> "CondensedRecompute":
+        self = cls(blocks, precond)
         self.refactor()
         return self
 
@@ -313,21 +314,21 @@ class CondensedRecompute(CondensedSchur):
         fro = FrozenCoeffs.empty(disc, n_mac=C)
         z = lambda k: torch.empty(k, dtype=torch.float64, device=dev)  # noqa: E731
         res = (z(C * d * n), z(C * n), z(C * disc.nf * bs))
-        sums = torch.zeros((disc.mesh.n_faces, bs, bs), dtype=torch.float64, device=dev)
+        sums = None
+        if self._with_precond:
+            sums = torch.zeros((disc.mesh.n_faces, bs, bs), dtype=torch.float64, device=dev)
         status = dd.status_buffer()
         L, st = _lib.lib(), current_stream()
         for m0, cnt in self._windows():
             rb.assemble_window(m0, cnt, 1, win, status, frozen=fro, res=res)
             _lib.check(L.mhdg_condense_window(dd.c, win.c, self._fac, m0, cnt, _lib.ptr(status), st),
                        "mhdg_condense_window")
-            _lib.check(L.mhdg_face_sum_window(dd.c, win.c, _lib.ptr(sums), m0, cnt, st), "mhdg_face_sum_window")
+            if sums is not None:
+                _lib.check(L.mhdg_face_sum_window(dd.c, win.c, _lib.ptr(sums), m0, cnt, st), "mhdg_face_sum_window")
         raise_status(status, "condense")
         del fro, res
-        inv = torch.empty_like(sums)
-        _lib.check(L.mhdg_precond_build_sums(dd.c, _lib.ptr(sums), _lib.ptr(inv), _lib.ptr(status), st),
-                   "mhdg_precond_build_sums")
-        self._precond_status = status  # checked when the preconditioner is asked for (krylov.py:194-238)
-        self.precond_inverse = inv
+        if sums is not None:
+            self._invert_face_sums(sums)
         del sums
         self.window = LocalBlocks(disc, **{k: (None if k == "state_state" else getattr(win, k))
                                            for k in LocalBlocks.KEYS})
@@ -337,9 +338,27 @@ class CondensedRecompute(CondensedSchur):
     def refactor_async(self, status: torch.Tensor) -> None:
         raise NotImplementedError("the coupling-recompute representation condenses window by window (refactor())")
 
+    def _invert_face_sums(self, sums: torch.Tensor) -> None:
+        dd = self.disc.device
+        status = dd.status_buffer()
+        inv = torch.empty_like(sums)
+        _lib.check(_lib.lib().mhdg_precond_build_sums(dd.c, _lib.ptr(sums), _lib.ptr(inv), _lib.ptr(status),
+                                                      current_stream()), "mhdg_precond_build_sums")
+        self._precond_status = status  # checked when the preconditioner is asked for (krylov.py:194-238)
+        self.precond_inverse = inv
+
     def block_precond_build(self):
         from .krylov import BlockPreconditioner
 
+        if self.precond_inverse is None:  # built lazily: one couplings pass for the trace-trace blocks
+            disc = self.disc
+            bs = disc.Lf * disc.ns
+            sums = torch.zeros((disc.mesh.n_faces, bs, bs), dtype=torch.float64, device=disc.device.device)
+            L, st = _lib.lib(), current_stream()
+            self._local(lambda m0, cnt: _lib.check(
+                L.mhdg_face_sum_window(disc.device.c, self.window.c, _lib.ptr(sums), m0, cnt, st),
+                "mhdg_face_sum_window"))
+            self._invert_face_sums(sums)
         raise_status(self._precond_status, "precond_build")
         return BlockPreconditioner(self, inverse=self.precond_inverse)
 

@@ -86,6 +86,10 @@ def test_recompute_equals_resident_bitwise(cfg, chunk, couplings_kernel):
     pre, pre0 = cond.block_precond_build(), K.block_precond_build(ref)
     assert torch.equal(pre.inverse, pre0.inverse)
     assert torch.equal(pre(x), pre0(x))
+    # the preconditioner built lazily from a couplings pass (CondensedRecompute.build(precond=False))
+    lazy = CondensedRecompute.build(rb, precond=False)
+    assert lazy.precond_inverse is None
+    assert torch.equal(lazy.block_precond_build().inverse, pre0.inverse)
 
 
 def test_dirk33_step_with_recompute_representation(monkeypatch):

@@ -6,7 +6,12 @@ free-stream far field at the truncated outer radius; free stream + U(-1e-3,
 macros, ~1.8 MB of device data per macro) need two or more GPUs (slabs of
 shells, bench.py / dist.py); one GPU holds the inner ~12.
 
-    python tools/c4_run.py [N_R]   (default 12)
+    python tools/c4_run.py [N_R] [max_newton]   (defaults 12, 5)
+
+With MHDG_APPLY_REPR=recompute (the coupling-recompute representation, B_min: only the S
+factors and the face preconditioner resident) the full 32 shells fit one B200:
+    MHDG_APPLY_REPR=recompute python tools/c4_run.py 32
+Each Newton step appends one JSON line to gpurun_out/c4_steps.jsonl as it completes.
 """
 import json
 import os
@@ -25,6 +30,9 @@ from paper_2402_11361_b200.discretization import Discretization  # noqa: E402
 from paper_2402_11361_b200.mesh import build_sphere_ogrid_mesh  # noqa: E402
 
 n_r = int(sys.argv[1]) if len(sys.argv) > 1 else 12
+max_newton = int(sys.argv[2]) if len(sys.argv) > 2 else 5
+REPR = os.environ.get("MHDG_APPLY_REPR", "matrix_free")
+STEPS = os.path.join(ROOT, "gpurun_out", "c4_steps.jsonl")
 w = 1.15 ** np.arange(32)
 r_full = 0.5 + 19.5 * np.concatenate([[0.0], np.cumsum(w)]) / np.sum(w)
 case = SphereCase()
@@ -51,13 +59,27 @@ t_setup = time.perf_counter() - t0
 log("device state")
 ptc = S.PtcState(dtau=1.0, tau_init=1.0, tau_max=1e8)
 t0 = time.perf_counter()
-st = S.newton_solve(disc, f, A.StageContext.steady(), max_newton=5, ptc=ptc, abs_tol=1e-10, rel_tol=1e-10,
-                    log=lambda s: log(f"newton {s.iterations}: residual {s.residuals[-1]:.4e}, "
-                                      f"krylov {s.krylov_iterations}"))
+
+
+def on_step(s):
+    log(f"newton {s.iterations}: residual {s.residuals[-1]:.4e}, krylov {s.krylov_iterations}")
+    os.makedirs(os.path.dirname(STEPS), exist_ok=True)
+    with open(STEPS, "a") as fh:
+        fh.write(json.dumps({"n_macros": disc.n_mac, "representation": REPR, "newton": s.iterations,
+                             "residuals": [float(r) for r in s.residuals], "dtau": [float(x) for x in s.dtau],
+                             "krylov_iterations": s.krylov_iterations, "krylov_matvecs": s.krylov_matvecs,
+                             "seconds_since_start": time.perf_counter() - t0,
+                             "timings": {k: float(v) for k, v in s.timings.items()},
+                             "peak_device_GB": torch.cuda.max_memory_allocated() / 1e9}) + "\n")
+
+
+st = S.newton_solve(disc, f, A.StageContext.steady(), max_newton=max_newton, ptc=ptc, abs_tol=1e-10, rel_tol=1e-10,
+                    log=on_step)
 torch.cuda.synchronize()
 t_run = time.perf_counter() - t0
 print(json.dumps({
     "config": f"C4 inner {n_r} of 32 shells (r_out {r_full[n_r]:.3f}), 24 x 48 cells, m=2, p=2",
+    "representation": REPR,
     "n_macros": disc.n_mac, "n_trace_dofs": disc.n_trace, "newton": st.iterations,
     "krylov_iterations": st.krylov_iterations, "krylov_matvecs": st.krylov_matvecs,
     "residuals": [float(r) for r in st.residuals], "dtau": [float(x) for x in st.dtau],

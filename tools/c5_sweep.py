@@ -27,7 +27,7 @@ from paper_2402_11361_b200 import _lib  # noqa: E402
 from paper_2402_11361_b200 import assembly as A  # noqa: E402
 from paper_2402_11361_b200 import stepper as S  # noqa: E402
 from paper_2402_11361_b200.cases import TgvCase  # noqa: E402
-from paper_2402_11361_b200.condense import CondensedSchur  # noqa: E402
+from paper_2402_11361_b200.condense import CondensedRecompute, CondensedSchur  # noqa: E402
 from paper_2402_11361_b200.discretization import Discretization  # noqa: E402
 from paper_2402_11361_b200.mesh import build_cube_mesh  # noqa: E402
 from paper_2402_11361_b200.partition import partition_mesh  # noqa: E402
@@ -36,6 +36,9 @@ from paper_2402_11361_b200.refmacro import lattice_size  # noqa: E402
 N1D = int(sys.argv[1]) if len(sys.argv) > 1 else 32
 BUDGET = 160e9  # bytes of device data per GPU (of ~180 GB HBM3e)
 CHUNK = 4096  # macros of Schur scratch
+# MHDG_C5_REPR=recompute: the coupling-recompute representation (B_min: only the S factors
+# resident, the couplings re-formed per window of CHUNK macros before each local apply)
+REPR = os.environ.get("MHDG_C5_REPR", "matrix_free")
 L_ = _lib.lib()
 
 
@@ -47,6 +50,8 @@ def bytes_per_macro(m, p):
     nq, nqf = (p + 1) ** d, (p + 1) ** (d - 1)
     n = L * ns
     blk = n * n + 3 * nf * (Lf * ns) ** 2 + m**d * nq * d * d * ns * ns + nf * m ** (d - 1) * nqf * d * ns * ns
+    if REPR == "recompute":  # the factor and the vectors; the blocks exist for CHUNK macros only
+        return 8 * (1.1 * n * n + 8 * n + 30 * L * ns) + 8.0 * (blk + 3 * n * n) * CHUNK / (6 * N1D**3)
     return 8 * (blk + 1.1 * n * n + 8 * n + 20 * L * ns)  # + the packed factor (scratch: CHUNK macros)
 
 
@@ -73,30 +78,44 @@ def run(m, p):
     f = A.to_device_fields(disc, u, np.zeros((disc.n_mac, 3, disc.L, 5)), uhat)
     f.q = A.gradient_refresh(disc, f.u, f.uhat)
     ctx = A.StageContext.dirk_stage(0.01, S.DirkTableau.dirk33().d[0], 0, [], f.u)
-    blocks, _ = A.jacobian(disc, f, ctx)
-    del f
-    torch.cuda.synchronize()
-    cond = CondensedSchur.allocate(blocks, scratch_macros=CHUNK)
-    st = disc.device.status_buffer()
-    cond.refactor_async(st)
-    torch.cuda.synchronize()
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
     e0, e1 = ev(), ev()
-    e0.record()
-    cond.refactor_async(st)
-    e1.record()
-    torch.cuda.synchronize()
-    A.raise_status(st, "condense")
+    if REPR == "recompute":
+        blocks = A.RecomputeBlocks(disc, f, ctx, chunk=CHUNK)
+        del f
+        cond = CondensedRecompute.build(blocks, precond=False)  # assembly + Schur + LU, window by window
+        torch.cuda.synchronize()
+        e0.record()
+        cond.refactor()
+        e1.record()
+        torch.cuda.synchronize()
+    else:
+        blocks, _ = A.jacobian(disc, f, ctx)
+        del f
+        torch.cuda.synchronize()
+        cond = CondensedSchur.allocate(blocks, scratch_macros=CHUNK)
+        st = disc.device.status_buffer()
+        cond.refactor_async(st)
+        torch.cuda.synchronize()
+        e0.record()
+        cond.refactor_async(st)
+        e1.record()
+        torch.cuda.synchronize()
+        A.raise_status(st, "condense")
     t_cond = e0.elapsed_time(e1) / 1e3
     xs = torch.as_tensor(np.random.default_rng(1).standard_normal((4, disc.n_trace)), device="cuda")
     y = torch.empty(disc.n_trace, dtype=torch.float64, device="cuda")
     for i in range(3):
         cond.apply_trace(xs[i], out=y)
     torch.cuda.synchronize()
-    with _lib.Timeline(64) as tl:
+    with _lib.Timeline(4096) as tl:
         cond.apply_trace(xs[0], out=y)
         torch.cuda.synchronize()
-    paths = sorted(k for k in tl.ms if k.startswith("apply"))
+    paths = sorted(k for k in tl.ms if k.startswith("apply") or (REPR == "recompute" and k == "assemble"))
+    out["representation"] = REPR
+    if REPR == "recompute":
+        out["condense_includes"] = "window-wise Jacobian assembly + Schur + LU"
+        out["apply_kernels_ms"] = {k: tl.ms[k] for k in paths}
     e0.record()
     for i in range(200):
         cond.apply_trace(xs[i & 3], out=y)
