@@ -25,6 +25,7 @@
 #include "dmma.cuh"
 #include "local_ops.cuh"
 #include "pointwise.cuh"
+#include "tma.cuh"
 
 namespace mhdg {
 
@@ -832,40 +833,46 @@ __global__ void __launch_bounds__(asm_threads<D>(), asm_min_ctas<D>())
 // state_state, small shared memory (several CTAs per SM).  Every value is formed by the
 // same expressions in the same order as in k_assemble, so the blocks are bitwise equal.
 //   volume: prims at all points, then (case, point) items write tiles of CPL_TP points to
-//     shared memory that leave as linear coalesced stores;
-//   faces, one at a time: prims, (case, point) items for S, d(flux.n)/d uhat and the stash
-//     (tile -> linear stores), then the face blocks as (node pair, row s) items: the
-//     quadrature weight products are formed once per 5 (= NS) entries and each thread
-//     writes NS consecutive doubles of the three blocks.
+//     shared memory that leave as one bulk copy (cp.async.bulk shared -> global) each;
+//   faces, all of them per phase: prims, (case, point) items for S, d(flux.n)/d uhat (rows
+//     padded for 16-byte loads, the diagonal of S in the pad) and the stash, then the face
+//     blocks as (face, node pair, row s) items: the quadrature weight products are formed
+//     once per NS entries and each thread writes NS consecutive doubles of the three blocks.
 constexpr int CPL_THREADS = 256, CPL_TP = 16;
 static int g_couplings_kernel = 1;  // A/B: 0 = k_assemble's couplings-only path
 extern "C" void mhdg_set_couplings_kernel(int on) { g_couplings_kernel = on; }
 
 template <int D>
 struct CplSmem {
-  int us, uh, prv, wq, tile, fpr, fw, wphi, fSd, fK1, ftile, total;
+  int us, uh, phf, prv, wq, tile, fpr, fw, wphi, fK1, total;
 };
+
+// rows of d(flux.n)/d uhat padded to K1P doubles with the diagonal of S in the last slot:
+// a row is K1P / 2 16-byte loads
+template <int D>
+__host__ __device__ constexpr int cpl_k1p() { return (D + 2 + 2) & ~1; }
 
 template <int D>
 __host__ __device__ inline CplSmem<D> cpl_smem(const Sz& s) {
-  constexpr int NS = D + 2;
+  constexpr int NS = D + 2, NF = D + 1;
   constexpr int PRIM = (int)((sizeof(Prim<D>) + 7) / 8);
   CplSmem<D> m;
   int o = 0;
   m.us = o, o += s.n;
   m.uh = o, o += s.ltr;
-  const int work = o, npv = s.n_sub * s.nq, npf = s.n_tri * s.nqf;
+  m.phf = o, o += s.nqf * s.nlocf;
+  o = (o + 1) & ~1;
+  const int work = o, npv = s.n_sub * s.nq, npf = NF * s.n_tri * s.nqf;
+  m.tile = o, o += CPL_TP * D * D * NS * NS;  // first: 16-byte aligned for the bulk stores
+  o = (o + 1) & ~1;
   m.prv = o, o += npv * PRIM;
   m.wq = o, o += npv;
-  m.tile = o, o += CPL_TP * D * D * NS * NS;
   const int vol_end = o;
-  o = work;  // the face arrays (one face at a time) share the volume arrays' memory
+  o = work;  // the face arrays (all faces) share the volume arrays' memory
+  m.fK1 = o, o += npf * NS * cpl_k1p<D>();
   m.fpr = o, o += npf * PRIM;
   m.fw = o, o += npf;
   m.wphi = o, o += npf * s.nlocf;
-  m.fSd = o, o += npf * NS;
-  m.fK1 = o, o += npf * NS * NS;
-  m.ftile = o, o += npf * D * NS * NS;
   m.total = o > vol_end ? o : vol_end;
   return m;
 }
@@ -873,15 +880,15 @@ __host__ __device__ inline CplSmem<D> cpl_smem(const Sz& s) {
 template <int D>
 __global__ void __launch_bounds__(CPL_THREADS, 3) k_couplings(mhdg_disc g, mhdg_flow flow, const double* __restrict__ u,
                                                            const double* __restrict__ uhat, mhdg_blocks bk) {
-  extern __shared__ double sm[];
-  constexpr int NS = D + 2, NF = D + 1, E = D + 1, NW = D * D * NS * NS, NWF = D * NS * NS;
+  extern __shared__ __align__(16) double sm[];
+  constexpr int NS = D + 2, NF = D + 1, E = D + 1, NW = D * D * NS * NS, NWF = D * NS * NS, K1P = cpl_k1p<D>();
   const Sz sz = make_sz<D>(g);
   const CplSmem<D> o = cpl_smem<D>(sz);
   const FlowC fl = make_flow<D>(flow);
   const int mac = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
   const int n = sz.n, Lf = sz.Lf, nq = sz.nq, nloc = sz.nloc, nqf = sz.nqf, nlocf = sz.nlocf, bs = sz.bs;
   const double det = g.det[mac];
-  double *us = sm + o.us, *uh = sm + o.uh, *wq = sm + o.wq, *tile = sm + o.tile;
+  double *us = sm + o.us, *uh = sm + o.uh, *phf = sm + o.phf, *wq = sm + o.wq, *tile = sm + o.tile;
   Prim<D>* prv = (Prim<D>*)(sm + o.prv);
   __shared__ short floc[ASM_MAXFLOC];
   for (int i = tid; i < sz.n_tri * Lf; i += nt) {
@@ -893,6 +900,7 @@ __global__ void __launch_bounds__(CPL_THREADS, 3) k_couplings(mhdg_disc g, mhdg_
   }
   for (int i = tid; i < n; i += nt) us[i] = u[(size_t)mac * n + i];
   for (int i = tid; i < sz.ltr; i += nt) uh[i] = uhat[g.gather[(size_t)mac * sz.ltr + i]];
+  for (int i = tid; i < nqf * nlocf; i += nt) phf[i] = g.phi_face[i];
   if (tid < NF) bk.trace_face_scale[mac * NF + tid] = g.bc_kind[mac * NF + tid] > 0 ? 0.0 : 1.0;
   __syncthreads();
   // ---- volume stash (assembly.py:459-463) ------------------------------------------------
@@ -913,6 +921,9 @@ __global__ void __launch_bounds__(CPL_THREADS, 3) k_couplings(mhdg_disc g, mhdg_
   }
   __syncthreads();
   double* Wv = bk.wdgdq_vol + (size_t)mac * npv * NW;
+  // a tile leaves as one bulk copy (TMA) issued by thread 0 when its global range is 16-byte
+  // aligned (NW odd in 3D: every tile of CPL_TP points is, if the macro's base is)
+  const bool bulk = (((size_t)mac * npv * NW) & 1) == 0 && ((CPL_TP * NW) & 1) == 0;
   for (int p0 = 0; p0 < npv; p0 += CPL_TP) {
     const int tp = min(CPL_TP, npv - p0);
     for (int idx = tid; idx < D * D * tp; idx += nt) {
@@ -928,135 +939,151 @@ __global__ void __launch_bounds__(CPL_THREADS, 3) k_couplings(mhdg_disc g, mhdg_
           for (int t = 0; t < NS; ++t) Wd[s * NS + t] = w * visc_dgdq<D>(pr, fl, k, l, s, t);
       });
     }
-    __syncthreads();
     double* dst = Wv + (size_t)p0 * NW;
-    for (int i = tid; i < tp * NW; i += nt) dst[i] = tile[i];
-    __syncthreads();
-  }
-  // ---- faces (assembly.py:556-612), one at a time ----------------------------------------
-  Prim<D>* fpr = (Prim<D>*)(sm + o.fpr);
-  double *fw = sm + o.fw, *wphi = sm + o.wphi, *fSd = sm + o.fSd, *fK1 = sm + o.fK1, *ftile = sm + o.ftile;
-  const int nqt = sz.n_tri * nqf;
-  for (int f = 0; f < NF; ++f) {
-    const double fscale = g.face_fac * g.areas[mac * NF + f];
-    for (int pp = tid; pp < nqt; pp += nt) {
-      const int T = pp / nqf, qq = pp - T * nqf;
-      const double* ph = g.phi_face + qq * nlocf;
-      const int* tc = g.tri_conn + T * nlocf;
-      double a_uh[NS];
-#pragma unroll
-      for (int c = 0; c < NS; ++c) {
-        const double* src = uh + f * Lf * NS + c;
-        double acc = 0.0;
-        for (int a = 0; a < nlocf; ++a) acc += ph[a] * src[tc[a] * NS];
-        a_uh[c] = acc;
+    if (bulk && ((tp * NW) & 1) == 0) {
+      fence_proxy_async();  // this thread's tile writes -> visible to the async proxy
+      __syncthreads();
+      if (tid == 0) {
+        bulk_s2g(dst, tile, (uint32_t)(tp * NW * sizeof(double)));
+        bulk_commit();
+        bulk_wait_read0();  // the tile has been read: the next pass may overwrite it
       }
-      fpr[pp] = prim<D>(a_uh, fl);
-      const double w = g.w_face_ref[T * nqf + qq] * fscale;
-      fw[pp] = w;
-      for (int a = 0; a < nlocf; ++a) wphi[pp * nlocf + a] = w * ph[a];
+      __syncthreads();
+    } else {
+      __syncthreads();
+      for (int i = tid; i < tp * NW; i += nt) dst[i] = tile[i];
+      __syncthreads();
     }
-    __syncthreads();
+  }
+  // ---- faces (assembly.py:556-612), all of them per phase ---------------------------------
+  Prim<D>* fpr = (Prim<D>*)(sm + o.fpr);
+  double *fw = sm + o.fw, *wphi = sm + o.wphi, *fK1 = sm + o.fK1;
+  const int nqt = sz.n_tri * nqf, npf = NF * nqt;
+  for (int pp = tid; pp < npf; pp += nt) {
+    const int f = pp / nqt, r = pp - f * nqt, T = r / nqf, qq = r - T * nqf;
+    const double* ph = phf + qq * nlocf;
+    const int* tc = g.tri_conn + T * nlocf;
+    double a_uh[NS];
+#pragma unroll
+    for (int c = 0; c < NS; ++c) {
+      const double* src = uh + f * Lf * NS + c;
+      double acc = 0.0;
+      for (int a = 0; a < nlocf; ++a) acc += ph[a] * src[tc[a] * NS];
+      a_uh[c] = acc;
+    }
+    fpr[pp] = prim<D>(a_uh, fl);
+    const double w = g.w_face_ref[T * nqf + qq] * (g.face_fac * g.areas[mac * NF + f]);
+    fw[pp] = w;
+    for (int a = 0; a < nlocf; ++a) wphi[pp * nlocf + a] = w * ph[a];
+  }
+  __syncthreads();
+  for (int idx = tid; idx < (NS + D * NS) * npf; idx += nt) {
+    const int cs = idx / npf, pp = idx - cs * npf, f = pp / nqt;
+    const Prim<D> pr = fpr[pp];
     double nv[D];
 #pragma unroll
     for (int k = 0; k < D; ++k) nv[k] = g.normals[(mac * NF + f) * D + k];
-    for (int idx = tid; idx < (NS + D * NS) * nqt; idx += nt) {
-      const int cs = idx / nqt, pp = idx - cs * nqt;
-      const Prim<D> pr = fpr[pp];
-      if (cs < NS) {
-        static_switch<NS>(cs, [&](auto sc) {
-          constexpr int sr = decltype(sc)::value;
+    if (cs < NS) {
+      static_switch<NS>(cs, [&](auto sc) {
+        constexpr int sr = decltype(sc)::value;
+        double* row = fK1 + (pp * NS + sr) * K1P;
 #pragma unroll
-          for (int t = 0; t < NS; ++t) {
-            const double S = (sr == t) ? stab_diag<D>(pr, fl, nv, sr) : 0.0;
-            if (sr == t) fSd[pp * NS + sr] = S;
-            double an = 0.0;
+        for (int t = 0; t < NS; ++t) {
+          const double S = (sr == t) ? stab_diag<D>(pr, fl, nv, sr) : 0.0;
+          if (sr == t) row[NS] = S;
+          double an = 0.0;
 #pragma unroll
-            for (int k = 0; k < D; ++k) an += euler_jac<D>(pr, fl, k, sr, t) * nv[k];
-            fK1[(pp * NS + sr) * NS + t] = an - S;
-          }
-        });
-      } else {
-        const double w = fw[pp];
-        double* Wf = ftile + pp * NWF + (cs - NS) * NS;
-        static_switch<D * NS>(cs - NS, [&](auto lsc) {
-          constexpr int l = decltype(lsc)::value / NS, sr = decltype(lsc)::value % NS;
+          for (int k = 0; k < D; ++k) an += euler_jac<D>(pr, fl, k, sr, t) * nv[k];
+          row[t] = an - S;
+        }
+      });
+    } else {
+      const double w = fw[pp];
+      // the point's stash rows straight to global memory (NS consecutive doubles per item;
+      // 5% of the macro's bytes)
+      double* Wf = bk.wdgdq_face + ((size_t)mac * npf + pp) * NWF + (cs - NS) * NS;
+      static_switch<D * NS>(cs - NS, [&](auto lsc) {
+        constexpr int l = decltype(lsc)::value / NS, sr = decltype(lsc)::value % NS;
 #pragma unroll
-          for (int t = 0; t < NS; ++t) {
-            double acc = 0.0;
+        for (int t = 0; t < NS; ++t) {
+          double acc = 0.0;
 #pragma unroll
-            for (int k = 0; k < D; ++k) acc += visc_dgdq<D>(pr, fl, k, l, sr, t) * nv[k];
-            Wf[t] = w * acc;
-          }
-        });
+          for (int k = 0; k < D; ++k) acc += visc_dgdq<D>(pr, fl, k, l, sr, t) * nv[k];
+          Wf[t] = w * acc;
+        }
+      });
+    }
+  }
+  __syncthreads();
+  // face blocks: item (face, node pair (gr, gc), row s) -> entries (gr NS + s, gc NS + t), t < NS
+  const int per_face = Lf * Lf * NS;
+#pragma unroll 1
+  for (int f = 0; f < NF; ++f)
+  for (int r = tid; r < per_face; r += nt) {
+    const int s = r % NS, pair = r / NS, gr = pair / Lf, gc = pair - gr * Lf;
+    double ust[NS], uss = 0.0, pr = 0.0;
+#pragma unroll
+    for (int t = 0; t < NS; ++t) ust[t] = 0.0;
+    for (int T = 0; T < sz.n_tri; ++T) {
+      const int a = floc[T * Lf + gr], b = floc[T * Lf + gc];
+      if (a < 0 || b < 0) continue;
+      const int p0 = f * nqt + T * nqf;
+      double ust_T[NS], uss_T = 0.0, pr_T = 0.0;
+#pragma unroll
+      for (int t = 0; t < NS; ++t) ust_T[t] = 0.0;
+#pragma unroll 3
+      for (int qq = 0; qq < nqf; ++qq) {
+        const double pq = wphi[(p0 + qq) * nlocf + a] * phf[qq * nlocf + b];
+        const double2* k2 = reinterpret_cast<const double2*>(fK1 + ((p0 + qq) * NS + s) * K1P);
+        double k1[K1P];
+#pragma unroll
+        for (int h = 0; h < K1P / 2; ++h) {
+          const double2 v = k2[h];
+          k1[2 * h] = v.x;
+          k1[2 * h + 1] = v.y;
+        }
+#pragma unroll
+        for (int t = 0; t < NS; ++t) ust_T[t] += pq * k1[t];
+        uss_T += pq * k1[NS];
+        pr_T += pq;
       }
+#pragma unroll
+      for (int t = 0; t < NS; ++t) ust[t] += ust_T[t];
+      uss += uss_T;
+      pr += pr_T;
     }
-    __syncthreads();
-    {
-      double* dst = bk.wdgdq_face + ((size_t)mac * NF + f) * nqt * NWF;
-      for (int i = tid; i < nqt * NWF; i += nt) dst[i] = ftile[i];
-    }
-    // face blocks: item (node pair (gr, gc), row s) -> entries (gr NS + s, gc NS + t), t < NS
     const int kind = g.bc_kind[mac * NF + f];
     const double* u_w = g.wall_u + (mac * NF + f) * D;
     double uw2 = 0.0;
 #pragma unroll
     for (int i = 0; i < D; ++i) uw2 += u_w[i] * u_w[i];
     const double e_tot = g.wall_e[mac * NF + f] + 0.5 * uw2;
-    const size_t fboff = ((size_t)mac * NF + f) * bs * bs;
-    for (int it = tid; it < Lf * Lf * NS; it += nt) {
-      const int s = it % NS, pair = it / NS, gc = pair % Lf, gr = pair / Lf;
-      double ust[NS], uss = 0.0, pr = 0.0;
+    const size_t row = ((size_t)mac * NF + f) * bs * bs + (size_t)(gr * NS + s) * bs + gc * NS;
 #pragma unroll
-      for (int t = 0; t < NS; ++t) ust[t] = 0.0;
-      for (int T = 0; T < sz.n_tri; ++T) {
-        const int a = floc[T * Lf + gr], b = floc[T * Lf + gc];
-        if (a < 0 || b < 0) continue;
-        const int p0 = T * nqf;
-        double ust_T[NS], uss_T = 0.0, pr_T = 0.0;
-#pragma unroll
-        for (int t = 0; t < NS; ++t) ust_T[t] = 0.0;
-        for (int qq = 0; qq < nqf; ++qq) {
-          const double pq = wphi[(p0 + qq) * nlocf + a] * g.phi_face[qq * nlocf + b];
-          const double* k1 = fK1 + ((p0 + qq) * NS + s) * NS;
-#pragma unroll
-          for (int t = 0; t < NS; ++t) ust_T[t] += pq * k1[t];
-          uss_T += pq * fSd[(p0 + qq) * NS + s];
-          pr_T += pq;
+    for (int t = 0; t < NS; ++t) {
+      // S is diagonal here (no frozen coefficients): the off-diagonal sums of k_assemble are
+      // sums of pq * 0.0, i.e. +0.0
+      const double uss_t = (s == t) ? uss : 0.0;
+      double tst, ttt;
+      if (kind == 0) {
+        tst = -uss_t;
+        ttt = -ust[t];
+      } else {
+        double khh = (s == t) ? 1.0 : 0.0, kuu = 0.0;
+        if (kind == 2) {
+          if (t == 0 && s >= 1 && s <= D) khh = -u_w[s - 1];
+          if (t == 0 && s == E) khh = -e_tot;
+          if (s == 0 && t == 0) kuu = -1.0;
+        } else if (kind == 3) {
+          if (s == t && (s == 0 || s == E)) kuu = -1.0;
         }
-#pragma unroll
-        for (int t = 0; t < NS; ++t) ust[t] += ust_T[t];
-        uss += uss_T;
-        pr += pr_T;
+        tst = pr * kuu;
+        ttt = pr * khh;
       }
-      const size_t row = fboff + (size_t)(gr * NS + s) * bs + gc * NS;
-#pragma unroll
-      for (int t = 0; t < NS; ++t) {
-        // S is diagonal here (no frozen coefficients): the off-diagonal sums of k_assemble are
-        // sums of pq * 0.0, i.e. +0.0
-        const double uss_t = (s == t) ? uss : 0.0;
-        double tst, ttt;
-        if (kind == 0) {
-          tst = -uss_t;
-          ttt = -ust[t];
-        } else {
-          double khh = (s == t) ? 1.0 : 0.0, kuu = 0.0;
-          if (kind == 2) {
-            if (t == 0 && s >= 1 && s <= D) khh = -u_w[s - 1];
-            if (t == 0 && s == E) khh = -e_tot;
-            if (s == 0 && t == 0) kuu = -1.0;
-          } else if (kind == 3) {
-            if (s == t && (s == 0 || s == E)) kuu = -1.0;
-          }
-          tst = pr * kuu;
-          ttt = pr * khh;
-        }
-        bk.face_state_trace[row + t] = ust[t];
-        bk.face_trace_state[row + t] = tst;
-        bk.face_trace_trace[row + t] = ttt;
-      }
+      bk.face_state_trace[row + t] = ust[t];
+      bk.face_trace_state[row + t] = tst;
+      bk.face_trace_trace[row + t] = ttt;
     }
-    __syncthreads();
   }
 }
 
