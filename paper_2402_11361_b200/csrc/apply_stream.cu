@@ -263,6 +263,10 @@ __device__ unsigned long long g_prof[16][3];
 #define PROF_ADD(k, j, v)
 #endif
 constexpr int MAXP = 256;  // pieces per macro (checked on the host)
+// larger piece tables only for the configurations that need them (3D m = 2, p = 3: ~300 pieces);
+// the others keep their static shared memory
+template <class C>
+__host__ __device__ constexpr int maxp_of() { return C::LTR > MHDG_NCONS ? 384 : MAXP; }
 
 // First group >= g0 that warp `warp` owns when groups are dealt round-robin
 // by global index over nw warps: consecutive pieces of one kind keep all warps busy.
@@ -351,10 +355,13 @@ __global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 ? 1 : 2)) k_apply_s
                                                              StreamIn sin) {
   constexpr int D = C::D, NS = C::NS, NF = C::NF, L = C::L, LF = C::LF, BS = C::BS, LTR = C::LTR, n = C::n;
   constexpr int NLOC = C::NLOC, NQ = C::NQ, NLOCF = C::NLOCF, NQF = C::NQF, NTRI = C::NTRI, NSUB = C::NSUB;
-  static_assert(LTR <= NCONS, "one local trace entry per consumer thread");
+  // local trace entries per consumer thread (1 except where ltr > NCONS: 3D m = 2, p = 3);
+  // entry e of thread tid is tid + j NCONS
+  constexpr int EPT = (LTR + NCONS - 1) / NCONS;
+  static_assert(2 * LTR <= ST_DBL, "the face-term hand-off piece must fit one ring stage");
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES];
-  __shared__ Piece pieces[MAXP];
+  __shared__ Piece pieces[maxp_of<C>()];
   __shared__ int npieces;
   __shared__ double cfls[16];  // z coefficients -(fac / det) area_f n_f,l of the current macro
   // z row of local node b of sub-face T of face f: [0] the volume node, [1] its face-node index
@@ -379,7 +386,7 @@ __global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 ? 1 : 2)) k_apply_s
     // the piece schedule is identical for every macro: build it once
     Sched<C, PART, MDRES> sc;
     int np = 0;
-    while (np < MAXP && sc.next(pieces[np])) ++np;
+    while (np < maxp_of<C>() && sc.next(pieces[np])) ++np;
     npieces = np;
   }
   {  // reference tables -> shared memory
@@ -501,9 +508,14 @@ __global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 ? 1 : 2)) k_apply_s
   ConsRing<STAGES> rg{smem_u32(full_bar), smem_u32(empty_bar), ring};
 
   // this thread's trace entry of the next macro, gathered one macro ahead
-  double x_next = 0.0;
-  if (PART != 2 && tid < LTR && blockIdx.x < g.n_mac && x)
-    x_next = __ldg(x + __ldg(g.gather + (size_t)blockIdx.x * LTR + tid));
+  double x_next[EPT];
+#pragma unroll
+  for (int j = 0; j < EPT; ++j) {
+    const int e = tid + j * NCONS;
+    x_next[j] = 0.0;
+    if (PART != 2 && e < LTR && blockIdx.x < g.n_mac && x)
+      x_next[j] = __ldg(x + __ldg(g.gather + (size_t)blockIdx.x * LTR + e));
+  }
 
   auto zcoef = [&](int m) {  // -(fac / det) area_f n_f,l of macro m for this thread's (f, l)
     const int e = tid - (NCONS - NF * D), f = e / D;
@@ -518,19 +530,30 @@ __global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 ? 1 : 2)) k_apply_s
     for (int a = 0; a < D; ++a)
 #pragma unroll
       for (int b = 0; b < D; ++b) ij[a][b] = __ldg(g.inv_jac + (size_t)mac * D * D + a * D + b);
-    double sc_mine = 0.0;  // trace_face_scale of this thread's face in the final sum
-    double ftt_mine = 0.0, cfgz_mine = 0.0;  // post part: this thread's A_hh x and g entries
-    if (PART != 1 && tid < LTR) sc_mine = __ldg(bk.trace_face_scale + mac * NF + tid / BS);
+    double sc_mine[EPT];  // trace_face_scale of this thread's face(s) in the final sum
+    double ftt_mine[EPT], cfgz_mine[EPT];  // post part: this thread's A_hh x and g entries
+#pragma unroll
+    for (int j = 0; j < EPT; ++j) {
+      const int e = tid + j * NCONS;
+      sc_mine[j] = ftt_mine[j] = cfgz_mine[j] = 0.0;
+      if (PART != 1 && e < LTR) sc_mine[j] = __ldg(bk.trace_face_scale + mac * NF + e / BS);
+    }
     PROF_T(t_start);
     if (PART != 2 && tid >= NCONS - NF * D) {  // the last consumer threads: one z coefficient each,
       cfls[tid - (NCONS - NF * D)] = cfl_next;      // loaded one macro ahead like the trace entries
       const int nm = mac + gridDim.x;
       if (nm < g.n_mac) cfl_next = zcoef(nm);
     }
-    if (PART != 2 && tid < LTR) {
-      xl[tid] = x_next;
-      const int nm = mac + gridDim.x;
-      if (nm < g.n_mac && x) x_next = __ldg(x + __ldg(g.gather + (size_t)nm * LTR + tid));
+    if (PART != 2) {
+#pragma unroll
+      for (int j = 0; j < EPT; ++j) {
+        const int e = tid + j * NCONS;
+        if (e < LTR) {
+          xl[e] = x_next[j];
+          const int nm = mac + gridDim.x;
+          if (nm < g.n_mac && x) x_next[j] = __ldg(x + __ldg(g.gather + (size_t)nm * LTR + e));
+        }
+      }
     }
     cbar();  // xl complete; the previous macro's readers of every work array are done
     if (tid == 0) { PROF_ADD(13, 2, t_start); }
@@ -718,16 +741,20 @@ __global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 ? 1 : 2)) k_apply_s
           if (aok && s0 + 1 < NS) cv[(K * NLOC + a) * NS + s0 + 1] = c1 + e1;
         }
       }
-      if (tid < LTR) {
-        const int idx = tid, s = idx % NS, gg = (idx / NS) % LF, f = idx / BS;
-        double acc = 0.0;
-        for (int e = fnp[gg]; e < fnp[gg + 1]; ++e) {
-          const int ent = fne[e], T = ent / NLOCF, a = ent % NLOCF;
-          const double* w = wfz + ((f * NTRI + T) * NQF) * NS + s;
 #pragma unroll
-          for (int q = 0; q < NQF; ++q) acc += pfs[q * NLOCF + a] * w[q * NS];
+      for (int j = 0; j < EPT; ++j) {
+        const int idx = tid + j * NCONS;
+        if (idx < LTR) {
+          const int s = idx % NS, gg = (idx / NS) % LF, f = idx / BS;
+          double acc = 0.0;
+          for (int e = fnp[gg]; e < fnp[gg + 1]; ++e) {
+            const int ent = fne[e], T = ent / NLOCF, a = ent % NLOCF;
+            const double* w = wfz + ((f * NTRI + T) * NQF) * NS + s;
+#pragma unroll
+            for (int q = 0; q < NQF; ++q) acc += pfs[q * NLOCF + a] * w[q * NS];
+          }
+          cfgz[idx] = acc;
         }
-        cfgz[idx] = acc;
       }
       cbar();
       for (int idx = tid; idx < n; idx += NCONS) {
@@ -824,9 +851,9 @@ __global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 ? 1 : 2)) k_apply_s
         for (int i = tid; i < n; i += NCONS) y1g[i] = y[i];
       }
       double* fc = Work<C>::fc(fac.work, g.n_mac, mac);
-      if (tid < LTR) {
-        fc[tid] = ftt[tid];
-        fc[LTR + tid] = cfgz[tid];
+      for (int e = tid; e < LTR; e += NCONS) {
+        fc[e] = ftt[e];
+        fc[LTR + e] = cfgz[e];
       }
       if (tid == 0) { PROF_ADD(15, 2, t_wb); }
       continue;  // the next macro's first barrier orders these reads before any overwrite
@@ -869,17 +896,21 @@ __global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 ? 1 : 2)) k_apply_s
         for (int i = tid; i < n; i += NCONS) y[i] = A[i];
       });
       seg_loop<1, 1>(rg, lane, [&](const double* A, int, int) {
-        if (tid < LTR) {  // one entry per thread, used by the same thread in the final sum
-          ftt_mine = A[tid];
-          cfgz_mine = A[LTR + tid];
+#pragma unroll
+        for (int j = 0; j < EPT; ++j) {  // this thread's entries, used by the same thread in the final sum
+          const int e = tid + j * NCONS;
+          if (e < LTR) {
+            ftt_mine[j] = A[e];
+            cfgz_mine[j] = A[LTR + e];
+          }
         }
       });
       if (tid == 0) { PROF_ADD(K_Y2, 1, t8); }
     }
     PROF_T(t9);
     cbar();  // y = y2 complete
-    if (tid < LTR) {  // y2 restricted to the face nodes, for A_hu
-      const int idx = tid, s = idx % NS, h = (idx / NS) % LF, f = idx / BS;
+    for (int idx = tid; idx < LTR; idx += NCONS) {  // y2 restricted to the face nodes, for A_hu
+      const int s = idx % NS, h = (idx / NS) % LF, f = idx / BS;
       yf[idx] = y[fvn[f * LF + h] * NS + s];
     }
     // tg[r][i][s] = sum_J (M^-1 D_r)[fnode_i][J] y2[J][s]: lane = (J half, row, s) for groups
@@ -952,17 +983,21 @@ __global__ void __launch_bounds__(NCONS + 32, (NCONS >= 1024 ? 1 : 2)) k_apply_s
     cbar();  // wf2, fts complete
 
     // y4 = ((A_hu y2 - A_hq z2) + A_hh x) - A_hq z, with -A_hq z = scale * cfg
-    if (tid < LTR) {
-      const int idx = tid, s = idx % NS, gg = (idx / NS) % LF, f = idx / BS;
-      double acc = 0.0;
-      for (int e = fnp[gg]; e < fnp[gg + 1]; ++e) {
-        const int ent = fne[e], T = ent / NLOCF, a = ent % NLOCF;
-        const double* w = wf2 + ((f * NTRI + T) * NQF) * NS + s;
 #pragma unroll
-        for (int q = 0; q < NQF; ++q) acc += pfs[q * NLOCF + a] * w[q * NS];
+    for (int j = 0; j < EPT; ++j) {
+      const int idx = tid + j * NCONS;
+      if (idx < LTR) {
+        const int s = idx % NS, gg = (idx / NS) % LF, f = idx / BS;
+        double acc = 0.0;
+        for (int e = fnp[gg]; e < fnp[gg + 1]; ++e) {
+          const int ent = fne[e], T = ent / NLOCF, a = ent % NLOCF;
+          const double* w = wf2 + ((f * NTRI + T) * NQF) * NS + s;
+#pragma unroll
+          for (int q = 0; q < NQF; ++q) acc += pfs[q * NLOCF + a] * w[q * NS];
+        }
+        y_loc[(size_t)mac * LTR + idx] = ((fts[idx] + sc_mine[j] * acc) + (PART == 2 ? ftt_mine[j] : ftt[idx])) +
+                                         sc_mine[j] * (PART == 2 ? cfgz_mine[j] : cfgz[idx]);
       }
-      y_loc[(size_t)mac * LTR + idx] = ((fts[idx] + sc_mine * acc) + (PART == 2 ? ftt_mine : ftt[idx])) +
-                                       sc_mine * (PART == 2 ? cfgz_mine : cfgz[idx]);
     }
     if (tid == 0) { PROF_ADD(12, 2, t_end); }
   }
@@ -1306,7 +1341,7 @@ extern "C" void mhdg_set_apply_split(int on) { g_split = on; }
 template <class C>
 static bool stream_ok(const mhdg_disc& g, const mhdg_blocks& b, const mhdg_factors& f) {
   static const int npieces = count_pieces<C>();
-  if (npieces > MAXP) return false;
+  if (npieces > maxp_of<C>()) return false;
   if (g.dim != C::D || g.L != C::L || g.Lf != C::LF || g.nloc != C::NLOC || g.nq != C::NQ || g.n_sub != C::NSUB ||
       g.n_tri != C::NTRI || g.nlocf != C::NLOCF || g.nqf != C::NQF)
     return false;
@@ -1470,6 +1505,7 @@ int cond_stream(const mhdg_disc& g, const mhdg_blocks& b, const mhdg_factors& f,
   MHDG_COND(3, 1, 1)
   MHDG_COND(3, 1, 3)
   MHDG_COND(3, 4, 1)
+  MHDG_COND(3, 2, 3)
 #undef MHDG_COND
   return -1;
 }
@@ -1486,6 +1522,7 @@ int apply_stream(const mhdg_disc& g, const mhdg_blocks& b, const mhdg_factors& f
   if (stream_ok<Cfg<3, 1, 1>>(g, b, f)) return launch_apply<Cfg<3, 1, 1>>(g, b, f, x, y_loc, st);
   if (stream_ok<Cfg<3, 1, 3>>(g, b, f)) return launch_apply<Cfg<3, 1, 3>>(g, b, f, x, y_loc, st);
   if (stream_ok<Cfg<3, 4, 1>>(g, b, f)) return launch_apply<Cfg<3, 4, 1>>(g, b, f, x, y_loc, st);
+  if (stream_ok<Cfg<3, 2, 3>>(g, b, f)) return launch_apply<Cfg<3, 2, 3>>(g, b, f, x, y_loc, st);
   return -1;
 }
 
