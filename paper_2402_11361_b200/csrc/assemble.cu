@@ -1093,7 +1093,11 @@ static int launch_couplings(const mhdg_disc& g, const mhdg_flow& fl, const doubl
   const Sz sz = make_sz<D>(g);
   const size_t bytes = sizeof(double) * cpl_smem<D>(sz).total;
   if (bytes > 227 * 1024 || sz.n_tri * sz.Lf > ASM_MAXFLOC) return -1;
-  if (bytes > 48 * 1024) cudaFuncSetAttribute(k_couplings<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  static size_t set_bytes = 0;  // once per size: launches inside a CUDA-graph capture stay pure launches
+  if (bytes > 48 * 1024 && bytes != set_bytes) {
+    cudaFuncSetAttribute(k_couplings<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    set_bytes = bytes;
+  }
   k_couplings<D><<<g.n_mac, CPL_THREADS, bytes, st>>>(g, fl, u, uhat, b);
   return launch_ok();
 }
