@@ -73,7 +73,10 @@ def main():
         for key, v in r["kernel_ms"].items():
             out["kernel_ms_total"][key] = out["kernel_ms_total"].get(key, 0.0) + v
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
-    path = os.path.join(ROOT, "gpurun_out", "r2_c3_run.json")
+    repr_ = os.environ.get("MHDG_APPLY_REPR", "matrix_free")
+    out["representation"] = repr_
+    out["peak_device_GB"] = torch.cuda.max_memory_allocated() / 1e9
+    path = os.path.join(ROOT, "gpurun_out", "r2_c3_run.json" if repr_ == "matrix_free" else f"r2_c3_run_{repr_}.json")
     with open(path, "w") as fh:
         json.dump(out, fh, indent=1)
     print("total", out["total_wall_s"], out["totals"], flush=True)

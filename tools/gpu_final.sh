@@ -17,3 +17,7 @@ timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/f
 echo "ref rc=$?" >> gpurun_out/fin_rc.txt
 timeout 600 python tools/c3_rates.py > gpurun_out/fin_c3_rates.txt 2>&1
 echo "c3rates rc=$?" >> gpurun_out/fin_rc.txt
+MHDG_APPLY_REPR=recompute timeout 600 python tools/c3_run.py 2 16 > gpurun_out/fin_c3_run_recompute.log 2>&1
+echo "c3 recompute run rc=$?" >> gpurun_out/fin_rc.txt
+timeout 600 python tools/c3_run.py 2 16 > gpurun_out/fin_c3_run.log 2>&1
+echo "c3 run rc=$?" >> gpurun_out/fin_rc.txt
