@@ -844,7 +844,7 @@ extern "C" void mhdg_set_couplings_kernel(int on) { g_couplings_kernel = on; }
 
 template <int D>
 struct CplSmem {
-  int us, uh, phf, prv, wq, tile, fpr, fw, wphi, fK1, total;
+  int us, uh, phf, stage, prv, wq, tile, fpr, fw, wphi, fK1, total;
 };
 
 // rows of d(flux.n)/d uhat padded to K1P doubles with the diagonal of S in the last slot:
@@ -861,6 +861,7 @@ __host__ __device__ inline CplSmem<D> cpl_smem(const Sz& s) {
   m.us = o, o += s.n;
   m.uh = o, o += s.ltr;
   m.phf = o, o += s.nqf * s.nlocf;
+  m.stage = o, o += (CPL_THREADS / 32) * 32 * NS;  // per-warp transpose buffers of the face-block stores
   o = (o + 1) & ~1;
   const int work = o, npv = s.n_sub * s.nq, npf = NF * s.n_tri * s.nqf;
   m.tile = o, o += CPL_TP * D * D * NS * NS;  // first: 16-byte aligned for the bulk stores
@@ -923,7 +924,10 @@ __global__ void __launch_bounds__(CPL_THREADS, 3) k_couplings(mhdg_disc g, mhdg_
   double* Wv = bk.wdgdq_vol + (size_t)mac * npv * NW;
   // a tile leaves as one bulk copy (TMA) issued by thread 0 when its global range is 16-byte
   // aligned (NW odd in 3D: every tile of CPL_TP points is, if the macro's base is)
-  const bool bulk = (((size_t)mac * npv * NW) & 1) == 0 && ((CPL_TP * NW) & 1) == 0;
+#ifndef MHDG_CPL_BULK
+#define MHDG_CPL_BULK 1
+#endif
+  const bool bulk = MHDG_CPL_BULK && (((size_t)mac * npv * NW) & 1) == 0 && ((CPL_TP * NW) & 1) == 0;
   for (int p0 = 0; p0 < npv; p0 += CPL_TP) {
     const int tp = min(CPL_TP, npv - p0);
     for (int idx = tid; idx < D * D * tp; idx += nt) {
@@ -1015,74 +1019,94 @@ __global__ void __launch_bounds__(CPL_THREADS, 3) k_couplings(mhdg_disc g, mhdg_
     }
   }
   __syncthreads();
-  // face blocks: item (face, node pair (gr, gc), row s) -> entries (gr NS + s, gc NS + t), t < NS
-  const int per_face = Lf * Lf * NS;
+  // face blocks: item r = ((gr NS + s) Lf + gc) of a face -> entries (gr NS + s, gc NS + t), t < NS,
+  // i.e. doubles [NS r, NS r + NS) of each of the three blocks: a warp's 32 consecutive items
+  // cover 32 NS contiguous doubles, handed through a per-warp shared-memory buffer so that every
+  // store instruction writes 256 contiguous bytes (five times fewer L2 write transactions than
+  // NS-double runs per lane)
+  const int per_face = Lf * Lf * NS, warp = tid >> 5, lane = tid & 31;
+  double* stg = sm + o.stage + warp * 32 * NS;
 #pragma unroll 1
-  for (int f = 0; f < NF; ++f)
-  for (int r = tid; r < per_face; r += nt) {
-    const int s = r % NS, pair = r / NS, gr = pair / Lf, gc = pair - gr * Lf;
-    double ust[NS], uss = 0.0, pr = 0.0;
-#pragma unroll
-    for (int t = 0; t < NS; ++t) ust[t] = 0.0;
-    for (int T = 0; T < sz.n_tri; ++T) {
-      const int a = floc[T * Lf + gr], b = floc[T * Lf + gc];
-      if (a < 0 || b < 0) continue;
-      const int p0 = f * nqt + T * nqf;
-      double ust_T[NS], uss_T = 0.0, pr_T = 0.0;
-#pragma unroll
-      for (int t = 0; t < NS; ++t) ust_T[t] = 0.0;
-#pragma unroll 3
-      for (int qq = 0; qq < nqf; ++qq) {
-        const double pq = wphi[(p0 + qq) * nlocf + a] * phf[qq * nlocf + b];
-        const double2* k2 = reinterpret_cast<const double2*>(fK1 + ((p0 + qq) * NS + s) * K1P);
-        double k1[K1P];
-#pragma unroll
-        for (int h = 0; h < K1P / 2; ++h) {
-          const double2 v = k2[h];
-          k1[2 * h] = v.x;
-          k1[2 * h + 1] = v.y;
-        }
-#pragma unroll
-        for (int t = 0; t < NS; ++t) ust_T[t] += pq * k1[t];
-        uss_T += pq * k1[NS];
-        pr_T += pq;
-      }
-#pragma unroll
-      for (int t = 0; t < NS; ++t) ust[t] += ust_T[t];
-      uss += uss_T;
-      pr += pr_T;
-    }
+  for (int f = 0; f < NF; ++f) {
     const int kind = g.bc_kind[mac * NF + f];
     const double* u_w = g.wall_u + (mac * NF + f) * D;
     double uw2 = 0.0;
 #pragma unroll
     for (int i = 0; i < D; ++i) uw2 += u_w[i] * u_w[i];
     const double e_tot = g.wall_e[mac * NF + f] + 0.5 * uw2;
-    const size_t row = ((size_t)mac * NF + f) * bs * bs + (size_t)(gr * NS + s) * bs + gc * NS;
+    const size_t fboff = ((size_t)mac * NF + f) * bs * bs;
+    for (int r0 = warp * 32; r0 < per_face; r0 += nt) {
+      const int r = r0 + lane;
+      const bool active = r < per_face;
+      const int cnt = min(32, per_face - r0) * NS;  // doubles this warp pass writes per block
+      const int row = r / Lf, gc = r - row * Lf, gr = row / NS, s = row - gr * NS;
+      double ust[NS], tst[NS], ttt[NS];
+      if (active) {
+        double uss = 0.0, pr = 0.0;
 #pragma unroll
-    for (int t = 0; t < NS; ++t) {
-      // S is diagonal here (no frozen coefficients): the off-diagonal sums of k_assemble are
-      // sums of pq * 0.0, i.e. +0.0
-      const double uss_t = (s == t) ? uss : 0.0;
-      double tst, ttt;
-      if (kind == 0) {
-        tst = -uss_t;
-        ttt = -ust[t];
-      } else {
-        double khh = (s == t) ? 1.0 : 0.0, kuu = 0.0;
-        if (kind == 2) {
-          if (t == 0 && s >= 1 && s <= D) khh = -u_w[s - 1];
-          if (t == 0 && s == E) khh = -e_tot;
-          if (s == 0 && t == 0) kuu = -1.0;
-        } else if (kind == 3) {
-          if (s == t && (s == 0 || s == E)) kuu = -1.0;
+        for (int t = 0; t < NS; ++t) ust[t] = 0.0;
+        for (int T = 0; T < sz.n_tri; ++T) {
+          const int a = floc[T * Lf + gr], b = floc[T * Lf + gc];
+          if (a < 0 || b < 0) continue;
+          const int p0 = f * nqt + T * nqf;
+          double ust_T[NS], uss_T = 0.0, pr_T = 0.0;
+#pragma unroll
+          for (int t = 0; t < NS; ++t) ust_T[t] = 0.0;
+#pragma unroll 3
+          for (int qq = 0; qq < nqf; ++qq) {
+            const double pq = wphi[(p0 + qq) * nlocf + a] * phf[qq * nlocf + b];
+            const double2* k2 = reinterpret_cast<const double2*>(fK1 + ((p0 + qq) * NS + s) * K1P);
+            double k1[K1P];
+#pragma unroll
+            for (int h = 0; h < K1P / 2; ++h) {
+              const double2 v = k2[h];
+              k1[2 * h] = v.x;
+              k1[2 * h + 1] = v.y;
+            }
+#pragma unroll
+            for (int t = 0; t < NS; ++t) ust_T[t] += pq * k1[t];
+            uss_T += pq * k1[NS];
+            pr_T += pq;
+          }
+#pragma unroll
+          for (int t = 0; t < NS; ++t) ust[t] += ust_T[t];
+          uss += uss_T;
+          pr += pr_T;
         }
-        tst = pr * kuu;
-        ttt = pr * khh;
+#pragma unroll
+        for (int t = 0; t < NS; ++t) {
+          // S is diagonal here (no frozen coefficients): the off-diagonal sums of k_assemble are
+          // sums of pq * 0.0, i.e. +0.0
+          const double uss_t = (s == t) ? uss : 0.0;
+          if (kind == 0) {
+            tst[t] = -uss_t;
+            ttt[t] = -ust[t];
+          } else {
+            double khh = (s == t) ? 1.0 : 0.0, kuu = 0.0;
+            if (kind == 2) {
+              if (t == 0 && s >= 1 && s <= D) khh = -u_w[s - 1];
+              if (t == 0 && s == E) khh = -e_tot;
+              if (s == 0 && t == 0) kuu = -1.0;
+            } else if (kind == 3) {
+              if (s == t && (s == 0 || s == E)) kuu = -1.0;
+            }
+            tst[t] = pr * kuu;
+            ttt[t] = pr * khh;
+          }
+        }
       }
-      bk.face_state_trace[row + t] = ust[t];
-      bk.face_trace_state[row + t] = tst;
-      bk.face_trace_trace[row + t] = ttt;
+      const size_t off = fboff + (size_t)NS * r0;
+#pragma unroll
+      for (int blk = 0; blk < 3; ++blk) {
+        double* dst = (blk == 0 ? bk.face_state_trace : blk == 1 ? bk.face_trace_state : bk.face_trace_trace) + off;
+        __syncwarp();
+        if (active) {
+#pragma unroll
+          for (int t = 0; t < NS; ++t) stg[lane * NS + t] = blk == 0 ? ust[t] : blk == 1 ? tst[t] : ttt[t];
+        }
+        __syncwarp();
+        for (int k = lane; k < cnt; k += 32) dst[k] = stg[k];
+      }
     }
   }
 }
