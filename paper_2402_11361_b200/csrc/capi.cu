@@ -176,9 +176,9 @@ static void macro_view(const mhdg_disc* g, const mhdg_blocks* b, const mhdg_fact
   bv->trace_face_scale += m0 * nf;
   }
   *fv = *f;
-  fv->lu += m0 * (size_t)mhdg_packed_lu_size((int)n);
-  fv->perm += m0 * n;
-  if (f->scratch_macros <= 0 || f->scratch_macros >= g->n_mac) fv->scratch += m0 * n * n;
+  if (fv->lu) fv->lu += m0 * (size_t)mhdg_packed_lu_size((int)n);
+  if (fv->perm) fv->perm += m0 * n;
+  if (fv->scratch && (f->scratch_macros <= 0 || f->scratch_macros >= g->n_mac)) fv->scratch += m0 * n * n;
   if (fv->work) fv->work += m0 * (size_t)(mhdg_apply_work_size(g) / g->n_mac);
 }
 
