@@ -90,6 +90,18 @@ def test_full_size_apply_properties(cfg):
         assert torch.equal(y_st, cond.apply_trace(x1))
         assert _rel(y_st, y_split) < 1e-10
         cond.ahat = None
+    # coupling-recompute representation at full size (windows of 4096 macros): the same
+    # factors and the same apply / rhs / recovery, bit for bit
+    from paper_2402_11361_b200.condense import condense
+
+    rc = condense(A.RecomputeBlocks(disc, f, ctx))
+    assert torch.equal(rc.lu, cond.lu) and torch.equal(rc.perm, cond.perm)
+    assert torch.equal(rc.apply_trace(x1), y_split)
+    assert torch.equal(rc.rhs(*res), cond.rhs(*res))
+    du_r, dq_r = rc.recover(res[0], res[1], x1)
+    du_0, dq_0 = cond.recover(res[0], res[1], x1)
+    assert torch.equal(du_r, du_0) and torch.equal(dq_r, dq_0)
+    del rc, du_r, dq_r, du_0, dq_0
     # rhs / recover consistency: the Newton correction (du, dq, dx) of the full
     # local system with dx = x1 satisfies A_hat dx - b = (trace residual of the
     # recovered correction), i.e. apply_trace(x) - rhs is linear in x with the
