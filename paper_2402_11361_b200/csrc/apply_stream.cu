@@ -13,6 +13,8 @@
 //     bytes in flight are set by the ring depth, not by thread count;
 //   * CTAs are persistent (grid = SMs x CTAs/SM) and walk the macros.
 // Results match k_apply_local to rounding; all reductions are in a fixed order.
+// Local trace entries are walked EPT = ceil(ltr / consumer threads) per thread (one for all
+// configurations but 3D m = 2, p = 3, whose ltr = 560 exceeds the 512 consumer threads).
 #include "dmma.cuh"
 #include "local_ops.cuh"
 #include "packed_lu.cuh"

@@ -20,6 +20,9 @@
 // together with the face blocks formed entry by entry and written once.  Every
 // accumulation runs in a fixed order (sub-element loop, sub-faces ascending,
 // inverse-incidence gathers): results are bitwise reproducible run to run.
+//
+// k_couplings (end of this file) re-forms only the coupling blocks the trace apply streams
+// (face blocks, dG/dq stashes) for the coupling-recompute representation (want_jac = 2).
 #include <type_traits>
 
 #include "dmma.cuh"
