@@ -21,6 +21,10 @@
  *   mhdg_precond_build      krylov.py:194-232   block_precond_build
  *   mhdg_precond_apply      krylov.py:234-236   (closure returned by it)
  *   mhdg_face_reduce        condense.py:48-51   _scatter_add (deterministic)
+ *   mhdg_*_window           the same operations on a window of macros whose blocks
+ *                           were just re-formed from (u, q, uhat): the paper's "store
+ *                           only S^-1 and transformation data" variant,
+ *                           condense.py:62-127 without resident LocalBlocks
  *
  * Layouts are the reference's (assembly.py:6-8): volume dof node*ns+s,
  * gradient dof (l*L+node)*ns+s, trace dof (f*Lf+g)*ns+s, local trace
