@@ -842,11 +842,6 @@ __global__ void __launch_bounds__(asm_threads<D>(), asm_min_ctas<D>())
 //     blocks as (face, node pair, row s) items: the quadrature weight products are formed
 //     once per NS entries and each thread writes NS consecutive doubles of the three blocks.
 constexpr int CPL_THREADS = 256, CPL_TP = 16;
-// MHDG_CPL_DB: two volume tiles; the items form their point's prim themselves (no prim array),
-// the bulk copy of tile k drains while tile k + 1 is computed: one barrier per tile
-#ifndef MHDG_CPL_DB
-#define MHDG_CPL_DB 0
-#endif
 static int g_couplings_kernel = 1;  // A/B: 0 = k_assemble's couplings-only path
 extern "C" void mhdg_set_couplings_kernel(int on) { g_couplings_kernel = on; }
 
@@ -872,10 +867,10 @@ __host__ __device__ inline CplSmem<D> cpl_smem(const Sz& s) {
   m.stage = o, o += (CPL_THREADS / 32) * 32 * NS;  // per-warp transpose buffers of the face-block stores
   o = (o + 1) & ~1;
   const int work = o, npv = s.n_sub * s.nq, npf = NF * s.n_tri * s.nqf;
-  m.tile = o, o += (MHDG_CPL_DB ? 2 : 1) * CPL_TP * D * D * NS * NS;  // first: 16-byte aligned for the bulk stores
+  m.tile = o, o += CPL_TP * D * D * NS * NS;  // first: 16-byte aligned for the bulk stores
   o = (o + 1) & ~1;
-  m.prv = o, o += MHDG_CPL_DB ? 0 : npv * PRIM;
-  m.wq = o, o += MHDG_CPL_DB ? 0 : npv;
+  m.prv = o, o += npv * PRIM;
+  m.wq = o, o += npv;
   const int vol_end = o;
   o = work;  // the face arrays (all faces) share the volume arrays' memory
   m.fK1 = o, o += npf * NS * cpl_k1p<D>();
@@ -912,55 +907,6 @@ __global__ void __launch_bounds__(CPL_THREADS, 3) k_couplings(mhdg_disc g, mhdg_
   for (int i = tid; i < nqf * nlocf; i += nt) phf[i] = g.phi_face[i];
   if (tid < NF) bk.trace_face_scale[mac * NF + tid] = g.bc_kind[mac * NF + tid] > 0 ? 0.0 : 1.0;
   __syncthreads();
-#if MHDG_CPL_DB
-  // ---- volume stash (assembly.py:459-463), double-buffered tiles -------------------------
-  const int npv = sz.n_sub * nq;
-  double* Wv = bk.wdgdq_vol + (size_t)mac * npv * NW;
-  const bool bulk = (((size_t)mac * npv * NW) & 1) == 0 && ((CPL_TP * NW) & 1) == 0;
-  (void)prv;
-  (void)wq;
-  for (int p0 = 0, kt = 0; p0 < npv; p0 += CPL_TP, ++kt) {
-    const int tp = min(CPL_TP, npv - p0);
-    double* buf = tile + (kt & 1) * CPL_TP * NW;
-    for (int idx = tid; idx < D * D * tp; idx += nt) {
-      const int cs = idx / tp, pp = idx - cs * tp, P = p0 + pp, K = P / nq, qq = P - K * nq;
-      const int* conn = g.sub_conn + K * nloc;
-      const double* ph = g.phi_vol + qq * nloc;
-      double uu[NS];
-#pragma unroll
-      for (int c = 0; c < NS; ++c) {
-        double acc = 0.0;
-        for (int a = 0; a < nloc; ++a) acc += ph[a] * us[conn[a] * NS + c];
-        uu[c] = acc;
-      }
-      const Prim<D> pr = prim<D>(uu, fl);
-      const double w = g.w_ref[P] * det;
-      double* Wd = buf + pp * NW + cs * NS * NS;
-      static_switch<D * D>(cs, [&](auto kl) {
-        constexpr int k = decltype(kl)::value / D, l = decltype(kl)::value % D;
-#pragma unroll
-        for (int s = 0; s < NS; ++s)
-#pragma unroll
-          for (int t = 0; t < NS; ++t) Wd[s * NS + t] = w * visc_dgdq<D>(pr, fl, k, l, s, t);
-      });
-    }
-    double* dst = Wv + (size_t)p0 * NW;
-    if (bulk && ((tp * NW) & 1) == 0) {
-      fence_proxy_async();
-      if (tid == 0) bulk_wait_read0();  // the previous tile's copy has read the other buffer
-      __syncthreads();
-      if (tid == 0) {
-        bulk_s2g(dst, buf, (uint32_t)(tp * NW * sizeof(double)));
-        bulk_commit();
-      }
-    } else {
-      __syncthreads();
-      for (int i = tid; i < tp * NW; i += nt) dst[i] = buf[i];
-    }
-  }
-  if (tid == 0) bulk_wait_read0();
-  __syncthreads();  // the face arrays reuse the tiles' memory
-#else
   // ---- volume stash (assembly.py:459-463) ------------------------------------------------
   const int npv = sz.n_sub * nq;
   for (int P = tid; P < npv; P += nt) {
@@ -1016,7 +962,6 @@ __global__ void __launch_bounds__(CPL_THREADS, 3) k_couplings(mhdg_disc g, mhdg_
       __syncthreads();
     }
   }
-#endif
   // ---- faces (assembly.py:556-612), all of them per phase ---------------------------------
   Prim<D>* fpr = (Prim<D>*)(sm + o.fpr);
   double *fw = sm + o.fw, *wphi = sm + o.wphi, *fK1 = sm + o.fK1;
