@@ -1,4 +1,5 @@
-# A/B of k_couplings variants: bulk-copy volume tiles (default build) vs linear copy-out (tools/prof/libmhdg_nobulk.so)
+# A/B of k_couplings variants: bulk-copy volume tiles (default build) vs linear copy-out
+# (tools/prof/libmhdg_nobulk.so = the library linked with assemble.cu compiled with -DMHDG_CPL_BULK=0)
 mkdir -p gpurun_out
 timeout 600 python -m pytest tests/test_gpu_recompute.py -m gpu -q -p no:cacheprovider > gpurun_out/ab_tests.log 2>&1
 echo "tests rc=$?" > gpurun_out/ab_rc.txt
